@@ -1,0 +1,294 @@
+/*
+ * fsvd_b200.h -- C-ABI boundary of the B200-native FlashSVD streaming encoder.
+ *
+ * This is the drop-in boundary for the reference's low-rank operator API
+ * (/root/reference/proj/include/flashsvd/{attention,ffn,encoder,memtier}.hpp).
+ * Every entry point below names the reference interface it replaces.  The
+ * C++ drop-in headers under include/flashsvd/ re-expose the reference
+ * signatures on top of these functions; Python (ctypes), cgo or JNI bind the
+ * same symbols directly.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no C++ or torch types cross this ABI.
+ *   - Host tensors are fp32, row-major, in the reference's orientation
+ *     (x * W: U is in x r, V is r x out, factorize.hpp:11-21).
+ *   - Device activations are row-major [batch, seq, d_model] in the pack's
+ *     dtype (bf16 or fp32).
+ *   - Status codes map 1:1 onto flashsvd::ErrorKind (errors.hpp:11-21), with
+ *     FSVD_ERR_CUDA added for device failures.  Exceptions never cross the
+ *     ABI; the message of the last failure on the calling thread is returned
+ *     by fsvd_last_error().
+ *   - There is no CPU fallback: every compute entry point launches sm_100a
+ *     kernels and fails with FSVD_ERR_CUDA when no usable device exists.
+ */
+#ifndef FSVD_B200_H
+#define FSVD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define FSVD_ABI_VERSION 1
+
+/* errors.hpp:11-21 (ErrorKind), in declaration order, offset by one. */
+typedef enum fsvd_status {
+  FSVD_OK = 0,
+  FSVD_ERR_SHAPE = 1,
+  FSVD_ERR_RANK = 2,
+  FSVD_ERR_CONFIG = 3,
+  FSVD_ERR_BUDGET = 4,
+  FSVD_ERR_ACCOUNTING = 5,
+  FSVD_ERR_FORMAT = 6,
+  FSVD_ERR_NUMERIC = 7,
+  FSVD_ERR_INFEASIBLE = 8,
+  FSVD_ERR_IO = 9,
+  FSVD_ERR_CUDA = 10
+} fsvd_status;
+
+/* Storage / arithmetic precision policy of a factor pack and its kernels.
+ * FSVD_F32 : fp32 storage, fp32 FMA accumulate (<= 1e-4 parity mode).
+ * FSVD_BF16: bf16 storage, tcgen05 bf16 MMA, fp32 accumulate (<= 2e-2). */
+typedef enum fsvd_dtype { FSVD_F32 = 0, FSVD_BF16 = 1 } fsvd_dtype;
+
+/* ffn.hpp:13 */
+typedef enum fsvd_activation {
+  FSVD_ACT_GELU_ERF = 0,
+  FSVD_ACT_GELU_TANH = 1,
+  FSVD_ACT_RELU = 2,
+  FSVD_ACT_IDENTITY = 3
+} fsvd_activation;
+
+/* encoder.hpp:21 */
+typedef enum fsvd_run_mode {
+  FSVD_MODE_DENSE = 0,
+  FSVD_MODE_NAIVE_LOWRANK = 1,
+  FSVD_MODE_FLASH_V1 = 2,
+  FSVD_MODE_FLASH_V2 = 3
+} fsvd_run_mode;
+
+/* memtier.hpp:159 */
+typedef enum fsvd_kernel_kind {
+  FSVD_KERNEL_ATTENTION = 0,
+  FSVD_KERNEL_FFN_V1 = 1,
+  FSVD_KERNEL_FFN_V2 = 2
+} fsvd_kernel_kind;
+
+/* memtier.hpp:169-178 (FormulaId) */
+typedef enum fsvd_formula {
+  FSVD_FORMULA_DENSE_ATTN = 0,
+  FSVD_FORMULA_FLASH_ATTN_DENSE_QKV = 1,
+  FSVD_FORMULA_FLASH_SVD_ATTN = 2,
+  FSVD_FORMULA_GROUPED_ATTN = 3,
+  FSVD_FORMULA_FFN_DENSE = 4,
+  FSVD_FORMULA_FFN_NAIVE_LOWRANK = 5,
+  FSVD_FORMULA_FFN_V1 = 6,
+  FSVD_FORMULA_FFN_V2 = 7
+} fsvd_formula;
+
+/* memtier.hpp:152-157 (TilePlan). */
+typedef struct fsvd_tile_plan {
+  size_t bm, br, bdf, sram_budget_bytes;
+} fsvd_tile_plan;
+
+/* geometry.hpp:11-20 */
+typedef struct fsvd_geometry {
+  size_t batch, seq_len, d_model, d_ff, heads, groups, rank, layers;
+} fsvd_geometry;
+
+/* FactorizedLinear (factorize.hpp:13-21): w (in x out) ~ u (in x r) v (r x out). */
+typedef struct fsvd_linear_desc {
+  size_t in_dim, rank, out_dim;
+  const float* u;    /* [in_dim][rank]  */
+  const float* v;    /* [rank][out_dim] */
+  const float* bias; /* [out_dim]       */
+} fsvd_linear_desc;
+
+/* AttentionFactorSet (factorize.hpp:28-40), groups stored contiguously:
+ *   u    [3][groups][d_model][rank]          (q, k, v)
+ *   v    [3][groups][rank][d_model/groups]
+ *   bias [3][groups][d_model/groups] == [3][d_model]                         */
+typedef struct fsvd_attn_desc {
+  size_t d_model, groups, rank;
+  const float* u;
+  const float* v;
+  const float* bias;
+} fsvd_attn_desc;
+
+/* FfnFactors (ffn.hpp:17-21) */
+typedef struct fsvd_ffn_desc {
+  fsvd_linear_desc up;   /* d_model -> d_ff */
+  fsvd_linear_desc down; /* d_ff -> d_model */
+  fsvd_activation activation;
+} fsvd_ffn_desc;
+
+/* EncoderLayer (encoder.hpp:49-67), fully factorized form. */
+typedef struct fsvd_layer_desc {
+  size_t heads;
+  fsvd_attn_desc attn;
+  fsvd_linear_desc out_proj;
+  fsvd_ffn_desc ffn;
+  const float* ln1_gamma; const float* ln1_beta; float ln1_eps;
+  const float* ln2_gamma; const float* ln2_beta; float ln2_eps;
+} fsvd_layer_desc;
+
+/* ------------------------------------------------------------------ */
+/* Library / errors                                                    */
+/* ------------------------------------------------------------------ */
+int fsvd_abi_version(void);
+/* Message of the last failed call on this thread ("" if none). */
+const char* fsvd_last_error(void);
+/* 1 if an sm_100 device is usable, else 0 (message in fsvd_last_error). */
+int fsvd_device_available(void);
+
+/* ------------------------------------------------------------------ */
+/* MemoryMeter (memtier.hpp:45-146, memtier.cpp:8-116)                  */
+/* Byte meter of the two-tier model.  4 B/element reference accounting  */
+/* plus a separate device high-water of the real (bf16/fp32) bytes.     */
+/* ------------------------------------------------------------------ */
+typedef struct fsvd_meter fsvd_meter;
+typedef enum fsvd_alloc_class {
+  FSVD_TRANSIENT = 0, FSVD_PERSISTENT = 1, FSVD_EXCLUDED = 2
+} fsvd_alloc_class;
+typedef enum fsvd_event_kind {
+  FSVD_EV_ALLOC = 0, FSVD_EV_FREE = 1, FSVD_EV_PIN = 2,
+  FSVD_EV_REGION_BEGIN = 3, FSVD_EV_REGION_END = 4
+} fsvd_event_kind;
+
+fsvd_status fsvd_meter_create(fsvd_meter** out);
+void fsvd_meter_destroy(fsvd_meter* m);
+fsvd_status fsvd_meter_alloc(fsvd_meter* m, const char* tag, fsvd_alloc_class cls,
+                             size_t bytes, uint64_t* id);
+fsvd_status fsvd_meter_free(fsvd_meter* m, uint64_t id);
+fsvd_status fsvd_meter_pin(fsvd_meter* m, const char* tag, size_t bytes);
+fsvd_status fsvd_meter_region_begin(fsvd_meter* m, const char* name, size_t* entry);
+fsvd_status fsvd_meter_region_end(fsvd_meter* m, const char* name, size_t entry);
+size_t fsvd_meter_current_transient(const fsvd_meter* m);
+size_t fsvd_meter_peak_transient(const fsvd_meter* m);
+size_t fsvd_meter_persistent(const fsvd_meter* m);
+size_t fsvd_meter_current_excluded(const fsvd_meter* m);
+void fsvd_meter_reset_peak(fsvd_meter* m);
+fsvd_status fsvd_meter_assert_clean(const fsvd_meter* m);
+size_t fsvd_meter_event_count(const fsvd_meter* m);
+fsvd_status fsvd_meter_event(const fsvd_meter* m, size_t index, int* kind, int* cls,
+                             size_t* bytes, uint64_t* id, char* tag, size_t tag_cap);
+/* Real device bytes: activation arena high-water and factor-pack bytes
+ * observed by operations run against this meter. */
+size_t fsvd_meter_device_peak_bytes(const fsvd_meter* m);
+size_t fsvd_meter_device_persistent_bytes(const fsvd_meter* m);
+
+/* ------------------------------------------------------------------ */
+/* Closed forms and plan validation (host only, no device needed)      */
+/* ------------------------------------------------------------------ */
+/* memtier.cpp:170-189: working-set bytes, FSVD_ERR_BUDGET / _CONFIG. */
+fsvd_status fsvd_validate_tile_plan(const fsvd_tile_plan* plan, fsvd_kernel_kind kind,
+                                    const fsvd_geometry* geom, size_t* bytes);
+/* memtier.cpp:191-212 */
+fsvd_status fsvd_expected_bytes(fsvd_formula id, const fsvd_geometry* geom, size_t* bytes);
+/* encoder.cpp:333-345 */
+size_t fsvd_flash_layer_peak_transient_bytes(const fsvd_geometry* geom);
+size_t fsvd_flash_layer_persistent_bytes(const fsvd_geometry* geom);
+size_t fsvd_flash_layer_bound_bytes(const fsvd_geometry* geom);
+
+/* ------------------------------------------------------------------ */
+/* Device factor packs (weights resident in HBM, kernel layouts)        */
+/* ------------------------------------------------------------------ */
+typedef struct fsvd_layer_pack fsvd_layer_pack;
+/* Uploads one fully factorized layer.  Validates like
+ * EncoderLayer::validate (encoder.cpp:156-222).  When dense != 0 the dense
+ * twin (encoder.cpp:295-331) is also built so FSVD_MODE_DENSE can run. */
+fsvd_status fsvd_layer_pack_create(const fsvd_layer_desc* layer, fsvd_dtype dtype,
+                                   int dense, fsvd_layer_pack** out);
+void fsvd_layer_pack_destroy(fsvd_layer_pack* p);
+size_t fsvd_layer_pack_device_bytes(const fsvd_layer_pack* p);
+/* 1 if this pack runs the tcgen05 tensor-core kernels, 0 if the SIMT
+ * kernels (fp32 policy or shapes outside the tensor-core tiling). */
+int fsvd_layer_pack_uses_tensor_cores(const fsvd_layer_pack* p);
+
+/* ------------------------------------------------------------------ */
+/* Device-resident async API (device pointers, cudaStream_t as void*)   */
+/* ------------------------------------------------------------------ */
+/* Bytes of workspace fsvd_model_fwd needs for this batch shape; the
+ * activation buffer planner sizes it by rank, not by hidden width. */
+fsvd_status fsvd_workspace_bytes(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                 size_t batch, size_t seq, fsvd_run_mode mode,
+                                 size_t* bytes);
+/* attention.cpp:202-269 (flash_svd_attention): x, ctx [batch, seq, d]. */
+fsvd_status fsvd_attention_fwd(const fsvd_layer_pack* p, size_t batch, size_t seq,
+                               const void* x, void* ctx, void* workspace,
+                               size_t workspace_bytes, void* stream);
+/* attention.cpp:366-391 (lowrank_output_projection) */
+fsvd_status fsvd_outproj_fwd(const fsvd_layer_pack* p, size_t batch, size_t seq,
+                             const void* ctx, void* out, void* workspace,
+                             size_t workspace_bytes, void* stream);
+/* ffn.cpp:118-156 (variant 1) and ffn.cpp:158-185 (variant 2) */
+fsvd_status fsvd_ffn_fwd(const fsvd_layer_pack* p, int variant, size_t batch, size_t seq,
+                         const void* x, void* out, void* workspace,
+                         size_t workspace_bytes, void* stream);
+/* encoder.cpp:224-260 (run_layer).  x and out may alias. */
+fsvd_status fsvd_layer_fwd(const fsvd_layer_pack* p, fsvd_run_mode mode, int pre_ln,
+                           size_t batch, size_t seq, const void* x, void* out,
+                           void* workspace, size_t workspace_bytes, void* stream);
+/* encoder.cpp:262-293 (run_model).  x and out may alias. */
+fsvd_status fsvd_model_fwd(const fsvd_layer_pack* const* packs, size_t n_layers,
+                           fsvd_run_mode mode, int pre_ln, size_t batch, size_t seq,
+                           const void* x, void* out, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* Host API: behavioural drop-ins for the reference free functions.     */
+/* fp32 host in/out, synchronous; H2D -> kernels -> D2H inside.  Shapes, */
+/* tile plans and meter pins/regions/transients are checked and charged */
+/* exactly as the reference does (4 B/element).  meter may be NULL.      */
+/* ------------------------------------------------------------------ */
+/* attention.hpp:18-21 */
+fsvd_status fsvd_flash_svd_attention(const float* x, size_t batch, size_t seq,
+                                     size_t width, const fsvd_attn_desc* set,
+                                     size_t heads, const fsvd_tile_plan* plan,
+                                     fsvd_dtype dtype, fsvd_meter* meter,
+                                     const char* pin_prefix, float* out,
+                                     size_t out_batch, size_t out_seq, size_t out_width);
+/* attention.hpp:49-51 */
+fsvd_status fsvd_lowrank_output_projection(const float* ctx, size_t batch, size_t seq,
+                                           size_t width, const fsvd_linear_desc* proj,
+                                           fsvd_dtype dtype, fsvd_meter* meter,
+                                           const char* pin_prefix, float* out,
+                                           size_t out_batch, size_t out_seq,
+                                           size_t out_width);
+/* ffn.hpp:33-34 (variant 1) and ffn.hpp:40-41 (variant 2) */
+fsvd_status fsvd_ffn(int variant, const float* x, size_t batch, size_t seq, size_t width,
+                     const fsvd_ffn_desc* f, const fsvd_tile_plan* plan, fsvd_dtype dtype,
+                     fsvd_meter* meter, const char* pin_prefix, float* out,
+                     size_t out_batch, size_t out_seq, size_t out_width);
+/* encoder.hpp:83-85 */
+fsvd_status fsvd_run_layer(const float* x, size_t batch, size_t seq, size_t width,
+                           const fsvd_layer_desc* layer, fsvd_run_mode mode,
+                           const fsvd_tile_plan* plan, int pre_ln, const char* meter_prefix,
+                           fsvd_dtype dtype, fsvd_meter* meter, float* out);
+/* encoder.hpp:90-92 */
+fsvd_status fsvd_run_model(const float* x, size_t batch, size_t seq, size_t width,
+                           const fsvd_layer_desc* layers, size_t n_layers,
+                           fsvd_run_mode mode, const fsvd_tile_plan* plan, int pre_ln,
+                           const char* meter_prefix, fsvd_dtype dtype, fsvd_meter* meter,
+                           float* out);
+
+/* ------------------------------------------------------------------ */
+/* Instrumentation                                                     */
+/* ------------------------------------------------------------------ */
+/* Number of kernels this library launched since load (all streams). */
+uint64_t fsvd_kernel_launch_count(void);
+/* Name of the kernel that dominated the last fsvd_model_fwd schedule. */
+const char* fsvd_kernel_name(int kernel_id);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSVD_B200_H */

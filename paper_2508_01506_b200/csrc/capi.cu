@@ -1,0 +1,708 @@
+// capi.cu -- the extern "C" boundary (include/fsvd_b200.h).
+//
+// Exceptions never cross this file's entry points: every call is wrapped in
+// guard(), which maps fsvd::Error kinds 1:1 onto fsvd_status and stores the
+// message for fsvd_last_error().
+//
+// The host API (fsvd_flash_svd_attention ... fsvd_run_model) is the
+// behavioural drop-in for the reference free functions: it performs the
+// reference's shape / plan checks with the same error kinds, charges the
+// meter with the same pins, regions and transient tags at 4 B/element
+// (attention.cpp:216-233, :375-379; ffn.cpp:123-128, :163-165;
+// encoder.cpp:224-293), then uploads, runs the device schedule and
+// downloads.
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/fsvd_b200.h"
+#include "common.cuh"
+#include "meter.hpp"
+#include "runtime.hpp"
+
+struct fsvd_meter {
+  fsvd::Meter m;
+};
+
+namespace fsvd {
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+fsvd_status guard(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return FSVD_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return static_cast<fsvd_status>(static_cast<int>(e.kind));
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return FSVD_ERR_CUDA;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return FSVD_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return FSVD_ERR_CUDA;
+  }
+}
+
+void require_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    fail(Kind::Cuda, std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                         "); this library has no CPU fallback");
+  }
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) fail(Kind::Cuda, "device is not sm_100 (Blackwell B200)");
+}
+
+// ------------------------------------------------------------- plan checks
+// memtier.cpp:125-189 (working set in fp32 elements, BudgetError names the
+// largest buffer).
+size_t working_set(const fsvd_tile_plan& plan, int kind, const fsvd_geometry& g,
+                   bool throw_on_budget) {
+  if (plan.bm == 0 || plan.br == 0 || plan.bdf == 0)
+    fail(Kind::Config, "tile dimensions must be positive");
+  if (g.groups == 0 || g.d_model % g.groups != 0) fail(Kind::Config, "groups must divide d_model");
+  const size_t bm = plan.bm, br = plan.br, bdf = plan.bdf, gd = g.d_model / g.groups,
+               r = g.rank;
+  struct Buf {
+    const char* name;
+    size_t n;
+  };
+  std::vector<Buf> bufs;
+  if (kind == FSVD_KERNEL_ATTENTION)
+    bufs = {{"q_tile", bm * gd},   {"k_tile", br * gd},     {"v_tile", br * gd},
+            {"score_tile", bm * br}, {"prob_tile", bm * br}, {"out_acc", bm * gd},
+            {"load_stage", std::max(bm, br) * gd}, {"row_max", bm}, {"row_sum", bm},
+            {"bias_row", gd}};
+  else if (kind == FSVD_KERNEL_FFN_V1)
+    bufs = {{"h_tile", bm * bdf}, {"p_row_tile", bm * r}, {"z_acc_tile", bm * r},
+            {"v1_panel", r * bdf}, {"u2_panel", bdf * r}, {"bias_slice", bdf}};
+  else if (kind == FSVD_KERNEL_FFN_V2)
+    bufs = {{"h_tile", bm * bdf},  {"p_tile", bm * r},     {"p_row_tile", bm * r},
+            {"z_acc_tile", bm * r}, {"v1_panel", r * bdf}, {"u2_panel", bdf * r},
+            {"bias_slice", bdf},    {"out_row", g.d_model}};
+  else
+    fail(Kind::Config, "unknown kernel kind");
+  size_t total = 0;
+  const Buf* largest = &bufs[0];
+  for (const Buf& b : bufs) {
+    total += b.n;
+    if (b.n > largest->n) largest = &b;
+  }
+  const size_t bytes = 4 * total;
+  if (throw_on_budget && bytes > plan.sram_budget_bytes)
+    fail(Kind::Budget, "tile working set " + std::to_string(bytes) + " bytes exceeds budget " +
+                           std::to_string(plan.sram_budget_bytes) + "; largest buffer is \"" +
+                           largest->name + "\" (" + std::to_string(4 * largest->n) + " bytes)");
+  return bytes;
+}
+
+fsvd_tile_plan plan_or_default(const fsvd_tile_plan* p) {
+  if (p) return *p;
+  return fsvd_tile_plan{16, 16, 64, 131072};
+}
+
+size_t expected(int id, const fsvd_geometry& g) {
+  const size_t b = g.batch, m = g.seq_len, da = g.d_model, df = g.d_ff, h = g.heads,
+               gr = g.groups, r = g.rank;
+  switch (id) {
+    case FSVD_FORMULA_DENSE_ATTN: return 4 * (3 * b * m * da + b * h * m * m);
+    case FSVD_FORMULA_FLASH_ATTN_DENSE_QKV: return 4 * (3 * b * m * da);
+    case FSVD_FORMULA_FLASH_SVD_ATTN: return 4 * (3 * h * b * m * r);
+    case FSVD_FORMULA_GROUPED_ATTN: return 4 * (3 * gr * b * m * r);
+    case FSVD_FORMULA_FFN_DENSE:
+    case FSVD_FORMULA_FFN_NAIVE_LOWRANK: return 4 * (b * m * df);
+    case FSVD_FORMULA_FFN_V1: return 4 * (2 * b * m * r);
+    case FSVD_FORMULA_FFN_V2: return 0;
+  }
+  fail(Kind::Config, "unknown formula id");
+}
+
+// ------------------------------------------------------------- host staging
+// Device copies of a host fp32 activation in the pack dtype, plus the
+// workspace, freed on scope exit.
+struct DevMem {
+  void* p = nullptr;
+  explicit DevMem(size_t bytes) {
+    if (bytes) FSVD_CUDA_CHECK(cudaMalloc(&p, bytes));
+  }
+  ~DevMem() {
+    if (p) cudaFree(p);
+  }
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+};
+
+void upload(const float* host, size_t n, fsvd_dtype dt, void* dev, cudaStream_t s) {
+  DevMem tmp(n * 4);
+  FSVD_CUDA_CHECK(cudaMemcpyAsync(tmp.p, host, n * 4, cudaMemcpyHostToDevice, s));
+  if (dt == FSVD_BF16) convert_f32<bf16>(static_cast<float*>(tmp.p), static_cast<bf16*>(dev), n, s);
+  else FSVD_CUDA_CHECK(cudaMemcpyAsync(dev, tmp.p, n * 4, cudaMemcpyDeviceToDevice, s));
+  FSVD_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+void download(const void* dev, size_t n, fsvd_dtype dt, float* host, cudaStream_t s) {
+  DevMem tmp(n * 4);
+  if (dt == FSVD_BF16) to_f32<bf16>(static_cast<const bf16*>(dev), static_cast<float*>(tmp.p), n, s);
+  else FSVD_CUDA_CHECK(cudaMemcpyAsync(tmp.p, dev, n * 4, cudaMemcpyDeviceToDevice, s));
+  FSVD_CUDA_CHECK(cudaMemcpyAsync(host, tmp.p, n * 4, cudaMemcpyDeviceToHost, s));
+  FSVD_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+// Runs fn(x_dev, out_dev, trans_dev, stream) on a temporary device arena and
+// reports the arena to the meter's device high-water.
+template <typename F>
+void run_on_device(const float* x, size_t n_in, float* out, size_t n_out, fsvd_dtype dt,
+                   size_t trans_bytes, const Pack& pack, Meter* meter, F&& fn) {
+  require_device();
+  const size_t es = dt == FSVD_BF16 ? 2 : 4;
+  const size_t in_b = (n_in * es + 255) & ~size_t(255), out_b = (n_out * es + 255) & ~size_t(255);
+  DevMem arena(in_b + out_b + trans_bytes + 256);
+  uint8_t* base = static_cast<uint8_t*>(arena.p);
+  cudaStream_t s = nullptr;
+  upload(x, n_in, dt, base, s);
+  fn(base, base + in_b, base + in_b + out_b, s);
+  FSVD_CUDA_CHECK(cudaGetLastError());
+  download(base + in_b, n_out, dt, out, s);
+  if (meter) meter->note_device(in_b + out_b + trans_bytes, pack.bytes);
+}
+
+std::unique_ptr<Pack> pack_attention(const fsvd_attn_desc& a, size_t heads, fsvd_dtype dt) {
+  PackRequest q;
+  q.attn = &a;
+  q.heads = heads;
+  q.d_model = a.d_model;
+  return std::unique_ptr<Pack>(build_pack(q, dt));
+}
+
+void check_dtype(fsvd_dtype dt) {
+  if (dt != FSVD_F32 && dt != FSVD_BF16) fail(Kind::Config, "unknown dtype");
+}
+
+// ---- reference-equivalent sublayers (checks + meter + device) ----------------
+void check_attention_io(size_t width, size_t d_model, size_t heads, size_t ob, size_t om,
+                        size_t ow, size_t b, size_t m) {
+  // attention.cpp:47-56
+  if (width != d_model) fail(Kind::Shape, "input feature width does not match the projections");
+  if (heads == 0 || d_model % heads != 0) fail(Kind::Config, "heads must divide d_model");
+  if (ob != b || om != m || ow != width)
+    fail(Kind::Shape, "attention output must be shaped like the input");
+}
+
+void host_attention(const float* x, size_t B, size_t M, size_t W, const fsvd_attn_desc& a,
+                    size_t heads, const fsvd_tile_plan& plan, fsvd_dtype dt, Meter* meter,
+                    const std::string& pfx, float* out, size_t ob, size_t om, size_t ow) {
+  check_dtype(dt);
+  check_attention_io(W, a.d_model, heads, ob, om, ow, B, M);
+  if (a.groups == 0 || heads % a.groups != 0)
+    fail(Kind::Config, "factor groups must evenly cover the heads");
+  if (B == 0 || M == 0) fail(Kind::Shape, "tensor extent must be at least 1");
+  const size_t d = a.d_model, G = a.groups, r = a.rank, gd = d / G;
+  fsvd_geometry geo{B, M, d, 1, heads, heads, 1, 1};
+  working_set(plan, FSVD_KERNEL_ATTENTION, geo, true);
+  static const char* names[3] = {"q", "k", "v"};
+  if (meter)
+    for (int mat = 0; mat < 3; ++mat)
+      for (size_t g = 0; g < G; ++g)
+        meter->pin(pfx + "." + names[mat] + ".g" + std::to_string(g) + ".v", 4 * r * gd);
+  MeterScope region(meter, "flash_svd_attention");
+  MeterBuffer pq(meter, "p_q", MeterClass::Transient, G * B * M * r);
+  MeterBuffer pk(meter, "p_k", MeterClass::Transient, G * B * M * r);
+  MeterBuffer pv(meter, "p_v", MeterClass::Transient, G * B * M * r);
+  auto pack = pack_attention(a, heads, dt);
+  const size_t trans = B * M * op_transient_elems(*pack, 0, FSVD_MODE_FLASH_V1) * pack->es;
+  run_on_device(x, B * M * d, out, B * M * d, dt, trans, *pack, meter,
+                [&](void* xd, void* od, void* td, cudaStream_t s) {
+                  attention_fwd(*pack, FSVD_MODE_FLASH_V1, B, M, xd, od, td, s);
+                });
+}
+
+void host_outproj(const float* ctx, size_t B, size_t M, size_t W, const fsvd_linear_desc& o,
+                  fsvd_dtype dt, Meter* meter, const std::string& pfx, float* out, size_t ob,
+                  size_t om, size_t ow) {
+  check_dtype(dt);
+  // attention.cpp:369-372
+  if (W != o.in_dim) fail(Kind::Shape, "context width does not match the projection factors");
+  if (ob != B || om != M || ow != W || o.out_dim != W)
+    fail(Kind::Shape, "output projection must preserve the activation shape");
+  const size_t d = o.in_dim, r = o.rank;
+  if (meter) {
+    meter->pin(pfx + ".out.u", 4 * d * r);
+    meter->pin(pfx + ".out.v", 4 * r * o.out_dim);
+  }
+  MeterScope region(meter, "lowrank_output_projection");
+  MeterBuffer p(meter, "p_out", MeterClass::Transient, B * M * r);
+  PackRequest q;
+  q.out_proj = &o;
+  q.d_model = d;
+  std::unique_ptr<Pack> pack(build_pack(q, dt));
+  const size_t trans = B * M * op_transient_elems(*pack, 1, FSVD_MODE_FLASH_V1) * pack->es;
+  run_on_device(ctx, B * M * d, out, B * M * d, dt, trans, *pack, meter,
+                [&](void* xd, void* od, void* td, cudaStream_t s) {
+                  outproj_fwd(*pack, FSVD_MODE_FLASH_V1, B, M, xd, od, td, s);
+                });
+}
+
+void check_ffn_io(size_t W, const fsvd_ffn_desc& f, size_t ob, size_t om, size_t ow, size_t B,
+                  size_t M) {
+  // ffn.cpp:40-50
+  if (f.up.in_dim != W || f.down.out_dim != W)
+    fail(Kind::Shape, "ffn factor dims do not match the activation width");
+  if (f.up.out_dim != f.down.in_dim) fail(Kind::Shape, "ffn up/down widths do not chain");
+  if (f.up.rank != f.down.rank) fail(Kind::Config, "ffn factor pairs must share one rank");
+  if (ob != B || om != M || ow != W) fail(Kind::Shape, "ffn output must be shaped like input");
+}
+
+void host_ffn(int variant, const float* x, size_t B, size_t M, size_t W, const fsvd_ffn_desc& f,
+              const fsvd_tile_plan& plan, fsvd_dtype dt, Meter* meter, const std::string& pfx,
+              float* out, size_t ob, size_t om, size_t ow) {
+  check_dtype(dt);
+  if (variant != 1 && variant != 2) fail(Kind::Config, "ffn variant must be 1 or 2");
+  check_ffn_io(W, f, ob, om, ow, B, M);
+  const size_t d = W, df = f.up.out_dim, r = f.up.rank;
+  fsvd_geometry geo{B, M, d, df, 1, 1, r, 1};
+  working_set(plan, variant == 1 ? FSVD_KERNEL_FFN_V1 : FSVD_KERNEL_FFN_V2, geo, true);
+  if (meter) {  // ffn.cpp:64-70
+    meter->pin(pfx + ".up.u", 4 * d * r);
+    meter->pin(pfx + ".up.v", 4 * r * df);
+    meter->pin(pfx + ".down.u", 4 * df * r);
+    meter->pin(pfx + ".down.v", 4 * r * d);
+  }
+  MeterScope region(meter, variant == 1 ? "ffn_v1" : "ffn_v2");
+  std::unique_ptr<MeterBuffer> pm, zm;
+  if (variant == 1) {
+    pm = std::make_unique<MeterBuffer>(meter, "p_mid", MeterClass::Transient, B * M * r);
+    zm = std::make_unique<MeterBuffer>(meter, "z_mid", MeterClass::Transient, B * M * r);
+  }
+  PackRequest q;
+  q.ffn = &f;
+  q.d_model = d;
+  std::unique_ptr<Pack> pack(build_pack(q, dt));
+  const int mode = variant == 1 ? FSVD_MODE_FLASH_V1 : FSVD_MODE_FLASH_V2;
+  const size_t trans = B * M * op_transient_elems(*pack, 2, mode) * pack->es;
+  run_on_device(x, B * M * d, out, B * M * d, dt, trans, *pack, meter,
+                [&](void* xd, void* od, void* td, cudaStream_t s) {
+                  ffn_fwd(*pack, mode, B, M, xd, od, td, s);
+                });
+  zm.reset();
+  pm.reset();
+}
+
+// Meter sequence of one layer (encoder.cpp:224-260) for every run mode; the
+// device work runs separately on the whole model (layer_fwd).
+void meter_layer(Meter* meter, const fsvd_layer_desc& L, int mode, const fsvd_tile_plan& plan,
+                 bool pre_ln, const std::string& pfx, size_t B, size_t M) {
+  const size_t d = L.attn.d_model, n = B * M * d, G = L.attn.groups, r = L.attn.rank,
+               gd = d / G, df = L.ffn.up.out_dim, fr = L.ffn.up.rank, pr = L.out_proj.rank,
+               H = L.heads;
+  MeterBuffer ctx(meter, pfx + ".attn_ctx", MeterClass::Excluded, n);
+  MeterBuffer branch(meter, pfx + ".sublayer_out", MeterClass::Excluded, n);
+  MeterBuffer resid(meter, pfx + ".resid", MeterClass::Excluded, n);
+  std::unique_ptr<MeterBuffer> normed;
+  if (pre_ln) normed = std::make_unique<MeterBuffer>(meter, pfx + ".norm_in", MeterClass::Excluded, n);
+  {
+    MeterScope sub(meter, pfx + ".attn");
+    if (mode == FSVD_MODE_DENSE) {
+      MeterScope rg(meter, "dense_attention");
+      MeterBuffer q(meter, "q_full", MeterClass::Transient, n);
+      MeterBuffer k(meter, "k_full", MeterClass::Transient, n);
+      MeterBuffer v(meter, "v_full", MeterClass::Transient, n);
+      MeterBuffer sc(meter, "scores", MeterClass::Transient, B * H * M * M);
+    } else if (mode == FSVD_MODE_NAIVE_LOWRANK) {
+      fsvd_geometry geo{B, M, d, 1, H, H, 1, 1};
+      working_set(plan, FSVD_KERNEL_ATTENTION, geo, true);
+      MeterScope rg(meter, "naive_lowrank_attention");
+      MeterBuffer q(meter, "q_full", MeterClass::Transient, n);
+      MeterBuffer k(meter, "k_full", MeterClass::Transient, n);
+      MeterBuffer v(meter, "v_full", MeterClass::Transient, n);
+    } else {
+      fsvd_geometry geo{B, M, d, 1, H, H, 1, 1};
+      working_set(plan, FSVD_KERNEL_ATTENTION, geo, true);
+      static const char* names[3] = {"q", "k", "v"};
+      if (meter)
+        for (int mat = 0; mat < 3; ++mat)
+          for (size_t g = 0; g < G; ++g)
+            meter->pin(pfx + ".attn." + names[mat] + ".g" + std::to_string(g) + ".v", 4 * r * gd);
+      {
+        MeterScope rg(meter, "flash_svd_attention");
+        MeterBuffer pq(meter, "p_q", MeterClass::Transient, G * B * M * r);
+        MeterBuffer pk(meter, "p_k", MeterClass::Transient, G * B * M * r);
+        MeterBuffer pv(meter, "p_v", MeterClass::Transient, G * B * M * r);
+      }
+      if (meter) {
+        meter->pin(pfx + ".attn.out.u", 4 * d * pr);
+        meter->pin(pfx + ".attn.out.v", 4 * pr * d);
+      }
+      MeterScope rg(meter, "lowrank_output_projection");
+      MeterBuffer p(meter, "p_out", MeterClass::Transient, B * M * pr);
+    }
+  }
+  {
+    MeterScope sub(meter, pfx + ".ffn");
+    if (mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK) {
+      MeterScope rg(meter, mode == FSVD_MODE_DENSE ? "ffn_dense" : "ffn_naive_lowrank");
+      MeterBuffer h(meter, "hidden", MeterClass::Transient, B * M * df);
+    } else {
+      const bool v1 = mode == FSVD_MODE_FLASH_V1;
+      fsvd_geometry geo{B, M, d, df, 1, 1, fr, 1};
+      working_set(plan, v1 ? FSVD_KERNEL_FFN_V1 : FSVD_KERNEL_FFN_V2, geo, true);
+      if (meter) {
+        meter->pin(pfx + ".ffn.up.u", 4 * d * fr);
+        meter->pin(pfx + ".ffn.up.v", 4 * fr * df);
+        meter->pin(pfx + ".ffn.down.u", 4 * df * fr);
+        meter->pin(pfx + ".ffn.down.v", 4 * fr * d);
+      }
+      MeterScope rg(meter, v1 ? "ffn_v1" : "ffn_v2");
+      if (v1) {
+        MeterBuffer pm(meter, "p_mid", MeterClass::Transient, B * M * fr);
+        MeterBuffer zm(meter, "z_mid", MeterClass::Transient, B * M * fr);
+      }
+    }
+  }
+}
+
+void check_mode(int mode) {
+  if (mode < FSVD_MODE_DENSE || mode > FSVD_MODE_FLASH_V2) fail(Kind::Config, "unknown run mode");
+}
+
+void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_layer_desc* layers,
+                    size_t n_layers, int mode, const fsvd_tile_plan& plan, bool pre_ln,
+                    const std::string& prefix, fsvd_dtype dt, Meter* meter, float* out,
+                    bool single_layer_api) {
+  check_dtype(dt);
+  check_mode(mode);
+  if (B == 0 || M == 0 || W == 0) fail(Kind::Shape, "run_model: x must be (batch, seq, d_model)");
+  if (x == out) fail(Kind::Config, "run_model: out must be a distinct tensor");
+  if (n_layers == 0) {
+    std::memcpy(out, x, sizeof(float) * B * M * W);
+    return;
+  }
+  for (size_t i = 0; i < n_layers; ++i) {
+    validate_layer(layers[i]);
+    if (layers[i].attn.d_model != W) fail(Kind::Shape, "run_layer: x must be (batch, seq, d_model)");
+  }
+  // meter: encoder.cpp:274-292 (ping/pong only for more than one layer)
+  {
+    std::unique_ptr<MeterBuffer> ping, pong;
+    if (!single_layer_api && n_layers > 1) {
+      ping = std::make_unique<MeterBuffer>(meter, prefix + ".interlayer.0", MeterClass::Excluded, B * M * W);
+      pong = std::make_unique<MeterBuffer>(meter, prefix + ".interlayer.1", MeterClass::Excluded, B * M * W);
+    }
+    for (size_t i = 0; i < n_layers; ++i) {
+      const std::string pfx = single_layer_api ? prefix : prefix + "." + std::to_string(i);
+      meter_layer(meter, layers[i], mode, plan, pre_ln, pfx, B, M);
+    }
+  }
+  // device
+  std::vector<std::unique_ptr<Pack>> packs;
+  size_t ws = 0, pack_bytes = 0;
+  for (size_t i = 0; i < n_layers; ++i) {
+    PackRequest q;
+    q.attn = &layers[i].attn;
+    q.heads = layers[i].heads;
+    q.out_proj = &layers[i].out_proj;
+    q.ffn = &layers[i].ffn;
+    q.ln1g = layers[i].ln1_gamma;
+    q.ln1b = layers[i].ln1_beta;
+    q.ln2g = layers[i].ln2_gamma;
+    q.ln2b = layers[i].ln2_beta;
+    q.eps1 = layers[i].ln1_eps;
+    q.eps2 = layers[i].ln2_eps;
+    q.d_model = W;
+    q.dense = mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK;
+    packs.emplace_back(build_pack(q, dt));
+    if (q.dense && !packs.back()->dense)
+      fail(Kind::Config, "dense / naive_lowrank modes run only on the bf16 tensor-core path");
+    ws = std::max(ws, layer_workspace_bytes(*packs.back(), B * M, mode));
+    pack_bytes += packs.back()->bytes;
+  }
+  run_on_device(x, B * M * W, out, B * M * W, dt, ws, *packs[0], nullptr,
+                [&](void* xd, void* od, void* td, cudaStream_t s) {
+                  for (size_t i = 0; i < n_layers; ++i)
+                    layer_fwd(*packs[i], mode, pre_ln, B, M, i == 0 ? xd : od, od, td, ws, s);
+                });
+  if (meter) meter->note_device(2 * B * M * W * packs[0]->es + ws, pack_bytes);
+}
+
+}  // namespace
+}  // namespace fsvd
+
+using namespace fsvd;
+
+extern "C" {
+
+int fsvd_abi_version(void) { return FSVD_ABI_VERSION; }
+const char* fsvd_last_error(void) { return g_last_error.c_str(); }
+int fsvd_device_available(void) {
+  return guard([] { require_device(); }) == FSVD_OK ? 1 : 0;
+}
+
+// ---------------------------------------------------------------- meter
+fsvd_status fsvd_meter_create(fsvd_meter** out) {
+  return guard([&] {
+    if (!out) fail(Kind::Config, "null out pointer");
+    *out = new fsvd_meter();
+  });
+}
+void fsvd_meter_destroy(fsvd_meter* m) { delete m; }
+fsvd_status fsvd_meter_alloc(fsvd_meter* m, const char* tag, fsvd_alloc_class cls, size_t bytes,
+                             uint64_t* id) {
+  return guard([&] {
+    const uint64_t h = m->m.alloc(tag ? tag : "", static_cast<MeterClass>(cls), bytes);
+    if (id) *id = h;
+  });
+}
+fsvd_status fsvd_meter_free(fsvd_meter* m, uint64_t id) {
+  return guard([&] { m->m.free(id); });
+}
+fsvd_status fsvd_meter_pin(fsvd_meter* m, const char* tag, size_t bytes) {
+  return guard([&] { m->m.pin(tag ? tag : "", bytes); });
+}
+fsvd_status fsvd_meter_region_begin(fsvd_meter* m, const char* name, size_t* entry) {
+  return guard([&] {
+    const size_t e = m->m.region_begin(name ? name : "");
+    if (entry) *entry = e;
+  });
+}
+fsvd_status fsvd_meter_region_end(fsvd_meter* m, const char* name, size_t entry) {
+  return guard([&] { m->m.region_end(name ? name : "", entry); });
+}
+size_t fsvd_meter_current_transient(const fsvd_meter* m) { return m->m.current_transient(); }
+size_t fsvd_meter_peak_transient(const fsvd_meter* m) { return m->m.peak_transient(); }
+size_t fsvd_meter_persistent(const fsvd_meter* m) { return m->m.persistent(); }
+size_t fsvd_meter_current_excluded(const fsvd_meter* m) { return m->m.current_excluded(); }
+void fsvd_meter_reset_peak(fsvd_meter* m) { m->m.reset_peak(); }
+fsvd_status fsvd_meter_assert_clean(const fsvd_meter* m) {
+  return guard([&] { m->m.assert_clean(); });
+}
+size_t fsvd_meter_event_count(const fsvd_meter* m) { return m->m.event_count(); }
+fsvd_status fsvd_meter_event(const fsvd_meter* m, size_t index, int* kind, int* cls, size_t* bytes,
+                             uint64_t* id, char* tag, size_t tag_cap) {
+  return guard([&] {
+    if (index >= m->m.event_count()) fail(Kind::Config, "event index out of range");
+    const MeterEventRec e = m->m.event(index);
+    if (kind) *kind = static_cast<int>(e.kind);
+    if (cls) *cls = static_cast<int>(e.cls);
+    if (bytes) *bytes = e.bytes;
+    if (id) *id = e.id;
+    if (tag && tag_cap) {
+      std::strncpy(tag, e.tag.c_str(), tag_cap - 1);
+      tag[tag_cap - 1] = 0;
+    }
+  });
+}
+size_t fsvd_meter_device_peak_bytes(const fsvd_meter* m) { return m->m.device_peak(); }
+size_t fsvd_meter_device_persistent_bytes(const fsvd_meter* m) { return m->m.device_persistent(); }
+
+// ---------------------------------------------------------------- closed forms
+fsvd_status fsvd_validate_tile_plan(const fsvd_tile_plan* plan, fsvd_kernel_kind kind,
+                                    const fsvd_geometry* geom, size_t* bytes) {
+  size_t b = 0;
+  fsvd_status st = guard([&] {
+    if (!plan || !geom) fail(Kind::Config, "null argument");
+    b = working_set(*plan, kind, *geom, false);
+    if (bytes) *bytes = b;
+    working_set(*plan, kind, *geom, true);
+  });
+  return st;
+}
+fsvd_status fsvd_expected_bytes(fsvd_formula id, const fsvd_geometry* geom, size_t* bytes) {
+  return guard([&] {
+    if (!geom || !bytes) fail(Kind::Config, "null argument");
+    *bytes = expected(id, *geom);
+  });
+}
+size_t fsvd_flash_layer_peak_transient_bytes(const fsvd_geometry* g) {
+  return 4 * 3 * g->groups * g->batch * g->seq_len * g->rank;
+}
+size_t fsvd_flash_layer_persistent_bytes(const fsvd_geometry* g) {
+  return 4 * g->rank * (7 * g->d_model + 2 * g->d_ff);
+}
+size_t fsvd_flash_layer_bound_bytes(const fsvd_geometry* g) {
+  const size_t c = std::max<size_t>(3 * g->groups, 7);
+  return 4 * c * g->rank * (g->batch * g->seq_len + g->d_model + g->d_ff);
+}
+
+// ---------------------------------------------------------------- packs
+fsvd_status fsvd_layer_pack_create(const fsvd_layer_desc* layer, fsvd_dtype dtype, int dense,
+                                   fsvd_layer_pack** out) {
+  return guard([&] {
+    if (!layer || !out) fail(Kind::Config, "null argument");
+    check_dtype(dtype);
+    validate_layer(*layer);
+    require_device();
+    PackRequest q;
+    q.attn = &layer->attn;
+    q.heads = layer->heads;
+    q.out_proj = &layer->out_proj;
+    q.ffn = &layer->ffn;
+    q.ln1g = layer->ln1_gamma;
+    q.ln1b = layer->ln1_beta;
+    q.ln2g = layer->ln2_gamma;
+    q.ln2b = layer->ln2_beta;
+    q.eps1 = layer->ln1_eps;
+    q.eps2 = layer->ln2_eps;
+    q.d_model = layer->attn.d_model;
+    q.dense = dense != 0;
+    std::unique_ptr<Pack> p(build_pack(q, dtype));
+    *out = new fsvd_layer_pack{p.release()};
+  });
+}
+void fsvd_layer_pack_destroy(fsvd_layer_pack* p) {
+  if (p) {
+    delete p->p;
+    delete p;
+  }
+}
+size_t fsvd_layer_pack_device_bytes(const fsvd_layer_pack* p) { return p ? p->p->bytes : 0; }
+int fsvd_layer_pack_uses_tensor_cores(const fsvd_layer_pack* p) {
+  return p && p->p->attn_tc && p->p->out_tc && p->p->ffn_tc ? 1 : 0;
+}
+
+// ---------------------------------------------------------------- device API
+fsvd_status fsvd_workspace_bytes(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                 size_t batch, size_t seq, fsvd_run_mode mode, size_t* bytes) {
+  return guard([&] {
+    if (!bytes) fail(Kind::Config, "null argument");
+    check_mode(mode);
+    size_t ws = 0;
+    for (size_t i = 0; i < n_layers; ++i)
+      ws = std::max(ws, layer_workspace_bytes(*packs[i]->p, batch * seq, mode));
+    *bytes = ws;
+  });
+}
+fsvd_status fsvd_attention_fwd(const fsvd_layer_pack* p, size_t batch, size_t seq, const void* x,
+                               void* ctx, void* ws, size_t ws_bytes, void* stream) {
+  return guard([&] {
+    const size_t need = batch * seq * op_transient_elems(*p->p, 0, FSVD_MODE_FLASH_V1) * p->p->es;
+    if (ws_bytes < need) fail(Kind::Config, "workspace too small for attention");
+    attention_fwd(*p->p, FSVD_MODE_FLASH_V1, batch, seq, x, ctx, ws, static_cast<cudaStream_t>(stream));
+  });
+}
+fsvd_status fsvd_outproj_fwd(const fsvd_layer_pack* p, size_t batch, size_t seq, const void* ctx,
+                             void* out, void* ws, size_t ws_bytes, void* stream) {
+  return guard([&] {
+    const size_t need = batch * seq * op_transient_elems(*p->p, 1, FSVD_MODE_FLASH_V1) * p->p->es;
+    if (ws_bytes < need) fail(Kind::Config, "workspace too small for the output projection");
+    outproj_fwd(*p->p, FSVD_MODE_FLASH_V1, batch, seq, ctx, out, ws, static_cast<cudaStream_t>(stream));
+  });
+}
+fsvd_status fsvd_ffn_fwd(const fsvd_layer_pack* p, int variant, size_t batch, size_t seq,
+                         const void* x, void* out, void* ws, size_t ws_bytes, void* stream) {
+  return guard([&] {
+    if (variant != 1 && variant != 2) fail(Kind::Config, "ffn variant must be 1 or 2");
+    const int mode = variant == 1 ? FSVD_MODE_FLASH_V1 : FSVD_MODE_FLASH_V2;
+    const size_t need = batch * seq * op_transient_elems(*p->p, 2, mode) * p->p->es;
+    if (ws_bytes < need) fail(Kind::Config, "workspace too small for the FFN");
+    ffn_fwd(*p->p, mode, batch, seq, x, out, ws, static_cast<cudaStream_t>(stream));
+  });
+}
+fsvd_status fsvd_layer_fwd(const fsvd_layer_pack* p, fsvd_run_mode mode, int pre_ln, size_t batch,
+                           size_t seq, const void* x, void* out, void* ws, size_t ws_bytes,
+                           void* stream) {
+  return guard([&] {
+    check_mode(mode);
+    layer_fwd(*p->p, mode, pre_ln != 0, batch, seq, x, out, ws, ws_bytes,
+              static_cast<cudaStream_t>(stream));
+  });
+}
+fsvd_status fsvd_model_fwd(const fsvd_layer_pack* const* packs, size_t n_layers,
+                           fsvd_run_mode mode, int pre_ln, size_t batch, size_t seq,
+                           const void* x, void* out, void* ws, size_t ws_bytes, void* stream) {
+  return guard([&] {
+    check_mode(mode);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n_layers == 0) {
+      if (x != out) fail(Kind::Config, "model_fwd with no layers needs x == out or a copy");
+      return;
+    }
+    for (size_t i = 0; i < n_layers; ++i)
+      layer_fwd(*packs[i]->p, mode, pre_ln != 0, batch, seq, i == 0 ? x : out, out, ws, ws_bytes, s);
+  });
+}
+
+// ---------------------------------------------------------------- host API
+fsvd_status fsvd_flash_svd_attention(const float* x, size_t batch, size_t seq, size_t width,
+                                     const fsvd_attn_desc* set, size_t heads,
+                                     const fsvd_tile_plan* plan, fsvd_dtype dtype,
+                                     fsvd_meter* meter, const char* pin_prefix, float* out,
+                                     size_t ob, size_t om, size_t ow) {
+  return guard([&] {
+    if (!x || !set || !out) fail(Kind::Config, "null argument");
+    host_attention(x, batch, seq, width, *set, heads, plan_or_default(plan), dtype,
+                   meter ? &meter->m : nullptr, pin_prefix ? pin_prefix : "attn", out, ob, om, ow);
+  });
+}
+fsvd_status fsvd_lowrank_output_projection(const float* ctx, size_t batch, size_t seq,
+                                           size_t width, const fsvd_linear_desc* proj,
+                                           fsvd_dtype dtype, fsvd_meter* meter,
+                                           const char* pin_prefix, float* out, size_t ob,
+                                           size_t om, size_t ow) {
+  return guard([&] {
+    if (!ctx || !proj || !out) fail(Kind::Config, "null argument");
+    host_outproj(ctx, batch, seq, width, *proj, dtype, meter ? &meter->m : nullptr,
+                 pin_prefix ? pin_prefix : "attn", out, ob, om, ow);
+  });
+}
+fsvd_status fsvd_ffn(int variant, const float* x, size_t batch, size_t seq, size_t width,
+                     const fsvd_ffn_desc* f, const fsvd_tile_plan* plan, fsvd_dtype dtype,
+                     fsvd_meter* meter, const char* pin_prefix, float* out, size_t ob, size_t om,
+                     size_t ow) {
+  return guard([&] {
+    if (!x || !f || !out) fail(Kind::Config, "null argument");
+    host_ffn(variant, x, batch, seq, width, *f, plan_or_default(plan), dtype,
+             meter ? &meter->m : nullptr, pin_prefix ? pin_prefix : "ffn", out, ob, om, ow);
+  });
+}
+fsvd_status fsvd_run_layer(const float* x, size_t batch, size_t seq, size_t width,
+                           const fsvd_layer_desc* layer, fsvd_run_mode mode,
+                           const fsvd_tile_plan* plan, int pre_ln, const char* meter_prefix,
+                           fsvd_dtype dtype, fsvd_meter* meter, float* out) {
+  return guard([&] {
+    if (!x || !layer || !out) fail(Kind::Config, "null argument");
+    if (x == out) fail(Kind::Config, "run_layer: out must be a distinct tensor");
+    host_run_model(x, batch, seq, width, layer, 1, mode, plan_or_default(plan), pre_ln != 0,
+                   meter_prefix ? meter_prefix : "layer", dtype, meter ? &meter->m : nullptr, out,
+                   true);
+  });
+}
+fsvd_status fsvd_run_model(const float* x, size_t batch, size_t seq, size_t width,
+                           const fsvd_layer_desc* layers, size_t n_layers, fsvd_run_mode mode,
+                           const fsvd_tile_plan* plan, int pre_ln, const char* meter_prefix,
+                           fsvd_dtype dtype, fsvd_meter* meter, float* out) {
+  return guard([&] {
+    if (!x || (!layers && n_layers) || !out) fail(Kind::Config, "null argument");
+    const std::string pfx = meter_prefix ? meter_prefix : "layer";
+    if (n_layers == 1)
+      host_run_model(x, batch, seq, width, layers, 1, mode, plan_or_default(plan), pre_ln != 0,
+                     pfx + ".0", dtype, meter ? &meter->m : nullptr, out, true);
+    else
+      host_run_model(x, batch, seq, width, layers, n_layers, mode, plan_or_default(plan),
+                     pre_ln != 0, pfx, dtype, meter ? &meter->m : nullptr, out, false);
+  });
+}
+
+uint64_t fsvd_kernel_launch_count(void) { return launch_count(); }
+
+const char* fsvd_kernel_name(int id) {
+  switch (id) {
+    case 0: return "k_gemm_bf16";
+    case 1: return "k_attn_rankspace";
+    case 2: return "k_ffn_stream";
+    case 3: return "k_ffn_fused";
+    case 4: return "k_resid_ln";
+    default: return "";
+  }
+}
+
+}  // extern "C"

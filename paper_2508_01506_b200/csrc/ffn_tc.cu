@@ -1,0 +1,469 @@
+// ffn_tc.cu -- K3 / K4: FlashSVD-FFN on tcgen05.
+//
+// K3 (FUSED = false) replaces the V1 feature-block stream of ffn_v1
+// (ffn.cpp:136-147 -> stream_feature_blocks :84-104):
+//     Z[tile] = sum_f act(P[tile] V_up[:, f] + b_up[f]) U_down[f, :]
+// K4 (FUSED = true) replaces ffn_v2 (ffn.cpp:158-185) end to end:
+//     P = X U_up ; stream as above ; out = Z V_down + b_down
+// with nothing but the [T, d_model] output leaving the SM.
+//
+// One CTA owns 128 token rows.  The rank-width P tile lives in shared memory
+// (bf16, K-major SW128 atoms) for the whole stream; Z accumulates in TMEM
+// (FR fp32 columns) across every feature block; the d_ff-wide hidden exists
+// only as one 128 x 128 block: H in TMEM -> registers (+b_up, GELU) -> bf16
+// smem -> A operand of the next MMA.  B operands (V_up^T / U_down^T /
+// U_up^T / V_down^T chunks) stream through a TMA ring of 32 KB stages.
+//
+// Tensor-pipe order per block f: MMA1(f+1) is issued as soon as the
+// epilogue has drained H(f) from TMEM, so the GELU of block f overlaps the
+// next block's up-projection; MMA2(f) follows once bf16 H(f) is in smem.
+//
+// Warps: 0 TMA producer, 1 MMA issuer + TMEM owner, 2..9 epilogue (two warps
+// per TMEM lane quadrant, alternating 32-column chunks).
+#include "common.cuh"
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace fsvd {
+namespace {
+
+using namespace ptx;
+
+constexpr int kThreads = 320;
+constexpr int kEpi = 256;
+constexpr int BMr = 128;        // token rows per CTA
+constexpr int BF = 128;         // features per block
+constexpr int ATOM = BMr * 128; // one [128 x 64] bf16 SW128 atom (16 KB)
+constexpr int STAGE = 32768;
+
+template <int FR>
+struct FfnCfg {
+  static_assert(FR % 64 == 0 && FR <= 384, "FR must be a multiple of 64, <= 384");
+  static constexpr int STAGES = FR <= 256 ? 4 : 3;
+  static constexpr int NATOM = FR / 64;
+  static constexpr int o_p = 0;                      // P / Z tile, NATOM atoms
+  static constexpr int o_h = NATOM * ATOM;           // H tile, 2 atoms
+  static constexpr int o_ring = o_h + 2 * ATOM;
+  static constexpr int o_bar = o_ring + STAGES * STAGE;
+  static constexpr int SMEM = 1024 + o_bar + 512;
+  static constexpr int t_z = 0;      // Z / P accumulator (FR cols)
+  static constexpr int t_h = 384;    // H (128 cols)
+  static constexpr int NPIECE = (FR + 255) / 256;  // N pieces of Z / P (<= 256 each)
+  static constexpr int PS = FR / NPIECE;            // rows per piece (multiple of 16)
+};
+
+struct FfnBars {
+  uint64_t full[4], empty[4];
+  uint64_t p_full, p_acc, p_ready, h_full, h_free, sh_full, sh_free, z_full, zs_ready;
+  uint64_t o_full[2], o_free[2];
+  uint32_t tmem;
+};
+
+
+// 32 consecutive fp32 columns of this thread's TMEM row.
+__device__ __forceinline__ void ld_chunk(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  tmem_ld32(taddr, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+// Stores 32 values as bf16 at columns [c0, c0+32) of a K-major tile made of
+// [128 x 64] SW128 atoms.
+__device__ __forceinline__ void st_chunk_smem(uint32_t tile, uint32_t row, int c0,
+                                              const float (&v)[32]) {
+  const uint32_t atom = tile + (c0 >> 6) * ATOM;
+  const int cc = (c0 & 63) >> 3;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    st_shared_v4(atom + swz_offset(row, cc + c, 128), pack_bf16(v[8 * c + 0], v[8 * c + 1]),
+                 pack_bf16(v[8 * c + 2], v[8 * c + 3]), pack_bf16(v[8 * c + 4], v[8 * c + 5]),
+                 pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+}
+__device__ __forceinline__ void st_chunk_global(bf16* dst, const float (&v)[32]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    d[c] = make_uint4(pack_bf16(v[8 * c + 0], v[8 * c + 1]), pack_bf16(v[8 * c + 2], v[8 * c + 3]),
+                      pack_bf16(v[8 * c + 4], v[8 * c + 5]), pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+}
+
+template <int FR, bool FUSED>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_ffn(const __grid_constant__ CUtensorMap tmX,    // X [T, d]     box 128x64 (FUSED)
+          const __grid_constant__ CUtensorMap tmP,    // P [T, FR]    box 128x64 (V1)
+          const __grid_constant__ CUtensorMap tmUup,  // U_up^T [FR, d]  box 256x64
+          const __grid_constant__ CUtensorMap tmVup,  // V_up^T [df, FR] box 128x64
+          const __grid_constant__ CUtensorMap tmUdn,  // U_dn^T [FR, df] box 256x64
+          const __grid_constant__ CUtensorMap tmVdn,  // V_dn^T [d, FR]  box 256x64
+          const float* __restrict__ b_up, const float* __restrict__ b_dn, int act, int T,
+          int d_model, int d_ff, bf16* __restrict__ z_out, bf16* __restrict__ out) {
+  using C = FfnCfg<FR>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  FfnBars* bars = reinterpret_cast<FfnBars*>(smem + C::o_bar);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int m0 = blockIdx.x * BMr;
+  const int NB = (d_ff + BF - 1) / BF;
+  const int KC = d_model / 64;                  // X / V_dn K-chunks... (d_model % 64 == 0)
+  const int NQ = (d_model + 255) / 256;         // output pieces (FUSED)
+  const int QS = d_model / NQ;                  // columns per output piece
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmUup);
+    tma_prefetch(&tmVup);
+    tma_prefetch(&tmUdn);
+    tma_prefetch(&tmVdn);
+    if (FUSED) tma_prefetch(&tmX); else tma_prefetch(&tmP);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&bars->full[i], 1);
+      mbar_init(&bars->empty[i], 1);
+    }
+    mbar_init(&bars->p_full, 1);
+    mbar_init(&bars->p_acc, 1);
+    mbar_init(&bars->p_ready, kEpi);
+    mbar_init(&bars->h_full, 1);
+    mbar_init(&bars->h_free, kEpi);
+    mbar_init(&bars->sh_full, kEpi);
+    mbar_init(&bars->sh_free, 1);
+    mbar_init(&bars->z_full, 1);
+    mbar_init(&bars->zs_ready, kEpi);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->o_full[i], 1);
+      mbar_init(&bars->o_free[i], kEpi);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&bars->tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem;
+  uint8_t* ring = smem + C::o_ring;
+
+  if (warp == 0) {
+    // ================================================= TMA producer
+    uint32_t st = 0, ph = 0;
+    auto next = [&]() {
+      if (++st == C::STAGES) { st = 0; ph ^= 1; }
+    };
+    auto acquire = [&](uint32_t bytes) -> uint8_t* {
+      mbar_wait(&bars->empty[st], ph ^ 1);
+      if (lane == 0) mbar_arrive_expect_tx(&bars->full[st], bytes);
+      return ring + st * STAGE;
+    };
+    auto load_mma1 = [&](int f) {
+      for (int a = 0; a < C::NATOM; a += 2) {
+        const int na = (a + 1 < C::NATOM) ? 2 : 1;
+        uint8_t* s = acquire(na * ATOM);
+        if (lane == 0)
+          for (int i = 0; i < na; ++i)
+            tma_load_2d(&tmVup, &bars->full[st], s + i * ATOM, (a + i) * 64, f * BF);
+        __syncwarp();
+        next();
+      }
+    };
+    auto load_mma2 = [&](int f) {
+      for (int p = 0; p < C::NPIECE; ++p) {
+        constexpr int np = C::PS;
+        for (int a2 = 0; a2 < 2; ++a2) {
+          uint8_t* s = acquire(np * 128);
+          if (lane == 0) tma_load_2d(&tmUdn, &bars->full[st], s, f * BF + a2 * 64, p * C::PS);
+          __syncwarp();
+          next();
+        }
+      }
+    };
+    if (FUSED) {
+      for (int kc = 0; kc < KC; ++kc) {
+        uint8_t* s = acquire(ATOM);
+        if (lane == 0) tma_load_2d(&tmX, &bars->full[st], s, kc * 64, m0);
+        __syncwarp();
+        next();
+        for (int p = 0; p < C::NPIECE; ++p) {
+          constexpr int np = C::PS;
+          uint8_t* s2 = acquire(np * 128);
+          if (lane == 0) tma_load_2d(&tmUup, &bars->full[st], s2, kc * 64, p * C::PS);
+          __syncwarp();
+          next();
+        }
+      }
+    } else {
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&bars->p_full, C::NATOM * ATOM);
+        for (int a = 0; a < C::NATOM; ++a)
+          tma_load_2d(&tmP, &bars->p_full, smem + C::o_p + a * ATOM, a * 64, m0);
+      }
+      __syncwarp();
+    }
+    load_mma1(0);
+    for (int f = 0; f < NB; ++f) {
+      if (f + 1 < NB) load_mma1(f + 1);
+      load_mma2(f);
+    }
+    if (FUSED) {
+      for (int q = 0; q < NQ; ++q) {
+        const int nq = QS;
+        for (int a = 0; a < C::NATOM; ++a) {
+          uint8_t* s = acquire(nq * 128);
+          if (lane == 0) tma_load_2d(&tmVdn, &bars->full[st], s, a * 64, q * QS);
+          __syncwarp();
+          next();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================= MMA issuer
+    uint32_t st = 0, ph = 0;
+    const uint32_t s_p = smem_u32(smem + C::o_p), s_h = smem_u32(smem + C::o_h);
+    const uint32_t s_ring = smem_u32(ring);
+    auto wait_full = [&]() -> uint32_t {
+      mbar_wait(&bars->full[st], ph);
+      tc_fence_after();
+      return s_ring + st * STAGE;
+    };
+    auto release = [&](uint32_t stage_idx) {
+      if (lane == 0) mma_commit(&bars->empty[stage_idx]);
+      __syncwarp();
+    };
+    auto next = [&]() {
+      if (++st == C::STAGES) { st = 0; ph ^= 1; }
+    };
+    if (FUSED) {
+      // P = X U_up into the Z columns of TMEM
+      for (int kc = 0; kc < KC; ++kc) {
+        const uint32_t xs = wait_full();
+        const uint32_t xst = st;
+        next();
+        for (int p = 0; p < C::NPIECE; ++p) {
+          constexpr int np = C::PS;
+          const uint32_t bs = wait_full();
+          if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16_ss(tmem + C::t_z + p * C::PS, desc_kmajor(xs + k * 32, 128),
+                          desc_kmajor(bs + k * 32, 128), idesc_bf16(128, np), (kc | k) != 0);
+          }
+          __syncwarp();
+          release(st);
+          next();
+        }
+        release(xst);
+      }
+      if (lane == 0) mma_commit(&bars->p_acc);
+      __syncwarp();
+      mbar_wait(&bars->p_ready, 0);
+    } else {
+      mbar_wait(&bars->p_full, 0);
+    }
+    tc_fence_after();
+    auto mma1 = [&](int f) {
+      if (f > 0) {
+        mbar_wait(&bars->h_free, (f - 1) & 1);
+        tc_fence_after();
+      }
+      for (int a = 0; a < C::NATOM; a += 2) {
+        const int na = (a + 1 < C::NATOM) ? 2 : 1;
+        const uint32_t bs = wait_full();
+        if (lane == 0) {
+          for (int i = 0; i < na; ++i)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16_ss(tmem + C::t_h, desc_kmajor(s_p + (a + i) * ATOM + k * 32, 128),
+                          desc_kmajor(bs + i * ATOM + k * 32, 128), idesc_bf16(128, BF),
+                          (a + i) != 0 || k != 0);
+        }
+        __syncwarp();
+        release(st);
+        next();
+      }
+      if (lane == 0) mma_commit(&bars->h_full);
+      __syncwarp();
+    };
+    auto mma2 = [&](int f) {
+      mbar_wait(&bars->sh_full, f & 1);
+      tc_fence_after();
+      for (int p = 0; p < C::NPIECE; ++p) {
+        constexpr int np = C::PS;
+        for (int a2 = 0; a2 < 2; ++a2) {
+          const uint32_t bs = wait_full();
+          if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16_ss(tmem + C::t_z + p * C::PS, desc_kmajor(s_h + a2 * ATOM + k * 32, 128),
+                          desc_kmajor(bs + k * 32, 128), idesc_bf16(128, np),
+                          (f | a2 | k) != 0);
+          }
+          __syncwarp();
+          release(st);
+          next();
+        }
+      }
+      if (lane == 0) mma_commit(&bars->sh_free);
+      __syncwarp();
+    };
+    mma1(0);
+    for (int f = 0; f < NB; ++f) {
+      if (f + 1 < NB) mma1(f + 1);
+      mma2(f);
+    }
+    if (lane == 0) mma_commit(&bars->z_full);
+    __syncwarp();
+    if (FUSED) {
+      mbar_wait(&bars->zs_ready, 0);
+      tc_fence_after();
+      for (int q = 0; q < NQ; ++q) {
+        const int nq = QS;
+        if (q >= 2) {
+          mbar_wait(&bars->o_free[q & 1], ((q >> 1) - 1) & 1);
+          tc_fence_after();
+        }
+        for (int a = 0; a < C::NATOM; ++a) {
+          const uint32_t bs = wait_full();
+          if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16_ss(tmem + (q & 1) * 256, desc_kmajor(s_p + a * ATOM + k * 32, 128),
+                          desc_kmajor(bs + k * 32, 128), idesc_bf16(128, nq), (a | k) != 0);
+          }
+          __syncwarp();
+          release(st);
+          next();
+        }
+        if (lane == 0) mma_commit(&bars->o_full[q & 1]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ================================================= epilogue (8 warps)
+    const uint32_t quad = warp & 3;
+    const uint32_t half = (warp - 2) >> 2;
+    const uint32_t row = quad * 32 + lane;
+    const uint32_t loff = (quad * 32) << 16;
+    const int grow = m0 + static_cast<int>(row);
+    const uint32_t s_p = smem_u32(smem + C::o_p), s_h = smem_u32(smem + C::o_h);
+    if (FUSED) {
+      mbar_wait(&bars->p_acc, 0);
+      tc_fence_after();
+      for (int c = half; c < FR / 32; c += 2) {
+        float v[32];
+        ld_chunk(tmem + C::t_z + loff + c * 32, v);
+        st_chunk_smem(s_p, row, c * 32, v);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bars->p_ready);
+    }
+    for (int f = 0; f < NB; ++f) {
+      mbar_wait(&bars->h_full, f & 1);
+      tc_fence_after();
+      float v[2][32];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) ld_chunk(tmem + C::t_h + loff + (half + 2 * i) * 32, v[i]);
+      tc_fence_before();
+      mbar_arrive(&bars->h_free);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int fb = f * BF + (half + 2 * i) * 32;
+        bias_act_chunk<32>(v[i], b_up + fb, d_ff - fb, act);
+      }
+      if (f > 0) mbar_wait(&bars->sh_free, (f - 1) & 1);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) st_chunk_smem(s_h, row, (half + 2 * i) * 32, v[i]);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bars->sh_full);
+    }
+    mbar_wait(&bars->z_full, 0);
+    tc_fence_after();
+    if (!FUSED) {
+      for (int c = half; c < FR / 32; c += 2) {
+        float v[32];
+        ld_chunk(tmem + C::t_z + loff + c * 32, v);
+        if (grow < T) st_chunk_global(z_out + (int64_t)grow * FR + c * 32, v);
+      }
+    } else {
+      for (int c = half; c < FR / 32; c += 2) {
+        float v[32];
+        ld_chunk(tmem + C::t_z + loff + c * 32, v);
+        st_chunk_smem(s_p, row, c * 32, v);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bars->zs_ready);
+      for (int q = 0; q < NQ; ++q) {
+        const int nq = QS;
+        mbar_wait(&bars->o_full[q & 1], (q >> 1) & 1);
+        tc_fence_after();
+        for (int c = half; c < nq / 32; c += 2) {
+          float v[32];
+          ld_chunk(tmem + (q & 1) * 256 + loff + c * 32, v);
+          const int n0 = q * QS + c * 32;
+          bias_act_chunk<32>(v, b_dn + n0, 32, 3);
+          if (grow < T) st_chunk_global(out + (int64_t)grow * d_model + n0, v);
+        }
+        tc_fence_before();
+        mbar_arrive(&bars->o_free[q & 1]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+template <int FR, bool FUSED>
+void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
+  using C = FfnCfg<FR>;
+  static bool attr = false;
+  if (!attr) {
+    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_ffn<FR, FUSED>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  const int boxp = C::PS;
+  const int boxd = a.d_model / ((a.d_model + 255) / 256);
+  const CUtensorMap tup = tmap_bf16(a.up_u_t, FR, a.d_model, a.d_model, boxp, 64, TmaSwizzle::B128);
+  const CUtensorMap tvup = tmap_bf16(a.up_v_t, a.d_ff, FR, FR, BF, 64, TmaSwizzle::B128);
+  const CUtensorMap tudn = tmap_bf16(a.dn_u_t, FR, a.d_ff, a.d_ff, boxp, 64, TmaSwizzle::B128);
+  const CUtensorMap tvdn = tmap_bf16(a.dn_v_t, a.d_model, FR, FR, boxd, 64, TmaSwizzle::B128);
+  CUtensorMap tx = tvup, tp = tvup;
+  if (FUSED)
+    tx = tmap_bf16(a.x, a.T, a.d_model, a.d_model, 128, 64, TmaSwizzle::B128);
+  else
+    tp = tmap_bf16(a.p_in, a.T, FR, FR, 128, 64, TmaSwizzle::B128);
+  const int grid = (a.T + BMr - 1) / BMr;
+  k_ffn<FR, FUSED><<<grid, kThreads, C::SMEM, s>>>(tx, tp, tup, tvup, tudn, tvdn, a.up_b, a.dn_b,
+                                                   a.act, a.T, a.d_model, a.d_ff, a.z_out, a.out);
+  check_launch(FUSED ? "k_ffn_fused" : "k_ffn_stream");
+}
+
+template <bool FUSED>
+void dispatch_ffn(const FfnTcArgs& a, cudaStream_t s) {
+  switch (a.rank_pad) {
+    case 64: launch_ffn<64, FUSED>(a, s); break;
+    case 128: launch_ffn<128, FUSED>(a, s); break;
+    case 192: launch_ffn<192, FUSED>(a, s); break;
+    case 256: launch_ffn<256, FUSED>(a, s); break;
+    case 320: launch_ffn<320, FUSED>(a, s); break;
+    case 384: launch_ffn<384, FUSED>(a, s); break;
+    default: throw CudaError("ffn: unsupported FFN rank padding");
+  }
+}
+
+}  // namespace
+
+bool ffn_tc_supported(int d_model, int d_ff, int rank_pad) {
+  const int nq = (d_model + 255) / 256;
+  return d_model % 64 == 0 && d_model % nq == 0 && (d_model / nq) % 32 == 0 && d_ff % 8 == 0 &&
+         rank_pad % 64 == 0 && rank_pad <= 384 && rank_pad >= 64;
+}
+
+void ffn_stream_bf16(const FfnTcArgs& a, cudaStream_t s) { dispatch_ffn<false>(a, s); }
+void ffn_fused_bf16(const FfnTcArgs& a, cudaStream_t s) { dispatch_ffn<true>(a, s); }
+
+}  // namespace fsvd

@@ -1,0 +1,221 @@
+// gemm_tc.cu -- K1: persistent tcgen05 GEMM with fused bias/activation epilogue.
+//
+// C[M,N] = A[M,K] * B[N,K]^T (+ bias[N]) (act), bf16 in/out, fp32 accumulate
+// in TMEM.  This is the B200 replacement of the reference's strided fp32
+// projection loop gemm_acc_ld (attention.cpp:19-31, ffn.cpp:26-38) wherever
+// it is used as a whole-matrix product: X*U (attention.cpp:239-247,
+// ffn.cpp:131-134), ctx*U_o / P*V_o + b_o (attention.cpp:381-389) and
+// Z*V_down + b_down (ffn.cpp:148-154).  Bias is applied in the epilogue,
+// which equals the reference's bias preload up to fp32 rounding order.
+//
+// Structure (one CTA per SM, persistent over 128 x BN output tiles):
+//   warp 0      TMA producer: A [128 x 64] and B [BN x 64] bf16 tiles (SW128)
+//               into a STAGES-deep smem ring guarded by full/empty mbarriers.
+//   warp 1      MMA issuer: one elected lane issues tcgen05.mma (M=128,
+//               N=BN, K=16) into one of two TMEM accumulators.
+//   warps 2..5  epilogue: tcgen05.ld 32 columns at a time, bias + act,
+//               bf16 pack, swizzled st.shared, TMA store (per warp 32x32 box).
+// The double-buffered TMEM accumulator lets tile i's epilogue overlap tile
+// i+1's MMAs.
+#include "common.cuh"
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace fsvd {
+namespace {
+
+using namespace ptx;
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;
+
+template <int BN, int STAGES>
+struct GemmCfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int C_BYTES = 4 * 2 * 32 * 32 * 2;  // 4 warps x 2 buffers x 32x32 bf16
+  static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + C_BYTES + 256;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, const float* __restrict__ bias, int act,
+                int M, int N, int K) {
+  using Cfg = GemmCfg<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + STAGES * Cfg::A_BYTES;
+  uint8_t* sC = sB + STAGES * Cfg::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + Cfg::C_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n;
+  const int nk = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    tma_prefetch(&tmC);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    uint32_t stage = 0, phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+          tma_load_2d(&tmA, &full[stage], sA + stage * Cfg::A_BYTES, kb * BK, m0);
+          tma_load_2d(&tmB, &full[stage], sB + stage * Cfg::B_BYTES, kb * BK, n0);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = idesc_bf16(BM, BN);
+    uint32_t stage = 0, phase = 0;
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const uint32_t acc = i & 1, use = i >> 1;
+      mbar_wait(&tempty[acc], (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem + acc * BN;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16_ss(d, desc_kmajor(a0 + k * 32, 128), desc_kmajor(b0 + k * 32, 128), idesc,
+                        (kb | k) != 0);
+          mma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) mma_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else {
+    // ---------------- epilogue ----------------
+    const uint32_t q = warp & 3;  // TMEM lane quadrant of this warp
+    uint8_t* cbuf = sC + (warp - 2) * 2 * 2048;
+    uint32_t nstore = 0;
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+      const uint32_t acc = i & 1, use = i >> 1;
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem + acc * BN + ((q * 32) << 16);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        if (n0 + c0 >= N) break;
+        uint32_t r[32];
+        tmem_ld32(tbase + c0, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        bias_act_chunk<32>(v, bias != nullptr ? bias + n0 + c0 : nullptr, N - (n0 + c0), act);
+        uint8_t* buf = cbuf + (nstore & 1) * 2048;
+        if (lane == 0) tma_store_wait_read<1>();
+        __syncwarp();
+        const uint32_t sb = smem_u32(buf);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          st_shared_v4(sb + swz_offset(lane, c, 64), pack_bf16(v[8 * c + 0], v[8 * c + 1]),
+                       pack_bf16(v[8 * c + 2], v[8 * c + 3]),
+                       pack_bf16(v[8 * c + 4], v[8 * c + 5]),
+                       pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmC, buf, n0 + c0, m0 + q * 32);
+          tma_store_commit();
+        }
+        ++nstore;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+    if (lane == 0) tma_store_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free<Cfg::TMEM_COLS>(tmem);
+  }
+}
+
+template <int BN, int STAGES>
+void launch_gemm(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, int64_t ldc,
+                 int M, int N, int K, const float* bias, int act, cudaStream_t s) {
+  using Cfg = GemmCfg<BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_bf16<BN, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    attr = true;
+  }
+  const CUtensorMap ta = tmap_bf16(A, M, K, lda, BM, BK, TmaSwizzle::B128);
+  const CUtensorMap tb = tmap_bf16(B, N, K, ldb, BN, BK, TmaSwizzle::B128);
+  const CUtensorMap tc = tmap_bf16(C, M, N, ldc, 32, 32, TmaSwizzle::B64);
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  k_gemm_bf16<BN, STAGES><<<grid, kThreads, Cfg::SMEM, s>>>(ta, tb, tc, bias, act, M, N, K);
+  check_launch("k_gemm_bf16");
+}
+
+}  // namespace
+
+bool gemm_bf16_supported(int M, int N, int K, int64_t lda, int64_t ldb, int64_t ldc) {
+  // TMA needs 16-byte aligned row pitches; tiles cover any M, N, K tails.
+  return M > 0 && N > 0 && K > 0 && lda % 8 == 0 && ldb % 8 == 0 && ldc % 8 == 0 && K % 8 == 0;
+}
+
+void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, int64_t ldc,
+               int M, int N, int K, const float* bias, int act, cudaStream_t s) {
+  if (N % 256 == 0 || N > 1024)
+    launch_gemm<256, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+  else if (N % 192 == 0)
+    launch_gemm<192, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+  else if (N % 128 == 0 || N > 64)
+    launch_gemm<128, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+  else
+    launch_gemm<64, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+}
+
+}  // namespace fsvd

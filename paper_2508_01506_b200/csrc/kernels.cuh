@@ -1,0 +1,112 @@
+// kernels.cuh -- host launchers of every device kernel in the library.
+//
+// Tensor-core kernels (bf16 storage, fp32 accumulate, tcgen05 + TMA):
+//   K1 gemm_bf16          low-rank projection GEMMs with fused epilogues
+//   K2 attn_rankspace     FlashSVD attention (rank-space online softmax)
+//   K3 ffn_stream         FlashSVD-FFN feature-block stream (V1 middle)
+//   K4 ffn_fused          FlashSVD-FFN V2, fully fused per 128-row tile
+//   K5 resid_layernorm    residual + LayerNorm row kernel
+// SIMT kernels (fp32 policy and shapes outside the tensor-core tiling):
+//   simt_gemm, simt_attention, simt_ffn_stream, resid_layernorm (fp32)
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fsvd {
+
+using bf16 = __nv_bfloat16;
+
+enum Act : int { ACT_GELU_ERF = 0, ACT_GELU_TANH = 1, ACT_RELU = 2, ACT_NONE = 3 };
+
+// ---- K1: C[M,N] = A[M,K] * B[N,K]^T (+ bias[N]) (act) (+ resid[M,N]) ---------
+// A, B, C, resid bf16 row-major with leading dims; bias fp32 or null.
+void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, int64_t ldc,
+               int M, int N, int K, const float* bias, int act, cudaStream_t s);
+bool gemm_bf16_supported(int M, int N, int K, int64_t lda, int64_t ldb, int64_t ldc);
+
+// ---- K2: rank-space FlashSVD attention --------------------------------------
+struct AttnTcArgs {
+  const bf16* P;       // [T, ldp] projected activations; columns (mat, group, rank_pad)
+  int64_t ldp;
+  int batch, seq, heads, groups, rank_pad, head_dim;
+  const bf16* vq_t;    // [H][dh][rp]   (V_q head slice, transposed)  -> Q = P_q Vq
+  const bf16* vk;      // [H][rp][dh]   (V_k head slice)              -> Qt = Q Vk^T
+  const bf16* vv_t;    // [H][dh][rp]   (V_v head slice, transposed)  -> O = Or Vv
+  const float* bq;     // [H][dh] (already multiplied by softmax scale * log2 e)
+  const float* bv;     // [H][dh]
+  float q_scale;       // 1/sqrt(dh) * log2(e)
+  bf16* ctx;           // [T, ldc]
+  int64_t ldc;
+};
+void attn_rankspace_bf16(const AttnTcArgs& a, cudaStream_t s);
+bool attn_rankspace_supported(int head_dim, int rank_pad);
+
+// ---- K3 / K4: FlashSVD-FFN -----------------------------------------------------
+struct FfnTcArgs {
+  int T, d_model, d_ff, rank_pad;
+  const bf16* x;       // [T, d_model]          (V2 input)
+  const bf16* up_u_t;  // [fr][d_model]          U_up^T
+  const bf16* up_v_t;  // [d_ff][fr]             V_up^T
+  const float* up_b;   // [d_ff]
+  const bf16* dn_u_t;  // [fr][d_ff]             U_down^T
+  const bf16* dn_v_t;  // [d_model][fr]          V_down^T
+  const float* dn_b;   // [d_model]
+  int act;
+  const bf16* p_in;    // [T, fr]   (V1: P = X U_up)
+  bf16* z_out;         // [T, fr]   (V1: Z)
+  bf16* out;           // [T, d_model] (V2)
+};
+void ffn_stream_bf16(const FfnTcArgs& a, cudaStream_t s);   // V1 middle: P -> Z
+void ffn_fused_bf16(const FfnTcArgs& a, cudaStream_t s);    // V2: X -> out
+bool ffn_tc_supported(int d_model, int d_ff, int rank_pad);
+
+// ---- K5: y = LN(a (+ b)) * gamma + beta, rows of width d ---------------------
+void resid_layernorm_bf16(const bf16* a, const bf16* b, const float* gamma, const float* beta,
+                          float eps, bf16* y, int rows, int d, cudaStream_t s);
+void resid_layernorm_f32(const float* a, const float* b, const float* gamma, const float* beta,
+                         float eps, float* y, int rows, int d, cudaStream_t s);
+void add_bf16(const bf16* a, const bf16* b, bf16* y, int64_t n, cudaStream_t s);
+void add_f32(const float* a, const float* b, float* y, int64_t n, cudaStream_t s);
+
+// ---- SIMT kernels (templated on storage T = float or bf16, fp32 accumulate) --
+// C[M,N] = A[M,K] * B[K,N] (+bias) (act), row-major with leading dims.
+template <typename T>
+void simt_gemm(const T* A, int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, int M,
+               int N, int K, const float* bias, int act, cudaStream_t s);
+
+struct AttnSimtArgs {
+  const void* P;     // [T][3][G][r] projected activations (row stride 3*G*r)
+  const void* v;     // [3][G][r][gd]
+  const float* bias; // [3][d]
+  int batch, seq, heads, groups, rank, d_model;
+  void* ctx;         // [T, d]
+};
+template <typename T>
+void simt_attention(const AttnSimtArgs& a, cudaStream_t s);
+
+struct FfnSimtArgs {
+  const void* p;     // [T, r]
+  const void* up_v;  // [r][d_ff]
+  const float* up_b; // [d_ff]
+  const void* dn_u;  // [d_ff][r]
+  void* z;           // [T, r]
+  int T, rank, d_ff, act;
+};
+template <typename T>
+void simt_ffn_stream(const FfnSimtArgs& a, cudaStream_t s);
+// ffn_v2 dataflow on CUDA cores: P and Z stay in shared memory (16-row tiles).
+template <typename T>
+void simt_ffn_fused(const T* x, const T* up_u, const T* up_v, const float* up_b, const T* dn_u,
+                    const T* dn_v, const float* dn_b, T* out, int Tn, int d, int rank, int d_ff,
+                    int act, cudaStream_t s);
+
+template <typename T>
+void convert_f32(const float* src, T* dst, int64_t n, cudaStream_t s);
+template <typename T>
+void to_f32(const T* src, float* dst, int64_t n, cudaStream_t s);
+
+uint64_t launch_count();
+
+}  // namespace fsvd

@@ -1,0 +1,532 @@
+// runtime.cu -- factor packs, activation buffer planner and the device
+// encoder schedule.
+//
+// Layer schedule (post-LN, encoder.cpp:241-247), bf16 tensor-core path:
+//   K1  P      = X Wqkv^T                      [T, 3*G*rp]   (attention.cpp:239-247)
+//   K2  ctx    = FlashSVD attention(P)         [T, d]        (attention.cpp:249-267)
+//   K1  Pout   = ctx Uo^T ; K1 branch = Pout Vo^T + b_o      (attention.cpp:381-389)
+//   K5  resid  = LN1(x + branch)                              (encoder.cpp:38-50)
+//   FFN V1: K1 P = resid Uup^T ; K3 Z = stream(P) ; K1 out = Z Vdn^T + b  (ffn.cpp:118-156)
+//   FFN V2: K4 out = fused(resid)                             (ffn.cpp:158-185)
+//   K5  y      = LN2(resid + ffn_out)
+// Buffers: two [T, d] scratch activations (ctx/branch/resid/ffn_out rotate
+// through them in place) plus one transient region sized by RANK, aliased by
+// every sublayer: max(3*G*rp, prp, 2*frp) elements per token.  The layer runs
+// in place (x may equal out), so a whole model needs no ping-pong pair.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <thread>
+
+#include "common.cuh"
+#include "runtime.hpp"
+
+namespace fsvd {
+
+uint16_t f32_to_bf16_bits(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+Pack::~Pack() {
+  if (mem) cudaFree(mem);
+}
+
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Builder {
+  std::vector<uint8_t> buf;
+  int es;
+  std::vector<std::pair<const void**, size_t>> fix;
+  std::vector<std::pair<const float**, size_t>> fixf;
+
+  size_t raw(const void* p, size_t bytes) {
+    const size_t off = align256(buf.size());
+    buf.resize(off + bytes);
+    if (bytes) std::memcpy(buf.data() + off, p, bytes);
+    return off;
+  }
+  void store(const void** dst, const std::vector<float>& v) {
+    size_t off;
+    if (es == 4) {
+      off = raw(v.data(), v.size() * 4);
+    } else {
+      std::vector<uint16_t> h(v.size());
+      for (size_t i = 0; i < v.size(); ++i) h[i] = f32_to_bf16_bits(v[i]);
+      off = raw(h.data(), h.size() * 2);
+    }
+    fix.push_back({dst, off});
+  }
+  void store_f32(const float** dst, const float* p, size_t n) { fixf.push_back({dst, raw(p, n * 4)}); }
+  void store_f32(const float** dst, const std::vector<float>& v) { store_f32(dst, v.data(), v.size()); }
+};
+
+int pad_to(int x, int m) { return (x + m - 1) / m * m; }
+
+// W^T[n][k] = sum_j U[k][j] V[j][n] (fp32 accumulate, j ascending) for the
+// dense twin (encoder.cpp:295-331 reconstructs W = U V the same way).
+std::vector<float> reconstruct_t(const float* u, const float* v, int K, int R, int N, int ldv,
+                                 int voff) {
+  std::vector<float> wt(static_cast<size_t>(N) * K);
+  auto work = [&](int n_begin, int n_end) {
+    for (int n = n_begin; n < n_end; ++n)
+      for (int k = 0; k < K; ++k) {
+        float acc = 0.0f;
+        for (int j = 0; j < R; ++j) acc += u[(size_t)k * R + j] * v[(size_t)j * ldv + voff + n];
+        wt[(size_t)n * K + k] = acc;
+      }
+  };
+  const int nt = 8;
+  std::vector<std::thread> ts;
+  for (int t = 0; t < nt; ++t) ts.emplace_back(work, N * t / nt, N * (t + 1) / nt);
+  for (auto& t : ts) t.join();
+  return wt;
+}
+
+}  // namespace
+
+Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
+  auto P = std::make_unique<Pack>();
+  Pack& p = *P;
+  p.dtype = dtype;
+  p.es = dtype == FSVD_BF16 ? 2 : 4;
+  p.d = static_cast<int>(q.d_model);
+  Builder b;
+  b.es = p.es;
+  const bool bf = dtype == FSVD_BF16;
+  const int d = p.d;
+
+  if (q.attn) {
+    const fsvd_attn_desc& a = *q.attn;
+    p.has_attn = true;
+    p.H = static_cast<int>(q.heads);
+    p.G = static_cast<int>(a.groups);
+    p.r = static_cast<int>(a.rank);
+    p.dh = d / p.H;
+    p.gd = d / p.G;
+    const int G = p.G, r = p.r, H = p.H, dh = p.dh, gd = p.gd, hpg = H / G;
+    p.rp = r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : 0;
+    p.attn_tc = bf && p.rp != 0 && attn_rankspace_supported(dh, p.rp) && d % 8 == 0;
+    if (p.attn_tc) {
+      const int rp = p.rp;
+      std::vector<float> w(static_cast<size_t>(3) * G * rp * d, 0.0f);
+      for (int m = 0; m < 3; ++m)
+        for (int g = 0; g < G; ++g)
+          for (int j = 0; j < r; ++j)
+            for (int k = 0; k < d; ++k)
+              w[((size_t)(m * G + g) * rp + j) * d + k] = a.u[((size_t)(m * G + g) * d + k) * r + j];
+      b.store(&p.wqkv_t, w);
+      std::vector<float> vq((size_t)H * dh * rp, 0.0f), vk((size_t)H * rp * dh, 0.0f),
+          vv((size_t)H * dh * rp, 0.0f);
+      for (int h = 0; h < H; ++h) {
+        const int g = h / hpg, hc = (h % hpg) * dh;
+        for (int j = 0; j < r; ++j)
+          for (int dd = 0; dd < dh; ++dd) {
+            vq[((size_t)h * dh + dd) * rp + j] = a.v[((size_t)(0 * G + g) * r + j) * gd + hc + dd];
+            vk[((size_t)h * rp + j) * dh + dd] = a.v[((size_t)(1 * G + g) * r + j) * gd + hc + dd];
+            vv[((size_t)h * dh + dd) * rp + j] = a.v[((size_t)(2 * G + g) * r + j) * gd + hc + dd];
+          }
+      }
+      b.store(&p.vq_t, vq);
+      b.store(&p.vk, vk);
+      b.store(&p.vv_t, vv);
+      b.store_f32(&p.bq, a.bias, d);
+      b.store_f32(&p.bv, a.bias + 2 * d, d);
+    } else {
+      std::vector<float> w((size_t)d * 3 * G * r);
+      for (int m = 0; m < 3; ++m)
+        for (int g = 0; g < G; ++g)
+          for (int k = 0; k < d; ++k)
+            for (int j = 0; j < r; ++j)
+              w[(size_t)k * 3 * G * r + (size_t)(m * G + g) * r + j] =
+                  a.u[((size_t)(m * G + g) * d + k) * r + j];
+      b.store(&p.wqkv, w);
+      b.store(&p.attn_v, std::vector<float>(a.v, a.v + (size_t)3 * G * r * gd));
+    }
+    b.store_f32(&p.attn_b, a.bias, 3 * (size_t)d);
+    if (q.dense && p.attn_tc) {
+      std::vector<float> wt((size_t)3 * d * d);
+      for (int m = 0; m < 3; ++m)
+        for (int g = 0; g < G; ++g) {
+          std::vector<float> part = reconstruct_t(a.u + (size_t)(m * G + g) * d * r,
+                                                  a.v + (size_t)(m * G + g) * r * gd, d, r, gd,
+                                                  gd, 0);
+          for (int c = 0; c < gd; ++c)
+            std::memcpy(&wt[((size_t)m * d + g * gd + c) * d], &part[(size_t)c * d], d * 4);
+        }
+      b.store(&p.dqkv_t, wt);
+      b.store_f32(&p.dqkv_b, a.bias, 3 * (size_t)d);
+      const int rp = p.rp;
+      std::vector<float> bd((size_t)3 * d * 3 * G * rp, 0.0f);
+      for (int m = 0; m < 3; ++m)
+        for (int g = 0; g < G; ++g)
+          for (int c = 0; c < gd; ++c)
+            for (int j = 0; j < r; ++j)
+              bd[((size_t)m * d + g * gd + c) * (3 * G * rp) + (m * G + g) * rp + j] =
+                  a.v[((size_t)(m * G + g) * r + j) * gd + c];
+      b.store(&p.dvbd_t, bd);
+      std::vector<float> id((size_t)H * 64 * 64, 0.0f);
+      for (int h = 0; h < H; ++h)
+        for (int i = 0; i < 64; ++i) id[((size_t)h * 64 + i) * 64 + i] = 1.0f;
+      b.store(&p.ident, id);
+      b.store_f32(&p.zeros, std::vector<float>((size_t)H * 64, 0.0f));
+    }
+  }
+  if (q.out_proj) {
+    const fsvd_linear_desc& o = *q.out_proj;
+    p.has_out = true;
+    p.pr = static_cast<int>(o.rank);
+    p.prp = pad_to(p.pr, 16);
+    p.out_tc = bf && d % 8 == 0;
+    if (p.out_tc) {
+      const int pr = p.pr, prp = p.prp;
+      std::vector<float> ut((size_t)prp * d, 0.0f), vt((size_t)d * prp, 0.0f);
+      for (int k = 0; k < d; ++k)
+        for (int j = 0; j < pr; ++j) ut[(size_t)j * d + k] = o.u[(size_t)k * pr + j];
+      for (int j = 0; j < pr; ++j)
+        for (int n = 0; n < d; ++n) vt[(size_t)n * prp + j] = o.v[(size_t)j * d + n];
+      b.store(&p.uo_t, ut);
+      b.store(&p.vo_t, vt);
+      if (q.dense) b.store(&p.do_t, reconstruct_t(o.u, o.v, d, pr, d, d, 0));
+    } else {
+      b.store(&p.uo, std::vector<float>(o.u, o.u + (size_t)d * o.rank));
+      b.store(&p.vo, std::vector<float>(o.v, o.v + (size_t)o.rank * d));
+    }
+    b.store_f32(&p.bo, o.bias, d);
+  }
+  if (q.ffn) {
+    const fsvd_ffn_desc& f = *q.ffn;
+    p.has_ffn = true;
+    p.fr = static_cast<int>(f.up.rank);
+    p.df = static_cast<int>(f.up.out_dim);
+    p.act = static_cast<int>(f.activation);
+    p.frp = pad_to(p.fr, 64);
+    const int fr = p.fr, frp = p.frp, df = p.df;
+    p.ffn_tc = bf && d % 8 == 0 && df % 8 == 0 && ffn_tc_supported(d, df, frp);
+    if (p.ffn_tc) {
+      std::vector<float> uu((size_t)frp * d, 0.0f), vu((size_t)df * frp, 0.0f),
+          ud((size_t)frp * df, 0.0f), vd((size_t)d * frp, 0.0f);
+      for (int k = 0; k < d; ++k)
+        for (int j = 0; j < fr; ++j) uu[(size_t)j * d + k] = f.up.u[(size_t)k * fr + j];
+      for (int j = 0; j < fr; ++j)
+        for (int c = 0; c < df; ++c) vu[(size_t)c * frp + j] = f.up.v[(size_t)j * df + c];
+      for (int c = 0; c < df; ++c)
+        for (int j = 0; j < fr; ++j) ud[(size_t)j * df + c] = f.down.u[(size_t)c * fr + j];
+      for (int j = 0; j < fr; ++j)
+        for (int n = 0; n < d; ++n) vd[(size_t)n * frp + j] = f.down.v[(size_t)j * d + n];
+      b.store(&p.uup_t, uu);
+      b.store(&p.vup_t, vu);
+      b.store(&p.udn_t, ud);
+      b.store(&p.vdn_t, vd);
+      if (q.dense) {
+        b.store(&p.din_t, reconstruct_t(f.up.u, f.up.v, d, fr, df, df, 0));
+        b.store(&p.dout_t, reconstruct_t(f.down.u, f.down.v, df, fr, d, d, 0));
+      }
+    } else {
+      b.store(&p.uup, std::vector<float>(f.up.u, f.up.u + (size_t)d * fr));
+      b.store(&p.vup, std::vector<float>(f.up.v, f.up.v + (size_t)fr * df));
+      b.store(&p.udn, std::vector<float>(f.down.u, f.down.u + (size_t)df * fr));
+      b.store(&p.vdn, std::vector<float>(f.down.v, f.down.v + (size_t)fr * d));
+    }
+    b.store_f32(&p.bup, f.up.bias, df);
+    b.store_f32(&p.bdn, f.down.bias, d);
+  }
+  if (q.ln1g) {
+    p.has_ln = true;
+    b.store_f32(&p.ln1g, q.ln1g, d);
+    b.store_f32(&p.ln1b, q.ln1b, d);
+    b.store_f32(&p.ln2g, q.ln2g, d);
+    b.store_f32(&p.ln2b, q.ln2b, d);
+    p.eps1 = q.eps1;
+    p.eps2 = q.eps2;
+  }
+  p.dense = q.dense && p.attn_tc && p.out_tc && p.ffn_tc;
+  p.bytes = align256(b.buf.size());
+  if (p.bytes) {
+    FSVD_CUDA_CHECK(cudaMalloc(&p.mem, p.bytes));
+    FSVD_CUDA_CHECK(cudaMemcpy(p.mem, b.buf.data(), b.buf.size(), cudaMemcpyHostToDevice));
+  }
+  auto* base = static_cast<uint8_t*>(p.mem);
+  for (auto& f : b.fix) *f.first = base + f.second;
+  for (auto& f : b.fixf) *f.first = reinterpret_cast<const float*>(base + f.second);
+  return P.release();
+}
+
+// ---------------------------------------------------------------- validation
+void validate_layer(const fsvd_layer_desc& L) {
+  const size_t d = L.attn.d_model;
+  if (d == 0) fail(Kind::Shape, "layer norm parameters are empty");
+  if (!L.ln1_gamma || !L.ln1_beta || !L.ln2_gamma || !L.ln2_beta)
+    fail(Kind::Shape, "layer norm parameters are missing");
+  if (L.heads == 0 || d % L.heads != 0) fail(Kind::Config, "heads must divide d_model");
+  const fsvd_attn_desc& s = L.attn;
+  if (s.groups == 0 || d % s.groups != 0) fail(Kind::Config, "groups must divide d_model");
+  if (L.heads % s.groups != 0) fail(Kind::Config, "groups must divide heads");
+  if (s.rank == 0 || !s.u || !s.v || !s.bias) fail(Kind::Shape, "attention factor U: missing");
+  const fsvd_linear_desc& o = L.out_proj;
+  if (o.in_dim != d || !o.u) fail(Kind::Shape, "out_proj U: expected shape (d, r)");
+  if (o.out_dim != d || !o.v) fail(Kind::Shape, "out_proj V: expected shape (r, d)");
+  if (!o.bias) fail(Kind::Shape, "out_proj bias: expected a length-d vector");
+  const fsvd_ffn_desc& f = L.ffn;
+  if (f.up.rank != f.down.rank) fail(Kind::Config, "FFN up/down factor ranks differ");
+  if (f.up.in_dim != d || !f.up.u) fail(Kind::Shape, "ffn up U: expected shape (d, r)");
+  if (f.down.out_dim != d || !f.down.v) fail(Kind::Shape, "ffn down V: expected shape (r, d)");
+  if (f.up.out_dim != f.down.in_dim || f.up.out_dim == 0)
+    fail(Kind::Shape, "ffn up V / down U: d_ff mismatch");
+  if (!f.up.v || !f.up.bias || !f.down.u || !f.down.bias)
+    fail(Kind::Shape, "ffn factor arrays are missing");
+  if (f.up.rank == 0 || o.rank == 0) fail(Kind::Shape, "factor rank must be positive");
+  if (static_cast<int>(f.activation) < 0 || static_cast<int>(f.activation) > 3)
+    fail(Kind::Config, "unknown activation");
+}
+
+// ---------------------------------------------------------------- planner
+size_t op_transient_elems(const Pack& p, int op, int mode) {
+  const size_t d = p.d;
+  if (op == 0) {
+    if (mode == FSVD_MODE_DENSE) return 3 * d;
+    const size_t proj = p.attn_tc ? 3 * (size_t)p.G * p.rp : 3 * (size_t)p.G * p.r;
+    return mode == FSVD_MODE_NAIVE_LOWRANK ? proj + 3 * d : proj;
+  }
+  if (op == 1) {
+    if (mode == FSVD_MODE_DENSE) return 0;
+    return p.out_tc ? p.prp : p.pr;
+  }
+  const size_t fr = p.ffn_tc ? p.frp : p.fr;
+  switch (mode) {
+    case FSVD_MODE_DENSE: return p.df;
+    case FSVD_MODE_NAIVE_LOWRANK: return 2 * fr + p.df;
+    case FSVD_MODE_FLASH_V1: return 2 * fr;
+    default: return 0;
+  }
+}
+
+size_t layer_workspace_bytes(const Pack& p, size_t T, int mode) {
+  size_t tr = 0;
+  for (int op = 0; op < 3; ++op) tr = std::max(tr, op_transient_elems(p, op, mode));
+  return 2 * align256(T * p.d * p.es) + align256(T * tr * p.es) + 256;
+}
+
+// ---------------------------------------------------------------- schedule
+namespace {
+
+template <typename T>
+T* as(void* p) {
+  return static_cast<T*>(p);
+}
+template <typename T>
+const T* as(const void* p) {
+  return static_cast<const T*>(p);
+}
+
+void ln(const Pack& p, const void* a, const void* b, const float* g, const float* be, float eps,
+        void* y, int rows, cudaStream_t s) {
+  if (p.dtype == FSVD_BF16)
+    resid_layernorm_bf16(as<bf16>(a), as<bf16>(b), g, be, eps, as<bf16>(y), rows, p.d, s);
+  else
+    resid_layernorm_f32(as<float>(a), as<float>(b), g, be, eps, as<float>(y), rows, p.d, s);
+}
+void add(const Pack& p, const void* a, const void* b, void* y, int64_t n, cudaStream_t s) {
+  if (p.dtype == FSVD_BF16) add_bf16(as<bf16>(a), as<bf16>(b), as<bf16>(y), n, s);
+  else add_f32(as<float>(a), as<float>(b), as<float>(y), n, s);
+}
+
+template <typename T>
+void simt_attention_t(const Pack& p, size_t B, size_t M, const void* x, void* ctx, void* trans,
+                      cudaStream_t s) {
+  const int T_ = static_cast<int>(B * M), n = 3 * p.G * p.r;
+  simt_gemm<T>(as<T>(x), p.d, as<T>(p.wqkv), n, as<T>(trans), n, T_, n, p.d, nullptr, ACT_NONE, s);
+  AttnSimtArgs a{trans, p.attn_v, p.attn_b, (int)B, (int)M, p.H, p.G, p.r, p.d, ctx};
+  simt_attention<T>(a, s);
+}
+
+void tc_attention(const Pack& p, size_t B, size_t M, const bf16* P, int64_t ldp, int groups,
+                  int rp, const void* vq, const void* vk, const void* vv, const float* bq,
+                  const float* bv, void* ctx, cudaStream_t s) {
+  AttnTcArgs a;
+  a.P = P;
+  a.ldp = ldp;
+  a.batch = (int)B;
+  a.seq = (int)M;
+  a.heads = p.H;
+  a.groups = groups;
+  a.rank_pad = rp;
+  a.head_dim = p.dh;
+  a.vq_t = as<bf16>(vq);
+  a.vk = as<bf16>(vk);
+  a.vv_t = as<bf16>(vv);
+  a.bq = bq;
+  a.bv = bv;
+  a.q_scale = kLog2e / std::sqrt(static_cast<float>(p.dh));
+  a.ctx = as<bf16>(ctx);
+  a.ldc = p.d;
+  attn_rankspace_bf16(a, s);
+}
+
+}  // namespace
+
+void attention_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* ctx,
+                   void* trans, cudaStream_t s) {
+  const int T = static_cast<int>(B * M);
+  if (mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK) {
+    if (!p.dense) fail(Kind::Config, "dense / naive_lowrank modes need a pack built with dense=1 "
+                                     "on the bf16 tensor-core path");
+    const int d3 = 3 * p.d;
+    bf16* qkv = as<bf16>(trans);
+    if (mode == FSVD_MODE_DENSE) {
+      gemm_bf16(as<bf16>(x), p.d, as<bf16>(p.dqkv_t), p.d, qkv, d3, T, d3, p.d, p.dqkv_b, ACT_NONE, s);
+    } else {
+      const int n = 3 * p.G * p.rp;
+      bf16* P = qkv + (size_t)T * d3;
+      gemm_bf16(as<bf16>(x), p.d, as<bf16>(p.wqkv_t), p.d, P, n, T, n, p.d, nullptr, ACT_NONE, s);
+      gemm_bf16(P, n, as<bf16>(p.dvbd_t), n, qkv, d3, T, d3, n, p.attn_b, ACT_NONE, s);
+    }
+    tc_attention(p, B, M, qkv, d3, p.H, 64, p.ident, p.ident, p.ident, p.zeros, p.zeros, ctx, s);
+    return;
+  }
+  if (p.attn_tc) {
+    const int n = 3 * p.G * p.rp;
+    bf16* P = as<bf16>(trans);
+    gemm_bf16(as<bf16>(x), p.d, as<bf16>(p.wqkv_t), p.d, P, n, T, n, p.d, nullptr, ACT_NONE, s);
+    tc_attention(p, B, M, P, n, p.G, p.rp, p.vq_t, p.vk, p.vv_t, p.bq, p.bv, ctx, s);
+  } else if (p.dtype == FSVD_BF16) {
+    simt_attention_t<bf16>(p, B, M, x, ctx, trans, s);
+  } else {
+    simt_attention_t<float>(p, B, M, x, ctx, trans, s);
+  }
+}
+
+void outproj_fwd(const Pack& p, int mode, size_t B, size_t M, const void* ctx, void* out,
+                 void* trans, cudaStream_t s) {
+  const int T = static_cast<int>(B * M), d = p.d;
+  if (mode == FSVD_MODE_DENSE) {
+    gemm_bf16(as<bf16>(ctx), d, as<bf16>(p.do_t), d, as<bf16>(out), d, T, d, d, p.bo, ACT_NONE, s);
+    return;
+  }
+  if (p.out_tc) {
+    bf16* P = as<bf16>(trans);
+    gemm_bf16(as<bf16>(ctx), d, as<bf16>(p.uo_t), d, P, p.prp, T, p.prp, d, nullptr, ACT_NONE, s);
+    gemm_bf16(P, p.prp, as<bf16>(p.vo_t), p.prp, as<bf16>(out), d, T, d, p.prp, p.bo, ACT_NONE, s);
+  } else if (p.dtype == FSVD_BF16) {
+    simt_gemm<bf16>(as<bf16>(ctx), d, as<bf16>(p.uo), p.pr, as<bf16>(trans), p.pr, T, p.pr, d,
+                    nullptr, ACT_NONE, s);
+    simt_gemm<bf16>(as<bf16>(trans), p.pr, as<bf16>(p.vo), d, as<bf16>(out), d, T, d, p.pr, p.bo,
+                    ACT_NONE, s);
+  } else {
+    simt_gemm<float>(as<float>(ctx), d, as<float>(p.uo), p.pr, as<float>(trans), p.pr, T, p.pr, d,
+                     nullptr, ACT_NONE, s);
+    simt_gemm<float>(as<float>(trans), p.pr, as<float>(p.vo), d, as<float>(out), d, T, d, p.pr,
+                     p.bo, ACT_NONE, s);
+  }
+}
+
+namespace {
+template <typename T>
+void simt_ffn_t(const Pack& p, int mode, size_t Tn, const void* x, void* out, void* trans,
+                cudaStream_t s) {
+  const int n = static_cast<int>(Tn), d = p.d, fr = p.fr, df = p.df;
+  if (mode == FSVD_MODE_FLASH_V2) {
+    simt_ffn_fused<T>(as<T>(x), as<T>(p.uup), as<T>(p.vup), p.bup, as<T>(p.udn), as<T>(p.vdn),
+                      p.bdn, as<T>(out), n, d, fr, df, p.act, s);
+    return;
+  }
+  T* P = as<T>(trans);
+  T* Z = P + (size_t)n * fr;
+  simt_gemm<T>(as<T>(x), d, as<T>(p.uup), fr, P, fr, n, fr, d, nullptr, ACT_NONE, s);
+  FfnSimtArgs a{P, p.vup, p.bup, p.udn, Z, n, fr, df, p.act};
+  simt_ffn_stream<T>(a, s);
+  simt_gemm<T>(Z, fr, as<T>(p.vdn), d, as<T>(out), d, n, d, fr, p.bdn, ACT_NONE, s);
+}
+}  // namespace
+
+void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* out, void* trans,
+             cudaStream_t s) {
+  const int T = static_cast<int>(B * M), d = p.d, df = p.df;
+  if (mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK) {
+    if (!p.dense) fail(Kind::Config, "dense / naive_lowrank modes need a pack built with dense=1");
+    if (mode == FSVD_MODE_DENSE) {
+      bf16* hid = as<bf16>(trans);
+      gemm_bf16(as<bf16>(x), d, as<bf16>(p.din_t), d, hid, df, T, df, d, p.bup, p.act, s);
+      gemm_bf16(hid, df, as<bf16>(p.dout_t), df, as<bf16>(out), d, T, d, df, p.bdn, ACT_NONE, s);
+    } else {
+      const int frp = p.frp;
+      bf16* P = as<bf16>(trans);
+      bf16* hid = P + (size_t)T * frp;
+      bf16* Z = hid + (size_t)T * df;
+      gemm_bf16(as<bf16>(x), d, as<bf16>(p.uup_t), d, P, frp, T, frp, d, nullptr, ACT_NONE, s);
+      gemm_bf16(P, frp, as<bf16>(p.vup_t), frp, hid, df, T, df, frp, p.bup, p.act, s);
+      gemm_bf16(hid, df, as<bf16>(p.udn_t), df, Z, frp, T, frp, df, nullptr, ACT_NONE, s);
+      gemm_bf16(Z, frp, as<bf16>(p.vdn_t), frp, as<bf16>(out), d, T, d, frp, p.bdn, ACT_NONE, s);
+    }
+    return;
+  }
+  if (p.ffn_tc) {
+    FfnTcArgs a{};
+    a.T = T;
+    a.d_model = d;
+    a.d_ff = df;
+    a.rank_pad = p.frp;
+    a.x = as<bf16>(x);
+    a.up_u_t = as<bf16>(p.uup_t);
+    a.up_v_t = as<bf16>(p.vup_t);
+    a.up_b = p.bup;
+    a.dn_u_t = as<bf16>(p.udn_t);
+    a.dn_v_t = as<bf16>(p.vdn_t);
+    a.dn_b = p.bdn;
+    a.act = p.act;
+    a.out = as<bf16>(out);
+    if (mode == FSVD_MODE_FLASH_V2) {
+      ffn_fused_bf16(a, s);
+    } else {
+      bf16* P = as<bf16>(trans);
+      bf16* Z = P + (size_t)T * p.frp;
+      gemm_bf16(as<bf16>(x), d, a.up_u_t, d, P, p.frp, T, p.frp, d, nullptr, ACT_NONE, s);
+      a.p_in = P;
+      a.z_out = Z;
+      ffn_stream_bf16(a, s);
+      gemm_bf16(Z, p.frp, a.dn_v_t, p.frp, as<bf16>(out), d, T, d, p.frp, p.bdn, ACT_NONE, s);
+    }
+  } else if (p.dtype == FSVD_BF16) {
+    simt_ffn_t<bf16>(p, mode, (size_t)T, x, out, trans, s);
+  } else {
+    simt_ffn_t<float>(p, mode, (size_t)T, x, out, trans, s);
+  }
+}
+
+void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const void* x, void* out,
+               void* ws, size_t ws_bytes, cudaStream_t s) {
+  const size_t T = B * M;
+  if (ws_bytes < layer_workspace_bytes(p, T, mode))
+    fail(Kind::Config, "workspace too small: need " + std::to_string(layer_workspace_bytes(p, T, mode)) +
+                           " bytes, got " + std::to_string(ws_bytes));
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+  const size_t act_bytes = align256(T * p.d * p.es);
+  void* A = base;
+  void* Bb = base + act_bytes;
+  void* trans = base + 2 * act_bytes;
+  const int rows = static_cast<int>(T);
+  if (!pre_ln) {
+    attention_fwd(p, mode, B, M, x, A, trans, s);                     // ctx    -> A
+    outproj_fwd(p, mode, B, M, A, Bb, trans, s);                      // branch -> B
+    ln(p, x, Bb, p.ln1g, p.ln1b, p.eps1, Bb, rows, s);                // resid  -> B (in place)
+    ffn_fwd(p, mode, B, M, Bb, A, trans, s);                          // ffn    -> A
+    ln(p, Bb, A, p.ln2g, p.ln2b, p.eps2, out, rows, s);               // out
+  } else {
+    ln(p, x, nullptr, p.ln1g, p.ln1b, p.eps1, A, rows, s);            // normed -> A
+    attention_fwd(p, mode, B, M, A, Bb, trans, s);                    // ctx    -> B
+    outproj_fwd(p, mode, B, M, Bb, A, trans, s);                      // branch -> A
+    add(p, x, A, Bb, (int64_t)T * p.d, s);                            // resid  -> B
+    ln(p, Bb, nullptr, p.ln2g, p.ln2b, p.eps2, A, rows, s);           // normed -> A
+    ffn_fwd(p, mode, B, M, A, out, trans, s);                         // ffn    -> out
+    add(p, Bb, out, out, (int64_t)T * p.d, s);                        // out = resid + ffn
+  }
+}
+
+}  // namespace fsvd

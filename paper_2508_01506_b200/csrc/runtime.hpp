@@ -1,0 +1,96 @@
+// runtime.hpp -- device factor packs, the activation buffer planner and the
+// device-side encoder schedule (everything between the C ABI and kernels).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <vector>
+
+#include "../../include/fsvd_b200.h"
+#include "errors.hpp"
+#include "kernels.cuh"
+
+namespace fsvd {
+
+// One encoder layer resident in HBM, in the layouts its kernels consume.
+//   Tensor-core (bf16) layouts are K-major transposes padded with zeros:
+//     wqkv_t [3*G*rp][d]   vq_t/vv_t [H][dh][rp]   vk [H][rp][dh]
+//     uo_t [prp][d]  vo_t [d][prp]  uup_t [frp][d]  vup_t [df][frp]
+//     udn_t [frp][df]  vdn_t [d][frp]
+//   SIMT layouts are the reference orientation (x * W):
+//     wqkv [d][3*G*r]  attn_v [3][G][r][gd]  uo [d][pr]  vo [pr][d] ...
+struct Pack {
+  fsvd_dtype dtype = FSVD_BF16;
+  int es = 2;  // bytes per stored element
+  int d = 0, df = 0, H = 1, G = 1, r = 0, pr = 0, fr = 0, dh = 0, gd = 0, act = 0;
+  float eps1 = 1e-5f, eps2 = 1e-5f;
+  int rp = 0, prp = 0, frp = 0;
+  bool has_attn = false, has_out = false, has_ffn = false, has_ln = false, dense = false;
+  bool attn_tc = false, out_tc = false, ffn_tc = false;
+  void* mem = nullptr;
+  size_t bytes = 0;
+  // attention
+  const void *wqkv_t = nullptr, *vq_t = nullptr, *vk = nullptr, *vv_t = nullptr;
+  const float *bq = nullptr, *bv = nullptr;
+  const void *wqkv = nullptr, *attn_v = nullptr;
+  const float* attn_b = nullptr;
+  // output projection
+  const void *uo_t = nullptr, *vo_t = nullptr, *uo = nullptr, *vo = nullptr;
+  const float* bo = nullptr;
+  // FFN
+  const void *uup_t = nullptr, *vup_t = nullptr, *udn_t = nullptr, *vdn_t = nullptr;
+  const void *uup = nullptr, *vup = nullptr, *udn = nullptr, *vdn = nullptr;
+  const float *bup = nullptr, *bdn = nullptr;
+  // LayerNorms
+  const float *ln1g = nullptr, *ln1b = nullptr, *ln2g = nullptr, *ln2b = nullptr;
+  // dense twin / materializing baselines (tensor-core path only)
+  const void *dqkv_t = nullptr;   // [3d][d]   dense W_q|W_k|W_v transposed
+  const float* dqkv_b = nullptr;  // [3d]
+  const void *dvbd_t = nullptr;   // [3d][3*G*rp] block-diagonal V (naive low-rank)
+  const void *ident = nullptr;    // [H][64][64] identity factors
+  const float* zeros = nullptr;   // [H*64] zero biases
+  const void *do_t = nullptr, *din_t = nullptr, *dout_t = nullptr;  // [d][d] [df][d] [d][df]
+
+  ~Pack();
+};
+
+struct PackRequest {
+  const fsvd_attn_desc* attn = nullptr;
+  size_t heads = 0;
+  const fsvd_linear_desc* out_proj = nullptr;
+  const fsvd_ffn_desc* ffn = nullptr;
+  const float *ln1g = nullptr, *ln1b = nullptr, *ln2g = nullptr, *ln2b = nullptr;
+  float eps1 = 1e-5f, eps2 = 1e-5f;
+  size_t d_model = 0;
+  bool dense = false;
+};
+
+Pack* build_pack(const PackRequest& req, fsvd_dtype dtype);
+
+// encoder.cpp:156-222 for the flat descriptor (throws Error).
+void validate_layer(const fsvd_layer_desc& L);
+
+// Activation buffer planner: bytes of device workspace one layer needs for
+// T = batch*seq tokens in the given mode (two [T, d] scratch buffers + the
+// rank-sized transient region, aliased across sublayers).
+size_t layer_workspace_bytes(const Pack& p, size_t T, int mode);
+size_t op_transient_elems(const Pack& p, int op, int mode);  // op: 0 attn, 1 out, 2 ffn
+
+// Device schedule (async on `s`).  x and out may alias in layer_fwd.
+void attention_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* ctx,
+                   void* trans, cudaStream_t s);
+void outproj_fwd(const Pack& p, int mode, size_t B, size_t M, const void* ctx, void* out,
+                 void* trans, cudaStream_t s);
+void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* out, void* trans,
+             cudaStream_t s);
+void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const void* x, void* out,
+               void* ws, size_t ws_bytes, cudaStream_t s);
+
+uint16_t f32_to_bf16_bits(float f);
+
+}  // namespace fsvd
+
+struct fsvd_layer_pack {
+  fsvd::Pack* p;
+};
