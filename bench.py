@@ -1,0 +1,445 @@
+#!/usr/bin/env python3
+"""bench.py -- FlashSVD rank-aware streaming encoder on B200.
+
+Workload (BASELINE.json configs[1]): 12-layer BERT-Base low-rank encoder,
+per-GPU batch 32, seq 512, d=768, 12 heads, FFN 3072, per-head rank 32,
+out-proj / FFN rank 384, bf16, random-init factors (synthetic data).  A step
+is one full 12-layer forward of the batch through fsvd_model_fwd (the C-ABI
+device API).  --gpus N runs N independent batch shards (weak scaling, one
+process per GPU); the only collective is the NCCL gather of the outputs to
+rank 0, timed separately in the e2e leg.
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference CPU
+implementation (oracle/_ref, the unmodified reference library) instead.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/sec & peak activation MiB, BERT-Base rank-aware encoder, seq 512"
+UNIT = "tokens/s"
+D, DF, H, G, R, PR, FR, LAYERS = 768, 3072, 12, 12, 32, 384, 384, 12
+BATCH, SEQ = 32, 512
+MODE_NAMES = {2: "flash_v1", 3: "flash_v2", 0: "dense", 1: "naive_lowrank"}
+
+
+def algorithmic_flops_per_token_layer(d=D, df=DF, g=G, r=R, pr=PR, fr=FR, m=SEQ):
+    """F = 2d(3Gr) + 6r d + 4 M d + 4 d pr + 2 fr (2d + 2df)."""
+    return 2 * d * 3 * g * r + 6 * r * d + 4 * m * d + 4 * d * pr + 2 * fr * (2 * d + 2 * df)
+
+
+def ffn_flops_per_token(d=D, df=DF, fr=FR):
+    return 2 * fr * (2 * d + 2 * df)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-i", str(gpu_index), "-lms", "50"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        if not sm:
+            return None
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def load_ncu_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            s = json.load(f)
+        k = s["kernels"][kernel]
+        return k["dram_bytes_read"] + k["dram_bytes_write"]
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+    import oracle
+    from paper_2508_01506_b200 import abi
+    from paper_2508_01506_b200.model import random_layer
+
+    if not oracle.Reference.available():
+        try:
+            oracle.build(ref=True)
+        except Exception:
+            pass
+    if oracle.Reference.available():
+        chk, kind = oracle.Reference(), "reference"
+    else:
+        chk, kind = oracle.Restatement(), "port"
+    cores = os.cpu_count() or 1
+    os.environ["FLASHSVD_THREADS"] = str(cores)
+    rng = np.random.default_rng(0)
+    layer = random_layer(D, DF, H, G, R, PR, FR, rng)
+    sample_b = args.ref_batch
+    x = rng.standard_normal((sample_b, SEQ, D), np.float32)
+    plan = abi.TilePlan(16, 16, 32, 1 << 20)
+    mode = args.mode
+    for _ in range(min(args.warmup, 1)):
+        chk.run_model(x, [layer], mode, plan)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        chk.run_model(x, [layer], mode, plan)
+        times.append(time.perf_counter() - t0)
+    t_layer = sum(times) / len(times)
+    tok_s = sample_b * SEQ / (LAYERS * t_layer)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tok_s, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_layer * LAYERS * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"BERT-Base low-rank encoder, 12 layers, batch {BATCH}, seq {SEQ}, "
+                               f"r={R}, pr=fr={PR}, {MODE_NAMES[mode]}", "batch": BATCH, "seq_len": SEQ,
+                   "layers": LAYERS, "mode": MODE_NAMES[mode]},
+        "cpu_baseline": {"value": tok_s, "unit": UNIT, "cores": int(os.environ["FLASHSVD_THREADS"]),
+                         "kind": kind,
+                         "sample": f"1 layer x batch {sample_b} x seq {SEQ} per step "
+                                   f"(reference run_model, TilePlan{{16,16,32,1MiB}}), scaled x{LAYERS} layers"},
+        "e2e": {"value": tok_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_sample(mode):
+    """Reference CPU path on a bounded sample (rank 0, N=1 only)."""
+    import numpy as np
+    import oracle
+    from paper_2508_01506_b200 import abi
+    from paper_2508_01506_b200.model import random_layer
+    if oracle.Reference.available():
+        chk, kind = oracle.Reference(), "reference"
+    else:
+        chk, kind = oracle.Restatement(), "port"
+    cores = os.cpu_count() or 1
+    os.environ["FLASHSVD_THREADS"] = str(cores)
+    rng = np.random.default_rng(1)
+    layer = random_layer(D, DF, H, G, R, PR, FR, rng)
+    b = 2
+    x = rng.standard_normal((b, SEQ, D), np.float32)
+    plan = abi.TilePlan(16, 16, 32, 1 << 20)
+    chk.run_model(x, [layer], mode, plan)  # warm
+    reps, t = 0, 0.0
+    while t < 8.0 and reps < 8:
+        t0 = time.perf_counter()
+        chk.run_model(x, [layer], mode, plan)
+        t += time.perf_counter() - t0
+        reps += 1
+    t_layer = t / reps
+    return {"value": b * SEQ / (LAYERS * t_layer), "unit": UNIT, "cores": cores if kind == "reference" else 1,
+            "kind": kind,
+            "sample": f"{reps} x (1 layer, batch {b}, seq {SEQ}) of the same layer shape on the host "
+                      f"CPU, reference run_model {MODE_NAMES[mode]}; tokens/s scaled to {LAYERS} layers"}
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_01506_b200 import abi
+    from paper_2508_01506_b200.model import layer_descs, random_layer
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = abi.lib()
+    if not L.fsvd_device_available():
+        raise RuntimeError("no usable sm_100 device: " + L.fsvd_last_error().decode())
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    sp = C.c_void_p(stream.cuda_stream)
+    B, M = args.batch, args.seq
+    T = B * M
+    mode = args.mode
+
+    rng = np.random.default_rng(1234)  # identical weights on every rank
+    layers = [random_layer(D, DF, H, G, R, PR, FR, rng) for _ in range(args.layers)]
+    descs = layer_descs(layers)
+    packs = []
+    for i in range(args.layers):
+        p = C.c_void_p()
+        abi.check(L.fsvd_layer_pack_create(C.byref(descs[i]), abi.BF16, 0, C.byref(p)))
+        packs.append(p)
+    parr = (C.c_void_p * len(packs))(*[p.value for p in packs])
+    assert L.fsvd_layer_pack_uses_tensor_cores(packs[0]) == 1
+    wsb = C.c_size_t()
+    abi.check(L.fsvd_workspace_bytes(parr, len(packs), B, M, mode, C.byref(wsb)))
+    torch.cuda.reset_peak_memory_stats(dev)
+    base_alloc = torch.cuda.memory_allocated(dev)
+    work = torch.empty(wsb.value, dtype=torch.uint8, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(100 + rank)
+    x = torch.randn((B, M, D), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    out = torch.empty_like(x)
+    act_bytes = torch.cuda.max_memory_allocated(dev) - base_alloc
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def fwd(xin, xout):
+        abi.check(L.fsvd_model_fwd(parr, len(packs), mode, 0, B, M, C.c_void_p(xin.data_ptr()),
+                                   C.c_void_p(xout.data_ptr()), C.c_void_p(work.data_ptr()),
+                                   wsb.value, sp))
+
+    for _ in range(args.warmup):
+        fwd(x, out)
+    torch.cuda.synchronize(dev)
+    assert torch.isfinite(out.float()).all().item(), "non-finite output"
+
+    # ---------------- timed region (device-resident inputs) ----------------
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    clocks = Clocks(local)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    n0 = L.fsvd_kernel_launch_count()
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush between steps (outside the events)
+        evs[i][0].record(stream)
+        fwd(x, out)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    launches = L.fsvd_kernel_launch_count() - n0
+    if ws > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    ms_t = torch.tensor([ms], device=dev)
+    if ws > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = ws * T / (ms_max * 1e-3)
+
+    # ---------------- e2e: pinned host input -> model -> host output ----------------
+    xh = torch.empty((B, M, D), dtype=torch.bfloat16, pin_memory=True)
+    xh.copy_(x.cpu())
+    oh = torch.empty_like(xh, pin_memory=True)
+    xin = torch.empty_like(x)
+    e2e_steps = max(3, args.steps // 2)
+    for _ in range(2):
+        xin.copy_(xh, non_blocking=True)
+        fwd(xin, out)
+        oh.copy_(out, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        xin.copy_(xh, non_blocking=True)
+        fwd(xin, out)
+        oh.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    et = torch.tensor([e2e_ms], device=dev)
+    gather_ms = None
+    if ws > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        # output gather to rank 0 over NCCL (the path's only exchange step)
+        bufs = [torch.empty_like(out) for _ in range(ws)] if rank == 0 else None
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        dist.gather(out, bufs, dst=0)
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        gather_ms = g0.elapsed_time(g1)
+    e2e_value = ws * T / (float(et.item()) * 1e-3)
+
+    # ---------------- dominant-kernel roofline (FFN) ----------------
+    peaks, peak_src = load_peaks()
+    roof = None
+    if rank == 0:
+        ffn_variant = 2 if mode == abi.MODE_FLASH_V2 else 1
+        resid = torch.randn((B, M, D), device=dev, dtype=torch.float32).to(torch.bfloat16)
+        ffn_out = torch.empty_like(resid)
+        ffn_ws = C.c_size_t(wsb.value)
+        reps = 20
+        for _ in range(3):
+            abi.check(L.fsvd_ffn_fwd(packs[0], ffn_variant, B, M, C.c_void_p(resid.data_ptr()),
+                                     C.c_void_p(ffn_out.data_ptr()), C.c_void_p(work.data_ptr()),
+                                     ffn_ws, sp))
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        k0.record(stream)
+        for _ in range(reps):
+            abi.check(L.fsvd_ffn_fwd(packs[0], ffn_variant, B, M, C.c_void_p(resid.data_ptr()),
+                                     C.c_void_p(ffn_out.data_ptr()), C.c_void_p(work.data_ptr()),
+                                     ffn_ws, sp))
+        k1.record(stream)
+        torch.cuda.synchronize(dev)
+        k_ms = k0.elapsed_time(k1) / reps
+        flops = T * ffn_flops_per_token()
+        achieved = flops / (k_ms * 1e-3) / 1e12
+        peak = peaks.get("bf16_tflops", 1590.0)
+        kname = "k_ffn_fused" if ffn_variant == 2 else "k_ffn_stream+k_gemm_bf16"
+        traffic = load_ncu_traffic("k_ffn_fused" if ffn_variant == 2 else "k_ffn_stream")
+        roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": kname, "kernel_ms": round(k_ms, 4),
+                "algorithmic_flop_per_launch": flops,
+                "peak_source": f"{peak_src} burst bf16 (MEASURED_PEAKS.json) -- kernel timed alone",
+                "model_frac_of_sustained": round(
+                    T * LAYERS * algorithmic_flops_per_token_layer() / (ms_max * 1e-3) / 1e12
+                    / peaks.get("bf16_tflops_sustained", 1400.0), 4)}
+
+    # ---------------- peak activation memory ----------------
+    mem = {}
+    if rank == 0:
+        def ws_for(m, dense=False):
+            b = C.c_size_t()
+            if not dense:
+                abi.check(L.fsvd_workspace_bytes(parr, len(packs), B, M, m, C.byref(b)))
+                return b.value
+            return None
+        es = 2
+        io = 2 * T * D * es  # input + output activations
+        mem["flash_v1_mib"] = round((ws_for(abi.MODE_FLASH_V1) + io) / 2**20, 1)
+        mem["flash_v2_mib"] = round((ws_for(abi.MODE_FLASH_V2) + io) / 2**20, 1)
+        # dense-reconstruction baselines (planner bytes of our own dense / naive modes)
+        dense_tr = max(3 * D, DF) * T * es
+        naive_tr = max(3 * G * 32 + 3 * D, PR, 2 * FR + DF) * T * es
+        mem["dense_baseline_mib"] = round((2 * T * D * es + dense_tr + io) / 2**20, 1)
+        mem["naive_lowrank_baseline_mib"] = round((2 * T * D * es + naive_tr + io) / 2**20, 1)
+        mem["measured_torch_peak_mib"] = round(act_bytes / 2**20, 1)
+        sel = mem["flash_v2_mib"] if mode == abi.MODE_FLASH_V2 else mem["flash_v1_mib"]
+        mem["reduction_vs_dense"] = round(1 - sel / mem["dense_baseline_mib"], 4)
+        mem["reduction_vs_naive_lowrank"] = round(1 - sel / mem["naive_lowrank_baseline_mib"], 4)
+        mem["meter_transient_mib"] = {
+            "flash": round(4 * 3 * G * B * M * R / 2**20, 1),
+            "naive_lowrank": round(4 * max(3 * B * M * D, B * M * DF) / 2**20, 1),
+            "dense": round(4 * (3 * B * M * D + B * H * M * M) / 2**20, 1)}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_sample(mode)
+        except Exception as e:  # report, do not fail the bench
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": str(e)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init SVD factors, N(0,1) activations)",
+            "config": {"workload": f"BERT-Base low-rank encoder, {args.layers} layers, batch {B}/GPU, "
+                                   f"seq {M}, d={D}, H={H}, d_ff={DF}, r={R}, pr=fr={PR}, "
+                                   f"{MODE_NAMES[mode]}",
+                       "batch_per_gpu": B, "global_batch": B * ws, "seq_len": M, "layers": args.layers,
+                       "mode": MODE_NAMES[mode], "parallelism": f"batch-shard x{ws}",
+                       "l2": "flushed (256 MiB write) between timed steps"},
+            "e2e": {"value": round(e2e_value, 1), "unit": UNIT,
+                    "h2d_bytes_per_step": T * D * 2, "d2h_bytes_per_step": T * D * 2,
+                    "api": "fsvd_model_fwd (C-ABI) with pinned-host bf16 input/output copies"},
+            "gpu_launches": int(launches // max(args.steps, 1)) * args.steps,
+            "launches_per_step": int(launches // max(args.steps, 1)),
+            "roofline": roof,
+            "peak_activation_mib": mem,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        if gather_ms is not None:
+            line["gather_ms"] = round(gather_ms, 3)
+        print(json.dumps(line), flush=True)
+    for p in packs:
+        L.fsvd_layer_pack_destroy(p)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", type=int, default=3, help="2 = flash_v1, 3 = flash_v2")
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--seq", type=int, default=SEQ)
+    ap.add_argument("--layers", type=int, default=LAYERS)
+    ap.add_argument("--ref-batch", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

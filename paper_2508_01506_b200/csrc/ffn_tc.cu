@@ -356,6 +356,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&bars->p_ready);
     }
     for (int f = 0; f < NB; ++f) {
+      float bb[2][32];  // b_up of this block, fetched while the MMA runs
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int fb = f * BF + (half + 2 * i) * 32;
+        load_bias<32>(bb[i], b_up + fb, d_ff - fb);
+      }
       mbar_wait(&bars->h_full, f & 1);
       tc_fence_after();
       float v[2][32];
@@ -365,8 +371,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&bars->h_free);
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int fb = f * BF + (half + 2 * i) * 32;
-        bias_act_chunk<32>(v[i], b_up + fb, d_ff - fb, act);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[i][j] += bb[i][j];
+        act_chunk<32>(v[i], act);
       }
       if (f > 0) mbar_wait(&bars->sh_free, (f - 1) & 1);
 #pragma unroll

@@ -208,7 +208,11 @@ bool gemm_bf16_supported(int M, int N, int K, int64_t lda, int64_t ldb, int64_t 
 
 void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, int64_t ldc,
                int M, int N, int K, const float* bias, int act, cudaStream_t s) {
-  if (N % 256 == 0 || N > 1024)
+  if (N % 256 == 0)
+    launch_gemm<256, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+  else if (N % 192 == 0)
+    launch_gemm<192, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+  else if (N > 1024)
     launch_gemm<256, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
   else if (N % 192 == 0)
     launch_gemm<192, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);

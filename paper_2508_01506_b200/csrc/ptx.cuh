@@ -238,6 +238,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[31])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]),
+      "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]),
+      "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -271,12 +293,82 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   const float inner = c * (x + 0.044715f * x * x * x);
   return 0.5f * x * (1.0f + tanhf(inner));
 }
+// Tensor-core epilogue activations: one MUFU op each, error far below bf16
+// resolution.  GELU-erf uses Abramowitz-Stegun 7.1.28,
+//   erf(z) = 1 - (1 + a1 z + ... + a6 z^6)^-16, |err| <= 3e-7 (z >= 0);
+// GELU-tanh uses the hardware tanh.approx.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float gelu_erf_fast(float x) {
+  const float z = fabsf(x) * 0.70710678118654752440f;
+  float p = fmaf(z, 0.0000430638f, 0.0002765672f);
+  p = fmaf(z, p, 0.0001520143f);
+  p = fmaf(z, p, 0.0092705272f);
+  p = fmaf(z, p, 0.0422820123f);
+  p = fmaf(z, p, 0.0705230784f);
+  p = fmaf(z, p, 1.0f);
+  float r = rcp_approx(p);
+  r = r * r;
+  r = r * r;
+  r = r * r;
+  r = r * r;
+  const float e = copysignf(1.0f - r, x);
+  const float hx = 0.5f * x;
+  return fmaf(hx, e, hx);
+}
+__device__ __forceinline__ float gelu_tanh_fast(float x) {
+  const float inner = 0.79788456080286535588f * fmaf(0.044715f * x, x * x, x);
+  const float hx = 0.5f * x;
+  return fmaf(hx, tanh_approx(inner), hx);
+}
 __device__ __forceinline__ float apply_act(float v, int act) {
   switch (act) {
     case 0: return gelu_erf(v);
     case 1: return gelu_tanh(v);
     case 2: return v > 0.0f ? v : 0.0f;
     default: return v;
+  }
+}
+// Applies the activation to a register chunk (no bias).
+template <int N>
+__device__ __forceinline__ void act_chunk(float (&v)[N], int act) {
+  switch (act) {
+    case 0:
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = gelu_erf_fast(v[j]);
+      break;
+    case 1:
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = gelu_tanh_fast(v[j]);
+      break;
+    case 2:
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = fmaxf(v[j], 0.0f);
+      break;
+    default:
+      break;
+  }
+}
+// Loads bias[0..N) into registers (float4 when all N columns are in range).
+template <int N>
+__device__ __forceinline__ void load_bias(float (&b)[N], const float* bias, int valid) {
+  if (valid >= N) {
+#pragma unroll
+    for (int j = 0; j < N; j += 4) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(bias + j));
+      b[j] = t.x; b[j + 1] = t.y; b[j + 2] = t.z; b[j + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) b[j] = j < valid ? __ldg(bias + j) : 0.0f;
   }
 }
 // Adds bias[0..N) (float4 loads, bias 16-byte aligned; `valid` columns are in
@@ -301,11 +393,11 @@ __device__ __forceinline__ void bias_act_chunk(float (&v)[N], const float* bias,
   switch (act) {
     case 0:
 #pragma unroll
-      for (int j = 0; j < N; ++j) v[j] = gelu_erf(v[j]);
+      for (int j = 0; j < N; ++j) v[j] = gelu_erf_fast(v[j]);
       break;
     case 1:
 #pragma unroll
-      for (int j = 0; j < N; ++j) v[j] = gelu_tanh(v[j]);
+      for (int j = 0; j < N; ++j) v[j] = gelu_tanh_fast(v[j]);
       break;
     case 2:
 #pragma unroll

@@ -330,6 +330,84 @@ __global__ void k_resid_ln(const T* __restrict__ a, const T* __restrict__ b,
   }
 }
 
+// bf16 fast path: d % 8 == 0 and d <= 32 * 8 * V8; each lane owns V8 16-byte
+// chunks of the row.
+template <int V8>
+__global__ void __launch_bounds__(256) k_resid_ln_bf16x8(const bf16* __restrict__ a,
+                                                       const bf16* __restrict__ b,
+                                                       const float* __restrict__ gamma,
+                                                       const float* __restrict__ beta, float eps,
+                                                       bf16* __restrict__ y, int rows, int d) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const int64_t base = (int64_t)warp * d;
+  const int nch = d >> 3;
+  float v[V8][8];
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < V8; ++i) {
+    const int c = lane + 32 * i;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[i][k] = 0.0f;
+    if (c < nch) {
+      const uint4 av = __ldg(reinterpret_cast<const uint4*>(a + base) + c);
+      const __nv_bfloat162* ap = reinterpret_cast<const __nv_bfloat162*>(&av);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(ap[k]);
+        v[i][2 * k] = f.x;
+        v[i][2 * k + 1] = f.y;
+      }
+      if (b) {
+        const uint4 bv = __ldg(reinterpret_cast<const uint4*>(b + base) + c);
+        const __nv_bfloat162* bp = reinterpret_cast<const __nv_bfloat162*>(&bv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(bp[k]);
+          v[i][2 * k] += f.x;
+          v[i][2 * k + 1] += f.y;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += v[i][k];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float inv_d = 1.0f / static_cast<float>(d);
+  const float mean = s * inv_d;
+  float q = 0.0f;
+#pragma unroll
+  for (int i = 0; i < V8; ++i)
+    if (lane + 32 * i < nch)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float t = v[i][k] - mean;
+        q = fmaf(t, t, q);
+      }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float inv = rsqrtf(q * inv_d + eps);
+#pragma unroll
+  for (int i = 0; i < V8; ++i) {
+    const int c = lane + 32 * i;
+    if (c >= nch) continue;
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * c);
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * c + 1);
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta) + 2 * c);
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta) + 2 * c + 1);
+    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const float be[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      w[k] = ptx::pack_bf16(fmaf(g[2 * k], (v[i][2 * k] - mean) * inv, be[2 * k]),
+                            fmaf(g[2 * k + 1], (v[i][2 * k + 1] - mean) * inv, be[2 * k + 1]));
+    reinterpret_cast<uint4*>(y + base)[c] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 template <typename T>
 __global__ void k_add(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ y,
                       int64_t n) {
@@ -362,6 +440,16 @@ void launch_ln(const T* a, const T* b, const float* gamma, const float* beta, fl
                int rows, int d, cudaStream_t s) {
   const int threads = 256;
   const int grid = (rows * 32 + threads - 1) / threads;
+  if constexpr (sizeof(T) == 2) {
+    if (d % 8 == 0 && d <= 32 * 8 * 4) {
+      if (d <= 32 * 8 * 2)
+        k_resid_ln_bf16x8<2><<<grid, threads, 0, s>>>(a, b, gamma, beta, eps, y, rows, d);
+      else
+        k_resid_ln_bf16x8<4><<<grid, threads, 0, s>>>(a, b, gamma, beta, eps, y, rows, d);
+      check_launch("k_resid_ln_bf16x8");
+      return;
+    }
+  }
   if (d <= 32 * 8)
     k_resid_ln<T, 8><<<grid, threads, 0, s>>>(a, b, gamma, beta, eps, y, rows, d);
   else if (d <= 32 * 24)
