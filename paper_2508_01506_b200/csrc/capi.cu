@@ -219,6 +219,7 @@ void host_attention(const float* x, size_t B, size_t M, size_t W, const fsvd_att
   MeterBuffer pq(meter, "p_q", MeterClass::Transient, G * B * M * r);
   MeterBuffer pk(meter, "p_k", MeterClass::Transient, G * B * M * r);
   MeterBuffer pv(meter, "p_v", MeterClass::Transient, G * B * M * r);
+  require_device();
   auto pack = pack_attention(a, heads, dt);
   const size_t trans = B * M * op_transient_elems(*pack, 0, FSVD_MODE_FLASH_V1) * pack->es;
   run_on_device(x, B * M * d, out, B * M * d, dt, trans, *pack, meter,
@@ -242,6 +243,7 @@ void host_outproj(const float* ctx, size_t B, size_t M, size_t W, const fsvd_lin
   }
   MeterScope region(meter, "lowrank_output_projection");
   MeterBuffer p(meter, "p_out", MeterClass::Transient, B * M * r);
+  require_device();
   PackRequest q;
   q.out_proj = &o;
   q.d_model = d;
@@ -284,6 +286,7 @@ void host_ffn(int variant, const float* x, size_t B, size_t M, size_t W, const f
     pm = std::make_unique<MeterBuffer>(meter, "p_mid", MeterClass::Transient, B * M * r);
     zm = std::make_unique<MeterBuffer>(meter, "z_mid", MeterClass::Transient, B * M * r);
   }
+  require_device();
   PackRequest q;
   q.ffn = &f;
   q.d_model = d;
@@ -404,6 +407,7 @@ void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_lay
     }
   }
   // device
+  require_device();
   std::vector<std::unique_ptr<Pack>> packs;
   size_t ws = 0, pack_bytes = 0;
   for (size_t i = 0; i < n_layers; ++i) {

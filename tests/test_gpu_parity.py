@@ -1,0 +1,284 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle.
+
+Tolerances (north star): fp32 policy <= 1e-4 relative, bf16 <= 2e-2 relative
+against the oracle fed the SAME bf16-rounded inputs and factors.
+Error metric: max|got - ref| / max|ref|.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2508_01506_b200 import abi
+from paper_2508_01506_b200.model import bf16_round, layer_descs, round_layer_bf16
+
+import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+PLAN = abi.TilePlan(16, 16, 64, 1 << 22)
+
+
+@pytest.fixture(scope="module")
+def L():
+    lib = abi.lib()
+    if not lib.fsvd_device_available():
+        pytest.fail("GPU tests need an sm_100 device: " + lib.fsvd_last_error().decode())
+    return lib
+
+
+@pytest.fixture(scope="module")
+def ora():
+    return oracle.Restatement()
+
+
+def tol(dtype):
+    return H.TOL_F32 if dtype == abi.F32 else H.TOL_BF16
+
+
+def prep(layer, x, dtype):
+    if dtype == abi.BF16:
+        round_layer_bf16(layer)
+        x = bf16_round(x)
+    return layer, x
+
+
+# name, d, df, heads, groups, r, pr, fr, B, M
+SHAPES = [
+    ("tiny_odd", 48, 96, 4, 2, 5, 7, 9, 2, 33),          # SIMT path (dh=12)
+    ("head64_r32", 256, 512, 4, 4, 32, 64, 128, 2, 130),  # tensor-core path, ragged M
+    ("bert_base_cfg1", 768, 3072, 12, 12, 32, 384, 384, 1, 128),
+    ("grouped_r16", 512, 1024, 8, 2, 16, 96, 192, 2, 200),
+    ("r64_fr256", 512, 2048, 8, 8, 64, 256, 256, 1, 257),
+    ("r8_fr128", 256, 1024, 4, 4, 8, 32, 128, 3, 64),
+]
+DTYPES = [abi.F32, abi.BF16]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=[s[0] for s in SHAPES])
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16"])
+def test_sublayers_match_oracle(L, ora, shape, dtype):
+    _, d, df, heads, groups, r, pr, fr, B, M = shape
+    layer = oracle.rand_layer(ora, d, df, heads, groups, r, 1000 + d, pr, fr)
+    x = ora.random((B, M, d), 7)
+    layer, x = prep(layer, x, dtype)
+    t = tol(dtype)
+    ref = ora.attention(x, layer.attn, heads, PLAN)
+    assert H.rel_err(H.attention(x, layer.attn, heads, PLAN, dtype), ref) <= t
+    ctx = ref if dtype == abi.F32 else bf16_round(ref)
+    assert H.rel_err(H.outproj(ctx, layer.out_proj, dtype), ora.outproj(ctx, layer.out_proj)) <= t
+    for v in (1, 2):
+        assert H.rel_err(H.ffn(v, x, layer.ffn, PLAN, dtype), ora.ffn(v, x, layer.ffn, PLAN)) <= t
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=[s[0] for s in SHAPES])
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16"])
+@pytest.mark.parametrize("mode", [abi.MODE_FLASH_V1, abi.MODE_FLASH_V2], ids=["v1", "v2"])
+def test_layer_matches_oracle(L, ora, shape, dtype, mode):
+    _, d, df, heads, groups, r, pr, fr, B, M = shape
+    layer = oracle.rand_layer(ora, d, df, heads, groups, r, 2000 + d, pr, fr)
+    x = ora.random((B, M, d), 8)
+    layer, x = prep(layer, x, dtype)
+    for pre in (False, True):
+        ref = ora.run_model(x, [layer], mode, PLAN, pre_ln=pre)
+        got = H.run_layer(x, layer, mode, PLAN, dtype, pre_ln=pre)
+        assert H.rel_err(got, ref) <= tol(dtype), (pre, H.rel_err(got, ref))
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16"])
+def test_four_layer_model_matches_oracle(L, ora, dtype):
+    layers = [oracle.rand_layer(ora, 256, 1024, 4, 4, 32, 3000 + i * 1013, 64, 128) for i in range(4)]
+    x = ora.random((2, 96, 256), 9)
+    if dtype == abi.BF16:
+        for l_ in layers:
+            round_layer_bf16(l_)
+        x = bf16_round(x)
+    ref = ora.run_model(x, layers, abi.MODE_FLASH_V2, PLAN)
+    got = H.run_model(x, layers, abi.MODE_FLASH_V2, PLAN, dtype)
+    assert H.rel_err(got, ref) <= tol(dtype)
+
+
+def test_random_attention_configs_f32(L, ora, reference):
+    """acceptance.cpp:216-248 style: random (B, M, H, G, r) vs the reference's
+    dense_attention on reconstructed weights (kKernelTol 1e-4)."""
+    rng = np.random.default_rng(4242)
+    for t in range(12):
+        b = int(rng.integers(1, 4)); m = int(rng.integers(1, 140)); heads = int(rng.integers(1, 9))
+        gd = int(rng.choice([4, 8, 16, 32, 64]))
+        d = heads * gd
+        groups = int(rng.choice([g for g in range(1, heads + 1) if heads % g == 0]))
+        rank = int(rng.integers(1, min(64, d // groups) + 1))
+        a = oracle.rand_attn(reference, d, groups, rank, 100000 + t * 631)
+        x = reference.random((b, m, d), 50000 + t)
+        got = H.attention(x, a, heads, PLAN, abi.F32)
+        ref = reference.dense_attention_twin(x, a, heads)
+        assert np.abs(got - ref).max() <= 1e-4, t
+
+
+def test_random_ffn_configs_f32(L, reference):
+    rng = np.random.default_rng(77)
+    for t in range(12):
+        b = int(rng.integers(1, 4)); m = int(rng.integers(1, 70)); d = int(rng.integers(4, 65))
+        df = int(rng.integers(8, 129)); rank = int(rng.integers(1, min(d, df) + 1))
+        f = oracle.rand_ffn(reference, d, df, rank, 300000 + t * 97, t % 4)
+        x = reference.random((b, m, d), 70000 + t)
+        ref = reference.ffn(0, x, f, PLAN)  # ffn_dense on reconstructed weights
+        for v in (1, 2):
+            assert np.abs(H.ffn(v, x, f, PLAN, abi.F32) - ref).max() <= 1e-4, (t, v)
+
+
+def test_zero_weight_layer_is_double_layernorm(L, ora):
+    """test_encoder.cpp:175-203: all-zero factors and biases -> LN2(LN1(x))."""
+    layer = oracle.rand_layer(ora, 64, 128, 4, 4, 8, 5, 8, 64)
+    for a in layer.arrays()[:12]:
+        a[...] = 0
+    x = ora.random((2, 16, 64), 3)
+
+    def ln(v, g, b):
+        mu = v.mean(-1, keepdims=True)
+        var = ((v - mu) ** 2).mean(-1, keepdims=True)
+        return g * (v - mu) / np.sqrt(var + 1e-5) + b
+    want = ln(ln(x.astype(np.float64), layer.ln1_gamma, layer.ln1_beta), layer.ln2_gamma, layer.ln2_beta)
+    got = H.run_layer(x, layer, abi.MODE_FLASH_V1, PLAN, abi.F32)
+    assert np.abs(got - want).max() <= 1e-5
+
+
+def test_tile_plan_invariance_and_determinism(L, ora):
+    """acceptance criterion 5 + determinism (test_attention.cpp:326-334)."""
+    layer = oracle.rand_layer(ora, 256, 512, 4, 4, 32, 424242, 64, 128)
+    round_layer_bf16(layer)
+    x = bf16_round(ora.random((2, 64, 256), 777))
+    outs = [H.run_layer(x, layer, abi.MODE_FLASH_V2, abi.TilePlan(bm, br, bdf, 1 << 22), abi.BF16)
+            for bm in (8, 32) for br in (4, 16) for bdf in (16, 64)]
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+# ------------------------------------------------------------------ meter goldens via the host API
+def test_meter_bert_base_peaks(L, ora):
+    """acceptance.cpp:614-655 (criterion 10): BERT-Base B=8 M=128 r=64 peaks
+    flash 9,437,184 / naive 12,582,912 / dense 15,728,640; attention 10,027,008."""
+    layer = oracle.rand_layer(ora, 768, 3072, 12, 12, 64, 20260822, 64, 64)
+    round_layer_bf16(layer)
+    x = bf16_round(ora.random((8, 128, 768), 31337))
+    peaks = {}
+    for mode in (abi.MODE_FLASH_V1, abi.MODE_NAIVE_LOWRANK, abi.MODE_DENSE):
+        m = H.Meter()
+        H.run_model(x, [layer], mode, abi.TilePlan.default(), abi.BF16, meter=m)
+        assert L.fsvd_meter_assert_clean(m.h) == 0
+        peaks[mode] = m.peak
+    assert peaks[abi.MODE_FLASH_V1] == 9437184
+    assert peaks[abi.MODE_NAIVE_LOWRANK] == 12582912
+    assert peaks[abi.MODE_DENSE] == 15728640
+    m = H.Meter()
+    H.attention(x, layer.attn, 12, abi.TilePlan.default(), abi.BF16, meter=m)
+    assert m.peak + m.persistent == 10027008
+
+
+def test_meter_small_layer_golden(L, ora):
+    """test_encoder.cpp:239-280: FlashV1 layer d=32 df=64 H=4 G=2 r=8 B=2 M=16 ->
+    peak 6,144 B, persistent 11,264 B; meter event log matches the reference's."""
+    layer = oracle.rand_layer(ora, 32, 64, 4, 2, 8, 11)
+    x = ora.random((2, 16, 32), 12)
+    m = H.Meter()
+    H.run_layer(x, layer, abi.MODE_FLASH_V1, abi.TilePlan.default(), abi.F32, meter=m)
+    assert m.peak == 6144 and m.persistent == 11264
+    tags = [e[2] for e in m.events()]
+    assert tags[:3] == ["layer.attn_ctx", "layer.sublayer_out", "layer.resid"]
+    assert "layer.attn.q.g0.v" in tags and "layer.ffn.down.v" in tags and "p_q" in tags
+
+
+def test_meter_ffn_v1_golden(L, ora):
+    """test_ffn.cpp:71-87: FFN V1 (B=2, M=64, d=64, df=256, r=32) peak 32,768."""
+    f = oracle.rand_ffn(ora, 64, 256, 32, 3)
+    x = ora.random((2, 64, 64), 4)
+    m = H.Meter()
+    H.ffn(1, x, f, abi.TilePlan(16, 16, 64, 1 << 20), abi.F32, meter=m)
+    assert m.peak == 32768 and m.persistent == 4 * 32 * (2 * 64 + 2 * 256)
+    m2 = H.Meter()
+    H.ffn(2, x, f, abi.TilePlan(16, 16, 64, 1 << 20), abi.F32, meter=m2)
+    assert m2.peak == 0
+
+
+# ------------------------------------------------------------------ baselines on the GPU
+@pytest.mark.parametrize("mode", [abi.MODE_DENSE, abi.MODE_NAIVE_LOWRANK], ids=["dense", "naive"])
+def test_materializing_baselines_match_reference(L, ora, reference, mode):
+    layer = oracle.rand_layer(ora, 256, 1024, 4, 4, 32, 77, 64, 128)
+    round_layer_bf16(layer)
+    x = bf16_round(ora.random((2, 100, 256), 5))
+    ref = reference.run_model(x, [layer], mode, PLAN)
+    got = H.run_model(x, [layer], mode, PLAN, abi.BF16)
+    assert H.rel_err(got, ref) <= H.TOL_BF16
+
+
+# ------------------------------------------------------------------ device API (torch plumbing)
+def test_device_api_matches_host_api(L, ora):
+    import torch
+    layers = [oracle.rand_layer(ora, 256, 512, 4, 4, 32, 50 + i, 64, 128) for i in range(2)]
+    for l_ in layers:
+        round_layer_bf16(l_)
+    B, M, d = 2, 160, 256
+    x = bf16_round(ora.random((B, M, d), 6))
+    host = H.run_model(x, layers, abi.MODE_FLASH_V2, PLAN, abi.BF16)
+    descs = layer_descs(layers)
+    packs = []
+    for i in range(2):
+        p = C.c_void_p()
+        abi.check(L.fsvd_layer_pack_create(C.byref(descs[i]), abi.BF16, 0, C.byref(p)))
+        packs.append(p)
+    parr = (C.c_void_p * 2)(*[p.value for p in packs])
+    ws = C.c_size_t()
+    abi.check(L.fsvd_workspace_bytes(parr, 2, B, M, abi.MODE_FLASH_V2, C.byref(ws)))
+    work = torch.empty(ws.value, dtype=torch.uint8, device="cuda")
+    xt = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    n0 = L.fsvd_kernel_launch_count()
+    abi.check(L.fsvd_model_fwd(parr, 2, abi.MODE_FLASH_V2, 0, B, M, C.c_void_p(xt.data_ptr()),
+                               C.c_void_p(xt.data_ptr()), C.c_void_p(work.data_ptr()), ws.value,
+                               C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert L.fsvd_kernel_launch_count() - n0 >= 2 * 4  # qkv gemm, attention, 2 outproj, ffn, 2 LN
+    got = xt.float().cpu().numpy()
+    assert np.array_equal(got, host)  # in-place device run == host API run, bit for bit
+    for p in packs:
+        L.fsvd_layer_pack_destroy(p)
+
+
+# ------------------------------------------------------------------ full-size properties (cfg2)
+def test_cfg2_full_size_properties(L, ora):
+    """BERT-Base B=32 M=512 bf16 (BASELINE configs[1], 2 of the 12 layers):
+    sequence 5 of the batched run equals the oracle run on sequence 5 alone
+    (sequences are independent), and every output row is LayerNorm-shaped."""
+    import torch
+    from paper_2508_01506_b200.model import random_layer
+    rng = np.random.default_rng(0)
+    layers = [round_layer_bf16(random_layer(768, 3072, 12, 12, 32, 384, 384, rng)) for _ in range(2)]
+    B, M, d = 32, 512, 768
+    descs = layer_descs(layers)
+    packs = []
+    for i in range(2):
+        p = C.c_void_p()
+        abi.check(L.fsvd_layer_pack_create(C.byref(descs[i]), abi.BF16, 0, C.byref(p)))
+        packs.append(p)
+    assert L.fsvd_layer_pack_uses_tensor_cores(packs[0]) == 1
+    parr = (C.c_void_p * 2)(*[p.value for p in packs])
+    ws = C.c_size_t()
+    abi.check(L.fsvd_workspace_bytes(parr, 2, B, M, abi.MODE_FLASH_V1, C.byref(ws)))
+    work = torch.empty(ws.value, dtype=torch.uint8, device="cuda")
+    x = torch.randn((B, M, d), generator=torch.Generator().manual_seed(1)).to(torch.bfloat16)
+    xd = x.cuda()
+    out = torch.empty_like(xd)
+    abi.check(L.fsvd_model_fwd(parr, 2, abi.MODE_FLASH_V1, 0, B, M, C.c_void_p(xd.data_ptr()),
+                               C.c_void_p(out.data_ptr()), C.c_void_p(work.data_ptr()), ws.value,
+                               C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    o = out.float().cpu().numpy()
+    assert np.isfinite(o).all()
+    g, b_ = layers[-1].ln2_gamma, layers[-1].ln2_beta
+    z = (o - b_) / g
+    assert np.abs(z.mean(-1)).max() < 0.05 and np.abs(z.var(-1) - 1).max() < 0.1
+    x5 = np.ascontiguousarray(x[5:6].float().numpy())
+    ref = ora.run_model(x5, layers, abi.MODE_FLASH_V1, abi.TilePlan(16, 16, 64, 1 << 22))
+    assert H.rel_err(o[5:6], ref) <= H.TOL_BF16
+    for p in packs:
+        L.fsvd_layer_pack_destroy(p)
