@@ -343,6 +343,28 @@ def run_gpu(args):
         k1.record(stream)
         torch.cuda.synchronize(dev)
         k_ms = k0.elapsed_time(k1) / reps
+        # sublayer timings (same stream, CUDA events) for the breakdown
+        sub = {}
+        for name, fn in (
+                ("attention_fwd", lambda: L.fsvd_attention_fwd(
+                    packs[0], B, M, C.c_void_p(resid.data_ptr()), C.c_void_p(ffn_out.data_ptr()),
+                    C.c_void_p(work.data_ptr()), ffn_ws, sp)),
+                ("outproj_fwd", lambda: L.fsvd_outproj_fwd(
+                    packs[0], B, M, C.c_void_p(resid.data_ptr()), C.c_void_p(ffn_out.data_ptr()),
+                    C.c_void_p(work.data_ptr()), ffn_ws, sp)),
+                ("layer_fwd", lambda: L.fsvd_layer_fwd(
+                    packs[0], mode, 0, B, M, C.c_void_p(resid.data_ptr()),
+                    C.c_void_p(ffn_out.data_ptr()), C.c_void_p(work.data_ptr()), ffn_ws, sp))):
+            for _ in range(2):
+                abi.check(fn())
+            torch.cuda.synchronize(dev)
+            k0.record(stream)
+            for _ in range(reps):
+                abi.check(fn())
+            k1.record(stream)
+            torch.cuda.synchronize(dev)
+            sub[name] = round(k0.elapsed_time(k1) / reps, 4)
+        sub["ffn_fwd"] = round(k_ms, 4)
         flops = T * ffn_flops_per_token()
         achieved = flops / (k_ms * 1e-3) / 1e12
         peak = peaks.get("bf16_tflops", 1590.0)
@@ -351,7 +373,7 @@ def run_gpu(args):
         roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": kname, "kernel_ms": round(k_ms, 4),
-                "algorithmic_flop_per_launch": flops,
+                "algorithmic_flop_per_launch": flops, "sublayer_ms": sub,
                 "peak_source": f"{peak_src} burst bf16 (MEASURED_PEAKS.json) -- kernel timed alone",
                 "model_frac_of_sustained": round(
                     T * LAYERS * algorithmic_flops_per_token_layer() / (ms_max * 1e-3) / 1e12

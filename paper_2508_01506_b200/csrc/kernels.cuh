@@ -27,21 +27,21 @@ void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, 
 bool gemm_bf16_supported(int M, int N, int K, int64_t lda, int64_t ldb, int64_t ldc);
 
 // ---- K2: rank-space FlashSVD attention --------------------------------------
+// out[t, h*rp : (h+1)*rp] = softmax(Qt_h K_g^T) V_g for each (sequence, head),
+// reading Qt / K / V as rank-width column blocks of one [T, qkv_cols] buffer:
+// head h's Qt at q_off + h*rp, group g's K at k_off + g*rp and V at v_off + g*rp.
+// Scores must already be scaled into the log2 domain.
 struct AttnTcArgs {
-  const bf16* P;       // [T, ldp] projected activations; columns (mat, group, rank_pad)
-  int64_t ldp;
-  int batch, seq, heads, groups, rank_pad, head_dim;
-  const bf16* vq_t;    // [H][dh][rp]   (V_q head slice, transposed)  -> Q = P_q Vq
-  const bf16* vk;      // [H][rp][dh]   (V_k head slice)              -> Qt = Q Vk^T
-  const bf16* vv_t;    // [H][dh][rp]   (V_v head slice, transposed)  -> O = Or Vv
-  const float* bq;     // [H][dh] (already multiplied by softmax scale * log2 e)
-  const float* bv;     // [H][dh]
-  float q_scale;       // 1/sqrt(dh) * log2(e)
-  bf16* ctx;           // [T, ldc]
-  int64_t ldc;
+  const bf16* qkv;
+  int64_t ldq;
+  int qkv_cols;
+  int q_off, k_off, v_off;
+  int batch, seq, heads, groups, rank_pad;
+  bf16* out;
+  int64_t ldo;
 };
 void attn_rankspace_bf16(const AttnTcArgs& a, cudaStream_t s);
-bool attn_rankspace_supported(int head_dim, int rank_pad);
+bool attn_rankspace_supported(int rank_pad);
 
 // ---- K3 / K4: FlashSVD-FFN -----------------------------------------------------
 struct FfnTcArgs {

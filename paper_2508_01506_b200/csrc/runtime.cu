@@ -37,7 +37,6 @@ Pack::~Pack() {
 
 namespace {
 
-constexpr float kLog2e = 1.4426950408889634f;
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -113,31 +112,56 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
     p.gd = d / p.G;
     const int G = p.G, r = p.r, H = p.H, dh = p.dh, gd = p.gd, hpg = H / G;
     p.rp = r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : 0;
-    p.attn_tc = bf && p.rp != 0 && attn_rankspace_supported(dh, p.rp) && d % 8 == 0;
+    p.attn_tc = bf && p.rp != 0 && attn_rankspace_supported(p.rp) && d % 8 == 0;
     if (p.attn_tc) {
+      // Folded rank-space projection (attn_tc.cu): rows [0, H*rp) hold
+      // Qt_h = s * U_q,g (V_q,h V_k,h^T), rows [H*rp, (H+G)*rp) U_k,g, then U_v,g.
       const int rp = p.rp;
-      std::vector<float> w(static_cast<size_t>(3) * G * rp * d, 0.0f);
-      for (int m = 0; m < 3; ++m)
+      const double sc = 1.4426950408889634 / std::sqrt(static_cast<double>(dh));
+      p.qkv_cols = (H + 2 * G) * rp;
+      std::vector<float> w((size_t)p.qkv_cols * d, 0.0f), bp((size_t)p.qkv_cols, 0.0f);
+      std::vector<double> mh((size_t)r * r);
+      for (int h = 0; h < H; ++h) {
+        const int g = h / hpg, hc = (h % hpg) * dh;
+        const float* vq = a.v + (size_t)(0 * G + g) * r * gd;
+        const float* vk = a.v + (size_t)(1 * G + g) * r * gd;
+        const float* uq = a.u + (size_t)(0 * G + g) * d * r;
+        for (int j = 0; j < r; ++j)
+          for (int i = 0; i < r; ++i) {
+            double acc = 0.0;
+            for (int c = 0; c < dh; ++c) acc += (double)vq[(size_t)j * gd + hc + c] * vk[(size_t)i * gd + hc + c];
+            mh[(size_t)j * r + i] = acc * sc;
+          }
+        for (int i = 0; i < r; ++i) {
+          float* row = &w[((size_t)h * rp + i) * d];
+          for (int k = 0; k < d; ++k) {
+            double acc = 0.0;
+            for (int j = 0; j < r; ++j) acc += (double)uq[(size_t)k * r + j] * mh[(size_t)j * r + i];
+            row[k] = static_cast<float>(acc);
+          }
+          double bb = 0.0;
+          for (int c = 0; c < dh; ++c) bb += (double)a.bias[h * dh + c] * vk[(size_t)i * gd + hc + c];
+          bp[(size_t)h * rp + i] = static_cast<float>(bb * sc);
+        }
+      }
+      for (int m = 1; m < 3; ++m)
         for (int g = 0; g < G; ++g)
           for (int j = 0; j < r; ++j)
             for (int k = 0; k < d; ++k)
-              w[((size_t)(m * G + g) * rp + j) * d + k] = a.u[((size_t)(m * G + g) * d + k) * r + j];
-      b.store(&p.wqkv_t, w);
-      std::vector<float> vq((size_t)H * dh * rp, 0.0f), vk((size_t)H * rp * dh, 0.0f),
-          vv((size_t)H * dh * rp, 0.0f);
+              w[((size_t)(H + (m - 1) * G + g) * rp + j) * d + k] =
+                  a.u[((size_t)(m * G + g) * d + k) * r + j];
+      b.store(&p.wproj_t, w);
+      b.store_f32(&p.bproj, bp);
+      // block-diagonal V_v: ctx[:, h*dh + c] = sum_j O_h[:, j] V_v,g[j, hc + c] (+ b_v)
+      std::vector<float> vc((size_t)d * H * rp, 0.0f);
       for (int h = 0; h < H; ++h) {
         const int g = h / hpg, hc = (h % hpg) * dh;
-        for (int j = 0; j < r; ++j)
-          for (int dd = 0; dd < dh; ++dd) {
-            vq[((size_t)h * dh + dd) * rp + j] = a.v[((size_t)(0 * G + g) * r + j) * gd + hc + dd];
-            vk[((size_t)h * rp + j) * dh + dd] = a.v[((size_t)(1 * G + g) * r + j) * gd + hc + dd];
-            vv[((size_t)h * dh + dd) * rp + j] = a.v[((size_t)(2 * G + g) * r + j) * gd + hc + dd];
-          }
+        for (int c = 0; c < dh; ++c)
+          for (int j = 0; j < r; ++j)
+            vc[((size_t)h * dh + c) * H * rp + (size_t)h * rp + j] =
+                a.v[((size_t)(2 * G + g) * r + j) * gd + hc + c];
       }
-      b.store(&p.vq_t, vq);
-      b.store(&p.vk, vk);
-      b.store(&p.vv_t, vv);
-      b.store_f32(&p.bq, a.bias, d);
+      b.store(&p.wvc_t, vc);
       b.store_f32(&p.bv, a.bias + 2 * d, d);
     } else {
       std::vector<float> w((size_t)d * 3 * G * r);
@@ -151,7 +175,9 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
       b.store(&p.attn_v, std::vector<float>(a.v, a.v + (size_t)3 * G * r * gd));
     }
     b.store_f32(&p.attn_b, a.bias, 3 * (size_t)d);
-    if (q.dense && p.attn_tc) {
+    if (q.dense && p.attn_tc && dh == 64) {
+      // dense twin W = U V per group (encoder.cpp:295-331); Q rows scaled by s
+      const float sc = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(dh)));
       std::vector<float> wt((size_t)3 * d * d);
       for (int m = 0; m < 3; ++m)
         for (int g = 0; g < G; ++g) {
@@ -159,24 +185,29 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
                                                   a.v + (size_t)(m * G + g) * r * gd, d, r, gd,
                                                   gd, 0);
           for (int c = 0; c < gd; ++c)
-            std::memcpy(&wt[((size_t)m * d + g * gd + c) * d], &part[(size_t)c * d], d * 4);
+            for (int k = 0; k < d; ++k)
+              wt[((size_t)m * d + g * gd + c) * d + k] = part[(size_t)c * d + k] * (m == 0 ? sc : 1.0f);
         }
       b.store(&p.dqkv_t, wt);
-      b.store_f32(&p.dqkv_b, a.bias, 3 * (size_t)d);
+      std::vector<float> bq(a.bias, a.bias + 3 * (size_t)d);
+      for (int i = 0; i < d; ++i) bq[i] *= sc;
+      b.store_f32(&p.dqkv_b, bq);
       const int rp = p.rp;
+      std::vector<float> wn((size_t)3 * G * rp * d, 0.0f);
+      for (int m = 0; m < 3; ++m)
+        for (int g = 0; g < G; ++g)
+          for (int j = 0; j < r; ++j)
+            for (int k = 0; k < d; ++k)
+              wn[((size_t)(m * G + g) * rp + j) * d + k] = a.u[((size_t)(m * G + g) * d + k) * r + j];
+      b.store(&p.wpn_t, wn);
       std::vector<float> bd((size_t)3 * d * 3 * G * rp, 0.0f);
       for (int m = 0; m < 3; ++m)
         for (int g = 0; g < G; ++g)
           for (int c = 0; c < gd; ++c)
             for (int j = 0; j < r; ++j)
               bd[((size_t)m * d + g * gd + c) * (3 * G * rp) + (m * G + g) * rp + j] =
-                  a.v[((size_t)(m * G + g) * r + j) * gd + c];
+                  a.v[((size_t)(m * G + g) * r + j) * gd + c] * (m == 0 ? sc : 1.0f);
       b.store(&p.dvbd_t, bd);
-      std::vector<float> id((size_t)H * 64 * 64, 0.0f);
-      for (int h = 0; h < H; ++h)
-        for (int i = 0; i < 64; ++i) id[((size_t)h * 64 + i) * 64 + i] = 1.0f;
-      b.store(&p.ident, id);
-      b.store_f32(&p.zeros, std::vector<float>((size_t)H * 64, 0.0f));
     }
   }
   if (q.out_proj) {
@@ -194,7 +225,34 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
         for (int n = 0; n < d; ++n) vt[(size_t)n * prp + j] = o.v[(size_t)j * d + n];
       b.store(&p.uo_t, ut);
       b.store(&p.vo_t, vt);
-      if (q.dense) b.store(&p.do_t, reconstruct_t(o.u, o.v, d, pr, d, d, 0));
+      if (q.dense || (q.attn && p.attn_tc)) {
+        // W_o = U_o V_o; stored transposed: wo_t[n][m] = W_o[m][n]
+        std::vector<float> wo_t = reconstruct_t(o.u, o.v, d, pr, d, d, 0);
+        if (q.dense) b.store(&p.do_t, wo_t);
+        if (q.attn && p.attn_tc) {
+          // folded rank-space out-projection: W_ov[(h, j)][n] = sum_c V_v,h[j, c] W_o[h dh + c][n]
+          const fsvd_attn_desc& a = *q.attn;
+          const int H = p.H, G = p.G, r = p.r, rp = p.rp, dh = p.dh, gd = p.gd, hpg = H / G;
+          std::vector<float> wov((size_t)d * H * rp, 0.0f), bov(d);
+          for (int n = 0; n < d; ++n) {
+            const float* won = &wo_t[(size_t)n * d];
+            for (int h = 0; h < H; ++h) {
+              const int g = h / hpg, hc = (h % hpg) * dh;
+              for (int j = 0; j < r; ++j) {
+                const float* vv = a.v + ((size_t)(2 * G + g) * r + j) * gd + hc;
+                double acc = 0.0;
+                for (int c = 0; c < dh; ++c) acc += (double)vv[c] * won[h * dh + c];
+                wov[(size_t)n * H * rp + (size_t)h * rp + j] = static_cast<float>(acc);
+              }
+            }
+            double bb = o.bias[n];
+            for (int m = 0; m < d; ++m) bb += (double)a.bias[2 * d + m] * won[m];
+            bov[n] = static_cast<float>(bb);
+          }
+          b.store(&p.wov_t, wov);
+          b.store_f32(&p.bov, bov);
+        }
+      }
     } else {
       b.store(&p.uo, std::vector<float>(o.u, o.u + (size_t)d * o.rank));
       b.store(&p.vo, std::vector<float>(o.v, o.v + (size_t)o.rank * d));
@@ -290,14 +348,19 @@ void validate_layer(const fsvd_layer_desc& L) {
 // ---------------------------------------------------------------- planner
 size_t op_transient_elems(const Pack& p, int op, int mode) {
   const size_t d = p.d;
-  if (op == 0) {
+  if (op == 0) {  // standalone attention (ctx in head width)
     if (mode == FSVD_MODE_DENSE) return 3 * d;
-    const size_t proj = p.attn_tc ? 3 * (size_t)p.G * p.rp : 3 * (size_t)p.G * p.r;
-    return mode == FSVD_MODE_NAIVE_LOWRANK ? proj + 3 * d : proj;
+    if (mode == FSVD_MODE_NAIVE_LOWRANK) return 3 * (size_t)p.G * p.rp + 3 * d;
+    return p.attn_tc ? (size_t)p.qkv_cols + (size_t)p.H * p.rp : 3 * (size_t)p.G * p.r;
   }
   if (op == 1) {
     if (mode == FSVD_MODE_DENSE) return 0;
     return p.out_tc ? p.prp : p.pr;
+  }
+  if (op == 3) {  // attention inside a layer (rank-space output goes to scratch)
+    if (p.attn_tc && p.out_tc && (mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2))
+      return p.qkv_cols;
+    return op_transient_elems(p, 0, mode);
   }
   const size_t fr = p.ffn_tc ? p.frp : p.fr;
   switch (mode) {
@@ -310,7 +373,7 @@ size_t op_transient_elems(const Pack& p, int op, int mode) {
 
 size_t layer_workspace_bytes(const Pack& p, size_t T, int mode) {
   size_t tr = 0;
-  for (int op = 0; op < 3; ++op) tr = std::max(tr, op_transient_elems(p, op, mode));
+  for (int op : {1, 2, 3}) tr = std::max(tr, op_transient_elems(p, op, mode));
   return 2 * align256(T * p.d * p.es) + align256(T * tr * p.es) + 256;
 }
 
@@ -347,27 +410,54 @@ void simt_attention_t(const Pack& p, size_t B, size_t M, const void* x, void* ct
   simt_attention<T>(a, s);
 }
 
-void tc_attention(const Pack& p, size_t B, size_t M, const bf16* P, int64_t ldp, int groups,
-                  int rp, const void* vq, const void* vk, const void* vv, const float* bq,
-                  const float* bv, void* ctx, cudaStream_t s) {
+void tc_attention(size_t B, size_t M, const bf16* qkv, int qkv_cols, int q_off, int k_off,
+                  int v_off, int heads, int groups, int rp, void* out, int64_t ldo,
+                  cudaStream_t s) {
   AttnTcArgs a;
-  a.P = P;
-  a.ldp = ldp;
+  a.qkv = qkv;
+  a.ldq = qkv_cols;
+  a.qkv_cols = qkv_cols;
+  a.q_off = q_off;
+  a.k_off = k_off;
+  a.v_off = v_off;
   a.batch = (int)B;
   a.seq = (int)M;
-  a.heads = p.H;
+  a.heads = heads;
   a.groups = groups;
   a.rank_pad = rp;
-  a.head_dim = p.dh;
-  a.vq_t = as<bf16>(vq);
-  a.vk = as<bf16>(vk);
-  a.vv_t = as<bf16>(vv);
-  a.bq = bq;
-  a.bv = bv;
-  a.q_scale = kLog2e / std::sqrt(static_cast<float>(p.dh));
-  a.ctx = as<bf16>(ctx);
-  a.ldc = p.d;
+  a.out = as<bf16>(out);
+  a.ldo = ldo;
   attn_rankspace_bf16(a, s);
+}
+
+// Tensor-core flash attention up to the rank-space output O [T, H*rp]:
+// K1 projection into [Qt | P_k | P_v], then K2.
+void tc_attention_rank(const Pack& p, size_t B, size_t M, const void* x, void* o_rank,
+                       void* trans, cudaStream_t s) {
+  const int T = static_cast<int>(B * M), n = p.qkv_cols;
+  bf16* qkv = as<bf16>(trans);
+  gemm_bf16(as<bf16>(x), p.d, as<bf16>(p.wproj_t), p.d, qkv, n, T, n, p.d, p.bproj, ACT_NONE, s);
+  tc_attention(B, M, qkv, n, 0, p.H * p.rp, (p.H + p.G) * p.rp, p.H, p.G, p.rp, o_rank,
+               (int64_t)p.H * p.rp, s);
+}
+
+// Materializing baselines: dense Q|K|V [T, 3d] (dense twin or rebuilt from
+// the factors) then the same attention kernel with r = head_dim.
+void tc_attention_dense(const Pack& p, int mode, size_t B, size_t M, const void* x, void* ctx,
+                        void* trans, cudaStream_t s) {
+  if (!p.dense) fail(Kind::Config, "dense / naive_lowrank modes need a pack built with dense=1 "
+                                   "on the bf16 tensor-core path");
+  const int T = static_cast<int>(B * M), d = p.d, d3 = 3 * p.d;
+  bf16* qkv = as<bf16>(trans);
+  if (mode == FSVD_MODE_DENSE) {
+    gemm_bf16(as<bf16>(x), d, as<bf16>(p.dqkv_t), d, qkv, d3, T, d3, d, p.dqkv_b, ACT_NONE, s);
+  } else {
+    const int n = 3 * p.G * p.rp;
+    bf16* P = qkv + (size_t)T * d3;
+    gemm_bf16(as<bf16>(x), d, as<bf16>(p.wpn_t), d, P, n, T, n, d, nullptr, ACT_NONE, s);
+    gemm_bf16(P, n, as<bf16>(p.dvbd_t), n, qkv, d3, T, d3, n, p.dqkv_b, ACT_NONE, s);
+  }
+  tc_attention(B, M, qkv, d3, 0, d, 2 * d, p.H, p.H, 64, ctx, d, s);
 }
 
 }  // namespace
@@ -376,26 +466,15 @@ void attention_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, v
                    void* trans, cudaStream_t s) {
   const int T = static_cast<int>(B * M);
   if (mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK) {
-    if (!p.dense) fail(Kind::Config, "dense / naive_lowrank modes need a pack built with dense=1 "
-                                     "on the bf16 tensor-core path");
-    const int d3 = 3 * p.d;
-    bf16* qkv = as<bf16>(trans);
-    if (mode == FSVD_MODE_DENSE) {
-      gemm_bf16(as<bf16>(x), p.d, as<bf16>(p.dqkv_t), p.d, qkv, d3, T, d3, p.d, p.dqkv_b, ACT_NONE, s);
-    } else {
-      const int n = 3 * p.G * p.rp;
-      bf16* P = qkv + (size_t)T * d3;
-      gemm_bf16(as<bf16>(x), p.d, as<bf16>(p.wqkv_t), p.d, P, n, T, n, p.d, nullptr, ACT_NONE, s);
-      gemm_bf16(P, n, as<bf16>(p.dvbd_t), n, qkv, d3, T, d3, n, p.attn_b, ACT_NONE, s);
-    }
-    tc_attention(p, B, M, qkv, d3, p.H, 64, p.ident, p.ident, p.ident, p.zeros, p.zeros, ctx, s);
+    tc_attention_dense(p, mode, B, M, x, ctx, trans, s);
     return;
   }
   if (p.attn_tc) {
-    const int n = 3 * p.G * p.rp;
-    bf16* P = as<bf16>(trans);
-    gemm_bf16(as<bf16>(x), p.d, as<bf16>(p.wqkv_t), p.d, P, n, T, n, p.d, nullptr, ACT_NONE, s);
-    tc_attention(p, B, M, P, n, p.G, p.rp, p.vq_t, p.vk, p.vv_t, p.bq, p.bv, ctx, s);
+    // rank-space output after the projection buffer, then back to head width
+    const int hr = p.H * p.rp;
+    bf16* o_rank = as<bf16>(trans) + (size_t)T * p.qkv_cols;
+    tc_attention_rank(p, B, M, x, o_rank, trans, s);
+    gemm_bf16(o_rank, hr, as<bf16>(p.wvc_t), hr, as<bf16>(ctx), p.d, T, p.d, hr, p.bv, ACT_NONE, s);
   } else if (p.dtype == FSVD_BF16) {
     simt_attention_t<bf16>(p, B, M, x, ctx, trans, s);
   } else {
@@ -425,6 +504,23 @@ void outproj_fwd(const Pack& p, int mode, size_t B, size_t M, const void* ctx, v
     simt_gemm<float>(as<float>(trans), p.pr, as<float>(p.vo), d, as<float>(out), d, T, d, p.pr,
                      p.bo, ACT_NONE, s);
   }
+}
+
+// attention + output projection of one layer: x -> branch.  On the tensor-
+// core flash path the rank-space attention output feeds the folded
+// out-projection directly (one GEMM, K = H*rp); `scratch` holds it.
+void attention_block(const Pack& p, int mode, size_t B, size_t M, const void* x, void* scratch,
+                     void* branch, void* trans, cudaStream_t s) {
+  const bool flash = mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2;
+  if (flash && p.attn_tc && p.out_tc) {
+    const int T = static_cast<int>(B * M), hr = p.H * p.rp;
+    tc_attention_rank(p, B, M, x, scratch, trans, s);
+    gemm_bf16(as<bf16>(scratch), hr, as<bf16>(p.wov_t), hr, as<bf16>(branch), p.d, T, p.d, hr,
+              p.bov, ACT_NONE, s);
+    return;
+  }
+  attention_fwd(p, mode, B, M, x, scratch, trans, s);
+  outproj_fwd(p, mode, B, M, scratch, branch, trans, s);
 }
 
 namespace {
@@ -513,15 +609,13 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
   void* trans = base + 2 * act_bytes;
   const int rows = static_cast<int>(T);
   if (!pre_ln) {
-    attention_fwd(p, mode, B, M, x, A, trans, s);                     // ctx    -> A
-    outproj_fwd(p, mode, B, M, A, Bb, trans, s);                      // branch -> B
+    attention_block(p, mode, B, M, x, A, Bb, trans, s);               // branch -> B
     ln(p, x, Bb, p.ln1g, p.ln1b, p.eps1, Bb, rows, s);                // resid  -> B (in place)
     ffn_fwd(p, mode, B, M, Bb, A, trans, s);                          // ffn    -> A
     ln(p, Bb, A, p.ln2g, p.ln2b, p.eps2, out, rows, s);               // out
   } else {
     ln(p, x, nullptr, p.ln1g, p.ln1b, p.eps1, A, rows, s);            // normed -> A
-    attention_fwd(p, mode, B, M, A, Bb, trans, s);                    // ctx    -> B
-    outproj_fwd(p, mode, B, M, Bb, A, trans, s);                      // branch -> A
+    attention_block(p, mode, B, M, A, Bb, A, trans, s);               // branch -> A (via B)
     add(p, x, A, Bb, (int64_t)T * p.d, s);                            // resid  -> B
     ln(p, Bb, nullptr, p.ln2g, p.ln2b, p.eps2, A, rows, s);           // normed -> A
     ffn_fwd(p, mode, B, M, A, out, trans, s);                         // ffn    -> out

@@ -30,26 +30,38 @@ struct Pack {
   bool attn_tc = false, out_tc = false, ffn_tc = false;
   void* mem = nullptr;
   size_t bytes = 0;
-  // attention
-  const void *wqkv_t = nullptr, *vq_t = nullptr, *vk = nullptr, *vv_t = nullptr;
-  const float *bq = nullptr, *bv = nullptr;
+  // attention, tensor-core path (folded rank-space form, see attn_tc.cu):
+  //   wproj_t [(H+2G)*rp][d]  rows: Qt of every head (U_q V_q V_k^T s), U_k, U_v
+  //   bproj   [(H+2G)*rp]     Qt bias s b_q V_k^T, zeros for P_k / P_v
+  //   wvc_t   [d][H*rp]       block-diagonal V_v (rank space -> head width)
+  //   bv      [d]
+  const void* wproj_t = nullptr;
+  const float* bproj = nullptr;
+  const void* wvc_t = nullptr;
+  const float* bv = nullptr;
+  int qkv_cols = 0;  // (H + 2G) * rp
+  // attention, SIMT path (reference layouts)
   const void *wqkv = nullptr, *attn_v = nullptr;
   const float* attn_b = nullptr;
-  // output projection
+  // output projection: low-rank factors (drop-in lowrank_output_projection) and,
+  // on the tensor-core path, the folded rank-space form used inside a layer:
+  //   wov_t [d][H*rp] = (blockdiag(V_v) U_o V_o)^T,  bov = b_v U_o V_o + b_o
   const void *uo_t = nullptr, *vo_t = nullptr, *uo = nullptr, *vo = nullptr;
   const float* bo = nullptr;
+  const void* wov_t = nullptr;
+  const float* bov = nullptr;
   // FFN
   const void *uup_t = nullptr, *vup_t = nullptr, *udn_t = nullptr, *vdn_t = nullptr;
   const void *uup = nullptr, *vup = nullptr, *udn = nullptr, *vdn = nullptr;
   const float *bup = nullptr, *bdn = nullptr;
   // LayerNorms
   const float *ln1g = nullptr, *ln1b = nullptr, *ln2g = nullptr, *ln2b = nullptr;
-  // dense twin / materializing baselines (tensor-core path only)
+  // dense twin / materializing baselines (tensor-core path only); the Q rows
+  // carry the softmax scale s = log2(e)/sqrt(dh)
   const void *dqkv_t = nullptr;   // [3d][d]   dense W_q|W_k|W_v transposed
   const float* dqkv_b = nullptr;  // [3d]
+  const void *wpn_t = nullptr;    // [3*G*rp][d] U_q|U_k|U_v transposed (naive low-rank)
   const void *dvbd_t = nullptr;   // [3d][3*G*rp] block-diagonal V (naive low-rank)
-  const void *ident = nullptr;    // [H][64][64] identity factors
-  const float* zeros = nullptr;   // [H*64] zero biases
   const void *do_t = nullptr, *din_t = nullptr, *dout_t = nullptr;  // [d][d] [df][d] [d][df]
 
   ~Pack();
