@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfsvd_b200.so")
+LIB_PATH = os.environ.get("FSVD_LIB") or os.path.join(_HERE, "lib", "libfsvd_b200.so")
 
 # fsvd_status (errors.hpp:11-21 ErrorKind, offset by one) -----------------
 OK, ERR_SHAPE, ERR_RANK, ERR_CONFIG, ERR_BUDGET, ERR_ACCOUNTING = 0, 1, 2, 3, 4, 5

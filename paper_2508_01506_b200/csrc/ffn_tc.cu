@@ -11,12 +11,20 @@
 // (bf16, K-major SW128 atoms) for the whole stream; Z accumulates in TMEM
 // (FR fp32 columns) across every feature block; the d_ff-wide hidden exists
 // only as one 128 x 128 block: H in TMEM -> registers (+b_up, GELU) -> bf16
-// smem -> A operand of the next MMA.  B operands (V_up^T / U_down^T /
-// U_up^T / V_down^T chunks) stream through a TMA ring of 32 KB stages.
+// smem -> A operand of the next MMA.
 //
-// Tensor-pipe order per block f: MMA1(f+1) is issued as soon as the
-// epilogue has drained H(f) from TMEM, so the GELU of block f overlaps the
-// next block's up-projection; MMA2(f) follows once bf16 H(f) is in smem.
+// Operand streaming: every B operand (V_up^T / U_down^T / U_up^T / V_down^T)
+// arrives as 16 KB slots ([<=128 rows x 64] bf16, SW128) through a TMA ring
+// of 32 KB stages (two slots per stage), so each barrier round trip carries
+// >= 8 MMAs.  The producer and the MMA issuer are single threads with
+// precomputed descriptors (the tensor pipe is issue-bound otherwise).  X
+// chunks of the fused up-projection are staged through the H buffer, which is
+// idle in that phase.
+//
+// Pipelining per feature block f: MMA1(f+1) is issued as soon as the
+// epilogue has drained H(f) from TMEM; MMA2(f) consumes the activated block
+// one 64-wide K atom at a time, so its first half overlaps the epilogue's
+// work on the second.
 //
 // Warps: 0 TMA producer, 1 MMA issuer + TMEM owner, 2..9 epilogue (two warps
 // per TMEM lane quadrant, alternating 32-column chunks).
@@ -31,34 +39,35 @@ using namespace ptx;
 
 constexpr int kThreads = 320;
 constexpr int kEpi = 256;
-constexpr int BMr = 128;        // token rows per CTA
-constexpr int BF = 128;         // features per block
-constexpr int ATOM = BMr * 128; // one [128 x 64] bf16 SW128 atom (16 KB)
-constexpr int STAGE = 32768;
+constexpr int BMr = 128;         // token rows per CTA
+constexpr int BF = 128;          // features per block
+constexpr int SLOT = BMr * 128;  // one [128 x 64] bf16 SW128 atom / ring slot (16 KB)
+constexpr int STAGE = 2 * SLOT;  // two slots per ring stage
 
 template <int FR>
 struct FfnCfg {
   static_assert(FR % 64 == 0 && FR <= 384, "FR must be a multiple of 64, <= 384");
-  static constexpr int STAGES = FR <= 256 ? 4 : 3;
   static constexpr int NATOM = FR / 64;
-  static constexpr int o_p = 0;                      // P / Z tile, NATOM atoms
-  static constexpr int o_h = NATOM * ATOM;           // H tile, 2 atoms
-  static constexpr int o_ring = o_h + 2 * ATOM;
+  static constexpr int PS = (FR % 128 == 0) ? 128 : 64;  // rows per Z / P piece
+  static constexpr int NPIECE = FR / PS;
+  static constexpr int STAGES_FIT = (227 * 1024 - 2048 - (NATOM + 2) * SLOT) / STAGE;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int o_p = 0;                  // P / Z tile, NATOM atoms
+  static constexpr int o_h = NATOM * SLOT;       // H tile (2 atoms) / X double buffer
+  static constexpr int o_ring = o_h + 2 * SLOT;
   static constexpr int o_bar = o_ring + STAGES * STAGE;
   static constexpr int SMEM = 1024 + o_bar + 512;
-  static constexpr int t_z = 0;      // Z / P accumulator (FR cols)
-  static constexpr int t_h = 384;    // H (128 cols)
-  static constexpr int NPIECE = (FR + 255) / 256;  // N pieces of Z / P (<= 256 each)
-  static constexpr int PS = FR / NPIECE;            // rows per piece (multiple of 16)
+  static constexpr int t_z = 0;    // Z / P accumulator (FR cols)
+  static constexpr int t_h = 384;  // H (128 cols)
 };
 
 struct FfnBars {
-  uint64_t full[4], empty[4];
-  uint64_t p_full, p_acc, p_ready, h_full, h_free, sh_full, sh_free, z_full, zs_ready;
+  uint64_t full[8], empty[8];
+  uint64_t x_full[2], x_empty[2];
+  uint64_t p_full, p_acc, p_ready, h_full, h_free, sh_full[2], sh_free[2], z_full, zs_ready;
   uint64_t o_full[2], o_free[2];
   uint32_t tmem;
 };
-
 
 // 32 consecutive fp32 columns of this thread's TMEM row.
 __device__ __forceinline__ void ld_chunk(uint32_t taddr, float (&v)[32]) {
@@ -72,7 +81,7 @@ __device__ __forceinline__ void ld_chunk(uint32_t taddr, float (&v)[32]) {
 // [128 x 64] SW128 atoms.
 __device__ __forceinline__ void st_chunk_smem(uint32_t tile, uint32_t row, int c0,
                                               const float (&v)[32]) {
-  const uint32_t atom = tile + (c0 >> 6) * ATOM;
+  const uint32_t atom = tile + (c0 >> 6) * SLOT;
   const int cc = (c0 & 63) >> 3;
 #pragma unroll
   for (int c = 0; c < 4; ++c)
@@ -88,14 +97,26 @@ __device__ __forceinline__ void st_chunk_global(bf16* dst, const float (&v)[32])
                       pack_bf16(v[8 * c + 4], v[8 * c + 5]), pack_bf16(v[8 * c + 6], v[8 * c + 7]));
 }
 
+#ifdef FSVD_TRACE
+__device__ long long g_trace[4096];
+}  // namespace
+extern "C" __attribute__((visibility("default"))) int fsvd_debug_trace_copy(long long* host, int n) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * n));
+}
+namespace {
+#define TRACE(slot) do { if (blockIdx.x == 0) g_trace[(slot)] = clock64(); } while (0)
+#else
+#define TRACE(slot) do { } while (0)
+#endif
+
 template <int FR, bool FUSED>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_ffn(const __grid_constant__ CUtensorMap tmX,    // X [T, d]     box 128x64 (FUSED)
-          const __grid_constant__ CUtensorMap tmP,    // P [T, FR]    box 128x64 (V1)
-          const __grid_constant__ CUtensorMap tmUup,  // U_up^T [FR, d]  box 256x64
+    k_ffn(const __grid_constant__ CUtensorMap tmX,    // X [T, d]        box 128x64 (FUSED)
+          const __grid_constant__ CUtensorMap tmP,    // P [T, FR]       box 128x64 (V1)
+          const __grid_constant__ CUtensorMap tmUup,  // U_up^T [FR, d]  box PSx64
           const __grid_constant__ CUtensorMap tmVup,  // V_up^T [df, FR] box 128x64
-          const __grid_constant__ CUtensorMap tmUdn,  // U_dn^T [FR, df] box 256x64
-          const __grid_constant__ CUtensorMap tmVdn,  // V_dn^T [d, FR]  box 256x64
+          const __grid_constant__ CUtensorMap tmUdn,  // U_dn^T [FR, df] box PSx64
+          const __grid_constant__ CUtensorMap tmVdn,  // V_dn^T [d, FR]  box QSx64
           const float* __restrict__ b_up, const float* __restrict__ b_dn, int act, int T,
           int d_model, int d_ff, bf16* __restrict__ z_out, bf16* __restrict__ out) {
   using C = FfnCfg<FR>;
@@ -106,10 +127,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t warp = warp_id(), lane = lane_id();
   const int m0 = blockIdx.x * BMr;
   const int NB = (d_ff + BF - 1) / BF;
-  const int KC = d_model / 64;                  // X / V_dn K-chunks... (d_model % 64 == 0)
-  const int NQ = (d_model + 255) / 256;         // output pieces (FUSED)
-  const int QS = d_model / NQ;                  // columns per output piece
+  const int KC = d_model / 64;                        // X K-chunks (FUSED)
+  const int QS = (d_model % 128 == 0) ? 128 : 64;     // output columns per piece (FUSED)
+  const int NQ = d_model / QS;
 
+  if (threadIdx.x == 0) TRACE(0);
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmUup);
     tma_prefetch(&tmVup);
@@ -120,19 +142,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars->full[i], 1);
       mbar_init(&bars->empty[i], 1);
     }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->x_full[i], 1);
+      mbar_init(&bars->x_empty[i], 1);
+      mbar_init(&bars->sh_full[i], kEpi);
+      mbar_init(&bars->sh_free[i], 1);
+      mbar_init(&bars->o_full[i], 1);
+      mbar_init(&bars->o_free[i], kEpi);
+    }
     mbar_init(&bars->p_full, 1);
     mbar_init(&bars->p_acc, 1);
     mbar_init(&bars->p_ready, kEpi);
     mbar_init(&bars->h_full, 1);
     mbar_init(&bars->h_free, kEpi);
-    mbar_init(&bars->sh_full, kEpi);
-    mbar_init(&bars->sh_free, 1);
     mbar_init(&bars->z_full, 1);
     mbar_init(&bars->zs_ready, kEpi);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars->o_full[i], 1);
-      mbar_init(&bars->o_free[i], kEpi);
-    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(&bars->tmem);
@@ -143,198 +167,164 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* ring = smem + C::o_ring;
 
   if (warp == 0) {
-    // ================================================= TMA producer
-    uint32_t st = 0, ph = 0;
-    auto next = [&]() {
-      if (++st == C::STAGES) { st = 0; ph ^= 1; }
-    };
-    auto acquire = [&](uint32_t bytes) -> uint8_t* {
-      mbar_wait(&bars->empty[st], ph ^ 1);
-      if (lane == 0) mbar_arrive_expect_tx(&bars->full[st], bytes);
-      return ring + st * STAGE;
-    };
-    auto load_mma1 = [&](int f) {
-      for (int a = 0; a < C::NATOM; a += 2) {
-        const int na = (a + 1 < C::NATOM) ? 2 : 1;
-        uint8_t* s = acquire(na * ATOM);
-        if (lane == 0)
-          for (int i = 0; i < na; ++i)
-            tma_load_2d(&tmVup, &bars->full[st], s + i * ATOM, (a + i) * 64, f * BF);
-        __syncwarp();
-        next();
-      }
-    };
-    auto load_mma2 = [&](int f) {
-      for (int p = 0; p < C::NPIECE; ++p) {
-        constexpr int np = C::PS;
-        for (int a2 = 0; a2 < 2; ++a2) {
-          uint8_t* s = acquire(np * 128);
-          if (lane == 0) tma_load_2d(&tmUdn, &bars->full[st], s, f * BF + a2 * 64, p * C::PS);
-          __syncwarp();
-          next();
+    // ================================================= TMA producer (one thread)
+    if (lane == 0) {
+      uint32_t st = 0, ph = 0;
+      // Streams n slots, two per stage.  slot(i, dst, size_only) returns the
+      // byte count of slot i and, unless size_only, issues its TMA.
+      auto emit = [&](int n, auto&& slot) {
+        for (int i = 0; i < n; i += 2) {
+          mbar_wait(&bars->empty[st], ph ^ 1);
+          uint8_t* base = ring + st * STAGE;
+          uint32_t bytes = slot(i, base, true);
+          if (i + 1 < n) bytes += slot(i + 1, base + SLOT, true);
+          mbar_arrive_expect_tx(&bars->full[st], bytes);
+          slot(i, base, false);
+          if (i + 1 < n) slot(i + 1, base + SLOT, false);
+          if (++st == C::STAGES) { st = 0; ph ^= 1; }
         }
-      }
-    };
-    if (FUSED) {
-      for (int kc = 0; kc < KC; ++kc) {
-        uint8_t* s = acquire(ATOM);
-        if (lane == 0) tma_load_2d(&tmX, &bars->full[st], s, kc * 64, m0);
-        __syncwarp();
-        next();
-        for (int p = 0; p < C::NPIECE; ++p) {
-          constexpr int np = C::PS;
-          uint8_t* s2 = acquire(np * 128);
-          if (lane == 0) tma_load_2d(&tmUup, &bars->full[st], s2, kc * 64, p * C::PS);
-          __syncwarp();
-          next();
+      };
+      auto mma1_slots = [&](int f) {
+        emit(C::NATOM, [&](int a, uint8_t* dst, bool size_only) -> uint32_t {
+          if (!size_only) tma_load_2d(&tmVup, &bars->full[st], dst, a * 64, f * BF);
+          return SLOT;
+        });
+      };
+      auto mma2_slots = [&](int f) {  // atom-major: (a0: p0..), (a1: p0..)
+        emit(2 * C::NPIECE, [&](int j, uint8_t* dst, bool size_only) -> uint32_t {
+          const int a = j / C::NPIECE, p = j % C::NPIECE;
+          if (!size_only)
+            tma_load_2d(&tmUdn, &bars->full[st], dst, f * BF + a * 64, p * C::PS);
+          return C::PS * 128;
+        });
+      };
+      if (FUSED) {
+        for (int kc = 0; kc < KC; ++kc) {
+          const int xb = kc & 1;
+          mbar_wait(&bars->x_empty[xb], ((kc >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&bars->x_full[xb], SLOT);
+          tma_load_2d(&tmX, &bars->x_full[xb], smem + C::o_h + xb * SLOT, kc * 64, m0);
+          emit(C::NPIECE, [&](int p, uint8_t* dst, bool size_only) -> uint32_t {
+            if (!size_only) tma_load_2d(&tmUup, &bars->full[st], dst, kc * 64, p * C::PS);
+            return C::PS * 128;
+          });
         }
-      }
-    } else {
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&bars->p_full, C::NATOM * ATOM);
+      } else {
+        mbar_arrive_expect_tx(&bars->p_full, C::NATOM * SLOT);
         for (int a = 0; a < C::NATOM; ++a)
-          tma_load_2d(&tmP, &bars->p_full, smem + C::o_p + a * ATOM, a * 64, m0);
+          tma_load_2d(&tmP, &bars->p_full, smem + C::o_p + a * SLOT, a * 64, m0);
       }
-      __syncwarp();
-    }
-    load_mma1(0);
-    for (int f = 0; f < NB; ++f) {
-      if (f + 1 < NB) load_mma1(f + 1);
-      load_mma2(f);
-    }
-    if (FUSED) {
-      for (int q = 0; q < NQ; ++q) {
-        const int nq = QS;
-        for (int a = 0; a < C::NATOM; ++a) {
-          uint8_t* s = acquire(nq * 128);
-          if (lane == 0) tma_load_2d(&tmVdn, &bars->full[st], s, a * 64, q * QS);
-          __syncwarp();
-          next();
-        }
+      TRACE(2);
+      mma1_slots(0);
+      for (int f = 0; f < NB; ++f) {
+        TRACE(2048 + f * 2);
+        if (f + 1 < NB) mma1_slots(f + 1);
+        TRACE(2048 + f * 2 + 1);
+        mma2_slots(f);
+      }
+      if (FUSED) {
+        for (int q = 0; q < NQ; ++q)
+          emit(C::NATOM, [&](int a, uint8_t* dst, bool size_only) -> uint32_t {
+            if (!size_only) tma_load_2d(&tmVdn, &bars->full[st], dst, a * 64, q * QS);
+            return QS * 128;
+          });
       }
     }
-  } else if (warp == 1) {
-    // ================================================= MMA issuer
-    uint32_t st = 0, ph = 0;
-    const uint32_t s_p = smem_u32(smem + C::o_p), s_h = smem_u32(smem + C::o_h);
-    const uint32_t s_ring = smem_u32(ring);
-    auto wait_full = [&]() -> uint32_t {
-      mbar_wait(&bars->full[st], ph);
-      tc_fence_after();
-      return s_ring + st * STAGE;
-    };
-    auto release = [&](uint32_t stage_idx) {
-      if (lane == 0) mma_commit(&bars->empty[stage_idx]);
-      __syncwarp();
-    };
-    auto next = [&]() {
-      if (++st == C::STAGES) { st = 0; ph ^= 1; }
-    };
-    if (FUSED) {
-      // P = X U_up into the Z columns of TMEM
-      for (int kc = 0; kc < KC; ++kc) {
-        const uint32_t xs = wait_full();
-        const uint32_t xst = st;
-        next();
-        for (int p = 0; p < C::NPIECE; ++p) {
-          constexpr int np = C::PS;
-          const uint32_t bs = wait_full();
-          if (lane == 0) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16_ss(tmem + C::t_z + p * C::PS, desc_kmajor(xs + k * 32, 128),
-                          desc_kmajor(bs + k * 32, 128), idesc_bf16(128, np), (kc | k) != 0);
-          }
-          __syncwarp();
-          release(st);
-          next();
-        }
-        release(xst);
-      }
-      if (lane == 0) mma_commit(&bars->p_acc);
-      __syncwarp();
-      mbar_wait(&bars->p_ready, 0);
-    } else {
-      mbar_wait(&bars->p_full, 0);
-    }
-    tc_fence_after();
-    auto mma1 = [&](int f) {
-      if (f > 0) {
-        mbar_wait(&bars->h_free, (f - 1) & 1);
-        tc_fence_after();
-      }
-      for (int a = 0; a < C::NATOM; a += 2) {
-        const int na = (a + 1 < C::NATOM) ? 2 : 1;
-        const uint32_t bs = wait_full();
-        if (lane == 0) {
-          for (int i = 0; i < na; ++i)
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16_ss(tmem + C::t_h, desc_kmajor(s_p + (a + i) * ATOM + k * 32, 128),
-                          desc_kmajor(bs + i * ATOM + k * 32, 128), idesc_bf16(128, BF),
-                          (a + i) != 0 || k != 0);
-        }
-        __syncwarp();
-        release(st);
-        next();
-      }
-      if (lane == 0) mma_commit(&bars->h_full);
-      __syncwarp();
-    };
-    auto mma2 = [&](int f) {
-      mbar_wait(&bars->sh_full, f & 1);
-      tc_fence_after();
-      for (int p = 0; p < C::NPIECE; ++p) {
-        constexpr int np = C::PS;
-        for (int a2 = 0; a2 < 2; ++a2) {
-          const uint32_t bs = wait_full();
-          if (lane == 0) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16_ss(tmem + C::t_z + p * C::PS, desc_kmajor(s_h + a2 * ATOM + k * 32, 128),
-                          desc_kmajor(bs + k * 32, 128), idesc_bf16(128, np),
-                          (f | a2 | k) != 0);
-          }
-          __syncwarp();
-          release(st);
-          next();
-        }
-      }
-      if (lane == 0) mma_commit(&bars->sh_free);
-      __syncwarp();
-    };
-    mma1(0);
-    for (int f = 0; f < NB; ++f) {
-      if (f + 1 < NB) mma1(f + 1);
-      mma2(f);
-    }
-    if (lane == 0) mma_commit(&bars->z_full);
     __syncwarp();
-    if (FUSED) {
-      mbar_wait(&bars->zs_ready, 0);
+  } else if (warp == 1) {
+    // ================================================= MMA issuer (one thread)
+    if (lane == 0) {
+      uint32_t st = 0, ph = 0;
+      const uint64_t dhi = desc_hi_kmajor(128);
+      const uint32_t s_p = smem_u32(smem + C::o_p), s_h = smem_u32(smem + C::o_h);
+      const uint32_t s_ring = smem_u32(ring);
+      // Consumes n slots two per stage: fn(i, slot_addr) issues slot i's MMAs;
+      // each stage is released once its MMAs have been issued.
+      auto consume = [&](int n, auto&& fn) {
+        for (int i = 0; i < n; i += 2) {
+          mbar_wait(&bars->full[st], ph);
+          tc_fence_after();
+          const uint32_t base = s_ring + st * STAGE;
+          fn(i, base);
+          if (i + 1 < n) fn(i + 1, base + SLOT);
+          mma_commit(&bars->empty[st]);
+          if (++st == C::STAGES) { st = 0; ph ^= 1; }
+        }
+      };
+      auto mma4 = [&](uint32_t d, uint32_t a, uint32_t b, uint32_t idesc, bool acc0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_bf16_ss(d, desc_at(dhi, a + k * 32), desc_at(dhi, b + k * 32), idesc,
+                      (acc0 || k != 0) ? 1u : 0u);
+      };
+      if (FUSED) {
+        // P = X U_up into the Z columns of TMEM
+        for (int kc = 0; kc < KC; ++kc) {
+          const int xb = kc & 1;
+          mbar_wait(&bars->x_full[xb], (kc >> 1) & 1);
+          tc_fence_after();
+          consume(C::NPIECE, [&](int p, uint32_t slot) {
+            mma4(tmem + C::t_z + p * C::PS, s_h + xb * SLOT, slot, idesc_bf16(128, C::PS), kc != 0);
+          });
+          mma_commit(&bars->x_empty[xb]);
+        }
+        mma_commit(&bars->p_acc);
+        TRACE(3);
+        mbar_wait(&bars->p_ready, 0);
+        TRACE(4);
+      } else {
+        mbar_wait(&bars->p_full, 0);
+      }
       tc_fence_after();
-      for (int q = 0; q < NQ; ++q) {
-        const int nq = QS;
-        if (q >= 2) {
-          mbar_wait(&bars->o_free[q & 1], ((q >> 1) - 1) & 1);
+      auto mma1 = [&](int f) {
+        TRACE(64 + f * 8 + 0);
+        if (f > 0) {
+          mbar_wait(&bars->h_free, (f - 1) & 1);
           tc_fence_after();
         }
-        for (int a = 0; a < C::NATOM; ++a) {
-          const uint32_t bs = wait_full();
-          if (lane == 0) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16_ss(tmem + (q & 1) * 256, desc_kmajor(s_p + a * ATOM + k * 32, 128),
-                          desc_kmajor(bs + k * 32, 128), idesc_bf16(128, nq), (a | k) != 0);
+        TRACE(64 + f * 8 + 1);
+        consume(C::NATOM, [&](int a, uint32_t slot) {
+          mma4(tmem + C::t_h, s_p + a * SLOT, slot, idesc_bf16(128, BF), a != 0);
+        });
+        mma_commit(&bars->h_full);
+        TRACE(64 + f * 8 + 2);
+      };
+      auto mma2 = [&](int f) {
+        consume(2 * C::NPIECE, [&](int j, uint32_t slot) {
+          const int a = j / C::NPIECE, p = j % C::NPIECE;
+          if (p == 0) {
+            TRACE(64 + f * 8 + 3 + a * 2);
+            mbar_wait(&bars->sh_full[a], f & 1);
+            tc_fence_after();
+            TRACE(64 + f * 8 + 4 + a * 2);
           }
-          __syncwarp();
-          release(st);
-          next();
+          mma4(tmem + C::t_z + p * C::PS, s_h + a * SLOT, slot, idesc_bf16(128, C::PS),
+               (f | a) != 0);
+          if (p == C::NPIECE - 1) mma_commit(&bars->sh_free[a]);
+        });
+      };
+      mma1(0);
+      for (int f = 0; f < NB; ++f) {
+        if (f + 1 < NB) mma1(f + 1);
+        mma2(f);
+      }
+      mma_commit(&bars->z_full);
+      if (FUSED) {
+        mbar_wait(&bars->zs_ready, 0);
+        tc_fence_after();
+        for (int q = 0; q < NQ; ++q) {
+          if (q >= 2) {
+            mbar_wait(&bars->o_free[q & 1], ((q >> 1) - 1) & 1);
+            tc_fence_after();
+          }
+          consume(C::NATOM, [&](int a, uint32_t slot) {
+            mma4(tmem + (q & 1) * 128, s_p + a * SLOT, slot, idesc_bf16(128, QS), a != 0);
+          });
+          mma_commit(&bars->o_full[q & 1]);
         }
-        if (lane == 0) mma_commit(&bars->o_full[q & 1]);
-        __syncwarp();
       }
     }
+    __syncwarp();
   } else {
     // ================================================= epilogue (8 warps)
     const uint32_t quad = warp & 3;
@@ -362,25 +352,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int fb = f * BF + (half + 2 * i) * 32;
         load_bias<32>(bb[i], b_up + fb, d_ff - fb);
       }
+      if (threadIdx.x == 64) TRACE(1024 + f * 8 + 0);
       mbar_wait(&bars->h_full, f & 1);
       tc_fence_after();
+      if (threadIdx.x == 64) TRACE(1024 + f * 8 + 1);
       float v[2][32];
 #pragma unroll
       for (int i = 0; i < 2; ++i) ld_chunk(tmem + C::t_h + loff + (half + 2 * i) * 32, v[i]);
       tc_fence_before();
       mbar_arrive(&bars->h_free);
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < 2; ++i) {  // i = K atom of the H block
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[i][j] += bb[i][j];
         act_chunk<32>(v[i], act);
+        if (threadIdx.x == 64) TRACE(1024 + f * 8 + 2 + i * 2);
+        if (f > 0) mbar_wait(&bars->sh_free[i], (f - 1) & 1);
+        if (threadIdx.x == 64) TRACE(1024 + f * 8 + 3 + i * 2);
+        st_chunk_smem(s_h, row, (half + 2 * i) * 32, v[i]);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&bars->sh_full[i]);
       }
-      if (f > 0) mbar_wait(&bars->sh_free, (f - 1) & 1);
-#pragma unroll
-      for (int i = 0; i < 2; ++i) st_chunk_smem(s_h, row, (half + 2 * i) * 32, v[i]);
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(&bars->sh_full);
     }
     mbar_wait(&bars->z_full, 0);
     tc_fence_after();
@@ -400,12 +393,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars->zs_ready);
       for (int q = 0; q < NQ; ++q) {
-        const int nq = QS;
         mbar_wait(&bars->o_full[q & 1], (q >> 1) & 1);
         tc_fence_after();
-        for (int c = half; c < nq / 32; c += 2) {
+        for (int c = half; c < QS / 32; c += 2) {
           float v[32];
-          ld_chunk(tmem + (q & 1) * 256 + loff + c * 32, v);
+          ld_chunk(tmem + (q & 1) * 128 + loff + c * 32, v);
           const int n0 = q * QS + c * 32;
           bias_act_chunk<32>(v, b_dn + n0, 32, 3);
           if (grow < T) st_chunk_global(out + (int64_t)grow * d_model + n0, v);
@@ -417,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) TRACE(1);
   if (warp == 1) {
     tc_fence_after();
     tmem_free<512>(tmem);
@@ -433,7 +426,7 @@ void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
     attr = true;
   }
   const int boxp = C::PS;
-  const int boxd = a.d_model / ((a.d_model + 255) / 256);
+  const int boxd = (a.d_model % 128 == 0) ? 128 : 64;
   const CUtensorMap tup = tmap_bf16(a.up_u_t, FR, a.d_model, a.d_model, boxp, 64, TmaSwizzle::B128);
   const CUtensorMap tvup = tmap_bf16(a.up_v_t, a.d_ff, FR, FR, BF, 64, TmaSwizzle::B128);
   const CUtensorMap tudn = tmap_bf16(a.dn_u_t, FR, a.d_ff, a.d_ff, boxp, 64, TmaSwizzle::B128);
@@ -465,9 +458,8 @@ void dispatch_ffn(const FfnTcArgs& a, cudaStream_t s) {
 }  // namespace
 
 bool ffn_tc_supported(int d_model, int d_ff, int rank_pad) {
-  const int nq = (d_model + 255) / 256;
-  return d_model % 64 == 0 && d_model % nq == 0 && (d_model / nq) % 32 == 0 && d_ff % 8 == 0 &&
-         rank_pad % 64 == 0 && rank_pad <= 384 && rank_pad >= 64;
+  return d_model % 64 == 0 && d_ff % 8 == 0 && rank_pad % 64 == 0 && rank_pad <= 384 &&
+         rank_pad >= 64;
 }
 
 void ffn_stream_bf16(const FfnTcArgs& a, cudaStream_t s) { dispatch_ffn<false>(a, s); }

@@ -83,49 +83,49 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
-    uint32_t stage = 0, phase = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
-      for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (lane == 0) {
+    // ---------------- TMA producer (one thread) ----------------
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
           tma_load_2d(&tmA, &full[stage], sA + stage * Cfg::A_BYTES, kb * BK, m0);
           tma_load_2d(&tmB, &full[stage], sB + stage * Cfg::B_BYTES, kb * BK, n0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc = idesc_bf16(BM, BN);
-    uint32_t stage = 0, phase = 0;
-    int i = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
-      const uint32_t acc = i & 1, use = i >> 1;
-      mbar_wait(&tempty[acc], (use & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t d = tmem + acc * BN;
-      for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&full[stage], phase);
+    // ---------------- MMA issuer (one thread, descriptors precomputed) ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(BM, BN);
+      const uint64_t dhi = desc_hi_kmajor(128);
+      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+      uint32_t stage = 0, phase = 0;
+      int i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const uint32_t acc = i & 1, use = i >> 1;
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = a_base + stage * Cfg::A_BYTES, b0 = b_base + stage * Cfg::B_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            mma_bf16_ss(d, desc_kmajor(a0 + k * 32, 128), desc_kmajor(b0 + k * 32, 128), idesc,
+            mma_bf16_ss(d, desc_at(dhi, a0 + k * 32), desc_at(dhi, b0 + k * 32), idesc,
                         (kb | k) != 0);
           mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        mma_commit(&tfull[acc]);
       }
-      if (lane == 0) mma_commit(&tfull[acc]);
-      __syncwarp();
     }
+    __syncwarp();
   } else {
     // ---------------- epilogue ----------------
     const uint32_t q = warp & 3;  // TMEM lane quadrant of this warp

@@ -168,7 +168,19 @@ __device__ __forceinline__ uint64_t desc_kmajor(uint32_t saddr, uint32_t row_byt
 // MN extent (<= swizzle width); 8-K-row groups are 8*row_bytes apart.
 __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t saddr, uint32_t row_bytes) {
   const uint32_t layout = row_bytes == 128 ? SW128 : row_bytes == 64 ? SW64 : SW32;
-  return smem_desc(saddr, 8 * row_bytes * 0 + 16, 8 * row_bytes, layout);
+  return smem_desc(saddr, 16, 8 * row_bytes, layout);
+}
+
+// Cheap descriptor construction inside MMA issue loops: the constant fields
+// are computed once (desc_hi_*), only the 14-bit start address varies.
+__device__ __forceinline__ uint64_t desc_hi_kmajor(uint32_t row_bytes) {
+  return desc_kmajor(0, row_bytes);
+}
+__device__ __forceinline__ uint64_t desc_hi_mnmajor(uint32_t row_bytes) {
+  return desc_mnmajor(0, row_bytes);
+}
+__device__ __forceinline__ uint64_t desc_at(uint64_t hi, uint32_t saddr) {
+  return hi | static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
 }
 
 // Instruction descriptor, kind::f16 with BF16 inputs and FP32 accumulate.
