@@ -97,25 +97,35 @@ class Clocks:
                 "samples": len(sm)}
 
 
+# This pool's MEASURED_PEAKS.json as recorded in SURVEY.md (line 6) when the
+# driver-written file is not present in the snapshot.
+SURVEY_PEAKS = {"hbm_gbs": 6531.6, "bf16_tflops": 1628.9, "bf16_tflops_sustained": 1400.1}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return p, "measured"
+        return p, "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+        return dict(SURVEY_PEAKS), "measured (MEASURED_PEAKS.json values recorded in SURVEY.md)"
 
 
-def load_ncu_traffic(kernel):
-    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    try:
-        with open(path) as f:
-            s = json.load(f)
-        k = s["kernels"][kernel]
-        return k["dram_bytes_read"] + k["dram_bytes_write"]
-    except Exception:
-        return None
+def load_ncu_traffic(prefix):
+    """DRAM bytes (read + write) per launch of the kernel whose name starts with
+    `prefix`, from the newest committed `ncu --set full` summary in profiles/."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")), reverse=True):
+        try:
+            with open(path) as f:
+                s = json.load(f)
+        except Exception:
+            continue
+        for name, k in s.get("kernels", {}).items():
+            if name.startswith(prefix) and "dram_bytes_read" in k:
+                return {"bytes": int(k["dram_bytes_read"] + k.get("dram_bytes_write", 0)),
+                        "source": os.path.relpath(path, ROOT), "kernel": name}
+    return None
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -367,17 +377,19 @@ def run_gpu(args):
         sub["ffn_fwd"] = round(k_ms, 4)
         flops = T * ffn_flops_per_token()
         achieved = flops / (k_ms * 1e-3) / 1e12
-        peak = peaks.get("bf16_tflops", 1590.0)
+        peak = peaks.get("bf16_tflops", SURVEY_PEAKS["bf16_tflops"])
         kname = "k_ffn_fused" if ffn_variant == 2 else "k_ffn_stream+k_gemm_bf16"
-        traffic = load_ncu_traffic("k_ffn_fused" if ffn_variant == 2 else "k_ffn_stream")
+        tr = load_ncu_traffic("k_ffn<")
+        traffic = tr["bytes"] if tr else None
         roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": kname, "kernel_ms": round(k_ms, 4),
                 "algorithmic_flop_per_launch": flops, "sublayer_ms": sub,
-                "peak_source": f"{peak_src} burst bf16 (MEASURED_PEAKS.json) -- kernel timed alone",
+                "traffic_source": tr,
+                "peak_source": f"{peak_src}: burst bf16 (kernel timed alone)",
                 "model_frac_of_sustained": round(
                     T * LAYERS * algorithmic_flops_per_token_layer() / (ms_max * 1e-3) / 1e12
-                    / peaks.get("bf16_tflops_sustained", 1400.0), 4)}
+                    / peaks.get("bf16_tflops_sustained", SURVEY_PEAKS["bf16_tflops_sustained"]), 4)}
 
     # ---------------- peak activation memory ----------------
     mem = {}
