@@ -285,6 +285,25 @@ uint64_t fsvd_kernel_launch_count(void);
 /* Name of the kernel that dominated the last fsvd_model_fwd schedule. */
 const char* fsvd_kernel_name(int kernel_id);
 
+/* ------------------------------------------------------------------ */
+/* Kernel test hooks: one tensor-core kernel on caller device buffers   */
+/* (bf16 row-major, fp32 vectors), asynchronous on `stream`.  Used by   */
+/* the per-kernel numerics tests against a torch fp32 reference.        */
+/* ------------------------------------------------------------------ */
+/* K1: C[M,N] = A[M,K] B[N,K]^T (+ bias) (act) */
+fsvd_status fsvd_test_gemm(const void* A, size_t lda, const void* B, size_t ldb, void* C,
+                           size_t ldc, size_t M, size_t N, size_t K, const float* bias,
+                           fsvd_activation act, int use_act, void* stream);
+/* K6: y = LN(resid + bf16(A B^T + bias)) * gamma + beta */
+fsvd_status fsvd_test_gemm_ln(const void* A, size_t lda, const void* B, size_t ldb,
+                              const float* bias, const void* resid, const float* gamma,
+                              const float* beta, float eps, void* y, size_t T, size_t N,
+                              size_t K, void* stream);
+/* K5: y = LN(a (+ b)) * gamma + beta */
+fsvd_status fsvd_test_resid_layernorm(const void* a, const void* b, const float* gamma,
+                                      const float* beta, float eps, void* y, size_t rows,
+                                      size_t d, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

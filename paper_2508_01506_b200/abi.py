@@ -137,6 +137,11 @@ def _declare(lib):
                                 C.c_int, C.c_char_p, C.c_int, vp, _fp]),
         "fsvd_kernel_launch_count": (C.c_uint64, []),
         "fsvd_kernel_name": (C.c_char_p, [C.c_int]),
+        "fsvd_test_gemm": (st, [vp, _sz, vp, _sz, vp, _sz, _sz, _sz, _sz, vp, C.c_int, C.c_int,
+                                vp]),
+        "fsvd_test_gemm_ln": (st, [vp, _sz, vp, _sz, vp, vp, vp, vp, C.c_float, vp, _sz, _sz,
+                                   _sz, vp]),
+        "fsvd_test_resid_layernorm": (st, [vp, vp, vp, vp, C.c_float, vp, _sz, _sz, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

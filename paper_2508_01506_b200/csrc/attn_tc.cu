@@ -133,17 +133,20 @@ __global__ void __launch_bounds__(kThreads, 2)
   } else if (warp == kMma) {
     // ------------------------------------------------ MMA issuer
     mbar_wait(&bars->pro, 0);
+    const uint64_t dq = desc_kmajor(s_q, C::RB);
+    const uint64_t dk0 = desc_kmajor(s_kv, C::RB);
+    const uint64_t dp0 = desc_kmajor(s_p, 128);
+    const uint64_t dv0 = desc_mnmajor(s_kv + up1k(C::TILE), C::RB);
     auto issue_s = [&](int j) {
       const uint32_t st = j % C::STAGES;
       mbar_wait(&bars->kv_full[st], (j / C::STAGES) & 1);
       if (j > 0) mbar_wait(&bars->s_free, (j - 1) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t pk = s_kv + st * C::KV_STAGE;
+      const uint64_t dk = dk0 + ((st * C::KV_STAGE) >> 4);
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < RP / 16; ++k)
-          mma_bf16_ss(tmem + C::t_s, desc_kmajor(s_q + k * 32, C::RB),
-                      desc_kmajor(pk + k * 32, C::RB), idesc_bf16(128, KT), k != 0);
+          mma_bf16_ss(tmem + C::t_s, dq + 2 * k, dk + 2 * k, idesc_bf16(128, KT), k != 0);
         mma_commit(&bars->s_full);
       }
       __syncwarp();
@@ -153,14 +156,13 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (j + 1 < nj) issue_s(j + 1);
       mbar_wait(&bars->p_full, j & 1);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t st = j % C::STAGES;
-        const uint32_t pv = s_kv + st * C::KV_STAGE + up1k(C::TILE);
+      const uint32_t st = j % C::STAGES;
+      const uint64_t dv = dv0 + ((st * C::KV_STAGE) >> 4);
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < KT / 16; ++k)
-          mma_bf16_ss(tmem + C::t_o, desc_kmajor(s_p + (k >> 2) * (QT * 128) + (k & 3) * 32, 128),
-                      desc_mnmajor(pv + k * 16 * C::RB, C::RB), idesc_bf16(128, RP, 0, 1),
-                      (j | k) != 0);
+          mma_bf16_ss(tmem + C::t_o, dp0 + (((k >> 2) * (QT * 128) + (k & 3) * 32) >> 4),
+                      dv + ((k * 16 * C::RB) >> 4), idesc_bf16(128, RP, 0, 1), (j | k) != 0);
         mma_commit(&bars->o_full);
         mma_commit(&bars->kv_empty[st]);
       }

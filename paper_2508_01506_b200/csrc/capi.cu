@@ -80,6 +80,7 @@ size_t working_set(const fsvd_tile_plan& plan, int kind, const fsvd_geometry& g,
     size_t n;
   };
   std::vector<Buf> bufs;
+  bufs.reserve(10);
   if (kind == FSVD_KERNEL_ATTENTION)
     bufs = {{"q_tile", bm * gd},   {"k_tile", br * gd},     {"v_tile", br * gd},
             {"score_tile", bm * br}, {"prob_tile", bm * br}, {"out_acc", bm * gd},
@@ -697,6 +698,41 @@ fsvd_status fsvd_run_model(const float* x, size_t batch, size_t seq, size_t widt
 }
 
 uint64_t fsvd_kernel_launch_count(void) { return launch_count(); }
+
+fsvd_status fsvd_test_gemm(const void* A, size_t lda, const void* B, size_t ldb, void* C,
+                           size_t ldc, size_t M, size_t N, size_t K, const float* bias,
+                           fsvd_activation act, int use_act, void* stream) {
+  return guard([&] {
+    require_device();
+    if (!gemm_bf16_supported((int)M, (int)N, (int)K, lda, ldb, ldc))
+      fail(Kind::Config, "gemm: unsupported shape");
+    gemm_bf16(static_cast<const bf16*>(A), lda, static_cast<const bf16*>(B), ldb,
+              static_cast<bf16*>(C), ldc, (int)M, (int)N, (int)K, bias,
+              use_act ? static_cast<int>(act) : ACT_NONE, static_cast<cudaStream_t>(stream));
+  });
+}
+fsvd_status fsvd_test_gemm_ln(const void* A, size_t lda, const void* B, size_t ldb,
+                              const float* bias, const void* resid, const float* gamma,
+                              const float* beta, float eps, void* y, size_t T, size_t N,
+                              size_t K, void* stream) {
+  return guard([&] {
+    require_device();
+    if (!gemm_ln_supported((int)N, (int)K)) fail(Kind::Config, "gemm_ln: unsupported shape");
+    gemm_ln_bf16(static_cast<const bf16*>(A), lda, static_cast<const bf16*>(B), ldb, bias,
+                 static_cast<const bf16*>(resid), gamma, beta, eps, static_cast<bf16*>(y), (int)T,
+                 (int)N, (int)K, static_cast<cudaStream_t>(stream));
+  });
+}
+fsvd_status fsvd_test_resid_layernorm(const void* a, const void* b, const float* gamma,
+                                      const float* beta, float eps, void* y, size_t rows,
+                                      size_t d, void* stream) {
+  return guard([&] {
+    require_device();
+    resid_layernorm_bf16(static_cast<const bf16*>(a), static_cast<const bf16*>(b), gamma, beta,
+                         eps, static_cast<bf16*>(y), (int)rows, (int)d,
+                         static_cast<cudaStream_t>(stream));
+  });
+}
 
 const char* fsvd_kernel_name(int id) {
   switch (id) {

@@ -26,10 +26,13 @@
 // one 64-wide K atom at a time, so its first half overlaps the epilogue's
 // work on the second.
 //
-// Warps: 0 TMA producer, 1 MMA issuer + TMEM owner, 2..9 epilogue (two warps
-// per TMEM lane quadrant, alternating 32-column chunks).
+// Warps: 0 and 11 TMA producers (alternating stages), 1 MMA issuer + TMEM
+// owner, 2..9 epilogue (two warps per TMEM lane quadrant, alternating
+// 32-column chunks), 10 residual producer of the fused post-LN epilogue
+// (ln_epi.cuh; V2 with LN2 only).
 #include "common.cuh"
 #include "kernels.cuh"
+#include "ln_epi.cuh"
 #include "ptx.cuh"
 
 namespace fsvd {
@@ -37,7 +40,7 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kThreads = 320;
+constexpr int kThreads = 384;
 constexpr int kEpi = 256;
 constexpr int BMr = 128;         // token rows per CTA
 constexpr int BF = 128;          // features per block
@@ -66,6 +69,7 @@ struct FfnBars {
   uint64_t x_full[2], x_empty[2];
   uint64_t p_full, p_acc, p_ready, h_full, h_free, sh_full[2], sh_free[2], z_full, zs_ready;
   uint64_t o_full[2], o_free[2];
+  uint64_t res_full[2], res_empty[2];  // residual boxes of the fused LN2 (H region)
   uint32_t tmem;
 };
 
@@ -117,8 +121,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const __grid_constant__ CUtensorMap tmVup,  // V_up^T [df, FR] box 128x64
           const __grid_constant__ CUtensorMap tmUdn,  // U_dn^T [FR, df] box PSx64
           const __grid_constant__ CUtensorMap tmVdn,  // V_dn^T [d, FR]  box QSx64
+          const __grid_constant__ CUtensorMap tmY,    // out [T, d]      box 128x64 (fused LN)
           const float* __restrict__ b_up, const float* __restrict__ b_dn, int act, int T,
-          int d_model, int d_ff, bf16* __restrict__ z_out, bf16* __restrict__ out) {
+          int d_model, int d_ff, bf16* __restrict__ z_out, bf16* __restrict__ out,
+          const float* __restrict__ ln_g, const float* __restrict__ ln_b, float ln_eps) {
   using C = FfnCfg<FR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -128,7 +134,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int m0 = blockIdx.x * BMr;
   const int NB = (d_ff + BF - 1) / BF;
   const int KC = d_model / 64;                        // X K-chunks (FUSED)
-  const int QS = (d_model % 128 == 0) ? 128 : 64;     // output columns per piece (FUSED)
+  const bool fuse_ln = FUSED && ln_g != nullptr;     // out = LN2(x + ffn(x)) (ln_epi.cuh)
+  const int QS = (d_model % 128 == 0 && !fuse_ln) ? 128 : 64;  // output columns per piece
   const int NQ = d_model / QS;
 
   if (threadIdx.x == 0) TRACE(0);
@@ -149,6 +156,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars->sh_free[i], 1);
       mbar_init(&bars->o_full[i], 1);
       mbar_init(&bars->o_free[i], kEpi);
+      mbar_init(&bars->res_full[i], 1);
+      mbar_init(&bars->res_empty[i], kEpi);
     }
     mbar_init(&bars->p_full, 1);
     mbar_init(&bars->p_acc, 1);
@@ -166,21 +175,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = bars->tmem;
   uint8_t* ring = smem + C::o_ring;
 
-  if (warp == 0) {
-    // ================================================= TMA producer (one thread)
+  if (warp == 0 || warp == 11) {
+    // ================================================= TMA producers
+    // One thread in each of warps 0 and 11, alternating ring stages: a TMA
+    // instruction holds its issuing thread for ~250 cycles whatever the box
+    // size (tests/cuda/tma_probe.cu), one issuer cannot feed the MMA.
     if (lane == 0) {
-      uint32_t st = 0, ph = 0;
+      const uint32_t me = warp == 0 ? 0 : 1;
+      uint32_t st = 0, ph = 0, it = 0;
       // Streams n slots, two per stage.  slot(i, dst, size_only) returns the
       // byte count of slot i and, unless size_only, issues its TMA.
       auto emit = [&](int n, auto&& slot) {
-        for (int i = 0; i < n; i += 2) {
-          mbar_wait(&bars->empty[st], ph ^ 1);
-          uint8_t* base = ring + st * STAGE;
-          uint32_t bytes = slot(i, base, true);
-          if (i + 1 < n) bytes += slot(i + 1, base + SLOT, true);
-          mbar_arrive_expect_tx(&bars->full[st], bytes);
-          slot(i, base, false);
-          if (i + 1 < n) slot(i + 1, base + SLOT, false);
+        for (int i = 0; i < n; i += 2, ++it) {
+          if ((it & 1) == me) {
+            mbar_wait(&bars->empty[st], ph ^ 1);
+            uint8_t* base = ring + st * STAGE;
+            uint32_t bytes = slot(i, base, true);
+            if (i + 1 < n) bytes += slot(i + 1, base + SLOT, true);
+            mbar_arrive_expect_tx(&bars->full[st], bytes);
+            slot(i, base, false);
+            if (i + 1 < n) slot(i + 1, base + SLOT, false);
+          }
           if (++st == C::STAGES) { st = 0; ph ^= 1; }
         }
       };
@@ -201,17 +216,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (FUSED) {
         for (int kc = 0; kc < KC; ++kc) {
           const int xb = kc & 1;
-          mbar_wait(&bars->x_empty[xb], ((kc >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(&bars->x_full[xb], SLOT);
-          tma_load_2d(&tmX, &bars->x_full[xb], smem + C::o_h + xb * SLOT, kc * 64, m0);
+          if (static_cast<uint32_t>(xb) == me) {
+            mbar_wait(&bars->x_empty[xb], ((kc >> 1) & 1) ^ 1);
+            mbar_arrive_expect_tx(&bars->x_full[xb], SLOT);
+            tma_load_2d(&tmX, &bars->x_full[xb], smem + C::o_h + xb * SLOT, kc * 64, m0);
+          }
           emit(C::NPIECE, [&](int p, uint8_t* dst, bool size_only) -> uint32_t {
             if (!size_only) tma_load_2d(&tmUup, &bars->full[st], dst, kc * 64, p * C::PS);
             return C::PS * 128;
           });
         }
       } else {
-        mbar_arrive_expect_tx(&bars->p_full, C::NATOM * SLOT);
-        for (int a = 0; a < C::NATOM; ++a)
+        if (me == 0) mbar_arrive_expect_tx(&bars->p_full, C::NATOM * SLOT);
+        for (int a = me; a < C::NATOM; a += 2)
           tma_load_2d(&tmP, &bars->p_full, smem + C::o_p + a * SLOT, a * 64, m0);
       }
       TRACE(2);
@@ -225,50 +242,75 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (FUSED) {
         for (int q = 0; q < NQ; ++q)
           emit(C::NATOM, [&](int a, uint8_t* dst, bool size_only) -> uint32_t {
-            if (!size_only) tma_load_2d(&tmVdn, &bars->full[st], dst, a * 64, q * QS);
+            if (!size_only)
+              tma_load_2d(&tmVdn, &bars->full[st], dst, a * 64,
+                          (fuse_ln ? lnepi::piece_of(q, NQ) : q) * QS);
             return QS * 128;
           });
       }
     }
     __syncwarp();
+  } else if (warp == 10) {
+    // ================================================= residual producer (fused LN2)
+    // The H tile is idle once every MMA2 has completed (z_full); the residual
+    // (= this tile of X) streams through it as two [128 x 64] boxes.
+    if (fuse_ln && lane == 0) {
+      mbar_wait(&bars->z_full, 0);
+      lnepi::produce_residual(&tmX, smem + C::o_h, bars->res_full, bars->res_empty, 2, d_model,
+                              m0);
+    }
+    __syncwarp();
   } else if (warp == 1) {
-    // ================================================= MMA issuer (one thread)
-    if (lane == 0) {
+    // ================================================= MMA issuer
+    // Warp-uniform loop (descriptors stay in uniform registers, ~1 issue
+    // slot per MMA); one elected lane issues and commits.
+    {
       uint32_t st = 0, ph = 0;
       const uint64_t dhi = desc_hi_kmajor(128);
-      const uint32_t s_p = smem_u32(smem + C::o_p), s_h = smem_u32(smem + C::o_h);
-      const uint32_t s_ring = smem_u32(ring);
-      // Consumes n slots two per stage: fn(i, slot_addr) issues slot i's MMAs;
+      const uint64_t d_p = desc_at(dhi, smem_u32(smem + C::o_p));
+      const uint64_t d_h = desc_at(dhi, smem_u32(smem + C::o_h));
+      const uint64_t d_ring = desc_at(dhi, smem_u32(ring));
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one()) mma_commit(bar);
+        __syncwarp();
+      };
+      // Consumes n slots two per stage: fn(i, slot_desc) issues slot i's MMAs;
       // each stage is released once its MMAs have been issued.
       auto consume = [&](int n, auto&& fn) {
         for (int i = 0; i < n; i += 2) {
           mbar_wait(&bars->full[st], ph);
           tc_fence_after();
-          const uint32_t base = s_ring + st * STAGE;
+          const uint64_t base = d_ring + ((st * STAGE) >> 4);
           fn(i, base);
-          if (i + 1 < n) fn(i + 1, base + SLOT);
-          mma_commit(&bars->empty[st]);
+          if (i + 1 < n) fn(i + 1, base + (SLOT >> 4));
+          commit(&bars->empty[st]);
           if (++st == C::STAGES) { st = 0; ph ^= 1; }
         }
       };
-      auto mma4 = [&](uint32_t d, uint32_t a, uint32_t b, uint32_t idesc, bool acc0) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          mma_bf16_ss(d, desc_at(dhi, a + k * 32), desc_at(dhi, b + k * 32), idesc,
-                      (acc0 || k != 0) ? 1u : 0u);
+      // 4 K-steps of 16 over one 64-wide SW128 atom (start address += 32 B)
+      auto mma4 = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, bool acc0) {
+        if (elect_one()) {
+          mma_bf16_ss(d, a, b, idesc, acc0 ? 1u : 0u);
+          mma_bf16_ss(d, a + 2, b + 2, idesc, 1u);
+          mma_bf16_ss(d, a + 4, b + 4, idesc, 1u);
+          mma_bf16_ss(d, a + 6, b + 6, idesc, 1u);
+        }
+        __syncwarp();
       };
+      constexpr uint32_t kAtom = SLOT >> 4;  // one [128 x 64] atom in descriptor units
       if (FUSED) {
         // P = X U_up into the Z columns of TMEM
         for (int kc = 0; kc < KC; ++kc) {
           const int xb = kc & 1;
           mbar_wait(&bars->x_full[xb], (kc >> 1) & 1);
           tc_fence_after();
-          consume(C::NPIECE, [&](int p, uint32_t slot) {
-            mma4(tmem + C::t_z + p * C::PS, s_h + xb * SLOT, slot, idesc_bf16(128, C::PS), kc != 0);
+          consume(C::NPIECE, [&](int p, uint64_t slot) {
+            mma4(tmem + C::t_z + p * C::PS, d_h + xb * kAtom, slot, idesc_bf16(128, C::PS),
+                 kc != 0);
           });
-          mma_commit(&bars->x_empty[xb]);
+          commit(&bars->x_empty[xb]);
         }
-        mma_commit(&bars->p_acc);
+        commit(&bars->p_acc);
         TRACE(3);
         mbar_wait(&bars->p_ready, 0);
         TRACE(4);
@@ -283,14 +325,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
         }
         TRACE(64 + f * 8 + 1);
-        consume(C::NATOM, [&](int a, uint32_t slot) {
-          mma4(tmem + C::t_h, s_p + a * SLOT, slot, idesc_bf16(128, BF), a != 0);
+        consume(C::NATOM, [&](int a, uint64_t slot) {
+          mma4(tmem + C::t_h, d_p + a * kAtom, slot, idesc_bf16(128, BF), a != 0);
         });
-        mma_commit(&bars->h_full);
+        commit(&bars->h_full);
         TRACE(64 + f * 8 + 2);
       };
       auto mma2 = [&](int f) {
-        consume(2 * C::NPIECE, [&](int j, uint32_t slot) {
+        consume(2 * C::NPIECE, [&](int j, uint64_t slot) {
           const int a = j / C::NPIECE, p = j % C::NPIECE;
           if (p == 0) {
             TRACE(64 + f * 8 + 3 + a * 2);
@@ -298,9 +340,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             TRACE(64 + f * 8 + 4 + a * 2);
           }
-          mma4(tmem + C::t_z + p * C::PS, s_h + a * SLOT, slot, idesc_bf16(128, C::PS),
+          mma4(tmem + C::t_z + p * C::PS, d_h + a * kAtom, slot, idesc_bf16(128, C::PS),
                (f | a) != 0);
-          if (p == C::NPIECE - 1) mma_commit(&bars->sh_free[a]);
+          if (p == C::NPIECE - 1) commit(&bars->sh_free[a]);
         });
       };
       mma1(0);
@@ -308,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (f + 1 < NB) mma1(f + 1);
         mma2(f);
       }
-      mma_commit(&bars->z_full);
+      commit(&bars->z_full);
       if (FUSED) {
         mbar_wait(&bars->zs_ready, 0);
         tc_fence_after();
@@ -317,14 +359,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&bars->o_free[q & 1], ((q >> 1) - 1) & 1);
             tc_fence_after();
           }
-          consume(C::NATOM, [&](int a, uint32_t slot) {
-            mma4(tmem + (q & 1) * 128, s_p + a * SLOT, slot, idesc_bf16(128, QS), a != 0);
+          const uint32_t idq = QS == 128 ? idesc_bf16(128, 128) : idesc_bf16(128, 64);
+          consume(C::NATOM, [&](int a, uint64_t slot) {
+            mma4(tmem + (q & 1) * QS, d_p + a * kAtom, slot, idq, a != 0);
           });
-          mma_commit(&bars->o_full[q & 1]);
+          commit(&bars->o_full[q & 1]);
         }
       }
     }
-    __syncwarp();
   } else {
     // ================================================= epilogue (8 warps)
     const uint32_t quad = warp & 3;
@@ -363,9 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&bars->h_free);
 #pragma unroll
       for (int i = 0; i < 2; ++i) {  // i = K atom of the H block
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[i][j] += bb[i][j];
-        act_chunk<32>(v[i], act);
+        bias_act_chunk2<32>(v[i], bb[i], act);
         if (threadIdx.x == 64) TRACE(1024 + f * 8 + 2 + i * 2);
         if (f > 0) mbar_wait(&bars->sh_free[i], (f - 1) & 1);
         if (threadIdx.x == 64) TRACE(1024 + f * 8 + 3 + i * 2);
@@ -392,18 +432,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&bars->zs_ready);
-      for (int q = 0; q < NQ; ++q) {
-        mbar_wait(&bars->o_full[q & 1], (q >> 1) & 1);
-        tc_fence_after();
-        for (int c = half; c < QS / 32; c += 2) {
-          float v[32];
-          ld_chunk(tmem + (q & 1) * 128 + loff + c * 32, v);
-          const int n0 = q * QS + c * 32;
-          bias_act_chunk<32>(v, b_dn + n0, 32, 3);
-          if (grow < T) st_chunk_global(out + (int64_t)grow * d_model + n0, v);
+      if (fuse_ln) {
+        // residual = the FFN input x, streamed through the idle H tile
+        // gamma / beta are staged in the weight ring, idle once all MMAs are done
+        lnepi::run(tmem, quad, half, row, grow, T, d_model, b_dn, smem_u32(smem + C::o_h),
+                   bars->res_full, bars->res_empty, 2, ln_g, ln_b, ln_eps, &tmY, m0,
+                   reinterpret_cast<float*>(ring), bars->o_full, bars->o_free, 1);
+      } else {
+        for (int q = 0; q < NQ; ++q) {
+          mbar_wait(&bars->o_full[q & 1], (q >> 1) & 1);
+          tc_fence_after();
+          for (int c = half; c < QS / 32; c += 2) {
+            float v[32];
+            ld_chunk(tmem + (q & 1) * QS + loff + c * 32, v);
+            const int n0 = q * QS + c * 32;
+            bias_act_chunk<32>(v, b_dn + n0, 32, 3);
+            if (grow < T) st_chunk_global(out + (int64_t)grow * d_model + n0, v);
+          }
+          tc_fence_before();
+          mbar_arrive(&bars->o_free[q & 1]);
         }
-        tc_fence_before();
-        mbar_arrive(&bars->o_free[q & 1]);
       }
     }
   }
@@ -430,15 +478,18 @@ void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
   const CUtensorMap tup = tmap_bf16(a.up_u_t, FR, a.d_model, a.d_model, boxp, 64, TmaSwizzle::B128);
   const CUtensorMap tvup = tmap_bf16(a.up_v_t, a.d_ff, FR, FR, BF, 64, TmaSwizzle::B128);
   const CUtensorMap tudn = tmap_bf16(a.dn_u_t, FR, a.d_ff, a.d_ff, boxp, 64, TmaSwizzle::B128);
-  const CUtensorMap tvdn = tmap_bf16(a.dn_v_t, a.d_model, FR, FR, boxd, 64, TmaSwizzle::B128);
-  CUtensorMap tx = tvup, tp = tvup;
+  const CUtensorMap tvdn = tmap_bf16(a.dn_v_t, a.d_model, FR, FR, FUSED && a.ln_g ? 64 : boxd, 64,
+                                     TmaSwizzle::B128);
+  CUtensorMap tx = tvup, tp = tvup, ty = tvup;
+  if (FUSED && a.ln_g) ty = tmap_bf16(a.out, a.T, a.d_model, a.d_model, 128, 64, TmaSwizzle::B128);
   if (FUSED)
     tx = tmap_bf16(a.x, a.T, a.d_model, a.d_model, 128, 64, TmaSwizzle::B128);
   else
     tp = tmap_bf16(a.p_in, a.T, FR, FR, 128, 64, TmaSwizzle::B128);
   const int grid = (a.T + BMr - 1) / BMr;
-  k_ffn<FR, FUSED><<<grid, kThreads, C::SMEM, s>>>(tx, tp, tup, tvup, tudn, tvdn, a.up_b, a.dn_b,
-                                                   a.act, a.T, a.d_model, a.d_ff, a.z_out, a.out);
+  k_ffn<FR, FUSED><<<grid, kThreads, C::SMEM, s>>>(tx, tp, tup, tvup, tudn, tvdn, ty, a.up_b, a.dn_b,
+                                                   a.act, a.T, a.d_model, a.d_ff, a.z_out, a.out,
+                                                   a.ln_g, a.ln_b, a.ln_eps);
   check_launch(FUSED ? "k_ffn_fused" : "k_ffn_stream");
 }
 

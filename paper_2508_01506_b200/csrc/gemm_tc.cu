@@ -9,8 +9,9 @@
 // which equals the reference's bias preload up to fp32 rounding order.
 //
 // Structure (one CTA per SM, persistent over 128 x BN output tiles):
-//   warp 0      TMA producer: A [128 x 64] and B [BN x 64] bf16 tiles (SW128)
-//               into a STAGES-deep smem ring guarded by full/empty mbarriers.
+//   warps 0, 6  TMA producers (alternate stages): A [128 x 64] and B [BN x 64]
+//               bf16 tiles (SW128) into a STAGES-deep smem ring guarded by
+//               full/empty mbarriers.
 //   warp 1      MMA issuer: one elected lane issues tcgen05.mma (M=128,
 //               N=BN, K=16) into one of two TMEM accumulators.
 //   warps 2..5  epilogue: tcgen05.ld 32 columns at a time, bias + act,
@@ -28,7 +29,7 @@ using namespace ptx;
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;  // 0 TMA, 1 MMA, 2..5 epilogue, 6 TMA
 
 template <int BN, int STAGES>
 struct GemmCfg {
@@ -82,28 +83,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ---------------- TMA producer (one thread) ----------------
+  if (warp == 0 || warp == kThreads / 32 - 1) {
+    // ---------------- TMA producers (one thread in each of two warps) ----------------
+    // A TMA instruction occupies its issuing thread for ~250 cycles whatever
+    // the box size (tests/cuda/tma_probe.cu), so two issuers alternate stages.
     if (lane == 0) {
+      const int me = warp == 0 ? 0 : 1;
       uint32_t stage = 0, phase = 0;
+      int it = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
-          tma_load_2d(&tmA, &full[stage], sA + stage * Cfg::A_BYTES, kb * BK, m0);
-          tma_load_2d(&tmB, &full[stage], sB + stage * Cfg::B_BYTES, kb * BK, n0);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          if ((it & 1) == me) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+            tma_load_2d(&tmA, &full[stage], sA + stage * Cfg::A_BYTES, kb * BK, m0);
+            tma_load_2d(&tmB, &full[stage], sB + stage * Cfg::B_BYTES, kb * BK, n0);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one thread, descriptors precomputed) ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer (warp-uniform loop, one elected lane issues) ----------------
+    {
       constexpr uint32_t idesc = idesc_bf16(BM, BN);
       const uint64_t dhi = desc_hi_kmajor(128);
-      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+      const uint64_t da = desc_at(dhi, smem_u32(sA)), db = desc_at(dhi, smem_u32(sB));
       uint32_t stage = 0, phase = 0;
       int i = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
@@ -114,18 +121,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = a_base + stage * Cfg::A_BYTES, b0 = b_base + stage * Cfg::B_BYTES;
+          const uint64_t a0 = da + ((stage * Cfg::A_BYTES) >> 4);
+          const uint64_t b0 = db + ((stage * Cfg::B_BYTES) >> 4);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            mma_bf16_ss(d, desc_at(dhi, a0 + k * 32), desc_at(dhi, b0 + k * 32), idesc,
-                        (kb | k) != 0);
-          mma_commit(&empty[stage]);
+            for (int k = 0; k < BK / 16; ++k)
+              mma_bf16_ss(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
+            mma_commit(&empty[stage]);
+          }
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[acc]);
+        if (elect_one()) mma_commit(&tfull[acc]);
+        __syncwarp();
       }
     }
-    __syncwarp();
   } else {
     // ---------------- epilogue ----------------
     const uint32_t q = warp & 3;  // TMEM lane quadrant of this warp

@@ -6,6 +6,7 @@
 //   K3 ffn_stream         FlashSVD-FFN feature-block stream (V1 middle)
 //   K4 ffn_fused          FlashSVD-FFN V2, fully fused per 128-row tile
 //   K5 resid_layernorm    residual + LayerNorm row kernel
+//   K6 gemm_ln            projection GEMM with residual + LayerNorm epilogue
 // SIMT kernels (fp32 policy and shapes outside the tensor-core tiling):
 //   simt_gemm, simt_attention, simt_ffn_stream, resid_layernorm (fp32)
 #pragma once
@@ -25,6 +26,13 @@ enum Act : int { ACT_GELU_ERF = 0, ACT_GELU_TANH = 1, ACT_RELU = 2, ACT_NONE = 3
 void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, int64_t ldc,
                int M, int N, int K, const float* bias, int act, cudaStream_t s);
 bool gemm_bf16_supported(int M, int N, int K, int64_t lda, int64_t ldb, int64_t ldc);
+
+// ---- K6: y = LN(resid + bf16(A[T,K] * B[N,K]^T + bias)) * gamma + beta --------
+// One CTA per 128 complete rows; N <= 768, K <= 512, multiples of 64.
+void gemm_ln_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, const float* bias,
+                  const bf16* resid, const float* gamma, const float* beta, float eps, bf16* y,
+                  int T, int N, int K, cudaStream_t s);
+bool gemm_ln_supported(int N, int K);
 
 // ---- K2: rank-space FlashSVD attention --------------------------------------
 // out[t, h*rp : (h+1)*rp] = softmax(Qt_h K_g^T) V_g for each (sequence, head),
@@ -57,6 +65,11 @@ struct FfnTcArgs {
   const bf16* p_in;    // [T, fr]   (V1: P = X U_up)
   bf16* z_out;         // [T, fr]   (V1: Z)
   bf16* out;           // [T, d_model] (V2)
+  // V2 only: when ln_g != null, out = LN(x + ffn(x)) * ln_g + ln_b (post-LN
+  // residual + LayerNorm fused into the epilogue; d_model <= 768).
+  const float* ln_g;
+  const float* ln_b;
+  float ln_eps;
 };
 void ffn_stream_bf16(const FfnTcArgs& a, cudaStream_t s);   // V1 middle: P -> Z
 void ffn_fused_bf16(const FfnTcArgs& a, cudaStream_t s);    // V2: X -> out

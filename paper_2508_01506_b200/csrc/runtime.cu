@@ -596,6 +596,57 @@ void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* o
   }
 }
 
+// out = LN2(x + FFN(x)) with the residual + LayerNorm fused into the FFN's
+// last GEMM (V2: the fused kernel's epilogue; V1: the Z V_down GEMM).
+// Returns false when the shape is outside the fused kernels' range.
+bool ffn_ln_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* out,
+                void* trans, cudaStream_t s) {
+  const int T = static_cast<int>(B * M), d = p.d;
+  if (!p.ffn_tc || !gemm_ln_supported(d, p.frp)) return false;
+  if (mode == FSVD_MODE_FLASH_V2) {
+    FfnTcArgs a{};
+    a.T = T;
+    a.d_model = d;
+    a.d_ff = p.df;
+    a.rank_pad = p.frp;
+    a.x = as<bf16>(x);
+    a.up_u_t = as<bf16>(p.uup_t);
+    a.up_v_t = as<bf16>(p.vup_t);
+    a.up_b = p.bup;
+    a.dn_u_t = as<bf16>(p.udn_t);
+    a.dn_v_t = as<bf16>(p.vdn_t);
+    a.dn_b = p.bdn;
+    a.act = p.act;
+    a.out = as<bf16>(out);
+    a.ln_g = p.ln2g;
+    a.ln_b = p.ln2b;
+    a.ln_eps = p.eps2;
+    ffn_fused_bf16(a, s);
+    return true;
+  }
+  if (mode != FSVD_MODE_FLASH_V1) return false;
+  FfnTcArgs a{};
+  a.T = T;
+  a.d_model = d;
+  a.d_ff = p.df;
+  a.rank_pad = p.frp;
+  a.up_v_t = as<bf16>(p.vup_t);
+  a.up_b = p.bup;
+  a.dn_u_t = as<bf16>(p.udn_t);
+  a.dn_v_t = as<bf16>(p.vdn_t);
+  a.dn_b = p.bdn;
+  a.act = p.act;
+  bf16* P = as<bf16>(trans);
+  bf16* Z = P + (size_t)T * p.frp;
+  gemm_bf16(as<bf16>(x), d, as<bf16>(p.uup_t), d, P, p.frp, T, p.frp, d, nullptr, ACT_NONE, s);
+  a.p_in = P;
+  a.z_out = Z;
+  ffn_stream_bf16(a, s);
+  gemm_ln_bf16(Z, p.frp, a.dn_v_t, p.frp, p.bdn, as<bf16>(x), p.ln2g, p.ln2b, p.eps2,
+               as<bf16>(out), T, d, p.frp, s);
+  return true;
+}
+
 void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const void* x, void* out,
                void* ws, size_t ws_bytes, cudaStream_t s) {
   const size_t T = B * M;
@@ -608,7 +659,17 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
   void* Bb = base + act_bytes;
   void* trans = base + 2 * act_bytes;
   const int rows = static_cast<int>(T);
-  if (!pre_ln) {
+  const bool flash = mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2;
+  if (!pre_ln && flash && p.attn_tc && p.out_tc && gemm_ln_supported(p.d, p.H * p.rp)) {
+    // rank-space attention -> A; folded out-projection + residual + LN1 -> B
+    tc_attention_rank(p, B, M, x, A, trans, s);
+    gemm_ln_bf16(as<bf16>(A), p.H * p.rp, as<bf16>(p.wov_t), p.H * p.rp, p.bov, as<bf16>(x),
+                 p.ln1g, p.ln1b, p.eps1, as<bf16>(Bb), rows, p.d, p.H * p.rp, s);
+    if (!ffn_ln_fwd(p, mode, B, M, Bb, out, trans, s)) {              // out = LN2(B + ffn(B))
+      ffn_fwd(p, mode, B, M, Bb, A, trans, s);
+      ln(p, Bb, A, p.ln2g, p.ln2b, p.eps2, out, rows, s);
+    }
+  } else if (!pre_ln) {
     attention_block(p, mode, B, M, x, A, Bb, trans, s);               // branch -> B
     ln(p, x, Bb, p.ln1g, p.ln1b, p.eps1, Bb, rows, s);                // resid  -> B (in place)
     ffn_fwd(p, mode, B, M, Bb, A, trans, s);                          // ffn    -> A

@@ -59,7 +59,20 @@ __global__ void __launch_bounds__(128, 1) k_probe(int n, int iters, int sync_eve
     uint32_t phase = 0;
     long long t0 = clock64();
     const bool leader = use_elect ? elect_one() : (lane == 0);
-    if (use_elect == 4) {
+    if (use_elect == 5 || use_elect == 6) {
+      // warp-uniform loop, precomputed descriptors; 5: one elect per 4 MMAs,
+      // 6: one elect per 16 MMAs
+      const uint64_t ad = desc_kmajor(a, 128), bd = desc_kmajor(b, 128);
+      const int per = use_elect == 5 ? 4 : 16;
+      for (int i = 0; i < iters; i += per) {
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (k < per) mma_bf16_ss(tmem, ad + 2 * (k & 3), bd + 2 * (k & 3), idesc, 1);
+        }
+        __syncwarp();
+      }
+    } else if (use_elect == 4) {
       if (lane == 0) {
         uint64_t ad[4], bd[4];
 #pragma unroll
@@ -152,9 +165,9 @@ int main() {
   long long* d;
   cudaMalloc(&d, blocks * sizeof(long long));
   std::vector<long long> h(blocks);
-  for (int el : {3, 4})
-  for (int mode : {0, 1, 2})
-  for (int sync : {0, 4, 16}) {
+  for (int el : {4, 5, 6})
+  for (int mode : {0})
+  for (int sync : {0}) {
     if (sync == 0 && mode > 0) continue;
     for (int n : {32, 64, 128, 192, 256}) {
       const int iters = 4096;

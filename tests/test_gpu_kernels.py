@@ -1,0 +1,97 @@
+"""Per-kernel numerics on the GPU: each tensor-core kernel, called through the
+C-ABI test hooks on device buffers, against a plain PyTorch fp32 reference of
+the same op on the same bf16 inputs.  Tolerances are relative to max|ref| and
+account for the bf16 output rounding (2^-8) plus fp32 accumulation order."""
+import ctypes as C
+
+import pytest
+
+from paper_2508_01506_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    L = abi.lib()
+    if not L.fsvd_device_available():
+        pytest.skip("no sm_100 device")
+    return L, torch
+
+
+def _p(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def _rel(got, ref):
+    return float((got.float() - ref).abs().max() / ref.abs().max().clamp_min(1e-30))
+
+
+def _ln_ref(torch, s, g, b, eps):
+    mu = s.mean(-1, keepdim=True)
+    var = ((s - mu) ** 2).mean(-1, keepdim=True)
+    return g * ((s - mu) / torch.sqrt(var + eps)) + b
+
+
+@pytest.mark.parametrize("T,N,K", [(128, 768, 384), (260, 256, 128), (384, 768, 128),
+                                   (128, 256, 384), (1000, 512, 512), (4096, 768, 384),
+                                   (16384, 768, 384)])
+def test_gemm_ln_vs_torch(env, T, N, K):
+    L, torch = env
+    g = torch.Generator(device="cuda").manual_seed(T + N + K)
+    dev = "cuda"
+    A = (torch.randn(T, K, device=dev, generator=g) / K ** 0.5).bfloat16()
+    B = torch.randn(N, K, device=dev, generator=g).bfloat16()
+    bias = torch.randn(N, device=dev, generator=g) * 0.02
+    R = torch.randn(T, N, device=dev, generator=g).bfloat16()
+    gam = 1 + 0.1 * torch.randn(N, device=dev, generator=g)
+    bet = 0.02 * torch.randn(N, device=dev, generator=g)
+    y = torch.empty(T, N, device=dev, dtype=torch.bfloat16)
+    s = torch.cuda.current_stream().cuda_stream
+    abi.check(L.fsvd_test_gemm_ln(_p(A), K, _p(B), K, _p(bias), _p(R), _p(gam), _p(bet), 1e-5,
+                                  _p(y), T, N, K, C.c_void_p(s)))
+    torch.cuda.synchronize()
+    branch = (A.float() @ B.float().t() + bias).bfloat16().float()  # the unfused stored value
+    ref = _ln_ref(torch, branch + R.float(), gam, bet, 1e-5)
+    assert _rel(y, ref) < 1.5e-2
+
+
+@pytest.mark.parametrize("M,N,K,act", [(16384, 1152, 768, None), (16384, 768, 384, None),
+                                       (333, 200, 72, 0), (4096, 3072, 384, 1), (128, 64, 64, 2)])
+def test_gemm_vs_torch(env, M, N, K, act):
+    L, torch = env
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = (torch.randn(M, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    B = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g) * 0.1
+    Cm = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    s = torch.cuda.current_stream().cuda_stream
+    abi.check(L.fsvd_test_gemm(_p(A), K, _p(B), K, _p(Cm), N, M, N, K, _p(bias),
+                               act if act is not None else 0, act is not None, C.c_void_p(s)))
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t() + bias
+    if act == 0:
+        ref = torch.nn.functional.gelu(ref)
+    elif act == 1:
+        ref = torch.nn.functional.gelu(ref, approximate="tanh")
+    elif act == 2:
+        ref = torch.relu(ref)
+    assert _rel(Cm, ref) < 1e-2
+
+
+@pytest.mark.parametrize("rows,d", [(16384, 768), (77, 1024), (5, 256)])
+def test_resid_layernorm_vs_torch(env, rows, d):
+    L, torch = env
+    g = torch.Generator(device="cuda").manual_seed(rows + d)
+    a = torch.randn(rows, d, device="cuda", generator=g).bfloat16()
+    b = torch.randn(rows, d, device="cuda", generator=g).bfloat16()
+    gam = 1 + 0.1 * torch.randn(d, device="cuda", generator=g)
+    bet = 0.02 * torch.randn(d, device="cuda", generator=g)
+    y = torch.empty_like(a)
+    s = torch.cuda.current_stream().cuda_stream
+    abi.check(L.fsvd_test_resid_layernorm(_p(a), _p(b), _p(gam), _p(bet), 1e-5, _p(y), rows, d,
+                                          C.c_void_p(s)))
+    torch.cuda.synchronize()
+    ref = _ln_ref(torch, a.float() + b.float(), gam, bet, 1e-5)
+    assert _rel(y, ref) < 1e-2

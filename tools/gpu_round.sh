@@ -13,9 +13,11 @@ fi
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 echo "bench rc=$?" >> gpurun_out/bench.err
 timeout 300 python tests/cuda/ffn_bench.py > gpurun_out/ffn_bench.txt 2>&1
+if [ "${NCU:-1}" = 0 ]; then echo done; exit 0; fi
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline \
   > gpurun_out/b_ncu.log 2>&1
+if [ "${NCU:-1}" = 1 ]; then echo done; exit 0; fi
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ffn -s 2 -c 1 \
   -o gpurun_out/prof_ffn -f python bench.py --steps 1 --warmup 1 --layers 1 --no-cpu-baseline \
   > gpurun_out/prof_ffn.log 2>&1
