@@ -299,6 +299,13 @@ fsvd_status fsvd_test_gemm_ln(const void* A, size_t lda, const void* B, size_t l
                               const float* bias, const void* resid, const float* gamma,
                               const float* beta, float eps, void* y, size_t T, size_t N,
                               size_t K, void* stream);
+/* K2: out[t, h*rp:(h+1)*rp] = softmax2(Qt_h K_g^T) V_g per sequence, rank
+ * space; qkv [batch*seq, cols] holds head h's Qt at q_off + h*rp, group g's K
+ * at k_off + g*rp and V at v_off + g*rp; scores are in the log2 domain. */
+fsvd_status fsvd_test_attention(const void* qkv, size_t cols, size_t q_off, size_t k_off,
+                                size_t v_off, size_t batch, size_t seq, size_t heads,
+                                size_t groups, size_t rank_pad, void* out, size_t ldo,
+                                void* stream);
 /* K5: y = LN(a (+ b)) * gamma + beta */
 fsvd_status fsvd_test_resid_layernorm(const void* a, const void* b, const float* gamma,
                                       const float* beta, float eps, void* y, size_t rows,

@@ -142,6 +142,7 @@ def _declare(lib):
         "fsvd_test_gemm_ln": (st, [vp, _sz, vp, _sz, vp, vp, vp, vp, C.c_float, vp, _sz, _sz,
                                    _sz, vp]),
         "fsvd_test_resid_layernorm": (st, [vp, vp, vp, vp, C.c_float, vp, _sz, _sz, vp]),
+        "fsvd_test_attention": (st, [vp, _sz, _sz, _sz, _sz, _sz, _sz, _sz, _sz, _sz, vp, _sz, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

@@ -24,9 +24,11 @@
 // It is also the dense-attention kernel of the materializing baselines: with
 // r = head_dim and Q/K/V as its three inputs it computes softmax(Q K^T) V.
 //
-// CTA = one (batch, head, 128-row query tile); 6 warps: 0-3 softmax (thread
-// = query row, TMEM lane quadrant warp%4), 4 TMA producer, 5 MMA issuer and
-// TMEM owner.  ~90 KB smem and 256 TMEM columns, so two CTAs share an SM.
+// CTA = one (batch, head, 128-row query tile); 10 warps: 0-7 softmax (two
+// threads per query row, 64 keys each; TMEM lane quadrant warp%4), 8 TMA
+// producer, 9 MMA issuer and TMEM owner.  ~92 KB smem and 256 TMEM columns,
+// so two CTAs share an SM (16 softmax warps per SM to hide MUFU / TMEM
+// latency; the softmax is issue- and latency-bound, not exp-bound).
 #include "common.cuh"
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -38,8 +40,9 @@ using namespace ptx;
 
 constexpr int QT = 128;  // query rows per CTA
 constexpr int KT = 128;  // keys per tile
-constexpr int kThreads = 192;
-constexpr int kTma = 4, kMma = 5;
+constexpr int kThreads = 320;
+constexpr int kSoftmax = 256;  // warps 0-7: two per TMEM lane quadrant, 64 keys each
+constexpr int kTma = 8, kMma = 9;
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -47,7 +50,42 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (x <= 0): x = n + f with n = round(x) taken from the
+// mantissa of x + 1.5*2^23, f in [-0.5, 0.5]; 2^f by a degree-3 polynomial
+// (relative error 2.1e-4, far below the bf16 rounding of P), 2^n added to
+// the exponent field.  A share of the probabilities takes this path so the
+// softmax is not bound by the 16/clk/SM MUFU rate alone (EMU_EVERY: one
+// pair of probabilities in EMU_EVERY takes the polynomial).
+#ifndef EMU_EVERY
+#define EMU_EVERY 4
+#endif
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.0f);
+  x.y = fmaxf(x.y, -125.0f);
+  const float2 magic = make_float2(12582912.0f, 12582912.0f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 f = __fadd2_rn(x, __fadd2_rn(magic, make_float2(-t.x, -t.y)));
+  float2 p = __ffma2_rn(f, make_float2(0.054848f, 0.054848f), make_float2(0.24180661f, 0.24180661f));
+  p = __ffma2_rn(p, f, make_float2(0.6932482f, 0.6932482f));
+  p = __ffma2_rn(p, f, make_float2(0.9999887f, 0.9999887f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 __host__ __device__ constexpr int up1k(int x) { return (x + 1023) / 1024 * 1024; }
+
+#ifdef FSVD_TRACE
+__device__ long long g_trace_at[2048];
+}  // namespace
+extern "C" __attribute__((visibility("default"))) int fsvd_debug_trace_attn_copy(long long* host, int n) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace_at, sizeof(long long) * n));
+}
+namespace {
+// CTA (q-tile 0, head 0, batch 1) and its SM's clock
+#define ATRACE(slot) do { if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 1) g_trace_at[(slot)] = clock64(); } while (0)
+#else
+#define ATRACE(slot) do { } while (0)
+#endif
 
 template <int RP>
 struct AttnCfg {
@@ -60,7 +98,7 @@ struct AttnCfg {
   static constexpr int KV_STAGE = 2 * up1k(TILE);
   static constexpr int o_p = o_kv + STAGES * KV_STAGE;
   static constexpr int o_bar = o_p + SP;
-  static constexpr int SMEM = 1024 + o_bar + 256;
+  static constexpr int SMEM = 1024 + o_bar + 2304;  // Bars: barriers + 2 x [2][128] floats
   static constexpr int t_s = 0, t_o = 128;  // TMEM columns
   static_assert(SMEM <= 227 * 1024, "shared memory budget");  // RP <= 32: two CTAs / SM
 };
@@ -70,7 +108,10 @@ struct Bars {
   uint64_t kv_full[3], kv_empty[3];
   uint64_t s_full, s_free, p_full, o_full;
   uint32_t tmem;
+  float xmax[2][QT];  // per-half row maxima of the current tile
+  float xsum[2][QT];  // per-half row sums at the end
 };
+static_assert(sizeof(Bars) <= 2304, "Bars outgrew its shared-memory reservation");
 
 template <int RP>
 __global__ void __launch_bounds__(kThreads, 2)
@@ -97,11 +138,12 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(&bars->kv_empty[i], 1);
     }
     mbar_init(&bars->s_full, 1);
-    mbar_init(&bars->s_free, 128);
-    mbar_init(&bars->p_full, 128);
+    mbar_init(&bars->s_free, kSoftmax);
+    mbar_init(&bars->p_full, kSoftmax);
     mbar_init(&bars->o_full, 1);
     fence_barrier_init();
   }
+  if (threadIdx.x == 0) ATRACE(0);
   if (warp == kMma) tmem_alloc<256>(&bars->tmem);
   tc_fence_before();
   __syncthreads();
@@ -133,6 +175,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   } else if (warp == kMma) {
     // ------------------------------------------------ MMA issuer
     mbar_wait(&bars->pro, 0);
+    if (lane == 0) ATRACE(1);
     const uint64_t dq = desc_kmajor(s_q, C::RB);
     const uint64_t dk0 = desc_kmajor(s_kv, C::RB);
     const uint64_t dp0 = desc_kmajor(s_p, 128);
@@ -140,7 +183,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     auto issue_s = [&](int j) {
       const uint32_t st = j % C::STAGES;
       mbar_wait(&bars->kv_full[st], (j / C::STAGES) & 1);
+      if (lane == 0) ATRACE(16 + j);
       if (j > 0) mbar_wait(&bars->s_free, (j - 1) & 1);
+      if (lane == 0) ATRACE(48 + j);
       tc_fence_after();
       const uint64_t dk = dk0 + ((st * C::KV_STAGE) >> 4);
       if (elect_one()) {
@@ -155,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int j = 0; j < nj; ++j) {
       if (j + 1 < nj) issue_s(j + 1);
       mbar_wait(&bars->p_full, j & 1);
+      if (lane == 0) ATRACE(80 + j);
       tc_fence_after();
       const uint32_t st = j % C::STAGES;
       const uint64_t dv = dv0 + ((st * C::KV_STAGE) >> 4);
@@ -169,93 +215,115 @@ __global__ void __launch_bounds__(kThreads, 2)
       __syncwarp();
     }
   } else {
-    // ------------------------------------------------ softmax (4 warps)
-    const uint32_t quad = warp & 3;
+    // ------------------------------------------------ softmax (8 warps)
+    // Two threads per query row (warps w and w+4 share TMEM lane quadrant
+    // w%4); each owns 64 of the tile's 128 keys, and the pair exchanges its
+    // row maxima through shared memory (named barrier per quadrant).
+    const uint32_t quad = warp & 3, half = warp >> 2;
     const uint32_t row = quad * 32 + lane;
     const uint32_t tq = tmem + ((quad * 32) << 16);
+    constexpr int KH = KT / 2;  // keys per thread
+    // O columns owned by this thread for rescale / output (16-column granules)
+    constexpr int CH = RP >= 32 ? RP / 2 : RP;
+    const bool owns_o = RP >= 32 || half == 0;
+    const int oc0 = RP >= 32 ? static_cast<int>(half) * CH : 0;
     float m_run = -INFINITY, l_run = 0.0f;
 
     // O lives in TMEM and accumulates across key tiles; before PV_j it is
-    // rescaled by alpha_j here (tcgen05.ld/st are warp-collective).
+    // rescaled by alpha_j (each half of the pair rescales half of the columns).
     auto rescale_o = [&](float alpha) {
 #pragma unroll
-      for (int c = 0; c < RP; c += 16) {
+      for (int c = 0; c < CH; c += 16) {
         uint32_t r[16];
-        tmem_ld16(tq + C::t_o + c, r);
+        tmem_ld16(tq + C::t_o + oc0 + c, r);
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-        tmem_st16(tq + C::t_o + c, r);
+        tmem_st16(tq + C::t_o + oc0 + c, r);
       }
       tmem_st_wait();
     };
 
     for (int j = 0; j < nj; ++j) {
+      if (threadIdx.x == 0) ATRACE(112 + j);
       mbar_wait(&bars->s_full, j & 1);
+      if (threadIdx.x == 0) ATRACE(144 + j);
       tc_fence_after();
-      float s[KT];
+      float s[KH];
 #pragma unroll
-      for (int c = 0; c < KT; c += 32) {
+      for (int c = 0; c < KH; c += 32) {
         uint32_t r[32];
-        tmem_ld32(tq + C::t_s + c, r);
+        tmem_ld32(tq + C::t_s + half * KH + c, r);
 #pragma unroll
         for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(r[i]);
       }
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&bars->s_free);
-      const int valid = seq - j * KT;  // keys of this tile inside the sequence
-      if (valid < KT) {
+      const int valid = seq - j * KT - static_cast<int>(half) * KH;  // in-sequence keys here
+      if (valid < KH) {
 #pragma unroll
-        for (int i = 0; i < KT; ++i) s[i] = (i < valid) ? s[i] : -INFINITY;
+        for (int i = 0; i < KH; ++i) s[i] = (i < valid) ? s[i] : -INFINITY;
       }
       float mx[8];  // 8 independent max chains
 #pragma unroll
       for (int i = 0; i < 8; ++i) mx[i] = s[i];
 #pragma unroll
-      for (int i = 8; i < KT; ++i) mx[i & 7] = fmaxf(mx[i & 7], s[i]);
-      const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      for (int i = 8; i < KH; ++i) mx[i & 7] = fmaxf(mx[i & 7], s[i]);
+      float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      bars->xmax[half][row] = tmax;
+      named_bar_sync(1 + quad, 64);
+      tmax = fmaxf(tmax, bars->xmax[half ^ 1][row]);
       const float m_new = fmaxf(m_run, tmax);
       const float alpha = ex2(m_run - m_new);
       m_run = m_new;
-      uint32_t pk[KT / 2];
-      float part = 0.0f;
+      uint32_t pk[KH / 2];
+      float2 sum2 = make_float2(0.0f, 0.0f);
+      const float2 nm = make_float2(-m_new, -m_new);
 #pragma unroll
-      for (int c = 0; c < KT / 8; ++c) {
-        float p[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) p[i] = ex2(s[8 * c + i] - m_new);
-        part += ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
-#pragma unroll
-        for (int i = 0; i < 4; ++i) pk[4 * c + i] = pack_bf16(p[2 * i], p[2 * i + 1]);
+      for (int c = 0; c < KH / 2; ++c) {
+        const float2 d = __fadd2_rn(make_float2(s[2 * c], s[2 * c + 1]), nm);
+        // one pair in EMU_EVERY on the FMA pipe, the rest on MUFU
+        const float2 p = (c % EMU_EVERY == EMU_EVERY - 1) ? ex2_poly2(d)
+                                                          : make_float2(ex2(d.x), ex2(d.y));
+        sum2 = __fadd2_rn(sum2, p);
+        pk[c] = pack_bf16(p.x, p.y);
       }
-      l_run = fmaf(l_run, alpha, part);
+      l_run = fmaf(l_run, alpha, sum2.x + sum2.y);
       // single-buffered probability tile and O accumulator: PV_{j-1} must be done
       if (j >= 1) {
+        if (threadIdx.x == 0) ATRACE(176 + j);
         mbar_wait(&bars->o_full, (j - 1) & 1);
+        if (threadIdx.x == 0) ATRACE(208 + j);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.0f)) rescale_o(alpha);
+        if (owns_o && __any_sync(0xffffffffu, alpha != 1.0f)) rescale_o(alpha);
       }
+      // this half's 64 keys are exactly one [128 x 64] SW128 atom of P
 #pragma unroll
-      for (int c = 0; c < KT / 8; ++c)
-        st_shared_v4(s_p + (c >> 3) * (QT * 128) + swz_offset(row, c & 7, 128), pk[4 * c],
-                     pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      for (int c = 0; c < KH / 8; ++c)
+        st_shared_v4(s_p + half * (QT * 128) + swz_offset(row, c, 128), pk[4 * c], pk[4 * c + 1],
+                     pk[4 * c + 2], pk[4 * c + 3]);
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&bars->p_full);
+      if (threadIdx.x == 0) ATRACE(240 + j);
     }
+    bars->xsum[half][row] = l_run;
     mbar_wait(&bars->o_full, (nj - 1) & 1);
+    if (threadIdx.x == 0) ATRACE(2);
     tc_fence_after();
-    const float inv = 1.0f / l_run;
+    named_bar_sync(1 + quad, 64);
+    const float inv = 1.0f / (l_run + bars->xsum[half ^ 1][row]);
     const int qrow = q0 + static_cast<int>(row);
 #pragma unroll
-    for (int c = 0; c < RP; c += 16) {
+    for (int c = 0; c < CH; c += 16) {
+      if (!owns_o) break;
       uint32_t r[16];
-      tmem_ld16(tq + C::t_o + c, r);
+      tmem_ld16(tq + C::t_o + oc0 + c, r);
       tmem_ld_wait();
       if (qrow < seq) {
-        uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)(row0 + qrow) * ldo + h * RP + c);
+        uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)(row0 + qrow) * ldo + h * RP + oc0 + c);
 #pragma unroll
         for (int v = 0; v < 2; ++v)
           dst[v] = make_uint4(
@@ -266,6 +334,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
   }
+  if (threadIdx.x == 0) ATRACE(3);
   tc_fence_before();
   __syncthreads();
   if (warp == kMma) {

@@ -723,6 +723,31 @@ fsvd_status fsvd_test_gemm_ln(const void* A, size_t lda, const void* B, size_t l
                  (int)N, (int)K, static_cast<cudaStream_t>(stream));
   });
 }
+fsvd_status fsvd_test_attention(const void* qkv, size_t cols, size_t q_off, size_t k_off,
+                                size_t v_off, size_t batch, size_t seq, size_t heads,
+                                size_t groups, size_t rank_pad, void* out, size_t ldo,
+                                void* stream) {
+  return guard([&] {
+    require_device();
+    if (!attn_rankspace_supported((int)rank_pad) || heads % groups != 0)
+      fail(Kind::Config, "attention: unsupported shape");
+    AttnTcArgs a;
+    a.qkv = static_cast<const bf16*>(qkv);
+    a.ldq = (int64_t)cols;
+    a.qkv_cols = (int)cols;
+    a.q_off = (int)q_off;
+    a.k_off = (int)k_off;
+    a.v_off = (int)v_off;
+    a.batch = (int)batch;
+    a.seq = (int)seq;
+    a.heads = (int)heads;
+    a.groups = (int)groups;
+    a.rank_pad = (int)rank_pad;
+    a.out = static_cast<bf16*>(out);
+    a.ldo = (int64_t)ldo;
+    attn_rankspace_bf16(a, static_cast<cudaStream_t>(stream));
+  });
+}
 fsvd_status fsvd_test_resid_layernorm(const void* a, const void* b, const float* gamma,
                                       const float* beta, float eps, void* y, size_t rows,
                                       size_t d, void* stream) {

@@ -256,8 +256,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (= this tile of X) streams through it as two [128 x 64] boxes.
     if (fuse_ln && lane == 0) {
       mbar_wait(&bars->z_full, 0);
-      lnepi::produce_residual(&tmX, smem + C::o_h, bars->res_full, bars->res_empty, 2, d_model,
-                              m0);
+      lnepi::produce_residual<64>(&tmX, smem + C::o_h, bars->res_full, bars->res_empty, 2,
+                                  d_model, m0);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -435,9 +435,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (fuse_ln) {
         // residual = the FFN input x, streamed through the idle H tile
         // gamma / beta are staged in the weight ring, idle once all MMAs are done
-        lnepi::run(tmem, quad, half, row, grow, T, d_model, b_dn, smem_u32(smem + C::o_h),
-                   bars->res_full, bars->res_empty, 2, ln_g, ln_b, ln_eps, &tmY, m0,
-                   reinterpret_cast<float*>(ring), bars->o_full, bars->o_free, 1);
+        lnepi::run<64>(tmem, quad, half, row, d_model, b_dn, smem_u32(smem + C::o_h),
+                       bars->res_full, bars->res_empty, 2, ln_g, ln_b, ln_eps, &tmY, m0,
+                       reinterpret_cast<float*>(ring), bars->o_full, bars->o_free, 1);
       } else {
         for (int q = 0; q < NQ; ++q) {
           mbar_wait(&bars->o_full[q & 1], (q >> 1) & 1);

@@ -45,13 +45,13 @@ using namespace ptx;
 constexpr int kThreads = 384;
 constexpr int kEpi = 256;
 constexpr int BMr = 128;            // rows per CTA
-constexpr int PN = lnepi::PN;       // output columns per piece
+constexpr int PN = 128;             // output columns per piece (N = 128 MMAs)
 constexpr int ATOM = BMr * 128;     // [128 x 64] bf16 A atom (16 KB)
-constexpr int SLOT = PN * 128;      // [64 x 64] bf16 B slot (8 KB)
-constexpr int SPS = 2;              // slots per ring stage
+constexpr int SLOT = PN * 128;      // [128 x 64] bf16 B slot (16 KB)
+constexpr int SPS = 1;              // slots per ring stage
 constexpr int STAGE = SPS * SLOT;
 constexpr int kMaxStages = 10;
-constexpr int RS = 2;               // residual ring depth ([128 x 64] bf16 boxes)
+constexpr int RS = 4;               // residual ring depth ([128 x 64] bf16 boxes)
 constexpr int RBOX = BMr * 128;
 
 #ifdef FSVD_TRACE
@@ -67,7 +67,7 @@ namespace {
 
 struct LnBars {
   uint64_t full[kMaxStages], empty[kMaxStages];
-  uint64_t a_full, acc_full[2], acc_empty[2], res_full[RS], res_empty[RS];
+  uint64_t a_full, acc_full[1], acc_empty[1], res_full[RS], res_empty[RS];
   uint32_t tmem;
 };
 
@@ -101,13 +101,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars->empty[i], 1);
     }
     mbar_init(&bars->a_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars->acc_full[i], 1);
-      mbar_init(&bars->acc_empty[i], kEpi);
-    }
+    mbar_init(&bars->acc_full[0], 1);
+    mbar_init(&bars->acc_empty[0], kEpi);
     for (int i = 0; i < RS; ++i) {
       mbar_init(&bars->res_full[i], 1);
-      mbar_init(&bars->res_empty[i], kEpi);
+      mbar_init(&bars->res_empty[i], lnepi::res_box_readers<PN>());
     }
     fence_barrier_init();
   }
@@ -160,13 +158,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t st = 0, ph = 0;
     int in_stage = 0;
     for (int q = 0; q < NP; ++q) {
-      const uint32_t acc = q & 1;
-      if (q >= 2) {
-        mbar_wait(&bars->acc_empty[acc], ((q >> 1) - 1) & 1);
+      // single accumulator: the epilogue must have drained piece q-1
+      if (q >= 1) {
+        mbar_wait(&bars->acc_empty[0], (q - 1) & 1);
         tc_fence_after();
       }
       LTRACE(16 + q);
-      const uint32_t d = tmem + acc * PN;
+      const uint32_t d = tmem;
       for (int a = 0; a < KA; ++a) {
         if (in_stage == 0) {
           mbar_wait(&bars->full[st], ph);
@@ -191,23 +189,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++st == (uint32_t)stages) { st = 0; ph ^= 1; }
         }
       }
-      if (elect_one()) mma_commit(&bars->acc_full[acc]);
+      if (elect_one()) mma_commit(&bars->acc_full[0]);
       __syncwarp();
       LTRACE(48 + q);
     }
   } else if (warp == 10) {
     // ============================================ residual producer (one thread)
     if (lane == 0)
-      lnepi::produce_residual(&tmR, rring, bars->res_full, bars->res_empty, RS, N, m0);
+      lnepi::produce_residual<PN>(&tmR, rring, bars->res_full, bars->res_empty, RS, N, m0);
     __syncwarp();
   } else {
     // ============================================ epilogue (8 warps)
     const uint32_t quad = warp & 3;
     const uint32_t half = (warp - 2) >> 2;  // which 32 columns of each piece
     const uint32_t row = quad * 32 + lane;
-    lnepi::run(tmem, quad, half, row, m0 + static_cast<int>(row), T, N, bias, smem_u32(rring),
-               bars->res_full, bars->res_empty, RS, gamma, beta, eps, &tmY, m0,
-               reinterpret_cast<float*>(sA), bars->acc_full, bars->acc_empty, 1);
+    lnepi::run<PN>(tmem, quad, half, row, N, bias, smem_u32(rring), bars->res_full,
+                   bars->res_empty, RS, gamma, beta, eps, &tmY, m0, reinterpret_cast<float*>(sA),
+                   bars->acc_full, bars->acc_empty, 1);
   }
   if (threadIdx.x == 64) LTRACE(100);
   tc_fence_before();

@@ -1,10 +1,12 @@
 // ln_epi.cuh -- residual + LayerNorm epilogue shared by the row-complete
 // tensor-core kernels (K6 k_gemm_ln, K4 k_ffn with the fused LN2).
 //
-// The producing MMA writes 64-column pieces of a 128-row output tile into a
-// double-buffered TMEM accumulator (columns [0, 64) and [64, 128)).  For each
-// piece the epilogue (8 warps, two per TMEM lane quadrant, each owning 32 of
-// the 64 columns) adds the bias, rounds to bf16 -- the value the unfused
+// The producing MMA writes PN-column pieces of a 128-row output tile into
+// TMEM columns [0, 128): PN = 64 double-buffers two accumulators, PN = 128
+// uses one (then MMAs are N = 128, which the tensor pipe runs at full rate
+// from shared memory; N = 64 runs at 2/3).  For each piece the epilogue (8
+// warps, two per TMEM lane quadrant, each owning PN/2 of the piece's
+// columns) adds the bias, rounds to bf16 -- the value the unfused
 // pipeline stores for the sublayer output --, adds the bf16 residual in fp32
 // and accumulates shifted row sums of that fp32 sum s.  s itself is parked in
 // TMEM as bf16, two per 32-bit column at [128, 128 + N/2), so the whole row
@@ -30,33 +32,20 @@ namespace lnepi {
 
 using namespace ptx;
 
-constexpr int PN = 64;            // output columns per piece
-constexpr int kPark = 2 * PN;     // first TMEM column of the parked values
+constexpr int kPark = 128;        // first TMEM column of the parked values
 constexpr int kEpiThreads = 256;
 constexpr int kMaxN = 2 * (512 - kPark);
+constexpr int kBox = 128 * 128;   // one [128 x 64] bf16 SW128 box
 
-__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
-  const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float2 t = __bfloat1622float2(p[k]);
-    f[2 * k] = t.x;
-    f[2 * k + 1] = t.y;
-  }
-}
-__device__ __forceinline__ float2 unpack_bf16(uint32_t w) {
-  __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&w);
-  return __bfloat1622float2(h);
-}
-// 32 residual values (16 bf16 pairs) of `row`, columns [half*32, half*32+32)
-// of one [128 x 64] SW128 box at shared address `box`.
-__device__ __forceinline__ void load_res32(uint32_t box, uint32_t row, uint32_t half,
+// 32 residual values (16 bf16 pairs) of `row`, columns [c, c+32) (c = 0 or
+// 32) of one [128 x 64] SW128 box at shared address `box`.
+__device__ __forceinline__ void load_res32(uint32_t box, uint32_t row, uint32_t c,
                                            uint32_t (&r)[16]) {
 #pragma unroll
   for (int k = 0; k < 4; ++k)
     asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r[4 * k]), "=r"(r[4 * k + 1]), "=r"(r[4 * k + 2]), "=r"(r[4 * k + 3])
-                 : "r"(box + swz_offset(row, half * 4 + k, 128)));
+                 : "r"(box + swz_offset(row, (c >> 3) + k, 128)));
 }
 // bf16x2 -> float2 (exact: bf16 is the top half of an fp32)
 __device__ __forceinline__ float2 bf2(uint32_t w) {
@@ -80,87 +69,107 @@ __device__ __forceinline__ int piece_of(int i, int NP) {
 }
 
 // Residual producer (one thread): streams the [128 x N] residual tile at row
-// m0, piece order piece_of(), through a ring of `depth` 16 KB boxes.
+// m0 as [128 x 64] boxes, pieces in piece_of() order, through a ring of
+// `depth` boxes.
+template <int PN>
 __device__ __forceinline__ void produce_residual(const CUtensorMap* tm, uint8_t* ring,
                                                  uint64_t* full, uint64_t* empty, int depth,
                                                  int N, int m0) {
+  constexpr int BPP = PN / 64;  // boxes per piece
   const int NP = N / PN;
-  for (int i = 0; i < NP; ++i) {
-    const int slot = i % depth;
-    mbar_wait(&empty[slot], ((i / depth) & 1) ^ 1);
-    mbar_arrive_expect_tx(&full[slot], 128 * 128);
-    tma_load_2d(tm, &full[slot], ring + slot * 128 * 128, piece_of(i, NP) * PN, m0);
+  for (int b = 0; b < NP * BPP; ++b) {
+    const int slot = b % depth;
+    mbar_wait(&empty[slot], ((b / depth) & 1) ^ 1);
+    mbar_arrive_expect_tx(&full[slot], kBox);
+    tma_load_2d(tm, &full[slot], ring + slot * kBox, piece_of(b / BPP, NP) * PN + (b % BPP) * 64,
+                m0);
   }
 }
+// Arrivals a residual box needs before it can be refilled.
+template <int PN>
+constexpr int res_box_readers() { return PN == 64 ? kEpiThreads : kEpiThreads / 2; }
 
-// Runs in all 256 epilogue threads.  `warp_in_epi` = 0..7 (two per lane
-// quadrant, quadrant = hardware warp id % 4), `row` = tile row of this thread.
+// Runs in all 256 epilogue threads: `quad` = TMEM lane quadrant (hardware
+// warp id % 4), `half` = which PN/2 columns of each piece, `row` = tile row.
+// Accumulator protocol: PN = 64 alternates acc_full/empty[0..1] (buffers at
+// columns 0 and 64); PN = 128 uses acc_full/empty[0] only.
 // Arithmetic runs on packed fp32 pairs (FADD2 / FFMA2) to halve the issue
 // count of this epilogue, which is instruction-bound.
+template <int PN>
 __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half, uint32_t row,
-                                    int grow, int T, int N, const float* __restrict__ bias,
-                                    uint32_t res_ring, uint64_t* res_full, uint64_t* res_empty,
-                                    int res_depth, const float* __restrict__ gamma,
+                                    int N, const float* __restrict__ bias, uint32_t res_ring,
+                                    uint64_t* res_full, uint64_t* res_empty, int res_depth,
+                                    const float* __restrict__ gamma,
                                     const float* __restrict__ beta, float eps,
                                     const CUtensorMap* tmY, int m0, float* gb_smem,
                                     uint64_t* acc_full, uint64_t* acc_empty, uint32_t bar_id) {
+  static_assert(PN == 64 || PN == 128, "piece width");
+  constexpr int CPT = PN / 64;  // 32-column chunks per thread per piece
   const uint32_t loff = (quad * 32) << 16;
   const int NP = N / PN;
 
   float2 shift = make_float2(0.0f, 0.0f), S1 = shift, S2 = shift;
   for (int i = 0; i < NP; ++i) {
     const int q = piece_of(i, NP);
-    const int c0 = q * PN + half * 32;
-    float4 b[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) b[k] = __ldg(reinterpret_cast<const float4*>(bias + c0) + k);
-    uint32_t r[16];
-    {
-      const int slot = i % res_depth;
-      mbar_wait(&res_full[slot], (i / res_depth) & 1);
-      load_res32(res_ring + slot * 128 * 128, row, half, r);
-      release_box(&res_empty[slot]);
-    }
-    const uint32_t acc = i & 1;
+    const uint32_t acc = PN == 64 ? (i & 1) : 0;
+    const uint32_t par = PN == 64 ? ((i >> 1) & 1) : (i & 1);
 #ifdef LN_TRACE
     if (threadIdx.x == 64) LN_TRACE(200 + i);
 #endif
-    mbar_wait(&acc_full[acc], (i >> 1) & 1);
+    mbar_wait(&acc_full[acc], par);
     tc_fence_after();
 #ifdef LN_TRACE
     if (threadIdx.x == 64) LN_TRACE(232 + i);
 #endif
-    uint32_t v[32];
-    tmem_ld32(tmem + loff + acc * PN + half * 32, v);
+    uint32_t v[CPT][32];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+      tmem_ld32(tmem + loff + acc * 64 + half * (PN / 2) + c * 32, v[c]);
     tmem_ld_wait();
     tc_fence_before();
     mbar_arrive(&acc_empty[acc]);
-    if (i == 0) {
-      const float s00 = bf2(pack2(make_float2(__uint_as_float(v[0]) + b[0].x, 0.0f))).x +
-                        bf2(r[0]).x;
-      shift = make_float2(-s00, -s00);
-    }
-    uint32_t park[16];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const float4& bq = b[k >> 1];
-      const float2 bb = (k & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
-      // o: the sublayer output exactly as the unfused path stores it (bf16)
-      const float2 o = bf2(pack2(
-          __fadd2_rn(make_float2(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1])), bb)));
-      const float2 sv = __fadd2_rn(o, bf2(r[k]));
-      park[k] = pack2(sv);
-      const float2 t = __fadd2_rn(sv, shift);
-      S1 = __fadd2_rn(S1, t);
-      S2 = __ffma2_rn(t, t, S2);
+    for (int c = 0; c < CPT; ++c) {
+      const int col = q * PN + half * (PN / 2) + c * 32;  // first output column
+      float4 b[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) b[k] = __ldg(reinterpret_cast<const float4*>(bias + col) + k);
+      uint32_t r[16];
+      {
+        // residual box of this chunk and the 32 columns of it
+        const int bx = PN == 64 ? i : 2 * i + static_cast<int>(half);
+        const int slot = bx % res_depth;
+        if (PN == 64 || c == 0) mbar_wait(&res_full[slot], (bx / res_depth) & 1);
+        load_res32(res_ring + slot * kBox, row, PN == 64 ? half * 32 : c * 32, r);
+        if (c == CPT - 1) release_box(&res_empty[slot]);
+      }
+      if (i == 0 && c == 0) {
+        const float s00 = bf2(pack2(make_float2(__uint_as_float(v[0][0]) + b[0].x, 0.0f))).x +
+                          bf2(r[0]).x;
+        shift = make_float2(-s00, -s00);
+      }
+      uint32_t park[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float4& bq = b[k >> 1];
+        const float2 bb = (k & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
+        // o: the sublayer output exactly as the unfused path stores it (bf16)
+        const float2 o = bf2(pack2(__fadd2_rn(
+            make_float2(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])), bb)));
+        const float2 sv = __fadd2_rn(o, bf2(r[k]));
+        park[k] = pack2(sv);
+        const float2 t = __fadd2_rn(sv, shift);
+        S1 = __fadd2_rn(S1, t);
+        S2 = __ffma2_rn(t, t, S2);
+      }
+      tmem_st16(tmem + loff + kPark + col / 2, park);
     }
-    tmem_st16(tmem + loff + kPark + q * 32 + half * 16, park);
   }
   tmem_st_wait();
 #ifdef LN_TRACE
   if (threadIdx.x == 64) LN_TRACE(300);
 #endif
-  const float nh = static_cast<float>(NP * 32);
+  const float nh = static_cast<float>(N / 2);
   const float s1 = S1.x + S1.y, s2 = S2.x + S2.y;
   const float mean_h = s1 / nh - shift.x;
   const float m2_h = fmaxf(s2 - s1 * (s1 / nh), 0.0f);
@@ -190,45 +199,76 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
     *reinterpret_cast<float4*>(gb_smem + N + c) = __ldg(reinterpret_cast<const float4*>(beta + c));
   }
   named_bar_sync(bar_id, kEpiThreads);
+#ifdef LN_TRACE
+  if (threadIdx.x == 64) LN_TRACE(301);
+#endif
 
   // second sweep: normalise, stage [128 x 64] bf16 boxes in the (drained)
-  // residual ring, TMA-store them
+  // residual ring, TMA-store them.  PN = 64: both halves fill one box per
+  // piece (two boxes alternate, 256-thread barriers); PN = 128: each half
+  // owns a box per piece and alternates its own two boxes (128-thread
+  // barriers, ids bar_id + 1 + half; needs res_depth >= 4).
+  const int ht = et & 127;  // thread index within the half (PN = 128)
   for (int i = 0; i < NP; ++i) {
     const int q = piece_of(i, NP);
-    const int c0 = q * PN + half * 32;
-    uint32_t park[16];
-    tmem_ld16(tmem + loff + kPark + q * 32 + half * 16, park);
-    tmem_ld_wait();
-    uint32_t w[16];
-#pragma unroll
-    for (int k = 0; k < 16; k += 2) {
-      const float4 g = *reinterpret_cast<const float4*>(gb_smem + c0 + 2 * k);
-      const float4 be = *reinterpret_cast<const float4*>(gb_smem + N + c0 + 2 * k);
-      const float2 n0 = __ffma2_rn(bf2(park[k]), rs2, off2);
-      const float2 n1 = __ffma2_rn(bf2(park[k + 1]), rs2, off2);
-      w[k] = pack2(__ffma2_rn(make_float2(g.x, g.y), n0, make_float2(be.x, be.y)));
-      w[k + 1] = pack2(__ffma2_rn(make_float2(g.z, g.w), n1, make_float2(be.z, be.w)));
-    }
-    const uint32_t box = res_ring + (i & 1) * 128 * 128;
-    if (i >= 2) {
-      // the store issued from this box two pieces ago must have read it
-      if (et == 0) tma_store_wait_read<1>();
-      named_bar_sync(bar_id, kEpiThreads);
+    uint32_t box;
+    if (PN == 64) {
+      box = res_ring + (i & 1) * kBox;
+      if (i >= 2) {
+        if (et == 0) tma_store_wait_read<1>();
+        named_bar_sync(bar_id, kEpiThreads);
+      }
+    } else {
+      box = res_ring + (2 * half + (i & 1)) * kBox;
+      if (i >= 2) {
+        if (ht == 0) tma_store_wait_read<1>();
+        named_bar_sync(bar_id + 1 + half, kEpiThreads / 2);
+      }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      st_shared_v4(box + swz_offset(row, half * 4 + k, 128), w[4 * k], w[4 * k + 1], w[4 * k + 2],
-                   w[4 * k + 3]);
+    for (int c = 0; c < CPT; ++c) {
+      const int col = q * PN + half * (PN / 2) + c * 32;
+      uint32_t park[16];
+      tmem_ld16(tmem + loff + kPark + col / 2, park);
+      tmem_ld_wait();
+      uint32_t w[16];
+#pragma unroll
+      for (int k = 0; k < 16; k += 2) {
+        const float4 g = *reinterpret_cast<const float4*>(gb_smem + col + 2 * k);
+        const float4 be = *reinterpret_cast<const float4*>(gb_smem + N + col + 2 * k);
+        const float2 n0 = __ffma2_rn(bf2(park[k]), rs2, off2);
+        const float2 n1 = __ffma2_rn(bf2(park[k + 1]), rs2, off2);
+        w[k] = pack2(__ffma2_rn(make_float2(g.x, g.y), n0, make_float2(be.x, be.y)));
+        w[k + 1] = pack2(__ffma2_rn(make_float2(g.z, g.w), n1, make_float2(be.z, be.w)));
+      }
+      const uint32_t chunk0 = PN == 64 ? half * 4 : c * 4;  // 16-byte chunk within the box row
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        st_shared_v4(box + swz_offset(row, chunk0 + k, 128), w[4 * k], w[4 * k + 1],
+                     w[4 * k + 2], w[4 * k + 3]);
+    }
     fence_proxy_async_smem();
-    named_bar_sync(bar_id, kEpiThreads);
-    if (et == 0) {
-      tma_store_2d_u32(tmY, box, q * PN, m0);
-      tma_store_commit();
+#ifdef LN_TRACE
+    if (threadIdx.x == 64) LN_TRACE(310 + i);
+#endif
+    if (PN == 64) {
+      named_bar_sync(bar_id, kEpiThreads);
+      if (et == 0) {
+        tma_store_2d_u32(tmY, box, q * PN, m0);
+        tma_store_commit();
+      }
+    } else {
+      named_bar_sync(bar_id + 1 + half, kEpiThreads / 2);
+      if (ht == 0) {
+        tma_store_2d_u32(tmY, box, q * PN + half * 64, m0);
+        tma_store_commit();
+      }
     }
   }
-  if (et == 0) tma_store_wait<0>();
-  (void)grow;
-  (void)T;
+  if ((PN == 64 && et == 0) || (PN == 128 && ht == 0)) tma_store_wait<0>();
+#ifdef LN_TRACE
+  if (threadIdx.x == 64) LN_TRACE(330);
+#endif
 }
 
 }  // namespace lnepi

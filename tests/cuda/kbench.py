@@ -53,3 +53,14 @@ g = torch.randn(768, device="cuda")
 yy = torch.empty_like(a)
 us = timeit(lambda: abi.check(L.fsvd_test_resid_layernorm(p(a), p(b), p(g), p(g), 1e-5, p(yy), T, 768, st)))
 print(f"resid_ln rows={T} d=768: {us:7.1f} us  {3 * T * 768 * 2 / us / 1e3:6.0f} GB/s", flush=True)
+
+for (B, M) in [(32, 512), (4, 4096)]:
+    H, G, rp = 12, 12, 32
+    cols = (H + 2 * G) * rp
+    qkv = (torch.randn(B * M, cols, device="cuda") * 0.6).bfloat16()
+    o = torch.empty(B * M, H * rp, device="cuda", dtype=torch.bfloat16)
+    us = timeit(lambda: abi.check(L.fsvd_test_attention(p(qkv), cols, 0, H * rp, (H + G) * rp, B, M, H, G, rp,
+                                                        p(o), H * rp, st)))
+    exps = B * H * M * M
+    print(f"attention B={B} M={M} H={H} rp={rp}: {us:7.1f} us  {exps / us / 1e6:6.2f} T exp/s "
+          f"(MUFU-only bound {16 * 148 * 1.92e9 / 1e12:.2f})", flush=True)

@@ -27,7 +27,7 @@ L.fsvd_debug_trace_ln_copy(buf, 1024)
 t0 = buf[0]
 rel = lambda i: buf[i] - t0 if buf[i] else None  # noqa: E731
 print("K", K, "alloc+sync", rel(3), "mma start", rel(1), "a_full", rel(2), "epi done", rel(100), "end", rel(101))
-print("pass1 end", rel(300))
+print("pass1 end", rel(300), "gamma/beta staged", rel(301), "pass2 pieces", [rel(310 + i) for i in range(12)], "stores drained", rel(330))
 for q in range(N // 64):
     print(f"piece {q:2d}: mma_begin {rel(16 + q)} mma_issued {rel(48 + q)} epi_wait_begin {rel(200 + q)} epi_got_acc {rel(232 + q)}")
 

@@ -95,3 +95,28 @@ def test_resid_layernorm_vs_torch(env, rows, d):
     torch.cuda.synchronize()
     ref = _ln_ref(torch, a.float() + b.float(), gam, bet, 1e-5)
     assert _rel(y, ref) < 1e-2
+
+
+@pytest.mark.parametrize("B,M,H,G,rp", [(2, 512, 12, 12, 32), (1, 130, 4, 2, 16), (3, 77, 2, 2, 64),
+                                         (1, 1024, 4, 4, 32)])
+def test_attention_rankspace_vs_torch(env, B, M, H, G, rp):
+    """K2 against softmax(2^(Qt K^T)) V in fp32 on the same bf16 inputs."""
+    L, torch = env
+    g = torch.Generator(device="cuda").manual_seed(B * M + H + rp)
+    cols = (H + 2 * G) * rp
+    qkv = (torch.randn(B * M, cols, device="cuda", generator=g) * 0.6).bfloat16()
+    out = torch.empty(B * M, H * rp, device="cuda", dtype=torch.bfloat16)
+    s = torch.cuda.current_stream().cuda_stream
+    abi.check(L.fsvd_test_attention(_p(qkv), cols, 0, H * rp, (H + G) * rp, B, M, H, G, rp,
+                                    _p(out), H * rp, C.c_void_p(s)))
+    torch.cuda.synchronize()
+    x = qkv.float().view(B, M, cols)
+    ref = torch.empty(B, M, H * rp, device="cuda")
+    for h in range(H):
+        gi = h // (H // G)
+        q = x[:, :, h * rp:(h + 1) * rp]
+        k = x[:, :, (H + gi) * rp:(H + gi + 1) * rp]
+        v = x[:, :, (H + G + gi) * rp:(H + G + gi + 1) * rp]
+        sc = (q @ k.transpose(1, 2)) * 0.6931471805599453  # log2-domain scores -> natural
+        ref[:, :, h * rp:(h + 1) * rp] = torch.softmax(sc, -1) @ v
+    assert _rel(out.view(B, M, H * rp), ref) < 2e-2
