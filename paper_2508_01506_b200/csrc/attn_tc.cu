@@ -24,6 +24,11 @@
 // It is also the dense-attention kernel of the materializing baselines: with
 // r = head_dim and Q/K/V as its three inputs it computes softmax(Q K^T) V.
 //
+// P never touches shared memory: the softmax warps tcgen05.st the bf16
+// probabilities into TMEM and the PV MMA reads its A operand from there (the
+// kernel is shared-memory-bandwidth bound otherwise: P would cost a 32 KB
+// st.shared plus a 32 KB MMA read per key tile).
+//
 // CTA = one (batch, head, 128-row query tile); 10 warps: 0-7 softmax (two
 // threads per query row, 64 keys each; TMEM lane quadrant warp%4), 8 TMA
 // producer, 9 MMA issuer and TMEM owner.  ~92 KB smem and 256 TMEM columns,
@@ -81,8 +86,8 @@ extern "C" __attribute__((visibility("default"))) int fsvd_debug_trace_attn_copy
   return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace_at, sizeof(long long) * n));
 }
 namespace {
-// CTA (q-tile 0, head 0, batch 1) and its SM's clock
-#define ATRACE(slot) do { if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 1) g_trace_at[(slot)] = clock64(); } while (0)
+// CTA 0 (first work item) and its SM clock
+#define ATRACE(slot) do { if (blockIdx.x == 0) g_trace_at[(slot)] = clock64(); } while (0)
 #else
 #define ATRACE(slot) do { } while (0)
 #endif
@@ -92,31 +97,34 @@ struct AttnCfg {
   static constexpr int STAGES = RP >= 64 ? 2 : 3;
   static constexpr int RB = RP * 2;       // bytes per rank-width row
   static constexpr int TILE = QT * RB;    // one Qt / P_k / P_v tile
-  static constexpr int SP = QT * KT * 2;  // probabilities
-  static constexpr int o_q = 0;
-  static constexpr int o_kv = o_q + up1k(TILE);
+  static constexpr int o_q = 0;           // two Qt slots (next item prefetched)
+  static constexpr int o_kv = o_q + 2 * up1k(TILE);
   static constexpr int KV_STAGE = 2 * up1k(TILE);
-  static constexpr int o_p = o_kv + STAGES * KV_STAGE;
-  static constexpr int o_bar = o_p + SP;
-  static constexpr int SMEM = 1024 + o_bar + 2304;  // Bars: barriers + 2 x [2][128] floats
-  static constexpr int t_s = 0, t_o = 128;  // TMEM columns
-  static_assert(SMEM <= 227 * 1024, "shared memory budget");  // RP <= 32: two CTAs / SM
+  static constexpr int o_bar = o_kv + STAGES * KV_STAGE;
+  static constexpr int SMEM = 1024 + o_bar + 3584;  // Bars
+  // TMEM columns: S (fp32, 128 keys), O (fp32, RP), P (bf16 pairs, 128 keys)
+  static constexpr int t_s = 0, t_o = 128, t_p = 192;
+  static_assert(2 * SMEM <= 228 * 1024, "two CTAs per SM");
 };
 
 struct Bars {
-  uint64_t pro;
+  uint64_t q_full[2], q_empty[2];
   uint64_t kv_full[3], kv_empty[3];
-  uint64_t s_full, s_free, p_full, o_full;
+  uint64_t s_full, s_free, p_full, o_full, o_free;
   uint32_t tmem;
-  float xmax[2][QT];  // per-half row maxima of the current tile
-  float xsum[2][QT];  // per-half row sums at the end
+  float xmax[2][2][QT];  // [tile parity][half][row]: per-half row maxima
+  float xsum[2][QT];     // per-half row sums at the end of an item
 };
-static_assert(sizeof(Bars) <= 2304, "Bars outgrew its shared-memory reservation");
+static_assert(sizeof(Bars) <= 3584, "Bars outgrew its shared-memory reservation");
 
+// Persistent: each CTA walks work items (batch, head, 128-query tile) with
+// stride gridDim.x; consecutive items share (batch, head) so K/V stay hot in
+// L2.  Q of the next item and its first K/V tiles are prefetched while the
+// current item finishes, and TMEM / barriers are set up once per CTA.
 template <int RP>
 __global__ void __launch_bounds__(kThreads, 2)
     k_attn_rankspace(const __grid_constant__ CUtensorMap tmQKV, bf16* __restrict__ out,
-                     int64_t ldo, int seq, int heads, int groups, int q_off, int k_off,
+                     int64_t ldo, int batch, int seq, int heads, int groups, int q_off, int k_off,
                      int v_off) {
   using C = AttnCfg<RP>;
   extern __shared__ uint8_t smem_raw[];
@@ -124,15 +132,17 @@ __global__ void __launch_bounds__(kThreads, 2)
                                              ~uintptr_t(1023));
   Bars* bars = reinterpret_cast<Bars*>(smem + C::o_bar);
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int g = h / (heads / groups);
-  const int row0 = b * seq;  // first token row of this sequence
-  const int q0 = qt * QT;
+  const int nqt = (seq + QT - 1) / QT;
+  const int items = nqt * heads * batch;
   const int nj = (seq + KT - 1) / KT;
+  const int hpg = heads / groups;
 
   if (warp == kTma && lane == 0) {
     tma_prefetch(&tmQKV);
-    mbar_init(&bars->pro, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->q_full[i], 1);
+      mbar_init(&bars->q_empty[i], 1);
+    }
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&bars->kv_full[i], 1);
       mbar_init(&bars->kv_empty[i], 1);
@@ -141,6 +151,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_init(&bars->s_free, kSoftmax);
     mbar_init(&bars->p_full, kSoftmax);
     mbar_init(&bars->o_full, 1);
+    mbar_init(&bars->o_free, kSoftmax);
     fence_barrier_init();
   }
   if (threadIdx.x == 0) ATRACE(0);
@@ -150,43 +161,45 @@ __global__ void __launch_bounds__(kThreads, 2)
   tc_fence_after();
   const uint32_t tmem = bars->tmem;
   const uint32_t s_q = smem_u32(smem + C::o_q), s_kv = smem_u32(smem + C::o_kv);
-  const uint32_t s_p = smem_u32(smem + C::o_p);
 
   if (warp == kTma) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
-      mbar_arrive_expect_tx(&bars->pro, C::TILE);
-      tma_load_2d(&tmQKV, &bars->pro, smem + C::o_q, q_off + h * RP, row0 + q0);
+      uint32_t st = 0, ph = 0;
+      int it = 0;
+      for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+        const int qt = w % nqt, h = (w / nqt) % heads, b = w / (nqt * heads);
+        const int g = h / hpg, row0 = b * seq;
+        const int qs = it & 1;
+        mbar_wait(&bars->q_empty[qs], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->q_full[qs], C::TILE);
+        tma_load_2d(&tmQKV, &bars->q_full[qs], smem + C::o_q + qs * up1k(C::TILE),
+                    q_off + h * RP, row0 + qt * QT);
+        for (int j = 0; j < nj; ++j) {
+          mbar_wait(&bars->kv_empty[st], ph ^ 1);
+          uint8_t* kv = smem + C::o_kv + st * C::KV_STAGE;
+          mbar_arrive_expect_tx(&bars->kv_full[st], 2 * C::TILE);
+          tma_load_2d(&tmQKV, &bars->kv_full[st], kv, k_off + g * RP, row0 + j * KT);
+          tma_load_2d(&tmQKV, &bars->kv_full[st], kv + up1k(C::TILE), v_off + g * RP,
+                      row0 + j * KT);
+          if (++st == C::STAGES) { st = 0; ph ^= 1; }
+        }
+      }
     }
     __syncwarp();
-    uint32_t st = 0, ph = 0;
-    for (int j = 0; j < nj; ++j) {
-      mbar_wait(&bars->kv_empty[st], ph ^ 1);
-      if (lane == 0) {
-        uint8_t* kv = smem + C::o_kv + st * C::KV_STAGE;
-        mbar_arrive_expect_tx(&bars->kv_full[st], 2 * C::TILE);
-        tma_load_2d(&tmQKV, &bars->kv_full[st], kv, k_off + g * RP, row0 + j * KT);
-        tma_load_2d(&tmQKV, &bars->kv_full[st], kv + up1k(C::TILE), v_off + g * RP,
-                    row0 + j * KT);
-      }
-      __syncwarp();
-      if (++st == C::STAGES) { st = 0; ph ^= 1; }
-    }
   } else if (warp == kMma) {
-    // ------------------------------------------------ MMA issuer
-    mbar_wait(&bars->pro, 0);
-    if (lane == 0) ATRACE(1);
-    const uint64_t dq = desc_kmajor(s_q, C::RB);
+    // ------------------------------------------------ MMA issuer (warp-uniform)
     const uint64_t dk0 = desc_kmajor(s_kv, C::RB);
-    const uint64_t dp0 = desc_kmajor(s_p, 128);
     const uint64_t dv0 = desc_mnmajor(s_kv + up1k(C::TILE), C::RB);
-    auto issue_s = [&](int j) {
-      const uint32_t st = j % C::STAGES;
-      mbar_wait(&bars->kv_full[st], (j / C::STAGES) & 1);
-      if (lane == 0) ATRACE(16 + j);
-      if (j > 0) mbar_wait(&bars->s_free, (j - 1) & 1);
-      if (lane == 0) ATRACE(48 + j);
+    int gt = 0;  // key tiles issued so far by this CTA (all items)
+    int it = 0;
+    // S for global tile index t of the item whose Qt is in slot qs
+    auto issue_s = [&](int t, int qs) {
+      const uint32_t st = t % C::STAGES;
+      mbar_wait(&bars->kv_full[st], (t / C::STAGES) & 1);
+      if (t > 0) mbar_wait(&bars->s_free, (t - 1) & 1);
       tc_fence_after();
+      const uint64_t dq = desc_kmajor(s_q + qs * up1k(C::TILE), C::RB);
       const uint64_t dk = dk0 + ((st * C::KV_STAGE) >> 4);
       if (elect_one()) {
 #pragma unroll
@@ -196,23 +209,36 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       __syncwarp();
     };
-    issue_s(0);
-    for (int j = 0; j < nj; ++j) {
-      if (j + 1 < nj) issue_s(j + 1);
-      mbar_wait(&bars->p_full, j & 1);
-      if (lane == 0) ATRACE(80 + j);
-      tc_fence_after();
-      const uint32_t st = j % C::STAGES;
-      const uint64_t dv = dv0 + ((st * C::KV_STAGE) >> 4);
-      if (elect_one()) {
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+      const int qs = it & 1;
+      mbar_wait(&bars->q_full[qs], (it >> 1) & 1);
+      if (lane == 0 && it == 0) ATRACE(1);
+      issue_s(gt, qs);
+      for (int j = 0; j < nj; ++j) {
+        const int t = gt + j;
+        if (j + 1 < nj) {
+          issue_s(t + 1, qs);
+        } else {
+          if (elect_one()) mma_commit(&bars->q_empty[qs]);  // after this item's last S
+          __syncwarp();
+        }
+        mbar_wait(&bars->p_full, t & 1);
+        if (j == 0 && it > 0) mbar_wait(&bars->o_free, (it - 1) & 1);  // O of the previous item read
+        tc_fence_after();
+        const uint32_t st = t % C::STAGES;
+        const uint64_t dv = dv0 + ((st * C::KV_STAGE) >> 4);
+        if (elect_one()) {
+          // O += P V: P (A operand) straight from TMEM, 8 columns per K = 16 step
 #pragma unroll
-        for (int k = 0; k < KT / 16; ++k)
-          mma_bf16_ss(tmem + C::t_o, dp0 + (((k >> 2) * (QT * 128) + (k & 3) * 32) >> 4),
-                      dv + ((k * 16 * C::RB) >> 4), idesc_bf16(128, RP, 0, 1), (j | k) != 0);
-        mma_commit(&bars->o_full);
-        mma_commit(&bars->kv_empty[st]);
+          for (int k = 0; k < KT / 16; ++k)
+            mma_bf16_ts(tmem + C::t_o, tmem + C::t_p + k * 8, dv + ((k * 16 * C::RB) >> 4),
+                        idesc_bf16(128, RP, 0, 1), (j | k) != 0);
+          mma_commit(&bars->o_full);
+          mma_commit(&bars->kv_empty[st]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
+      gt += nj;
     }
   } else {
     // ------------------------------------------------ softmax (8 warps)
@@ -227,10 +253,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     constexpr int CH = RP >= 32 ? RP / 2 : RP;
     const bool owns_o = RP >= 32 || half == 0;
     const int oc0 = RP >= 32 ? static_cast<int>(half) * CH : 0;
-    float m_run = -INFINITY, l_run = 0.0f;
 
-    // O lives in TMEM and accumulates across key tiles; before PV_j it is
-    // rescaled by alpha_j (each half of the pair rescales half of the columns).
     auto rescale_o = [&](float alpha) {
 #pragma unroll
       for (int c = 0; c < CH; c += 16) {
@@ -244,94 +267,103 @@ __global__ void __launch_bounds__(kThreads, 2)
       tmem_st_wait();
     };
 
-    for (int j = 0; j < nj; ++j) {
-      if (threadIdx.x == 0) ATRACE(112 + j);
-      mbar_wait(&bars->s_full, j & 1);
-      if (threadIdx.x == 0) ATRACE(144 + j);
-      tc_fence_after();
-      float s[KH];
-#pragma unroll
-      for (int c = 0; c < KH; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(tq + C::t_s + half * KH + c, r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(r[i]);
-      }
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&bars->s_free);
-      const int valid = seq - j * KT - static_cast<int>(half) * KH;  // in-sequence keys here
-      if (valid < KH) {
-#pragma unroll
-        for (int i = 0; i < KH; ++i) s[i] = (i < valid) ? s[i] : -INFINITY;
-      }
-      float mx[8];  // 8 independent max chains
-#pragma unroll
-      for (int i = 0; i < 8; ++i) mx[i] = s[i];
-#pragma unroll
-      for (int i = 8; i < KH; ++i) mx[i & 7] = fmaxf(mx[i & 7], s[i]);
-      float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-      bars->xmax[half][row] = tmax;
-      named_bar_sync(1 + quad, 64);
-      tmax = fmaxf(tmax, bars->xmax[half ^ 1][row]);
-      const float m_new = fmaxf(m_run, tmax);
-      const float alpha = ex2(m_run - m_new);
-      m_run = m_new;
-      uint32_t pk[KH / 2];
-      float2 sum2 = make_float2(0.0f, 0.0f);
-      const float2 nm = make_float2(-m_new, -m_new);
-#pragma unroll
-      for (int c = 0; c < KH / 2; ++c) {
-        const float2 d = __fadd2_rn(make_float2(s[2 * c], s[2 * c + 1]), nm);
-        // one pair in EMU_EVERY on the FMA pipe, the rest on MUFU
-        const float2 p = (c % EMU_EVERY == EMU_EVERY - 1) ? ex2_poly2(d)
-                                                          : make_float2(ex2(d.x), ex2(d.y));
-        sum2 = __fadd2_rn(sum2, p);
-        pk[c] = pack_bf16(p.x, p.y);
-      }
-      l_run = fmaf(l_run, alpha, sum2.x + sum2.y);
-      // single-buffered probability tile and O accumulator: PV_{j-1} must be done
-      if (j >= 1) {
-        if (threadIdx.x == 0) ATRACE(176 + j);
-        mbar_wait(&bars->o_full, (j - 1) & 1);
-        if (threadIdx.x == 0) ATRACE(208 + j);
+    int gt = 0;
+    int it = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+      const int qt = w % nqt, h = (w / nqt) % heads, b = w / (nqt * heads);
+      const int row0 = b * seq, q0 = qt * QT;
+      float m_run = -INFINITY, l_run = 0.0f;
+      for (int j = 0; j < nj; ++j) {
+        const int t = gt + j;
+        if (threadIdx.x == 0 && it == 0) ATRACE(112 + j);
+        mbar_wait(&bars->s_full, t & 1);
+        if (threadIdx.x == 0 && it == 0) ATRACE(144 + j);
         tc_fence_after();
-        if (owns_o && __any_sync(0xffffffffu, alpha != 1.0f)) rescale_o(alpha);
-      }
-      // this half's 64 keys are exactly one [128 x 64] SW128 atom of P
+        float s[KH];
 #pragma unroll
-      for (int c = 0; c < KH / 8; ++c)
-        st_shared_v4(s_p + half * (QT * 128) + swz_offset(row, c, 128), pk[4 * c], pk[4 * c + 1],
-                     pk[4 * c + 2], pk[4 * c + 3]);
-      fence_proxy_async_smem();
+        for (int c = 0; c < KH; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tq + C::t_s + half * KH + c, r);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(r[i]);
+        }
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&bars->s_free);
+        const int valid = seq - j * KT - static_cast<int>(half) * KH;  // in-sequence keys here
+        if (valid < KH) {
+#pragma unroll
+          for (int i = 0; i < KH; ++i) s[i] = (i < valid) ? s[i] : -INFINITY;
+        }
+        float mx[8];  // 8 independent max chains
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = s[i];
+#pragma unroll
+        for (int i = 8; i < KH; ++i) mx[i & 7] = fmaxf(mx[i & 7], s[i]);
+        float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                           fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        bars->xmax[t & 1][half][row] = tmax;
+        named_bar_sync(1 + quad, 64);
+        tmax = fmaxf(tmax, bars->xmax[t & 1][half ^ 1][row]);
+        const float m_new = fmaxf(m_run, tmax);
+        const float alpha = ex2(m_run - m_new);
+        m_run = m_new;
+        uint32_t pk[KH / 2];
+        float2 sum2 = make_float2(0.0f, 0.0f);
+        const float2 nm = make_float2(-m_new, -m_new);
+#pragma unroll
+        for (int c = 0; c < KH / 2; ++c) {
+          const float2 d = __fadd2_rn(make_float2(s[2 * c], s[2 * c + 1]), nm);
+          // one pair in EMU_EVERY on the FMA pipe, the rest on MUFU
+          const float2 p = (c % EMU_EVERY == EMU_EVERY - 1) ? ex2_poly2(d)
+                                                            : make_float2(ex2(d.x), ex2(d.y));
+          sum2 = __fadd2_rn(sum2, p);
+          pk[c] = pack_bf16(p.x, p.y);
+        }
+        l_run = fmaf(l_run, alpha, sum2.x + sum2.y);
+        // single-buffered probability tile and O accumulator: PV of the
+        // previous tile of this item must be done
+        if (j >= 1) {
+          mbar_wait(&bars->o_full, (t - 1) & 1);
+          tc_fence_after();
+          if (owns_o && __any_sync(0xffffffffu, alpha != 1.0f)) rescale_o(alpha);
+        }
+        // this half's 64 keys -> TMEM columns [t_p + 32*half, +32) of this row
+        tmem_st32(tq + C::t_p + half * 32, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bars->p_full);
+      }
+      gt += nj;
+      bars->xsum[half][row] = l_run;
+      mbar_wait(&bars->o_full, (gt - 1) & 1);
+      tc_fence_after();
+      named_bar_sync(1 + quad, 64);
+      const float inv = 1.0f / (l_run + bars->xsum[half ^ 1][row]);
+      const int qrow = q0 + static_cast<int>(row);
+#pragma unroll
+      for (int c = 0; c < CH; c += 16) {
+        if (!owns_o) break;
+        uint32_t r[16];
+        tmem_ld16(tq + C::t_o + oc0 + c, r);
+        tmem_ld_wait();
+        if (qrow < seq) {
+          uint4* dst =
+              reinterpret_cast<uint4*>(out + (int64_t)(row0 + qrow) * ldo + h * RP + oc0 + c);
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+            dst[v] = make_uint4(
+                pack_bf16(__uint_as_float(r[8 * v + 0]) * inv, __uint_as_float(r[8 * v + 1]) * inv),
+                pack_bf16(__uint_as_float(r[8 * v + 2]) * inv, __uint_as_float(r[8 * v + 3]) * inv),
+                pack_bf16(__uint_as_float(r[8 * v + 4]) * inv, __uint_as_float(r[8 * v + 5]) * inv),
+                pack_bf16(__uint_as_float(r[8 * v + 6]) * inv, __uint_as_float(r[8 * v + 7]) * inv));
+        }
+      }
+      // O read: the next item's first PV may overwrite it; the xsum slots
+      // are rewritten only after the next item's tile barriers
       tc_fence_before();
-      mbar_arrive(&bars->p_full);
-      if (threadIdx.x == 0) ATRACE(240 + j);
-    }
-    bars->xsum[half][row] = l_run;
-    mbar_wait(&bars->o_full, (nj - 1) & 1);
-    if (threadIdx.x == 0) ATRACE(2);
-    tc_fence_after();
-    named_bar_sync(1 + quad, 64);
-    const float inv = 1.0f / (l_run + bars->xsum[half ^ 1][row]);
-    const int qrow = q0 + static_cast<int>(row);
-#pragma unroll
-    for (int c = 0; c < CH; c += 16) {
-      if (!owns_o) break;
-      uint32_t r[16];
-      tmem_ld16(tq + C::t_o + oc0 + c, r);
-      tmem_ld_wait();
-      if (qrow < seq) {
-        uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)(row0 + qrow) * ldo + h * RP + oc0 + c);
-#pragma unroll
-        for (int v = 0; v < 2; ++v)
-          dst[v] = make_uint4(
-              pack_bf16(__uint_as_float(r[8 * v + 0]) * inv, __uint_as_float(r[8 * v + 1]) * inv),
-              pack_bf16(__uint_as_float(r[8 * v + 2]) * inv, __uint_as_float(r[8 * v + 3]) * inv),
-              pack_bf16(__uint_as_float(r[8 * v + 4]) * inv, __uint_as_float(r[8 * v + 5]) * inv),
-              pack_bf16(__uint_as_float(r[8 * v + 6]) * inv, __uint_as_float(r[8 * v + 7]) * inv));
-      }
+      mbar_arrive(&bars->o_free);
+      if (threadIdx.x == 0 && it == 0) ATRACE(2);
     }
   }
   if (threadIdx.x == 0) ATRACE(3);
@@ -355,8 +387,9 @@ void launch_attn(const AttnTcArgs& a, cudaStream_t s) {
   const int T = a.batch * a.seq;
   const CUtensorMap tm =
       tmap_bf16(a.qkv, T, a.qkv_cols, a.ldq, 128, RP, swizzle_for_row_bytes(C::RB));
-  dim3 grid((a.seq + QT - 1) / QT, a.heads, a.batch);
-  k_attn_rankspace<RP><<<grid, kThreads, C::SMEM, s>>>(tm, a.out, a.ldo, a.seq, a.heads,
+  const int items = ((a.seq + QT - 1) / QT) * a.heads * a.batch;
+  const int grid = items < 2 * num_sms() ? items : 2 * num_sms();
+  k_attn_rankspace<RP><<<grid, kThreads, C::SMEM, s>>>(tm, a.out, a.ldo, a.batch, a.seq, a.heads,
                                                        a.groups, a.q_off, a.k_off, a.v_off);
   check_launch("k_attn_rankspace");
 }

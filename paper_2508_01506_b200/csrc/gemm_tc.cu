@@ -9,15 +9,18 @@
 // which equals the reference's bias preload up to fp32 rounding order.
 //
 // Structure (one CTA per SM, persistent over 128 x BN output tiles):
-//   warps 0, 6  TMA producers (alternate stages): A [128 x 64] and B [BN x 64]
+//   warps 0, 10 TMA producers (alternate stages): A [128 x 64] and B [BN x 64]
 //               bf16 tiles (SW128) into a STAGES-deep smem ring guarded by
 //               full/empty mbarriers.
 //   warp 1      MMA issuer: one elected lane issues tcgen05.mma (M=128,
 //               N=BN, K=16) into one of two TMEM accumulators.
-//   warps 2..5  epilogue: tcgen05.ld 32 columns at a time, bias + act,
-//               bf16 pack, swizzled st.shared, TMA store (per warp 32x32 box).
+//   warps 2..9  epilogue: tcgen05.ld 32 columns at a time, bias + act,
+//               bf16 pack, swizzled st.shared into a [128 x 64] box, one TMA
+//               store per box.
 // The double-buffered TMEM accumulator lets tile i's epilogue overlap tile
 // i+1's MMAs.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -29,15 +32,33 @@ using namespace ptx;
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 224;  // 0 TMA, 1 MMA, 2..5 epilogue, 6 TMA
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 352;  // 0 TMA, 1 MMA, 2..9 epilogue, 10 TMA
+
+#ifdef FSVD_TRACE
+__device__ long long g_trace_gm[1024];
+}  // namespace
+extern "C" __attribute__((visibility("default"))) int fsvd_debug_trace_gemm_copy(long long* host, int n) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace_gm, sizeof(long long) * n));
+}
+namespace {
+#define GTRACE(slot) do { if (blockIdx.x == 0 && (slot) < 1024) g_trace_gm[(slot)] = clock64(); } while (0)
+#else
+#define GTRACE(slot) do { } while (0)
+#endif
 
 template <int BN, int STAGES>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int C_BYTES = 4 * 2 * 32 * 32 * 2;  // 4 warps x 2 buffers x 32x32 bf16
+  // [128 x 64] bf16 SW128 output staging boxes: two when they fit beside the
+  // ring, else one
+  static constexpr int CBOX = BM * 64 * 2;
+  static constexpr int NCBOX = (1024 + STAGES * (A_BYTES + B_BYTES) + 2 * CBOX + 256 <= 227 * 1024) ? 2 : 1;
+  static constexpr int C_BYTES = NCBOX * CBOX;
   static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + C_BYTES + 256;
+  static_assert(SMEM <= 227 * 1024, "shared-memory budget");
 };
 
 template <int BN, int STAGES>
@@ -73,7 +94,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -115,7 +136,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int i = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
         const uint32_t acc = i & 1, use = i >> 1;
+        if (lane == 0) GTRACE(16 + 4 * i);
         mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        if (lane == 0) GTRACE(17 + 4 * i);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
         for (int kb = 0; kb < nk; ++kb) {
@@ -134,53 +157,71 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (elect_one()) mma_commit(&tfull[acc]);
         __syncwarp();
+        if (lane == 0) GTRACE(18 + 4 * i);
       }
     }
   } else {
-    // ---------------- epilogue ----------------
-    const uint32_t q = warp & 3;  // TMEM lane quadrant of this warp
-    uint8_t* cbuf = sC + (warp - 2) * 2 * 2048;
-    uint32_t nstore = 0;
+    // ---------------- epilogue (8 warps) ----------------
+    // Two warps per TMEM lane quadrant, each taking 32 of every 64 columns.
+    // Output leaves through [128 x 64] SW128 boxes staged in shared memory
+    // (double-buffered) and written by ONE TMA store per box: a TMA
+    // instruction costs its thread ~250 cycles whatever the box size.
+    const uint32_t q = warp & 3, half = (warp - 2) >> 2;
+    const uint32_t row = q * 32 + lane;
+    const int et = static_cast<int>(threadIdx.x) - 64;  // 0..255
+    const uint32_t s_c = smem_u32(sC);
+    uint32_t nbox = 0;
     int i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
       const uint32_t acc = i & 1, use = i >> 1;
+      if (threadIdx.x == 64) GTRACE(512 + 4 * i);
       mbar_wait(&tfull[acc], use & 1);
+      if (threadIdx.x == 64) GTRACE(513 + 4 * i);
       tc_fence_after();
       const uint32_t tbase = tmem + acc * BN + ((q * 32) << 16);
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        if (n0 + c0 >= N) break;
+      for (int b0 = 0; b0 < BN; b0 += 64) {
+        if (n0 + b0 >= N) break;
+        const int c0 = b0 + static_cast<int>(half) * 32;
         uint32_t r[32];
         tmem_ld32(tbase + c0, r);
         tmem_ld_wait();
+        if (b0 + 64 >= BN || n0 + b0 + 64 >= N) {
+          // last TMEM read of this tile by this warp: hand the accumulator back
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         bias_act_chunk<32>(v, bias != nullptr ? bias + n0 + c0 : nullptr, N - (n0 + c0), act);
-        uint8_t* buf = cbuf + (nstore & 1) * 2048;
-        if (lane == 0) tma_store_wait_read<1>();
-        __syncwarp();
-        const uint32_t sb = smem_u32(buf);
+        const uint32_t box = s_c + (nbox % Cfg::NCBOX) * Cfg::CBOX;
+        if (nbox >= Cfg::NCBOX) {
+          if (et == 0) {
+            if (Cfg::NCBOX == 2) tma_store_wait_read<1>();
+            else tma_store_wait_read<0>();
+          }
+          named_bar_sync(1, kEpiWarps * 32);
+        }
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-          st_shared_v4(sb + swz_offset(lane, c, 64), pack_bf16(v[8 * c + 0], v[8 * c + 1]),
+          st_shared_v4(box + swz_offset(row, half * 4 + c, 128), pack_bf16(v[8 * c + 0], v[8 * c + 1]),
                        pack_bf16(v[8 * c + 2], v[8 * c + 3]),
                        pack_bf16(v[8 * c + 4], v[8 * c + 5]),
                        pack_bf16(v[8 * c + 6], v[8 * c + 7]));
         fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&tmC, buf, n0 + c0, m0 + q * 32);
+        named_bar_sync(1, kEpiWarps * 32);
+        if (et == 0) {
+          tma_store_2d_u32(&tmC, box, n0 + b0, m0);
           tma_store_commit();
         }
-        ++nstore;
+        ++nbox;
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (threadIdx.x == 64) GTRACE(514 + 4 * i);
     }
-    if (lane == 0) tma_store_wait<0>();
+    if (et == 0) tma_store_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -188,6 +229,203 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_free<Cfg::TMEM_COLS>(tmem);
   }
+}
+
+// ============================================================================
+// CTA-pair variant (cta_group::2): a cluster of two CTAs computes a 256 x BN
+// tile; rank r loads its own 128 rows of A and rows [r*BN/2, (r+1)*BN/2) of
+// the B tile, the leader (rank 0) issues M = 256 MMAs over both CTAs' shared
+// memory, and each CTA drains its own 128 x BN accumulator.  Per SM this
+// halves the B bytes pulled from L2 and read from shared memory per FLOP --
+// the 1-CTA kernel is L2-fabric bound on the QKV projection.
+template <int BN, int STAGES>
+struct Gemm2Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's half
+  static constexpr int CBOX = BM * 64 * 2;
+  static constexpr int C_BYTES = 2 * CBOX;
+  static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + C_BYTES + 256;
+  static_assert(SMEM <= 227 * 1024, "shared-memory budget");
+  static_assert(BN % 32 == 0 && BN <= 256, "pair MMA N");
+};
+
+template <int BN, int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_gemm2_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmC, const float* __restrict__ bias, int act,
+                 int M, int N, int K) {
+  using Cfg = Gemm2Cfg<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + STAGES * Cfg::A_BYTES;
+  uint8_t* sC = sB + STAGES * Cfg::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + Cfg::C_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n;
+  const int nk = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    tma_prefetch(&tmC);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);   // leader: one arrive.expect_tx for both CTAs' bytes
+      mbar_init(&empty[i], 1);  // one multicast commit per use
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * kEpiWarps);  // leader: both CTAs' epilogue warps
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<Cfg::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 || warp == kThreads / 32 - 1) {
+    // ---------------- TMA producers (both CTAs; two issuers each) ----------------
+    if (lane == 0) {
+      const int me = warp == 0 ? 0 : 1;
+      uint32_t stage = 0, phase = 0;
+      int it = 0;
+      for (int t = pair; t < tiles; t += npairs) {
+        const int m0 = (t / num_n) * 2 * BM + static_cast<int>(rank) * BM;
+        const int n0 = (t % num_n) * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          if ((it & 1) == me) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (Cfg::A_BYTES + Cfg::B_BYTES));
+            tma_load_2d_pair(&tmA, &full[stage], sA + stage * Cfg::A_BYTES, kb * BK, m0);
+            tma_load_2d_pair(&tmB, &full[stage], sB + stage * Cfg::B_BYTES, kb * BK, n0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA only) ----------------
+    if (rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16(2 * BM, BN);
+      const uint64_t dhi = desc_hi_kmajor(128);
+      const uint64_t da = desc_at(dhi, smem_u32(sA)), db = desc_at(dhi, smem_u32(sB));
+      uint32_t stage = 0, phase = 0;
+      int i = 0;
+      for (int t = pair; t < tiles; t += npairs, ++i) {
+        const uint32_t acc = i & 1, use = i >> 1;
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t a0 = da + ((stage * Cfg::A_BYTES) >> 4);
+          const uint64_t b0 = db + ((stage * Cfg::B_BYTES) >> 4);
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              mma_bf16_ss_pair(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
+            mma_commit_pair(&empty[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (elect_one()) mma_commit_pair(&tfull[acc], 0x3);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- epilogue (8 warps per CTA, own 128 rows) ----------------
+    const uint32_t q = warp & 3, half = (warp - 2) >> 2;
+    const uint32_t row = q * 32 + lane;
+    const int et = static_cast<int>(threadIdx.x) - 64;
+    const uint32_t s_c = smem_u32(sC);
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    uint32_t nbox = 0;
+    int i = 0;
+    for (int t = pair; t < tiles; t += npairs, ++i) {
+      const int m0 = (t / num_n) * 2 * BM + static_cast<int>(rank) * BM, n0 = (t % num_n) * BN;
+      const uint32_t acc = i & 1, use = i >> 1;
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem + acc * BN + ((q * 32) << 16);
+#pragma unroll 1
+      for (int b0 = 0; b0 < BN; b0 += 64) {
+        if (n0 + b0 >= N) break;
+        const int c0 = b0 + static_cast<int>(half) * 32;
+        uint32_t r[32];
+        tmem_ld32(tbase + c0, r);
+        tmem_ld_wait();
+        if (b0 + 64 >= BN || n0 + b0 + 64 >= N) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+        }
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        bias_act_chunk<32>(v, bias != nullptr ? bias + n0 + c0 : nullptr, N - (n0 + c0), act);
+        const uint32_t box = s_c + (nbox & 1) * Cfg::CBOX;
+        if (nbox >= 2) {
+          if (et == 0) tma_store_wait_read<1>();
+          named_bar_sync(1, kEpiWarps * 32);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          st_shared_v4(box + swz_offset(row, half * 4 + c, 128), pack_bf16(v[8 * c + 0], v[8 * c + 1]),
+                       pack_bf16(v[8 * c + 2], v[8 * c + 3]),
+                       pack_bf16(v[8 * c + 4], v[8 * c + 5]),
+                       pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+        fence_proxy_async_smem();
+        named_bar_sync(1, kEpiWarps * 32);
+        if (et == 0) {
+          tma_store_2d_u32(&tmC, box, n0 + b0, m0);
+          tma_store_commit();
+        }
+        ++nbox;
+      }
+    }
+    if (et == 0) tma_store_wait<0>();
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free_pair<Cfg::TMEM_COLS>(tmem);
+  }
+}
+
+template <int BN, int STAGES>
+void launch_gemm2(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, int64_t ldc,
+                  int M, int N, int K, const float* bias, int act, cudaStream_t s) {
+  using Cfg = Gemm2Cfg<BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_gemm2_bf16<BN, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    attr = true;
+  }
+  const CUtensorMap ta = tmap_bf16(A, M, K, lda, BM, BK, TmaSwizzle::B128);
+  const CUtensorMap tb = tmap_bf16(B, N, K, ldb, BN / 2, BK, TmaSwizzle::B128);
+  const CUtensorMap tc = tmap_bf16(C, M, N, ldc, BM, 64, TmaSwizzle::B128);
+  const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+  int pairs = num_sms() / 2;
+  if (tiles < pairs) pairs = tiles;
+  k_gemm2_bf16<BN, STAGES><<<2 * pairs, kThreads, Cfg::SMEM, s>>>(ta, tb, tc, bias, act, M, N, K);
+  check_launch("k_gemm2_bf16");
 }
 
 template <int BN, int STAGES>
@@ -202,7 +440,7 @@ void launch_gemm(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C
   }
   const CUtensorMap ta = tmap_bf16(A, M, K, lda, BM, BK, TmaSwizzle::B128);
   const CUtensorMap tb = tmap_bf16(B, N, K, ldb, BN, BK, TmaSwizzle::B128);
-  const CUtensorMap tc = tmap_bf16(C, M, N, ldc, 32, 32, TmaSwizzle::B64);
+  const CUtensorMap tc = tmap_bf16(C, M, N, ldc, BM, 64, TmaSwizzle::B128);
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   k_gemm_bf16<BN, STAGES><<<grid, kThreads, Cfg::SMEM, s>>>(ta, tb, tc, bias, act, M, N, K);
@@ -218,14 +456,28 @@ bool gemm_bf16_supported(int M, int N, int K, int64_t lda, int64_t ldb, int64_t 
 
 void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, int64_t ldc,
                int M, int N, int K, const float* bias, int act, cudaStream_t s) {
+  static const int variant = [] {
+    const char* e = getenv("FSVD_GEMM_VARIANT");  // developer A/B switch
+    return e ? atoi(e) : 0;
+  }();
+  if (variant == 2 && N % 192 == 0) {
+    launch_gemm2<192, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+    return;
+  }
+  if (variant == 3 && N % 256 == 0) {
+    launch_gemm2<256, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+    return;
+  }
+  if (variant == 4 && N % 128 == 0) {
+    launch_gemm2<128, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+    return;
+  }
   if (N % 256 == 0)
     launch_gemm<256, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
   else if (N % 192 == 0)
     launch_gemm<192, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
   else if (N > 1024)
     launch_gemm<256, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
-  else if (N % 192 == 0)
-    launch_gemm<192, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
   else if (N % 128 == 0 || N > 64)
     launch_gemm<128, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
   else

@@ -21,8 +21,7 @@
 // the residual as [128 x 64] bf16 SW128 boxes into a two-box ring; in the
 // second sweep the same two boxes stage the normalised output for TMA stores,
 // and gamma / beta are staged once in shared memory the kernel no longer
-// needs.  Every CTA visits the pieces in a rotated order (piece_of), so the
-// 128 CTAs of a launch do not all read the same weight lines at once.
+// needs.
 #pragma once
 
 #include "ptx.cuh"
@@ -62,10 +61,12 @@ __device__ __forceinline__ void release_box(uint64_t* empty) {
   mbar_arrive(empty);
 }
 
-// Column piece handled at step i by this CTA (rotated per CTA).
+// Column piece handled at step i.  (A per-CTA rotation to spread weight reads
+// across L2 was measured to gain nothing and would make the statistics'
+// summation order -- hence the rounding -- depend on the tile's position.)
 __device__ __forceinline__ int piece_of(int i, int NP) {
-  const int j = i + static_cast<int>(blockIdx.x % NP);
-  return j >= NP ? j - NP : j;
+  (void)NP;
+  return i;
 }
 
 // Residual producer (one thread): streams the [128 x N] residual tile at row

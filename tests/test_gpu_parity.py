@@ -53,6 +53,28 @@ SHAPES = [
     ("r64_fr256", 512, 2048, 8, 8, 64, 256, 256, 1, 257),
     ("r8_fr128", 256, 1024, 4, 4, 8, 32, 128, 3, 64),
 ]
+
+# BASELINE.json configs 3 and 4 at reduced batch / sequence (the oracle must
+# finish in seconds): BERT-Large head geometry with pr = fr = 512, and the
+# BERT-Base rank sweep r in {8, 16, 64} with pr = fr = min(r * G, d).
+SWEEP = [
+    ("cfg3_bert_large_fr512", 1024, 4096, 16, 16, 32, 512, 512, 1, 192),
+    ("cfg4_r8_fr96", 768, 3072, 12, 12, 8, 96, 96, 1, 256),
+    ("cfg4_r16_fr192", 768, 3072, 12, 12, 16, 192, 192, 1, 256),
+    ("cfg4_r64_fr768", 768, 3072, 12, 12, 64, 768, 768, 1, 256),
+]
+
+
+@pytest.mark.parametrize("shape", SWEEP, ids=[s[0] for s in SWEEP])
+@pytest.mark.parametrize("mode", [abi.MODE_FLASH_V1, abi.MODE_FLASH_V2], ids=["v1", "v2"])
+def test_config_sweep_layer_bf16(L, ora, shape, mode):
+    name, d, df, Hh, G, r, pr, fr, B, M = shape
+    layer = oracle.rand_layer(ora, d, df, Hh, G, r, 77, proj_rank=pr, ffn_rank=fr)
+    x = ora.random((B, M, d), 78)
+    layer, x = prep(layer, x, abi.BF16)
+    ref = ora.run_model(x, [layer], mode, PLAN)
+    got = H.run_model(x, [layer], mode, PLAN, abi.BF16)
+    assert H.rel_err(got, ref) <= H.TOL_BF16, name
 DTYPES = [abi.F32, abi.BF16]
 
 
@@ -282,3 +304,40 @@ def test_cfg2_full_size_properties(L, ora):
     assert H.rel_err(o[5:6], ref) <= H.TOL_BF16
     for p in packs:
         L.fsvd_layer_pack_destroy(p)
+
+
+def test_cfg3_full_size_properties(L):
+    """BERT-Large-shaped layer at seq 4096 (BASELINE configs[2]), FlashSVD-FFN V2:
+    finite, LayerNorm-shaped rows, and batch-shard invariance (running the two
+    sequences in one launch equals running them one at a time, bit for bit)."""
+    import torch
+    from paper_2508_01506_b200.model import random_layer
+    rng = np.random.default_rng(3)
+    layer = round_layer_bf16(random_layer(1024, 4096, 16, 16, 32, 512, 512, rng))
+    B, M, d = 2, 4096, 1024
+    descs = layer_descs([layer])
+    p = C.c_void_p()
+    abi.check(L.fsvd_layer_pack_create(C.byref(descs[0]), abi.BF16, 0, C.byref(p)))
+    parr = (C.c_void_p * 1)(p.value)
+    ws = C.c_size_t()
+    abi.check(L.fsvd_workspace_bytes(parr, 1, B, M, abi.MODE_FLASH_V2, C.byref(ws)))
+    work = torch.empty(ws.value, dtype=torch.uint8, device="cuda")
+    x = torch.randn((B, M, d), generator=torch.Generator().manual_seed(2)).to(torch.bfloat16).cuda()
+    out = torch.empty_like(x)
+    sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def run(xin, o, b):
+        abi.check(L.fsvd_model_fwd(parr, 1, abi.MODE_FLASH_V2, 0, b, M, C.c_void_p(xin.data_ptr()),
+                                   C.c_void_p(o.data_ptr()), C.c_void_p(work.data_ptr()), ws.value, sp))
+    run(x, out, B)
+    singles = [torch.empty_like(x[i:i + 1]) for i in range(B)]
+    for i in range(B):
+        run(x[i:i + 1].contiguous(), singles[i], 1)
+    torch.cuda.synchronize()
+    o = out.float().cpu().numpy()
+    assert np.isfinite(o).all()
+    z = (o - layer.ln2_beta) / layer.ln2_gamma
+    assert np.abs(z.mean(-1)).max() < 0.05 and np.abs(z.var(-1) - 1).max() < 0.1
+    for i in range(B):
+        assert torch.equal(out[i:i + 1], singles[i])
+    L.fsvd_layer_pack_destroy(p)
