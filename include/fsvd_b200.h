@@ -240,6 +240,22 @@ fsvd_status fsvd_model_fwd(const fsvd_layer_pack* const* packs, size_t n_layers,
                            const void* x, void* out, void* workspace,
                            size_t workspace_bytes, void* stream);
 
+/* Serving loop over host memory: runs n_batches forwards of [batch, seq, d]
+ * bf16 activations read from x_host[i] and written to out_host[i] (pinned host
+ * buffers; the same pointer may repeat).  Host->device copies, the forward and
+ * device->host copies of consecutive batches overlap on three streams through
+ * two device slots; everything is ordered before the caller's `stream`, so an
+ * event recorded on it after the call covers all copies.  workspace must hold
+ * fsvd_stream_workspace_bytes(). */
+fsvd_status fsvd_stream_workspace_bytes(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                        size_t batch, size_t seq, fsvd_run_mode mode,
+                                        size_t* bytes);
+fsvd_status fsvd_model_fwd_stream(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                  fsvd_run_mode mode, int pre_ln, size_t batch, size_t seq,
+                                  size_t n_batches, const void* const* x_host,
+                                  void* const* out_host, void* workspace, size_t workspace_bytes,
+                                  void* stream);
+
 /* ------------------------------------------------------------------ */
 /* Host API: behavioural drop-ins for the reference free functions.     */
 /* fp32 host in/out, synchronous; H2D -> kernels -> D2H inside.  Shapes, */

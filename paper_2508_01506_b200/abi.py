@@ -125,6 +125,9 @@ def _declare(lib):
         "fsvd_ffn_fwd": (st, [vp, C.c_int, _sz, _sz, vp, vp, vp, _sz, vp]),
         "fsvd_layer_fwd": (st, [vp, C.c_int, C.c_int, _sz, _sz, vp, vp, vp, _sz, vp]),
         "fsvd_model_fwd": (st, [P(vp), _sz, C.c_int, C.c_int, _sz, _sz, vp, vp, vp, _sz, vp]),
+        "fsvd_stream_workspace_bytes": (st, [P(vp), _sz, _sz, _sz, C.c_int, P(_sz)]),
+        "fsvd_model_fwd_stream": (st, [P(vp), _sz, C.c_int, C.c_int, _sz, _sz, _sz, P(vp), P(vp),
+                                       vp, _sz, vp]),
         "fsvd_flash_svd_attention": (st, [_fp, _sz, _sz, _sz, P(AttnDesc), _sz, P(TilePlan),
                                           C.c_int, vp, C.c_char_p, _fp, _sz, _sz, _sz]),
         "fsvd_lowrank_output_projection": (st, [_fp, _sz, _sz, _sz, P(LinearDesc), C.c_int, vp,

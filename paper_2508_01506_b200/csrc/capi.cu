@@ -636,6 +636,103 @@ fsvd_status fsvd_model_fwd(const fsvd_layer_pack* const* packs, size_t n_layers,
   });
 }
 
+namespace {
+size_t stream_slot_bytes(const fsvd_layer_pack* const* packs, size_t batch, size_t seq) {
+  const Pack& p0 = *packs[0]->p;
+  return (batch * seq * p0.d * p0.es + 255) & ~size_t(255);
+}
+// Internal copy streams and events of the serving loop (one set per thread).
+struct StreamSet {
+  cudaStream_t in = nullptr, out = nullptr;
+  cudaEvent_t h2d[2], comp[2], d2h[2];
+  int device = -1;
+  ~StreamSet() {
+    if (in) {
+      cudaStreamDestroy(in);
+      cudaStreamDestroy(out);
+      for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(h2d[i]);
+        cudaEventDestroy(comp[i]);
+        cudaEventDestroy(d2h[i]);
+      }
+    }
+  }
+};
+StreamSet& stream_set() {
+  thread_local StreamSet ss;
+  int dev = 0;
+  FSVD_CUDA_CHECK(cudaGetDevice(&dev));
+  if (ss.in == nullptr || ss.device != dev) {
+    FSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&ss.in, cudaStreamNonBlocking));
+    FSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&ss.out, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      FSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ss.h2d[i], cudaEventDisableTiming));
+      FSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ss.comp[i], cudaEventDisableTiming));
+      FSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ss.d2h[i], cudaEventDisableTiming));
+    }
+    ss.device = dev;
+  }
+  return ss;
+}
+}  // namespace
+
+fsvd_status fsvd_stream_workspace_bytes(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                        size_t batch, size_t seq, fsvd_run_mode mode,
+                                        size_t* bytes) {
+  return guard([&] {
+    if (!bytes || !packs || n_layers == 0) fail(Kind::Config, "null argument");
+    check_mode(mode);
+    size_t ws = 0;
+    for (size_t i = 0; i < n_layers; ++i)
+      ws = std::max(ws, layer_workspace_bytes(*packs[i]->p, batch * seq, mode));
+    *bytes = ws + 2 * stream_slot_bytes(packs, batch, seq) + 256;
+  });
+}
+
+fsvd_status fsvd_model_fwd_stream(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                  fsvd_run_mode mode, int pre_ln, size_t batch, size_t seq,
+                                  size_t n_batches, const void* const* x_host,
+                                  void* const* out_host, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  return guard([&] {
+    check_mode(mode);
+    if (!packs || n_layers == 0 || (n_batches && (!x_host || !out_host)))
+      fail(Kind::Config, "null argument");
+    require_device();
+    size_t need = 0;
+    for (size_t i = 0; i < n_layers; ++i)
+      need = std::max(need, layer_workspace_bytes(*packs[i]->p, batch * seq, mode));
+    const size_t slot = stream_slot_bytes(packs, batch, seq);
+    if (ws_bytes < need + 2 * slot + 256)
+      fail(Kind::Config, "workspace too small: need " + std::to_string(need + 2 * slot + 256) +
+                             " bytes (fsvd_stream_workspace_bytes)");
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+    uint8_t* dev[2] = {base, base + slot};
+    void* model_ws = base + 2 * slot;
+    const size_t bytes = batch * seq * packs[0]->p->d * packs[0]->p->es;
+    cudaStream_t sc = static_cast<cudaStream_t>(stream);
+    StreamSet& ss = stream_set();
+    for (size_t i = 0; i < n_batches; ++i) {
+      const int k = static_cast<int>(i & 1);
+      // slot k is free once batch i-2 has been copied out of it
+      if (i >= 2) FSVD_CUDA_CHECK(cudaStreamWaitEvent(ss.in, ss.d2h[k], 0));
+      FSVD_CUDA_CHECK(cudaMemcpyAsync(dev[k], x_host[i], bytes, cudaMemcpyHostToDevice, ss.in));
+      FSVD_CUDA_CHECK(cudaEventRecord(ss.h2d[k], ss.in));
+      FSVD_CUDA_CHECK(cudaStreamWaitEvent(sc, ss.h2d[k], 0));
+      for (size_t l = 0; l < n_layers; ++l)
+        layer_fwd(*packs[l]->p, mode, pre_ln != 0, batch, seq, dev[k], dev[k], model_ws,
+                  ws_bytes - (static_cast<uint8_t*>(model_ws) - static_cast<uint8_t*>(ws)), sc);
+      FSVD_CUDA_CHECK(cudaEventRecord(ss.comp[k], sc));
+      FSVD_CUDA_CHECK(cudaStreamWaitEvent(ss.out, ss.comp[k], 0));
+      FSVD_CUDA_CHECK(cudaMemcpyAsync(out_host[i], dev[k], bytes, cudaMemcpyDeviceToHost, ss.out));
+      FSVD_CUDA_CHECK(cudaEventRecord(ss.d2h[k], ss.out));
+    }
+    // the caller's stream covers every copy
+    for (size_t i = n_batches >= 2 ? n_batches - 2 : 0; i < n_batches; ++i)
+      FSVD_CUDA_CHECK(cudaStreamWaitEvent(sc, ss.d2h[i & 1], 0));
+  });
+}
+
 // ---------------------------------------------------------------- host API
 fsvd_status fsvd_flash_svd_attention(const float* x, size_t batch, size_t seq, size_t width,
                                      const fsvd_attn_desc* set, size_t heads,

@@ -341,3 +341,43 @@ def test_cfg3_full_size_properties(L):
     for i in range(B):
         assert torch.equal(out[i:i + 1], singles[i])
     L.fsvd_layer_pack_destroy(p)
+
+
+def test_stream_serving_loop_matches_device_api(L):
+    """fsvd_model_fwd_stream (host buffers, overlapped copies on internal
+    streams) returns, for every batch, exactly what fsvd_model_fwd returns."""
+    import torch
+    from paper_2508_01506_b200.model import random_layer
+    rng = np.random.default_rng(11)
+    layers = [round_layer_bf16(random_layer(256, 512, 4, 4, 32, 64, 128, rng)) for _ in range(2)]
+    B, M, d, n = 3, 130, 256, 5
+    descs = layer_descs(layers)
+    packs = []
+    for i in range(2):
+        p = C.c_void_p()
+        abi.check(L.fsvd_layer_pack_create(C.byref(descs[i]), abi.BF16, 0, C.byref(p)))
+        packs.append(p)
+    parr = (C.c_void_p * 2)(*[p.value for p in packs])
+    sws, ws = C.c_size_t(), C.c_size_t()
+    abi.check(L.fsvd_stream_workspace_bytes(parr, 2, B, M, abi.MODE_FLASH_V2, C.byref(sws)))
+    abi.check(L.fsvd_workspace_bytes(parr, 2, B, M, abi.MODE_FLASH_V2, C.byref(ws)))
+    work = torch.empty(sws.value, dtype=torch.uint8, device="cuda")
+    g = torch.Generator().manual_seed(4)
+    xs = [torch.randn((B, M, d), generator=g).to(torch.bfloat16).pin_memory() for _ in range(n)]
+    outs = [torch.empty_like(x).pin_memory() for x in xs]
+    xa = (C.c_void_p * n)(*[x.data_ptr() for x in xs])
+    oa = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+    st = torch.cuda.current_stream()
+    abi.check(L.fsvd_model_fwd_stream(parr, 2, abi.MODE_FLASH_V2, 0, B, M, n, xa, oa,
+                                      C.c_void_p(work.data_ptr()), sws.value, C.c_void_p(st.cuda_stream)))
+    st.synchronize()
+    for i in range(n):
+        xd = xs[i].cuda()
+        od = torch.empty_like(xd)
+        abi.check(L.fsvd_model_fwd(parr, 2, abi.MODE_FLASH_V2, 0, B, M, C.c_void_p(xd.data_ptr()),
+                                   C.c_void_p(od.data_ptr()), C.c_void_p(work.data_ptr()), ws.value,
+                                   C.c_void_p(st.cuda_stream)))
+        st.synchronize()
+        assert torch.equal(od.cpu(), outs[i]), i
+    for p in packs:
+        L.fsvd_layer_pack_destroy(p)
