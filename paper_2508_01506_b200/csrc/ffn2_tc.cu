@@ -1,0 +1,430 @@
+// ffn2_tc.cu -- K4 on a CTA pair: FlashSVD-FFN V2 with cta_group::2 MMAs.
+//
+// Same dataflow as k_ffn<FR, true> (ffn_tc.cu; ffn_v2, ffn.cpp:158-185):
+//     P = X U_up ; Z = sum_f act(P V_up[:, f] + b_up[f]) U_down[f, :] ;
+//     out = Z V_down + b_down   (optionally LN(x + out), ln_epi.cuh)
+// but a cluster of two CTAs on one TPC owns 256 token rows: each CTA keeps
+// its own 128 rows of X, P, H and Z (shared memory / TMEM) and streams only
+// HALF of every weight slot; the even CTA issues M = 256 MMAs that read A
+// from both CTAs and B (the weights) split between them.  Per SM this halves
+// the weight bytes pulled from L2 and the B-operand bytes read from shared
+// memory -- the single-CTA kernel is shared-memory-bandwidth bound (N = 128
+// SS MMAs alone read 128 B/clk, TMA fills and the H tile come on top).
+//
+// Barrier ownership: the leader (rank 0) owns every barrier the MMA issuer
+// waits on (full, x_full, p_ready, h_free, sh_full, zs_ready, o_free); TMA
+// bytes of both CTAs complete on the leader's full barriers and the peer's
+// epilogue warps arrive remotely.  Barriers the MMA signals (empty, x_empty,
+// p_acc, h_full, sh_free, z_full, o_full) exist in both CTAs and receive a
+// multicast commit.
+//
+// Warps: 0 and 11 TMA producers, 1 MMA issuer (leader) + TMEM owner, 2..9
+// epilogue, 10 residual producer of the fused LN.
+#include "common.cuh"
+#include "kernels.cuh"
+#include "ln_epi.cuh"
+#include "ptx.cuh"
+
+namespace fsvd {
+namespace {
+
+using namespace ptx;
+
+constexpr int kThreads = 384;
+constexpr int kEpiWarps = 8;
+constexpr int BMr = 128;            // token rows per CTA (256 per pair)
+constexpr int BF = 128;             // features per block
+constexpr int ATOM = BMr * 128;     // [128 x 64] bf16 SW128 atom of own rows (16 KB)
+constexpr int HSLOT = 64 * 128;     // ring slot: half of a 128-row weight box (8 KB)
+constexpr int STAGE = 2 * HSLOT;
+
+template <int FR>
+struct Ffn2Cfg {
+  static_assert(FR % 128 == 0 && FR <= 384, "pair FFN: FR in {128, 256, 384}");
+  static constexpr int NATOM = FR / 64;
+  static constexpr int PS = 128;  // Z / P piece width (pair MMA N)
+  static constexpr int NPIECE = FR / PS;
+  static constexpr int STAGES_FIT = (227 * 1024 - 2048 - (NATOM + 2) * ATOM) / STAGE;
+  static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
+  static constexpr int o_p = 0;
+  static constexpr int o_h = NATOM * ATOM;
+  static constexpr int o_ring = o_h + 2 * ATOM;
+  static constexpr int o_bar = o_ring + STAGES * STAGE;
+  static constexpr int SMEM = 1024 + o_bar + 1024;
+  static constexpr int t_z = 0, t_h = 384;
+  static_assert(SMEM <= 227 * 1024, "shared-memory budget");
+};
+
+struct Ffn2Bars {
+  uint64_t full[12], empty[12];
+  uint64_t x_full[2], x_empty[2];
+  uint64_t p_acc, p_ready, h_full, h_free, sh_full[2], sh_free[2], z_full, zs_ready;
+  uint64_t o_full[2], o_free[2];
+  uint64_t res_full[2], res_empty[2];
+  uint32_t tmem;
+};
+static_assert(sizeof(Ffn2Bars) <= 1024, "barrier block");
+
+__device__ __forceinline__ void ld_chunk(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  tmem_ld32(taddr, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void st_chunk_smem(uint32_t tile, uint32_t row, int c0,
+                                              const float (&v)[32]) {
+  const uint32_t atom = tile + (c0 >> 6) * ATOM;
+  const int cc = (c0 & 63) >> 3;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    st_shared_v4(atom + swz_offset(row, cc + c, 128), pack_bf16(v[8 * c + 0], v[8 * c + 1]),
+                 pack_bf16(v[8 * c + 2], v[8 * c + 3]), pack_bf16(v[8 * c + 4], v[8 * c + 5]),
+                 pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+}
+__device__ __forceinline__ void st_chunk_global(bf16* dst, const float (&v)[32]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    d[c] = make_uint4(pack_bf16(v[8 * c + 0], v[8 * c + 1]), pack_bf16(v[8 * c + 2], v[8 * c + 3]),
+                      pack_bf16(v[8 * c + 4], v[8 * c + 5]), pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+}
+// Epilogue warp -> leader barrier (after the caller's per-thread fences).
+__device__ __forceinline__ void warp_arrive_leader(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
+}
+
+template <int FR>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_ffn2(const __grid_constant__ CUtensorMap tmX,    // X [T, d]        box 128 x 64
+           const __grid_constant__ CUtensorMap tmUup,  // U_up^T [FR, d]  box 64 x 64
+           const __grid_constant__ CUtensorMap tmVup,  // V_up^T [df, FR] box 64 x 64
+           const __grid_constant__ CUtensorMap tmUdn,  // U_dn^T [FR, df] box 64 x 64
+           const __grid_constant__ CUtensorMap tmVdn,  // V_dn^T [d, FR]  box QS/2 x 64
+           const __grid_constant__ CUtensorMap tmY,    // out [T, d]      box 128 x 64 (LN)
+           const float* __restrict__ b_up, const float* __restrict__ b_dn, int act, int T,
+           int d_model, int d_ff, bf16* __restrict__ out, const float* __restrict__ ln_g,
+           const float* __restrict__ ln_b, float ln_eps) {
+  using C = Ffn2Cfg<FR>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  Ffn2Bars* bars = reinterpret_cast<Ffn2Bars*>(smem + C::o_bar);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_rank();
+  const int m0 = (blockIdx.x >> 1) * (2 * BMr) + static_cast<int>(rank) * BMr;  // own rows
+  const int NB = (d_ff + BF - 1) / BF;
+  const int KC = d_model / 64;
+  const bool fuse_ln = ln_g != nullptr;
+  const int QS = fuse_ln ? 64 : 128;  // output columns per piece (pair MMA N)
+  const int NQ = d_model / QS;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmX);
+    tma_prefetch(&tmUup);
+    tma_prefetch(&tmVup);
+    tma_prefetch(&tmUdn);
+    tma_prefetch(&tmVdn);
+    if (fuse_ln) tma_prefetch(&tmY);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&bars->full[i], 1);
+      mbar_init(&bars->empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->x_full[i], 1);
+      mbar_init(&bars->x_empty[i], 1);
+      mbar_init(&bars->sh_full[i], 2 * kEpiWarps);
+      mbar_init(&bars->sh_free[i], 1);
+      mbar_init(&bars->o_full[i], 1);
+      mbar_init(&bars->o_free[i], 2 * kEpiWarps);
+      mbar_init(&bars->res_full[i], 1);
+      mbar_init(&bars->res_empty[i], lnepi::res_box_readers<64>());
+    }
+    mbar_init(&bars->p_acc, 1);
+    mbar_init(&bars->p_ready, 2 * kEpiWarps);
+    mbar_init(&bars->h_full, 1);
+    mbar_init(&bars->h_free, 2 * kEpiWarps);
+    mbar_init(&bars->z_full, 1);
+    mbar_init(&bars->zs_ready, 2 * kEpiWarps);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<512>(&bars->tmem);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem;
+  uint8_t* ring = smem + C::o_ring;
+
+  if (warp == 0 || warp == 11) {
+    // ================================================= TMA producers (both CTAs)
+    if (lane == 0) {
+      const uint32_t me = warp == 0 ? 0 : 1;
+      uint32_t st = 0, ph = 0, it = 0;
+      // n half-slots, two per stage; slot(i, dst) issues half-slot i and
+      // returns its bytes.  The leader arms the full barrier for both CTAs.
+      auto emit = [&](int n, auto&& slot, uint32_t slot_bytes) {
+        for (int i = 0; i < n; i += 2, ++it) {
+          if ((it & 1) == me) {
+            mbar_wait(&bars->empty[st], ph ^ 1);
+            const int k = (i + 1 < n) ? 2 : 1;
+            if (rank == 0) mbar_arrive_expect_tx(&bars->full[st], 2 * k * slot_bytes);
+            uint8_t* base = ring + st * STAGE;
+            slot(i, base);
+            if (k == 2) slot(i + 1, base + HSLOT);
+          }
+          if (++st == C::STAGES) { st = 0; ph ^= 1; }
+        }
+      };
+      const int hr = static_cast<int>(rank) * 64;  // this CTA's half of a 128-row weight box
+      for (int kc = 0; kc < KC; ++kc) {
+        const int xb = kc & 1;
+        if (static_cast<uint32_t>(xb) == me) {
+          mbar_wait(&bars->x_empty[xb], ((kc >> 1) & 1) ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&bars->x_full[xb], 2 * ATOM);
+          tma_load_2d_pair(&tmX, &bars->x_full[xb], smem + C::o_h + xb * ATOM, kc * 64, m0);
+        }
+        emit(C::NPIECE, [&](int p, uint8_t* dst) {
+          tma_load_2d_pair(&tmUup, &bars->full[st], dst, kc * 64, p * C::PS + hr);
+        }, HSLOT);
+      }
+      auto mma1_slots = [&](int f) {
+        emit(C::NATOM, [&](int a, uint8_t* dst) {
+          tma_load_2d_pair(&tmVup, &bars->full[st], dst, a * 64, f * BF + hr);
+        }, HSLOT);
+      };
+      auto mma2_slots = [&](int f) {  // atom-major: (a0: p0..), (a1: p0..)
+        emit(2 * C::NPIECE, [&](int j, uint8_t* dst) {
+          const int a = j / C::NPIECE, p = j % C::NPIECE;
+          tma_load_2d_pair(&tmUdn, &bars->full[st], dst, f * BF + a * 64, p * C::PS + hr);
+        }, HSLOT);
+      };
+      mma1_slots(0);
+      for (int f = 0; f < NB; ++f) {
+        if (f + 1 < NB) mma1_slots(f + 1);
+        mma2_slots(f);
+      }
+      for (int q = 0; q < NQ; ++q)
+        emit(C::NATOM, [&](int a, uint8_t* dst) {
+          tma_load_2d_pair(&tmVdn, &bars->full[st], dst, a * 64, q * QS + static_cast<int>(rank) * (QS / 2));
+        }, (QS / 2) * 128);
+    }
+    __syncwarp();
+  } else if (warp == 10) {
+    // ================================================= residual producer (fused LN)
+    if (fuse_ln && lane == 0) {
+      mbar_wait(&bars->z_full, 0);
+      lnepi::produce_residual<64>(&tmX, smem + C::o_h, bars->res_full, bars->res_empty, 2,
+                                  d_model, m0);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ================================================= MMA issuer (leader only)
+    if (rank == 0) {
+      uint32_t st = 0, ph = 0;
+      const uint64_t dhi = desc_hi_kmajor(128);
+      const uint64_t d_p = desc_at(dhi, smem_u32(smem + C::o_p));
+      const uint64_t d_h = desc_at(dhi, smem_u32(smem + C::o_h));
+      const uint64_t d_ring = desc_at(dhi, smem_u32(ring));
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one()) mma_commit_pair(bar, 0x3);
+        __syncwarp();
+      };
+      auto consume = [&](int n, auto&& fn) {
+        for (int i = 0; i < n; i += 2) {
+          mbar_wait(&bars->full[st], ph);
+          tc_fence_after();
+          const uint64_t base = d_ring + ((st * STAGE) >> 4);
+          fn(i, base);
+          if (i + 1 < n) fn(i + 1, base + (HSLOT >> 4));
+          commit(&bars->empty[st]);
+          if (++st == C::STAGES) { st = 0; ph ^= 1; }
+        }
+      };
+      auto mma4 = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, bool acc0) {
+        if (elect_one()) {
+          mma_bf16_ss_pair(d, a, b, idesc, acc0 ? 1u : 0u);
+          mma_bf16_ss_pair(d, a + 2, b + 2, idesc, 1u);
+          mma_bf16_ss_pair(d, a + 4, b + 4, idesc, 1u);
+          mma_bf16_ss_pair(d, a + 6, b + 6, idesc, 1u);
+        }
+        __syncwarp();
+      };
+      constexpr uint32_t kAtom = ATOM >> 4;
+      constexpr uint32_t id128 = idesc_bf16(2 * BMr, 128);
+      // P = X U_up into the Z columns
+      for (int kc = 0; kc < KC; ++kc) {
+        const int xb = kc & 1;
+        mbar_wait(&bars->x_full[xb], (kc >> 1) & 1);
+        tc_fence_after();
+        consume(C::NPIECE, [&](int p, uint64_t slot) {
+          mma4(tmem + C::t_z + p * C::PS, d_h + xb * kAtom, slot, id128, kc != 0);
+        });
+        commit(&bars->x_empty[xb]);
+      }
+      commit(&bars->p_acc);
+      mbar_wait(&bars->p_ready, 0);
+      tc_fence_after();
+      auto mma1 = [&](int f) {
+        if (f > 0) {
+          mbar_wait(&bars->h_free, (f - 1) & 1);
+          tc_fence_after();
+        }
+        consume(C::NATOM, [&](int a, uint64_t slot) {
+          mma4(tmem + C::t_h, d_p + a * kAtom, slot, id128, a != 0);
+        });
+        commit(&bars->h_full);
+      };
+      auto mma2 = [&](int f) {
+        consume(2 * C::NPIECE, [&](int j, uint64_t slot) {
+          const int a = j / C::NPIECE, p = j % C::NPIECE;
+          if (p == 0) {
+            mbar_wait(&bars->sh_full[a], f & 1);
+            tc_fence_after();
+          }
+          mma4(tmem + C::t_z + p * C::PS, d_h + a * kAtom, slot, id128, (f | a) != 0);
+          if (p == C::NPIECE - 1) commit(&bars->sh_free[a]);
+        });
+      };
+      mma1(0);
+      for (int f = 0; f < NB; ++f) {
+        if (f + 1 < NB) mma1(f + 1);
+        mma2(f);
+      }
+      commit(&bars->z_full);
+      mbar_wait(&bars->zs_ready, 0);
+      tc_fence_after();
+      const uint32_t idq = fuse_ln ? idesc_bf16(2 * BMr, 64) : idesc_bf16(2 * BMr, 128);
+      for (int q = 0; q < NQ; ++q) {
+        if (q >= 2) {
+          mbar_wait(&bars->o_free[q & 1], ((q >> 1) - 1) & 1);
+          tc_fence_after();
+        }
+        consume(C::NATOM, [&](int a, uint64_t slot) {
+          mma4(tmem + (q & 1) * QS, d_p + a * kAtom, slot, idq, a != 0);
+        });
+        commit(&bars->o_full[q & 1]);
+      }
+    }
+  } else {
+    // ================================================= epilogue (8 warps, own rows)
+    const uint32_t quad = warp & 3;
+    const uint32_t half = (warp - 2) >> 2;
+    const uint32_t row = quad * 32 + lane;
+    const uint32_t loff = (quad * 32) << 16;
+    const int grow = m0 + static_cast<int>(row);
+    const uint32_t s_p = smem_u32(smem + C::o_p), s_h = smem_u32(smem + C::o_h);
+    mbar_wait(&bars->p_acc, 0);
+    tc_fence_after();
+    for (int c = half; c < FR / 32; c += 2) {
+      float v[32];
+      ld_chunk(tmem + C::t_z + loff + c * 32, v);
+      st_chunk_smem(s_p, row, c * 32, v);
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    warp_arrive_leader(&bars->p_ready);
+    for (int f = 0; f < NB; ++f) {
+      float bb[2][32];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int fb = f * BF + (half + 2 * i) * 32;
+        load_bias<32>(bb[i], b_up + fb, d_ff - fb);
+      }
+      mbar_wait(&bars->h_full, f & 1);
+      tc_fence_after();
+      float v[2][32];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) ld_chunk(tmem + C::t_h + loff + (half + 2 * i) * 32, v[i]);
+      tc_fence_before();
+      warp_arrive_leader(&bars->h_free);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        bias_act_chunk2<32>(v[i], bb[i], act);
+        if (f > 0) mbar_wait(&bars->sh_free[i], (f - 1) & 1);
+        st_chunk_smem(s_h, row, (half + 2 * i) * 32, v[i]);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        warp_arrive_leader(&bars->sh_full[i]);
+      }
+    }
+    mbar_wait(&bars->z_full, 0);
+    tc_fence_after();
+    for (int c = half; c < FR / 32; c += 2) {
+      float v[32];
+      ld_chunk(tmem + C::t_z + loff + c * 32, v);
+      st_chunk_smem(s_p, row, c * 32, v);
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    warp_arrive_leader(&bars->zs_ready);
+    if (fuse_ln) {
+      lnepi::run<64>(tmem, quad, half, row, d_model, b_dn, smem_u32(smem + C::o_h),
+                     bars->res_full, bars->res_empty, 2, ln_g, ln_b, ln_eps, &tmY, m0,
+                     reinterpret_cast<float*>(ring), bars->o_full, bars->o_free, 1,
+                     mapa_shared(smem_u32(&bars->o_free[0]), 0));
+    } else {
+      for (int q = 0; q < NQ; ++q) {
+        mbar_wait(&bars->o_full[q & 1], (q >> 1) & 1);
+        tc_fence_after();
+        for (int c = half; c < QS / 32; c += 2) {
+          float v[32];
+          ld_chunk(tmem + (q & 1) * QS + loff + c * 32, v);
+          const int n0 = q * QS + c * 32;
+          bias_act_chunk<32>(v, b_dn + n0, 32, 3);
+          if (grow < T) st_chunk_global(out + (int64_t)grow * d_model + n0, v);
+        }
+        tc_fence_before();
+        warp_arrive_leader(&bars->o_free[q & 1]);
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free_pair<512>(tmem);
+  }
+}
+
+template <int FR>
+void launch_ffn2(const FfnTcArgs& a, cudaStream_t s) {
+  using C = Ffn2Cfg<FR>;
+  static bool attr = false;
+  if (!attr) {
+    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_ffn2<FR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM));
+    attr = true;
+  }
+  const bool ln = a.ln_g != nullptr;
+  const int qs = ln ? 64 : 128;
+  const CUtensorMap tx = tmap_bf16(a.x, a.T, a.d_model, a.d_model, BMr, 64, TmaSwizzle::B128);
+  const CUtensorMap tup = tmap_bf16(a.up_u_t, FR, a.d_model, a.d_model, 64, 64, TmaSwizzle::B128);
+  const CUtensorMap tvup = tmap_bf16(a.up_v_t, a.d_ff, FR, FR, 64, 64, TmaSwizzle::B128);
+  const CUtensorMap tudn = tmap_bf16(a.dn_u_t, FR, a.d_ff, a.d_ff, 64, 64, TmaSwizzle::B128);
+  const CUtensorMap tvdn = tmap_bf16(a.dn_v_t, a.d_model, FR, FR, qs / 2, 64, TmaSwizzle::B128);
+  const CUtensorMap ty =
+      ln ? tmap_bf16(a.out, a.T, a.d_model, a.d_model, BMr, 64, TmaSwizzle::B128) : tx;
+  const int pairs = (a.T + 2 * BMr - 1) / (2 * BMr);
+  k_ffn2<FR><<<2 * pairs, kThreads, C::SMEM, s>>>(tx, tup, tvup, tudn, tvdn, ty, a.up_b, a.dn_b,
+                                                 a.act, a.T, a.d_model, a.d_ff, a.out, a.ln_g,
+                                                 a.ln_b, a.ln_eps);
+  check_launch("k_ffn2");
+}
+
+}  // namespace
+
+bool ffn_pair_supported(int d_model, int d_ff, int rank_pad) {
+  return d_model % 128 == 0 && d_ff % 128 == 0 && rank_pad % 128 == 0 && rank_pad <= 384;
+}
+
+void ffn_fused_pair_bf16(const FfnTcArgs& a, cudaStream_t s) {
+  switch (a.rank_pad) {
+    case 128: launch_ffn2<128>(a, s); break;
+    case 256: launch_ffn2<256>(a, s); break;
+    case 384: launch_ffn2<384>(a, s); break;
+    default: throw CudaError("ffn_fused_pair_bf16: unsupported FFN rank padding");
+  }
+}
+
+}  // namespace fsvd

@@ -73,6 +73,10 @@ struct FfnTcArgs {
 };
 void ffn_stream_bf16(const FfnTcArgs& a, cudaStream_t s);   // V1 middle: P -> Z
 void ffn_fused_bf16(const FfnTcArgs& a, cudaStream_t s);    // V2: X -> out
+// V2 on a CTA pair (cta_group::2, 256 rows per cluster): half the weight bytes
+// per SM; d_model, d_ff, rank_pad multiples of 128, rank_pad <= 384.
+void ffn_fused_pair_bf16(const FfnTcArgs& a, cudaStream_t s);
+bool ffn_pair_supported(int d_model, int d_ff, int rank_pad);
 bool ffn_tc_supported(int d_model, int d_ff, int rank_pad);
 
 // ---- K5: y = LN(a (+ b)) * gamma + beta, rows of width d ---------------------

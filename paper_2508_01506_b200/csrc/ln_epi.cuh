@@ -93,7 +93,9 @@ constexpr int res_box_readers() { return PN == 64 ? kEpiThreads : kEpiThreads / 
 // Runs in all 256 epilogue threads: `quad` = TMEM lane quadrant (hardware
 // warp id % 4), `half` = which PN/2 columns of each piece, `row` = tile row.
 // Accumulator protocol: PN = 64 alternates acc_full/empty[0..1] (buffers at
-// columns 0 and 64); PN = 128 uses acc_full/empty[0] only.
+// columns 0 and 64); PN = 128 uses acc_full/empty[0] only.  In a CTA pair
+// (acc_empty_leader != 0: shared::cluster address of the leader's
+// acc_empty[0]) each warp releases the accumulator with one remote arrive.
 // Arithmetic runs on packed fp32 pairs (FADD2 / FFMA2) to halve the issue
 // count of this epilogue, which is instruction-bound.
 template <int PN>
@@ -103,7 +105,8 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
                                     const float* __restrict__ gamma,
                                     const float* __restrict__ beta, float eps,
                                     const CUtensorMap* tmY, int m0, float* gb_smem,
-                                    uint64_t* acc_full, uint64_t* acc_empty, uint32_t bar_id) {
+                                    uint64_t* acc_full, uint64_t* acc_empty, uint32_t bar_id,
+                                    uint32_t acc_empty_leader = 0) {
   static_assert(PN == 64 || PN == 128, "piece width");
   constexpr int CPT = PN / 64;  // 32-column chunks per thread per piece
   const uint32_t loff = (quad * 32) << 16;
@@ -128,7 +131,13 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
       tmem_ld32(tmem + loff + acc * 64 + half * (PN / 2) + c * 32, v[c]);
     tmem_ld_wait();
     tc_fence_before();
-    mbar_arrive(&acc_empty[acc]);
+    if (acc_empty_leader) {
+      // CTA pair: one arrive per warp on the leader CTA's barrier
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(acc_empty_leader + acc * 8);
+    } else {
+      mbar_arrive(&acc_empty[acc]);
+    }
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       const int col = q * PN + half * (PN / 2) + c * 32;  // first output column

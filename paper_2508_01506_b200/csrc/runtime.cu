@@ -14,6 +14,7 @@
 // every sublayer: max(3*G*rp, prp, 2*frp) elements per token.  The layer runs
 // in place (x may equal out), so a whole model needs no ping-pong pair.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -542,6 +543,17 @@ void simt_ffn_t(const Pack& p, int mode, size_t Tn, const void* x, void* out, vo
 }
 }  // namespace
 
+// The CTA-pair FFN (ffn2_tc.cu) is opt-in (FSVD_FFN_PAIR=1): it is correct
+// but measured slower than the single-CTA kernel on cfg2 (113 vs 85 us; see
+// DESIGN.md), so the single-CTA kernel is the default.
+bool use_ffn_pair(const Pack& p, int T) {
+  static const bool enabled = [] {
+    const char* e = getenv("FSVD_FFN_PAIR");
+    return e && e[0] == '1';
+  }();
+  return enabled && T >= 256 && ffn_pair_supported(p.d, p.df, p.frp);
+}
+
 void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* out, void* trans,
              cudaStream_t s) {
   const int T = static_cast<int>(B * M), d = p.d, df = p.df;
@@ -579,7 +591,8 @@ void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* o
     a.act = p.act;
     a.out = as<bf16>(out);
     if (mode == FSVD_MODE_FLASH_V2) {
-      ffn_fused_bf16(a, s);
+      if (use_ffn_pair(p, T)) ffn_fused_pair_bf16(a, s);
+      else ffn_fused_bf16(a, s);
     } else {
       bf16* P = as<bf16>(trans);
       bf16* Z = P + (size_t)T * p.frp;
@@ -621,7 +634,8 @@ bool ffn_ln_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void
     a.ln_g = p.ln2g;
     a.ln_b = p.ln2b;
     a.ln_eps = p.eps2;
-    ffn_fused_bf16(a, s);
+    if (use_ffn_pair(p, T)) ffn_fused_pair_bf16(a, s);
+    else ffn_fused_bf16(a, s);
     return true;
   }
   if (mode != FSVD_MODE_FLASH_V1) return false;

@@ -120,3 +120,40 @@ def test_attention_rankspace_vs_torch(env, B, M, H, G, rp):
         sc = (q @ k.transpose(1, 2)) * 0.6931471805599453  # log2-domain scores -> natural
         ref[:, :, h * rp:(h + 1) * rp] = torch.softmax(sc, -1) @ v
     assert _rel(out.view(B, M, H * rp), ref) < 2e-2
+
+
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_ffn_pair_and_single_agree(env, pair):
+    """The CTA-pair FFN (ffn2_tc.cu, opt-in) and the single-CTA kernel compute the same
+    V2 FFN (+LN) layer: both within bf16 tolerance of the oracle is checked by
+    the layer parity tests; here the two kernels are compared with each other
+    on a cfg2-sized tile set (T = 2048) through the device layer API."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import ctypes as C, numpy as np, torch, sys
+sys.path.insert(0, %r)
+from paper_2508_01506_b200 import abi
+from paper_2508_01506_b200.model import layer_descs, random_layer, round_layer_bf16
+L = abi.lib()
+rng = np.random.default_rng(5)
+layer = round_layer_bf16(random_layer(768, 3072, 12, 12, 32, 384, 384, rng))
+d = layer_descs([layer]); p = C.c_void_p()
+abi.check(L.fsvd_layer_pack_create(C.byref(d[0]), abi.BF16, 0, C.byref(p)))
+x = torch.randn((4, 512, 768), generator=torch.Generator().manual_seed(3)).to(torch.bfloat16).cuda()
+out = torch.empty_like(x); ws = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for v in (2,):
+    abi.check(L.fsvd_ffn_fwd(p, v, 4, 512, C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()),
+                             C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+torch.cuda.synchronize()
+np.save(sys.argv[1], out.float().cpu().numpy())
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = f"/tmp/ffn_pair_{pair}.npy"
+    env_ = dict(os.environ, FSVD_FFN_PAIR=pair)
+    subprocess.run([sys.executable, "-c", code, out], check=True, env=env_, timeout=300)
+    if pair == "0":
+        import numpy as np
+        a, b = np.load("/tmp/ffn_pair_1.npy"), np.load("/tmp/ffn_pair_0.npy")
+        assert np.isfinite(a).all()
+        assert float(np.abs(a - b).max() / np.abs(b).max()) < 2e-2
