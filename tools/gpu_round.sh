@@ -21,10 +21,13 @@ if [ "${NCU:-1}" = 1 ]; then echo done; exit 0; fi
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ffn -s 2 -c 1 \
   -o gpurun_out/prof_ffn -f python bench.py --steps 1 --warmup 1 --layers 1 --no-cpu-baseline \
   > gpurun_out/prof_ffn.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm_ln -s 2 -c 1 \
+  -o gpurun_out/prof_gemm_ln -f python bench.py --steps 1 --warmup 1 --layers 1 --no-cpu-baseline \
+  > gpurun_out/prof_gemm_ln.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_attn -s 2 -c 1 \
   -o gpurun_out/prof_attn -f python bench.py --steps 1 --warmup 1 --layers 1 --no-cpu-baseline \
   > gpurun_out/prof_attn.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 4 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm_bf16 -s 2 -c 1 \
   -o gpurun_out/prof_gemm -f python bench.py --steps 1 --warmup 1 --layers 1 --no-cpu-baseline \
   > gpurun_out/prof_gemm.log 2>&1
 echo done
