@@ -211,6 +211,22 @@ size_t fsvd_layer_pack_device_bytes(const fsvd_layer_pack* p);
 int fsvd_layer_pack_uses_tensor_cores(const fsvd_layer_pack* p);
 
 /* ------------------------------------------------------------------ */
+/* FSVD1 model files (model_io.hpp:14-30, written by the reference's     */
+/* save_model): container validation with byte offsets, assembly by the  */
+/* canonical tensor names, upload as device factor packs.                */
+/* ------------------------------------------------------------------ */
+/* Host only: parses and assembles `path`; fills the geometry of layer 0
+ * (layers = count).  FSVD_ERR_FORMAT carries the offending byte offset in
+ * fsvd_last_error_offset(). */
+fsvd_status fsvd_model_file_probe(const char* path, size_t* n_layers, fsvd_geometry* geom);
+/* Loads every layer into packs[0 .. n_layers) (capacity >= layer count);
+ * packs == NULL only reports n_layers. */
+fsvd_status fsvd_model_load(const char* path, fsvd_dtype dtype, int dense,
+                            fsvd_layer_pack** packs, size_t capacity, size_t* n_layers);
+/* Byte offset of the last FSVD_ERR_FORMAT on this thread. */
+size_t fsvd_last_error_offset(void);
+
+/* ------------------------------------------------------------------ */
 /* Device-resident async API (device pointers, cudaStream_t as void*)   */
 /* ------------------------------------------------------------------ */
 /* Bytes of workspace fsvd_model_fwd needs for this batch shape; the

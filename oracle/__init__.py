@@ -134,6 +134,9 @@ class Reference(_Base):
                                     _P(abi.TilePlan), C.c_int, _fp, m3]
         L.ref_validate_tile_plan.argtypes = [_P(abi.TilePlan), C.c_int, _P(abi.Geometry),
                                              _P(_sz)]
+        L.ref_save_model.argtypes = [C.c_char_p, _P(abi.LayerDesc), _sz]
+        L.ref_read_error_offset.argtypes = [C.c_char_p]
+        L.ref_read_error_offset.restype = C.c_longlong
         L.ref_expected_bytes.argtypes = [C.c_int, _P(abi.Geometry)]
         L.ref_expected_bytes.restype = _sz
         L.ref_flops_exact.argtypes = [_P(abi.Geometry), C.c_int]

@@ -14,6 +14,7 @@
 
 #include "flashsvd/attention.hpp"
 #include "flashsvd/encoder.hpp"
+#include "flashsvd/model_io.hpp"
 #include "flashsvd/ffn.hpp"
 #include "flashsvd/memtier.hpp"
 #include "flashsvd/planner.hpp"
@@ -253,6 +254,28 @@ unsigned long long ref_flops_exact(const fsvd_geometry* g, int mode) {
   Geometry geo{g->batch, g->seq_len, g->d_model, g->d_ff, g->heads, g->groups, g->rank,
                g->layers};
   return flops_exact(geo, static_cast<RunMode>(mode));
+}
+
+// FSVD1 (model_io.hpp): writes the layers with the reference's own
+// save_model (canonical names, JSON sidecar at <path>.json).
+int ref_save_model(const char* path, const fsvd_layer_desc* layers, size_t n_layers) {
+  return guard([&] {
+    std::vector<EncoderLayer> ls;
+    for (size_t i = 0; i < n_layers; ++i) ls.push_back(layer_of(layers[i]));
+    save_model(path, ls);
+  });
+}
+// Byte offset of the FormatError the reference reader raises for `path`
+// (-1: the container parsed; -2: another error).
+long long ref_read_error_offset(const char* path) {
+  try {
+    read_tensor_file(path);
+    return -1;
+  } catch (const FormatError& e) {
+    return static_cast<long long>(e.byte_offset());
+  } catch (...) {
+    return -2;
+  }
 }
 
 }  // extern "C"

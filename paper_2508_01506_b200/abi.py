@@ -125,6 +125,9 @@ def _declare(lib):
         "fsvd_ffn_fwd": (st, [vp, C.c_int, _sz, _sz, vp, vp, vp, _sz, vp]),
         "fsvd_layer_fwd": (st, [vp, C.c_int, C.c_int, _sz, _sz, vp, vp, vp, _sz, vp]),
         "fsvd_model_fwd": (st, [P(vp), _sz, C.c_int, C.c_int, _sz, _sz, vp, vp, vp, _sz, vp]),
+        "fsvd_model_file_probe": (st, [C.c_char_p, P(_sz), P(Geometry)]),
+        "fsvd_model_load": (st, [C.c_char_p, C.c_int, C.c_int, P(vp), _sz, P(_sz)]),
+        "fsvd_last_error_offset": (_sz, []),
         "fsvd_stream_workspace_bytes": (st, [P(vp), _sz, _sz, _sz, C.c_int, P(_sz)]),
         "fsvd_model_fwd_stream": (st, [P(vp), _sz, C.c_int, C.c_int, _sz, _sz, _sz, P(vp), P(vp),
                                        vp, _sz, vp]),

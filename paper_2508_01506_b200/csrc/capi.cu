@@ -19,6 +19,7 @@
 #include "../../include/fsvd_b200.h"
 #include "common.cuh"
 #include "meter.hpp"
+#include "model_file.hpp"
 #include "runtime.hpp"
 
 struct fsvd_meter {
@@ -675,6 +676,49 @@ StreamSet& stream_set() {
   return ss;
 }
 }  // namespace
+
+fsvd_status fsvd_model_file_probe(const char* path, size_t* n_layers, fsvd_geometry* geom) {
+  return guard([&] {
+    if (!path) fail(Kind::Config, "null argument");
+    std::unique_ptr<ModelFile> mf = read_model_file(path);
+    if (n_layers) *n_layers = mf->layers.size();
+    if (geom) {
+      *geom = fsvd_geometry{};
+      geom->layers = mf->layers.size();
+      if (!mf->layers.empty()) {
+        const fsvd_layer_desc& d = mf->layers[0].desc;
+        geom->d_model = d.attn.d_model;
+        geom->d_ff = d.ffn.up.out_dim;
+        geom->heads = d.heads;
+        geom->groups = d.attn.groups;
+        geom->rank = d.attn.rank;
+      }
+    }
+  });
+}
+fsvd_status fsvd_model_load(const char* path, fsvd_dtype dtype, int dense,
+                            fsvd_layer_pack** packs, size_t capacity, size_t* n_layers) {
+  return guard([&] {
+    if (!path) fail(Kind::Config, "null argument");
+    check_dtype(dtype);
+    std::unique_ptr<ModelFile> mf = read_model_file(path);
+    if (n_layers) *n_layers = mf->layers.size();
+    if (!packs) return;
+    if (capacity < mf->layers.size())
+      fail(Kind::Config, "pack capacity " + std::to_string(capacity) + " < " +
+                             std::to_string(mf->layers.size()) + " layers in the file");
+    require_device();
+    std::vector<std::unique_ptr<fsvd_layer_pack>> made;
+    for (const ModelFile::Layer& L : mf->layers) {
+      fsvd_layer_pack* p = nullptr;
+      const fsvd_status st = fsvd_layer_pack_create(&L.desc, dtype, dense, &p);
+      if (st != FSVD_OK) throw Error(static_cast<Kind>(st), fsvd_last_error());
+      made.emplace_back(p);
+    }
+    for (size_t i = 0; i < made.size(); ++i) packs[i] = made[i].release();
+  });
+}
+size_t fsvd_last_error_offset(void) { return format_error_offset(); }
 
 fsvd_status fsvd_stream_workspace_bytes(const fsvd_layer_pack* const* packs, size_t n_layers,
                                         size_t batch, size_t seq, fsvd_run_mode mode,

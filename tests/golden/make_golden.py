@@ -64,5 +64,19 @@ def main():
     print("wrote", len(out), "arrays")
 
 
+def make_tiny_model(path=os.path.join(HERE, "tiny_model.fsvd")):
+    """tiny_model.fsvd: two BERT-like layers (d=32, H=G=4, r=4, pr=8, fr=16;
+    GELU-erf then GELU-tanh) written by the reference's own save_model."""
+    from paper_2508_01506_b200.model import layer_descs, random_layer
+    ref = oracle.Reference()
+    rng = np.random.default_rng(123)
+    layers = [random_layer(32, 64, 4, 4, 4, 8, 16, rng),
+              random_layer(32, 64, 4, 4, 4, 8, 16, rng, activation=1)]
+    assert ref.lib.ref_save_model(path.encode(), layer_descs(layers), 2) == 0
+    if os.path.exists(path + ".json"):
+        os.remove(path + ".json")
+
+
 if __name__ == "__main__":
     main()
+    make_tiny_model()
