@@ -475,7 +475,7 @@ def main():
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--seq", type=int, default=SEQ)
     ap.add_argument("--layers", type=int, default=LAYERS)
-    ap.add_argument("--ref-batch", type=int, default=1)
+    ap.add_argument("--ref-batch", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
