@@ -247,13 +247,13 @@ def run_gpu(args):
     parr = (C.c_void_p * len(packs))(*[p.value for p in packs])
     assert L.fsvd_layer_pack_uses_tensor_cores(packs[0]) == 1
     wsb = C.c_size_t()
-    abi.check(L.fsvd_workspace_bytes(parr, len(packs), B, M, mode, C.byref(wsb)))
+    abi.check(L.fsvd_workspace_bytes_ln(parr, len(packs), B, M, mode, 0, C.byref(wsb)))
     torch.cuda.reset_peak_memory_stats(dev)
     base_alloc = torch.cuda.memory_allocated(dev)
     work = torch.empty(wsb.value, dtype=torch.uint8, device=dev)
     gen = torch.Generator(device=dev)
     gen.manual_seed(100 + rank)
-    x = torch.randn((B, M, D), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    x = torch.empty((B, M, D), device=dev, dtype=torch.bfloat16).normal_(generator=gen)
     out = torch.empty_like(x)
     act_bytes = torch.cuda.max_memory_allocated(dev) - base_alloc
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
@@ -404,7 +404,7 @@ def run_gpu(args):
         def ws_for(m, dense=False):
             b = C.c_size_t()
             if not dense:
-                abi.check(L.fsvd_workspace_bytes(parr, len(packs), B, M, m, C.byref(b)))
+                abi.check(L.fsvd_workspace_bytes_ln(parr, len(packs), B, M, m, 0, C.byref(b)))
                 return b.value
             return None
         es = 2

@@ -234,6 +234,12 @@ size_t fsvd_last_error_offset(void);
 fsvd_status fsvd_workspace_bytes(const fsvd_layer_pack* const* packs, size_t n_layers,
                                  size_t batch, size_t seq, fsvd_run_mode mode,
                                  size_t* bytes);
+/* Exact requirement of one layer ordering: pre_ln = 0 (post-LN, the
+ * reference default, fused LayerNorm epilogues) or 1.  fsvd_workspace_bytes
+ * returns the larger of the two. */
+fsvd_status fsvd_workspace_bytes_ln(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                    size_t batch, size_t seq, fsvd_run_mode mode, int pre_ln,
+                                    size_t* bytes);
 /* attention.cpp:202-269 (flash_svd_attention): x, ctx [batch, seq, d]. */
 fsvd_status fsvd_attention_fwd(const fsvd_layer_pack* p, size_t batch, size_t seq,
                                const void* x, void* ctx, void* workspace,

@@ -120,6 +120,7 @@ def _declare(lib):
         "fsvd_layer_pack_device_bytes": (_sz, [vp]),
         "fsvd_layer_pack_uses_tensor_cores": (C.c_int, [vp]),
         "fsvd_workspace_bytes": (st, [P(vp), _sz, _sz, _sz, C.c_int, P(_sz)]),
+        "fsvd_workspace_bytes_ln": (st, [P(vp), _sz, _sz, _sz, C.c_int, C.c_int, P(_sz)]),
         "fsvd_attention_fwd": (st, [vp, _sz, _sz, vp, vp, vp, _sz, vp]),
         "fsvd_outproj_fwd": (st, [vp, _sz, _sz, vp, vp, vp, _sz, vp]),
         "fsvd_ffn_fwd": (st, [vp, C.c_int, _sz, _sz, vp, vp, vp, _sz, vp]),

@@ -429,7 +429,7 @@ void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_lay
     packs.emplace_back(build_pack(q, dt));
     if (q.dense && !packs.back()->dense)
       fail(Kind::Config, "dense / naive_lowrank modes run only on the bf16 tensor-core path");
-    ws = std::max(ws, layer_workspace_bytes(*packs.back(), B * M, mode));
+    ws = std::max(ws, layer_workspace_bytes(*packs.back(), B * M, mode, pre_ln != 0));
     pack_bytes += packs.back()->bytes;
   }
   run_on_device(x, B * M * W, out, B * M * W, dt, ws, *packs[0], nullptr,
@@ -584,6 +584,18 @@ fsvd_status fsvd_workspace_bytes(const fsvd_layer_pack* const* packs, size_t n_l
     size_t ws = 0;
     for (size_t i = 0; i < n_layers; ++i)
       ws = std::max(ws, layer_workspace_bytes(*packs[i]->p, batch * seq, mode));
+    *bytes = ws;
+  });
+}
+fsvd_status fsvd_workspace_bytes_ln(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                    size_t batch, size_t seq, fsvd_run_mode mode, int pre_ln,
+                                    size_t* bytes) {
+  return guard([&] {
+    if (!bytes) fail(Kind::Config, "null argument");
+    check_mode(mode);
+    size_t ws = 0;
+    for (size_t i = 0; i < n_layers; ++i)
+      ws = std::max(ws, layer_workspace_bytes(*packs[i]->p, batch * seq, mode, pre_ln != 0));
     *bytes = ws;
   });
 }
@@ -745,7 +757,7 @@ fsvd_status fsvd_model_fwd_stream(const fsvd_layer_pack* const* packs, size_t n_
     require_device();
     size_t need = 0;
     for (size_t i = 0; i < n_layers; ++i)
-      need = std::max(need, layer_workspace_bytes(*packs[i]->p, batch * seq, mode));
+      need = std::max(need, layer_workspace_bytes(*packs[i]->p, batch * seq, mode, pre_ln != 0));
     const size_t slot = stream_slot_bytes(packs, batch, seq);
     if (ws_bytes < need + 2 * slot + 256)
       fail(Kind::Config, "workspace too small: need " + std::to_string(need + 2 * slot + 256) +

@@ -361,7 +361,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (fuse_ln) {
       lnepi::run<64>(tmem, quad, half, row, d_model, b_dn, smem_u32(smem + C::o_h),
                      bars->res_full, bars->res_empty, 2, ln_g, ln_b, ln_eps, &tmY, m0,
-                     reinterpret_cast<float*>(ring), bars->o_full, bars->o_free, 1,
+                     reinterpret_cast<float*>(ring), smem_u32(smem + C::o_h), bars->o_full,
+                     bars->o_free, 1,
                      mapa_shared(smem_u32(&bars->o_free[0]), 0));
     } else {
       for (int q = 0; q < NQ; ++q) {

@@ -437,7 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // gamma / beta are staged in the weight ring, idle once all MMAs are done
         lnepi::run<64>(tmem, quad, half, row, d_model, b_dn, smem_u32(smem + C::o_h),
                        bars->res_full, bars->res_empty, 2, ln_g, ln_b, ln_eps, &tmY, m0,
-                       reinterpret_cast<float*>(ring), bars->o_full, bars->o_free, 1);
+                       reinterpret_cast<float*>(ring), smem_u32(smem + C::o_h), bars->o_full,
+                       bars->o_free, 1);
       } else {
         for (int q = 0; q < NQ; ++q) {
           mbar_wait(&bars->o_full[q & 1], (q >> 1) & 1);

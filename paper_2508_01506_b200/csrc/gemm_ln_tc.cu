@@ -51,7 +51,7 @@ constexpr int SLOT = PN * 128;      // [128 x 64] bf16 B slot (16 KB)
 constexpr int SPS = 1;              // slots per ring stage
 constexpr int STAGE = SPS * SLOT;
 constexpr int kMaxStages = 10;
-constexpr int RS = 4;               // residual ring depth ([128 x 64] bf16 boxes)
+constexpr int RS = 2;               // residual ring depth ([128 x 64] bf16 boxes)
 constexpr int RBOX = BMr * 128;
 
 #ifdef FSVD_TRACE
@@ -203,9 +203,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t quad = warp & 3;
     const uint32_t half = (warp - 2) >> 2;  // which 32 columns of each piece
     const uint32_t row = quad * 32 + lane;
+    // second sweep: output boxes staged in the B ring, gamma / beta in the A
+    // region (both idle once every MMA has completed)
     lnepi::run<PN>(tmem, quad, half, row, N, bias, smem_u32(rring), bars->res_full,
                    bars->res_empty, RS, gamma, beta, eps, &tmY, m0, reinterpret_cast<float*>(sA),
-                   bars->acc_full, bars->acc_empty, 1);
+                   smem_u32(ring), bars->acc_full, bars->acc_empty, 1);
   }
   if (threadIdx.x == 64) LTRACE(100);
   tc_fence_before();
@@ -231,7 +233,8 @@ void gemm_ln_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, const 
   int stages =
       (227 * 1024 - 1024 - KA * ATOM - RS * RBOX - static_cast<int>(sizeof(LnBars))) / STAGE;
   stages = stages > kMaxStages ? kMaxStages : stages;
-  if (stages < 2) throw CudaError("gemm_ln_bf16: K too large for the shared-memory ring");
+  // the ring doubles as the second sweep's 4-box output staging
+  if (stages * STAGE < 4 * RBOX) throw CudaError("gemm_ln_bf16: K too large for the shared-memory ring");
   const int smem = 1024 + KA * ATOM + stages * STAGE + RS * RBOX + static_cast<int>(sizeof(LnBars));
   static int attr = 0;
   if (attr < smem) {

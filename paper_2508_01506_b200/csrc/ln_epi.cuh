@@ -105,8 +105,8 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
                                     const float* __restrict__ gamma,
                                     const float* __restrict__ beta, float eps,
                                     const CUtensorMap* tmY, int m0, float* gb_smem,
-                                    uint64_t* acc_full, uint64_t* acc_empty, uint32_t bar_id,
-                                    uint32_t acc_empty_leader = 0) {
+                                    uint32_t out_stage, uint64_t* acc_full, uint64_t* acc_empty,
+                                    uint32_t bar_id, uint32_t acc_empty_leader = 0) {
   static_assert(PN == 64 || PN == 128, "piece width");
   constexpr int CPT = PN / 64;  // 32-column chunks per thread per piece
   const uint32_t loff = (quad * 32) << 16;
@@ -213,23 +213,24 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
   if (threadIdx.x == 64) LN_TRACE(301);
 #endif
 
-  // second sweep: normalise, stage [128 x 64] bf16 boxes in the (drained)
-  // residual ring, TMA-store them.  PN = 64: both halves fill one box per
-  // piece (two boxes alternate, 256-thread barriers); PN = 128: each half
-  // owns a box per piece and alternates its own two boxes (128-thread
-  // barriers, ids bar_id + 1 + half; needs res_depth >= 4).
+  // second sweep: normalise, stage [128 x 64] bf16 boxes at out_stage (an
+  // idle shared-memory region of 2 boxes for PN = 64, 4 for PN = 128) and
+  // TMA-store them.  PN = 64: both halves fill one box per piece (two boxes
+  // alternate, 256-thread barriers); PN = 128: each half owns a box per piece
+  // and alternates its own two boxes (128-thread barriers, ids bar_id + 1 +
+  // half).
   const int ht = et & 127;  // thread index within the half (PN = 128)
   for (int i = 0; i < NP; ++i) {
     const int q = piece_of(i, NP);
     uint32_t box;
     if (PN == 64) {
-      box = res_ring + (i & 1) * kBox;
+      box = out_stage + (i & 1) * kBox;
       if (i >= 2) {
         if (et == 0) tma_store_wait_read<1>();
         named_bar_sync(bar_id, kEpiThreads);
       }
     } else {
-      box = res_ring + (2 * half + (i & 1)) * kBox;
+      box = out_stage + (2 * half + (i & 1)) * kBox;
       if (i >= 2) {
         if (ht == 0) tma_store_wait_read<1>();
         named_bar_sync(bar_id + 1 + half, kEpiThreads / 2);

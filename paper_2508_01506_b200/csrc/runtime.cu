@@ -372,10 +372,42 @@ size_t op_transient_elems(const Pack& p, int op, int mode) {
   }
 }
 
-size_t layer_workspace_bytes(const Pack& p, size_t T, int mode) {
+namespace {
+// Fused post-LN tensor-core schedule (layer_fwd): rank-space attention output
+// A [T, H*rp], LN1 output B [T, d], transient QKV / FFN-V1 region; A holds a
+// [T, d] FFN output instead when the FFN cannot take its LN fused.
+bool fused_post_ln(const Pack& p, int mode) {
+  const bool flash = mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2;
+  return flash && p.attn_tc && p.out_tc && gemm_ln_supported(p.d, p.H * p.rp);
+}
+bool ffn_ln_fusable(const Pack& p, int mode) {
+  return p.ffn_tc && gemm_ln_supported(p.d, p.frp) &&
+         (mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2);
+}
+struct WsLayout {
+  size_t a, b, t;  // bytes of the A / B / transient regions (256-aligned)
+  size_t total() const { return a + b + t + 256; }
+};
+WsLayout ws_layout(const Pack& p, size_t T, int mode, bool pre_ln) {
+  if (!pre_ln && fused_post_ln(p, mode)) {
+    const bool ffn_fused = ffn_ln_fusable(p, mode);
+    const size_t a_cols = ffn_fused ? static_cast<size_t>(p.H * p.rp) : p.d;
+    size_t t_cols = p.qkv_cols;
+    if (mode == FSVD_MODE_FLASH_V1) t_cols = std::max(t_cols, 2 * static_cast<size_t>(p.frp));
+    if (!ffn_fused) t_cols = std::max(t_cols, op_transient_elems(p, 2, mode));
+    return {align256(T * a_cols * p.es), align256(T * p.d * p.es), align256(T * t_cols * p.es)};
+  }
   size_t tr = 0;
   for (int op : {1, 2, 3}) tr = std::max(tr, op_transient_elems(p, op, mode));
-  return 2 * align256(T * p.d * p.es) + align256(T * tr * p.es) + 256;
+  return {align256(T * p.d * p.es), align256(T * p.d * p.es), align256(T * tr * p.es)};
+}
+}  // namespace
+
+size_t layer_workspace_bytes(const Pack& p, size_t T, int mode, bool pre_ln) {
+  return ws_layout(p, T, mode, pre_ln).total();
+}
+size_t layer_workspace_bytes(const Pack& p, size_t T, int mode) {
+  return std::max(layer_workspace_bytes(p, T, mode, false), layer_workspace_bytes(p, T, mode, true));
 }
 
 // ---------------------------------------------------------------- schedule
@@ -664,17 +696,16 @@ bool ffn_ln_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void
 void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const void* x, void* out,
                void* ws, size_t ws_bytes, cudaStream_t s) {
   const size_t T = B * M;
-  if (ws_bytes < layer_workspace_bytes(p, T, mode))
-    fail(Kind::Config, "workspace too small: need " + std::to_string(layer_workspace_bytes(p, T, mode)) +
+  const WsLayout lay = ws_layout(p, T, mode, pre_ln);
+  if (ws_bytes < lay.total())
+    fail(Kind::Config, "workspace too small: need " + std::to_string(lay.total()) +
                            " bytes, got " + std::to_string(ws_bytes));
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
-  const size_t act_bytes = align256(T * p.d * p.es);
   void* A = base;
-  void* Bb = base + act_bytes;
-  void* trans = base + 2 * act_bytes;
+  void* Bb = base + lay.a;
+  void* trans = base + lay.a + lay.b;
   const int rows = static_cast<int>(T);
-  const bool flash = mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2;
-  if (!pre_ln && flash && p.attn_tc && p.out_tc && gemm_ln_supported(p.d, p.H * p.rp)) {
+  if (!pre_ln && fused_post_ln(p, mode)) {
     // rank-space attention -> A; folded out-projection + residual + LN1 -> B
     tc_attention_rank(p, B, M, x, A, trans, s);
     gemm_ln_bf16(as<bf16>(A), p.H * p.rp, as<bf16>(p.wov_t), p.H * p.rp, p.bov, as<bf16>(x),

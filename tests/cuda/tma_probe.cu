@@ -3,6 +3,7 @@
 // into a ring of `depth` slots and re-issues as soon as each slot lands (no
 // consumer), so the rate is what the TMA path delivers.  Variants: box rows,
 // ring depth, number of CTAs reading the SAME lines vs. distinct lines.
+#include <algorithm>
 #include <cstdio>
 #include <vector>
 
@@ -28,7 +29,7 @@ __global__ void __launch_bounds__(128, 1) k_tma(const __grid_constant__ CUtensor
     fence_barrier_init();
   }
   __syncthreads();
-  const int nbox_rows = rows_total / box_rows;
+  const int nbox_rows = rows_total / box_rows;  // rows_total = span actually read
   const int start = same ? 0 : (blockIdx.x * 7) % nbox_rows;
   long long t0 = clock64();
   if (lane == 0) {
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(128, 1) k_tma(const __grid_constant__ CUtensor
 }
 
 int main() {
-  const int rows_total = 8192;  // 8192 x 64 bf16 = 1 MB, L2 resident
+  const int rows_total = 8192 * 64;  // 64 MB; the kernel reads the first `span` rows
   void* mat;
   cudaMalloc(&mat, (size_t)rows_total * 64 * 2);
   cudaMemset(mat, 0, (size_t)rows_total * 64 * 2);
@@ -64,19 +65,20 @@ int main() {
   int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   cudaFuncSetAttribute(k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  printf("box_rows depth grid warps prefetch : B/clk per SM (median CTA)\n");
-  const int same = 0;
-  for (int grid : {128})
-    for (int nw : {1, 2, 4})
-      for (int pf : {0, 1})
-      for (int box_rows : {64, 128, 256})
-        for (int depth : {4}) {
+  printf("span_rows box_rows depth grid warps same : B/clk per SM (median CTA), chip B/clk\n");
+  const int pf = 1;
+  for (int span : {8192, 8192 * 64})
+   for (int same : {0, 1})
+    for (int grid : {74, 148})
+    for (int nw : {2, 4})
+      for (int box_rows : {128, 256})
+        for (int depth : {3}) {
           if (nw * depth * box_rows * 128 > 190 * 1024) continue;
           CUtensorMap tm = tmap_bf16(mat, rows_total, 64, 64, box_rows, 64, TmaSwizzle::B128);
           const int iters = 2000 * 64 / box_rows;
           for (int rep = 0; rep < 2; ++rep)
             k_tma<<<grid, 32 * nw, nw * depth * box_rows * 128 + 1024>>>(
-                tm, box_rows, depth, iters, rows_total, same, pf, d_cyc);
+                tm, box_rows, depth, iters, span, same, pf, d_cyc);
           cudaError_t e = cudaDeviceSynchronize();
           if (e != cudaSuccess) {
             printf("error %s\n", cudaGetErrorString(e));
@@ -86,8 +88,8 @@ int main() {
           cudaMemcpy(c.data(), d_cyc, grid * sizeof(long long), cudaMemcpyDeviceToHost);
           std::sort(c.begin(), c.end());
           const double bytes = (double)iters * box_rows * 128;
-          printf("%4d %3d %4d %d %d : %6.1f B/clk\n", box_rows, depth, grid, nw, pf,
-                 bytes / c[c.size() / 2]);
+          printf("%6d %4d %3d %4d %d %d : %6.1f B/clk  chip %7.0f B/clk\n", span, box_rows, depth,
+                 grid, nw, same, bytes / c[c.size() / 2], grid * bytes / c[c.size() - 1]);
         }
   (void)nsm;
   return 0;

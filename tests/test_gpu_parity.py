@@ -266,6 +266,44 @@ def test_device_api_matches_host_api(L, ora):
         L.fsvd_layer_pack_destroy(p)
 
 
+def test_workspace_planner_per_ordering(L, ora):
+    """fsvd_workspace_bytes_ln sizes exactly one LayerNorm ordering: the
+    post-LN fused schedule keeps rank-space attention output [T, H*rp], so it
+    needs less than the pre-LN one; each runs in its own exact size, a pre-LN
+    run in the post-LN size fails with a Config error, and the generic
+    planner covers both."""
+    import torch
+    layers = [oracle.rand_layer(ora, 256, 1024, 4, 4, 32, 70, 64, 128)]
+    round_layer_bf16(layers[0])
+    B, M, d = 2, 128, 256
+    descs = layer_descs(layers)
+    p = C.c_void_p()
+    abi.check(L.fsvd_layer_pack_create(C.byref(descs[0]), abi.BF16, 0, C.byref(p)))
+    parr = (C.c_void_p * 1)(p.value)
+    post, pre, both = C.c_size_t(), C.c_size_t(), C.c_size_t()
+    abi.check(L.fsvd_workspace_bytes_ln(parr, 1, B, M, abi.MODE_FLASH_V2, 0, C.byref(post)))
+    abi.check(L.fsvd_workspace_bytes_ln(parr, 1, B, M, abi.MODE_FLASH_V2, 1, C.byref(pre)))
+    abi.check(L.fsvd_workspace_bytes(parr, 1, B, M, abi.MODE_FLASH_V2, C.byref(both)))
+    assert post.value < pre.value and both.value == max(post.value, pre.value)
+    x = bf16_round(ora.random((B, M, d), 8))
+    xt = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for pre_ln, size in ((0, post.value), (1, pre.value)):
+        ref = H.run_model(x, layers, abi.MODE_FLASH_V2, PLAN, abi.BF16, pre_ln=pre_ln)
+        work = torch.empty(size, dtype=torch.uint8, device="cuda")
+        out = torch.empty_like(xt)
+        abi.check(L.fsvd_model_fwd(parr, 1, abi.MODE_FLASH_V2, pre_ln, B, M,
+                                   C.c_void_p(xt.data_ptr()), C.c_void_p(out.data_ptr()),
+                                   C.c_void_p(work.data_ptr()), size, s))
+        torch.cuda.synchronize()
+        assert np.array_equal(out.float().cpu().numpy(), ref)
+    work = torch.empty(post.value, dtype=torch.uint8, device="cuda")
+    st = L.fsvd_model_fwd(parr, 1, abi.MODE_FLASH_V2, 1, B, M, C.c_void_p(xt.data_ptr()),
+                          C.c_void_p(xt.data_ptr()), C.c_void_p(work.data_ptr()), post.value, s)
+    assert st == abi.ERR_CONFIG and b"workspace too small" in L.fsvd_last_error()
+    L.fsvd_layer_pack_destroy(p)
+
+
 # ------------------------------------------------------------------ full-size properties (cfg2)
 def test_cfg2_full_size_properties(L, ora):
     """BERT-Base B=32 M=512 bf16 (BASELINE configs[1], 2 of the 12 layers):
