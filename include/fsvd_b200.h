@@ -227,6 +227,61 @@ fsvd_status fsvd_model_load(const char* path, fsvd_dtype dtype, int dense,
 size_t fsvd_last_error_offset(void);
 
 /* ------------------------------------------------------------------ */
+/* Device factorization: svd.cpp factor_rank_r,     */
+/* factorize.cpp factorize_linear / factorize_attention, ffn.cpp         */
+/* factorize_ffn, model_io.cpp synth_model's factorization step.  Host    */
+/* pointers, synchronous; all matrices of a call are factorized in one   */
+/* batched device run (fp64 one-sided block Jacobi).                     */
+/* ------------------------------------------------------------------ */
+/* svd.cpp:412-456 (factor_rank_r): a row-major m x n -> u (m x r), v (r x n),
+ * even sqrt(sigma) split, largest-|.| entry of each u column positive.
+ * FSVD_ERR_RANK: r == 0 or r > min(m, n). */
+fsvd_status fsvd_factor_rank_r(const float* a, size_t m, size_t n, size_t rank, float* u,
+                               float* v);
+typedef struct fsvd_factor_job {
+  const float* a; /* row-major m x n */
+  size_t m, n, rank;
+  float* u; /* m x rank */
+  float* v; /* rank x n */
+} fsvd_factor_job;
+fsvd_status fsvd_factor_rank_r_batch(const fsvd_factor_job* jobs, size_t count);
+/* factorize.cpp:21-64 (factorize_attention): w* are d x d (in x out), b* d.
+ * Outputs in the fsvd_attn_desc layout: u [3][G][d][r], v [3][G][r][d/G],
+ * bias [3][G][d/G] (q, k, v order).  FSVD_ERR_CONFIG: groups does not divide
+ * d; FSVD_ERR_RANK: rank 0 or > d/groups. */
+fsvd_status fsvd_factorize_attention(const float* wq, const float* bq, const float* wk,
+                                     const float* bk, const float* wv, const float* bv,
+                                     size_t d_model, size_t groups, size_t rank, float* u,
+                                     float* v, float* bias);
+/* One dense encoder layer (encoder.hpp:32-47 DenseAttentionWeights /
+ * DenseFfnWeights), weights (in x out) row-major. */
+typedef struct fsvd_dense_layer {
+  size_t d_model, d_ff;
+  const float *wq, *bq, *wk, *bk, *wv, *bv; /* d x d, d */
+  const float *wo, *bo;                     /* d x d, d */
+  const float *w_in, *b_in;                 /* d x d_ff, d_ff */
+  const float *w_out, *b_out;               /* d_ff x d, d */
+} fsvd_dense_layer;
+/* Caller-owned outputs of one layer, in the fsvd_layer_desc layouts. */
+typedef struct fsvd_factor_buffers {
+  float *attn_u, *attn_v, *attn_b; /* [3][G][d][r], [3][G][r][d/G], [3][G][d/G] */
+  float *out_u, *out_v, *out_b;    /* d x pr, pr x d, d */
+  float *up_u, *up_v, *up_b;       /* d x fr, fr x d_ff, d_ff */
+  float *down_u, *down_v, *down_b; /* d_ff x fr, fr x d, d */
+} fsvd_factor_buffers;
+/* synth_model's factorization step (model_io.cpp:486-533) for n_layers dense
+ * layers in one batched device run.  Zero ranks resolve as the reference:
+ * rank -> d/groups, proj_rank -> min(rank*groups, d), ffn_rank ->
+ * min(proj_rank, d, d_ff) (model_io.cpp:489-499); the resolved values are
+ * written back through the pointers.  out == NULL only resolves and checks
+ * the ranks (size the buffers, then call again). */
+fsvd_status fsvd_factorize_layers(const fsvd_dense_layer* layers, size_t n_layers,
+                                  size_t groups, size_t* rank, size_t* proj_rank,
+                                  size_t* ffn_rank, const fsvd_factor_buffers* out);
+/* Jacobi sweeps the last factorization call ran (max over its matrices). */
+int fsvd_last_factor_sweeps(void);
+
+/* ------------------------------------------------------------------ */
 /* Device-resident async API (device pointers, cudaStream_t as void*)   */
 /* ------------------------------------------------------------------ */
 /* Bytes of workspace fsvd_model_fwd needs for this batch shape; the

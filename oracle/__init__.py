@@ -141,6 +141,9 @@ class Reference(_Base):
         L.ref_expected_bytes.restype = _sz
         L.ref_flops_exact.argtypes = [_P(abi.Geometry), C.c_int]
         L.ref_flops_exact.restype = C.c_ulonglong
+        L.ref_factor_rank_r.argtypes = [_fp, _sz, _sz, _sz, _fp, _fp]
+        L.ref_svd.argtypes = [_fp, _sz, _sz, _fp, _fp, _fp]
+        L.ref_factorize_attention.argtypes = [_fp] * 6 + [_sz, _sz, _sz, _fp, _fp, _fp]
 
     def _chk(self, st):
         if st:
@@ -194,6 +197,39 @@ class Reference(_Base):
 
     def flops_exact(self, geom, mode):
         return self.lib.ref_flops_exact(geom, mode)
+
+    def factor_rank_r(self, a, r):
+        """svd.cpp:412-456 -> (u [m, r], v [r, n])."""
+        a = np.ascontiguousarray(a, np.float32)
+        m, n = a.shape
+        u = np.zeros((m, r), np.float32)
+        v = np.zeros((r, n), np.float32)
+        self._chk(self.lib.ref_factor_rank_r(_f(a), m, n, r, _f(u), _f(v)))
+        return u, v
+
+    def svd(self, a):
+        """svd.cpp:288-302 -> (u [m, p], s [p], vt [p, n])."""
+        a = np.ascontiguousarray(a, np.float32)
+        m, n = a.shape
+        p = min(m, n)
+        u = np.zeros((m, p), np.float32)
+        s = np.zeros((p,), np.float32)
+        vt = np.zeros((p, n), np.float32)
+        self._chk(self.lib.ref_svd(_f(a), m, n, _f(u), _f(s), _f(vt)))
+        return u, s, vt
+
+    def factorize_attention(self, ws, bs, groups, rank):
+        """factorize.cpp:21-64 -> (u [3,G,d,r], v [3,G,r,d/G], bias [3,G,d/G])."""
+        d = ws[0].shape[0]
+        gd = d // groups
+        u = np.zeros((3, groups, d, rank), np.float32)
+        v = np.zeros((3, groups, rank, gd), np.float32)
+        b = np.zeros((3, groups, gd), np.float32)
+        args = []
+        for w, bb in zip(ws, bs):
+            args += [_f(np.ascontiguousarray(w, np.float32)), _f(np.ascontiguousarray(bb, np.float32))]
+        self._chk(self.lib.ref_factorize_attention(*args, d, groups, rank, _f(u), _f(v), _f(b)))
+        return u, v, b
 
 
 def abi_check(st):

@@ -15,6 +15,7 @@
 #include "flashsvd/attention.hpp"
 #include "flashsvd/encoder.hpp"
 #include "flashsvd/model_io.hpp"
+#include "flashsvd/factorize.hpp"
 #include "flashsvd/ffn.hpp"
 #include "flashsvd/memtier.hpp"
 #include "flashsvd/planner.hpp"
@@ -276,6 +277,45 @@ long long ref_read_error_offset(const char* path) {
   } catch (...) {
     return -2;
   }
+}
+
+// svd.cpp:412-456 -- leading-r even-split factors of a row-major m x n matrix.
+int ref_factor_rank_r(const float* a, size_t m, size_t n, size_t r, float* u, float* v) {
+  return guard([&] {
+    LowRankPair p = factor_rank_r(mat(a, m, n), r);
+    std::memcpy(u, p.u.data(), m * r * sizeof(float));
+    std::memcpy(v, p.v.data(), r * n * sizeof(float));
+  });
+}
+// svd.cpp:260-302 -- full thin SVD (float outputs; p = min(m, n)).
+int ref_svd(const float* a, size_t m, size_t n, float* u, float* s, float* vt) {
+  return guard([&] {
+    SvdResult f = svd(mat(a, m, n));
+    const size_t p = f.s.size();
+    std::memcpy(u, f.u.data(), m * p * sizeof(float));
+    std::memcpy(s, f.s.data(), p * sizeof(float));
+    std::memcpy(vt, f.vt.data(), p * n * sizeof(float));
+  });
+}
+// factorize.cpp:21-64 -- per-group factors written in the fsvd_attn_desc
+// layout: u [3][G][d][r], v [3][G][r][d/G], bias [3][G][d/G].
+int ref_factorize_attention(const float* wq, const float* bq, const float* wk, const float* bk,
+                            const float* wv, const float* bv, size_t d, size_t groups,
+                            size_t rank, float* u, float* v, float* bias) {
+  return guard([&] {
+    AttentionFactorSet s = factorize_attention(mat(wq, d, d), vec(bq, d), mat(wk, d, d),
+                                               vec(bk, d), mat(wv, d, d), vec(bv, d), groups,
+                                               rank);
+    const size_t gd = d / groups;
+    for (size_t m = 0; m < 3; ++m)
+      for (size_t g = 0; g < groups; ++g) {
+        const FactorizedLinear& f = (m == 0 ? s.q : m == 1 ? s.k : s.v)[g];
+        const size_t i = m * groups + g;
+        std::memcpy(u + i * d * rank, f.u.data(), d * rank * sizeof(float));
+        std::memcpy(v + i * rank * gd, f.v.data(), rank * gd * sizeof(float));
+        std::memcpy(bias + i * gd, f.bias.data(), gd * sizeof(float));
+      }
+  });
 }
 
 }  // extern "C"

@@ -53,6 +53,21 @@ class LinearDesc(C.Structure):
                 ("u", _fp), ("v", _fp), ("bias", _fp)]
 
 
+class FactorJob(C.Structure):
+    _fields_ = [("a", _fp), ("m", _sz), ("n", _sz), ("rank", _sz), ("u", _fp), ("v", _fp)]
+
+
+class DenseLayer(C.Structure):
+    _fields_ = [("d_model", _sz), ("d_ff", _sz)] + [
+        (n, _fp) for n in ("wq", "bq", "wk", "bk", "wv", "bv", "wo", "bo", "w_in", "b_in",
+                           "w_out", "b_out")]
+
+
+class FactorBuffers(C.Structure):
+    _fields_ = [(n, _fp) for n in ("attn_u", "attn_v", "attn_b", "out_u", "out_v", "out_b",
+                                   "up_u", "up_v", "up_b", "down_u", "down_v", "down_b")]
+
+
 class AttnDesc(C.Structure):
     _fields_ = [("d_model", _sz), ("groups", _sz), ("rank", _sz),
                 ("u", _fp), ("v", _fp), ("bias", _fp)]
@@ -129,6 +144,12 @@ def _declare(lib):
         "fsvd_model_file_probe": (st, [C.c_char_p, P(_sz), P(Geometry)]),
         "fsvd_model_load": (st, [C.c_char_p, C.c_int, C.c_int, P(vp), _sz, P(_sz)]),
         "fsvd_last_error_offset": (_sz, []),
+        "fsvd_factor_rank_r": (st, [_fp, _sz, _sz, _sz, _fp, _fp]),
+        "fsvd_factor_rank_r_batch": (st, [P(FactorJob), _sz]),
+        "fsvd_factorize_attention": (st, [_fp] * 6 + [_sz, _sz, _sz, _fp, _fp, _fp]),
+        "fsvd_factorize_layers": (st, [P(DenseLayer), _sz, _sz, P(_sz), P(_sz), P(_sz),
+                                       P(FactorBuffers)]),
+        "fsvd_last_factor_sweeps": (C.c_int, []),
         "fsvd_stream_workspace_bytes": (st, [P(vp), _sz, _sz, _sz, C.c_int, P(_sz)]),
         "fsvd_model_fwd_stream": (st, [P(vp), _sz, C.c_int, C.c_int, _sz, _sz, _sz, P(vp), P(vp),
                                        vp, _sz, vp]),

@@ -18,6 +18,7 @@
 
 #include "../../include/fsvd_b200.h"
 #include "common.cuh"
+#include "factorize.hpp"
 #include "meter.hpp"
 #include "model_file.hpp"
 #include "runtime.hpp"
@@ -443,6 +444,30 @@ void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_lay
 }  // namespace
 }  // namespace fsvd
 
+namespace fsvd {
+namespace {
+// factorize.cpp:25-39: geometry checks of factorize_attention.
+void check_attention_factoring(size_t d, size_t groups, size_t rank) {
+  if (groups == 0 || d % groups != 0) fail(Kind::Config, "groups must divide d_model");
+  if (rank == 0) fail(Kind::Rank, "rank must be at least 1");
+  if (rank > d / groups) fail(Kind::Rank, "rank exceeds per-group width d_model/groups");
+}
+// factorize.cpp:52-62: column block g of each projection -> one job.
+void attention_jobs(const float* const w[3], size_t d, size_t groups, size_t rank, float* u,
+                    float* v, std::vector<FactorJob>& js) {
+  const size_t gd = d / groups;
+  for (size_t m = 0; m < 3; ++m)
+    for (size_t g = 0; g < groups; ++g) {
+      const size_t i = m * groups + g;
+      js.push_back({w[m] + g * gd, d, d, gd, rank, u + i * d * rank, v + i * rank * gd});
+    }
+}
+void copy_attention_bias(const float* const b[3], size_t d, float* bias) {
+  for (size_t m = 0; m < 3; ++m) std::memcpy(bias + m * d, b[m], d * sizeof(float));
+}
+}  // namespace
+}  // namespace fsvd
+
 using namespace fsvd;
 
 extern "C" {
@@ -731,6 +756,103 @@ fsvd_status fsvd_model_load(const char* path, fsvd_dtype dtype, int dense,
   });
 }
 size_t fsvd_last_error_offset(void) { return format_error_offset(); }
+
+// ------------------------------------------------------------ factorization
+fsvd_status fsvd_factor_rank_r(const float* a, size_t m, size_t n, size_t rank, float* u,
+                               float* v) {
+  return guard([&] {
+    check_factor_job(m, n, rank);
+    require_device();
+    factor_rank_r_batch({FactorJob{a, n, m, n, rank, u, v}});
+  });
+}
+fsvd_status fsvd_factor_rank_r_batch(const fsvd_factor_job* jobs, size_t count) {
+  return guard([&] {
+    if (count && !jobs) fail(Kind::Config, "null argument");
+    std::vector<FactorJob> js;
+    for (size_t i = 0; i < count; ++i) {
+      check_factor_job(jobs[i].m, jobs[i].n, jobs[i].rank);
+      js.push_back({jobs[i].a, jobs[i].n, jobs[i].m, jobs[i].n, jobs[i].rank, jobs[i].u, jobs[i].v});
+    }
+    require_device();
+    factor_rank_r_batch(js);
+  });
+}
+
+
+fsvd_status fsvd_factorize_attention(const float* wq, const float* bq, const float* wk,
+                                     const float* bk, const float* wv, const float* bv,
+                                     size_t d_model, size_t groups, size_t rank, float* u,
+                                     float* v, float* bias) {
+  return guard([&] {
+    if (!wq || !bq || !wk || !bk || !wv || !bv || !u || !v || !bias)
+      fail(Kind::Config, "null argument");
+    if (d_model == 0) fail(Kind::Shape, "attention projections must be square d_model x d_model");
+    check_attention_factoring(d_model, groups, rank);
+    require_device();
+    const float* w[3] = {wq, wk, wv};
+    const float* b[3] = {bq, bk, bv};
+    std::vector<FactorJob> js;
+    attention_jobs(w, d_model, groups, rank, u, v, js);
+    factor_rank_r_batch(js);
+    copy_attention_bias(b, d_model, bias);
+  });
+}
+
+fsvd_status fsvd_factorize_layers(const fsvd_dense_layer* layers, size_t n_layers,
+                                  size_t groups, size_t* rank, size_t* proj_rank,
+                                  size_t* ffn_rank, const fsvd_factor_buffers* out) {
+  return guard([&] {
+    if (!layers || n_layers == 0) fail(Kind::Config, "synth_model: need at least one layer");
+    if (!rank || !proj_rank || !ffn_rank) fail(Kind::Config, "null argument");
+    const size_t d = layers[0].d_model, df = layers[0].d_ff;
+    for (size_t l = 0; l < n_layers; ++l)
+      if (layers[l].d_model != d || layers[l].d_ff != df || d == 0 || df == 0)
+        fail(Kind::Shape, "every layer must share a nonzero d_model / d_ff");
+    // model_io.cpp:482-499: zero knobs resolve to the matched defaults
+    if (groups == 0 || d % groups != 0) fail(Kind::Config, "groups must divide d_model");
+    const size_t r = *rank == 0 ? d / groups : *rank;
+    const size_t pr = *proj_rank == 0 ? std::min(r * groups, d) : *proj_rank;
+    const size_t fr = *ffn_rank == 0 ? std::min(pr, std::min(d, df)) : *ffn_rank;
+    check_attention_factoring(d, groups, r);
+    if (pr > d) fail(Kind::Rank, "proj_rank exceeds d_model");
+    if (fr > std::min(d, df)) fail(Kind::Rank, "ffn_rank exceeds min(d_model, d_ff)");
+    check_factor_job(d, d, pr);
+    check_factor_job(d, df, fr);
+    *rank = r;
+    *proj_rank = pr;
+    *ffn_rank = fr;
+    if (!out) return;
+    require_device();
+    std::vector<FactorJob> js;
+    for (size_t l = 0; l < n_layers; ++l) {
+      const fsvd_dense_layer& L = layers[l];
+      const fsvd_factor_buffers& o = out[l];
+      const float* w[3] = {L.wq, L.wk, L.wv};
+      for (const float* p : {L.wq, L.bq, L.wk, L.bk, L.wv, L.bv, L.wo, L.bo, L.w_in, L.b_in,
+                             L.w_out, L.b_out})
+        if (!p) fail(Kind::Config, "null dense weight");
+      for (float* p : {o.attn_u, o.attn_v, o.attn_b, o.out_u, o.out_v, o.out_b, o.up_u, o.up_v,
+                       o.up_b, o.down_u, o.down_v, o.down_b})
+        if (!p) fail(Kind::Config, "null output buffer");
+      attention_jobs(w, d, groups, r, o.attn_u, o.attn_v, js);
+      js.push_back({L.wo, d, d, d, pr, o.out_u, o.out_v});
+      js.push_back({L.w_in, df, d, df, fr, o.up_u, o.up_v});
+      js.push_back({L.w_out, d, df, d, fr, o.down_u, o.down_v});
+    }
+    factor_rank_r_batch(js);
+    for (size_t l = 0; l < n_layers; ++l) {
+      const fsvd_dense_layer& L = layers[l];
+      const fsvd_factor_buffers& o = out[l];
+      const float* b[3] = {L.bq, L.bk, L.bv};
+      copy_attention_bias(b, d, o.attn_b);
+      std::memcpy(o.out_b, L.bo, d * sizeof(float));
+      std::memcpy(o.up_b, L.b_in, df * sizeof(float));
+      std::memcpy(o.down_b, L.b_out, d * sizeof(float));
+    }
+  });
+}
+int fsvd_last_factor_sweeps(void) { return last_factor_sweeps(); }
 
 fsvd_status fsvd_stream_workspace_bytes(const fsvd_layer_pack* const* packs, size_t n_layers,
                                         size_t batch, size_t seq, fsvd_run_mode mode,
