@@ -81,6 +81,18 @@ def test_bert_base_shapes_match_reference(L, reference):
     assert 0 < L.fsvd_last_factor_sweeps() <= 60
 
 
+def test_very_tall_uses_row_split_clusters(L, reference):
+    """M = 6001 rows need 8-CTA clusters (row slices of 752) and uneven
+    padding; wide orientation of the same shape goes through A^T."""
+    a = _rand((6001, 40), 3, 0.01)
+    b = _rand((37, 5003), 4)
+    (u, v), (u2, v2) = F.factor_rank_r_batch([a, b], [8, 30])
+    ru, rv = reference.factor_rank_r(a, 8)
+    assert _close(u, ru) < TOL and _close(v, rv) < TOL
+    ru, rv = reference.factor_rank_r(b, 30)
+    assert _close(u2, ru) < TOL and _close(v2, rv) < TOL
+
+
 def test_deterministic(L):
     a = _rand((300, 200), 5)
     u1, v1 = F.factor_rank_r(a, 50)
