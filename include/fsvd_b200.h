@@ -282,6 +282,46 @@ fsvd_status fsvd_factorize_layers(const fsvd_dense_layer* layers, size_t n_layer
 int fsvd_last_factor_sweeps(void);
 
 /* ------------------------------------------------------------------ */
+/* Decoder rows: rank-space KV cache, causal        */
+/* prefill and single-token decode steps on the flash tensor-core path. */
+/* planner.cpp:123-141 closed forms; PAPER.md "Decoder Memory Cost      */
+/* Analysis".  The cache of one layer is [batch, max_seq, 2*G*rp] bf16   */
+/* (per token: G rank-space key blocks P_k, then G value blocks P_v).    */
+/* Causal semantics: layer by layer, the output at position i is the    */
+/* encoder layer's output on the prefix [0, i] of its inputs, last row   */
+/* (tests pin exactly that).                                              */
+/* ------------------------------------------------------------------ */
+/* planner.cpp:123-127: 4 * 2 * layers * B * M * r (FSVD_ERR_CONFIG on an
+ * invalid geometry or layers == 0). */
+fsvd_status fsvd_decoder_kv_cache_bytes(const fsvd_geometry* geom, size_t* bytes);
+/* planner.cpp:129-132: cache + 4 * (3 B M r + 2 B M r). */
+fsvd_status fsvd_decoder_prefill_bytes(const fsvd_geometry* geom, size_t* bytes);
+/* planner.cpp:134-141: step t in [1, seq_len]:
+ * 4 * (2 * layers * B r t + B r (t - 1) + 5 B r). */
+fsvd_status fsvd_decoder_decode_step_bytes(const fsvd_geometry* geom, size_t t, size_t* bytes);
+/* Device bytes of one layer's cache. */
+fsvd_status fsvd_kv_cache_bytes(const fsvd_layer_pack* pack, size_t batch, size_t max_seq,
+                                size_t* bytes);
+/* Workspace for prefills of up to max_seq tokens and for decode steps. */
+fsvd_status fsvd_decoder_workspace_bytes(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                         size_t batch, size_t max_seq, int pre_ln,
+                                         size_t* bytes);
+/* Causal forward of x [batch, seq, d] (seq <= max_seq) through every layer;
+ * fills rows [0, seq) of kv_caches[l] (device, one per layer).  x == out
+ * allowed.  Async on `stream`. */
+fsvd_status fsvd_decoder_prefill(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                 int pre_ln, size_t batch, size_t seq, const void* x, void* out,
+                                 void* const* kv_caches, size_t max_seq, void* ws,
+                                 size_t ws_bytes, void* stream);
+/* One new token per sequence at position pos (< max_seq; rows [0, pos) of
+ * every cache must hold the earlier tokens): x, out [batch, d]; appends row
+ * pos to every cache and attends keys [0, pos]. */
+fsvd_status fsvd_decoder_step(const fsvd_layer_pack* const* packs, size_t n_layers, int pre_ln,
+                              size_t batch, size_t pos, const void* x, void* out,
+                              void* const* kv_caches, size_t max_seq, void* ws, size_t ws_bytes,
+                              void* stream);
+
+/* ------------------------------------------------------------------ */
 /* Device-resident async API (device pointers, cudaStream_t as void*)   */
 /* ------------------------------------------------------------------ */
 /* Bytes of workspace fsvd_model_fwd needs for this batch shape; the

@@ -142,6 +142,7 @@ class Reference(_Base):
         L.ref_flops_exact.argtypes = [_P(abi.Geometry), C.c_int]
         L.ref_flops_exact.restype = C.c_ulonglong
         L.ref_factor_rank_r.argtypes = [_fp, _sz, _sz, _sz, _fp, _fp]
+        L.ref_decoder_bytes.argtypes = [C.c_int, _P(abi.Geometry), _sz, _P(_sz)]
         L.ref_svd.argtypes = [_fp, _sz, _sz, _fp, _fp, _fp]
         L.ref_factorize_attention.argtypes = [_fp] * 6 + [_sz, _sz, _sz, _fp, _fp, _fp]
 
@@ -197,6 +198,12 @@ class Reference(_Base):
 
     def flops_exact(self, geom, mode):
         return self.lib.ref_flops_exact(geom, mode)
+
+    def decoder_bytes(self, which, geom, t=0):
+        """planner.cpp:123-141 -> (status, bytes); which 0 cache, 1 prefill, 2 step."""
+        b = _sz(0)
+        st = self.lib.ref_decoder_bytes(which, geom, t, C.byref(b))
+        return st, b.value
 
     def factor_rank_r(self, a, r):
         """svd.cpp:412-456 -> (u [m, r], v [r, n])."""

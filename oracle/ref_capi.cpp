@@ -279,6 +279,16 @@ long long ref_read_error_offset(const char* path) {
   }
 }
 
+// planner.cpp:123-141 -- decoder closed forms; which 0 kv cache, 1 prefill,
+// 2 decode step at t.  Returns the reference's status (0 ok).
+int ref_decoder_bytes(int which, const fsvd_geometry* g, size_t t, size_t* out) {
+  return guard([&] {
+    Geometry geo{g->batch, g->seq_len, g->d_model, g->d_ff, g->heads, g->groups, g->rank,
+                 g->layers};
+    *out = which == 0 ? decoder_kv_cache_bytes(geo)
+                      : which == 1 ? decoder_prefill_bytes(geo) : decoder_decode_step_bytes(geo, t);
+  });
+}
 // svd.cpp:412-456 -- leading-r even-split factors of a row-major m x n matrix.
 int ref_factor_rank_r(const float* a, size_t m, size_t n, size_t r, float* u, float* v) {
   return guard([&] {

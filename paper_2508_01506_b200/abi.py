@@ -150,6 +150,15 @@ def _declare(lib):
         "fsvd_factorize_layers": (st, [P(DenseLayer), _sz, _sz, P(_sz), P(_sz), P(_sz),
                                        P(FactorBuffers)]),
         "fsvd_last_factor_sweeps": (C.c_int, []),
+        "fsvd_decoder_kv_cache_bytes": (st, [P(Geometry), P(_sz)]),
+        "fsvd_decoder_prefill_bytes": (st, [P(Geometry), P(_sz)]),
+        "fsvd_decoder_decode_step_bytes": (st, [P(Geometry), _sz, P(_sz)]),
+        "fsvd_kv_cache_bytes": (st, [vp, _sz, _sz, P(_sz)]),
+        "fsvd_decoder_workspace_bytes": (st, [P(vp), _sz, _sz, _sz, C.c_int, P(_sz)]),
+        "fsvd_decoder_prefill": (st, [P(vp), _sz, C.c_int, _sz, _sz, vp, vp, P(vp), _sz, vp, _sz,
+                                      vp]),
+        "fsvd_decoder_step": (st, [P(vp), _sz, C.c_int, _sz, _sz, vp, vp, P(vp), _sz, vp, _sz,
+                                   vp]),
         "fsvd_stream_workspace_bytes": (st, [P(vp), _sz, _sz, _sz, C.c_int, P(_sz)]),
         "fsvd_model_fwd_stream": (st, [P(vp), _sz, C.c_int, C.c_int, _sz, _sz, _sz, P(vp), P(vp),
                                        vp, _sz, vp]),

@@ -125,7 +125,7 @@ template <int RP>
 __global__ void __launch_bounds__(kThreads, 2)
     k_attn_rankspace(const __grid_constant__ CUtensorMap tmQKV, bf16* __restrict__ out,
                      int64_t ldo, int batch, int seq, int heads, int groups, int q_off, int k_off,
-                     int v_off) {
+                     int v_off, int causal) {
   using C = AttnCfg<RP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_arrive_expect_tx(&bars->q_full[qs], C::TILE);
         tma_load_2d(&tmQKV, &bars->q_full[qs], smem + C::o_q + qs * up1k(C::TILE),
                     q_off + h * RP, row0 + qt * QT);
-        for (int j = 0; j < nj; ++j) {
+        const int nji = causal ? min(nj, qt + 1) : nj;  // key tiles of this item
+        for (int j = 0; j < nji; ++j) {
           mbar_wait(&bars->kv_empty[st], ph ^ 1);
           uint8_t* kv = smem + C::o_kv + st * C::KV_STAGE;
           mbar_arrive_expect_tx(&bars->kv_full[st], 2 * C::TILE);
@@ -211,12 +212,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     };
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
       const int qs = it & 1;
+      const int nji = causal ? min(nj, w % nqt + 1) : nj;
       mbar_wait(&bars->q_full[qs], (it >> 1) & 1);
       if (lane == 0 && it == 0) ATRACE(1);
       issue_s(gt, qs);
-      for (int j = 0; j < nj; ++j) {
+      for (int j = 0; j < nji; ++j) {
         const int t = gt + j;
-        if (j + 1 < nj) {
+        if (j + 1 < nji) {
           issue_s(t + 1, qs);
         } else {
           if (elect_one()) mma_commit(&bars->q_empty[qs]);  // after this item's last S
@@ -238,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         __syncwarp();
       }
-      gt += nj;
+      gt += nji;
     }
   } else {
     // ------------------------------------------------ softmax (8 warps)
@@ -272,8 +274,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
       const int qt = w % nqt, h = (w / nqt) % heads, b = w / (nqt * heads);
       const int row0 = b * seq, q0 = qt * QT;
+      const int nji = causal ? min(nj, qt + 1) : nj;
       float m_run = -INFINITY, l_run = 0.0f;
-      for (int j = 0; j < nj; ++j) {
+      for (int j = 0; j < nji; ++j) {
         const int t = gt + j;
         if (threadIdx.x == 0 && it == 0) ATRACE(112 + j);
         mbar_wait(&bars->s_full, t & 1);
@@ -290,7 +293,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&bars->s_free);
-        const int valid = seq - j * KT - static_cast<int>(half) * KH;  // in-sequence keys here
+        // keys of this thread's half that are in the sequence (and, causal,
+        // not after the query: key index <= query index)
+        int valid = seq - j * KT - static_cast<int>(half) * KH;
+        if (causal && j == qt)
+          valid = min(valid, static_cast<int>(row) - static_cast<int>(half) * KH + 1);
         if (valid < KH) {
 #pragma unroll
           for (int i = 0; i < KH; ++i) s[i] = (i < valid) ? s[i] : -INFINITY;
@@ -334,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         tc_fence_before();
         mbar_arrive(&bars->p_full);
       }
-      gt += nj;
+      gt += nji;
       bars->xsum[half][row] = l_run;
       mbar_wait(&bars->o_full, (gt - 1) & 1);
       tc_fence_after();
@@ -390,7 +397,8 @@ void launch_attn(const AttnTcArgs& a, cudaStream_t s) {
   const int items = ((a.seq + QT - 1) / QT) * a.heads * a.batch;
   const int grid = items < 2 * num_sms() ? items : 2 * num_sms();
   k_attn_rankspace<RP><<<grid, kThreads, C::SMEM, s>>>(tm, a.out, a.ldo, a.batch, a.seq, a.heads,
-                                                       a.groups, a.q_off, a.k_off, a.v_off);
+                                                       a.groups, a.q_off, a.k_off, a.v_off,
+                                                       a.causal ? 1 : 0);
   check_launch("k_attn_rankspace");
 }
 

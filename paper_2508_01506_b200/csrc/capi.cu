@@ -854,6 +854,115 @@ fsvd_status fsvd_factorize_layers(const fsvd_dense_layer* layers, size_t n_layer
 }
 int fsvd_last_factor_sweeps(void) { return last_factor_sweeps(); }
 
+// ------------------------------------------------------------ decoder rows
+namespace {
+// geometry.hpp:24-34 (Geometry::validate) + planner.cpp:41-43 (require_layers)
+void validate_decoder_geometry(const fsvd_geometry& g) {
+  if (g.batch == 0 || g.seq_len == 0 || g.d_model == 0 || g.d_ff == 0)
+    fail(Kind::Config, "geometry extents must be positive");
+  if (g.heads == 0 || g.d_model % g.heads != 0) fail(Kind::Config, "heads must divide d_model");
+  if (g.groups == 0 || g.d_model % g.groups != 0) fail(Kind::Config, "groups must divide d_model");
+  if (g.rank == 0) fail(Kind::Rank, "rank must be at least 1");
+  if (g.rank > g.d_model / g.groups) fail(Kind::Rank, "rank exceeds per-group width d_model/groups");
+  if (g.layers == 0) fail(Kind::Config, "decoder needs at least one layer");
+}
+size_t kv_closed(const fsvd_geometry& g) {
+  validate_decoder_geometry(g);
+  return 4 * 2 * g.layers * g.batch * g.seq_len * g.rank;
+}
+void check_decoder_call(const fsvd_layer_pack* const* packs, size_t n_layers,
+                        void* const* caches, size_t batch, size_t max_seq) {
+  if (!packs || n_layers == 0 || !caches) fail(Kind::Config, "null argument");
+  if (batch == 0 || max_seq == 0) fail(Kind::Config, "batch and max_seq must be positive");
+  for (size_t i = 0; i < n_layers; ++i) {
+    if (!packs[i] || !caches[i]) fail(Kind::Config, "null layer pack or cache");
+    check_decoder_pack(*packs[i]->p);
+  }
+}
+}  // namespace
+
+fsvd_status fsvd_decoder_kv_cache_bytes(const fsvd_geometry* geom, size_t* bytes) {
+  return guard([&] {
+    if (!geom || !bytes) fail(Kind::Config, "null argument");
+    *bytes = kv_closed(*geom);
+  });
+}
+fsvd_status fsvd_decoder_prefill_bytes(const fsvd_geometry* geom, size_t* bytes) {
+  return guard([&] {
+    if (!geom || !bytes) fail(Kind::Config, "null argument");
+    const size_t bmr = geom->batch * geom->seq_len * geom->rank;
+    *bytes = kv_closed(*geom) + 4 * (3 * bmr + 2 * bmr);
+  });
+}
+fsvd_status fsvd_decoder_decode_step_bytes(const fsvd_geometry* geom, size_t t, size_t* bytes) {
+  return guard([&] {
+    if (!geom || !bytes) fail(Kind::Config, "null argument");
+    validate_decoder_geometry(*geom);
+    if (t < 1 || t > geom->seq_len) fail(Kind::Config, "decode step must lie in [1, seq_len]");
+    const size_t br = geom->batch * geom->rank;
+    *bytes = 4 * (2 * geom->layers * br * t + br * (t - 1) + 5 * br);
+  });
+}
+fsvd_status fsvd_kv_cache_bytes(const fsvd_layer_pack* pack, size_t batch, size_t max_seq,
+                                size_t* bytes) {
+  return guard([&] {
+    if (!pack || !bytes) fail(Kind::Config, "null argument");
+    check_decoder_pack(*pack->p);
+    *bytes = kv_cache_bytes(*pack->p, batch, max_seq);
+  });
+}
+fsvd_status fsvd_decoder_workspace_bytes(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                         size_t batch, size_t max_seq, int pre_ln,
+                                         size_t* bytes) {
+  return guard([&] {
+    if (!packs || n_layers == 0 || !bytes) fail(Kind::Config, "null argument");
+    size_t ws = 0;
+    for (size_t i = 0; i < n_layers; ++i) {
+      check_decoder_pack(*packs[i]->p);
+      ws = std::max(ws, decoder_workspace_bytes(*packs[i]->p, batch, max_seq, pre_ln != 0));
+    }
+    *bytes = ws;
+  });
+}
+fsvd_status fsvd_decoder_prefill(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                 int pre_ln, size_t batch, size_t seq, const void* x, void* out,
+                                 void* const* kv_caches, size_t max_seq, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  return guard([&] {
+    check_decoder_call(packs, n_layers, kv_caches, batch, max_seq);
+    if (seq == 0 || seq > max_seq) fail(Kind::Config, "prefill length must lie in [1, max_seq]");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (size_t i = 0; i < n_layers; ++i) {
+      AttnMode am;
+      am.kind = AttnMode::Prefill;
+      am.cache = kv_caches[i];
+      am.max_seq = max_seq;
+      am.pos = 0;
+      layer_fwd(*packs[i]->p, FSVD_MODE_FLASH_V2, pre_ln != 0, batch, seq, i == 0 ? x : out, out,
+                ws, ws_bytes, s, am);
+    }
+  });
+}
+fsvd_status fsvd_decoder_step(const fsvd_layer_pack* const* packs, size_t n_layers, int pre_ln,
+                              size_t batch, size_t pos, const void* x, void* out,
+                              void* const* kv_caches, size_t max_seq, void* ws, size_t ws_bytes,
+                              void* stream) {
+  return guard([&] {
+    check_decoder_call(packs, n_layers, kv_caches, batch, max_seq);
+    if (pos >= max_seq) fail(Kind::Config, "decode position must be below max_seq");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (size_t i = 0; i < n_layers; ++i) {
+      AttnMode am;
+      am.kind = AttnMode::Decode;
+      am.cache = kv_caches[i];
+      am.max_seq = max_seq;
+      am.pos = pos;
+      layer_fwd(*packs[i]->p, FSVD_MODE_FLASH_V2, pre_ln != 0, batch, 1, i == 0 ? x : out, out,
+                ws, ws_bytes, s, am);
+    }
+  });
+}
+
 fsvd_status fsvd_stream_workspace_bytes(const fsvd_layer_pack* const* packs, size_t n_layers,
                                         size_t batch, size_t seq, fsvd_run_mode mode,
                                         size_t* bytes) {

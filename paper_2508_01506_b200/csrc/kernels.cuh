@@ -47,8 +47,28 @@ struct AttnTcArgs {
   int batch, seq, heads, groups, rank_pad;
   bf16* out;
   int64_t ldo;
+  bool causal = false;  // decoder prefill: key j visible to query i iff j <= i
 };
 void attn_rankspace_bf16(const AttnTcArgs& a, cudaStream_t s);
+
+// ---- decoder: rank-space KV cache (decode.cu) ------------------------------------
+struct DecodeArgs {
+  const bf16* qkv;  // [batch, ldq] projection rows of the new tokens
+  int64_t ldq;
+  int q_off;
+  const bf16* cache;  // [batch, max_seq, 2*groups*rank_pad]
+  int max_seq, batch, heads, groups, rank_pad;
+  int len;     // cached tokens attended (new token included)
+  int splits;  // decode_splits(batch, heads, len)
+  float* part;  // splits > 1: [batch*heads, splits, rank_pad + 2]
+  bf16* out;
+  int64_t ldo;
+};
+int decode_splits(int batch, int heads, int len);
+size_t decode_partial_bytes(int batch, int heads, int rank_pad, int max_len);
+void attn_decode_bf16(const DecodeArgs& a, cudaStream_t s);
+void kv_store_bf16(const bf16* src, int64_t lds, int c0, int width, int batch, int rows_per_b,
+                   bf16* cache, int max_seq, int pos0, cudaStream_t s);
 bool attn_rankspace_supported(int rank_pad);
 
 // ---- K3 / K4: FlashSVD-FFN -----------------------------------------------------

@@ -445,7 +445,7 @@ void simt_attention_t(const Pack& p, size_t B, size_t M, const void* x, void* ct
 
 void tc_attention(size_t B, size_t M, const bf16* qkv, int qkv_cols, int q_off, int k_off,
                   int v_off, int heads, int groups, int rp, void* out, int64_t ldo,
-                  cudaStream_t s) {
+                  cudaStream_t s, bool causal = false) {
   AttnTcArgs a;
   a.qkv = qkv;
   a.ldq = qkv_cols;
@@ -460,18 +460,47 @@ void tc_attention(size_t B, size_t M, const bf16* qkv, int qkv_cols, int q_off, 
   a.rank_pad = rp;
   a.out = as<bf16>(out);
   a.ldo = ldo;
+  a.causal = causal;
   attn_rankspace_bf16(a, s);
 }
 
 // Tensor-core flash attention up to the rank-space output O [T, H*rp]:
 // K1 projection into [Qt | P_k | P_v], then K2.
 void tc_attention_rank(const Pack& p, size_t B, size_t M, const void* x, void* o_rank,
-                       void* trans, cudaStream_t s) {
+                       void* trans, cudaStream_t s, const AttnMode& am = AttnMode{}) {
   const int T = static_cast<int>(B * M), n = p.qkv_cols;
   bf16* qkv = as<bf16>(trans);
   gemm_bf16(as<bf16>(x), p.d, as<bf16>(p.wproj_t), p.d, qkv, n, T, n, p.d, p.bproj, ACT_NONE, s);
-  tc_attention(B, M, qkv, n, 0, p.H * p.rp, (p.H + p.G) * p.rp, p.H, p.G, p.rp, o_rank,
-               (int64_t)p.H * p.rp, s);
+  const int hr = p.H * p.rp, kv_w = 2 * p.G * p.rp;
+  if (am.kind == AttnMode::Full) {
+    tc_attention(B, M, qkv, n, 0, hr, (p.H + p.G) * p.rp, p.H, p.G, p.rp, o_rank, hr, s);
+    return;
+  }
+  // decoder rows: the new tokens' [P_k | P_v] columns go to the rank-space cache
+  kv_store_bf16(qkv, n, hr, kv_w, static_cast<int>(B), static_cast<int>(M), as<bf16>(am.cache),
+                static_cast<int>(am.max_seq), static_cast<int>(am.pos), s);
+  if (am.kind == AttnMode::Prefill) {
+    tc_attention(B, M, qkv, n, 0, hr, (p.H + p.G) * p.rp, p.H, p.G, p.rp, o_rank, hr, s, true);
+    return;
+  }
+  DecodeArgs a;
+  a.qkv = qkv;
+  a.ldq = n;
+  a.q_off = 0;
+  a.cache = as<bf16>(am.cache);
+  a.max_seq = static_cast<int>(am.max_seq);
+  a.batch = static_cast<int>(B);
+  a.heads = p.H;
+  a.groups = p.G;
+  a.rank_pad = p.rp;
+  a.len = static_cast<int>(am.pos) + 1;
+  a.splits = decode_splits(a.batch, a.heads, a.len);
+  // split partials live right after the projection rows
+  a.part = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(qkv + (size_t)T * n) + 255) & ~uintptr_t(255));
+  a.out = as<bf16>(o_rank);
+  a.ldo = hr;
+  attn_decode_bf16(a, s);
 }
 
 // Materializing baselines: dense Q|K|V [T, 3d] (dense twin or rebuilt from
@@ -543,11 +572,11 @@ void outproj_fwd(const Pack& p, int mode, size_t B, size_t M, const void* ctx, v
 // core flash path the rank-space attention output feeds the folded
 // out-projection directly (one GEMM, K = H*rp); `scratch` holds it.
 void attention_block(const Pack& p, int mode, size_t B, size_t M, const void* x, void* scratch,
-                     void* branch, void* trans, cudaStream_t s) {
+                     void* branch, void* trans, cudaStream_t s, const AttnMode& am = AttnMode{}) {
   const bool flash = mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2;
   if (flash && p.attn_tc && p.out_tc) {
     const int T = static_cast<int>(B * M), hr = p.H * p.rp;
-    tc_attention_rank(p, B, M, x, scratch, trans, s);
+    tc_attention_rank(p, B, M, x, scratch, trans, s, am);
     gemm_bf16(as<bf16>(scratch), hr, as<bf16>(p.wov_t), hr, as<bf16>(branch), p.d, T, p.d, hr,
               p.bov, ACT_NONE, s);
     return;
@@ -694,20 +723,28 @@ bool ffn_ln_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void
 }
 
 void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const void* x, void* out,
-               void* ws, size_t ws_bytes, cudaStream_t s) {
+               void* ws, size_t ws_bytes, cudaStream_t s, const AttnMode& am) {
   const size_t T = B * M;
   const WsLayout lay = ws_layout(p, T, mode, pre_ln);
-  if (ws_bytes < lay.total())
-    fail(Kind::Config, "workspace too small: need " + std::to_string(lay.total()) +
-                           " bytes, got " + std::to_string(ws_bytes));
+  const size_t need =
+      lay.total() + (am.kind == AttnMode::Decode
+                         ? align256(decode_partial_bytes(static_cast<int>(B), p.H, p.rp,
+                                                         static_cast<int>(am.pos) + 1)) + 256
+                         : 0);
+  if (ws_bytes < need)
+    fail(Kind::Config, "workspace too small: need " + std::to_string(need) + " bytes, got " +
+                           std::to_string(ws_bytes));
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
   void* A = base;
   void* Bb = base + lay.a;
   void* trans = base + lay.a + lay.b;
   const int rows = static_cast<int>(T);
+  if (am.kind != AttnMode::Full && !(p.attn_tc && p.out_tc &&
+                                      (mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2)))
+    fail(Kind::Config, "decoder rows run on the bf16 tensor-core flash path");
   if (!pre_ln && fused_post_ln(p, mode)) {
     // rank-space attention -> A; folded out-projection + residual + LN1 -> B
-    tc_attention_rank(p, B, M, x, A, trans, s);
+    tc_attention_rank(p, B, M, x, A, trans, s, am);
     gemm_ln_bf16(as<bf16>(A), p.H * p.rp, as<bf16>(p.wov_t), p.H * p.rp, p.bov, as<bf16>(x),
                  p.ln1g, p.ln1b, p.eps1, as<bf16>(Bb), rows, p.d, p.H * p.rp, s);
     if (!ffn_ln_fwd(p, mode, B, M, Bb, out, trans, s)) {              // out = LN2(B + ffn(B))
@@ -715,18 +752,36 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
       ln(p, Bb, A, p.ln2g, p.ln2b, p.eps2, out, rows, s);
     }
   } else if (!pre_ln) {
-    attention_block(p, mode, B, M, x, A, Bb, trans, s);               // branch -> B
+    attention_block(p, mode, B, M, x, A, Bb, trans, s, am);           // branch -> B
     ln(p, x, Bb, p.ln1g, p.ln1b, p.eps1, Bb, rows, s);                // resid  -> B (in place)
     ffn_fwd(p, mode, B, M, Bb, A, trans, s);                          // ffn    -> A
     ln(p, Bb, A, p.ln2g, p.ln2b, p.eps2, out, rows, s);               // out
   } else {
     ln(p, x, nullptr, p.ln1g, p.ln1b, p.eps1, A, rows, s);            // normed -> A
-    attention_block(p, mode, B, M, A, Bb, A, trans, s);               // branch -> A (via B)
+    attention_block(p, mode, B, M, A, Bb, A, trans, s, am);           // branch -> A (via B)
     add(p, x, A, Bb, (int64_t)T * p.d, s);                            // resid  -> B
     ln(p, Bb, nullptr, p.ln2g, p.ln2b, p.eps2, A, rows, s);           // normed -> A
     ffn_fwd(p, mode, B, M, A, out, trans, s);                         // ffn    -> out
     add(p, Bb, out, out, (int64_t)T * p.d, s);                        // out = resid + ffn
   }
+}
+
+void check_decoder_pack(const Pack& p) {
+  if (!(p.attn_tc && p.out_tc))
+    fail(Kind::Config, "decoder rows run on the bf16 tensor-core flash path (bf16 pack, "
+                       "rank padding 16/32/64)");
+}
+
+size_t kv_cache_bytes(const Pack& p, size_t B, size_t max_seq) {
+  return B * max_seq * 2 * p.G * p.rp * p.es;
+}
+
+size_t decoder_workspace_bytes(const Pack& p, size_t B, size_t max_seq, bool pre_ln) {
+  const size_t prefill = layer_workspace_bytes(p, B * max_seq, FSVD_MODE_FLASH_V2, pre_ln);
+  const size_t step = layer_workspace_bytes(p, B, FSVD_MODE_FLASH_V2, pre_ln) +
+                      align256(decode_partial_bytes(static_cast<int>(B), p.H, p.rp,
+                                                    static_cast<int>(max_seq))) + 256;
+  return std::max(prefill, step);
 }
 
 }  // namespace fsvd

@@ -97,8 +97,20 @@ void outproj_fwd(const Pack& p, int mode, size_t B, size_t M, const void* ctx, v
                  void* trans, cudaStream_t s);
 void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* out, void* trans,
              cudaStream_t s);
+// Attention variant of a layer run: the encoder's full attention, or the
+// decoder rows (f4) on a layer's rank-space KV cache [B, max_seq, 2*G*rp].
+struct AttnMode {
+  enum Kind { Full, Prefill, Decode } kind = Full;
+  void* cache = nullptr;
+  size_t max_seq = 0;
+  size_t pos = 0;  // Decode: position of the new token (keys 0..pos)
+};
 void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const void* x, void* out,
-               void* ws, size_t ws_bytes, cudaStream_t s);
+               void* ws, size_t ws_bytes, cudaStream_t s, const AttnMode& am = AttnMode{});
+// Decoder: workspace for prefill of up to max_seq tokens and for decode steps.
+size_t decoder_workspace_bytes(const Pack& p, size_t B, size_t max_seq, bool pre_ln);
+size_t kv_cache_bytes(const Pack& p, size_t B, size_t max_seq);
+void check_decoder_pack(const Pack& p);
 
 uint16_t f32_to_bf16_bits(float f);
 
