@@ -472,7 +472,9 @@ void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, 
     launch_gemm2<128, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
     return;
   }
-  if (N % 256 == 0)
+  if (M <= 128 && N % 64 == 0 && N >= 128)  // one row tile (decode rows): most CTAs
+    launch_gemm<64, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+  else if (N % 256 == 0)
     launch_gemm<256, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
   else if (N % 192 == 0)
     launch_gemm<192, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);

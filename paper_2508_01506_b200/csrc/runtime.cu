@@ -722,17 +722,79 @@ bool ffn_ln_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void
   return true;
 }
 
+namespace {
+// Decode step (T = batch rows, one token each): A [T, max(H*rp, d)], B [T, d],
+// transient = max(projection rows + split partials, FFN chain P | hidden | Z |
+// branch).
+struct DecodeLayout {
+  size_t a, b, t;
+  size_t total() const { return a + b + t + 256; }
+};
+DecodeLayout decode_layout(const Pack& p, size_t T, size_t len) {
+  const size_t es = p.es;
+  const size_t attn = align256(T * p.qkv_cols * es) +
+                      align256(decode_partial_bytes(static_cast<int>(T), p.H, p.rp,
+                                                    static_cast<int>(len)));
+  const size_t ffn = align256(T * (2 * (size_t)p.frp + p.df + p.d) * es);
+  return {align256(T * std::max<size_t>((size_t)p.H * p.rp, p.d) * es), align256(T * p.d * es),
+          std::max(attn, ffn)};
+}
+// Skinny FFN branch for decode rows: four GEMMs spread over many CTAs
+// (the fused K4 runs one CTA per 128-row tile, i.e. one CTA here).
+void ffn_branch_skinny(const Pack& p, int T, const void* x, void* branch, void* trans,
+                       cudaStream_t s) {
+  bf16* P = as<bf16>(trans);
+  bf16* hid = P + (size_t)T * p.frp;
+  bf16* Z = hid + (size_t)T * p.df;
+  gemm_bf16(as<bf16>(x), p.d, as<bf16>(p.uup_t), p.d, P, p.frp, T, p.frp, p.d, nullptr, ACT_NONE, s);
+  gemm_bf16(P, p.frp, as<bf16>(p.vup_t), p.frp, hid, p.df, T, p.df, p.frp, p.bup, p.act, s);
+  gemm_bf16(hid, p.df, as<bf16>(p.udn_t), p.df, Z, p.frp, T, p.frp, p.df, nullptr, ACT_NONE, s);
+  gemm_bf16(Z, p.frp, as<bf16>(p.vdn_t), p.frp, as<bf16>(branch), p.d, T, p.d, p.frp, p.bdn,
+            ACT_NONE, s);
+}
+void layer_decode(const Pack& p, bool pre_ln, size_t B, const void* x, void* out, void* ws,
+                  size_t ws_bytes, cudaStream_t s, const AttnMode& am) {
+  const DecodeLayout lay = decode_layout(p, B, am.pos + 1);
+  if (ws_bytes < lay.total())
+    fail(Kind::Config, "workspace too small: need " + std::to_string(lay.total()) + " bytes, got " +
+                           std::to_string(ws_bytes));
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+  void* A = base;
+  void* Bb = base + lay.a;
+  void* trans = base + lay.a + lay.b;
+  const int T = static_cast<int>(B), hr = p.H * p.rp;
+  bf16* branch = as<bf16>(trans) + (size_t)T * (2 * p.frp + p.df);  // FFN chain's last slot
+  if (!pre_ln) {
+    tc_attention_rank(p, B, 1, x, A, trans, s, am);                          // O_rank -> A
+    gemm_bf16(as<bf16>(A), hr, as<bf16>(p.wov_t), hr, branch, p.d, T, p.d, hr, p.bov, ACT_NONE, s);
+    ln(p, x, branch, p.ln1g, p.ln1b, p.eps1, Bb, T, s);                       // resid -> B
+    ffn_branch_skinny(p, T, Bb, branch, trans, s);
+    ln(p, Bb, branch, p.ln2g, p.ln2b, p.eps2, out, T, s);                     // out
+  } else {
+    ln(p, x, nullptr, p.ln1g, p.ln1b, p.eps1, Bb, T, s);                      // normed -> B
+    tc_attention_rank(p, B, 1, Bb, A, trans, s, am);                          // O_rank -> A
+    gemm_bf16(as<bf16>(A), hr, as<bf16>(p.wov_t), hr, branch, p.d, T, p.d, hr, p.bov, ACT_NONE, s);
+    add(p, x, branch, Bb, (int64_t)T * p.d, s);                               // resid -> B
+    ln(p, Bb, nullptr, p.ln2g, p.ln2b, p.eps2, A, T, s);                      // normed -> A
+    ffn_branch_skinny(p, T, A, branch, trans, s);
+    add(p, Bb, branch, out, (int64_t)T * p.d, s);                             // out
+  }
+}
+}  // namespace
+
 void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const void* x, void* out,
                void* ws, size_t ws_bytes, cudaStream_t s, const AttnMode& am) {
+  if (am.kind == AttnMode::Decode) {
+    if (M != 1) fail(Kind::Config, "a decode step carries one token per sequence");
+    if (!(p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16))
+      fail(Kind::Config, "decoder rows run on the bf16 tensor-core flash path");
+    layer_decode(p, pre_ln, B, x, out, ws, ws_bytes, s, am);
+    return;
+  }
   const size_t T = B * M;
   const WsLayout lay = ws_layout(p, T, mode, pre_ln);
-  const size_t need =
-      lay.total() + (am.kind == AttnMode::Decode
-                         ? align256(decode_partial_bytes(static_cast<int>(B), p.H, p.rp,
-                                                         static_cast<int>(am.pos) + 1)) + 256
-                         : 0);
-  if (ws_bytes < need)
-    fail(Kind::Config, "workspace too small: need " + std::to_string(need) + " bytes, got " +
+  if (ws_bytes < lay.total())
+    fail(Kind::Config, "workspace too small: need " + std::to_string(lay.total()) + " bytes, got " +
                            std::to_string(ws_bytes));
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
   void* A = base;
@@ -767,7 +829,7 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
 }
 
 void check_decoder_pack(const Pack& p) {
-  if (!(p.attn_tc && p.out_tc))
+  if (!(p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16))
     fail(Kind::Config, "decoder rows run on the bf16 tensor-core flash path (bf16 pack, "
                        "rank padding 16/32/64)");
 }
@@ -778,10 +840,8 @@ size_t kv_cache_bytes(const Pack& p, size_t B, size_t max_seq) {
 
 size_t decoder_workspace_bytes(const Pack& p, size_t B, size_t max_seq, bool pre_ln) {
   const size_t prefill = layer_workspace_bytes(p, B * max_seq, FSVD_MODE_FLASH_V2, pre_ln);
-  const size_t step = layer_workspace_bytes(p, B, FSVD_MODE_FLASH_V2, pre_ln) +
-                      align256(decode_partial_bytes(static_cast<int>(B), p.H, p.rp,
-                                                    static_cast<int>(max_seq))) + 256;
-  return std::max(prefill, step);
+  (void)pre_ln;
+  return std::max(prefill, decode_layout(p, B, max_seq).total());
 }
 
 }  // namespace fsvd
