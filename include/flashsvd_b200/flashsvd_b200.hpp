@@ -34,6 +34,7 @@
 #include "flashsvd/attention.hpp"
 #include "flashsvd/encoder.hpp"
 #include "flashsvd/errors.hpp"
+#include "flashsvd/factorize.hpp"
 #include "flashsvd/ffn.hpp"
 #include "flashsvd/memtier.hpp"
 #include "flashsvd/tensor.hpp"
@@ -317,6 +318,83 @@ inline void run_layer(const Tensor& x, const EncoderLayer& layer, RunMode mode,
       out.data()));
   mm.replay(meter);
   st.raise_if_failed();
+}
+
+// ------------------------------------------------------------ factorization
+// svd.cpp:412-456: leading-r even-split factors on the device (fp64 Jacobi).
+inline LowRankPair factor_rank_r(const Tensor& a, std::size_t r) {
+  if (a.ndim() != 2) throw ShapeError("factorization input must be 2-D");
+  const std::size_t m = a.shape()[0], n = a.shape()[1];
+  LowRankPair out{Tensor({m, r == 0 ? 1 : r}), Tensor({r == 0 ? 1 : r, n})};
+  detail::check(fsvd_factor_rank_r(a.data(), m, n, r, out.u.data(), out.v.data()));
+  return out;
+}
+
+// factorize.cpp:10-17
+inline FactorizedLinear factorize_linear(const Tensor& w, const Tensor& bias, std::size_t rank) {
+  if (w.shape().size() != 2) throw ShapeError("factorize_linear expects a matrix");
+  if (bias.shape().size() != 1 || bias.shape()[0] != w.shape()[1])
+    throw ShapeError("bias length must match the output dimension");
+  LowRankPair pair = b200::factor_rank_r(w, rank);
+  return FactorizedLinear{std::move(pair.u), std::move(pair.v), bias};
+}
+
+// ffn.cpp:108-116 -- both matrices in one device run
+inline FfnFactors factorize_ffn(const Tensor& w_in, const Tensor& b_in, const Tensor& w_out,
+                                const Tensor& b_out, std::size_t rank, Activation act) {
+  for (const Tensor* w : {&w_in, &w_out})
+    if (w->shape().size() != 2) throw ShapeError("factorize_linear expects a matrix");
+  if (b_in.shape().size() != 1 || b_in.shape()[0] != w_in.shape()[1] ||
+      b_out.shape().size() != 1 || b_out.shape()[0] != w_out.shape()[1])
+    throw ShapeError("bias length must match the output dimension");
+  FfnFactors f;
+  f.up = FactorizedLinear{Tensor({w_in.shape()[0], rank ? rank : 1}),
+                          Tensor({rank ? rank : 1, w_in.shape()[1]}), b_in};
+  f.down = FactorizedLinear{Tensor({w_out.shape()[0], rank ? rank : 1}),
+                            Tensor({rank ? rank : 1, w_out.shape()[1]}), b_out};
+  fsvd_factor_job jobs[2] = {
+      {w_in.data(), w_in.shape()[0], w_in.shape()[1], rank, f.up.u.data(), f.up.v.data()},
+      {w_out.data(), w_out.shape()[0], w_out.shape()[1], rank, f.down.u.data(), f.down.v.data()}};
+  detail::check(fsvd_factor_rank_r_batch(jobs, 2));
+  f.activation = act;
+  return f;
+}
+
+// factorize.cpp:21-64 -- all 3*groups blocks in one device run
+inline AttentionFactorSet factorize_attention(const Tensor& wq, const Tensor& bq, const Tensor& wk,
+                                              const Tensor& bk, const Tensor& wv, const Tensor& bv,
+                                              std::size_t groups, std::size_t rank) {
+  const Tensor* weights[3] = {&wq, &wk, &wv};
+  const Tensor* biases[3] = {&bq, &bk, &bv};
+  const std::size_t d = wq.shape().size() == 2 ? wq.shape()[0] : 0;
+  for (int i = 0; i < 3; ++i) {
+    const Tensor& w = *weights[i];
+    if (w.shape().size() != 2 || w.shape()[0] != d || w.shape()[1] != d)
+      throw ShapeError("attention projections must be square d_model x d_model");
+    if (biases[i]->shape().size() != 1 || biases[i]->shape()[0] != d)
+      throw ShapeError("attention bias length must be d_model");
+  }
+  const std::size_t gd = groups && d % groups == 0 ? d / groups : 1, rr = rank ? rank : 1;
+  std::vector<float> u(3 * std::max<std::size_t>(groups, 1) * d * rr),
+      v(3 * std::max<std::size_t>(groups, 1) * rr * gd), b(3 * d);
+  detail::check(fsvd_factorize_attention(wq.data(), bq.data(), wk.data(), bk.data(), wv.data(),
+                                         bv.data(), d, groups, rank, u.data(), v.data(),
+                                         b.data()));
+  AttentionFactorSet set;
+  set.d_model = d;
+  set.groups = groups;
+  set.rank = rank;
+  std::vector<FactorizedLinear>* out[3] = {&set.q, &set.k, &set.v};
+  for (std::size_t m = 0; m < 3; ++m)
+    for (std::size_t g = 0; g < groups; ++g) {
+      const std::size_t i = m * groups + g;
+      FactorizedLinear f{Tensor({d, rank}), Tensor({rank, gd}), Tensor({gd})};
+      std::copy(u.begin() + i * d * rank, u.begin() + (i + 1) * d * rank, f.u.data());
+      std::copy(v.begin() + i * rank * gd, v.begin() + (i + 1) * rank * gd, f.v.data());
+      std::copy(b.begin() + i * gd, b.begin() + (i + 1) * gd, f.bias.data());
+      out[m]->push_back(std::move(f));
+    }
+  return set;
 }
 
 }  // namespace b200

@@ -8,6 +8,7 @@
 //   * the error contract: same exception type for bad inputs.
 // Built by tests/cpp/Makefile against the reference objects in oracle/_ref
 // (test infrastructure); run by tests/test_gpu_dropin.py on the GPU box.
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -17,6 +18,7 @@
 
 #include "flashsvd/attention.hpp"
 #include "flashsvd/encoder.hpp"
+#include "flashsvd/factorize.hpp"
 #include "flashsvd/ffn.hpp"
 #include "flashsvd_b200/flashsvd_b200.hpp"
 #include "support/oracles.hpp"
@@ -230,6 +232,48 @@ int main() {
               },
               shape_like, shape_like);
     }
+  }
+
+  // factorization (svd.cpp / factorize.cpp): device factors vs the reference's
+  // own Jacobi, 1e-5 absolute (test_tensor.cpp:276-287's bar)
+  {
+    auto maxdiff = [](const Tensor& a, const Tensor& b) {
+      double d = 0.0;
+      for (std::size_t i = 0; i < a.numel(); ++i)
+        d = std::max(d, std::abs(double(a.at(i)) - double(b.at(i))));
+      return d;
+    };
+    for (const auto& c : std::vector<std::array<std::size_t, 3>>{
+             {8, 8, 3}, {40, 8, 4}, {8, 40, 4}, {96, 96, 48}, {300, 64, 32}}) {
+      Tensor a = oracle::random_tensor({c[0], c[1]}, 77 + c[0] + c[1], 1.0);
+      LowRankPair ref = factor_rank_r(a, c[2]);
+      LowRankPair got = b200::factor_rank_r(a, c[2]);
+      const double du = maxdiff(got.u, ref.u), dv = maxdiff(got.v, ref.v);
+      report("factor_rank_r " + std::to_string(c[0]) + "x" + std::to_string(c[1]) + " r" +
+                 std::to_string(c[2]),
+             du < 1e-5 && dv < 1e-5, "du=" + std::to_string(du) + " dv=" + std::to_string(dv));
+    }
+    const std::size_t d = 64, G = 4, r = 8;
+    Tensor wq = oracle::random_tensor({d, d}, 11, 0.125), wk = oracle::random_tensor({d, d}, 12, 0.125),
+           wv = oracle::random_tensor({d, d}, 13, 0.125), bq = oracle::random_tensor({d}, 14, 0.02),
+           bk = oracle::random_tensor({d}, 15, 0.02), bv = oracle::random_tensor({d}, 16, 0.02);
+    AttentionFactorSet ref = factorize_attention(wq, bq, wk, bk, wv, bv, G, r);
+    AttentionFactorSet got = b200::factorize_attention(wq, bq, wk, bk, wv, bv, G, r);
+    double worst = 0.0;
+    for (std::size_t g = 0; g < G; ++g)
+      for (const auto* pr : {&ref.q, &ref.k, &ref.v}) {
+        const auto& gg = pr == &ref.q ? got.q : pr == &ref.k ? got.k : got.v;
+        worst = std::max({worst, maxdiff(gg[g].u, (*pr)[g].u), maxdiff(gg[g].v, (*pr)[g].v),
+                          maxdiff(gg[g].bias, (*pr)[g].bias)});
+      }
+    report("factorize_attention 64/G4/r8", worst < 1e-5, "max=" + std::to_string(worst));
+    Tensor w = oracle::random_tensor({48, 80}, 21, 0.1);
+    expect_throw<RankError>("factor_rank_r rank 0 -> RankError",
+                            [&] { (void)b200::factor_rank_r(w, 0); });
+    expect_throw<RankError>("factor_rank_r rank > min -> RankError",
+                            [&] { (void)b200::factor_rank_r(w, 49); });
+    expect_throw<ConfigError>("factorize_attention groups 5 -> ConfigError",
+                              [&] { (void)b200::factorize_attention(wq, bq, wk, bk, wv, bv, 5, 2); });
   }
 
   // error contract (errors.hpp): same exception types as the reference
