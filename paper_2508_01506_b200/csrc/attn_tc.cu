@@ -45,6 +45,7 @@ using namespace ptx;
 
 constexpr int QT = 128;  // query rows per CTA
 constexpr int KT = 128;  // keys per tile
+constexpr float kRescaleSlack = 8.0f;  // log2 headroom before the running max moves
 constexpr int kThreads = 320;
 constexpr int kSoftmax = 256;  // warps 0-7: two per TMEM lane quadrant, 64 keys each
 constexpr int kTma = 8, kMma = 9;
@@ -312,7 +313,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         bars->xmax[t & 1][half][row] = tmax;
         named_bar_sync(1 + quad, 64);
         tmax = fmaxf(tmax, bars->xmax[t & 1][half ^ 1][row]);
-        const float m_new = fmaxf(m_run, tmax);
+        // Lazy rescaling: keep the running max unless the tile's max exceeds
+        // it by more than kRescaleSlack (log2 units), so p <= 2^slack and the
+        // O / l rescale (and its TMEM round trip) is skipped for most tiles.
+        // O / l is the same quotient for any reference max.
+        const float m_new = tmax > m_run + kRescaleSlack ? tmax : m_run;
         const float alpha = ex2(m_run - m_new);
         m_run = m_new;
         uint32_t pk[KH / 2];
