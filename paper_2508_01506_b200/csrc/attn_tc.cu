@@ -102,21 +102,23 @@ struct AttnCfg {
   static constexpr int o_kv = o_q + 2 * up1k(TILE);
   static constexpr int KV_STAGE = 2 * up1k(TILE);
   static constexpr int o_bar = o_kv + STAGES * KV_STAGE;
-  static constexpr int SMEM = 1024 + o_bar + 3584;  // Bars
-  // TMEM columns: S (fp32, 128 keys), O (fp32, RP), P (bf16 pairs, 128 keys)
+  static constexpr int SMEM = 1024 + o_bar + 4608;  // Bars
+  // TMEM columns: S (fp32, 128 keys), O (fp32, RP; two buffers when they fit
+  // so an item's output is written while the next item runs), P (bf16 pairs)
   static constexpr int t_s = 0, t_o = 128, t_p = 192;
+  static constexpr int NOB = RP <= 32 ? 2 : 1;
   static_assert(2 * SMEM <= 228 * 1024, "two CTAs per SM");
 };
 
 struct Bars {
   uint64_t q_full[2], q_empty[2];
   uint64_t kv_full[3], kv_empty[3];
-  uint64_t s_full, s_free, p_full, o_full, o_free;
+  uint64_t s_full, s_free, p_full, o_full, o_free[2];
   uint32_t tmem;
   float xmax[2][2][QT];  // [tile parity][half][row]: per-half row maxima
-  float xsum[2][QT];     // per-half row sums at the end of an item
+  float xsum[2][2][QT];  // [item parity][half][row]: per-half row sums of an item
 };
-static_assert(sizeof(Bars) <= 3584, "Bars outgrew its shared-memory reservation");
+static_assert(sizeof(Bars) <= 4608, "Bars outgrew its shared-memory reservation");
 
 // Persistent: each CTA walks work items (batch, head, 128-query tile) with
 // stride gridDim.x; consecutive items share (batch, head) so K/V stay hot in
@@ -152,7 +154,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_init(&bars->s_free, kSoftmax);
     mbar_init(&bars->p_full, kSoftmax);
     mbar_init(&bars->o_full, 1);
-    mbar_init(&bars->o_free, kSoftmax);
+    mbar_init(&bars->o_free[0], kSoftmax);
+    mbar_init(&bars->o_free[1], kSoftmax);
     fence_barrier_init();
   }
   if (threadIdx.x == 0) ATRACE(0);
@@ -226,15 +229,17 @@ __global__ void __launch_bounds__(kThreads, 2)
           __syncwarp();
         }
         mbar_wait(&bars->p_full, t & 1);
-        if (j == 0 && it > 0) mbar_wait(&bars->o_free, (it - 1) & 1);  // O of the previous item read
+        // this item's O buffer must have been read out by the softmax warps
+        if (j == 0 && it >= C::NOB) mbar_wait(&bars->o_free[it % C::NOB], ((it / C::NOB) - 1) & 1);
         tc_fence_after();
         const uint32_t st = t % C::STAGES;
         const uint64_t dv = dv0 + ((st * C::KV_STAGE) >> 4);
+        const uint32_t t_o = tmem + C::t_o + (it % C::NOB) * RP;
         if (elect_one()) {
           // O += P V: P (A operand) straight from TMEM, 8 columns per K = 16 step
 #pragma unroll
           for (int k = 0; k < KT / 16; ++k)
-            mma_bf16_ts(tmem + C::t_o, tmem + C::t_p + k * 8, dv + ((k * 16 * C::RB) >> 4),
+            mma_bf16_ts(t_o, tmem + C::t_p + k * 8, dv + ((k * 16 * C::RB) >> 4),
                         idesc_bf16(128, RP, 0, 1), (j | k) != 0);
           mma_commit(&bars->o_full);
           mma_commit(&bars->kv_empty[st]);
@@ -257,25 +262,57 @@ __global__ void __launch_bounds__(kThreads, 2)
     const bool owns_o = RP >= 32 || half == 0;
     const int oc0 = RP >= 32 ? static_cast<int>(half) * CH : 0;
 
-    auto rescale_o = [&](float alpha) {
+    auto rescale_o = [&](uint32_t t_o, float alpha) {
 #pragma unroll
       for (int c = 0; c < CH; c += 16) {
         uint32_t r[16];
-        tmem_ld16(tq + C::t_o + oc0 + c, r);
+        tmem_ld16(tq + t_o + oc0 + c, r);
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-        tmem_st16(tq + C::t_o + oc0 + c, r);
+        tmem_st16(tq + t_o + oc0 + c, r);
       }
       tmem_st_wait();
+    };
+    // O / l of a finished item -> out (rank space); releases its O buffer.
+    // The partner half's l is in xsum[item parity], written before a named
+    // barrier both halves have passed since.
+    auto epilogue = [&](int it_e, int row0_e, int q0_e, int h_e, float l_e) {
+      const int ob = it_e % C::NOB;
+      const float inv = 1.0f / (l_e + bars->xsum[it_e & 1][half ^ 1][row]);
+      const int qrow = q0_e + static_cast<int>(row);
+#pragma unroll
+      for (int c = 0; c < CH; c += 16) {
+        if (!owns_o) break;
+        uint32_t r[16];
+        tmem_ld16(tq + C::t_o + ob * RP + oc0 + c, r);
+        tmem_ld_wait();
+        if (qrow < seq) {
+          uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)(row0_e + qrow) * ldo + h_e * RP +
+                                                oc0 + c);
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+            dst[v] = make_uint4(
+                pack_bf16(__uint_as_float(r[8 * v + 0]) * inv, __uint_as_float(r[8 * v + 1]) * inv),
+                pack_bf16(__uint_as_float(r[8 * v + 2]) * inv, __uint_as_float(r[8 * v + 3]) * inv),
+                pack_bf16(__uint_as_float(r[8 * v + 4]) * inv, __uint_as_float(r[8 * v + 5]) * inv),
+                pack_bf16(__uint_as_float(r[8 * v + 6]) * inv, __uint_as_float(r[8 * v + 7]) * inv));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bars->o_free[ob]);
     };
 
     int gt = 0;
     int it = 0;
+    // the previous item, whose output is written during this item's first tile
+    int pv_row0 = 0, pv_q0 = 0, pv_h = 0;
+    float pv_l = 0.0f;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
       const int qt = w % nqt, h = (w / nqt) % heads, b = w / (nqt * heads);
       const int row0 = b * seq, q0 = qt * QT;
       const int nji = causal ? min(nj, qt + 1) : nj;
+      const uint32_t t_o = C::t_o + (it % C::NOB) * RP;
       float m_run = -INFINITY, l_run = 0.0f;
       for (int j = 0; j < nji; ++j) {
         const int t = gt + j;
@@ -333,49 +370,40 @@ __global__ void __launch_bounds__(kThreads, 2)
           pk[c] = pack_bf16(p.x, p.y);
         }
         l_run = fmaf(l_run, alpha, sum2.x + sum2.y);
-        // single-buffered probability tile and O accumulator: PV of the
-        // previous tile of this item must be done
-        if (j >= 1) {
+        // single-buffered probability tile: the previous PV (this item's, or
+        // the previous item's last one) must be done before P is rewritten
+        const bool prev_pv = j >= 1 || (C::NOB == 2 && it > 0);
+        if (prev_pv) {
           mbar_wait(&bars->o_full, (t - 1) & 1);
           tc_fence_after();
-          if (owns_o && __any_sync(0xffffffffu, alpha != 1.0f)) rescale_o(alpha);
+          if (j >= 1 && owns_o && __any_sync(0xffffffffu, alpha != 1.0f)) rescale_o(t_o, alpha);
         }
         // this half's 64 keys -> TMEM columns [t_p + 32*half, +32) of this row
         tmem_st32(tq + C::t_p + half * 32, pk);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars->p_full);
+        if (C::NOB == 2 && j == 0 && it > 0) epilogue(it - 1, pv_row0, pv_q0, pv_h, pv_l);
       }
       gt += nji;
-      bars->xsum[half][row] = l_run;
+      bars->xsum[it & 1][half][row] = l_run;
+      if (C::NOB == 1) {
+        mbar_wait(&bars->o_full, (gt - 1) & 1);
+        tc_fence_after();
+        named_bar_sync(1 + quad, 64);
+        epilogue(it, row0, q0, h, l_run);
+      }
+      pv_row0 = row0;
+      pv_q0 = q0;
+      pv_h = h;
+      pv_l = l_run;
+      if (threadIdx.x == 0 && it == 0) ATRACE(2);
+    }
+    if (C::NOB == 2 && it > 0) {  // the last item's output
       mbar_wait(&bars->o_full, (gt - 1) & 1);
       tc_fence_after();
       named_bar_sync(1 + quad, 64);
-      const float inv = 1.0f / (l_run + bars->xsum[half ^ 1][row]);
-      const int qrow = q0 + static_cast<int>(row);
-#pragma unroll
-      for (int c = 0; c < CH; c += 16) {
-        if (!owns_o) break;
-        uint32_t r[16];
-        tmem_ld16(tq + C::t_o + oc0 + c, r);
-        tmem_ld_wait();
-        if (qrow < seq) {
-          uint4* dst =
-              reinterpret_cast<uint4*>(out + (int64_t)(row0 + qrow) * ldo + h * RP + oc0 + c);
-#pragma unroll
-          for (int v = 0; v < 2; ++v)
-            dst[v] = make_uint4(
-                pack_bf16(__uint_as_float(r[8 * v + 0]) * inv, __uint_as_float(r[8 * v + 1]) * inv),
-                pack_bf16(__uint_as_float(r[8 * v + 2]) * inv, __uint_as_float(r[8 * v + 3]) * inv),
-                pack_bf16(__uint_as_float(r[8 * v + 4]) * inv, __uint_as_float(r[8 * v + 5]) * inv),
-                pack_bf16(__uint_as_float(r[8 * v + 6]) * inv, __uint_as_float(r[8 * v + 7]) * inv));
-        }
-      }
-      // O read: the next item's first PV may overwrite it; the xsum slots
-      // are rewritten only after the next item's tile barriers
-      tc_fence_before();
-      mbar_arrive(&bars->o_free);
-      if (threadIdx.x == 0 && it == 0) ATRACE(2);
+      epilogue(it - 1, pv_row0, pv_q0, pv_h, pv_l);
     }
   }
   if (threadIdx.x == 0) ATRACE(3);
