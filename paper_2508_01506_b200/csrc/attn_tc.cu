@@ -163,6 +163,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();
+  pdl_wait();
   const uint32_t tmem = bars->tmem;
   const uint32_t s_q = smem_u32(smem + C::o_q), s_kv = smem_u32(smem + C::o_kv);
 
@@ -429,9 +431,8 @@ void launch_attn(const AttnTcArgs& a, cudaStream_t s) {
       tmap_bf16(a.qkv, T, a.qkv_cols, a.ldq, 128, RP, swizzle_for_row_bytes(C::RB));
   const int items = ((a.seq + QT - 1) / QT) * a.heads * a.batch;
   const int grid = items < 2 * num_sms() ? items : 2 * num_sms();
-  k_attn_rankspace<RP><<<grid, kThreads, C::SMEM, s>>>(tm, a.out, a.ldo, a.batch, a.seq, a.heads,
-                                                       a.groups, a.q_off, a.k_off, a.v_off,
-                                                       a.causal ? 1 : 0);
+  launch_pdl(k_attn_rankspace<RP>, dim3(grid), dim3(kThreads), C::SMEM, s, tm, a.out, a.ldo,
+             a.batch, a.seq, a.heads, a.groups, a.q_off, a.k_off, a.v_off, a.causal ? 1 : 0);
   check_launch("k_attn_rankspace");
 }
 

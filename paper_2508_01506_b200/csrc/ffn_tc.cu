@@ -172,6 +172,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();
+  pdl_wait();
   const uint32_t tmem = bars->tmem;
   uint8_t* ring = smem + C::o_ring;
 
@@ -488,9 +490,9 @@ void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
   else
     tp = tmap_bf16(a.p_in, a.T, FR, FR, 128, 64, TmaSwizzle::B128);
   const int grid = (a.T + BMr - 1) / BMr;
-  k_ffn<FR, FUSED><<<grid, kThreads, C::SMEM, s>>>(tx, tp, tup, tvup, tudn, tvdn, ty, a.up_b, a.dn_b,
-                                                   a.act, a.T, a.d_model, a.d_ff, a.z_out, a.out,
-                                                   a.ln_g, a.ln_b, a.ln_eps);
+  launch_pdl(k_ffn<FR, FUSED>, dim3(grid), dim3(kThreads), C::SMEM, s, tx, tp, tup, tvup, tudn,
+             tvdn, ty, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff, a.z_out, a.out, a.ln_g,
+             a.ln_b, a.ln_eps);
   check_launch(FUSED ? "k_ffn_fused" : "k_ffn_stream");
 }
 

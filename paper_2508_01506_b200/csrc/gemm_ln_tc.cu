@@ -115,6 +115,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (threadIdx.x == 0) LTRACE(3);
   tc_fence_after();
+  pdl_trigger();
+  pdl_wait();
   const uint32_t tmem = bars->tmem;
 
   if (warp == 0 || warp == 11) {
@@ -247,8 +249,8 @@ void gemm_ln_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, const 
   const CUtensorMap tr = tmap_bf16(resid, T, N, N, BMr, 64, TmaSwizzle::B128);
   const CUtensorMap ty = tmap_bf16(y, T, N, N, BMr, 64, TmaSwizzle::B128);
   const int grid = (T + BMr - 1) / BMr;
-    k_gemm_ln<<<grid, kThreads, smem, s>>>(ta, tb, tr, ty, bias, gamma, beta, eps, y, T, N, K,
-                                         stages);
+  launch_pdl(k_gemm_ln, dim3(grid), dim3(kThreads), smem, s, ta, tb, tr, ty, bias, gamma, beta,
+             eps, y, T, N, K, stages);
   check_launch("k_gemm_ln");
 }
 

@@ -102,6 +102,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();
+  pdl_wait();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0 || warp == kThreads / 32 - 1) {
@@ -443,7 +445,8 @@ void launch_gemm(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C
   const CUtensorMap tc = tmap_bf16(C, M, N, ldc, BM, 64, TmaSwizzle::B128);
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  k_gemm_bf16<BN, STAGES><<<grid, kThreads, Cfg::SMEM, s>>>(ta, tb, tc, bias, act, M, N, K);
+  launch_pdl(k_gemm_bf16<BN, STAGES>, dim3(grid), dim3(kThreads), Cfg::SMEM, s, ta, tb, tc, bias,
+             act, M, N, K);
   check_launch("k_gemm_bf16");
 }
 

@@ -57,6 +57,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: a kernel launched with launch_pdl() may start
+// while its predecessor on the stream drains.  pdl_trigger() lets the next
+// kernel be scheduled; pdl_wait() blocks until the predecessor grid has
+// completed and its memory is visible -- every kernel calls it after its
+// prologue (barriers, TMEM, descriptor prefetch) and before any global access.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------- fences
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
