@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int g = h / hpg, row0 = b * seq;
         const int qs = it & 1;
         mbar_wait(&bars->q_empty[qs], ((it >> 1) & 1) ^ 1);
+        if (it < 100) ATRACE(500 + it);
         mbar_arrive_expect_tx(&bars->q_full[qs], C::TILE);
         tma_load_2d(&tmQKV, &bars->q_full[qs], smem + C::o_q + qs * up1k(C::TILE),
                     q_off + h * RP, row0 + qt * QT);
@@ -216,12 +217,18 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       __syncwarp();
     };
+    // S of an item's first tile is issued while the previous item's last
+    // tile is still in the softmax (right after its S was read out), so the
+    // softmax warps find it ready when they move on.
+    if (static_cast<int>(blockIdx.x) < items) {
+      mbar_wait(&bars->q_full[0], 0);
+      if (lane == 0) ATRACE(1);
+      issue_s(0, 0);
+    }
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
       const int qs = it & 1;
       const int nji = causal ? min(nj, w % nqt + 1) : nj;
-      mbar_wait(&bars->q_full[qs], (it >> 1) & 1);
-      if (lane == 0 && it == 0) ATRACE(1);
-      issue_s(gt, qs);
+      if (lane == 0 && it < 100) ATRACE(400 + it);
       for (int j = 0; j < nji; ++j) {
         const int t = gt + j;
         if (j + 1 < nji) {
@@ -229,6 +236,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         } else {
           if (elect_one()) mma_commit(&bars->q_empty[qs]);  // after this item's last S
           __syncwarp();
+          if (w + static_cast<int>(gridDim.x) < items) {
+            mbar_wait(&bars->q_full[qs ^ 1], ((it + 1) >> 1) & 1);
+            issue_s(t + 1, qs ^ 1);
+          }
         }
         mbar_wait(&bars->p_full, t & 1);
         // this item's O buffer must have been read out by the softmax warps
@@ -315,6 +326,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int row0 = b * seq, q0 = qt * QT;
       const int nji = causal ? min(nj, qt + 1) : nj;
       const uint32_t t_o = C::t_o + (it % C::NOB) * RP;
+      if (threadIdx.x == 0 && it < 100) ATRACE(300 + it);
       float m_run = -INFINITY, l_run = 0.0f;
       for (int j = 0; j < nji; ++j) {
         const int t = gt + j;
@@ -386,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         tc_fence_before();
         mbar_arrive(&bars->p_full);
         if (C::NOB == 2 && j == 0 && it > 0) epilogue(it - 1, pv_row0, pv_q0, pv_h, pv_l);
+        if (threadIdx.x == 0 && it < 100) ATRACE(600 + it * 4 + min(j, 3));
       }
       gt += nji;
       bars->xsum[it & 1][half][row] = l_run;

@@ -30,3 +30,7 @@ print(" j | mma: kv_full  s_free  p_full | softmax: wait_s  got_s  wait_o  got_o
 for j in range((M + 127) // 128):
     print(f"{j:2d} | {r(16 + j):7d} {r(48 + j):7d} {r(80 + j):7d} | {r(112 + j):7d} {r(144 + j):7d} "
           f"{r(176 + j):7d} {r(208 + j):7d} {r(240 + j):7d}")
+print("item | tma_q  mma_start  softmax_start  tile_p_arrive[0..3]")
+for it in range(12):
+    print(f"{it:3d} | {r(500 + it):7d} {r(400 + it):7d} {r(300 + it):7d} | " +
+          " ".join(f"{r(600 + it * 4 + j):7d}" for j in range(4)))
