@@ -22,6 +22,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace fsvd {
 namespace {
@@ -36,6 +37,8 @@ __device__ __forceinline__ float bf2f(uint16_t v) { return __uint_as_float(uint3
 __global__ void k_kv_store(const bf16* __restrict__ src, int64_t lds, int c0, int width,
                            int batch, int rows_per_b, bf16* __restrict__ cache, int max_seq,
                            int pos0) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int vec = width / 8;  // uint4 per row
   const int64_t total = (int64_t)batch * rows_per_b * vec;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -64,6 +67,8 @@ __global__ void __launch_bounds__(kDecThreads)
   __shared__ float wred[kDecThreads / 32];
   __shared__ float ored[kDecThreads / 32][RP];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   if (tid < RP)
     q[tid] = bf2f(reinterpret_cast<const uint16_t*>(qkv)[(int64_t)b * ldq + q_off + h * RP + tid]);
   __syncthreads();
@@ -150,6 +155,8 @@ template <int RP>
 __global__ void k_attn_combine(const float* __restrict__ part, int heads, int splits,
                                bf16* __restrict__ out, int64_t ldo) {
   const int bh = blockIdx.x, b = bh / heads, h = bh % heads, c = threadIdx.x;
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   if (c >= RP) return;
   const float* pp = part + (int64_t)bh * splits * (RP + 2);
   float m = -INFINITY;
@@ -167,12 +174,12 @@ __global__ void k_attn_combine(const float* __restrict__ part, int heads, int sp
 template <int RP>
 void launch_decode(const DecodeArgs& a, cudaStream_t s) {
   const int bh = a.batch * a.heads;
-  k_attn_decode<RP><<<dim3(bh, a.splits), kDecThreads, 0, s>>>(
-      a.qkv, a.ldq, a.q_off, a.cache, a.max_seq, a.heads, a.groups, a.len, a.splits, a.part,
-      a.out, a.ldo);
+  launch_pdl(k_attn_decode<RP>, dim3(bh, a.splits), dim3(kDecThreads), 0, s, a.qkv, a.ldq,
+             a.q_off, a.cache, a.max_seq, a.heads, a.groups, a.len, a.splits, a.part, a.out, a.ldo);
   check_launch("k_attn_decode");
   if (a.splits > 1) {
-    k_attn_combine<RP><<<bh, 64, 0, s>>>(a.part, a.heads, a.splits, a.out, a.ldo);
+    launch_pdl(k_attn_combine<RP>, dim3(bh), dim3(64), 0, s, static_cast<const float*>(a.part),
+               a.heads, a.splits, a.out, a.ldo);
     check_launch("k_attn_combine");
   }
 }
@@ -196,7 +203,8 @@ void kv_store_bf16(const bf16* src, int64_t lds, int c0, int width, int batch, i
                    bf16* cache, int max_seq, int pos0, cudaStream_t s) {
   const int64_t total = (int64_t)batch * rows_per_b * (width / 8);
   const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 4 * num_sms()));
-  k_kv_store<<<grid, 256, 0, s>>>(src, lds, c0, width, batch, rows_per_b, cache, max_seq, pos0);
+  launch_pdl(k_kv_store, dim3(grid), dim3(256), 0, s, src, lds, c0, width, batch, rows_per_b,
+             cache, max_seq, pos0);
   check_launch("k_kv_store");
 }
 

@@ -471,6 +471,14 @@ void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, 
     launch_gemm2<256, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
     return;
   }
+  if (variant == 5 && N % 128 == 0) {  // single-CTA 128-wide tiles (wave-quantization probe)
+    launch_gemm<128, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+    return;
+  }
+  if (variant == 6 && N % 64 == 0) {
+    launch_gemm<64, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+    return;
+  }
   if (variant == 4 && N % 128 == 0) {
     launch_gemm2<128, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
     return;

@@ -338,6 +338,8 @@ __global__ void __launch_bounds__(256) k_resid_ln_bf16x8(const bf16* __restrict_
                                                        const float* __restrict__ gamma,
                                                        const float* __restrict__ beta, float eps,
                                                        bf16* __restrict__ y, int rows, int d) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -411,6 +413,8 @@ __global__ void __launch_bounds__(256) k_resid_ln_bf16x8(const bf16* __restrict_
 template <typename T>
 __global__ void k_add(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ y,
                       int64_t n) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[i] = cvt<T>(ld(a + i) + ld(b + i));
@@ -443,9 +447,11 @@ void launch_ln(const T* a, const T* b, const float* gamma, const float* beta, fl
   if constexpr (sizeof(T) == 2) {
     if (d % 8 == 0 && d <= 32 * 8 * 4) {
       if (d <= 32 * 8 * 2)
-        k_resid_ln_bf16x8<2><<<grid, threads, 0, s>>>(a, b, gamma, beta, eps, y, rows, d);
+        launch_pdl(k_resid_ln_bf16x8<2>, dim3(grid), dim3(threads), 0, s, a, b, gamma, beta, eps, y,
+                   rows, d);
       else
-        k_resid_ln_bf16x8<4><<<grid, threads, 0, s>>>(a, b, gamma, beta, eps, y, rows, d);
+        launch_pdl(k_resid_ln_bf16x8<4>, dim3(grid), dim3(threads), 0, s, a, b, gamma, beta, eps, y,
+                   rows, d);
       check_launch("k_resid_ln_bf16x8");
       return;
     }
@@ -530,11 +536,11 @@ void resid_layernorm_f32(const float* a, const float* b, const float* gamma, con
   launch_ln<float>(a, b, gamma, beta, eps, y, rows, d, s);
 }
 void add_bf16(const bf16* a, const bf16* b, bf16* y, int64_t n, cudaStream_t s) {
-  k_add<bf16><<<elementwise_grid(n), 256, 0, s>>>(a, b, y, n);
+  launch_pdl(k_add<bf16>, dim3(elementwise_grid(n)), dim3(256), 0, s, a, b, y, n);
   check_launch("k_add");
 }
 void add_f32(const float* a, const float* b, float* y, int64_t n, cudaStream_t s) {
-  k_add<float><<<elementwise_grid(n), 256, 0, s>>>(a, b, y, n);
+  launch_pdl(k_add<float>, dim3(elementwise_grid(n)), dim3(256), 0, s, a, b, y, n);
   check_launch("k_add");
 }
 template <typename T>
