@@ -115,7 +115,14 @@ def load_ncu_traffic(prefix):
     """DRAM bytes (read + write) per launch of the kernel whose name starts with
     `prefix`, from the newest committed `ncu --set full` summary in profiles/."""
     import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")), reverse=True):
+    import re
+
+    def order(path):  # (round, version): r01_ncu_summary.json < r01_ncu_summary_v4.json
+        m = re.search(r"r(\d+)_ncu_summary(?:_v(\d+))?\.json$", path)
+        return (int(m.group(1)), int(m.group(2) or 0)) if m else (-1, -1)
+
+    paths = glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary*.json"))
+    for path in sorted(paths, key=order, reverse=True):
         try:
             with open(path) as f:
                 s = json.load(f)
