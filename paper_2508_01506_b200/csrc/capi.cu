@@ -53,6 +53,11 @@ fsvd_status guard(F&& f) {
   }
 }
 
+// tensor.cpp: every extent of a reference tensor is >= 1 (ShapeError otherwise)
+void check_extents(size_t batch, size_t seq) {
+  if (batch == 0 || seq == 0) fail(Kind::Shape, "tensor extent must be at least 1");
+}
+
 void require_device() {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -627,6 +632,7 @@ fsvd_status fsvd_workspace_bytes_ln(const fsvd_layer_pack* const* packs, size_t 
 fsvd_status fsvd_attention_fwd(const fsvd_layer_pack* p, size_t batch, size_t seq, const void* x,
                                void* ctx, void* ws, size_t ws_bytes, void* stream) {
   return guard([&] {
+    check_extents(batch, seq);
     const size_t need = batch * seq * op_transient_elems(*p->p, 0, FSVD_MODE_FLASH_V1) * p->p->es;
     if (ws_bytes < need) fail(Kind::Config, "workspace too small for attention");
     attention_fwd(*p->p, FSVD_MODE_FLASH_V1, batch, seq, x, ctx, ws, static_cast<cudaStream_t>(stream));
@@ -635,6 +641,7 @@ fsvd_status fsvd_attention_fwd(const fsvd_layer_pack* p, size_t batch, size_t se
 fsvd_status fsvd_outproj_fwd(const fsvd_layer_pack* p, size_t batch, size_t seq, const void* ctx,
                              void* out, void* ws, size_t ws_bytes, void* stream) {
   return guard([&] {
+    check_extents(batch, seq);
     const size_t need = batch * seq * op_transient_elems(*p->p, 1, FSVD_MODE_FLASH_V1) * p->p->es;
     if (ws_bytes < need) fail(Kind::Config, "workspace too small for the output projection");
     outproj_fwd(*p->p, FSVD_MODE_FLASH_V1, batch, seq, ctx, out, ws, static_cast<cudaStream_t>(stream));
@@ -643,6 +650,7 @@ fsvd_status fsvd_outproj_fwd(const fsvd_layer_pack* p, size_t batch, size_t seq,
 fsvd_status fsvd_ffn_fwd(const fsvd_layer_pack* p, int variant, size_t batch, size_t seq,
                          const void* x, void* out, void* ws, size_t ws_bytes, void* stream) {
   return guard([&] {
+    check_extents(batch, seq);
     if (variant != 1 && variant != 2) fail(Kind::Config, "ffn variant must be 1 or 2");
     const int mode = variant == 1 ? FSVD_MODE_FLASH_V1 : FSVD_MODE_FLASH_V2;
     const size_t need = batch * seq * op_transient_elems(*p->p, 2, mode) * p->p->es;
@@ -654,6 +662,7 @@ fsvd_status fsvd_layer_fwd(const fsvd_layer_pack* p, fsvd_run_mode mode, int pre
                            size_t seq, const void* x, void* out, void* ws, size_t ws_bytes,
                            void* stream) {
   return guard([&] {
+    check_extents(batch, seq);
     check_mode(mode);
     layer_fwd(*p->p, mode, pre_ln != 0, batch, seq, x, out, ws, ws_bytes,
               static_cast<cudaStream_t>(stream));
@@ -663,6 +672,7 @@ fsvd_status fsvd_model_fwd(const fsvd_layer_pack* const* packs, size_t n_layers,
                            fsvd_run_mode mode, int pre_ln, size_t batch, size_t seq,
                            const void* x, void* out, void* ws, size_t ws_bytes, void* stream) {
   return guard([&] {
+    check_extents(batch, seq);
     check_mode(mode);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (n_layers == 0) {
@@ -929,6 +939,7 @@ fsvd_status fsvd_decoder_prefill(const fsvd_layer_pack* const* packs, size_t n_l
                                  void* const* kv_caches, size_t max_seq, void* ws,
                                  size_t ws_bytes, void* stream) {
   return guard([&] {
+    check_extents(batch, seq);
     check_decoder_call(packs, n_layers, kv_caches, batch, max_seq);
     if (seq == 0 || seq > max_seq) fail(Kind::Config, "prefill length must lie in [1, max_seq]");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -948,6 +959,7 @@ fsvd_status fsvd_decoder_step(const fsvd_layer_pack* const* packs, size_t n_laye
                               void* const* kv_caches, size_t max_seq, void* ws, size_t ws_bytes,
                               void* stream) {
   return guard([&] {
+    check_extents(batch, 1);
     check_decoder_call(packs, n_layers, kv_caches, batch, max_seq);
     if (pos >= max_seq) fail(Kind::Config, "decode position must be below max_seq");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -982,6 +994,7 @@ fsvd_status fsvd_model_fwd_stream(const fsvd_layer_pack* const* packs, size_t n_
                                   void* const* out_host, void* ws, size_t ws_bytes,
                                   void* stream) {
   return guard([&] {
+    check_extents(batch, seq);
     check_mode(mode);
     if (!packs || n_layers == 0 || (n_batches && (!x_host || !out_host)))
       fail(Kind::Config, "null argument");

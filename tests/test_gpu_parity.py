@@ -419,3 +419,33 @@ def test_stream_serving_loop_matches_device_api(L):
         assert torch.equal(od.cpu(), outs[i]), i
     for p in packs:
         L.fsvd_layer_pack_destroy(p)
+
+
+# ------------------------------------------------------------------ empty inputs
+@pytest.mark.parametrize("shape", [(0, 16, 64), (2, 0, 64)], ids=["batch0", "seq0"])
+def test_empty_inputs_rejected_like_reference(L, ora, reference, shape):
+    """The reference cannot even build a zero-extent tensor (tensor.cpp:
+    ShapeError "tensor extent must be at least 1"); every entry point here
+    raises the same error kind, host and device API alike."""
+    import torch
+    layer = oracle.rand_layer(ora, 64, 128, 4, 2, 8, 21, 16, 16)
+    x = np.zeros(shape, np.float32)
+    with pytest.raises(abi.FsvdError) as r:
+        reference.run_model(x, [layer], abi.MODE_FLASH_V2, PLAN)
+    assert r.value.status == abi.ERR_SHAPE
+    for mode in (abi.MODE_FLASH_V1, abi.MODE_FLASH_V2):
+        with pytest.raises(abi.FsvdError) as e:
+            H.run_model(x, [layer], mode, PLAN, abi.BF16)
+        assert e.value.status == abi.ERR_SHAPE
+    descs = layer_descs([layer])
+    p = C.c_void_p()
+    abi.check(L.fsvd_layer_pack_create(C.byref(descs[0]), abi.BF16, 0, C.byref(p)))
+    parr = (C.c_void_p * 1)(p.value)
+    buf = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    st = L.fsvd_model_fwd(parr, 1, abi.MODE_FLASH_V2, 0, shape[0], shape[1],
+                          C.c_void_p(buf.data_ptr()), C.c_void_p(buf.data_ptr()),
+                          C.c_void_p(buf.data_ptr()), buf.numel(),
+                          C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert st == abi.ERR_SHAPE and b"at least 1" in L.fsvd_last_error()
+    torch.cuda.synchronize()
+    L.fsvd_layer_pack_destroy(p)
