@@ -320,6 +320,17 @@ fsvd_status fsvd_decoder_step(const fsvd_layer_pack* const* packs, size_t n_laye
                               size_t batch, size_t pos, const void* x, void* out,
                               void* const* kv_caches, size_t max_seq, void* ws, size_t ws_bytes,
                               void* stream);
+/* The decode step of fixed buffers (x, out [batch, d], caches, workspace)
+ * captured once into a CUDA graph; each replay takes the position as an
+ * argument (read on the device), so a serving loop pays one graph launch per
+ * token instead of ~11 kernel launches per layer. */
+typedef struct fsvd_decoder_graph fsvd_decoder_graph;
+fsvd_status fsvd_decoder_graph_create(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                      int pre_ln, size_t batch, const void* x, void* out,
+                                      void* const* kv_caches, size_t max_seq, void* ws,
+                                      size_t ws_bytes, fsvd_decoder_graph** graph);
+fsvd_status fsvd_decoder_graph_step(fsvd_decoder_graph* graph, size_t pos, void* stream);
+void fsvd_decoder_graph_destroy(fsvd_decoder_graph* graph);
 
 /* ------------------------------------------------------------------ */
 /* Device-resident async API (device pointers, cudaStream_t as void*)   */

@@ -159,6 +159,10 @@ def _declare(lib):
                                       vp]),
         "fsvd_decoder_step": (st, [P(vp), _sz, C.c_int, _sz, _sz, vp, vp, P(vp), _sz, vp, _sz,
                                    vp]),
+        "fsvd_decoder_graph_create": (st, [P(vp), _sz, C.c_int, _sz, vp, vp, P(vp), _sz, vp, _sz,
+                                           P(vp)]),
+        "fsvd_decoder_graph_step": (st, [vp, _sz, vp]),
+        "fsvd_decoder_graph_destroy": (None, [vp]),
         "fsvd_stream_workspace_bytes": (st, [P(vp), _sz, _sz, _sz, C.c_int, P(_sz)]),
         "fsvd_model_fwd_stream": (st, [P(vp), _sz, C.c_int, C.c_int, _sz, _sz, _sz, P(vp), P(vp),
                                        vp, _sz, vp]),

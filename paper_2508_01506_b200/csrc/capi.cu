@@ -26,6 +26,15 @@
 struct fsvd_meter {
   fsvd::Meter m;
 };
+struct fsvd_decoder_graph {
+  cudaGraphExec_t exec = nullptr;
+  int* pos_dev = nullptr;
+  size_t max_seq = 0;
+  ~fsvd_decoder_graph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (pos_dev) cudaFree(pos_dev);
+  }
+};
 
 namespace fsvd {
 namespace {
@@ -954,6 +963,57 @@ fsvd_status fsvd_decoder_prefill(const fsvd_layer_pack* const* packs, size_t n_l
     }
   });
 }
+fsvd_status fsvd_decoder_graph_create(const fsvd_layer_pack* const* packs, size_t n_layers,
+                                      int pre_ln, size_t batch, const void* x, void* out,
+                                      void* const* kv_caches, size_t max_seq, void* ws,
+                                      size_t ws_bytes, fsvd_decoder_graph** graph) {
+  return guard([&] {
+    check_extents(batch, 1);
+    check_decoder_call(packs, n_layers, kv_caches, batch, max_seq);
+    if (!graph || !x || !out || !ws) fail(Kind::Config, "null argument");
+    require_device();
+    auto g = std::make_unique<fsvd_decoder_graph>();
+    g->max_seq = max_seq;
+    FSVD_CUDA_CHECK(cudaMalloc(&g->pos_dev, sizeof(int)));
+    FSVD_CUDA_CHECK(cudaMemset(g->pos_dev, 0, sizeof(int)));
+    cudaStream_t cs = nullptr;
+    FSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t gr = nullptr;
+    FSVD_CUDA_CHECK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    try {
+      for (size_t i = 0; i < n_layers; ++i) {
+        AttnMode am;
+        am.kind = AttnMode::Decode;
+        am.cache = kv_caches[i];
+        am.max_seq = max_seq;
+        am.pos_dev = g->pos_dev;
+        layer_fwd(*packs[i]->p, FSVD_MODE_FLASH_V2, pre_ln != 0, batch, 1, i == 0 ? x : out, out,
+                  ws, ws_bytes, cs, am);
+      }
+    } catch (...) {
+      cudaStreamEndCapture(cs, &gr);
+      if (gr) cudaGraphDestroy(gr);
+      cudaStreamDestroy(cs);
+      throw;
+    }
+    FSVD_CUDA_CHECK(cudaStreamEndCapture(cs, &gr));
+    const cudaError_t ie = cudaGraphInstantiate(&g->exec, gr, 0);
+    cudaGraphDestroy(gr);
+    cudaStreamDestroy(cs);
+    FSVD_CUDA_CHECK(ie);
+    *graph = g.release();
+  });
+}
+fsvd_status fsvd_decoder_graph_step(fsvd_decoder_graph* graph, size_t pos, void* stream) {
+  return guard([&] {
+    if (!graph) fail(Kind::Config, "null argument");
+    if (pos >= graph->max_seq) fail(Kind::Config, "decode position must be below max_seq");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    set_device_int(graph->pos_dev, static_cast<int>(pos), s);
+    FSVD_CUDA_CHECK(cudaGraphLaunch(graph->exec, s));
+  });
+}
+void fsvd_decoder_graph_destroy(fsvd_decoder_graph* graph) { delete graph; }
 fsvd_status fsvd_decoder_step(const fsvd_layer_pack* const* packs, size_t n_layers, int pre_ln,
                               size_t batch, size_t pos, const void* x, void* out,
                               void* const* kv_caches, size_t max_seq, void* ws, size_t ws_bytes,

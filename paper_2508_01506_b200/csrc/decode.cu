@@ -36,9 +36,10 @@ __device__ __forceinline__ float bf2f(uint16_t v) { return __uint_as_float(uint3
 // width)) -> cache rows b * max_seq + pos0 + m for src row b * rows_per_b + m
 __global__ void k_kv_store(const bf16* __restrict__ src, int64_t lds, int c0, int width,
                            int batch, int rows_per_b, bf16* __restrict__ cache, int max_seq,
-                           int pos0) {
+                           int pos0, const int* __restrict__ pos_dev) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
+  if (pos_dev) pos0 = *pos_dev;  // graph replay: the position lives on the device
   const int vec = width / 8;  // uint4 per row
   const int64_t total = (int64_t)batch * rows_per_b * vec;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -55,8 +56,11 @@ template <int RP>
 __global__ void __launch_bounds__(kDecThreads)
     k_attn_decode(const bf16* __restrict__ qkv, int64_t ldq, int q_off, const bf16* __restrict__ cache,
                   int max_seq, int heads, int groups, int len, int splits, float* __restrict__ part,
-                  bf16* __restrict__ out, int64_t ldo) {
+                  bf16* __restrict__ out, int64_t ldo, const int* __restrict__ pos_dev) {
   const int bh = blockIdx.x, b = bh / heads, h = bh % heads, g = h / (heads / groups);
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  if (pos_dev) len = *pos_dev + 1;
   const int chunk = (len + splits - 1) / splits;
   const int k0 = blockIdx.y * chunk, k1 = min(len, k0 + chunk);
   const int width = 2 * groups * RP;
@@ -67,8 +71,6 @@ __global__ void __launch_bounds__(kDecThreads)
   __shared__ float wred[kDecThreads / 32];
   __shared__ float ored[kDecThreads / 32][RP];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  ptx::pdl_trigger();
-  ptx::pdl_wait();
   if (tid < RP)
     q[tid] = bf2f(reinterpret_cast<const uint16_t*>(qkv)[(int64_t)b * ldq + q_off + h * RP + tid]);
   __syncthreads();
@@ -175,7 +177,8 @@ template <int RP>
 void launch_decode(const DecodeArgs& a, cudaStream_t s) {
   const int bh = a.batch * a.heads;
   launch_pdl(k_attn_decode<RP>, dim3(bh, a.splits), dim3(kDecThreads), 0, s, a.qkv, a.ldq,
-             a.q_off, a.cache, a.max_seq, a.heads, a.groups, a.len, a.splits, a.part, a.out, a.ldo);
+             a.q_off, a.cache, a.max_seq, a.heads, a.groups, a.len, a.splits, a.part, a.out, a.ldo,
+             a.pos_dev);
   check_launch("k_attn_decode");
   if (a.splits > 1) {
     launch_pdl(k_attn_combine<RP>, dim3(bh), dim3(64), 0, s, static_cast<const float*>(a.part),
@@ -184,7 +187,14 @@ void launch_decode(const DecodeArgs& a, cudaStream_t s) {
   }
 }
 
+__global__ void k_set_int(int* p, int v) { *p = v; }
+
 }  // namespace
+
+void set_device_int(int* p, int v, cudaStream_t s) {
+  k_set_int<<<1, 1, 0, s>>>(p, v);
+  check_launch("k_set_int");
+}
 
 int decode_splits(int batch, int heads, int len) {
   // enough CTAs for two per SM, chunks no longer than the score staging
@@ -200,11 +210,11 @@ size_t decode_partial_bytes(int batch, int heads, int rank_pad, int max_len) {
 }
 
 void kv_store_bf16(const bf16* src, int64_t lds, int c0, int width, int batch, int rows_per_b,
-                   bf16* cache, int max_seq, int pos0, cudaStream_t s) {
+                   bf16* cache, int max_seq, int pos0, const int* pos_dev, cudaStream_t s) {
   const int64_t total = (int64_t)batch * rows_per_b * (width / 8);
   const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 4 * num_sms()));
   launch_pdl(k_kv_store, dim3(grid), dim3(256), 0, s, src, lds, c0, width, batch, rows_per_b,
-             cache, max_seq, pos0);
+             cache, max_seq, pos0, pos_dev);
   check_launch("k_kv_store");
 }
 

@@ -63,12 +63,14 @@ struct DecodeArgs {
   float* part;  // splits > 1: [batch*heads, splits, rank_pad + 2]
   bf16* out;
   int64_t ldo;
+  const int* pos_dev = nullptr;  // non-null: len = *pos_dev + 1 (graph replay)
 };
 int decode_splits(int batch, int heads, int len);
+void set_device_int(int* p, int v, cudaStream_t s);
 size_t decode_partial_bytes(int batch, int heads, int rank_pad, int max_len);
 void attn_decode_bf16(const DecodeArgs& a, cudaStream_t s);
 void kv_store_bf16(const bf16* src, int64_t lds, int c0, int width, int batch, int rows_per_b,
-                   bf16* cache, int max_seq, int pos0, cudaStream_t s);
+                   bf16* cache, int max_seq, int pos0, const int* pos_dev, cudaStream_t s);
 bool attn_rankspace_supported(int rank_pad);
 
 // ---- K3 / K4: FlashSVD-FFN -----------------------------------------------------

@@ -478,7 +478,7 @@ void tc_attention_rank(const Pack& p, size_t B, size_t M, const void* x, void* o
   }
   // decoder rows: the new tokens' [P_k | P_v] columns go to the rank-space cache
   kv_store_bf16(qkv, n, hr, kv_w, static_cast<int>(B), static_cast<int>(M), as<bf16>(am.cache),
-                static_cast<int>(am.max_seq), static_cast<int>(am.pos), s);
+                static_cast<int>(am.max_seq), static_cast<int>(am.pos), am.pos_dev, s);
   if (am.kind == AttnMode::Prefill) {
     tc_attention(B, M, qkv, n, 0, hr, (p.H + p.G) * p.rp, p.H, p.G, p.rp, o_rank, hr, s, true);
     return;
@@ -493,8 +493,9 @@ void tc_attention_rank(const Pack& p, size_t B, size_t M, const void* x, void* o
   a.heads = p.H;
   a.groups = p.G;
   a.rank_pad = p.rp;
-  a.len = static_cast<int>(am.pos) + 1;
+  a.len = static_cast<int>(am.pos_dev ? am.max_seq : am.pos + 1);
   a.splits = decode_splits(a.batch, a.heads, a.len);
+  a.pos_dev = am.pos_dev;
   // split partials live right after the projection rows
   a.part = reinterpret_cast<float*>(
       (reinterpret_cast<uintptr_t>(qkv + (size_t)T * n) + 255) & ~uintptr_t(255));
@@ -754,7 +755,7 @@ void ffn_branch_skinny(const Pack& p, int T, const void* x, void* branch, void* 
 }
 void layer_decode(const Pack& p, bool pre_ln, size_t B, const void* x, void* out, void* ws,
                   size_t ws_bytes, cudaStream_t s, const AttnMode& am) {
-  const DecodeLayout lay = decode_layout(p, B, am.pos + 1);
+  const DecodeLayout lay = decode_layout(p, B, am.pos_dev ? am.max_seq : am.pos + 1);
   if (ws_bytes < lay.total())
     fail(Kind::Config, "workspace too small: need " + std::to_string(lay.total()) + " bytes, got " +
                            std::to_string(ws_bytes));

@@ -104,6 +104,9 @@ struct AttnMode {
   void* cache = nullptr;
   size_t max_seq = 0;
   size_t pos = 0;  // Decode: position of the new token (keys 0..pos)
+  // Decode under graph capture: the position is read from pos_dev at run
+  // time, and the split count / partial buffers are sized for max_seq.
+  const int* pos_dev = nullptr;
 };
 void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const void* x, void* out,
                void* ws, size_t ws_bytes, cudaStream_t s, const AttnMode& am = AttnMode{});

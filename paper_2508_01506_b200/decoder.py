@@ -17,7 +17,8 @@ from .model import layer_descs
 
 
 class Decoder:
-    def __init__(self, layers, batch: int, max_seq: int, pre_ln: bool = False):
+    def __init__(self, layers, batch: int, max_seq: int, pre_ln: bool = False,
+                 graph: bool = False):
         import torch
         self.L = abi.lib()
         self.batch, self.max_seq, self.pre_ln = batch, max_seq, bool(pre_ln)
@@ -38,6 +39,17 @@ class Decoder:
                                                       int(self.pre_ln), C.byref(wb)))
         self.ws = torch.empty(wb.value, dtype=torch.uint8, device="cuda")
         self.pos = 0
+        # graph mode: the step runs on fixed token buffers, captured once
+        self.graph = None
+        if graph:
+            self.xbuf = torch.zeros((batch, self.d), dtype=torch.bfloat16, device="cuda")
+            self.obuf = torch.zeros((batch, self.d), dtype=torch.bfloat16, device="cuda")
+            g = C.c_void_p()
+            abi.check(self.L.fsvd_decoder_graph_create(
+                self.parr, len(self.packs), int(self.pre_ln), batch,
+                C.c_void_p(self.xbuf.data_ptr()), C.c_void_p(self.obuf.data_ptr()), self.carr,
+                max_seq, C.c_void_p(self.ws.data_ptr()), self.ws.numel(), C.byref(g)))
+            self.graph = g
 
     def _stream(self):
         import torch
@@ -59,6 +71,11 @@ class Decoder:
         """x_t [batch, d] bf16: the token at position self.pos -> its output."""
         import torch
         assert x_t.dtype == torch.bfloat16 and x_t.is_contiguous()
+        if self.graph is not None:
+            self.xbuf.copy_(x_t)
+            abi.check(self.L.fsvd_decoder_graph_step(self.graph, self.pos, self._stream()))
+            self.pos += 1
+            return self.obuf.clone()
         out = torch.empty_like(x_t)
         abi.check(self.L.fsvd_decoder_step(
             self.parr, len(self.packs), int(self.pre_ln), self.batch, self.pos,
@@ -68,6 +85,9 @@ class Decoder:
         return out
 
     def close(self):
+        if self.graph is not None:
+            self.L.fsvd_decoder_graph_destroy(self.graph)
+            self.graph = None
         for p in self.packs:
             self.L.fsvd_layer_pack_destroy(p)
         self.packs = []

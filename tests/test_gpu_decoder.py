@@ -92,6 +92,29 @@ def test_decode_steps_equal_prefix_encoder(L, ora, pre_ln):
     full.close()
 
 
+@pytest.mark.parametrize("pre_ln", [False, True])
+def test_graph_decode_equals_direct_steps(L, ora, pre_ln):
+    """The captured decode step (position read on the device, split count
+    sized for max_seq) replays to the same bits as direct steps."""
+    import torch
+    layers = _layers(ora, seed=600)
+    B, P, S, d = 2, 60, 12, 256
+    x = bf16_round(ora.random((B, P + S, d), 44))
+    xd = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    outs = []
+    for graph in (False, True):
+        dec = Decoder(layers, B, 700, pre_ln, graph=graph)
+        dec.prefill(xd[:, :P].contiguous())
+        outs.append(np.stack([dec.step(xd[:, P + k].contiguous()).float().cpu().numpy()
+                              for k in range(S)], axis=1))
+        dec.close()
+    # direct steps size the cache splits by the live length, the graph by
+    # max_seq: the fp32 merge order differs, so agreement is to rounding
+    assert H.rel_err(outs[1], outs[0]) <= 1e-2
+    ref = _causal_ref(ora, x, layers, pre_ln)[:, P:]
+    assert H.rel_err(outs[1], ref) <= H.TOL_BF16
+
+
 def test_decode_long_cache_uses_split_combine(L, ora):
     """B=1, 12 heads, 1500 cached tokens: the decode kernel splits the cache
     over CTAs and merges the partial softmax states."""
