@@ -190,6 +190,12 @@ fsvd_status fsvd_validate_tile_plan(const fsvd_tile_plan* plan, fsvd_kernel_kind
                                     const fsvd_geometry* geom, size_t* bytes);
 /* memtier.cpp:191-212 */
 fsvd_status fsvd_expected_bytes(fsvd_formula id, const fsvd_geometry* geom, size_t* bytes);
+/* planner.cpp:60-79 (flops_exact): algorithmic FLOP of one layer in `mode`
+ * (uniform rank: rank = proj_rank = ffn_rank). */
+fsvd_status fsvd_flops_exact(const fsvd_geometry* geom, fsvd_run_mode mode, uint64_t* flops);
+/* planner.cpp:89-98 (io_bytes): fp32 activation + weight bytes in / out. */
+fsvd_status fsvd_io_bytes(const fsvd_geometry* geom, fsvd_run_mode mode, uint64_t* in_bytes,
+                          uint64_t* out_bytes);
 /* encoder.cpp:333-345 */
 size_t fsvd_flash_layer_peak_transient_bytes(const fsvd_geometry* geom);
 size_t fsvd_flash_layer_persistent_bytes(const fsvd_geometry* geom);

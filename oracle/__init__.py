@@ -142,6 +142,9 @@ class Reference(_Base):
         L.ref_flops_exact.argtypes = [_P(abi.Geometry), C.c_int]
         L.ref_flops_exact.restype = C.c_ulonglong
         L.ref_factor_rank_r.argtypes = [_fp, _sz, _sz, _sz, _fp, _fp]
+        L.ref_io_bytes.argtypes = [_P(abi.Geometry), C.c_int, _P(C.c_ulonglong),
+                                   _P(C.c_ulonglong)]
+        L.ref_flops_exact_checked.argtypes = [_P(abi.Geometry), C.c_int, _P(C.c_ulonglong)]
         L.ref_decoder_bytes.argtypes = [C.c_int, _P(abi.Geometry), _sz, _P(_sz)]
         L.ref_svd.argtypes = [_fp, _sz, _sz, _fp, _fp, _fp]
         L.ref_factorize_attention.argtypes = [_fp] * 6 + [_sz, _sz, _sz, _fp, _fp, _fp]

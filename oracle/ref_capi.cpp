@@ -251,6 +251,23 @@ size_t ref_expected_bytes(int formula, const fsvd_geometry* g) {
 }
 
 // planner.cpp:60-79 (uniform-rank FLOP count used by the reference bench)
+// planner.cpp:89-98
+int ref_io_bytes(const fsvd_geometry* g, int mode, unsigned long long* in, unsigned long long* out) {
+  return guard([&] {
+    Geometry geo{g->batch, g->seq_len, g->d_model, g->d_ff, g->heads, g->groups, g->rank,
+                 g->layers};
+    IoBytes io = io_bytes(geo, static_cast<RunMode>(mode));
+    *in = io.in;
+    *out = io.out;
+  });
+}
+int ref_flops_exact_checked(const fsvd_geometry* g, int mode, unsigned long long* f) {
+  return guard([&] {
+    Geometry geo{g->batch, g->seq_len, g->d_model, g->d_ff, g->heads, g->groups, g->rank,
+                 g->layers};
+    *f = flops_exact(geo, static_cast<RunMode>(mode));
+  });
+}
 unsigned long long ref_flops_exact(const fsvd_geometry* g, int mode) {
   Geometry geo{g->batch, g->seq_len, g->d_model, g->d_ff, g->heads, g->groups, g->rank,
                g->layers};

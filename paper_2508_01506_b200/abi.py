@@ -127,6 +127,8 @@ def _declare(lib):
         "fsvd_meter_device_persistent_bytes": (_sz, [vp]),
         "fsvd_validate_tile_plan": (st, [P(TilePlan), C.c_int, P(Geometry), P(_sz)]),
         "fsvd_expected_bytes": (st, [C.c_int, P(Geometry), P(_sz)]),
+        "fsvd_flops_exact": (st, [P(Geometry), C.c_int, P(C.c_uint64)]),
+        "fsvd_io_bytes": (st, [P(Geometry), C.c_int, P(C.c_uint64), P(C.c_uint64)]),
         "fsvd_flash_layer_peak_transient_bytes": (_sz, [P(Geometry)]),
         "fsvd_flash_layer_persistent_bytes": (_sz, [P(Geometry)]),
         "fsvd_flash_layer_bound_bytes": (_sz, [P(Geometry)]),

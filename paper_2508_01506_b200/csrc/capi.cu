@@ -567,6 +567,51 @@ fsvd_status fsvd_expected_bytes(fsvd_formula id, const fsvd_geometry* geom, size
     *bytes = expected(id, *geom);
   });
 }
+namespace {
+// geometry.hpp:24-34
+void validate_geometry(const fsvd_geometry& g) {
+  if (g.batch == 0 || g.seq_len == 0 || g.d_model == 0 || g.d_ff == 0)
+    fail(Kind::Config, "geometry extents must be positive");
+  if (g.heads == 0 || g.d_model % g.heads != 0) fail(Kind::Config, "heads must divide d_model");
+  if (g.groups == 0 || g.d_model % g.groups != 0) fail(Kind::Config, "groups must divide d_model");
+  if (g.rank == 0) fail(Kind::Rank, "rank must be at least 1");
+  if (g.rank > g.d_model / g.groups) fail(Kind::Rank, "rank exceeds per-group width d_model/groups");
+}
+uint64_t gemm_flops(uint64_t m, uint64_t k, uint64_t n) { return 2 * m * k * n; }
+}  // namespace
+
+fsvd_status fsvd_flops_exact(const fsvd_geometry* geom, fsvd_run_mode mode, uint64_t* flops) {
+  return guard([&] {
+    if (!geom || !flops) fail(Kind::Config, "null argument");
+    check_mode(mode);
+    const fsvd_geometry& g = *geom;
+    validate_geometry(g);
+    const uint64_t bm = (uint64_t)g.batch * g.seq_len, m = g.seq_len, da = g.d_model,
+                   df = g.d_ff, h = g.heads, gr = g.groups, r = g.rank, dh = da / h;
+    const uint64_t score_value = g.batch * h * (gemm_flops(m, dh, m) + gemm_flops(m, m, dh));
+    if (mode == FSVD_MODE_DENSE) {
+      *flops = 4 * gemm_flops(bm, da, da) + score_value + gemm_flops(bm, da, df) +
+               gemm_flops(bm, df, da);
+      return;
+    }
+    *flops = 3 * gr * gemm_flops(bm, da, r) + 3 * gr * gemm_flops(bm, r, da / gr) + score_value +
+             gemm_flops(bm, da, r) + gemm_flops(bm, r, da) + gemm_flops(bm, da, r) +
+             gemm_flops(bm, r, df) + gemm_flops(bm, df, r) + gemm_flops(bm, r, da);
+  });
+}
+fsvd_status fsvd_io_bytes(const fsvd_geometry* geom, fsvd_run_mode mode, uint64_t* in_bytes,
+                          uint64_t* out_bytes) {
+  return guard([&] {
+    if (!geom || !in_bytes || !out_bytes) fail(Kind::Config, "null argument");
+    check_mode(mode);
+    validate_geometry(*geom);
+    const uint64_t bm = (uint64_t)geom->batch * geom->seq_len, da = geom->d_model,
+                   df = geom->d_ff, r = geom->rank;
+    *out_bytes = 4 * 2 * bm * da;
+    *in_bytes = mode == FSVD_MODE_DENSE ? 4 * (3 * bm * da + 2 * bm * df)
+                                        : 4 * (4 * bm * r + 3 * r * da + 2 * r * df);
+  });
+}
 size_t fsvd_flash_layer_peak_transient_bytes(const fsvd_geometry* g) {
   return 4 * 3 * g->groups * g->batch * g->seq_len * g->rank;
 }

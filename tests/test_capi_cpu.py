@@ -208,3 +208,27 @@ def test_layer_validation_errors():
     d = layer.desc()
     d.ffn.down.rank = 5
     assert L.fsvd_layer_pack_create(C.byref(d), abi.BF16, 0, C.byref(p)) == abi.ERR_CONFIG
+
+
+def test_flops_and_io_closed_forms_match_reference(reference):
+    """planner.cpp:60-98 flops_exact / io_bytes, bit-exact, all modes, with the
+    reference's geometry errors."""
+    import itertools
+    n = 0
+    for B, M, d, H, G, r in itertools.product((1, 32), (1, 128, 512), (64, 768), (4, 12), (1, 4),
+                                              (1, 8, 16)):
+        if d % H or d % G:
+            continue
+        g = abi.Geometry(B, M, d, 4 * d, H, G, r, 1)
+        for mode in range(4):
+            f, fi, fo = C.c_uint64(), C.c_uint64(), C.c_uint64()
+            st = L.fsvd_flops_exact(g, mode, C.byref(f))
+            rf = C.c_ulonglong()
+            rst = reference.lib.ref_flops_exact_checked(g, mode, C.byref(rf))
+            assert st == rst and (st or f.value == rf.value), (B, M, d, H, G, r, mode)
+            st = L.fsvd_io_bytes(g, mode, C.byref(fi), C.byref(fo))
+            ri, ro = C.c_ulonglong(), C.c_ulonglong()
+            rst = reference.lib.ref_io_bytes(g, mode, C.byref(ri), C.byref(ro))
+            assert st == rst and (st or (fi.value, fo.value) == (ri.value, ro.value))
+            n += 1
+    assert n > 200
