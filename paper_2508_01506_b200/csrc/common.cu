@@ -1,5 +1,6 @@
 // common.cu -- TMA descriptor encoding, launch accounting, device queries.
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -37,6 +38,14 @@ void check_launch(const char* what) {
   note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FSVD_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
 }
 
 int num_sms() {
