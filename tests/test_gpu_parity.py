@@ -449,3 +449,90 @@ def test_empty_inputs_rejected_like_reference(L, ora, reference, shape):
     assert st == abi.ERR_SHAPE and b"at least 1" in L.fsvd_last_error()
     torch.cuda.synchronize()
     L.fsvd_layer_pack_destroy(p)
+
+
+# ------------------------------------------------------------------ FFN known answers
+def _identity_slice(rows, cols):
+    m = np.zeros((rows, cols), np.float32)
+    k = min(rows, cols)
+    m[np.arange(k), np.arange(k)] = 1.0
+    return m
+
+
+@pytest.mark.parametrize("dims", [(6, 8, 3), (256, 512, 64)], ids=["ref_6x8_r3", "tc_256x512_r64"])
+@pytest.mark.parametrize("dtype", [abi.F32, abi.BF16], ids=["f32", "bf16"])
+def test_ffn_v2_identity_slice_embeds_leading_columns(L, ora, dims, dtype):
+    """test_ffn.cpp:113-128: identity-slice factors, identity activation, zero
+    biases -> out[:, :, j] == x[:, :, j] for j < r, else 0, EXACTLY."""
+    from paper_2508_01506_b200.model import FfnFactors, LinearFactors
+    d, df, r = dims
+    f = FfnFactors(LinearFactors(_identity_slice(d, r), _identity_slice(r, df), np.zeros(df)),
+                   LinearFactors(_identity_slice(df, r), _identity_slice(r, d), np.zeros(d)),
+                   abi.ACT_IDENTITY)
+    x = bf16_round(ora.random((1, 5 if d == 6 else 130, d), 840))
+    got = H.ffn(2, x, f, PLAN, dtype)
+    want = np.where(np.arange(d) < r, x, 0.0).astype(np.float32)
+    assert np.array_equal(got, want)
+
+
+def test_ffn_v1_identity_chain_is_factor_product(L, ora):
+    """test_ffn.cpp:47-69: identity activation, zero biases -> the plain chain
+    x U_up V_up U_down V_down (fp64 numpy), < 1e-4."""
+    f = oracle.rand_ffn(ora, 12, 24, 5, 800, act=abi.ACT_IDENTITY)
+    f.up.bias[...] = 0
+    f.down.bias[...] = 0
+    x = ora.random((2, 9, 12), 801)
+    got = H.ffn(1, x, f, PLAN, abi.F32)
+    chain = (x.astype(np.float64) @ f.up.u @ f.up.v @ f.down.u @ f.down.v)
+    assert np.abs(got - chain).max() < 1e-4
+
+
+@pytest.mark.parametrize("act", [abi.ACT_GELU_ERF, abi.ACT_GELU_TANH, abi.ACT_RELU,
+                                 abi.ACT_IDENTITY], ids=["erf", "tanh", "relu", "identity"])
+@pytest.mark.parametrize("variant", [1, 2], ids=["v1", "v2"])
+def test_ffn_activations_match_oracle(L, ora, act, variant):
+    """All four activations (ffn.cpp:16-24) through the tensor-core FFN vs the
+    oracle restatement (bf16 policy) and the SIMT fp32 path (fp32 policy)."""
+    f = oracle.rand_ffn(ora, 256, 1024, 128, 850 + act, act=act)
+    x = ora.random((2, 130, 256), 851)
+    ref = ora.ffn(variant, x, f, PLAN)
+    assert H.rel_err(H.ffn(variant, x, f, PLAN, abi.F32), ref) <= H.TOL_F32
+    for a in (f.up.u, f.up.v, f.up.bias, f.down.u, f.down.v, f.down.bias):
+        a[...] = bf16_round(a)
+    xb = bf16_round(x)
+    ref = ora.ffn(variant, xb, f, PLAN)
+    assert H.rel_err(H.ffn(variant, xb, f, PLAN, abi.BF16), ref) <= H.TOL_BF16
+
+
+def test_bert_base_r64_twelve_layers_finite(L, ora):
+    """test_encoder.cpp:593-622: BERT-Base, 12 layers, full per-head rank
+    r = 64 (rank padding 64: single-buffered attention O), FlashV2 runs and
+    every output is finite and LayerNorm-shaped."""
+    import torch
+    from paper_2508_01506_b200.model import random_layer
+    rng = np.random.default_rng(3)
+    layers = [round_layer_bf16(random_layer(768, 3072, 12, 12, 64, 768, 768, rng))
+              for _ in range(12)]
+    B, M, d = 2, 384, 768
+    descs = layer_descs(layers)
+    packs = []
+    for i in range(12):
+        p = C.c_void_p()
+        abi.check(L.fsvd_layer_pack_create(C.byref(descs[i]), abi.BF16, 0, C.byref(p)))
+        packs.append(p)
+    parr = (C.c_void_p * 12)(*[p.value for p in packs])
+    ws = C.c_size_t()
+    abi.check(L.fsvd_workspace_bytes(parr, 12, B, M, abi.MODE_FLASH_V2, C.byref(ws)))
+    work = torch.empty(ws.value, dtype=torch.uint8, device="cuda")
+    x = torch.randn((B, M, d), generator=torch.Generator().manual_seed(2)).to(torch.bfloat16).cuda()
+    abi.check(L.fsvd_model_fwd(parr, 12, abi.MODE_FLASH_V2, 0, B, M, C.c_void_p(x.data_ptr()),
+                               C.c_void_p(x.data_ptr()), C.c_void_p(work.data_ptr()), ws.value,
+                               C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    o = x.float().cpu().numpy()
+    assert np.isfinite(o).all()
+    g, b_ = layers[-1].ln2_gamma, layers[-1].ln2_beta
+    z = (o - b_) / g
+    assert np.abs(z.mean(-1)).max() < 0.05 and np.abs(z.std(-1) - 1).max() < 0.05
+    for p in packs:
+        L.fsvd_layer_pack_destroy(p)
