@@ -94,6 +94,11 @@ __device__ __forceinline__ void warp_arrive_leader(uint64_t* bar) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
 }
+// Same, without release ordering (TMEM-drained signals carry no smem data).
+__device__ __forceinline__ void warp_arrive_leader_relaxed(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(bar), 0));
+}
 
 template <int FR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -325,19 +330,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_before();
     warp_arrive_leader(&bars->p_ready);
     for (int f = 0; f < NB; ++f) {
-      float bb[2][32];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int fb = f * BF + (half + 2 * i) * 32;
-        load_bias<32>(bb[i], b_up + fb, d_ff - fb);
-      }
       mbar_wait(&bars->h_full, f & 1);
       tc_fence_after();
       float v[2][32];
 #pragma unroll
       for (int i = 0; i < 2; ++i) ld_chunk(tmem + C::t_h + loff + (half + 2 * i) * 32, v[i]);
       tc_fence_before();
-      warp_arrive_leader(&bars->h_free);
+      warp_arrive_leader_relaxed(&bars->h_free);
+      float bb[2][32];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int fb = f * BF + (half + 2 * i) * 32;
+        load_bias<32>(bb[i], b_up + fb, d_ff - fb);
+      }
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         bias_act_chunk2<32>(v[i], bb[i], act);

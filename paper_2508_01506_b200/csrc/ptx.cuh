@@ -353,6 +353,13 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// Remote arrive with no memory ordering (signals that carry no generic-proxy
+// data, e.g. "TMEM region drained"): skips the release fence, which would
+// also wait for this thread's in-flight global loads.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
 // TMA load issued by either CTA of the pair; the transaction bytes complete on
 // the LEADER's barrier (rank bit of the shared::cluster address cleared).
 __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint64_t* bar, void* dst,
