@@ -120,6 +120,29 @@ struct Bars {
 };
 static_assert(sizeof(Bars) <= 4608, "Bars outgrew its shared-memory reservation");
 
+// Work item w -> (query tile, head, batch).  Encoder: query tile fastest, so
+// consecutive items share (batch, head) and K/V stay hot in L2.  Causal: the
+// query tile is the SLOWEST index and runs from the last (most key tiles)
+// down, so the stride-gridDim walk hands every CTA a mix of long and short
+// items instead of a fixed query-tile position (largest work first).
+struct Item {
+  int qt, h, b;
+};
+__device__ __forceinline__ Item item_of(int w, int nqt, int heads, int batch, int causal) {
+  Item it;
+  if (causal) {
+    const int hb = heads * batch, rem = w % hb;
+    it.qt = nqt - 1 - w / hb;
+    it.h = rem % heads;
+    it.b = rem / heads;
+  } else {
+    it.qt = w % nqt;
+    it.h = (w / nqt) % heads;
+    it.b = w / (nqt * heads);
+  }
+  return it;
+}
+
 // Persistent: each CTA walks work items (batch, head, 128-query tile) with
 // stride gridDim.x; consecutive items share (batch, head) so K/V stay hot in
 // L2.  Q of the next item and its first K/V tiles are prefetched while the
@@ -174,7 +197,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       uint32_t st = 0, ph = 0;
       int it = 0;
       for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
-        const int qt = w % nqt, h = (w / nqt) % heads, b = w / (nqt * heads);
+        const Item iw = item_of(w, nqt, heads, batch, causal);
+        const int qt = iw.qt, h = iw.h, b = iw.b;
         const int g = h / hpg, row0 = b * seq;
         const int qs = it & 1;
         mbar_wait(&bars->q_empty[qs], ((it >> 1) & 1) ^ 1);
@@ -227,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
       const int qs = it & 1;
-      const int nji = causal ? min(nj, w % nqt + 1) : nj;
+      const int nji = causal ? min(nj, item_of(w, nqt, heads, batch, causal).qt + 1) : nj;
       if (lane == 0 && it < 100) ATRACE(400 + it);
       for (int j = 0; j < nji; ++j) {
         const int t = gt + j;
@@ -322,7 +346,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     int pv_row0 = 0, pv_q0 = 0, pv_h = 0;
     float pv_l = 0.0f;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
-      const int qt = w % nqt, h = (w / nqt) % heads, b = w / (nqt * heads);
+      const Item iw = item_of(w, nqt, heads, batch, causal);
+      const int qt = iw.qt, h = iw.h, b = iw.b;
       const int row0 = b * seq, q0 = qt * QT;
       const int nji = causal ? min(nj, qt + 1) : nj;
       const uint32_t t_o = C::t_o + (it % C::NOB) * RP;
