@@ -59,6 +59,7 @@ struct Ffn2Bars {
   uint64_t full[12], empty[12];
   uint64_t x_full[2], x_empty[2];
   uint64_t p_acc, p_ready, h_full, h_free, sh_full[2], sh_free[2], z_full, zs_ready;
+  uint64_t sh_loc[2];  // this CTA's epilogue warps -> relay (local, no cluster fence)
   uint64_t o_full[2], o_free[2];
   uint64_t res_full[2], res_empty[2];
   uint32_t tmem;
@@ -100,6 +101,19 @@ __device__ __forceinline__ void warp_arrive_leader_relaxed(uint64_t* bar) {
   if ((threadIdx.x & 31) == 0) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(bar), 0));
 }
 
+#ifdef FSVD_TRACE
+__device__ long long g_trace2[8192];
+}  // namespace
+extern "C" __attribute__((visibility("default"))) int fsvd_debug_trace2_copy(long long* host, int n) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace2, sizeof(long long) * n));
+}
+namespace {
+// cluster 0 only; slot offset 4096 for the peer CTA
+#define TRACE2(slot) do { if (blockIdx.x < 2) g_trace2[(slot) + 4096 * blockIdx.x] = clock64(); } while (0)
+#else
+#define TRACE2(slot) do { } while (0)
+#endif
+
 template <int FR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_ffn2(const __grid_constant__ CUtensorMap tmX,    // X [T, d]        box 128 x 64
@@ -111,6 +125,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
            const float* __restrict__ b_up, const float* __restrict__ b_dn, int act, int T,
            int d_model, int d_ff, bf16* __restrict__ out, const float* __restrict__ ln_g,
            const float* __restrict__ ln_b, float ln_eps) {
+  if (threadIdx.x == 0) TRACE2(0);
   using C = Ffn2Cfg<FR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -139,8 +154,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->x_full[i], 1);
       mbar_init(&bars->x_empty[i], 1);
-      mbar_init(&bars->sh_full[i], 2 * kEpiWarps);
+      mbar_init(&bars->sh_full[i], 2);  // one relay arrival per CTA
       mbar_init(&bars->sh_free[i], 1);
+      mbar_init(&bars->sh_loc[i], kEpiWarps);
       mbar_init(&bars->o_full[i], 1);
       mbar_init(&bars->o_free[i], 2 * kEpiWarps);
       mbar_init(&bars->res_full[i], 1);
@@ -206,7 +222,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       };
       mma1_slots(0);
       for (int f = 0; f < NB; ++f) {
+        if (me == 0) TRACE2(2048 + f * 2);
         if (f + 1 < NB) mma1_slots(f + 1);
+        if (me == 0) TRACE2(2048 + f * 2 + 1);
         mma2_slots(f);
       }
       for (int q = 0; q < NQ; ++q)
@@ -216,7 +234,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 10) {
-    // ================================================= residual producer (fused LN)
+    // ================================================= relay + residual producer
+    // Stream phase: the epilogue warps of this CTA arrive locally on sh_loc;
+    // this lane forwards ONE release.cluster arrival per H atom to the
+    // leader, so the cluster-scope fence is paid once per atom instead of on
+    // every epilogue warp's critical path.
+    if (lane == 0) {
+      for (int f = 0; f < NB; ++f)
+        for (int a = 0; a < 2; ++a) {
+          mbar_wait(&bars->sh_loc[a], f & 1);
+          mbar_arrive_cluster(mapa_shared(smem_u32(&bars->sh_full[a]), 0));
+        }
+    }
+    __syncwarp();
     if (fuse_ln && lane == 0) {
       mbar_wait(&bars->z_full, 0);
       lnepi::produce_residual<64>(&tmX, smem + C::o_h, bars->res_full, bars->res_empty, 2,
@@ -271,21 +301,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->p_ready, 0);
       tc_fence_after();
       auto mma1 = [&](int f) {
+        TRACE2(64 + f * 8 + 0);
         if (f > 0) {
           mbar_wait(&bars->h_free, (f - 1) & 1);
           tc_fence_after();
         }
+        TRACE2(64 + f * 8 + 1);
         consume(C::NATOM, [&](int a, uint64_t slot) {
           mma4(tmem + C::t_h, d_p + a * kAtom, slot, id128, a != 0);
         });
         commit(&bars->h_full);
+        TRACE2(64 + f * 8 + 2);
       };
       auto mma2 = [&](int f) {
         consume(2 * C::NPIECE, [&](int j, uint64_t slot) {
           const int a = j / C::NPIECE, p = j % C::NPIECE;
           if (p == 0) {
+            TRACE2(64 + f * 8 + 3 + a * 2);
             mbar_wait(&bars->sh_full[a], f & 1);
             tc_fence_after();
+            TRACE2(64 + f * 8 + 4 + a * 2);
           }
           mma4(tmem + C::t_z + p * C::PS, d_h + a * kAtom, slot, id128, (f | a) != 0);
           if (p == C::NPIECE - 1) commit(&bars->sh_free[a]);
@@ -297,8 +332,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         mma2(f);
       }
       commit(&bars->z_full);
+      TRACE2(2);
       mbar_wait(&bars->zs_ready, 0);
       tc_fence_after();
+      TRACE2(3);
       const uint32_t idq = fuse_ln ? idesc_bf16(2 * BMr, 64) : idesc_bf16(2 * BMr, 128);
       for (int q = 0; q < NQ; ++q) {
         if (q >= 2) {
@@ -330,8 +367,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_before();
     warp_arrive_leader(&bars->p_ready);
     for (int f = 0; f < NB; ++f) {
+      if (threadIdx.x == 64) TRACE2(1024 + f * 8 + 0);
       mbar_wait(&bars->h_full, f & 1);
       tc_fence_after();
+      if (threadIdx.x == 64) TRACE2(1024 + f * 8 + 1);
       float v[2][32];
 #pragma unroll
       for (int i = 0; i < 2; ++i) ld_chunk(tmem + C::t_h + loff + (half + 2 * i) * 32, v[i]);
@@ -346,11 +385,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         bias_act_chunk2<32>(v[i], bb[i], act);
+        if (threadIdx.x == 64) TRACE2(1024 + f * 8 + 2 + i * 2);
         if (f > 0) mbar_wait(&bars->sh_free[i], (f - 1) & 1);
+        if (threadIdx.x == 64) TRACE2(1024 + f * 8 + 3 + i * 2);
         st_chunk_smem(s_h, row, (half + 2 * i) * 32, v[i]);
         fence_proxy_async_smem();
         tc_fence_before();
-        warp_arrive_leader(&bars->sh_full[i]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->sh_loc[i]);
       }
     }
     mbar_wait(&bars->z_full, 0);
@@ -385,6 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if (threadIdx.x == 0 || threadIdx.x == 64) TRACE2(1 + (threadIdx.x == 64 ? 4 : 0));
   tc_fence_before();
   cluster_sync_all();
   if (warp == 1) {

@@ -132,9 +132,10 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
     tmem_ld_wait();
     tc_fence_before();
     if (acc_empty_leader) {
-      // CTA pair: one arrive per warp on the leader CTA's barrier
+      // CTA pair: one arrive per warp on the leader CTA's barrier; the signal
+      // is "TMEM drained" (no shared-memory data), so no release fence
       __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(acc_empty_leader + acc * 8);
+      if ((threadIdx.x & 31) == 0) mbar_arrive_cluster_relaxed(acc_empty_leader + acc * 8);
     } else {
       mbar_arrive(&acc_empty[acc]);
     }
