@@ -189,7 +189,26 @@ void launch_decode(const DecodeArgs& a, cudaStream_t s) {
 
 __global__ void k_set_int(int* p, int v) { *p = v; }
 
+// z[i] = bf16(sum_s part[s][i]), splits summed in order
+__global__ void k_z_partial_sum(const float* __restrict__ part, int splits, int64_t n,
+                                bf16* __restrict__ z) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.0f;
+    for (int sp = 0; sp < splits; ++sp) acc += part[sp * n + i];
+    z[i] = __float2bfloat16_rn(acc);
+  }
+}
+
 }  // namespace
+
+void z_partial_sum_bf16(const float* part, int splits, int64_t n, bf16* z, cudaStream_t s) {
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 4 * num_sms()));
+  launch_pdl(k_z_partial_sum, dim3(grid), dim3(256), 0, s, part, splits, n, z);
+  check_launch("k_z_partial_sum");
+}
 
 void set_device_int(int* p, int v, cudaStream_t s) {
   k_set_int<<<1, 1, 0, s>>>(p, v);

@@ -124,7 +124,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const __grid_constant__ CUtensorMap tmY,    // out [T, d]      box 128x64 (fused LN)
           const float* __restrict__ b_up, const float* __restrict__ b_dn, int act, int T,
           int d_model, int d_ff, bf16* __restrict__ z_out, bf16* __restrict__ out,
-          const float* __restrict__ ln_g, const float* __restrict__ ln_b, float ln_eps) {
+          const float* __restrict__ ln_g, const float* __restrict__ ln_b, float ln_eps,
+          int split_blocks, float* __restrict__ z_part) {
   using C = FfnCfg<FR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -132,7 +133,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   FfnBars* bars = reinterpret_cast<FfnBars*>(smem + C::o_bar);
   const uint32_t warp = warp_id(), lane = lane_id();
   const int m0 = blockIdx.x * BMr;
-  const int NB = (d_ff + BF - 1) / BF;
+  // V1 with split_blocks > 0: blockIdx.y streams feature blocks
+  // [fb0, fb0 + NB) only and writes an fp32 partial Z (summed by the caller;
+  // decode rows use this to spread one row tile's d_ff over many CTAs)
+  const int NBall = (d_ff + BF - 1) / BF;
+  const int fb0 = split_blocks ? static_cast<int>(blockIdx.y) * split_blocks : 0;
+  const int NB = split_blocks ? min(split_blocks, NBall - fb0) : NBall;
   const int KC = d_model / 64;                        // X K-chunks (FUSED)
   const bool fuse_ln = FUSED && ln_g != nullptr;     // out = LN2(x + ffn(x)) (ln_epi.cuh)
   const int QS = (d_model % 128 == 0 && !fuse_ln) ? 128 : 64;  // output columns per piece
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       auto mma1_slots = [&](int f) {
         emit(C::NATOM, [&](int a, uint8_t* dst, bool size_only) -> uint32_t {
-          if (!size_only) tma_load_2d(&tmVup, &bars->full[st], dst, a * 64, f * BF);
+          if (!size_only) tma_load_2d(&tmVup, &bars->full[st], dst, a * 64, (fb0 + f) * BF);
           return SLOT;
         });
       };
@@ -211,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         emit(2 * C::NPIECE, [&](int j, uint8_t* dst, bool size_only) -> uint32_t {
           const int a = j / C::NPIECE, p = j % C::NPIECE;
           if (!size_only)
-            tma_load_2d(&tmUdn, &bars->full[st], dst, f * BF + a * 64, p * C::PS);
+            tma_load_2d(&tmUdn, &bars->full[st], dst, (fb0 + f) * BF + a * 64, p * C::PS);
           return C::PS * 128;
         });
       };
@@ -393,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float bb[2][32];  // b_up of this block, fetched while the MMA runs
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int fb = f * BF + (half + 2 * i) * 32;
+        const int fb = (fb0 + f) * BF + (half + 2 * i) * 32;
         load_bias<32>(bb[i], b_up + fb, d_ff - fb);
       }
       if (threadIdx.x == 64) TRACE(1024 + f * 8 + 0);
@@ -423,7 +429,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = half; c < FR / 32; c += 2) {
         float v[32];
         ld_chunk(tmem + C::t_z + loff + c * 32, v);
-        if (grow < T) st_chunk_global(z_out + (int64_t)grow * FR + c * 32, v);
+        if (grow >= T) continue;
+        if (z_part) {
+          float4* d = reinterpret_cast<float4*>(
+              z_part + ((int64_t)blockIdx.y * T + grow) * FR + c * 32);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            d[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        } else {
+          st_chunk_global(z_out + (int64_t)grow * FR + c * 32, v);
+        }
       }
     } else {
       for (int c = half; c < FR / 32; c += 2) {
@@ -490,9 +505,11 @@ void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
   else
     tp = tmap_bf16(a.p_in, a.T, FR, FR, 128, 64, TmaSwizzle::B128);
   const int grid = (a.T + BMr - 1) / BMr;
-  launch_pdl(k_ffn<FR, FUSED>, dim3(grid), dim3(kThreads), C::SMEM, s, tx, tp, tup, tvup, tudn,
-             tvdn, ty, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff, a.z_out, a.out, a.ln_g,
-             a.ln_b, a.ln_eps);
+  const int nball = (a.d_ff + BF - 1) / BF;
+  const int splits = (!FUSED && a.split_blocks) ? (nball + a.split_blocks - 1) / a.split_blocks : 1;
+  launch_pdl(k_ffn<FR, FUSED>, dim3(grid, splits), dim3(kThreads), C::SMEM, s, tx, tp, tup, tvup,
+             tudn, tvdn, ty, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff, a.z_out, a.out,
+             a.ln_g, a.ln_b, a.ln_eps, FUSED ? 0 : a.split_blocks, FUSED ? nullptr : a.z_part);
   check_launch(FUSED ? "k_ffn_fused" : "k_ffn_stream");
 }
 

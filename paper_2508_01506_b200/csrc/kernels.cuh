@@ -92,8 +92,14 @@ struct FfnTcArgs {
   const float* ln_g;
   const float* ln_b;
   float ln_eps;
+  // V1 only: split_blocks > 0 spreads the d_ff feature blocks of each row
+  // tile over ceil(blocks / split_blocks) CTAs, each writing an fp32 partial
+  // Z to z_part[split][T][rank_pad] (z_out unused); sum with z_partial_sum.
+  int split_blocks = 0;
+  float* z_part = nullptr;
 };
 void ffn_stream_bf16(const FfnTcArgs& a, cudaStream_t s);   // V1 middle: P -> Z
+void z_partial_sum_bf16(const float* part, int splits, int64_t n, bf16* z, cudaStream_t s);
 void ffn_fused_bf16(const FfnTcArgs& a, cudaStream_t s);    // V2: X -> out
 // V2 on a CTA pair (cta_group::2, 256 rows per cluster): half the weight bytes
 // per SM; d_model, d_ff, rank_pad multiples of 128, rank_pad <= 384.

@@ -736,22 +736,42 @@ DecodeLayout decode_layout(const Pack& p, size_t T, size_t len) {
   const size_t attn = align256(T * p.qkv_cols * es) +
                       align256(decode_partial_bytes(static_cast<int>(T), p.H, p.rp,
                                                     static_cast<int>(len)));
-  const size_t ffn = align256(T * (2 * (size_t)p.frp + p.df + p.d) * es);
+  // FFN chain: P | Z | branch (bf16) + the fp32 per-split partial Z
+  const size_t nblk = (static_cast<size_t>(p.df) + 127) / 128;
+  const size_t ffn = align256(T * (2 * (size_t)p.frp + p.d) * es) +
+                     align256(nblk * T * p.frp * sizeof(float));
   return {align256(T * std::max<size_t>((size_t)p.H * p.rp, p.d) * es), align256(T * p.d * es),
           std::max(attn, ffn)};
 }
-// Skinny FFN branch for decode rows: four GEMMs spread over many CTAs
-// (the fused K4 runs one CTA per 128-row tile, i.e. one CTA here).
+// Skinny FFN branch for decode rows (one row tile): P = x U_up (64-wide GEMM
+// tiles), the feature stream K3 with every 128-feature block on its own CTA
+// (fp32 partial Z per block, summed in order), then Z V_down + b.
 void ffn_branch_skinny(const Pack& p, int T, const void* x, void* branch, void* trans,
                        cudaStream_t s) {
   bf16* P = as<bf16>(trans);
-  bf16* hid = P + (size_t)T * p.frp;
-  bf16* Z = hid + (size_t)T * p.df;
+  bf16* Z = P + (size_t)T * p.frp;
+  bf16* br = as<bf16>(branch);
+  float* part = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(Z + (size_t)T * p.frp + (size_t)T * p.d) + 255) & ~uintptr_t(255));
   gemm_bf16(as<bf16>(x), p.d, as<bf16>(p.uup_t), p.d, P, p.frp, T, p.frp, p.d, nullptr, ACT_NONE, s);
-  gemm_bf16(P, p.frp, as<bf16>(p.vup_t), p.frp, hid, p.df, T, p.df, p.frp, p.bup, p.act, s);
-  gemm_bf16(hid, p.df, as<bf16>(p.udn_t), p.df, Z, p.frp, T, p.frp, p.df, nullptr, ACT_NONE, s);
-  gemm_bf16(Z, p.frp, as<bf16>(p.vdn_t), p.frp, as<bf16>(branch), p.d, T, p.d, p.frp, p.bdn,
-            ACT_NONE, s);
+  FfnTcArgs a{};
+  a.T = T;
+  a.d_model = p.d;
+  a.d_ff = p.df;
+  a.rank_pad = p.frp;
+  a.up_v_t = as<bf16>(p.vup_t);
+  a.up_b = p.bup;
+  a.dn_u_t = as<bf16>(p.udn_t);
+  a.dn_v_t = as<bf16>(p.vdn_t);
+  a.dn_b = p.bdn;
+  a.act = p.act;
+  a.p_in = P;
+  a.split_blocks = 1;
+  a.z_part = part;
+  ffn_stream_bf16(a, s);
+  const int splits = (p.df + 127) / 128;
+  z_partial_sum_bf16(part, splits, (int64_t)T * p.frp, Z, s);
+  gemm_bf16(Z, p.frp, as<bf16>(p.vdn_t), p.frp, br, p.d, T, p.d, p.frp, p.bdn, ACT_NONE, s);
 }
 void layer_decode(const Pack& p, bool pre_ln, size_t B, const void* x, void* out, void* ws,
                   size_t ws_bytes, cudaStream_t s, const AttnMode& am) {
@@ -764,7 +784,7 @@ void layer_decode(const Pack& p, bool pre_ln, size_t B, const void* x, void* out
   void* Bb = base + lay.a;
   void* trans = base + lay.a + lay.b;
   const int T = static_cast<int>(B), hr = p.H * p.rp;
-  bf16* branch = as<bf16>(trans) + (size_t)T * (2 * p.frp + p.df);  // FFN chain's last slot
+  bf16* branch = as<bf16>(trans) + (size_t)T * 2 * p.frp;  // after the FFN chain's P | Z
   if (!pre_ln) {
     tc_attention_rank(p, B, 1, x, A, trans, s, am);                          // O_rank -> A
     gemm_bf16(as<bf16>(A), hr, as<bf16>(p.wov_t), hr, branch, p.d, T, p.d, hr, p.bov, ACT_NONE, s);
