@@ -66,6 +66,18 @@ __global__ void __launch_bounds__(kDecThreads)
   const int width = 2 * groups * RP;
   const bf16* kbase = cache + (int64_t)b * max_seq * width + g * RP;
   const bf16* vbase = kbase + groups * RP;
+  // The new token (position len - 1) is read from the projection rows, not
+  // the cache: this kernel also appends it (the first head of each group,
+  // split 0 writes the group's K and V rows), so no reader races the write.
+  const int pos = len - 1;
+  const bf16* knew = qkv + (int64_t)b * ldq + q_off + heads * RP + g * RP;
+  const bf16* vnew = knew + groups * RP;
+  if (blockIdx.y == 0 && h % (heads / groups) == 0 && threadIdx.x < 2 * (RP / 8)) {
+    const int half = threadIdx.x / (RP / 8), v8 = threadIdx.x % (RP / 8);
+    const uint4 x = reinterpret_cast<const uint4*>(half ? vnew : knew)[v8];
+    bf16* dst = const_cast<bf16*>(half ? vbase : kbase) + (int64_t)pos * width;
+    reinterpret_cast<uint4*>(dst)[v8] = x;
+  }
   __shared__ float q[RP];
   __shared__ float sc[kDecChunk];
   __shared__ float wred[kDecThreads / 32];
@@ -78,7 +90,7 @@ __global__ void __launch_bounds__(kDecThreads)
   // scores of this chunk (one cache row per thread per pass)
   float mx = -INFINITY;
   for (int j = k0 + tid; j < k1; j += kDecThreads) {
-    const uint4* kr = reinterpret_cast<const uint4*>(kbase + (int64_t)j * width);
+    const uint4* kr = reinterpret_cast<const uint4*>(j == pos ? knew : kbase + (int64_t)j * width);
     float s = 0.0f;
 #pragma unroll
     for (int v = 0; v < RP / 8; ++v) {
@@ -109,7 +121,7 @@ __global__ void __launch_bounds__(kDecThreads)
   for (int j = k0 + tid; j < k1; j += kDecThreads) {
     const float p = exp2f(sc[j - k0] - m);
     l += p;
-    const uint4* vr = reinterpret_cast<const uint4*>(vbase + (int64_t)j * width);
+    const uint4* vr = reinterpret_cast<const uint4*>(j == pos ? vnew : vbase + (int64_t)j * width);
 #pragma unroll
     for (int v = 0; v < RP / 8; ++v) {
       const uint4 u = vr[v];

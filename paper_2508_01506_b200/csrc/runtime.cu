@@ -476,9 +476,11 @@ void tc_attention_rank(const Pack& p, size_t B, size_t M, const void* x, void* o
     tc_attention(B, M, qkv, n, 0, hr, (p.H + p.G) * p.rp, p.H, p.G, p.rp, o_rank, hr, s);
     return;
   }
-  // decoder rows: the new tokens' [P_k | P_v] columns go to the rank-space cache
-  kv_store_bf16(qkv, n, hr, kv_w, static_cast<int>(B), static_cast<int>(M), as<bf16>(am.cache),
-                static_cast<int>(am.max_seq), static_cast<int>(am.pos), am.pos_dev, s);
+  // decoder rows: the new tokens' [P_k | P_v] columns go to the rank-space
+  // cache (prefill: one strided copy; decode: appended by k_attn_decode)
+  if (am.kind == AttnMode::Prefill)
+    kv_store_bf16(qkv, n, hr, kv_w, static_cast<int>(B), static_cast<int>(M), as<bf16>(am.cache),
+                  static_cast<int>(am.max_seq), static_cast<int>(am.pos), am.pos_dev, s);
   if (am.kind == AttnMode::Prefill) {
     tc_attention(B, M, qkv, n, 0, hr, (p.H + p.G) * p.rp, p.H, p.G, p.rp, o_rank, hr, s, true);
     return;
