@@ -15,8 +15,9 @@
 // k_attn_decode: grid (B*H, splits); a CTA scores one chunk of the cache for
 // one (sequence, head) -- scores to shared memory, chunk max, p = 2^(s - m),
 // l and O = sum p * P_v in fp32 -- and writes (m, l, O) partials;
-// k_attn_combine merges the splits (max-rescaled sums) into the rank-space
-// output row [B, H*rp] consumed by the fused out-projection + LN1.
+// the last CTA of each (sequence, head) to finish merges the splits
+// (max-rescaled sums, in split order) into the rank-space output row
+// [B, H*rp] consumed by the out-projection + LN1.
 #include <algorithm>
 #include <cstdint>
 
@@ -56,7 +57,8 @@ template <int RP>
 __global__ void __launch_bounds__(kDecThreads)
     k_attn_decode(const bf16* __restrict__ qkv, int64_t ldq, int q_off, const bf16* __restrict__ cache,
                   int max_seq, int heads, int groups, int len, int splits, float* __restrict__ part,
-                  bf16* __restrict__ out, int64_t ldo, const int* __restrict__ pos_dev) {
+                  bf16* __restrict__ out, int64_t ldo, const int* __restrict__ pos_dev,
+                  unsigned* __restrict__ arrivals) {
   const int bh = blockIdx.x, b = bh / heads, h = bh % heads, g = h / (heads / groups);
   ptx::pdl_trigger();
   ptx::pdl_wait();
@@ -163,40 +165,43 @@ __global__ void __launch_bounds__(kDecThreads)
       }
     }
   }
-}
-
-template <int RP>
-__global__ void k_attn_combine(const float* __restrict__ part, int heads, int splits,
-                               bf16* __restrict__ out, int64_t ldo) {
-  const int bh = blockIdx.x, b = bh / heads, h = bh % heads, c = threadIdx.x;
-  ptx::pdl_trigger();
-  ptx::pdl_wait();
-  if (c >= RP) return;
-  const float* pp = part + (int64_t)bh * splits * (RP + 2);
-  float m = -INFINITY;
-  for (int s = 0; s < splits; ++s) m = fmaxf(m, pp[s * (RP + 2)]);
-  float l = 0.0f, o = 0.0f;
-  for (int s = 0; s < splits; ++s) {
-    const float* q = pp + s * (RP + 2);
-    const float w = q[1] > 0.0f ? exp2f(q[0] - m) : 0.0f;  // empty chunks carry l = 0
-    l = fmaf(w, q[1], l);
-    o = fmaf(w, q[2 + c], o);
+  if (splits == 1) return;
+  // the last split CTA of this (sequence, head) merges the partials (in split
+  // order, whichever CTA arrives last) and re-arms the arrival counter
+  __shared__ int last;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    last = atomicAdd(&arrivals[bh], 1u) == static_cast<unsigned>(splits - 1);
   }
-  out[(int64_t)b * ldo + h * RP + c] = __float2bfloat16_rn(o / l);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (tid < RP) {
+    const volatile float* pp = part + (int64_t)bh * splits * (RP + 2);
+    float mm = -INFINITY;
+    for (int sp = 0; sp < splits; ++sp) mm = fmaxf(mm, pp[sp * (RP + 2)]);
+    float l = 0.0f, o = 0.0f;
+    for (int sp = 0; sp < splits; ++sp) {
+      const volatile float* qp = pp + sp * (RP + 2);
+      const float w = qp[1] > 0.0f ? exp2f(qp[0] - mm) : 0.0f;  // empty chunks carry l = 0
+      l = fmaf(w, qp[1], l);
+      o = fmaf(w, qp[2 + tid], o);
+    }
+    out[(int64_t)b * ldo + h * RP + tid] = __float2bfloat16_rn(o / l);
+  }
+  if (tid == 0) arrivals[bh] = 0u;
 }
 
 template <int RP>
 void launch_decode(const DecodeArgs& a, cudaStream_t s) {
   const int bh = a.batch * a.heads;
+  unsigned* arrivals = reinterpret_cast<unsigned*>(a.part + (size_t)bh * a.splits * (RP + 2));
+  if (a.splits > 1) FSVD_CUDA_CHECK(cudaMemsetAsync(arrivals, 0, bh * sizeof(unsigned), s));
   launch_pdl(k_attn_decode<RP>, dim3(bh, a.splits), dim3(kDecThreads), 0, s, a.qkv, a.ldq,
              a.q_off, a.cache, a.max_seq, a.heads, a.groups, a.len, a.splits, a.part, a.out, a.ldo,
-             a.pos_dev);
+             a.pos_dev, arrivals);
   check_launch("k_attn_decode");
-  if (a.splits > 1) {
-    launch_pdl(k_attn_combine<RP>, dim3(bh), dim3(64), 0, s, static_cast<const float*>(a.part),
-               a.heads, a.splits, a.out, a.ldo);
-    check_launch("k_attn_combine");
-  }
 }
 
 __global__ void k_set_int(int* p, int v) { *p = v; }
@@ -237,7 +242,8 @@ int decode_splits(int batch, int heads, int len) {
 
 size_t decode_partial_bytes(int batch, int heads, int rank_pad, int max_len) {
   return (size_t)batch * heads * decode_splits(batch, heads, max_len) * (rank_pad + 2) *
-         sizeof(float);
+             sizeof(float) +
+         (size_t)batch * heads * sizeof(unsigned);  // split arrival counters
 }
 
 void kv_store_bf16(const bf16* src, int64_t lds, int c0, int width, int batch, int rows_per_b,
