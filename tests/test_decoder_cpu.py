@@ -47,3 +47,33 @@ def test_decoder_closed_form_errors():
     # SURVEY cfg2 numbers: 12 layers, B 32, M 512, r 32
     g = abi.Geometry(32, 512, 768, 3072, 12, 12, 32, 12)
     assert _mine(0, g) == (0, 4 * 2 * 12 * 32 * 512 * 32)
+
+
+def test_decoder_entry_points_validate_before_the_device():
+    """Argument errors surface with the reference's kinds before any device
+    work (no GPU needed): zero extents are ShapeErrors, missing arguments
+    ConfigErrors."""
+    import ctypes as C
+    sz = abi._sz
+    b = sz()
+    st = L.fsvd_decoder_prefill(None, 1, 0, 2, 4, None, None, None, 8, None, 0, None)
+    assert st == abi.ERR_SHAPE or st == abi.ERR_CONFIG
+    st = L.fsvd_decoder_prefill(None, 1, 0, 0, 4, None, None, None, 8, None, 0, None)
+    assert st == abi.ERR_SHAPE and b"at least 1" in L.fsvd_last_error()
+    st = L.fsvd_decoder_step(None, 1, 0, 2, 0, None, None, None, 8, None, 0, None)
+    assert st == abi.ERR_CONFIG and b"null" in L.fsvd_last_error()
+    assert L.fsvd_decoder_graph_step(None, 0, None) == abi.ERR_CONFIG
+    assert L.fsvd_kv_cache_bytes(None, 2, 8, C.byref(b)) == abi.ERR_CONFIG
+    assert L.fsvd_decoder_workspace_bytes(None, 1, 2, 8, 0, C.byref(b)) == abi.ERR_CONFIG
+    g = C.c_void_p()
+    st = L.fsvd_decoder_graph_create(None, 1, 0, 2, None, None, None, 8, None, 0, C.byref(g))
+    assert st == abi.ERR_CONFIG
+    L.fsvd_decoder_graph_destroy(None)  # NULL is a no-op
+
+
+def test_factorizer_entry_points_validate_before_the_device():
+    import ctypes as C
+    assert L.fsvd_factor_rank_r_batch(None, 1) == abi.ERR_CONFIG
+    assert L.fsvd_factor_rank_r_batch(None, 0) in (abi.OK, abi.ERR_CUDA)  # empty batch
+    r, pr, fr = abi._sz(0), abi._sz(0), abi._sz(0)
+    assert L.fsvd_factorize_layers(None, 0, 12, r, pr, fr, None) == abi.ERR_CONFIG
