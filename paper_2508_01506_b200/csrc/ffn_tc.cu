@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float* __restrict__ b_up, const float* __restrict__ b_dn, int act, int T,
           int d_model, int d_ff, bf16* __restrict__ z_out, bf16* __restrict__ out,
           const float* __restrict__ ln_g, const float* __restrict__ ln_b, float ln_eps,
-          int split_blocks, float* __restrict__ z_part) {
+          int split_blocks, float* __restrict__ z_part, const bf16* __restrict__ resid) {
   using C = FfnCfg<FR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -465,7 +465,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             ld_chunk(tmem + (q & 1) * QS + loff + c * 32, v);
             const int n0 = q * QS + c * 32;
             bias_act_chunk<32>(v, b_dn + n0, 32, 3);
-            if (grow < T) st_chunk_global(out + (int64_t)grow * d_model + n0, v);
+            if (grow < T) {
+              if (resid) {  // pre-LN layers: out = resid + ffn(x)
+                const uint4* rr = reinterpret_cast<const uint4*>(resid + (int64_t)grow * d_model + n0);
+#pragma unroll
+                for (int q8 = 0; q8 < 4; ++q8) {
+                  const uint4 u = rr[q8];
+                  const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    v[8 * q8 + 2 * e] += __uint_as_float(w4[e] << 16);
+                    v[8 * q8 + 2 * e + 1] += __uint_as_float(w4[e] & 0xffff0000u);
+                  }
+                }
+              }
+              st_chunk_global(out + (int64_t)grow * d_model + n0, v);
+            }
           }
           tc_fence_before();
           mbar_arrive(&bars->o_free[q & 1]);
@@ -509,7 +524,8 @@ void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
   const int splits = (!FUSED && a.split_blocks) ? (nball + a.split_blocks - 1) / a.split_blocks : 1;
   launch_pdl(k_ffn<FR, FUSED>, dim3(grid, splits), dim3(kThreads), C::SMEM, s, tx, tp, tup, tvup,
              tudn, tvdn, ty, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff, a.z_out, a.out,
-             a.ln_g, a.ln_b, a.ln_eps, FUSED ? 0 : a.split_blocks, FUSED ? nullptr : a.z_part);
+             a.ln_g, a.ln_b, a.ln_eps, FUSED ? 0 : a.split_blocks, FUSED ? nullptr : a.z_part,
+             FUSED ? a.resid : nullptr);
   check_launch(FUSED ? "k_ffn_fused" : "k_ffn_stream");
 }
 

@@ -65,7 +65,7 @@ template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const float* __restrict__ bias, int act,
-                int M, int N, int K) {
+                int M, int N, int K, const bf16* __restrict__ resid, int64_t ldr) {
   using Cfg = GemmCfg<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -199,6 +199,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         bias_act_chunk<32>(v, bias != nullptr ? bias + n0 + c0 : nullptr, N - (n0 + c0), act);
+        if (resid != nullptr && m0 + static_cast<int>(row) < M) {  // C = A B^T + bias + R
+          const uint4* rr = reinterpret_cast<const uint4*>(resid + (int64_t)(m0 + row) * ldr + n0 + c0);
+#pragma unroll
+          for (int q8 = 0; q8 < 4; ++q8) {
+            if (n0 + c0 + 8 * q8 >= N) break;
+            const uint4 u = rr[q8];
+            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              v[8 * q8 + 2 * e] += __uint_as_float(w4[e] << 16);
+              v[8 * q8 + 2 * e + 1] += __uint_as_float(w4[e] & 0xffff0000u);
+            }
+          }
+        }
         const uint32_t box = s_c + (nbox % Cfg::NCBOX) * Cfg::CBOX;
         if (nbox >= Cfg::NCBOX) {
           if (et == 0) {
@@ -432,7 +446,8 @@ void launch_gemm2(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* 
 
 template <int BN, int STAGES>
 void launch_gemm(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, int64_t ldc,
-                 int M, int N, int K, const float* bias, int act, cudaStream_t s) {
+                 int M, int N, int K, const float* bias, int act, cudaStream_t s,
+                 const bf16* resid = nullptr, int64_t ldr = 0) {
   using Cfg = GemmCfg<BN, STAGES>;
   static bool attr = false;
   if (!attr) {
@@ -446,7 +461,7 @@ void launch_gemm(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   launch_pdl(k_gemm_bf16<BN, STAGES>, dim3(grid), dim3(kThreads), Cfg::SMEM, s, ta, tb, tc, bias,
-             act, M, N, K);
+             act, M, N, K, resid, ldr);
   check_launch("k_gemm_bf16");
 }
 
@@ -458,43 +473,44 @@ bool gemm_bf16_supported(int M, int N, int K, int64_t lda, int64_t ldb, int64_t 
 }
 
 void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, int64_t ldc,
-               int M, int N, int K, const float* bias, int act, cudaStream_t s) {
+               int M, int N, int K, const float* bias, int act, cudaStream_t s, const bf16* resid,
+               int64_t ldr) {
   static const int variant = [] {
     const char* e = getenv("FSVD_GEMM_VARIANT");  // developer A/B switch
     return e ? atoi(e) : 0;
   }();
-  if (variant == 2 && N % 192 == 0) {
+  if (!resid && variant == 2 && N % 192 == 0) {
     launch_gemm2<192, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
     return;
   }
-  if (variant == 3 && N % 256 == 0) {
+  if (!resid && variant == 3 && N % 256 == 0) {
     launch_gemm2<256, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
     return;
   }
-  if (variant == 5 && N % 128 == 0) {  // single-CTA 128-wide tiles (wave-quantization probe)
-    launch_gemm<128, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+  if (!resid && variant == 5 && N % 128 == 0) {  // single-CTA 128-wide tiles (wave-quantization probe)
+    launch_gemm<128, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
     return;
   }
-  if (variant == 6 && N % 64 == 0) {
-    launch_gemm<64, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+  if (!resid && variant == 6 && N % 64 == 0) {
+    launch_gemm<64, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
     return;
   }
-  if (variant == 4 && N % 128 == 0) {
+  if (!resid && variant == 4 && N % 128 == 0) {
     launch_gemm2<128, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
     return;
   }
   if (M <= 128 && N % 64 == 0 && N >= 128)  // one row tile (decode rows): most CTAs
-    launch_gemm<64, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+    launch_gemm<64, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
   else if (N % 256 == 0)
-    launch_gemm<256, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+    launch_gemm<256, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
   else if (N % 192 == 0)
-    launch_gemm<192, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+    launch_gemm<192, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
   else if (N > 1024)
-    launch_gemm<256, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+    launch_gemm<256, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
   else if (N % 128 == 0 || N > 64)
-    launch_gemm<128, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+    launch_gemm<128, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
   else
-    launch_gemm<64, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s);
+    launch_gemm<64, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
 }
 
 }  // namespace fsvd

@@ -23,8 +23,10 @@ enum Act : int { ACT_GELU_ERF = 0, ACT_GELU_TANH = 1, ACT_RELU = 2, ACT_NONE = 3
 
 // ---- K1: C[M,N] = A[M,K] * B[N,K]^T (+ bias[N]) (act) (+ resid[M,N]) ---------
 // A, B, C, resid bf16 row-major with leading dims; bias fp32 or null.
+// C = A B^T (+ bias) (act) (+ resid, [M, N] with leading dimension ldr)
 void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, int64_t ldc,
-               int M, int N, int K, const float* bias, int act, cudaStream_t s);
+               int M, int N, int K, const float* bias, int act, cudaStream_t s,
+               const bf16* resid = nullptr, int64_t ldr = 0);
 bool gemm_bf16_supported(int M, int N, int K, int64_t lda, int64_t ldb, int64_t ldc);
 
 // ---- K6: y = LN(resid + bf16(A[T,K] * B[N,K]^T + bias)) * gamma + beta --------
@@ -97,6 +99,8 @@ struct FfnTcArgs {
   // Z to z_part[split][T][rank_pad] (z_out unused); sum with z_partial_sum.
   int split_blocks = 0;
   float* z_part = nullptr;
+  // V2 without LN only: out = resid + ffn(x) (pre-LN layers)
+  const bf16* resid = nullptr;
 };
 void ffn_stream_bf16(const FfnTcArgs& a, cudaStream_t s);   // V1 middle: P -> Z
 void z_partial_sum_bf16(const float* part, int splits, int64_t n, bf16* z, cudaStream_t s);

@@ -673,6 +673,43 @@ void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* o
   }
 }
 
+// out = resid + FFN(x) with the residual added in the FFN's last epilogue
+// (pre-LN layers).  Returns false outside the tensor-core flash path.
+bool ffn_resid_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, const void* resid,
+                   void* out, void* trans, cudaStream_t s) {
+  const int T = static_cast<int>(B * M), d = p.d;
+  if (!p.ffn_tc || !(mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2)) return false;
+  if (mode == FSVD_MODE_FLASH_V2 && use_ffn_pair(p, T)) return false;
+  FfnTcArgs a{};
+  a.T = T;
+  a.d_model = d;
+  a.d_ff = p.df;
+  a.rank_pad = p.frp;
+  a.x = as<bf16>(x);
+  a.up_u_t = as<bf16>(p.uup_t);
+  a.up_v_t = as<bf16>(p.vup_t);
+  a.up_b = p.bup;
+  a.dn_u_t = as<bf16>(p.udn_t);
+  a.dn_v_t = as<bf16>(p.vdn_t);
+  a.dn_b = p.bdn;
+  a.act = p.act;
+  a.out = as<bf16>(out);
+  if (mode == FSVD_MODE_FLASH_V2) {
+    a.resid = as<bf16>(resid);
+    ffn_fused_bf16(a, s);
+    return true;
+  }
+  bf16* P = as<bf16>(trans);
+  bf16* Z = P + (size_t)T * p.frp;
+  gemm_bf16(as<bf16>(x), d, a.up_u_t, d, P, p.frp, T, p.frp, d, nullptr, ACT_NONE, s);
+  a.p_in = P;
+  a.z_out = Z;
+  ffn_stream_bf16(a, s);
+  gemm_bf16(Z, p.frp, a.dn_v_t, p.frp, as<bf16>(out), d, T, d, p.frp, p.bdn, ACT_NONE, s,
+            as<bf16>(resid), d);
+  return true;
+}
+
 // out = LN2(x + FFN(x)) with the residual + LayerNorm fused into the FFN's
 // last GEMM (V2: the fused kernel's epilogue; V1: the Z V_down GEMM).
 // Returns false when the shape is outside the fused kernels' range.
@@ -841,6 +878,17 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
     ln(p, x, Bb, p.ln1g, p.ln1b, p.eps1, Bb, rows, s);                // resid  -> B (in place)
     ffn_fwd(p, mode, B, M, Bb, A, trans, s);                          // ffn    -> A
     ln(p, Bb, A, p.ln2g, p.ln2b, p.eps2, out, rows, s);               // out
+  } else if (p.attn_tc && p.out_tc && p.dtype == FSVD_BF16 &&
+             (mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2) &&
+             !(mode == FSVD_MODE_FLASH_V2 && use_ffn_pair(p, T)) && p.ffn_tc) {
+    // pre-LN, tensor-core path: both residual adds ride in GEMM epilogues
+    const int hr = p.H * p.rp;
+    ln(p, x, nullptr, p.ln1g, p.ln1b, p.eps1, A, rows, s);            // normed  -> A
+    tc_attention_rank(p, B, M, A, Bb, trans, s, am);                  // O_rank  -> B
+    gemm_bf16(as<bf16>(Bb), hr, as<bf16>(p.wov_t), hr, as<bf16>(A), p.d, rows, p.d, hr, p.bov,
+              ACT_NONE, s, as<bf16>(x), p.d);                         // x + attn -> A
+    ln(p, A, nullptr, p.ln2g, p.ln2b, p.eps2, Bb, rows, s);           // normed  -> B
+    ffn_resid_fwd(p, mode, B, M, Bb, A, out, trans, s);               // A + ffn -> out
   } else {
     ln(p, x, nullptr, p.ln1g, p.ln1b, p.eps1, A, rows, s);            // normed -> A
     attention_block(p, mode, B, M, A, Bb, A, trans, s, am);           // branch -> A (via B)
