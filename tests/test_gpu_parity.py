@@ -540,3 +540,39 @@ def test_bert_base_r64_twelve_layers_finite(L, ora):
     assert np.abs(z.mean(-1)).max() < 0.05 and np.abs(z.std(-1) - 1).max() < 0.05
     for p in packs:
         L.fsvd_layer_pack_destroy(p)
+
+
+# ------------------------------------------------------------------ randomized layer configs (bf16)
+def test_random_layer_configs_bf16(L, ora):
+    """acceptance.cpp:290-325 style (the reference's 20 random layer configs),
+    on the bf16 policy: random geometry that lands on the tensor-core path
+    (d a multiple of 128 up to 1024, head widths 32/64/128, grouped and
+    per-head, ranks 8-64, out-proj / FFN ranks 64-512 incl. > 384 unfused
+    fallbacks), post- and pre-LN, FFN V1 and V2, ragged sequence lengths --
+    every output within 2e-2 of the oracle fed the same bf16 inputs."""
+    rng = np.random.default_rng(90210)
+    for t in range(12):
+        gd = int(rng.choice([32, 64, 128]))
+        heads = int(rng.choice([2, 4, 8]))
+        d = heads * gd
+        if d % 128:
+            d, heads = 2 * d, 2 * heads
+        groups = int(rng.choice([g for g in range(1, heads + 1) if heads % g == 0]))
+        r = int(rng.choice([8, 16, 32, 64]))
+        r = min(r, d // groups)
+        pr = int(rng.choice([64, 128, 192, 256]))
+        fr = int(rng.choice([64, 128, 256, 384, 512]))
+        df = int(rng.choice([2, 4])) * d
+        fr = min(fr, d, df)
+        pr = min(pr, d)
+        b, m = int(rng.integers(1, 3)), int(rng.integers(1, 260))
+        mode = abi.MODE_FLASH_V1 if t % 3 == 0 else abi.MODE_FLASH_V2
+        pre = bool(t % 4 == 1)
+        layer = oracle.rand_layer(ora, d, df, heads, groups, r, 5000 + 17 * t, proj_rank=pr,
+                                  ffn_rank=fr)
+        x = ora.random((b, m, d), 6000 + t)
+        layer, x = prep(layer, x, abi.BF16)
+        ref = ora.run_model(x, [layer], mode, PLAN, pre)
+        got = H.run_model(x, [layer], mode, PLAN, abi.BF16, pre_ln=pre)
+        err = H.rel_err(got, ref)
+        assert err <= H.TOL_BF16, (t, d, df, heads, groups, r, pr, fr, b, m, mode, pre, err)
