@@ -47,16 +47,21 @@ constexpr int BF = 128;          // features per block
 constexpr int SLOT = BMr * 128;  // one [128 x 64] bf16 SW128 atom / ring slot (16 KB)
 constexpr int STAGE = 2 * SLOT;  // two slots per ring stage
 
-template <int FR>
+// WIDE (K3 only, FFN ranks above 384): Z no longer fits TMEM next to H, so
+// the rank is cut into slices of FR columns, one CTA per (row tile, slice);
+// P is not resident -- MMA1 streams it with V_up as (P atom, V_up atom) slot
+// pairs, and each slice recomputes the hidden block.
+template <int FR, bool WIDE = false>
 struct FfnCfg {
   static_assert(FR % 64 == 0 && FR <= 384, "FR must be a multiple of 64, <= 384");
   static constexpr int NATOM = FR / 64;
   static constexpr int PS = (FR % 128 == 0) ? 128 : 64;  // rows per Z / P piece
   static constexpr int NPIECE = FR / PS;
-  static constexpr int STAGES_FIT = (227 * 1024 - 2048 - (NATOM + 2) * SLOT) / STAGE;
+  static constexpr int PATOMS = WIDE ? 0 : NATOM;        // resident P atoms
+  static constexpr int STAGES_FIT = (227 * 1024 - 2048 - (PATOMS + 2) * SLOT) / STAGE;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int o_p = 0;                  // P / Z tile, NATOM atoms
-  static constexpr int o_h = NATOM * SLOT;       // H tile (2 atoms) / X double buffer
+  static constexpr int o_h = PATOMS * SLOT;      // H tile (2 atoms) / X double buffer
   static constexpr int o_ring = o_h + 2 * SLOT;
   static constexpr int o_bar = o_ring + STAGES * STAGE;
   static constexpr int SMEM = 1024 + o_bar + 512;
@@ -113,7 +118,7 @@ namespace {
 #define TRACE(slot) do { } while (0)
 #endif
 
-template <int FR, bool FUSED>
+template <int FR, bool FUSED, bool WIDE>
 __global__ void __launch_bounds__(kThreads, 1)
     k_ffn(const __grid_constant__ CUtensorMap tmX,    // X [T, d]        box 128x64 (FUSED)
           const __grid_constant__ CUtensorMap tmP,    // P [T, FR]       box 128x64 (V1)
@@ -125,8 +130,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float* __restrict__ b_up, const float* __restrict__ b_dn, int act, int T,
           int d_model, int d_ff, bf16* __restrict__ z_out, bf16* __restrict__ out,
           const float* __restrict__ ln_g, const float* __restrict__ ln_b, float ln_eps,
-          int split_blocks, float* __restrict__ z_part, const bf16* __restrict__ resid) {
-  using C = FfnCfg<FR>;
+          int split_blocks, float* __restrict__ z_part, const bf16* __restrict__ resid,
+          int frk) {
+  static_assert(!(WIDE && FUSED), "wide ranks run the V1 chain");
+  using C = FfnCfg<FR, WIDE>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -136,8 +143,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   // V1 with split_blocks > 0: blockIdx.y streams feature blocks
   // [fb0, fb0 + NB) only and writes an fp32 partial Z (summed by the caller;
   // decode rows use this to spread one row tile's d_ff over many CTAs)
+  // blockIdx.y = split * (frk / FR) + slice: the rank slice [zc0, zc0 + FR)
+  // of a frk-wide P / Z (frk == FR unless WIDE)
+  const int nsl = frk / FR;
+  const int zc0 = static_cast<int>(blockIdx.y % nsl) * FR;
+  const int split = static_cast<int>(blockIdx.y / nsl);
+  const int NK = WIDE ? frk / 64 : C::NATOM;  // K atoms of MMA1
   const int NBall = (d_ff + BF - 1) / BF;
-  const int fb0 = split_blocks ? static_cast<int>(blockIdx.y) * split_blocks : 0;
+  const int fb0 = split_blocks ? split * split_blocks : 0;
   const int NB = split_blocks ? min(split_blocks, NBall - fb0) : NBall;
   const int KC = d_model / 64;                        // X K-chunks (FUSED)
   const bool fuse_ln = FUSED && ln_g != nullptr;     // out = LN2(x + ffn(x)) (ln_epi.cuh)
@@ -208,6 +221,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
       auto mma1_slots = [&](int f) {
+        if (WIDE) {  // (P atom a, V_up atom a) per stage
+          emit(2 * NK, [&](int j, uint8_t* dst, bool size_only) -> uint32_t {
+            if (!size_only) {
+              if (j & 1) tma_load_2d(&tmVup, &bars->full[st], dst, (j >> 1) * 64, (fb0 + f) * BF);
+              else tma_load_2d(&tmP, &bars->full[st], dst, (j >> 1) * 64, m0);
+            }
+            return SLOT;
+          });
+          return;
+        }
         emit(C::NATOM, [&](int a, uint8_t* dst, bool size_only) -> uint32_t {
           if (!size_only) tma_load_2d(&tmVup, &bars->full[st], dst, a * 64, (fb0 + f) * BF);
           return SLOT;
@@ -217,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         emit(2 * C::NPIECE, [&](int j, uint8_t* dst, bool size_only) -> uint32_t {
           const int a = j / C::NPIECE, p = j % C::NPIECE;
           if (!size_only)
-            tma_load_2d(&tmUdn, &bars->full[st], dst, (fb0 + f) * BF + a * 64, p * C::PS);
+            tma_load_2d(&tmUdn, &bars->full[st], dst, (fb0 + f) * BF + a * 64, zc0 + p * C::PS);
           return C::PS * 128;
         });
       };
@@ -234,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             return C::PS * 128;
           });
         }
-      } else {
+      } else if (!WIDE) {
         if (me == 0) mbar_arrive_expect_tx(&bars->p_full, C::NATOM * SLOT);
         for (int a = me; a < C::NATOM; a += 2)
           tma_load_2d(&tmP, &bars->p_full, smem + C::o_p + a * SLOT, a * 64, m0);
@@ -322,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         TRACE(3);
         mbar_wait(&bars->p_ready, 0);
         TRACE(4);
-      } else {
+      } else if (!WIDE) {
         mbar_wait(&bars->p_full, 0);
       }
       tc_fence_after();
@@ -333,9 +356,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
         }
         TRACE(64 + f * 8 + 1);
-        consume(C::NATOM, [&](int a, uint64_t slot) {
-          mma4(tmem + C::t_h, d_p + a * kAtom, slot, idesc_bf16(128, BF), a != 0);
-        });
+        if (WIDE) {
+          uint64_t pa = 0;
+          consume(2 * NK, [&](int j, uint64_t slot) {
+            if (j & 1) mma4(tmem + C::t_h, pa, slot, idesc_bf16(128, BF), j > 1);
+            else pa = slot;
+          });
+        } else {
+          consume(C::NATOM, [&](int a, uint64_t slot) {
+            mma4(tmem + C::t_h, d_p + a * kAtom, slot, idesc_bf16(128, BF), a != 0);
+          });
+        }
         commit(&bars->h_full);
         TRACE(64 + f * 8 + 2);
       };
@@ -432,12 +463,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (grow >= T) continue;
         if (z_part) {
           float4* d = reinterpret_cast<float4*>(
-              z_part + ((int64_t)blockIdx.y * T + grow) * FR + c * 32);
+              z_part + ((int64_t)split * T + grow) * frk + zc0 + c * 32);
 #pragma unroll
           for (int k = 0; k < 8; ++k)
             d[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
         } else {
-          st_chunk_global(z_out + (int64_t)grow * FR + c * 32, v);
+          st_chunk_global(z_out + (int64_t)grow * frk + zc0 + c * 32, v);
         }
       }
     } else {
@@ -497,40 +528,53 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int FR, bool FUSED>
+// FR = Z columns per CTA; frk = a.rank_pad (the P / Z width, K of MMA1).
+template <int FR, bool FUSED, bool WIDE = false>
 void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
-  using C = FfnCfg<FR>;
+  using C = FfnCfg<FR, WIDE>;
   static bool attr = false;
   if (!attr) {
-    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_ffn<FR, FUSED>,
+    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_ffn<FR, FUSED, WIDE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
+  const int frk = a.rank_pad;
   const int boxp = C::PS;
   const int boxd = (a.d_model % 128 == 0) ? 128 : 64;
-  const CUtensorMap tup = tmap_bf16(a.up_u_t, FR, a.d_model, a.d_model, boxp, 64, TmaSwizzle::B128);
-  const CUtensorMap tvup = tmap_bf16(a.up_v_t, a.d_ff, FR, FR, BF, 64, TmaSwizzle::B128);
-  const CUtensorMap tudn = tmap_bf16(a.dn_u_t, FR, a.d_ff, a.d_ff, boxp, 64, TmaSwizzle::B128);
-  const CUtensorMap tvdn = tmap_bf16(a.dn_v_t, a.d_model, FR, FR, FUSED && a.ln_g ? 64 : boxd, 64,
+  const CUtensorMap tup = tmap_bf16(a.up_u_t, frk, a.d_model, a.d_model, boxp, 64, TmaSwizzle::B128);
+  const CUtensorMap tvup = tmap_bf16(a.up_v_t, a.d_ff, frk, frk, BF, 64, TmaSwizzle::B128);
+  const CUtensorMap tudn = tmap_bf16(a.dn_u_t, frk, a.d_ff, a.d_ff, boxp, 64, TmaSwizzle::B128);
+  const CUtensorMap tvdn = tmap_bf16(a.dn_v_t, a.d_model, frk, frk, FUSED && a.ln_g ? 64 : boxd, 64,
                                      TmaSwizzle::B128);
   CUtensorMap tx = tvup, tp = tvup, ty = tvup;
   if (FUSED && a.ln_g) ty = tmap_bf16(a.out, a.T, a.d_model, a.d_model, 128, 64, TmaSwizzle::B128);
   if (FUSED)
     tx = tmap_bf16(a.x, a.T, a.d_model, a.d_model, 128, 64, TmaSwizzle::B128);
   else
-    tp = tmap_bf16(a.p_in, a.T, FR, FR, 128, 64, TmaSwizzle::B128);
+    tp = tmap_bf16(a.p_in, a.T, frk, frk, 128, 64, TmaSwizzle::B128);
   const int grid = (a.T + BMr - 1) / BMr;
   const int nball = (a.d_ff + BF - 1) / BF;
   const int splits = (!FUSED && a.split_blocks) ? (nball + a.split_blocks - 1) / a.split_blocks : 1;
-  launch_pdl(k_ffn<FR, FUSED>, dim3(grid, splits), dim3(kThreads), C::SMEM, s, tx, tp, tup, tvup,
-             tudn, tvdn, ty, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff, a.z_out, a.out,
-             a.ln_g, a.ln_b, a.ln_eps, FUSED ? 0 : a.split_blocks, FUSED ? nullptr : a.z_part,
-             FUSED ? a.resid : nullptr);
+  launch_pdl(k_ffn<FR, FUSED, WIDE>, dim3(grid, splits * (frk / FR)), dim3(kThreads), C::SMEM, s,
+             tx, tp, tup, tvup, tudn, tvdn, ty, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff,
+             a.z_out, a.out, a.ln_g, a.ln_b, a.ln_eps, FUSED ? 0 : a.split_blocks,
+             FUSED ? nullptr : a.z_part, FUSED ? a.resid : nullptr, frk);
   check_launch(FUSED ? "k_ffn_fused" : "k_ffn_stream");
 }
 
 template <bool FUSED>
 void dispatch_ffn(const FfnTcArgs& a, cudaStream_t s) {
+  if (!FUSED && a.rank_pad > 384) {
+    switch (ffn_wide_slice(a.rank_pad)) {
+      case 64: launch_ffn<64, false, true>(a, s); return;
+      case 128: launch_ffn<128, false, true>(a, s); return;
+      case 192: launch_ffn<192, false, true>(a, s); return;
+      case 256: launch_ffn<256, false, true>(a, s); return;
+      case 320: launch_ffn<320, false, true>(a, s); return;
+      case 384: launch_ffn<384, false, true>(a, s); return;
+      default: throw CudaError("ffn: unsupported FFN rank padding");
+    }
+  }
   switch (a.rank_pad) {
     case 64: launch_ffn<64, FUSED>(a, s); break;
     case 128: launch_ffn<128, FUSED>(a, s); break;
@@ -544,9 +588,28 @@ void dispatch_ffn(const FfnTcArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+// Rank padding: multiples of 64 up to 384 (Z resident in TMEM); above that
+// the smallest n * S (S <= 384, a multiple of 64, n slices) covering the rank,
+// fewest slices on ties -- e.g. 512 = 2 x 256, 768 = 2 x 384, 1024 = 4 x 256.
+int ffn_rank_pad(int fr) {
+  const int p64 = (fr + 63) / 64 * 64;
+  if (p64 <= 384) return p64;
+  const int n0 = (fr + 383) / 384;
+  int best = 0;
+  for (int n = n0; n <= n0 + 2; ++n) {
+    const int sl = ((fr + n - 1) / n + 63) / 64 * 64;
+    if (best == 0 || n * sl < best) best = n * sl;
+  }
+  return best;
+}
+int ffn_wide_slice(int rank_pad) {
+  if (rank_pad <= 384) return rank_pad;
+  for (int n = (rank_pad + 383) / 384;; ++n)
+    if (rank_pad % n == 0 && (rank_pad / n) % 64 == 0) return rank_pad / n;
+}
 bool ffn_tc_supported(int d_model, int d_ff, int rank_pad) {
-  return d_model % 64 == 0 && d_ff % 8 == 0 && rank_pad % 64 == 0 && rank_pad <= 384 &&
-         rank_pad >= 64;
+  return d_model % 64 == 0 && d_ff % 8 == 0 && rank_pad % 64 == 0 && rank_pad >= 64 &&
+         rank_pad <= kFfnMaxRankPad && ffn_wide_slice(rank_pad) <= 384;
 }
 
 void ffn_stream_bf16(const FfnTcArgs& a, cudaStream_t s) { dispatch_ffn<false>(a, s); }

@@ -110,6 +110,11 @@ void ffn_fused_bf16(const FfnTcArgs& a, cudaStream_t s);    // V2: X -> out
 void ffn_fused_pair_bf16(const FfnTcArgs& a, cudaStream_t s);
 bool ffn_pair_supported(int d_model, int d_ff, int rank_pad);
 bool ffn_tc_supported(int d_model, int d_ff, int rank_pad);
+// FFN rank padding (ffn_tc.cu): <= 384 -> multiple of 64 (V2 fused / K3 with Z
+// resident); above -> n slices of ffn_wide_slice() columns (K3 only, V1 chain)
+constexpr int kFfnMaxRankPad = 1536;
+int ffn_rank_pad(int fr);
+int ffn_wide_slice(int rank_pad);
 
 // ---- K5: y = LN(a (+ b)) * gamma + beta, rows of width d ---------------------
 void resid_layernorm_bf16(const bf16* a, const bf16* b, const float* gamma, const float* beta,

@@ -266,9 +266,10 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
     p.fr = static_cast<int>(f.up.rank);
     p.df = static_cast<int>(f.up.out_dim);
     p.act = static_cast<int>(f.activation);
-    p.frp = pad_to(p.fr, 64);
+    p.frp = ffn_rank_pad(p.fr);
     const int fr = p.fr, frp = p.frp, df = p.df;
     p.ffn_tc = bf && d % 8 == 0 && df % 8 == 0 && ffn_tc_supported(d, df, frp);
+    p.ffn_wide = p.ffn_tc && frp > 384;
     if (p.ffn_tc) {
       std::vector<float> uu((size_t)frp * d, 0.0f), vu((size_t)df * frp, 0.0f),
           ud((size_t)frp * df, 0.0f), vd((size_t)d * frp, 0.0f);
@@ -368,7 +369,7 @@ size_t op_transient_elems(const Pack& p, int op, int mode) {
     case FSVD_MODE_DENSE: return p.df;
     case FSVD_MODE_NAIVE_LOWRANK: return 2 * fr + p.df;
     case FSVD_MODE_FLASH_V1: return 2 * fr;
-    default: return 0;
+    default: return p.ffn_wide ? 2 * fr : 0;  // wide ranks: V2 stages P and Z
   }
 }
 
@@ -393,7 +394,8 @@ WsLayout ws_layout(const Pack& p, size_t T, int mode, bool pre_ln) {
     const bool ffn_fused = ffn_ln_fusable(p, mode);
     const size_t a_cols = ffn_fused ? static_cast<size_t>(p.H * p.rp) : p.d;
     size_t t_cols = p.qkv_cols;
-    if (mode == FSVD_MODE_FLASH_V1) t_cols = std::max(t_cols, 2 * static_cast<size_t>(p.frp));
+    if (mode == FSVD_MODE_FLASH_V1 || p.ffn_wide)
+      t_cols = std::max(t_cols, 2 * static_cast<size_t>(p.frp));
     if (!ffn_fused) t_cols = std::max(t_cols, op_transient_elems(p, 2, mode));
     return {align256(T * a_cols * p.es), align256(T * p.d * p.es), align256(T * t_cols * p.es)};
   }
@@ -654,7 +656,7 @@ void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* o
     a.dn_b = p.bdn;
     a.act = p.act;
     a.out = as<bf16>(out);
-    if (mode == FSVD_MODE_FLASH_V2) {
+    if (mode == FSVD_MODE_FLASH_V2 && !p.ffn_wide) {
       if (use_ffn_pair(p, T)) ffn_fused_pair_bf16(a, s);
       else ffn_fused_bf16(a, s);
     } else {
@@ -694,7 +696,7 @@ bool ffn_resid_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, c
   a.dn_b = p.bdn;
   a.act = p.act;
   a.out = as<bf16>(out);
-  if (mode == FSVD_MODE_FLASH_V2) {
+  if (mode == FSVD_MODE_FLASH_V2 && !p.ffn_wide) {
     a.resid = as<bf16>(resid);
     ffn_fused_bf16(a, s);
     return true;
@@ -717,7 +719,7 @@ bool ffn_ln_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void
                 void* trans, cudaStream_t s) {
   const int T = static_cast<int>(B * M), d = p.d;
   if (!p.ffn_tc || !gemm_ln_supported(d, p.frp)) return false;
-  if (mode == FSVD_MODE_FLASH_V2) {
+  if (mode == FSVD_MODE_FLASH_V2 && !p.ffn_wide) {
     FfnTcArgs a{};
     a.T = T;
     a.d_model = d;
@@ -739,7 +741,7 @@ bool ffn_ln_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void
     else ffn_fused_bf16(a, s);
     return true;
   }
-  if (mode != FSVD_MODE_FLASH_V1) return false;
+  if (mode != FSVD_MODE_FLASH_V1 && mode != FSVD_MODE_FLASH_V2) return false;
   FfnTcArgs a{};
   a.T = T;
   a.d_model = d;

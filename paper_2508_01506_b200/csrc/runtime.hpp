@@ -28,6 +28,7 @@ struct Pack {
   int rp = 0, prp = 0, frp = 0;
   bool has_attn = false, has_out = false, has_ffn = false, has_ln = false, dense = false;
   bool attn_tc = false, out_tc = false, ffn_tc = false;
+  bool ffn_wide = false;  // frp > 384: sliced K3, V2 runs the V1 chain (ffn_tc.cu)
   void* mem = nullptr;
   size_t bytes = 0;
   // attention, tensor-core path (folded rank-space form, see attn_tc.cu):

@@ -66,6 +66,23 @@ def test_causal_prefill_equals_prefix_encoder(L, ora, pre_ln):
     dec.close()
 
 
+def test_decode_wide_ffn_rank(L, ora):
+    """FFN rank 512 (> 384: sliced feature stream, split per feature block in
+    decode): prefill + steps equal the causal reference."""
+    import torch
+    layers = _layers(ora, n=1, fr=512, seed=700)
+    B, P, S, d = 2, 60, 6, 256
+    x = bf16_round(ora.random((B, P + S, d), 43))
+    xd = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    dec = Decoder(layers, B, 128, False)
+    pre = dec.prefill(xd[:, :P].contiguous()).float().cpu().numpy()
+    steps = np.stack([dec.step(xd[:, P + k].contiguous()).float().cpu().numpy() for k in range(S)], 1)
+    ref = _causal_ref(ora, x, layers, False)
+    assert H.rel_err(pre, ref[:, :P]) <= H.TOL_BF16
+    assert H.rel_err(steps, ref[:, P:]) <= H.TOL_BF16
+    dec.close()
+
+
 @pytest.mark.parametrize("pre_ln", [False, True])
 def test_decode_steps_equal_prefix_encoder(L, ora, pre_ln):
     """prefill 100 tokens, then 40 single-token steps across the 128 tile

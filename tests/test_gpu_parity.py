@@ -62,6 +62,10 @@ SWEEP = [
     ("cfg4_r8_fr96", 768, 3072, 12, 12, 8, 96, 96, 1, 256),
     ("cfg4_r16_fr192", 768, 3072, 12, 12, 16, 192, 192, 1, 256),
     ("cfg4_r64_fr768", 768, 3072, 12, 12, 64, 768, 768, 1, 256),
+    ("cfg4_r32_fr1024", 768, 3072, 12, 12, 32, 384, 1024, 1, 256),
+    # wide FFN ranks (> 384: sliced K3, ffn_tc.cu WIDE): odd rank, ragged rows
+    ("wide_fr448_ragged", 256, 1024, 4, 4, 32, 64, 448, 2, 130),
+    ("wide_fr640", 512, 2048, 8, 8, 16, 128, 640, 1, 200),
 ]
 
 
@@ -75,6 +79,27 @@ def test_config_sweep_layer_bf16(L, ora, shape, mode):
     ref = ora.run_model(x, [layer], mode, PLAN)
     got = H.run_model(x, [layer], mode, PLAN, abi.BF16)
     assert H.rel_err(got, ref) <= H.TOL_BF16, name
+
+
+@pytest.mark.parametrize("fr,frp,slices", [(384, 384, 1), (448, 512, 2), (512, 512, 2),
+                                           (640, 640, 2), (768, 768, 2), (1024, 1024, 4)])
+def test_wide_ffn_ranks_stay_on_tensor_cores(L, ora, fr, frp, slices):
+    """FFN ranks above 384 keep the bf16 pack on the tensor-core path (rank
+    padded to slices of <= 384 columns) and match the oracle through the
+    fsvd_ffn_fwd boundary in both variants."""
+    layer = oracle.rand_layer(ora, 256, 1024, 4, 4, 16, 91, 64, fr)
+    x = ora.random((1, 150, 256), 92)
+    layer, x = prep(layer, x, abi.BF16)
+    descs = layer_descs([layer])
+    p = C.c_void_p()
+    abi.check(L.fsvd_layer_pack_create(C.byref(descs[0]), abi.BF16, 0, C.byref(p)))
+    assert L.fsvd_layer_pack_uses_tensor_cores(p) == 1
+    L.fsvd_layer_pack_destroy(p)
+    for v in (1, 2):
+        assert H.rel_err(H.ffn(v, x, layer.ffn, PLAN, abi.BF16),
+                         ora.ffn(v, x, layer.ffn, PLAN)) <= H.TOL_BF16, (fr, v)
+
+
 DTYPES = [abi.F32, abi.BF16]
 
 
