@@ -565,6 +565,14 @@ void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
 template <bool FUSED>
 void dispatch_ffn(const FfnTcArgs& a, cudaStream_t s) {
   if (!FUSED && a.rank_pad > 384) {
+    static const bool recompute = [] {
+      const char* e = getenv("FSVD_FFN_WIDE_RECOMPUTE");
+      return e && e[0] == '1';
+    }();
+    if (!recompute && ffn_wide_cluster_supported(a)) {  // ffn_wide_tc.cu
+      ffn_wide_cluster_bf16(a, s);
+      return;
+    }
     switch (ffn_wide_slice(a.rank_pad)) {
       case 64: launch_ffn<64, false, true>(a, s); return;
       case 128: launch_ffn<128, false, true>(a, s); return;

@@ -115,6 +115,10 @@ bool ffn_tc_supported(int d_model, int d_ff, int rank_pad);
 constexpr int kFfnMaxRankPad = 1536;
 int ffn_rank_pad(int fr);
 int ffn_wide_slice(int rank_pad);
+// K3 for rank_pad > 384 on a cluster of rank_pad / slice CTAs sharing each
+// hidden block over DSMEM (ffn_wide_tc.cu); split_blocks must be 0.
+bool ffn_wide_cluster_supported(const FfnTcArgs& a);
+void ffn_wide_cluster_bf16(const FfnTcArgs& a, cudaStream_t s);
 
 // ---- K5: y = LN(a (+ b)) * gamma + beta, rows of width d ---------------------
 void resid_layernorm_bf16(const bf16* a, const bf16* b, const float* gamma, const float* beta,
