@@ -106,6 +106,8 @@ def main():
     ap.add_argument("--cfg", type=int, nargs="+", default=[3, 4])
     ap.add_argument("--out", default=None)
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--batches", default="1,8", help="cfg3 batch sizes")
+    ap.add_argument("--modes", default="v2,v1", help="cfg3 FFN variants")
     args = ap.parse_args()
     import torch
     L = abi.lib()
@@ -113,8 +115,9 @@ def main():
         raise SystemExit("no sm_100 device: " + L.fsvd_last_error().decode())
     rows = []
     if 3 in args.cfg:
-        for B in (1, 8):
-            for mode in (abi.MODE_FLASH_V2, abi.MODE_FLASH_V1):
+        modes = {"v2": abi.MODE_FLASH_V2, "v1": abi.MODE_FLASH_V1}
+        for B in [int(v) for v in args.batches.split(",")]:
+            for mode in [modes[m] for m in args.modes.split(",")]:
                 rows.append(dict(cfg=3, **run(L, torch, 1024, 4096, 16, 32, 512, 512, B, 4096, 24,
                                               mode, args.steps)))
                 print(json.dumps(rows[-1]), flush=True)
