@@ -100,6 +100,18 @@ def test_wide_ffn_ranks_stay_on_tensor_cores(L, ora, fr, frp, slices):
                          ora.ffn(v, x, layer.ffn, PLAN)) <= H.TOL_BF16, (fr, v)
 
 
+@pytest.mark.parametrize("fr,df", [(1024, 200), (640, 392), (576, 1160)])
+def test_wide_ffn_ragged_feature_blocks(L, ora, fr, df):
+    """Wide-rank cluster kernel with fewer hidden blocks than slices
+    (fr 1024 = 4 slices, d_ff 200 = 2 blocks) and ragged last blocks."""
+    layer = oracle.rand_layer(ora, 128, df, 2, 2, 16, 93, 64, fr)
+    x = ora.random((1, 140, 128), 94)
+    layer, x = prep(layer, x, abi.BF16)
+    for v in (1, 2):
+        assert H.rel_err(H.ffn(v, x, layer.ffn, PLAN, abi.BF16),
+                         ora.ffn(v, x, layer.ffn, PLAN)) <= H.TOL_BF16, (fr, df, v)
+
+
 DTYPES = [abi.F32, abi.BF16]
 
 
