@@ -427,6 +427,23 @@ def run_gpu(args):
         sel = mem["flash_v2_mib"] if mode == abi.MODE_FLASH_V2 else mem["flash_v1_mib"]
         mem["reduction_vs_dense"] = round(1 - sel / mem["dense_baseline_mib"], 4)
         mem["reduction_vs_naive_lowrank"] = round(1 - sel / mem["naive_lowrank_baseline_mib"], 4)
+        # the dense-reconstruction GPU baseline measured on this model
+        # (tools/torch_baseline.py, PyTorch bf16 + cuBLAS + SDPA, the same
+        # accounting: allocations above weights and input)
+        ours_above = (ws_for(mode) + T * D * es) / 2**20
+        mem["above_weights_and_input_mib"] = round(ours_above, 1)
+        try:
+            if (B, M) != (BATCH, SEQ):
+                raise ValueError("torch baseline measured at the default shape only")
+            with open(os.path.join(ROOT, "profiles", "r01_torch_gpu_baseline.json")) as f:
+                rows = [json.loads(line) for line in f if line.strip()]
+            tb = next(r for r in rows if r["baseline"] == "torch naive_lowrank")
+            ref_mib = tb["peak_activation_mib_above_weights_and_input"]
+            mem["torch_dense_reconstruction_measured_mib"] = ref_mib
+            mem["reduction_vs_torch_dense_reconstruction"] = round(1 - ours_above / ref_mib, 4)
+            mem["torch_baseline_source"] = "profiles/r01_torch_gpu_baseline.json (B=32, M=512, 12 layers)"
+        except Exception:
+            pass
         mem["meter_transient_mib"] = {
             "flash": round(4 * 3 * G * B * M * R / 2**20, 1),
             "naive_lowrank": round(4 * max(3 * B * M * D, B * M * DF) / 2**20, 1),
