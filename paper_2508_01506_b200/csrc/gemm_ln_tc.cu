@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               const __grid_constant__ CUtensorMap tmY,  // y     [T, N] box 128 x 64
               const float* __restrict__ bias,
               const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
-              bf16* __restrict__ y, int T, int N, int K, int stages) {
+              bf16* __restrict__ y, int T, int N, int K, int stages,
+              bf16* __restrict__ sum_out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // region (both idle once every MMA has completed)
     lnepi::run<PN>(tmem, quad, half, row, N, bias, smem_u32(rring), bars->res_full,
                    bars->res_empty, RS, gamma, beta, eps, &tmY, m0, reinterpret_cast<float*>(sA),
-                   smem_u32(ring), bars->acc_full, bars->acc_empty, 1);
+                   smem_u32(ring), bars->acc_full, bars->acc_empty, 1, 0, sum_out, T);
   }
   if (threadIdx.x == 64) LTRACE(100);
   tc_fence_before();
@@ -229,7 +230,7 @@ bool gemm_ln_supported(int N, int K) {
 
 void gemm_ln_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, const float* bias,
                   const bf16* resid, const float* gamma, const float* beta, float eps, bf16* y,
-                  int T, int N, int K, cudaStream_t s) {
+                  int T, int N, int K, cudaStream_t s, bf16* sum_out) {
   if (!gemm_ln_supported(N, K)) throw CudaError("gemm_ln_bf16: unsupported shape");
   const int KA = K / 64;
   int stages =
@@ -250,7 +251,7 @@ void gemm_ln_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, const 
   const CUtensorMap ty = tmap_bf16(y, T, N, N, BMr, 64, TmaSwizzle::B128);
   const int grid = (T + BMr - 1) / BMr;
   launch_pdl(k_gemm_ln, dim3(grid), dim3(kThreads), smem, s, ta, tb, tr, ty, bias, gamma, beta,
-             eps, y, T, N, K, stages);
+             eps, y, T, N, K, stages, sum_out);
   check_launch("k_gemm_ln");
 }
 

@@ -31,9 +31,11 @@ bool gemm_bf16_supported(int M, int N, int K, int64_t lda, int64_t ldb, int64_t 
 
 // ---- K6: y = LN(resid + bf16(A[T,K] * B[N,K]^T + bias)) * gamma + beta --------
 // One CTA per 128 complete rows; N <= 768, K <= 512, multiples of 64.
+// sum_out (optional, [T, N]): also store the un-normalised resid + A*B^T + bias
+// (the pre-LN residual stream).
 void gemm_ln_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, const float* bias,
                   const bf16* resid, const float* gamma, const float* beta, float eps, bf16* y,
-                  int T, int N, int K, cudaStream_t s);
+                  int T, int N, int K, cudaStream_t s, bf16* sum_out = nullptr);
 bool gemm_ln_supported(int N, int K);
 
 // ---- K2: rank-space FlashSVD attention --------------------------------------

@@ -106,7 +106,8 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
                                     const float* __restrict__ beta, float eps,
                                     const CUtensorMap* tmY, int m0, float* gb_smem,
                                     uint32_t out_stage, uint64_t* acc_full, uint64_t* acc_empty,
-                                    uint32_t bar_id, uint32_t acc_empty_leader = 0) {
+                                    uint32_t bar_id, uint32_t acc_empty_leader = 0,
+                                    bf16* __restrict__ sum_out = nullptr, int rows = 0) {
   static_assert(PN == 64 || PN == 128, "piece width");
   constexpr int CPT = PN / 64;  // 32-column chunks per thread per piece
   const uint32_t loff = (quad * 32) << 16;
@@ -174,6 +175,13 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
         S2 = __ffma2_rn(t, t, S2);
       }
       tmem_st16(tmem + loff + kPark + col / 2, park);
+      if (sum_out != nullptr && m0 + static_cast<int>(row) < rows) {
+        // pre-LN residual stream: the un-normalised sum, as the unfused path stores it
+        uint4* d = reinterpret_cast<uint4*>(sum_out + (int64_t)(m0 + static_cast<int>(row)) * N + col);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          d[k] = make_uint4(park[4 * k], park[4 * k + 1], park[4 * k + 2], park[4 * k + 3]);
+      }
     }
   }
   tmem_st_wait();

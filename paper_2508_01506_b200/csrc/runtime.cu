@@ -401,7 +401,10 @@ WsLayout ws_layout(const Pack& p, size_t T, int mode, bool pre_ln) {
   }
   size_t tr = 0;
   for (int op : {1, 2, 3}) tr = std::max(tr, op_transient_elems(p, op, mode));
-  return {align256(T * p.d * p.es), align256(T * p.d * p.es), align256(T * tr * p.es)};
+  // B also holds the rank-space attention output [T, H*rp] on the pre-LN
+  // tensor-core path (H*rp can exceed d when the rank padding exceeds dh)
+  const size_t b_cols = std::max<size_t>(p.d, p.attn_tc ? static_cast<size_t>(p.H * p.rp) : 0);
+  return {align256(T * p.d * p.es), align256(T * b_cols * p.es), align256(T * tr * p.es)};
 }
 }  // namespace
 
@@ -612,6 +615,16 @@ void simt_ffn_t(const Pack& p, int mode, size_t Tn, const void* x, void* out, vo
 // The CTA-pair FFN (ffn2_tc.cu) is opt-in (FSVD_FFN_PAIR=1): it is correct
 // but measured slower than the single-CTA kernel on cfg2 (113 vs 85 us; see
 // DESIGN.md), so the single-CTA kernel is the default.
+// FSVD_PRE_LN_UNFUSED=1 keeps the pre-LN out-projection and LN2 as separate
+// kernels (comparison runs).
+bool pre_ln_unfused() {
+  static const bool v = [] {
+    const char* e = getenv("FSVD_PRE_LN_UNFUSED");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 bool use_ffn_pair(const Pack& p, int T) {
   static const bool enabled = [] {
     const char* e = getenv("FSVD_FFN_PAIR");
@@ -880,6 +893,18 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
     ln(p, x, Bb, p.ln1g, p.ln1b, p.eps1, Bb, rows, s);                // resid  -> B (in place)
     ffn_fwd(p, mode, B, M, Bb, A, trans, s);                          // ffn    -> A
     ln(p, Bb, A, p.ln2g, p.ln2b, p.eps2, out, rows, s);               // out
+  } else if (p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16 &&
+             mode == FSVD_MODE_FLASH_V2 && !p.ffn_wide && !use_ffn_pair(p, T) &&
+             gemm_ln_supported(p.d, p.H * p.rp) && !pre_ln_unfused()) {
+    // pre-LN, fused: the out-projection epilogue stores the residual stream
+    // s = x + attn (into out) and LN2(s) (into A) in one pass; the FFN adds
+    // its branch onto s in its own epilogue
+    const int hr = p.H * p.rp;
+    ln(p, x, nullptr, p.ln1g, p.ln1b, p.eps1, A, rows, s);            // normed  -> A
+    tc_attention_rank(p, B, M, A, Bb, trans, s, am);                  // O_rank  -> B
+    gemm_ln_bf16(as<bf16>(Bb), hr, as<bf16>(p.wov_t), hr, p.bov, as<bf16>(x), p.ln2g, p.ln2b,
+                 p.eps2, as<bf16>(A), rows, p.d, hr, s, as<bf16>(out));  // LN2 -> A, s -> out
+    ffn_resid_fwd(p, mode, B, M, A, out, out, trans, s);              // s + ffn -> out
   } else if (p.attn_tc && p.out_tc && p.dtype == FSVD_BF16 &&
              (mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2) &&
              !(mode == FSVD_MODE_FLASH_V2 && use_ffn_pair(p, T)) && p.ffn_tc) {

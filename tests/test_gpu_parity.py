@@ -341,6 +341,42 @@ def test_workspace_planner_per_ordering(L, ora):
     L.fsvd_layer_pack_destroy(p)
 
 
+@pytest.mark.parametrize("pre_ln", [0, 1], ids=["post_ln", "pre_ln"])
+def test_model_in_place_equals_out_of_place(L, ora, pre_ln):
+    """fsvd_model_fwd with out == x (the documented in-place use) gives the
+    bits of a separate output buffer, over three layers; the pre-LN schedule
+    stores its residual stream in the output buffer mid-layer."""
+    import torch
+    layers = [round_layer_bf16(oracle.rand_layer(ora, 256, 1024, 4, 4, 32, 80 + i, 64, 128))
+              for i in range(3)]
+    B, M, d = 2, 200, 256
+    descs = layer_descs(layers)
+    packs = []
+    for i in range(3):
+        p = C.c_void_p()
+        abi.check(L.fsvd_layer_pack_create(C.byref(descs[i]), abi.BF16, 0, C.byref(p)))
+        packs.append(p)
+    parr = (C.c_void_p * 3)(*[p.value for p in packs])
+    ws = C.c_size_t()
+    abi.check(L.fsvd_workspace_bytes(parr, 3, B, M, abi.MODE_FLASH_V2, C.byref(ws)))
+    work = torch.empty(ws.value, dtype=torch.uint8, device="cuda")
+    x = torch.from_numpy(bf16_round(ora.random((B, M, d), 81))).cuda().to(torch.bfloat16)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    out = torch.empty_like(x)
+    abi.check(L.fsvd_model_fwd(parr, 3, abi.MODE_FLASH_V2, pre_ln, B, M, C.c_void_p(x.data_ptr()),
+                               C.c_void_p(out.data_ptr()), C.c_void_p(work.data_ptr()), ws.value, s))
+    y = x.clone()
+    abi.check(L.fsvd_model_fwd(parr, 3, abi.MODE_FLASH_V2, pre_ln, B, M, C.c_void_p(y.data_ptr()),
+                               C.c_void_p(y.data_ptr()), C.c_void_p(work.data_ptr()), ws.value, s))
+    torch.cuda.synchronize()
+    assert torch.equal(out, y)
+    ref = H.run_model(x.float().cpu().numpy(), layers, abi.MODE_FLASH_V2, PLAN, abi.BF16,
+                      pre_ln=pre_ln)
+    assert np.array_equal(out.float().cpu().numpy(), ref)
+    for p in packs:
+        L.fsvd_layer_pack_destroy(p)
+
+
 # ------------------------------------------------------------------ full-size properties (cfg2)
 def test_cfg2_full_size_properties(L, ora):
     """BERT-Base B=32 M=512 bf16 (BASELINE configs[1], 2 of the 12 layers):
