@@ -449,8 +449,9 @@ void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_lay
   }
   run_on_device(x, B * M * W, out, B * M * W, dt, ws, *packs[0], nullptr,
                 [&](void* xd, void* od, void* td, cudaStream_t s) {
-                  for (size_t i = 0; i < n_layers; ++i)
-                    layer_fwd(*packs[i], mode, pre_ln, B, M, i == 0 ? xd : od, od, td, ws, s);
+                  std::vector<const Pack*> pp;
+                  for (auto& p : packs) pp.push_back(p.get());
+                  model_layers_fwd(pp.data(), n_layers, mode, pre_ln, B, M, xd, od, td, ws, s);
                 });
   if (meter) meter->note_device(2 * B * M * W * packs[0]->es + ws, pack_bytes);
 }
@@ -733,8 +734,9 @@ fsvd_status fsvd_model_fwd(const fsvd_layer_pack* const* packs, size_t n_layers,
       if (x != out) fail(Kind::Config, "model_fwd with no layers needs x == out or a copy");
       return;
     }
-    for (size_t i = 0; i < n_layers; ++i)
-      layer_fwd(*packs[i]->p, mode, pre_ln != 0, batch, seq, i == 0 ? x : out, out, ws, ws_bytes, s);
+    std::vector<const Pack*> pp;
+    for (size_t i = 0; i < n_layers; ++i) pp.push_back(packs[i]->p);
+    model_layers_fwd(pp.data(), n_layers, mode, pre_ln != 0, batch, seq, x, out, ws, ws_bytes, s);
   });
 }
 
@@ -1117,6 +1119,8 @@ fsvd_status fsvd_model_fwd_stream(const fsvd_layer_pack* const* packs, size_t n_
     const size_t bytes = batch * seq * packs[0]->p->d * packs[0]->p->es;
     cudaStream_t sc = static_cast<cudaStream_t>(stream);
     StreamSet& ss = stream_set();
+    std::vector<const Pack*> pp;
+    for (size_t l = 0; l < n_layers; ++l) pp.push_back(packs[l]->p);
     for (size_t i = 0; i < n_batches; ++i) {
       const int k = static_cast<int>(i & 1);
       // slot k is free once batch i-2 has been copied out of it
@@ -1124,9 +1128,8 @@ fsvd_status fsvd_model_fwd_stream(const fsvd_layer_pack* const* packs, size_t n_
       FSVD_CUDA_CHECK(cudaMemcpyAsync(dev[k], x_host[i], bytes, cudaMemcpyHostToDevice, ss.in));
       FSVD_CUDA_CHECK(cudaEventRecord(ss.h2d[k], ss.in));
       FSVD_CUDA_CHECK(cudaStreamWaitEvent(sc, ss.h2d[k], 0));
-      for (size_t l = 0; l < n_layers; ++l)
-        layer_fwd(*packs[l]->p, mode, pre_ln != 0, batch, seq, dev[k], dev[k], model_ws,
-                  ws_bytes - (static_cast<uint8_t*>(model_ws) - static_cast<uint8_t*>(ws)), sc);
+      model_layers_fwd(pp.data(), n_layers, mode, pre_ln != 0, batch, seq, dev[k], dev[k], model_ws,
+                       ws_bytes - (static_cast<uint8_t*>(model_ws) - static_cast<uint8_t*>(ws)), sc);
       FSVD_CUDA_CHECK(cudaEventRecord(ss.comp[k], sc));
       FSVD_CUDA_CHECK(cudaStreamWaitEvent(ss.out, ss.comp[k], 0));
       FSVD_CUDA_CHECK(cudaMemcpyAsync(out_host[i], dev[k], bytes, cudaMemcpyDeviceToHost, ss.out));

@@ -127,11 +127,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const __grid_constant__ CUtensorMap tmUdn,  // U_dn^T [FR, df] box PSx64
           const __grid_constant__ CUtensorMap tmVdn,  // V_dn^T [d, FR]  box QSx64
           const __grid_constant__ CUtensorMap tmY,    // out [T, d]      box 128x64 (fused LN)
+          const __grid_constant__ CUtensorMap tmR,    // LN residual [T, d] box 128x64 (= X
+                                                      // unless pre-LN chaining)
           const float* __restrict__ b_up, const float* __restrict__ b_dn, int act, int T,
           int d_model, int d_ff, bf16* __restrict__ z_out, bf16* __restrict__ out,
           const float* __restrict__ ln_g, const float* __restrict__ ln_b, float ln_eps,
           int split_blocks, float* __restrict__ z_part, const bf16* __restrict__ resid,
-          int frk) {
+          int frk, bf16* __restrict__ sum_out) {
   static_assert(!(WIDE && FUSED), "wide ranks run the V1 chain");
   using C = FfnCfg<FR, WIDE>;
   extern __shared__ uint8_t smem_raw[];
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (= this tile of X) streams through it as two [128 x 64] boxes.
     if (fuse_ln && lane == 0) {
       mbar_wait(&bars->z_full, 0);
-      lnepi::produce_residual<64>(&tmX, smem + C::o_h, bars->res_full, bars->res_empty, 2,
+      lnepi::produce_residual<64>(&tmR, smem + C::o_h, bars->res_full, bars->res_empty, 2,
                                   d_model, m0);
     }
     __syncwarp();
@@ -486,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         lnepi::run<64>(tmem, quad, half, row, d_model, b_dn, smem_u32(smem + C::o_h),
                        bars->res_full, bars->res_empty, 2, ln_g, ln_b, ln_eps, &tmY, m0,
                        reinterpret_cast<float*>(ring), smem_u32(smem + C::o_h), bars->o_full,
-                       bars->o_free, 1);
+                       bars->o_free, 1, 0, sum_out, T);
       } else {
         for (int q = 0; q < NQ; ++q) {
           mbar_wait(&bars->o_full[q & 1], (q >> 1) & 1);
@@ -546,19 +548,22 @@ void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
   const CUtensorMap tudn = tmap_bf16(a.dn_u_t, frk, a.d_ff, a.d_ff, boxp, 64, TmaSwizzle::B128);
   const CUtensorMap tvdn = tmap_bf16(a.dn_v_t, a.d_model, frk, frk, FUSED && a.ln_g ? 64 : boxd, 64,
                                      TmaSwizzle::B128);
-  CUtensorMap tx = tvup, tp = tvup, ty = tvup;
+  CUtensorMap tx = tvup, tp = tvup, ty = tvup, tr = tvup;
   if (FUSED && a.ln_g) ty = tmap_bf16(a.out, a.T, a.d_model, a.d_model, 128, 64, TmaSwizzle::B128);
-  if (FUSED)
+  if (FUSED) {
     tx = tmap_bf16(a.x, a.T, a.d_model, a.d_model, 128, 64, TmaSwizzle::B128);
-  else
+    tr = a.ln_resid ? tmap_bf16(a.ln_resid, a.T, a.d_model, a.d_model, 128, 64, TmaSwizzle::B128)
+                    : tx;
+  } else
     tp = tmap_bf16(a.p_in, a.T, frk, frk, 128, 64, TmaSwizzle::B128);
   const int grid = (a.T + BMr - 1) / BMr;
   const int nball = (a.d_ff + BF - 1) / BF;
   const int splits = (!FUSED && a.split_blocks) ? (nball + a.split_blocks - 1) / a.split_blocks : 1;
   launch_pdl(k_ffn<FR, FUSED, WIDE>, dim3(grid, splits * (frk / FR)), dim3(kThreads), C::SMEM, s,
-             tx, tp, tup, tvup, tudn, tvdn, ty, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff,
+             tx, tp, tup, tvup, tudn, tvdn, ty, tr, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff,
              a.z_out, a.out, a.ln_g, a.ln_b, a.ln_eps, FUSED ? 0 : a.split_blocks,
-             FUSED ? nullptr : a.z_part, FUSED ? a.resid : nullptr, frk);
+             FUSED ? nullptr : a.z_part, FUSED ? a.resid : nullptr, frk,
+             FUSED && a.ln_g ? a.sum_out : nullptr);
   check_launch(FUSED ? "k_ffn_fused" : "k_ffn_stream");
 }
 

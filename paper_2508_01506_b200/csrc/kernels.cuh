@@ -103,6 +103,10 @@ struct FfnTcArgs {
   float* z_part = nullptr;
   // V2 without LN only: out = resid + ffn(x) (pre-LN layers)
   const bf16* resid = nullptr;
+  // V2 with LN (pre-LN layer chaining): the LN residual is ln_resid instead of
+  // x, and the un-normalised ln_resid + ffn(x) is also stored to sum_out
+  const bf16* ln_resid = nullptr;
+  bf16* sum_out = nullptr;
 };
 void ffn_stream_bf16(const FfnTcArgs& a, cudaStream_t s);   // V1 middle: P -> Z
 void z_partial_sum_bf16(const float* part, int splits, int64_t n, bf16* z, cudaStream_t s);

@@ -857,8 +857,36 @@ void layer_decode(const Pack& p, bool pre_ln, size_t B, const void* x, void* out
 }
 }  // namespace
 
+namespace {
+// The fused pre-LN tensor-core schedule (layer_fwd) applies to this pack.
+bool pre_ln_fused(const Pack& p, int mode, size_t T) {
+  return p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16 &&
+         mode == FSVD_MODE_FLASH_V2 && !p.ffn_wide && !use_ffn_pair(p, static_cast<int>(T)) &&
+         gemm_ln_supported(p.d, p.H * p.rp) && !pre_ln_unfused();
+}
+// Layer p can apply q's LN1 in its FFN epilogue (ln_epi.cuh shape range).
+bool pre_ln_linkable(const Pack& p, const Pack& q, int mode, size_t T) {
+  return pre_ln_fused(p, mode, T) && pre_ln_fused(q, mode, T) && q.d == p.d &&
+         gemm_ln_supported(p.d, p.frp);
+}
+}  // namespace
+
+void model_layers_fwd(const Pack* const* packs, size_t n, int mode, bool pre_ln, size_t B, size_t M,
+                      const void* x, void* out, void* ws, size_t ws_bytes, cudaStream_t s) {
+  bool done = false;
+  for (size_t i = 0; i < n; ++i) {
+    LayerLink lk;
+    lk.ln1_done = done;
+    if (pre_ln && i + 1 < n && pre_ln_linkable(*packs[i], *packs[i + 1], mode, B * M))
+      lk.next = packs[i + 1];
+    layer_fwd(*packs[i], mode, pre_ln, B, M, i == 0 ? x : out, out, ws, ws_bytes, s, AttnMode{}, lk);
+    done = lk.next != nullptr;
+  }
+}
+
 void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const void* x, void* out,
-               void* ws, size_t ws_bytes, cudaStream_t s, const AttnMode& am) {
+               void* ws, size_t ws_bytes, cudaStream_t s, const AttnMode& am,
+               const LayerLink& link) {
   if (am.kind == AttnMode::Decode) {
     if (M != 1) fail(Kind::Config, "a decode step carries one token per sequence");
     if (!(p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16))
@@ -893,18 +921,40 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
     ln(p, x, Bb, p.ln1g, p.ln1b, p.eps1, Bb, rows, s);                // resid  -> B (in place)
     ffn_fwd(p, mode, B, M, Bb, A, trans, s);                          // ffn    -> A
     ln(p, Bb, A, p.ln2g, p.ln2b, p.eps2, out, rows, s);               // out
-  } else if (p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16 &&
-             mode == FSVD_MODE_FLASH_V2 && !p.ffn_wide && !use_ffn_pair(p, T) &&
-             gemm_ln_supported(p.d, p.H * p.rp) && !pre_ln_unfused()) {
+  } else if (pre_ln && pre_ln_fused(p, mode, T)) {
     // pre-LN, fused: the out-projection epilogue stores the residual stream
     // s = x + attn (into out) and LN2(s) (into A) in one pass; the FFN adds
-    // its branch onto s in its own epilogue
+    // its branch onto s in its own epilogue and, when chained, also applies
+    // the next layer's LN1 (into A, where that layer's attention reads it)
     const int hr = p.H * p.rp;
-    ln(p, x, nullptr, p.ln1g, p.ln1b, p.eps1, A, rows, s);            // normed  -> A
+    if (!link.ln1_done) ln(p, x, nullptr, p.ln1g, p.ln1b, p.eps1, A, rows, s);  // normed -> A
     tc_attention_rank(p, B, M, A, Bb, trans, s, am);                  // O_rank  -> B
     gemm_ln_bf16(as<bf16>(Bb), hr, as<bf16>(p.wov_t), hr, p.bov, as<bf16>(x), p.ln2g, p.ln2b,
                  p.eps2, as<bf16>(A), rows, p.d, hr, s, as<bf16>(out));  // LN2 -> A, s -> out
-    ffn_resid_fwd(p, mode, B, M, A, out, out, trans, s);              // s + ffn -> out
+    if (link.next) {
+      FfnTcArgs a{};
+      a.T = rows;
+      a.d_model = p.d;
+      a.d_ff = p.df;
+      a.rank_pad = p.frp;
+      a.x = as<bf16>(A);
+      a.up_u_t = as<bf16>(p.uup_t);
+      a.up_v_t = as<bf16>(p.vup_t);
+      a.up_b = p.bup;
+      a.dn_u_t = as<bf16>(p.udn_t);
+      a.dn_v_t = as<bf16>(p.vdn_t);
+      a.dn_b = p.bdn;
+      a.act = p.act;
+      a.out = as<bf16>(A);                 // next layer's LN1(s + ffn)
+      a.ln_g = link.next->ln1g;
+      a.ln_b = link.next->ln1b;
+      a.ln_eps = link.next->eps1;
+      a.ln_resid = as<bf16>(out);          // s
+      a.sum_out = as<bf16>(out);           // s + ffn: the residual stream
+      ffn_fused_bf16(a, s);
+    } else {
+      ffn_resid_fwd(p, mode, B, M, A, out, out, trans, s);            // s + ffn -> out
+    }
   } else if (p.attn_tc && p.out_tc && p.dtype == FSVD_BF16 &&
              (mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2) &&
              !(mode == FSVD_MODE_FLASH_V2 && use_ffn_pair(p, T)) && p.ffn_tc) {

@@ -109,8 +109,20 @@ struct AttnMode {
   // time, and the split count / partial buffers are sized for max_seq.
   const int* pos_dev = nullptr;
 };
+// Pre-LN layer chaining (model loops): `next` = the following layer, whose
+// LN1 this layer applies in its FFN epilogue (the normalised rows land in the
+// workspace A region); `ln1_done` = this layer's LN1 was applied that way.
+struct LayerLink {
+  const Pack* next = nullptr;
+  bool ln1_done = false;
+};
 void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const void* x, void* out,
-               void* ws, size_t ws_bytes, cudaStream_t s, const AttnMode& am = AttnMode{});
+               void* ws, size_t ws_bytes, cudaStream_t s, const AttnMode& am = AttnMode{},
+               const LayerLink& link = LayerLink{});
+// n layers in place (x -> out, out may equal x), pre-LN layers chained
+// through LayerLink where both sides run the fused schedule.
+void model_layers_fwd(const Pack* const* packs, size_t n, int mode, bool pre_ln, size_t B, size_t M,
+                      const void* x, void* out, void* ws, size_t ws_bytes, cudaStream_t s);
 // Decoder: workspace for prefill of up to max_seq tokens and for decode steps.
 size_t decoder_workspace_bytes(const Pack& p, size_t B, size_t max_seq, bool pre_ln);
 size_t kv_cache_bytes(const Pack& p, size_t B, size_t max_seq);
