@@ -861,7 +861,8 @@ namespace {
 // The fused pre-LN tensor-core schedule (layer_fwd) applies to this pack.
 bool pre_ln_fused(const Pack& p, int mode, size_t T) {
   return p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16 &&
-         mode == FSVD_MODE_FLASH_V2 && !p.ffn_wide && !use_ffn_pair(p, static_cast<int>(T)) &&
+         (mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2) && !p.ffn_wide &&
+         !(mode == FSVD_MODE_FLASH_V2 && use_ffn_pair(p, static_cast<int>(T))) &&
          gemm_ln_supported(p.d, p.H * p.rp) && !pre_ln_unfused();
 }
 // Layer p can apply q's LN1 in its FFN epilogue (ln_epi.cuh shape range).
@@ -931,7 +932,31 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
     tc_attention_rank(p, B, M, A, Bb, trans, s, am);                  // O_rank  -> B
     gemm_ln_bf16(as<bf16>(Bb), hr, as<bf16>(p.wov_t), hr, p.bov, as<bf16>(x), p.ln2g, p.ln2b,
                  p.eps2, as<bf16>(A), rows, p.d, hr, s, as<bf16>(out));  // LN2 -> A, s -> out
-    if (link.next) {
+    if (link.next && mode == FSVD_MODE_FLASH_V1) {
+      // V1: P = A U_up, K3 stream -> Z, then Z V_down + b on the LN kernel:
+      // s + ffn -> out and the next layer's LN1 -> A
+      bf16* P = as<bf16>(trans);
+      bf16* Z = P + (size_t)rows * p.frp;
+      gemm_bf16(as<bf16>(A), p.d, as<bf16>(p.uup_t), p.d, P, p.frp, rows, p.frp, p.d, nullptr,
+                ACT_NONE, s);
+      FfnTcArgs a{};
+      a.T = rows;
+      a.d_model = p.d;
+      a.d_ff = p.df;
+      a.rank_pad = p.frp;
+      a.up_v_t = as<bf16>(p.vup_t);
+      a.up_b = p.bup;
+      a.dn_u_t = as<bf16>(p.udn_t);
+      a.dn_v_t = as<bf16>(p.vdn_t);
+      a.dn_b = p.bdn;
+      a.act = p.act;
+      a.p_in = P;
+      a.z_out = Z;
+      ffn_stream_bf16(a, s);
+      gemm_ln_bf16(Z, p.frp, as<bf16>(p.vdn_t), p.frp, p.bdn, as<bf16>(out), link.next->ln1g,
+                   link.next->ln1b, link.next->eps1, as<bf16>(A), rows, p.d, p.frp, s,
+                   as<bf16>(out));
+    } else if (link.next) {
       FfnTcArgs a{};
       a.T = rows;
       a.d_model = p.d;

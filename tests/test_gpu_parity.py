@@ -158,7 +158,8 @@ def test_four_layer_model_matches_oracle(L, ora, dtype):
     assert H.rel_err(got, ref) <= tol(dtype)
 
 
-def test_pre_ln_chained_model_matches_oracle(L, ora):
+@pytest.mark.parametrize("mode", [abi.MODE_FLASH_V1, abi.MODE_FLASH_V2], ids=["v1", "v2"])
+def test_pre_ln_chained_model_matches_oracle(L, ora, mode):
     """Pre-LN stack: consecutive fused layers apply the next layer's LN1 in the
     FFN epilogue (runtime.cu model_layers_fwd); a wide-rank layer in the middle
     breaks the chain on both sides.  Whole stack against the oracle."""
@@ -166,8 +167,8 @@ def test_pre_ln_chained_model_matches_oracle(L, ora):
     layers = [round_layer_bf16(oracle.rand_layer(ora, 256, 1024, 4, 4, r, 4000 + 31 * i, pr, fr))
               for i, (r, pr, fr) in enumerate(specs)]
     x = bf16_round(ora.random((2, 150, 256), 95))
-    ref = ora.run_model(x, layers, abi.MODE_FLASH_V2, PLAN, pre_ln=True)
-    got = H.run_model(x, layers, abi.MODE_FLASH_V2, PLAN, abi.BF16, pre_ln=True)
+    ref = ora.run_model(x, layers, mode, PLAN, pre_ln=True)
+    got = H.run_model(x, layers, mode, PLAN, abi.BF16, pre_ln=True)
     assert H.rel_err(got, ref) <= H.TOL_BF16, H.rel_err(got, ref)
 
 
