@@ -999,14 +999,21 @@ fsvd_status fsvd_decoder_prefill(const fsvd_layer_pack* const* packs, size_t n_l
     check_decoder_call(packs, n_layers, kv_caches, batch, max_seq);
     if (seq == 0 || seq > max_seq) fail(Kind::Config, "prefill length must lie in [1, max_seq]");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    bool done = false;  // pre-LN chaining as in model_layers_fwd (runtime.cu)
     for (size_t i = 0; i < n_layers; ++i) {
       AttnMode am;
       am.kind = AttnMode::Prefill;
       am.cache = kv_caches[i];
       am.max_seq = max_seq;
       am.pos = 0;
+      LayerLink lk;
+      lk.ln1_done = done;
+      if (pre_ln && i + 1 < n_layers &&
+          pre_ln_link_ok(*packs[i]->p, *packs[i + 1]->p, FSVD_MODE_FLASH_V2, batch * seq))
+        lk.next = packs[i + 1]->p;
       layer_fwd(*packs[i]->p, FSVD_MODE_FLASH_V2, pre_ln != 0, batch, seq, i == 0 ? x : out, out,
-                ws, ws_bytes, s, am);
+                ws, ws_bytes, s, am, lk);
+      done = lk.next != nullptr;
     }
   });
 }

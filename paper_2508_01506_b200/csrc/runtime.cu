@@ -872,6 +872,10 @@ bool pre_ln_linkable(const Pack& p, const Pack& q, int mode, size_t T) {
 }
 }  // namespace
 
+bool pre_ln_link_ok(const Pack& p, const Pack& q, int mode, size_t T) {
+  return pre_ln_linkable(p, q, mode, T);
+}
+
 void model_layers_fwd(const Pack* const* packs, size_t n, int mode, bool pre_ln, size_t B, size_t M,
                       const void* x, void* out, void* ws, size_t ws_bytes, cudaStream_t s) {
   bool done = false;

@@ -123,6 +123,8 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
 // through LayerLink where both sides run the fused schedule.
 void model_layers_fwd(const Pack* const* packs, size_t n, int mode, bool pre_ln, size_t B, size_t M,
                       const void* x, void* out, void* ws, size_t ws_bytes, cudaStream_t s);
+// Whether pre-LN layer p may apply q's LN1 in its FFN epilogue (T rows).
+bool pre_ln_link_ok(const Pack& p, const Pack& q, int mode, size_t T);
 // Decoder: workspace for prefill of up to max_seq tokens and for decode steps.
 size_t decoder_workspace_bytes(const Pack& p, size_t B, size_t max_seq, bool pre_ln);
 size_t kv_cache_bytes(const Pack& p, size_t B, size_t max_seq);
