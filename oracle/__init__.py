@@ -136,6 +136,7 @@ class Reference(_Base):
                                              _P(_sz)]
         L.ref_save_model.argtypes = [C.c_char_p, _P(abi.LayerDesc), _sz]
         L.ref_read_error_offset.argtypes = [C.c_char_p]
+        L.ref_load_model.argtypes = [C.c_char_p, _P(_sz)]
         L.ref_read_error_offset.restype = C.c_longlong
         L.ref_expected_bytes.argtypes = [C.c_int, _P(abi.Geometry)]
         L.ref_expected_bytes.restype = _sz

@@ -283,6 +283,15 @@ int ref_save_model(const char* path, const fsvd_layer_desc* layers, size_t n_lay
     save_model(path, ls);
   });
 }
+// model_io.cpp:268-345 load_model (assemble + EncoderLayer::validate);
+// returns the reference's status and the number of layers assembled.
+int ref_load_model(const char* path, size_t* n_layers) {
+  return guard([&] {
+    std::vector<EncoderLayer> ls = load_model(path);
+    if (n_layers) *n_layers = ls.size();
+  });
+}
+
 // Byte offset of the FormatError the reference reader raises for `path`
 // (-1: the container parsed; -2: another error).
 long long ref_read_error_offset(const char* path) {

@@ -13,6 +13,7 @@
 // downloads.
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <string>
 
@@ -748,7 +749,7 @@ size_t stream_slot_bytes(const fsvd_layer_pack* const* packs, size_t batch, size
 // Internal copy streams and events of the serving loop (one set per thread).
 struct StreamSet {
   cudaStream_t in = nullptr, out = nullptr;
-  cudaEvent_t h2d[2], comp[2], d2h[2];
+  cudaEvent_t h2d[2], comp[2], d2h[2], entry = nullptr;
   int device = -1;
   ~StreamSet() {
     if (in) {
@@ -759,24 +760,31 @@ struct StreamSet {
         cudaEventDestroy(comp[i]);
         cudaEventDestroy(d2h[i]);
       }
+      cudaEventDestroy(entry);
     }
   }
 };
 StreamSet& stream_set() {
-  thread_local StreamSet ss;
+  // one set per (host thread, device): a thread that switches devices keeps
+  // each device's streams instead of leaking them
+  thread_local std::map<int, std::unique_ptr<StreamSet>> sets;
   int dev = 0;
   FSVD_CUDA_CHECK(cudaGetDevice(&dev));
-  if (ss.in == nullptr || ss.device != dev) {
-    FSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&ss.in, cudaStreamNonBlocking));
-    FSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&ss.out, cudaStreamNonBlocking));
+  std::unique_ptr<StreamSet>& slot = sets[dev];
+  if (!slot) {
+    auto ss = std::make_unique<StreamSet>();
+    FSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&ss->in, cudaStreamNonBlocking));
+    FSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&ss->out, cudaStreamNonBlocking));
+    FSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ss->entry, cudaEventDisableTiming));
     for (int i = 0; i < 2; ++i) {
-      FSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ss.h2d[i], cudaEventDisableTiming));
-      FSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ss.comp[i], cudaEventDisableTiming));
-      FSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ss.d2h[i], cudaEventDisableTiming));
+      FSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ss->h2d[i], cudaEventDisableTiming));
+      FSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ss->comp[i], cudaEventDisableTiming));
+      FSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ss->d2h[i], cudaEventDisableTiming));
     }
-    ss.device = dev;
+    ss->device = dev;
+    slot = std::move(ss);
   }
-  return ss;
+  return *slot;
 }
 }  // namespace
 
@@ -1128,6 +1136,12 @@ fsvd_status fsvd_model_fwd_stream(const fsvd_layer_pack* const* packs, size_t n_
     StreamSet& ss = stream_set();
     std::vector<const Pack*> pp;
     for (size_t l = 0; l < n_layers; ++l) pp.push_back(packs[l]->p);
+    // The copy streams start behind everything already queued on the
+    // caller's stream (e.g. a previous call's forward or D2H still using the
+    // same workspace slots).
+    FSVD_CUDA_CHECK(cudaEventRecord(ss.entry, sc));
+    FSVD_CUDA_CHECK(cudaStreamWaitEvent(ss.in, ss.entry, 0));
+    FSVD_CUDA_CHECK(cudaStreamWaitEvent(ss.out, ss.entry, 0));
     for (size_t i = 0; i < n_batches; ++i) {
       const int k = static_cast<int>(i & 1);
       // slot k is free once batch i-2 has been copied out of it

@@ -123,7 +123,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
            const __grid_constant__ CUtensorMap tmVdn,  // V_dn^T [d, FR]  box QS/2 x 64
            const __grid_constant__ CUtensorMap tmY,    // out [T, d]      box 128 x 64 (LN)
            const float* __restrict__ b_up, const float* __restrict__ b_dn, int act, int T,
-           int d_model, int d_ff, bf16* __restrict__ out, const float* __restrict__ ln_g,
+           int d_model, int d_ff, bf16* out, const float* __restrict__ ln_g,
            const float* __restrict__ ln_b, float ln_eps) {
   if (threadIdx.x == 0) TRACE2(0);
   using C = Ffn2Cfg<FR>;

@@ -130,10 +130,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const __grid_constant__ CUtensorMap tmR,    // LN residual [T, d] box 128x64 (= X
                                                       // unless pre-LN chaining)
           const float* __restrict__ b_up, const float* __restrict__ b_dn, int act, int T,
-          int d_model, int d_ff, bf16* __restrict__ z_out, bf16* __restrict__ out,
+          int d_model, int d_ff, bf16* z_out, bf16* out,
           const float* __restrict__ ln_g, const float* __restrict__ ln_b, float ln_eps,
-          int split_blocks, float* __restrict__ z_part, const bf16* __restrict__ resid,
-          int frk, bf16* __restrict__ sum_out) {
+          int split_blocks, float* __restrict__ z_part, const bf16* resid,
+          int frk, bf16* sum_out) {
   static_assert(!(WIDE && FUSED), "wide ranks run the V1 chain");
   using C = FfnCfg<FR, WIDE>;
   extern __shared__ uint8_t smem_raw[];

@@ -78,8 +78,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               const __grid_constant__ CUtensorMap tmY,  // y     [T, N] box 128 x 64
               const float* __restrict__ bias,
               const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
-              bf16* __restrict__ y, int T, int N, int K, int stages,
-              bf16* __restrict__ sum_out) {
+              bf16* y, int T, int N, int K, int stages,
+              bf16* sum_out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));

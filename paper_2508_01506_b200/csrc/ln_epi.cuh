@@ -107,7 +107,7 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
                                     const CUtensorMap* tmY, int m0, float* gb_smem,
                                     uint32_t out_stage, uint64_t* acc_full, uint64_t* acc_empty,
                                     uint32_t bar_id, uint32_t acc_empty_leader = 0,
-                                    bf16* __restrict__ sum_out = nullptr, int rows = 0) {
+                                    bf16* sum_out = nullptr, int rows = 0) {
   static_assert(PN == 64 || PN == 128, "piece width");
   constexpr int CPT = PN / 64;  // 32-column chunks per thread per piece
   const uint32_t loff = (quad * 32) << 16;

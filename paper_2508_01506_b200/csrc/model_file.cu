@@ -149,9 +149,21 @@ class Assembler {
   std::map<std::string, Record> m_;
 };
 
+// EncoderLayer::validate()'s shape checks (encoder.cpp:14-25), same messages.
+void check_vec(const Record& t, size_t n, const char* what) {
+  if (t.shape.size() != 1 || t.numel() != n)
+    fail(Kind::Shape, std::string(what) + ": expected a length-" + std::to_string(n) + " vector");
+}
+
+void check_mat(const Record& t, size_t rows, size_t cols, const char* what) {
+  if (t.shape.size() != 2 || t.shape[0] != rows || t.shape[1] != cols)
+    fail(Kind::Shape, std::string(what) + ": expected shape (" + std::to_string(rows) + ", " +
+                          std::to_string(cols) + ")");
+}
+
+size_t mat_cols(const Record& t) { return t.shape.size() == 2 ? t.shape[1] : 0; }
+
 fsvd_linear_desc linear(Record& u, Record& v, Record& b) {
-  if (u.shape.size() != 2 || v.shape.size() != 2)
-    fail(Kind::Shape, "factor halves must be matrices");
   fsvd_linear_desc d{};
   d.in_dim = u.shape[0];
   d.rank = u.shape[1];
@@ -191,40 +203,123 @@ std::unique_ptr<ModelFile> read_model_file(const std::string& path) {
     ModelFile::Layer& L = mf->layers[i];
     fsvd_layer_desc& d = L.desc;
     d = fsvd_layer_desc{};
+    // model_io.cpp:288-337 (assemble): the same lookups in the same order ...
     d.heads = a.count(p + "heads", "heads");
-    d.ln1_gamma = a.get(p + "ln1.gamma").data.data();
-    d.ln1_beta = a.get(p + "ln1.beta").data.data();
+    Record& g1 = a.get(p + "ln1.gamma");
+    Record& b1 = a.get(p + "ln1.beta");
     d.ln1_eps = a.scalar(p + "ln1.eps");
-    d.ln2_gamma = a.get(p + "ln2.gamma").data.data();
-    d.ln2_beta = a.get(p + "ln2.beta").data.data();
+    Record& g2 = a.get(p + "ln2.gamma");
+    Record& b2 = a.get(p + "ln2.beta");
     d.ln2_eps = a.scalar(p + "ln2.eps");
     const float act = a.scalar(p + "ffn.act");
     if (!(act == 0.0f || act == 1.0f || act == 2.0f || act == 3.0f))
       fail(Kind::Config, "bad activation code in model file");
-    if (!a.has(p + "attn.q.head.0.U") || !a.has(p + "ffn.up.U"))
+    const bool attn_dense = a.has(p + "attn.q.W");
+    if (attn_dense)
+      for (const char* n : {"attn.q.W", "attn.q.b", "attn.k.W", "attn.k.b", "attn.v.W",
+                            "attn.v.b", "attn.out.W", "attn.out.b"})
+        a.get(p + n);
+    const bool attn_fact = a.has(p + "attn.q.head.0.U");
+    size_t G = 0;
+    std::vector<Record*> qkv[3];
+    const char* names[3] = {"q", "k", "v"};
+    Record *ou = nullptr, *ov = nullptr, *ob = nullptr;
+    size_t r = 0;
+    if (attn_fact) {
+      while (a.has(p + "attn.q.head." + std::to_string(G) + ".U")) ++G;
+      for (int m = 0; m < 3; ++m)
+        for (size_t g = 0; g < G; ++g) {
+          const std::string gp = p + "attn." + names[m] + ".head." + std::to_string(g) + ".";
+          qkv[m].push_back(&a.get(gp + "U"));
+          qkv[m].push_back(&a.get(gp + "V"));
+          qkv[m].push_back(&a.get(gp + "b"));
+        }
+      if (qkv[0][0]->shape.size() != 2) fail(Kind::Shape, "attention factor U must be a matrix");
+      r = qkv[0][0]->shape[1];
+      ou = &a.get(p + "attn.out.U");
+      ov = &a.get(p + "attn.out.V");
+      ob = &a.get(p + "attn.out.bias");
+    }
+    const bool ffn_dense = a.has(p + "ffn.in.W");
+    if (ffn_dense)
+      for (const char* n : {"ffn.in.W", "ffn.in.b", "ffn.out.W", "ffn.out.b"}) a.get(p + n);
+    const bool ffn_fact = a.has(p + "ffn.up.U");
+    Record *uu = nullptr, *uv = nullptr, *ub = nullptr, *du = nullptr, *dv = nullptr,
+           *db = nullptr;
+    if (ffn_fact) {
+      uu = &a.get(p + "ffn.up.U");
+      uv = &a.get(p + "ffn.up.V");
+      ub = &a.get(p + "ffn.up.b");
+      du = &a.get(p + "ffn.down.U");
+      dv = &a.get(p + "ffn.down.V");
+      db = &a.get(p + "ffn.down.b");
+    }
+    // ... then EncoderLayer::validate() (encoder.cpp:156-215), check by check.
+    const size_t dm = g1.numel();  // d_model() = ln1.gamma.numel()
+    if (dm == 0) fail(Kind::Shape, "layer norm parameters are empty");
+    check_vec(g1, dm, "ln1.gamma");
+    check_vec(b1, dm, "ln1.beta");
+    check_vec(g2, dm, "ln2.gamma");
+    check_vec(b2, dm, "ln2.beta");
+    if (d.heads == 0 || dm % d.heads != 0) fail(Kind::Config, "heads must divide d_model");
+    if (!attn_dense && !attn_fact) fail(Kind::Config, "layer has no attention weights");
+    if (!ffn_dense && !ffn_fact) fail(Kind::Config, "layer has no FFN weights");
+    if (attn_fact) {
+      if (qkv[0][0]->shape[0] != dm) fail(Kind::Shape, "attention factors d_model mismatch");
+      if (G == 0 || dm % G != 0) fail(Kind::Config, "groups must divide d_model");
+      if (d.heads % G != 0) fail(Kind::Config, "groups must divide heads");
+      const size_t gd = dm / G;
+      for (size_t g = 0; g < G; ++g)
+        for (int m = 0; m < 3; ++m) {
+          check_mat(*qkv[m][3 * g], dm, r, "attention factor U");
+          check_mat(*qkv[m][3 * g + 1], r, gd, "attention factor V");
+          check_vec(*qkv[m][3 * g + 2], gd, "attention factor bias");
+        }
+      const size_t pr = mat_cols(*ou);
+      check_mat(*ou, dm, pr, "out_proj U");
+      check_mat(*ov, pr, dm, "out_proj V");
+      check_vec(*ob, dm, "out_proj bias");
+    }
+    if (attn_dense) {
+      for (const char* n : {"attn.q.W", "attn.k.W", "attn.v.W", "attn.out.W"})
+        check_mat(a.get(p + n), dm, dm, "attention weight");
+      for (const char* n : {"attn.q.b", "attn.k.b", "attn.v.b", "attn.out.b"})
+        check_vec(a.get(p + n), dm, "attention bias");
+    }
+    // d_ff(): the factor's out_dim, else the dense input bias length
+    const size_t df = ffn_fact ? mat_cols(*uv) : a.get(p + "ffn.in.b").numel();
+    if (ffn_fact) {
+      const size_t fr = mat_cols(*uu);
+      if (fr != mat_cols(*du)) fail(Kind::Config, "FFN up/down factor ranks differ");
+      check_mat(*uu, dm, fr, "ffn up U");
+      check_mat(*uv, fr, df, "ffn up V");
+      check_vec(*ub, df, "ffn up bias");
+      check_mat(*du, df, fr, "ffn down U");
+      check_mat(*dv, fr, dm, "ffn down V");
+      check_vec(*db, dm, "ffn down bias");
+    }
+    if (ffn_dense) {
+      check_mat(a.get(p + "ffn.in.W"), dm, df, "ffn input weight");
+      check_vec(a.get(p + "ffn.in.b"), df, "ffn input bias");
+      check_mat(a.get(p + "ffn.out.W"), df, dm, "ffn output weight");
+      check_vec(a.get(p + "ffn.out.b"), dm, "ffn output bias");
+    }
+    if (!attn_fact || !ffn_fact)
       fail(Kind::Config, "layer " + std::to_string(i) +
                              " has no factorized attention / FFN; the device path runs "
                              "factorized layers");
-    size_t G = 0;
-    while (a.has(p + "attn.q.head." + std::to_string(G) + ".U")) ++G;
-    Record& q0 = a.get(p + "attn.q.head.0.U");
-    if (q0.shape.size() != 2) fail(Kind::Shape, "attention factor U must be a matrix");
-    const size_t dm = q0.shape[0], r = q0.shape[1];
-    const char* names[3] = {"q", "k", "v"};
+    d.ln1_gamma = g1.data.data();
+    d.ln1_beta = b1.data.data();
+    d.ln2_gamma = g2.data.data();
+    d.ln2_beta = b2.data.data();
     for (int m = 0; m < 3; ++m)
       for (size_t g = 0; g < G; ++g) {
-        const std::string gp = p + "attn." + names[m] + ".head." + std::to_string(g) + ".";
-        Record& u = a.get(gp + "U");
-        Record& v = a.get(gp + "V");
-        Record& b = a.get(gp + "b");
-        if (u.shape.size() != 2 || u.shape[0] != dm || u.shape[1] != r)
-          fail(Kind::Shape, gp + "U: expected shape (d, r)");
-        if (v.shape.size() != 2 || v.shape[0] != r || v.shape[1] * G != dm)
-          fail(Kind::Shape, gp + "V: expected shape (r, d/groups)");
-        if (b.numel() * G != dm) fail(Kind::Shape, gp + "b: expected d/groups values");
-        L.attn_u.insert(L.attn_u.end(), u.data.begin(), u.data.end());
-        L.attn_v.insert(L.attn_v.end(), v.data.begin(), v.data.end());
-        L.attn_b.insert(L.attn_b.end(), b.data.begin(), b.data.end());
+        // fsvd_attn_desc layout: u [3, G, d, r], v [3, G, r, d/G], bias [3, d]
+        L.attn_u.insert(L.attn_u.end(), qkv[m][3 * g]->data.begin(), qkv[m][3 * g]->data.end());
+        L.attn_v.insert(L.attn_v.end(), qkv[m][3 * g + 1]->data.begin(),
+                        qkv[m][3 * g + 1]->data.end());
+        L.attn_b.insert(L.attn_b.end(), qkv[m][3 * g + 2]->data.begin(),
+                        qkv[m][3 * g + 2]->data.end());
       }
     d.attn.d_model = dm;
     d.attn.groups = G;
@@ -232,14 +327,10 @@ std::unique_ptr<ModelFile> read_model_file(const std::string& path) {
     d.attn.u = L.attn_u.data();
     d.attn.v = L.attn_v.data();
     d.attn.bias = L.attn_b.data();
-    d.out_proj = linear(a.get(p + "attn.out.U"), a.get(p + "attn.out.V"),
-                        a.get(p + "attn.out.bias"));
-    d.ffn.up = linear(a.get(p + "ffn.up.U"), a.get(p + "ffn.up.V"), a.get(p + "ffn.up.b"));
-    d.ffn.down =
-        linear(a.get(p + "ffn.down.U"), a.get(p + "ffn.down.V"), a.get(p + "ffn.down.b"));
+    d.out_proj = linear(*ou, *ov, *ob);
+    d.ffn.up = linear(*uu, *uv, *ub);
+    d.ffn.down = linear(*du, *dv, *db);
     d.ffn.activation = static_cast<fsvd_activation>(static_cast<int>(act));
-    if (a.get(p + "ln1.gamma").numel() != dm || a.get(p + "ln2.gamma").numel() != dm)
-      fail(Kind::Shape, "layer norm parameters must have d_model values");
     validate_layer(d);
   }
   mf->keep = std::make_shared<Assembler>(std::move(a));

@@ -271,9 +271,9 @@ __global__ void __launch_bounds__(256) k_simt_ffn(const T* __restrict__ x, const
 // biased variance (tensor.cpp:88-102).  Rows up to 32*VPL values stay in
 // registers; wider rows take the strided path.
 template <typename T, int VPL>
-__global__ void k_resid_ln(const T* __restrict__ a, const T* __restrict__ b,
+__global__ void k_resid_ln(const T* a, const T* b,
                            const float* __restrict__ gamma, const float* __restrict__ beta,
-                           float eps, T* __restrict__ y, int rows, int d) {
+                           float eps, T* y, int rows, int d) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -333,11 +333,11 @@ __global__ void k_resid_ln(const T* __restrict__ a, const T* __restrict__ b,
 // bf16 fast path: d % 8 == 0 and d <= 32 * 8 * V8; each lane owns V8 16-byte
 // chunks of the row.
 template <int V8>
-__global__ void __launch_bounds__(256) k_resid_ln_bf16x8(const bf16* __restrict__ a,
-                                                       const bf16* __restrict__ b,
+__global__ void __launch_bounds__(256) k_resid_ln_bf16x8(const bf16* a,
+                                                       const bf16* b,
                                                        const float* __restrict__ gamma,
                                                        const float* __restrict__ beta, float eps,
-                                                       bf16* __restrict__ y, int rows, int d) {
+                                                       bf16* y, int rows, int d) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;

@@ -30,9 +30,13 @@ class Decoder:
             abi.check(self.L.fsvd_layer_pack_create(C.byref(descs[i]), abi.BF16, 0, C.byref(p)))
             self.packs.append(p)
         self.parr = (C.c_void_p * len(self.packs))(*[p.value for p in self.packs])
-        cb = abi._sz()
-        abi.check(self.L.fsvd_kv_cache_bytes(self.packs[0], batch, max_seq, C.byref(cb)))
-        self.caches = [torch.zeros(cb.value, dtype=torch.uint8, device="cuda") for _ in layers]
+        # one cache per layer, each sized by its own pack (layers may differ in
+        # groups or rank padding, so a cache sized by layer 0 could be short)
+        self.caches = []
+        for p in self.packs:
+            cb = abi._sz()
+            abi.check(self.L.fsvd_kv_cache_bytes(p, batch, max_seq, C.byref(cb)))
+            self.caches.append(torch.zeros(cb.value, dtype=torch.uint8, device="cuda"))
         self.carr = (C.c_void_p * len(layers))(*[c.data_ptr() for c in self.caches])
         wb = abi._sz()
         abi.check(self.L.fsvd_decoder_workspace_bytes(self.parr, len(self.packs), batch, max_seq,

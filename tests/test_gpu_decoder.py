@@ -83,6 +83,26 @@ def test_decode_wide_ffn_rank(L, ora):
     dec.close()
 
 
+def test_decode_heterogeneous_layer_ranks(L, ora):
+    """Layers with different per-head ranks (16 then 64: the second layer's
+    cache row is 4x wider): every layer's cache is sized from its own pack,
+    so prefill + steps still equal the causal reference."""
+    import torch
+    layers = [round_layer_bf16(oracle.rand_layer(ora, 256, 1024, 4, 4, r, 900 + r, 128, 128))
+              for r in (16, 64)]
+    B, P, S, d = 2, 70, 4, 256
+    x = bf16_round(ora.random((B, P + S, d), 44))
+    xd = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    dec = Decoder(layers, B, 96, False)
+    assert dec.caches[1].numel() == 4 * dec.caches[0].numel()
+    pre = dec.prefill(xd[:, :P].contiguous()).float().cpu().numpy()
+    steps = np.stack([dec.step(xd[:, P + k].contiguous()).float().cpu().numpy() for k in range(S)], 1)
+    ref = _causal_ref(ora, x, layers, False)
+    assert H.rel_err(pre, ref[:, :P]) <= H.TOL_BF16
+    assert H.rel_err(steps, ref[:, P:]) <= H.TOL_BF16
+    dec.close()
+
+
 @pytest.mark.parametrize("pre_ln", [False, True])
 def test_decode_steps_equal_prefix_encoder(L, ora, pre_ln):
     """prefill 100 tokens, then 40 single-token steps across the 128 tile

@@ -512,6 +512,50 @@ def test_stream_serving_loop_matches_device_api(L):
         L.fsvd_layer_pack_destroy(p)
 
 
+def test_stream_serving_back_to_back_calls_without_sync(L):
+    """Two fsvd_model_fwd_stream calls queued with no host sync in between
+    share the workspace slots: the second call's first copies must wait for
+    the first call's forwards and read-backs (the copy streams
+    are ordered after the caller's stream at entry)."""
+    import torch
+    from paper_2508_01506_b200.model import random_layer
+    rng = np.random.default_rng(12)
+    layers = [round_layer_bf16(random_layer(256, 512, 4, 4, 32, 64, 128, rng)) for _ in range(3)]
+    B, M, d, n = 8, 512, 256, 2
+    descs = layer_descs(layers)
+    packs = []
+    for i in range(3):
+        p = C.c_void_p()
+        abi.check(L.fsvd_layer_pack_create(C.byref(descs[i]), abi.BF16, 0, C.byref(p)))
+        packs.append(p)
+    parr = (C.c_void_p * 3)(*[p.value for p in packs])
+    sws, ws = C.c_size_t(), C.c_size_t()
+    abi.check(L.fsvd_stream_workspace_bytes(parr, 3, B, M, abi.MODE_FLASH_V2, C.byref(sws)))
+    abi.check(L.fsvd_workspace_bytes(parr, 3, B, M, abi.MODE_FLASH_V2, C.byref(ws)))
+    work = torch.empty(sws.value, dtype=torch.uint8, device="cuda")
+    g = torch.Generator().manual_seed(5)
+    xs = [torch.randn((B, M, d), generator=g).to(torch.bfloat16).pin_memory() for _ in range(2 * n)]
+    outs = [torch.zeros_like(x).pin_memory() for x in xs]
+    st = torch.cuda.current_stream()
+    for call in range(2):
+        xa = (C.c_void_p * n)(*[x.data_ptr() for x in xs[call * n:(call + 1) * n]])
+        oa = (C.c_void_p * n)(*[o.data_ptr() for o in outs[call * n:(call + 1) * n]])
+        abi.check(L.fsvd_model_fwd_stream(parr, 3, abi.MODE_FLASH_V2, 0, B, M, n, xa, oa,
+                                          C.c_void_p(work.data_ptr()), sws.value,
+                                          C.c_void_p(st.cuda_stream)))
+    st.synchronize()
+    for i in range(2 * n):
+        xd = xs[i].cuda()
+        od = torch.empty_like(xd)
+        abi.check(L.fsvd_model_fwd(parr, 3, abi.MODE_FLASH_V2, 0, B, M, C.c_void_p(xd.data_ptr()),
+                                   C.c_void_p(od.data_ptr()), C.c_void_p(work.data_ptr()), ws.value,
+                                   C.c_void_p(st.cuda_stream)))
+        st.synchronize()
+        assert torch.equal(od.cpu(), outs[i]), i
+    for p in packs:
+        L.fsvd_layer_pack_destroy(p)
+
+
 # ------------------------------------------------------------------ empty inputs
 @pytest.mark.parametrize("shape", [(0, 16, 64), (2, 0, 64)], ids=["batch0", "seq0"])
 def test_empty_inputs_rejected_like_reference(L, ora, reference, shape):

@@ -131,6 +131,91 @@ def test_missing_and_duplicate_tensors(tmp_path, reference):
     assert st == abi.ERR_IO
 
 
+def _records(path):
+    """(name, ndarray) list of an FSVD1 file, in file order."""
+    data = open(path, "rb").read()
+    out, off = [], 12
+    for _ in range(struct.unpack_from("<I", data, 8)[0]):
+        nl = struct.unpack_from("<H", data, off)[0]
+        name = data[off + 2:off + 2 + nl].decode()
+        nd = data[off + 3 + nl]
+        ext = struct.unpack_from(f"<{nd}Q", data, off + 4 + nl)
+        at = off + 4 + nl + 8 * nd
+        n = int(np.prod(ext))
+        out.append((name, np.frombuffer(data, "<f4", n, at).reshape(ext)))
+        off = at + 4 * n
+    return out
+
+
+def _write_records(recs, path):
+    body = b""
+    for name, a in recs:
+        nb = name.encode()
+        body += struct.pack("<H", len(nb)) + nb + bytes([0, a.ndim])
+        body += struct.pack(f"<{a.ndim}Q", *a.shape) + np.ascontiguousarray(a, "<f4").tobytes()
+    with open(path, "wb") as f:
+        f.write(b"FSVD" + struct.pack("<II", 1, len(recs)) + body)
+    return path
+
+
+# EncoderLayer::validate() checks (encoder.cpp:156-221) a file can violate
+# while the container is well formed: the loader must refuse each with the
+# reference's error kind and message instead of reading past a short tensor.
+BAD_SHAPES = [
+    ("ffn_up_bias_short", "layer.0.ffn.up.b", lambda a: a[:1], "ffn up bias"),
+    ("ffn_down_bias_short", "layer.0.ffn.down.b", lambda a: a[:3], "ffn down bias"),
+    ("ln1_beta_short", "layer.0.ln1.beta", lambda a: a[:1], "ln1.beta"),
+    ("ln2_beta_2d", "layer.0.ln2.beta", lambda a: a.reshape(1, -1), "ln2.beta"),
+    ("ln2_gamma_short", "layer.0.ln2.gamma", lambda a: a[:-1], "ln2.gamma"),
+    ("out_bias_short", "layer.0.attn.out.bias", lambda a: a[:1], "out_proj bias"),
+    ("out_v_rank", "layer.0.attn.out.V", lambda a: a[:-1], "out_proj V"),
+    ("up_v_rank", "layer.0.ffn.up.V", lambda a: a[:-1], "ffn up V"),
+    ("down_v_rank", "layer.0.ffn.down.V", lambda a: a[:-1], "ffn down V"),
+    ("down_u_rows", "layer.0.ffn.down.U", lambda a: a[:-1], "ffn down U"),
+    ("attn_bias_short", "layer.0.attn.k.head.1.b", lambda a: a[:-1], "attention factor bias"),
+    ("attn_v_2d_flat", "layer.0.attn.v.head.0.V", lambda a: a.reshape(-1), "attention factor V"),
+    ("attn_u_rank", "layer.0.attn.q.head.1.U", lambda a: a[:, :-1], "attention factor U"),
+]
+
+
+@pytest.mark.parametrize("case,name,edit,what", BAD_SHAPES, ids=[b[0] for b in BAD_SHAPES])
+def test_layer_shape_checks_match_reference(tmp_path, reference, case, name, edit, what):
+    from paper_2508_01506_b200.model import random_layer
+    rng = np.random.default_rng(3)
+    path = _ref_model(tmp_path, reference, [random_layer(32, 64, 4, 2, 4, 8, 8, rng)])
+    recs = [(n, edit(a) if n == name else a) for n, a in _records(path)]
+    assert any(n == name for n, _ in recs)
+    bad = _write_records(recs, str(tmp_path / f"{case}.fsvd"))
+    n = C.c_size_t()
+    ref_st = reference.lib.ref_load_model(bad.encode(), C.byref(n))
+    ref_msg = reference.lib.ref_last_error().decode()
+    st, msg, *_ = _probe(bad)
+    assert ref_st == abi.ERR_SHAPE and what in ref_msg, ref_msg
+    assert (st, msg) == (ref_st, ref_msg)
+
+
+def test_rank_mismatch_is_config_error_like_reference(tmp_path, reference):
+    from paper_2508_01506_b200.model import random_layer
+    rng = np.random.default_rng(4)
+    path = _ref_model(tmp_path, reference, [random_layer(32, 64, 4, 2, 4, 8, 8, rng)])
+    recs = [(n, a[:, :-1] if n == "layer.0.ffn.down.U" else a) for n, a in _records(path)]
+    bad = _write_records(recs, str(tmp_path / "rank.fsvd"))
+    n = C.c_size_t()
+    ref_st = reference.lib.ref_load_model(bad.encode(), C.byref(n))
+    st, msg, *_ = _probe(bad)
+    assert ref_st == abi.ERR_CONFIG
+    assert (st, msg) == (ref_st, reference.lib.ref_last_error().decode())
+
+
+def test_rewritten_model_roundtrips(tmp_path, reference):
+    """_records/_write_records reproduce the reference writer's bytes."""
+    from paper_2508_01506_b200.model import random_layer
+    rng = np.random.default_rng(5)
+    path = _ref_model(tmp_path, reference, [random_layer(32, 64, 4, 2, 4, 8, 8, rng)])
+    again = _write_records(_records(path), str(tmp_path / "again.fsvd"))
+    assert open(path, "rb").read() == open(again, "rb").read()
+
+
 def test_committed_golden_model_assembles():
     st, msg, _, n, g = _probe(os.path.join(HERE, "golden", "tiny_model.fsvd"))
     assert st == abi.OK, msg

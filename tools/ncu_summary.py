@@ -30,6 +30,11 @@ METRICS = {
     "launch__shared_mem_per_block_dynamic": "smem_dynamic",
     "sm__cycles_elapsed.avg.per_second": "sm_clock",
     "lts__t_bytes.sum": "l2_bytes",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu_pipe_pct",
+    "sm__inst_executed_pipe_xu.sum": "xu_inst",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
+    "sm__inst_executed.avg.per_cycle_active": "ipc",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1, "usecond": 1,
          "ms": 1e3, "msecond": 1e3, "nsecond": 1e-3, "hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9}
@@ -76,6 +81,9 @@ def launches(path):
 
 
 def main():
+    if len(sys.argv) < 2 or sys.argv[1] in ("-h", "--help"):
+        print(__doc__)
+        sys.exit(0 if len(sys.argv) >= 2 else 2)
     out = sys.argv[1]
     args = sys.argv[2:]
     res = {"kernels": {}, "launch_list": None}
