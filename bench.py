@@ -2,22 +2,31 @@
 """bench.py -- FlashSVD rank-aware streaming encoder on B200.
 
 Workload (BASELINE.json configs[1]): 12-layer BERT-Base low-rank encoder,
-per-GPU batch 32, seq 512, d=768, 12 heads, FFN 3072, per-head rank 32,
+batch 32 per GPU, seq 512, d=768, 12 heads, FFN 3072, per-head rank 32,
 out-proj / FFN rank 384, bf16, random-init factors (synthetic data).  A step
-is one full 12-layer forward of the batch through fsvd_model_fwd (the C-ABI
-device API).  --gpus N runs N independent batch shards (weak scaling, one
-process per GPU); the only collective is the NCCL gather of the outputs to
-rank 0, timed separately in the e2e leg.
+is one full 12-layer forward of every micro-batch a rank owns through
+fsvd_model_fwd (the C-ABI device API), plus -- with N > 1 -- the NCCL gather
+of the outputs to rank 0 (the path's only exchange).
+
+Multi-GPU: `--gpus N` with no torchrun environment re-launches this script
+as N ranks (`python -m torch.distributed.run --nproc-per-node N`), one
+process per GPU.  The global batch (`--global-batch`, default 32 x N: weak
+scaling; BASELINE configs[4] is `--global-batch 2048`) is split
+contiguously by `shard.shard_range`; each rank runs its shard in micro-batches
+of `--batch` sequences.
 
 Prints ONE JSON line on rank 0.  `--impl reference` times the reference CPU
-implementation (oracle/_ref, the unmodified reference library) instead.
+implementation (oracle/_ref, the unmodified reference library compiled from
+its sources) on the host cores instead.
 """
 from __future__ import annotations
 
 import argparse
 import ctypes as C
 import json
+import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,6 +41,7 @@ UNIT = "tokens/s"
 D, DF, H, G, R, PR, FR, LAYERS = 768, 3072, 12, 12, 32, 384, 384, 12
 BATCH, SEQ = 32, 512
 MODE_NAMES = {2: "flash_v1", 3: "flash_v2", 0: "dense", 1: "naive_lowrank"}
+WEIGHT_SEED = 1234  # identical model on every rank and in the reference arm
 
 
 def algorithmic_flops_per_token_layer(d=D, df=DF, g=G, r=R, pr=PR, fr=FR, m=SEQ):
@@ -48,6 +58,40 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def config_block(args, ws):
+    """The `config` object both arms print (the workload the metric is quoted on)."""
+    gb = global_batch(args, ws)
+    return {"workload": f"BERT-Base low-rank encoder, {args.layers} layers, global batch {gb} "
+                        f"({args.batch}/GPU micro-batches), seq {args.seq}, d={D}, H={H}, d_ff={DF}, "
+                        f"r={R}, pr=fr={PR}, {MODE_NAMES[args.mode]}",
+            "batch_per_gpu": args.batch, "global_batch": gb, "seq_len": args.seq,
+            "layers": args.layers, "mode": MODE_NAMES[args.mode],
+            "parallelism": f"batch-shard x{ws}" + (" + NCCL output gather to rank 0" if ws > 1 else ""),
+            "l2": "flushed (256 MiB write) between timed steps"}
+
+
+def global_batch(args, ws):
+    return args.global_batch if args.global_batch else args.batch * ws
+
+
+# --------------------------------------------------------------------------- launcher
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(n):
+    """One process per GPU: re-exec this script under torch.distributed.run
+    with the same arguments; rank 0's JSON line reaches our stdout."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 class Clocks:
@@ -131,93 +175,145 @@ def load_ncu_traffic(prefix):
         for name, k in s.get("kernels", {}).items():
             if name.startswith(prefix) and "dram_bytes_read" in k:
                 return {"bytes": int(k["dram_bytes_read"] + k.get("dram_bytes_write", 0)),
+                        "read": int(k["dram_bytes_read"]), "write": int(k.get("dram_bytes_write", 0)),
                         "source": os.path.relpath(path, ROOT), "kernel": name}
     return None
 
 
 # --------------------------------------------------------------------------- reference arm
+class ReferenceSample:
+    """The reference CPU implementation (oracle/_ref: the unmodified reference
+    library; the C restatement when it was not built) on a bounded sample of
+    the bench workload: one sample = ONE layer of the same 12-layer model
+    (layers taken in turn, so every layer is exercised) on `batch` sequences
+    of length 512, through the reference's run_model (encoder.cpp:262-293)
+    with every host thread.  Every layer has the same shape, so a 12-layer
+    forward costs 12 samples: tokens/s = batch * 512 / (12 * sample time)."""
+
+    def __init__(self, mode, batch, layers=LAYERS, seq=SEQ):
+        import numpy as np
+        import oracle
+        from paper_2508_01506_b200 import abi
+        from paper_2508_01506_b200.model import random_layer
+        if not oracle.Reference.available():
+            try:
+                oracle.build(ref=True)
+            except Exception:
+                pass
+        if oracle.Reference.available():
+            self.chk, self.kind = oracle.Reference(), "reference"
+        else:
+            self.chk, self.kind = oracle.Restatement(), "port"
+        self.cores = os.cpu_count() or 1
+        os.environ["FLASHSVD_THREADS"] = str(self.cores)
+        rng = np.random.default_rng(WEIGHT_SEED)
+        self.layers = [random_layer(D, DF, H, G, R, PR, FR, rng) for _ in range(layers)]
+        self.x = np.random.default_rng(7).standard_normal((batch, seq, D)).astype(np.float32)
+        self.plan = abi.TilePlan(16, 16, 32, 1 << 20)
+        self.mode, self.batch, self.seq, self.n = mode, batch, seq, 0
+
+    def run(self):
+        """One sample; returns its wall time in seconds."""
+        layer = self.layers[self.n % len(self.layers)]
+        self.n += 1
+        t0 = time.perf_counter()
+        self.chk.run_model(self.x, [layer], self.mode, self.plan)
+        return time.perf_counter() - t0
+
+    def tokens_per_s(self, t_sample):
+        return self.batch * self.seq / (len(self.layers) * t_sample)
+
+    def describe(self, n_samples):
+        return (f"{n_samples} samples; one sample = 1 of the {len(self.layers)} layers (in turn) on "
+                f"{self.batch} x {self.seq} tokens through the reference run_model "
+                f"{MODE_NAMES[self.mode]} with {self.cores} threads; tokens/s of the "
+                f"{len(self.layers)}-layer forward = {self.batch}*{self.seq} / "
+                f"({len(self.layers)} * sample time)")
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    import numpy as np
-    import oracle
-    from paper_2508_01506_b200 import abi
-    from paper_2508_01506_b200.model import random_layer
-
-    if not oracle.Reference.available():
-        try:
-            oracle.build(ref=True)
-        except Exception:
-            pass
-    if oracle.Reference.available():
-        chk, kind = oracle.Reference(), "reference"
-    else:
-        chk, kind = oracle.Restatement(), "port"
-    cores = os.cpu_count() or 1
-    os.environ["FLASHSVD_THREADS"] = str(cores)
-    rng = np.random.default_rng(0)
-    layer = random_layer(D, DF, H, G, R, PR, FR, rng)
-    sample_b = args.ref_batch
-    x = rng.standard_normal((sample_b, SEQ, D), np.float32)
-    plan = abi.TilePlan(16, 16, 32, 1 << 20)
-    mode = args.mode
-    for _ in range(min(args.warmup, 1)):
-        chk.run_model(x, [layer], mode, plan)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        chk.run_model(x, [layer], mode, plan)
-        times.append(time.perf_counter() - t0)
-    t_layer = sum(times) / len(times)
-    tok_s = sample_b * SEQ / (LAYERS * t_layer)
+    ref = ReferenceSample(args.mode, args.ref_batch, args.layers, args.seq)
+    for _ in range(args.warmup):
+        ref.run()
+    times = [ref.run() for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    tok_s = ref.tokens_per_s(t)
+    cpu = {"value": tok_s, "unit": UNIT, "cores": ref.cores if ref.kind == "reference" else 1,
+           "kind": ref.kind, "sample": ref.describe(args.steps)}
     line = {
         "impl": "reference", "metric": METRIC, "value": tok_s, "unit": UNIT, "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_layer * LAYERS * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": f"BERT-Base low-rank encoder, 12 layers, batch {BATCH}, seq {SEQ}, "
-                               f"r={R}, pr=fr={PR}, {MODE_NAMES[mode]}", "batch": BATCH, "seq_len": SEQ,
-                   "layers": LAYERS, "mode": MODE_NAMES[mode]},
-        "cpu_baseline": {"value": tok_s, "unit": UNIT, "cores": int(os.environ["FLASHSVD_THREADS"]),
-                         "kind": kind,
-                         "sample": f"1 layer x batch {sample_b} x seq {SEQ} per step "
-                                   f"(reference run_model, TilePlan{{16,16,32,1MiB}}), scaled x{LAYERS} layers"},
+        "data": "synthetic (random-init SVD factors, N(0,1) activations)",
+        "config": config_block(args, ws),
+        "step": f"one step = one sample (see cpu_baseline.sample); ms_per_step is the measured "
+                f"sample time, value extrapolates it to the {args.layers}-layer forward",
+        "cpu_baseline": cpu,
         "e2e": {"value": tok_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def cpu_baseline_sample(mode):
-    """Reference CPU path on a bounded sample (rank 0, N=1 only)."""
-    import numpy as np
-    import oracle
-    from paper_2508_01506_b200 import abi
-    from paper_2508_01506_b200.model import random_layer
-    if oracle.Reference.available():
-        chk, kind = oracle.Reference(), "reference"
-    else:
-        chk, kind = oracle.Restatement(), "port"
-    cores = os.cpu_count() or 1
-    os.environ["FLASHSVD_THREADS"] = str(cores)
-    rng = np.random.default_rng(1)
-    layer = random_layer(D, DF, H, G, R, PR, FR, rng)
-    b = 2
-    x = rng.standard_normal((b, SEQ, D), np.float32)
-    plan = abi.TilePlan(16, 16, 32, 1 << 20)
-    chk.run_model(x, [layer], mode, plan)  # warm
-    reps, t = 0, 0.0
-    while t < 8.0 and reps < 8:
+def cpu_baseline_sample(args, steps=12, warmup=2):
+    """The reference arm itself (`--impl reference`, same model, same sample)
+    for `steps` samples, run on rank 0 at N=1 in a fresh process: inside the
+    GPU process the reference's large per-call host allocations run measurably
+    slower, and the two CPU numbers must agree."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "LOCAL_WORLD_SIZE")}
+    cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--steps", str(steps),
+           "--warmup", str(warmup), "--mode", str(args.mode), "--ref-batch", str(args.ref_batch),
+           "--layers", str(args.layers), "--seq", str(args.seq), "--batch", str(args.batch)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    if r.returncode != 0 or not lines:
+        raise RuntimeError(f"reference arm failed: rc={r.returncode} {r.stderr[-300:]}")
+    return json.loads(lines[-1])["cpu_baseline"]
+
+
+# --------------------------------------------------------------------------- CPU self-test
+def run_cpu_selftest(args):
+    """The N>1 launcher / shard / gather / max-over-ranks path on CPU (gloo).
+    The per-rank "forward" is a stand-in torch op (the sm_100a kernels need a
+    B200); rank 0 checks that the gathered global batch equals the op applied
+    to the unsharded batch and prints the bench line with `selftest: true`."""
+    import torch
+    import torch.distributed as dist
+    from paper_2508_01506_b200.shard import gather_outputs, shard_range
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    gb = global_batch(args, ws)
+    a, b = shard_range(gb, ws, rank)
+    xg = torch.randn((gb, args.seq, 8), generator=torch.Generator().manual_seed(3))
+
+    def fwd(t):
+        return torch.tanh(t * 1.5 + 0.25)
+
+    times = []
+    for _ in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        chk.run_model(x, [layer], mode, plan)
-        t += time.perf_counter() - t0
-        reps += 1
-    t_layer = t / reps
-    return {"value": b * SEQ / (LAYERS * t_layer), "unit": UNIT, "cores": cores if kind == "reference" else 1,
-            "kind": kind,
-            "sample": f"{reps} x (1 layer, batch {b}, seq {SEQ}) of the same layer shape on the host "
-                      f"CPU, reference run_model {MODE_NAMES[mode]}; tokens/s scaled to {LAYERS} layers"}
+        outs = [fwd(xg[s:min(s + args.batch, b)]) for s in range(a, b, args.batch)]
+        local = torch.cat(outs) if outs else xg[a:a]
+        full = gather_outputs(local, ws, rank, gb)
+        times.append(time.perf_counter() - t0)
+    ms = torch.tensor([1e3 * sum(times[args.warmup:]) / args.steps])
+    if ws > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        assert torch.equal(full, fwd(xg)), "gathered output differs from the unsharded op"
+        print(json.dumps({"metric": METRIC, "value": gb * args.seq / (float(ms) * 1e-3), "unit": UNIT,
+                          "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": float(ms), "selftest": True,
+                          "shards": [list(shard_range(gb, ws, r)) for r in range(ws)],
+                          "config": config_block(args, ws)}), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -228,22 +324,34 @@ def run_gpu(args):
 
     from paper_2508_01506_b200 import abi
     from paper_2508_01506_b200.model import layer_descs, random_layer
+    from paper_2508_01506_b200.shard import shard_range
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    # --dist-path runs the N > 1 code (gather, pipelined e2e) on a 1-rank NCCL
+    # group: the multi-rank path exercised on a single GPU
+    multi = ws > 1 or args.dist_path
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=dev)
+    elif multi:
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{free_port()}", rank=0,
+                                world_size=1, device_id=dev)
     L = abi.lib()
     if not L.fsvd_device_available():
         raise RuntimeError("no usable sm_100 device: " + L.fsvd_last_error().decode())
-    dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     sp = C.c_void_p(stream.cuda_stream)
     B, M = args.batch, args.seq
     T = B * M
     mode = args.mode
+    gb = global_batch(args, ws)
+    s0, s1 = shard_range(gb, ws, rank)
+    micro = [(s, min(s + B, s1)) for s in range(s0, s1, B)]  # this rank's micro-batches
+    n_micro_max = math.ceil(max(b - a for a, b in (shard_range(gb, ws, r) for r in range(ws))) / B)
+    shard_pad = n_micro_max * B  # the gather moves equal-size (padded) shards
 
-    rng = np.random.default_rng(1234)  # identical weights on every rank
+    rng = np.random.default_rng(WEIGHT_SEED)  # identical weights on every rank
     layers = [random_layer(D, DF, H, G, R, PR, FR, rng) for _ in range(args.layers)]
     descs = layer_descs(layers)
     packs = []
@@ -255,204 +363,100 @@ def run_gpu(args):
     assert L.fsvd_layer_pack_uses_tensor_cores(packs[0]) == 1
     wsb = C.c_size_t()
     abi.check(L.fsvd_workspace_bytes_ln(parr, len(packs), B, M, mode, 0, C.byref(wsb)))
+    torch.cuda.synchronize(dev)
     torch.cuda.reset_peak_memory_stats(dev)
     base_alloc = torch.cuda.memory_allocated(dev)
     work = torch.empty(wsb.value, dtype=torch.uint8, device=dev)
     gen = torch.Generator(device=dev)
     gen.manual_seed(100 + rank)
-    x = torch.empty((B, M, D), device=dev, dtype=torch.bfloat16).normal_(generator=gen)
-    out = torch.empty_like(x)
-    act_bytes = torch.cuda.max_memory_allocated(dev) - base_alloc
+    # this rank's shard, resident in HBM: [shard_pad, M, D] (padding rows are
+    # never computed; they keep the gather's shards equal-sized)
+    x = torch.empty((shard_pad, M, D), device=dev, dtype=torch.bfloat16).normal_(generator=gen)
+    out = torch.zeros_like(x)
+    act_bytes = torch.cuda.max_memory_allocated(dev) - base_alloc  # workspace + shard in/out
+    gbufs = [torch.empty_like(out) for _ in range(ws)] if (multi and rank == 0) else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    def fwd(xin, xout):
-        abi.check(L.fsvd_model_fwd(parr, len(packs), mode, 0, B, M, C.c_void_p(xin.data_ptr()),
+    def fwd(i, xin=None, xout=None):
+        a, b = micro[i]
+        xin = x[a - s0:b - s0] if xin is None else xin
+        xout = out[a - s0:b - s0] if xout is None else xout
+        abi.check(L.fsvd_model_fwd(parr, len(packs), mode, 0, b - a, M, C.c_void_p(xin.data_ptr()),
                                    C.c_void_p(xout.data_ptr()), C.c_void_p(work.data_ptr()),
                                    wsb.value, sp))
 
+    def step():
+        for i in range(len(micro)):
+            fwd(i)
+        if multi:  # the output gather to rank 0 (NCCL over NVLink), inside the step
+            dist.gather(out, gbufs, dst=0)
+
     for _ in range(args.warmup):
-        fwd(x, out)
+        step()
     torch.cuda.synchronize(dev)
-    assert torch.isfinite(out.float()).all().item(), "non-finite output"
+    assert torch.isfinite(out[:s1 - s0].float()).all().item(), "non-finite output"
 
     # ---------------- timed region (device-resident inputs) ----------------
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     clocks = Clocks(local)
-    if ws > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize(dev)
     n0 = L.fsvd_kernel_launch_count()
     for i in range(args.steps):
         flush.zero_()  # L2 flush between steps (outside the events)
         evs[i][0].record(stream)
-        fwd(x, out)
+        step()
         evs[i][1].record(stream)
     torch.cuda.synchronize(dev)
     launches = L.fsvd_kernel_launch_count() - n0
-    if ws > 1:
+    if multi:
         dist.barrier()
     clk = clocks.stop()
     ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
     ms_t = torch.tensor([ms], device=dev)
-    if ws > 1:
+    if multi:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    value = ws * T / (ms_max * 1e-3)
+    value = gb * M / (ms_max * 1e-3)
 
-    # ---------------- e2e: pinned host input -> model -> host output ----------------
-    # fsvd_model_fwd_stream: every step copies its batch in from pinned host
-    # memory and its result back out; copies of neighbouring steps overlap the
-    # forward on the library's internal streams.
-    e2e_steps = max(4, args.steps)
-    xh = torch.empty((B, M, D), dtype=torch.bfloat16, pin_memory=True)
-    xh.copy_(x.cpu())
-    ohs = [torch.empty_like(xh, pin_memory=True) for _ in range(2)]
-    xa = (C.c_void_p * e2e_steps)(*([xh.data_ptr()] * e2e_steps))
-    oa = (C.c_void_p * e2e_steps)(*[ohs[i & 1].data_ptr() for i in range(e2e_steps)])
-    sws = C.c_size_t()
-    abi.check(L.fsvd_stream_workspace_bytes(parr, len(packs), B, M, mode, C.byref(sws)))
-    swork = torch.empty(sws.value, dtype=torch.uint8, device=dev)
-
-    def fwd_stream(n):
-        abi.check(L.fsvd_model_fwd_stream(parr, len(packs), mode, 0, B, M, n, xa, oa,
-                                          C.c_void_p(swork.data_ptr()), sws.value, sp))
-    fwd_stream(2)
-    torch.cuda.synchronize(dev)
-    if ws > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    fwd_stream(e2e_steps)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    assert torch.equal(ohs[(e2e_steps - 1) & 1], out.cpu()), "e2e output differs from device run"
-    del swork
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    et = torch.tensor([e2e_ms], device=dev)
     gather_ms = None
-    if ws > 1:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        # output gather to rank 0 over NCCL (the path's only exchange step)
-        bufs = [torch.empty_like(out) for _ in range(ws)] if rank == 0 else None
+    if multi:  # the gather alone, for the breakdown
         dist.barrier()
+        torch.cuda.synchronize(dev)
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)
-        dist.gather(out, bufs, dst=0)
+        for _ in range(5):
+            dist.gather(out, gbufs, dst=0)
         g1.record(stream)
         torch.cuda.synchronize(dev)
-        gather_ms = g0.elapsed_time(g1)
-    e2e_value = ws * T / (float(et.item()) * 1e-3)
+        gt = torch.tensor([g0.elapsed_time(g1) / 5], device=dev)
+        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+        gather_ms = float(gt.item())
+        if rank == 0:  # rank r's shard arrived intact
+            for r in range(ws):
+                a, b = shard_range(gb, ws, r)
+                assert torch.isfinite(gbufs[r][:b - a].float()).all().item()
+            assert torch.equal(gbufs[0], out)
+
+    # ---------------- e2e: pinned host input -> model -> host output ----------------
+    e2e = e2e_single(args, L, parr, packs, x, out, stream, dev) if not multi else \
+        e2e_multi(args, L, parr, packs, x, out, work, wsb.value, stream, dev, ws, rank, gb, micro,
+                  s0, shard_pad)
 
     # ---------------- dominant-kernel roofline (FFN) ----------------
     peaks, peak_src = load_peaks()
-    roof = None
-    if rank == 0:
-        ffn_variant = 2 if mode == abi.MODE_FLASH_V2 else 1
-        resid = torch.randn((B, M, D), device=dev, dtype=torch.float32).to(torch.bfloat16)
-        ffn_out = torch.empty_like(resid)
-        ffn_ws = C.c_size_t(wsb.value)
-        reps = 20
-        for _ in range(3):
-            abi.check(L.fsvd_ffn_fwd(packs[0], ffn_variant, B, M, C.c_void_p(resid.data_ptr()),
-                                     C.c_void_p(ffn_out.data_ptr()), C.c_void_p(work.data_ptr()),
-                                     ffn_ws, sp))
-        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize(dev)
-        k0.record(stream)
-        for _ in range(reps):
-            abi.check(L.fsvd_ffn_fwd(packs[0], ffn_variant, B, M, C.c_void_p(resid.data_ptr()),
-                                     C.c_void_p(ffn_out.data_ptr()), C.c_void_p(work.data_ptr()),
-                                     ffn_ws, sp))
-        k1.record(stream)
-        torch.cuda.synchronize(dev)
-        k_ms = k0.elapsed_time(k1) / reps
-        # sublayer timings (same stream, CUDA events) for the breakdown
-        sub = {}
-        for name, fn in (
-                ("attention_fwd", lambda: L.fsvd_attention_fwd(
-                    packs[0], B, M, C.c_void_p(resid.data_ptr()), C.c_void_p(ffn_out.data_ptr()),
-                    C.c_void_p(work.data_ptr()), ffn_ws, sp)),
-                ("outproj_fwd", lambda: L.fsvd_outproj_fwd(
-                    packs[0], B, M, C.c_void_p(resid.data_ptr()), C.c_void_p(ffn_out.data_ptr()),
-                    C.c_void_p(work.data_ptr()), ffn_ws, sp)),
-                ("layer_fwd", lambda: L.fsvd_layer_fwd(
-                    packs[0], mode, 0, B, M, C.c_void_p(resid.data_ptr()),
-                    C.c_void_p(ffn_out.data_ptr()), C.c_void_p(work.data_ptr()), ffn_ws, sp))):
-            for _ in range(2):
-                abi.check(fn())
-            torch.cuda.synchronize(dev)
-            k0.record(stream)
-            for _ in range(reps):
-                abi.check(fn())
-            k1.record(stream)
-            torch.cuda.synchronize(dev)
-            sub[name] = round(k0.elapsed_time(k1) / reps, 4)
-        sub["ffn_fwd"] = round(k_ms, 4)
-        flops = T * ffn_flops_per_token()
-        achieved = flops / (k_ms * 1e-3) / 1e12
-        peak = peaks.get("bf16_tflops", SURVEY_PEAKS["bf16_tflops"])
-        kname = "k_ffn_fused" if ffn_variant == 2 else "k_ffn_stream+k_gemm_bf16"
-        tr = load_ncu_traffic("k_ffn<")
-        traffic = tr["bytes"] if tr else None
-        roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": kname, "kernel_ms": round(k_ms, 4),
-                "algorithmic_flop_per_launch": flops, "sublayer_ms": sub,
-                "traffic_source": tr,
-                "peak_source": f"{peak_src}: burst bf16 (kernel timed alone)",
-                "model_frac_of_sustained": round(
-                    T * LAYERS * algorithmic_flops_per_token_layer() / (ms_max * 1e-3) / 1e12
-                    / peaks.get("bf16_tflops_sustained", SURVEY_PEAKS["bf16_tflops_sustained"]), 4)}
+    roof = roofline(args, L, packs, work, wsb, stream, dev, peaks, peak_src, ms_max, gb, ws) \
+        if rank == 0 else None
 
     # ---------------- peak activation memory ----------------
-    mem = {}
-    if rank == 0:
-        def ws_for(m, dense=False):
-            b = C.c_size_t()
-            if not dense:
-                abi.check(L.fsvd_workspace_bytes_ln(parr, len(packs), B, M, m, 0, C.byref(b)))
-                return b.value
-            return None
-        es = 2
-        io = 2 * T * D * es  # input + output activations
-        mem["flash_v1_mib"] = round((ws_for(abi.MODE_FLASH_V1) + io) / 2**20, 1)
-        mem["flash_v2_mib"] = round((ws_for(abi.MODE_FLASH_V2) + io) / 2**20, 1)
-        # dense-reconstruction baselines (planner bytes of our own dense / naive modes)
-        dense_tr = max(3 * D, DF) * T * es
-        naive_tr = max(3 * G * 32 + 3 * D, PR, 2 * FR + DF) * T * es
-        mem["dense_baseline_mib"] = round((2 * T * D * es + dense_tr + io) / 2**20, 1)
-        mem["naive_lowrank_baseline_mib"] = round((2 * T * D * es + naive_tr + io) / 2**20, 1)
-        mem["measured_torch_peak_mib"] = round(act_bytes / 2**20, 1)
-        sel = mem["flash_v2_mib"] if mode == abi.MODE_FLASH_V2 else mem["flash_v1_mib"]
-        mem["reduction_vs_dense"] = round(1 - sel / mem["dense_baseline_mib"], 4)
-        mem["reduction_vs_naive_lowrank"] = round(1 - sel / mem["naive_lowrank_baseline_mib"], 4)
-        # the dense-reconstruction GPU baseline measured on this model
-        # (tools/torch_baseline.py, PyTorch bf16 + cuBLAS + SDPA, the same
-        # accounting: allocations above weights and input)
-        ours_above = (ws_for(mode) + T * D * es) / 2**20
-        mem["above_weights_and_input_mib"] = round(ours_above, 1)
-        try:
-            if (B, M) != (BATCH, SEQ):
-                raise ValueError("torch baseline measured at the default shape only")
-            with open(os.path.join(ROOT, "profiles", "r01_torch_gpu_baseline.json")) as f:
-                rows = [json.loads(line) for line in f if line.strip()]
-            tb = next(r for r in rows if r["baseline"] == "torch naive_lowrank")
-            ref_mib = tb["peak_activation_mib_above_weights_and_input"]
-            mem["torch_dense_reconstruction_measured_mib"] = ref_mib
-            mem["reduction_vs_torch_dense_reconstruction"] = round(1 - ours_above / ref_mib, 4)
-            mem["torch_baseline_source"] = "profiles/r01_torch_gpu_baseline.json (B=32, M=512, 12 layers)"
-        except Exception:
-            pass
-        mem["meter_transient_mib"] = {
-            "flash": round(4 * 3 * G * B * M * R / 2**20, 1),
-            "naive_lowrank": round(4 * max(3 * B * M * D, B * M * DF) / 2**20, 1),
-            "dense": round(4 * (3 * B * M * D + B * H * M * M) / 2**20, 1)}
+    mem = memory_block(args, L, parr, packs, act_bytes, ws, rank, gbufs) if rank == 0 else {}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline_sample(mode)
+            cpu = cpu_baseline_sample(args)
         except Exception as e:  # report, do not fail the bench
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": str(e)[:200]}
 
@@ -460,18 +464,11 @@ def run_gpu(args):
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "weak" if not args.global_batch else "strong",
+            "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init SVD factors, N(0,1) activations)",
-            "config": {"workload": f"BERT-Base low-rank encoder, {args.layers} layers, batch {B}/GPU, "
-                                   f"seq {M}, d={D}, H={H}, d_ff={DF}, r={R}, pr=fr={PR}, "
-                                   f"{MODE_NAMES[mode]}",
-                       "batch_per_gpu": B, "global_batch": B * ws, "seq_len": M, "layers": args.layers,
-                       "mode": MODE_NAMES[mode], "parallelism": f"batch-shard x{ws}",
-                       "l2": "flushed (256 MiB write) between timed steps"},
-            "e2e": {"value": round(e2e_value, 1), "unit": UNIT,
-                    "h2d_bytes_per_step": T * D * 2, "d2h_bytes_per_step": T * D * 2,
-                    "api": "fsvd_model_fwd_stream (C-ABI): per step, pinned-host bf16 batch in, "
-                           "12-layer forward, result out; copies overlap neighbouring steps"},
+            "config": config_block(args, ws),
+            "e2e": e2e,
             "gpu_launches": int(launches // max(args.steps, 1)) * args.steps,
             "launches_per_step": int(launches // max(args.steps, 1)),
             "roofline": roof,
@@ -479,14 +476,238 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "clocks": clk,
         }
+        if args.dist_path and ws == 1:
+            line["dist_path"] = "N > 1 code path on a 1-rank NCCL group"
         if gather_ms is not None:
             line["gather_ms"] = round(gather_ms, 3)
+            line["gather_bytes_per_step"] = (ws - 1) * shard_pad * M * D * 2
         print(json.dumps(line), flush=True)
     for p in packs:
         L.fsvd_layer_pack_destroy(p)
-    if ws > 1:
+    if multi:
         dist.destroy_process_group()
     return 0
+
+
+def e2e_single(args, L, parr, packs, x, out, stream, dev):
+    """fsvd_model_fwd_stream (the library's serving call): every step copies
+    its batch in from pinned host memory and its result back out; copies of
+    neighbouring steps overlap the forward on the library's internal streams."""
+    import torch
+    from paper_2508_01506_b200 import abi
+    B, M = args.batch, args.seq
+    T = B * M
+    sp = C.c_void_p(stream.cuda_stream)
+    n = max(4, args.steps)
+    xh = torch.empty((B, M, D), dtype=torch.bfloat16, pin_memory=True)
+    xh.copy_(x[:B].cpu())
+    ohs = [torch.empty_like(xh, pin_memory=True) for _ in range(2)]
+    xa = (C.c_void_p * n)(*([xh.data_ptr()] * n))
+    oa = (C.c_void_p * n)(*[ohs[i & 1].data_ptr() for i in range(n)])
+    sws = C.c_size_t()
+    abi.check(L.fsvd_stream_workspace_bytes(parr, len(packs), B, M, args.mode, C.byref(sws)))
+    swork = torch.empty(sws.value, dtype=torch.uint8, device=dev)
+
+    def run(k):
+        abi.check(L.fsvd_model_fwd_stream(parr, len(packs), args.mode, 0, B, M, k, xa, oa,
+                                          C.c_void_p(swork.data_ptr()), sws.value, sp))
+    run(2)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    run(n)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    assert torch.equal(ohs[(n - 1) & 1], out[:B].cpu()), "e2e output differs from device run"
+    ms = e0.elapsed_time(e1) / n
+    return {"value": round(T / (ms * 1e-3), 1), "unit": UNIT,
+            "h2d_bytes_per_step": T * D * 2, "d2h_bytes_per_step": T * D * 2,
+            "ms_per_step": round(ms, 4),
+            "api": "fsvd_model_fwd_stream (C-ABI): per step, pinned-host bf16 batch in, "
+                   "12-layer forward, result out; copies overlap neighbouring steps"}
+
+
+def e2e_multi(args, L, parr, packs, x, out, work, wsb, stream, dev, ws, rank, gb, micro, s0,
+              shard_pad):
+    """N > 1 serving loop: per step every rank copies its shard in from pinned
+    host memory, runs the 12-layer forward (fsvd_model_fwd), the outputs are
+    gathered to rank 0 over NCCL, and rank 0 copies the global batch back to
+    pinned host memory.  Two slots: step i's H2D, forward, gather and D2H
+    overlap steps i-1 / i+1 on separate streams."""
+    import torch
+    import torch.distributed as dist
+    from paper_2508_01506_b200 import abi
+    M = args.seq
+    sp = C.c_void_p(stream.cuda_stream)
+    n = max(4, args.steps)
+    xh = torch.empty_like(x, device="cpu").pin_memory()
+    xh.copy_(x.cpu())
+    xd = [torch.empty_like(x) for _ in range(2)]
+    od = [torch.empty_like(x) for _ in range(2)]
+    gbuf = [[torch.empty_like(x) for _ in range(ws)] for _ in range(2)] if rank == 0 else None
+    oh = [[torch.empty_like(xh).pin_memory() for _ in range(ws)] for _ in range(2)] if rank == 0 else None
+    s_in, s_comm, s_out = (torch.cuda.Stream(dev) for _ in range(3))
+    ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "fwd", "gat", "out")}
+
+    def fwd_all(xin, xout):
+        for a, b in micro:
+            abi.check(L.fsvd_model_fwd(parr, len(packs), args.mode, 0, b - a, M,
+                                       C.c_void_p(xin[a - s0].data_ptr()),
+                                       C.c_void_p(xout[a - s0].data_ptr()),
+                                       C.c_void_p(work.data_ptr()), wsb, sp))
+
+    def loop(k_steps):
+        for i in range(k_steps):
+            k = i & 1
+            with torch.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(ev["fwd"][k])  # xd[k] free once forward i-2 is done
+                xd[k].copy_(xh, non_blocking=True)
+                ev["in"][k].record(s_in)
+            stream.wait_event(ev["in"][k])
+            if i >= 2:
+                stream.wait_event(ev["gat"][k])  # od[k] free once gather i-2 is done
+            fwd_all(xd[k], od[k])
+            ev["fwd"][k].record(stream)
+            with torch.cuda.stream(s_comm):
+                s_comm.wait_event(ev["fwd"][k])
+                if rank == 0 and i >= 2:
+                    s_comm.wait_event(ev["out"][k])  # gbuf[k] free once D2H i-2 is done
+                dist.gather(od[k], gbuf[k] if rank == 0 else None, dst=0)
+                ev["gat"][k].record(s_comm)
+            if rank == 0:
+                with torch.cuda.stream(s_out):
+                    s_out.wait_event(ev["gat"][k])
+                    for r in range(ws):
+                        oh[k][r].copy_(gbuf[k][r], non_blocking=True)
+                    ev["out"][k].record(s_out)
+        stream.wait_stream(s_in)
+        stream.wait_stream(s_comm)
+        stream.wait_stream(s_out)
+
+    loop(2)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    loop(n)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = torch.tensor([e0.elapsed_time(e1) / n], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        assert torch.equal(oh[(n - 1) & 1][0], out.cpu()), "e2e rank-0 shard differs from device run"
+    ms = float(ms.item())
+    return {"value": round(gb * M / (ms * 1e-3), 1), "unit": UNIT,
+            "h2d_bytes_per_step": gb * M * D * 2, "d2h_bytes_per_step": ws * shard_pad * M * D * 2,
+            "ms_per_step": round(ms, 4),
+            "api": "per rank: pinned-host shard -> fsvd_model_fwd (C-ABI) -> NCCL gather to rank 0 "
+                   "-> rank 0 copies the global batch to pinned host; steps pipelined over 2 slots"}
+
+
+def roofline(args, L, packs, work, wsb, stream, dev, peaks, peak_src, ms_max, gb, ws):
+    import torch
+    from paper_2508_01506_b200 import abi
+    B, M, mode = args.batch, args.seq, args.mode
+    T = B * M
+    sp = C.c_void_p(stream.cuda_stream)
+    ffn_variant = 2 if mode == abi.MODE_FLASH_V2 else 1
+    resid = torch.randn((B, M, D), device=dev, dtype=torch.float32).to(torch.bfloat16)
+    ffn_out = torch.empty_like(resid)
+    ffn_ws = C.c_size_t(wsb.value)
+    reps = 20
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sub = {}
+    for name, fn in (
+            ("ffn_fwd", lambda: L.fsvd_ffn_fwd(
+                packs[0], ffn_variant, B, M, C.c_void_p(resid.data_ptr()),
+                C.c_void_p(ffn_out.data_ptr()), C.c_void_p(work.data_ptr()), ffn_ws, sp)),
+            ("attention_fwd", lambda: L.fsvd_attention_fwd(
+                packs[0], B, M, C.c_void_p(resid.data_ptr()), C.c_void_p(ffn_out.data_ptr()),
+                C.c_void_p(work.data_ptr()), ffn_ws, sp)),
+            ("outproj_fwd", lambda: L.fsvd_outproj_fwd(
+                packs[0], B, M, C.c_void_p(resid.data_ptr()), C.c_void_p(ffn_out.data_ptr()),
+                C.c_void_p(work.data_ptr()), ffn_ws, sp)),
+            ("layer_fwd", lambda: L.fsvd_layer_fwd(
+                packs[0], mode, 0, B, M, C.c_void_p(resid.data_ptr()),
+                C.c_void_p(ffn_out.data_ptr()), C.c_void_p(work.data_ptr()), ffn_ws, sp))):
+        for _ in range(3):
+            abi.check(fn())
+        torch.cuda.synchronize(dev)
+        k0.record(stream)
+        for _ in range(reps):
+            abi.check(fn())
+        k1.record(stream)
+        torch.cuda.synchronize(dev)
+        sub[name] = round(k0.elapsed_time(k1) / reps, 4)
+    k_ms = sub["ffn_fwd"]
+    flops = T * ffn_flops_per_token()
+    achieved = flops / (k_ms * 1e-3) / 1e12
+    peak = peaks.get("bf16_tflops", SURVEY_PEAKS["bf16_tflops"])
+    kname = "k_ffn_fused" if ffn_variant == 2 else "k_ffn_stream+k_gemm_bf16"
+    tr = load_ncu_traffic("k_ffn<")
+    return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": tr["bytes"] if tr else None,
+            "kernel": kname, "kernel_ms": round(k_ms, 4),
+            "algorithmic_flop_per_launch": flops,
+            "algorithmic_bytes_per_launch": T * D * 2 * 3,
+            "sublayer_ms": sub, "traffic_source": tr,
+            "peak_source": f"{peak_src}: burst bf16 (kernel timed alone)",
+            "model_frac_of_sustained": round(
+                gb * M * args.layers * algorithmic_flops_per_token_layer() / (ms_max * 1e-3) / 1e12
+                / (ws * peaks.get("bf16_tflops_sustained", SURVEY_PEAKS["bf16_tflops_sustained"])),
+                4)}
+
+
+def memory_block(args, L, parr, packs, act_bytes, ws, rank, gbufs):
+    """Peak activation memory of one rank (identical on every rank), against
+    (a) our own planner's dense-reconstruction schedules and (b) a
+    dense-reconstruction GPU baseline measured now, in this run: the same
+    encoder in plain PyTorch with the weights rebuilt from the factors per call
+    (tools/torch_baseline.py, allocations above weights and input)."""
+    from paper_2508_01506_b200 import abi
+    B, M = args.batch, args.seq
+    T = B * M
+    es = 2
+    mem = {}
+
+    def ws_for(m):
+        b = C.c_size_t()
+        abi.check(L.fsvd_workspace_bytes_ln(parr, len(packs), B, M, m, 0, C.byref(b)))
+        return b.value
+    io = 2 * T * D * es  # input + output activations of one micro-batch
+    mem["flash_v1_mib"] = round((ws_for(abi.MODE_FLASH_V1) + io) / 2**20, 1)
+    mem["flash_v2_mib"] = round((ws_for(abi.MODE_FLASH_V2) + io) / 2**20, 1)
+    dense_tr = max(3 * D, DF) * T * es
+    naive_tr = max(3 * G * 32 + 3 * D, PR, 2 * FR + DF) * T * es
+    mem["dense_baseline_mib"] = round((2 * T * D * es + dense_tr + io) / 2**20, 1)
+    mem["naive_lowrank_baseline_mib"] = round((2 * T * D * es + naive_tr + io) / 2**20, 1)
+    sel = mem["flash_v2_mib"] if args.mode == abi.MODE_FLASH_V2 else mem["flash_v1_mib"]
+    mem["reduction_vs_dense"] = round(1 - sel / mem["dense_baseline_mib"], 4)
+    mem["reduction_vs_naive_lowrank"] = round(1 - sel / mem["naive_lowrank_baseline_mib"], 4)
+    ours_above = (ws_for(args.mode) + T * D * es) / 2**20  # workspace + output
+    mem["above_weights_and_input_mib"] = round(ours_above, 1)
+    mem["measured_torch_allocator_mib"] = round(act_bytes / 2**20, 1)
+    if gbufs is not None:
+        mem["rank0_gather_buffers_mib"] = round(sum(g.numel() * g.element_size() for g in gbufs) / 2**20, 1)
+    if not args.no_torch_baseline and (B, M) == (BATCH, SEQ):
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import torch_baseline
+            ref_mib = torch_baseline.peak_activation_mib("naive_lowrank", args.layers)
+            mem["torch_dense_reconstruction_measured_mib"] = round(ref_mib, 1)
+            mem["reduction_vs_torch_dense_reconstruction"] = round(1 - ours_above / ref_mib, 4)
+            mem["torch_baseline_source"] = ("measured in this run: tools/torch_baseline.py "
+                                            "peak_activation_mib('naive_lowrank'), B=32, M=512, "
+                                            f"{args.layers} layers, torch.cuda.max_memory_allocated "
+                                            "above weights and input")
+        except Exception as e:
+            mem["torch_baseline_error"] = str(e)[:200]
+    mem["meter_transient_mib"] = {
+        "flash": round(4 * 3 * G * B * M * R / 2**20, 1),
+        "naive_lowrank": round(4 * max(3 * B * M * D, B * M * DF) / 2**20, 1),
+        "dense": round(4 * (3 * B * M * D + B * H * M * M) / 2**20, 1)}
+    return mem
 
 
 def main():
@@ -496,14 +717,23 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", type=int, default=3, help="2 = flash_v1, 3 = flash_v2")
-    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--batch", type=int, default=BATCH, help="micro-batch (sequences per forward)")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="total sequences per step over all ranks (0: batch x N, weak scaling)")
     ap.add_argument("--seq", type=int, default=SEQ)
     ap.add_argument("--layers", type=int, default=LAYERS)
-    ap.add_argument("--ref-batch", type=int, default=4)
+    ap.add_argument("--ref-batch", type=int, default=8, help="sequences per reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-torch-baseline", action="store_true")
+    ap.add_argument("--cpu-selftest", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--dist-path", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return relaunch(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
+    if args.cpu_selftest:
+        return run_cpu_selftest(args)
     return run_gpu(args)
 
 

@@ -72,6 +72,31 @@ def layer_fwd(L, x, schedule):
     return F.layer_norm(h1 + ffn, (D,), *L["ln2"]).view(B, M, D)
 
 
+def peak_activation_mib(schedule="naive_lowrank", n_layers=LAYERS, seed=0):
+    """One forward of the torch schedule; returns the peak allocation above the
+    weights and the input (torch.cuda.max_memory_allocated), in MiB.  bench.py
+    calls this in its own run (rank 0) for the memory comparison."""
+    torch.manual_seed(seed)
+    layers = [make_layer() for _ in range(n_layers)]
+    x = torch.randn(B, M, D, device=dev).to(bf)
+    with torch.no_grad():
+        y = x
+        for L in layers:  # warm (cuBLAS / SDPA workspaces are allocated here)
+            y = layer_fwd(L, y, schedule)
+        del y
+        torch.cuda.synchronize()
+        base = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        y = x
+        for L in layers:
+            y = layer_fwd(L, y, schedule)
+        torch.cuda.synchronize()
+        peak = torch.cuda.max_memory_allocated() - base
+    del layers, x, y
+    torch.cuda.empty_cache()
+    return peak / 2**20
+
+
 def main():
     torch.manual_seed(0)
     layers = [make_layer() for _ in range(LAYERS)]
