@@ -445,6 +445,10 @@ def run_gpu(args):
         e2e_multi(args, L, parr, packs, x, out, work, wsb.value, stream, dev, ws, rank, gb, micro,
                   s0, shard_pad)
 
+    # ---------------- e2e through the reference-signature drop-in ----------------
+    if rank == 0 and not multi and not args.no_dropin_e2e:
+        e2e["dropin"] = e2e_dropin(args, L, layers, x, out)
+
     # ---------------- dominant-kernel roofline (FFN) ----------------
     peaks, peak_src = load_peaks()
     roof = roofline(args, L, packs, work, wsb, stream, dev, peaks, peak_src, ms_max, gb, ws) \
@@ -525,6 +529,45 @@ def e2e_single(args, L, parr, packs, x, out, stream, dev):
             "ms_per_step": round(ms, 4),
             "api": "fsvd_model_fwd_stream (C-ABI): per step, pinned-host bf16 batch in, "
                    "12-layer forward, result out; copies overlap neighbouring steps"}
+
+
+def e2e_dropin(args, L, layers, x, out):
+    """fsvd_run_model -- the C-ABI behind flashsvd::b200::run_model, the
+    reference's run_model signature (encoder.hpp:90-92): fp32 host tensors in
+    and out, synchronous, every layer passed as fp32 factor arrays on every
+    call (the reference bench's loop, commands.cpp:289-307).  The first call
+    builds and caches the device packs; the timed calls hash the factors,
+    find the cached packs and run H2D -> 12 layers -> D2H."""
+    import numpy as np
+    import torch
+    from paper_2508_01506_b200 import abi
+    from paper_2508_01506_b200.model import layer_descs
+    B, M = args.batch, args.seq
+    xh = np.ascontiguousarray(x[:B].float().cpu().numpy())
+    oh = np.zeros_like(xh)
+    descs = layer_descs(layers)
+    plan = abi.TilePlan(16, 16, 32, 1 << 20)
+
+    def call():
+        abi.check(L.fsvd_run_model(abi.fptr(xh), B, M, D, descs, len(layers), args.mode, plan, 0,
+                                   b"layer", abi.BF16, None, abi.fptr(oh)))
+    t0 = time.perf_counter()
+    call()
+    first = time.perf_counter() - t0
+    n = 5
+    t0 = time.perf_counter()
+    for _ in range(n):
+        call()
+    ms = (time.perf_counter() - t0) / n * 1e3
+    ref = out[:B].float().cpu().numpy()
+    diff = float(np.abs(oh - ref).max())
+    assert diff <= 0.05 * float(np.abs(ref).max()), f"drop-in output differs: {diff}"
+    return {"value": round(B * M / (ms * 1e-3), 1), "unit": UNIT, "ms_per_step": round(ms, 3),
+            "first_call_ms": round(first * 1e3, 1), "h2d_bytes_per_step": B * M * D * 4,
+            "d2h_bytes_per_step": B * M * D * 4,
+            "api": "fsvd_run_model (flashsvd::b200::run_model): fp32 host tensors, factors "
+                   "passed per call, device packs found in the content-hashed pack cache; "
+                   "host wall clock per synchronous call"}
 
 
 def e2e_multi(args, L, parr, packs, x, out, work, wsb, stream, dev, ws, rank, gb, micro, s0,
@@ -725,6 +768,7 @@ def main():
     ap.add_argument("--ref-batch", type=int, default=8, help="sequences per reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-torch-baseline", action="store_true")
+    ap.add_argument("--no-dropin-e2e", action="store_true")
     ap.add_argument("--cpu-selftest", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--dist-path", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()

@@ -216,6 +216,16 @@ size_t fsvd_layer_pack_device_bytes(const fsvd_layer_pack* p);
  * kernels (fp32 policy or shapes outside the tensor-core tiling). */
 int fsvd_layer_pack_uses_tensor_cores(const fsvd_layer_pack* p);
 
+/* Pack cache of the host drop-ins (fsvd_flash_svd_attention ...
+ * fsvd_run_model): their device packs are kept per (device, dtype, content
+ * hash of every factor / bias / LayerNorm array), so repeated calls on the
+ * same layers -- the reference's run_model loop, commands.cpp:289-307 -- do
+ * not rebuild or re-upload them; a changed value rebuilds.  LRU, capped at
+ * FSVD_PACK_CACHE_MB (default 2048, 0 disables). */
+fsvd_status fsvd_pack_cache_stats(size_t* entries, size_t* bytes, uint64_t* hits,
+                                  uint64_t* misses);
+fsvd_status fsvd_pack_cache_clear(void);
+
 /* ------------------------------------------------------------------ */
 /* FSVD1 model files (model_io.hpp:14-30, written by the reference's     */
 /* save_model): container validation with byte offsets, assembly by the  */

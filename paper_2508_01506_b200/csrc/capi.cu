@@ -13,9 +13,13 @@
 // downloads.
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/fsvd_b200.h"
 #include "common.cuh"
@@ -149,7 +153,8 @@ size_t expected(int id, const fsvd_geometry& g) {
 
 // ------------------------------------------------------------- host staging
 // Device copies of a host fp32 activation in the pack dtype, plus the
-// workspace, freed on scope exit.
+// workspace.  The buffers are cached per (host thread, device) and only grow,
+// so a repeated synchronous call does no cudaMalloc / cudaFree.
 struct DevMem {
   void* p = nullptr;
   explicit DevMem(size_t bytes) {
@@ -162,22 +167,63 @@ struct DevMem {
   DevMem& operator=(const DevMem&) = delete;
 };
 
+struct ScratchSet {
+  void* p[2] = {nullptr, nullptr};  // 0: arena (in / out / workspace), 1: fp32 staging
+  size_t cap[2] = {0, 0};
+  int device = -1;
+  ~ScratchSet() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) return;
+    if (device >= 0) cudaSetDevice(device);
+    for (void* q : p)
+      if (q) cudaFree(q);
+    if (cur >= 0) cudaSetDevice(cur);
+  }
+};
+
+void* scratch(int slot, size_t bytes) {
+  thread_local std::map<int, std::unique_ptr<ScratchSet>> sets;
+  int dev = 0;
+  FSVD_CUDA_CHECK(cudaGetDevice(&dev));
+  std::unique_ptr<ScratchSet>& ss = sets[dev];
+  if (!ss) {
+    ss = std::make_unique<ScratchSet>();
+    ss->device = dev;
+  }
+  if (bytes > ss->cap[slot]) {
+    if (ss->p[slot]) {
+      FSVD_CUDA_CHECK(cudaDeviceSynchronize());
+      cudaFree(ss->p[slot]);
+      ss->p[slot] = nullptr;
+      ss->cap[slot] = 0;
+    }
+    FSVD_CUDA_CHECK(cudaMalloc(&ss->p[slot], bytes));
+    ss->cap[slot] = bytes;
+  }
+  return ss->p[slot];
+}
+
 void upload(const float* host, size_t n, fsvd_dtype dt, void* dev, cudaStream_t s) {
-  DevMem tmp(n * 4);
-  FSVD_CUDA_CHECK(cudaMemcpyAsync(tmp.p, host, n * 4, cudaMemcpyHostToDevice, s));
-  if (dt == FSVD_BF16) convert_f32<bf16>(static_cast<float*>(tmp.p), static_cast<bf16*>(dev), n, s);
-  else FSVD_CUDA_CHECK(cudaMemcpyAsync(dev, tmp.p, n * 4, cudaMemcpyDeviceToDevice, s));
-  FSVD_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (dt == FSVD_BF16) {
+    float* tmp = static_cast<float*>(scratch(1, n * 4));
+    FSVD_CUDA_CHECK(cudaMemcpyAsync(tmp, host, n * 4, cudaMemcpyHostToDevice, s));
+    convert_f32<bf16>(tmp, static_cast<bf16*>(dev), n, s);
+  } else {
+    FSVD_CUDA_CHECK(cudaMemcpyAsync(dev, host, n * 4, cudaMemcpyHostToDevice, s));
+  }
 }
 void download(const void* dev, size_t n, fsvd_dtype dt, float* host, cudaStream_t s) {
-  DevMem tmp(n * 4);
-  if (dt == FSVD_BF16) to_f32<bf16>(static_cast<const bf16*>(dev), static_cast<float*>(tmp.p), n, s);
-  else FSVD_CUDA_CHECK(cudaMemcpyAsync(tmp.p, dev, n * 4, cudaMemcpyDeviceToDevice, s));
-  FSVD_CUDA_CHECK(cudaMemcpyAsync(host, tmp.p, n * 4, cudaMemcpyDeviceToHost, s));
+  if (dt == FSVD_BF16) {
+    float* tmp = static_cast<float*>(scratch(1, n * 4));
+    to_f32<bf16>(static_cast<const bf16*>(dev), tmp, n, s);
+    FSVD_CUDA_CHECK(cudaMemcpyAsync(host, tmp, n * 4, cudaMemcpyDeviceToHost, s));
+  } else {
+    FSVD_CUDA_CHECK(cudaMemcpyAsync(host, dev, n * 4, cudaMemcpyDeviceToHost, s));
+  }
   FSVD_CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
-// Runs fn(x_dev, out_dev, trans_dev, stream) on a temporary device arena and
+// Runs fn(x_dev, out_dev, trans_dev, stream) on the cached device arena and
 // reports the arena to the meter's device high-water.
 template <typename F>
 void run_on_device(const float* x, size_t n_in, float* out, size_t n_out, fsvd_dtype dt,
@@ -185,8 +231,7 @@ void run_on_device(const float* x, size_t n_in, float* out, size_t n_out, fsvd_d
   require_device();
   const size_t es = dt == FSVD_BF16 ? 2 : 4;
   const size_t in_b = (n_in * es + 255) & ~size_t(255), out_b = (n_out * es + 255) & ~size_t(255);
-  DevMem arena(in_b + out_b + trans_bytes + 256);
-  uint8_t* base = static_cast<uint8_t*>(arena.p);
+  uint8_t* base = static_cast<uint8_t*>(scratch(0, in_b + out_b + trans_bytes + 256));
   cudaStream_t s = nullptr;
   upload(x, n_in, dt, base, s);
   fn(base, base + in_b, base + in_b + out_b, s);
@@ -195,12 +240,172 @@ void run_on_device(const float* x, size_t n_in, float* out, size_t n_out, fsvd_d
   if (meter) meter->note_device(in_b + out_b + trans_bytes, pack.bytes);
 }
 
-std::unique_ptr<Pack> pack_attention(const fsvd_attn_desc& a, size_t heads, fsvd_dtype dt) {
+// ------------------------------------------------------------- pack cache
+// The host drop-ins receive fp32 factors on every call (the reference's
+// signatures, encoder.hpp:83-92), and the reference's own bench loop calls
+// run_model again and again on the same layers (commands.cpp:289-307).  A
+// pack (fp64 folds on the host, bf16 / fp32 device layouts, H2D) is therefore
+// cached per (device, dtype, content): the key is a 64-bit hash of every
+// factor, bias and LayerNorm array plus the geometry, computed over the host
+// threads in parallel.  An unchanged layer costs one read of its host arrays;
+// any changed value -- even written in place at the same address -- rebuilds.
+// LRU, capped at FSVD_PACK_CACHE_MB (default 2048; 0 disables the cache).
+struct Span {
+  const void* p;
+  size_t n;
+};
+
+inline uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+constexpr uint64_t kP1 = 0x9E3779B185EBCA87ull, kP2 = 0xC2B2AE3D27D4EB4Full,
+                   kP3 = 0x165667B19E3779F9ull;
+
+uint64_t hash_bytes(const uint8_t* p, size_t n, uint64_t seed) {
+  uint64_t a[4] = {seed + kP1 + kP2, seed + kP2, seed, seed - kP1};
+  size_t i = 0;
+  for (; i + 32 <= n; i += 32)
+    for (int l = 0; l < 4; ++l) {
+      uint64_t w;
+      std::memcpy(&w, p + i + 8 * l, 8);
+      a[l] = rotl64(a[l] + w * kP2, 31) * kP1;
+    }
+  uint64_t h = rotl64(a[0], 1) + rotl64(a[1], 7) + rotl64(a[2], 12) + rotl64(a[3], 18) + n;
+  for (; i < n; ++i) h = rotl64(h ^ (p[i] * kP3), 11) * kP1;
+  h ^= h >> 33;
+  h *= kP2;
+  h ^= h >> 29;
+  h *= kP3;
+  h ^= h >> 32;
+  return h;
+}
+
+uint64_t hash_spans(const std::vector<Span>& spans) {
+  constexpr size_t kChunk = size_t(1) << 20;
+  std::vector<Span> chunks;
+  for (const Span& sp : spans) {
+    if (sp.n == 0 || sp.p == nullptr) {
+      chunks.push_back({nullptr, 0});  // still contributes its position
+      continue;
+    }
+    for (size_t o = 0; o < sp.n; o += kChunk)
+      chunks.push_back({static_cast<const uint8_t*>(sp.p) + o, std::min(kChunk, sp.n - o)});
+  }
+  std::vector<uint64_t> hs(chunks.size());
+  auto work = [&](size_t w, size_t nw) {
+    for (size_t i = w; i < chunks.size(); i += nw)
+      hs[i] = chunks[i].p ? hash_bytes(static_cast<const uint8_t*>(chunks[i].p), chunks[i].n, i)
+                          : kP3 + i;
+  };
+  size_t nw = std::min<size_t>(std::max(1u, std::thread::hardware_concurrency()), 16);
+  nw = std::min(nw, chunks.size() / 2 + 1);
+  std::vector<std::thread> pool;
+  for (size_t w = 1; w < nw; ++w) pool.emplace_back(work, w, nw);
+  work(0, nw);
+  for (auto& t : pool) t.join();
+  uint64_t h = kP1 ^ chunks.size();
+  for (uint64_t x : hs) h = rotl64(h ^ (x * kP2), 27) * kP1 + kP3;
+  return h;
+}
+
+uint64_t hash_request(const PackRequest& q, fsvd_dtype dt) {
+  std::vector<uint64_t> hdr = {static_cast<uint64_t>(dt), q.heads, q.d_model,
+                               static_cast<uint64_t>(q.dense)};
+  uint32_t e1, e2;
+  std::memcpy(&e1, &q.eps1, 4);
+  std::memcpy(&e2, &q.eps2, 4);
+  hdr.push_back((uint64_t(e1) << 32) | e2);
+  std::vector<Span> spans;
+  auto lin = [&](const fsvd_linear_desc* l) {
+    if (!l) {
+      hdr.insert(hdr.end(), {0, 0, 0});
+      return;
+    }
+    hdr.insert(hdr.end(), {l->in_dim, l->rank, l->out_dim});
+    spans.push_back({l->u, 4 * l->in_dim * l->rank});
+    spans.push_back({l->v, 4 * l->rank * l->out_dim});
+    spans.push_back({l->bias, 4 * l->out_dim});
+  };
+  if (q.attn) {
+    const fsvd_attn_desc& a = *q.attn;
+    hdr.insert(hdr.end(), {1, a.d_model, a.groups, a.rank});
+    spans.push_back({a.u, 4 * 3 * a.groups * a.d_model * a.rank});
+    spans.push_back({a.v, 4 * 3 * a.rank * a.d_model});
+    spans.push_back({a.bias, 4 * 3 * a.d_model});
+  } else {
+    hdr.push_back(0);
+  }
+  lin(q.out_proj);
+  if (q.ffn) {
+    hdr.insert(hdr.end(), {2, static_cast<uint64_t>(q.ffn->activation)});
+    lin(&q.ffn->up);
+    lin(&q.ffn->down);
+  } else {
+    hdr.push_back(0);
+  }
+  for (const float* v : {q.ln1g, q.ln1b, q.ln2g, q.ln2b}) {
+    hdr.push_back(v != nullptr);
+    if (v) spans.push_back({v, 4 * q.d_model});
+  }
+  spans.insert(spans.begin(), Span{hdr.data(), hdr.size() * sizeof(uint64_t)});
+  return hash_spans(spans);
+}
+
+struct PackCache {
+  struct Entry {
+    std::shared_ptr<Pack> pack;
+    uint64_t tick;
+  };
+  std::mutex mu;
+  std::map<std::pair<int, uint64_t>, Entry> map;
+  size_t bytes = 0;
+  uint64_t tick = 0, hits = 0, misses = 0;
+  size_t cap() const {
+    const char* e = std::getenv("FSVD_PACK_CACHE_MB");
+    return (e ? static_cast<size_t>(std::strtoull(e, nullptr, 10)) : 2048) << 20;
+  }
+};
+PackCache& pack_cache() {
+  static PackCache* c = new PackCache();  // leaked: outlives static destructors
+  return *c;
+}
+
+std::shared_ptr<Pack> cached_pack(const PackRequest& q, fsvd_dtype dt) {
+  PackCache& c = pack_cache();
+  const size_t cap = c.cap();
+  if (cap == 0) return std::shared_ptr<Pack>(build_pack(q, dt));
+  int dev = 0;
+  FSVD_CUDA_CHECK(cudaGetDevice(&dev));
+  const std::pair<int, uint64_t> key{dev, hash_request(q, dt)};
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.map.find(key);
+    if (it != c.map.end()) {
+      it->second.tick = ++c.tick;
+      ++c.hits;
+      return it->second.pack;
+    }
+    ++c.misses;
+  }
+  std::shared_ptr<Pack> p(build_pack(q, dt));
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto ins = c.map.emplace(key, PackCache::Entry{p, ++c.tick});
+  if (ins.second) c.bytes += p->bytes;
+  while (c.bytes > cap && c.map.size() > 1) {  // evict least recently used
+    auto lru = c.map.begin();
+    for (auto it = c.map.begin(); it != c.map.end(); ++it)
+      if (it->second.tick < lru->second.tick) lru = it;
+    if (lru->first == key) break;
+    c.bytes -= lru->second.pack->bytes;
+    c.map.erase(lru);
+  }
+  return ins.first->second.pack;
+}
+
+std::shared_ptr<Pack> pack_attention(const fsvd_attn_desc& a, size_t heads, fsvd_dtype dt) {
   PackRequest q;
   q.attn = &a;
   q.heads = heads;
   q.d_model = a.d_model;
-  return std::unique_ptr<Pack>(build_pack(q, dt));
+  return cached_pack(q, dt);
 }
 
 void check_dtype(fsvd_dtype dt) {
@@ -265,7 +470,7 @@ void host_outproj(const float* ctx, size_t B, size_t M, size_t W, const fsvd_lin
   PackRequest q;
   q.out_proj = &o;
   q.d_model = d;
-  std::unique_ptr<Pack> pack(build_pack(q, dt));
+  std::shared_ptr<Pack> pack = cached_pack(q, dt);
   const size_t trans = B * M * op_transient_elems(*pack, 1, FSVD_MODE_FLASH_V1) * pack->es;
   run_on_device(ctx, B * M * d, out, B * M * d, dt, trans, *pack, meter,
                 [&](void* xd, void* od, void* td, cudaStream_t s) {
@@ -308,7 +513,7 @@ void host_ffn(int variant, const float* x, size_t B, size_t M, size_t W, const f
   PackRequest q;
   q.ffn = &f;
   q.d_model = d;
-  std::unique_ptr<Pack> pack(build_pack(q, dt));
+  std::shared_ptr<Pack> pack = cached_pack(q, dt);
   const int mode = variant == 1 ? FSVD_MODE_FLASH_V1 : FSVD_MODE_FLASH_V2;
   const size_t trans = B * M * op_transient_elems(*pack, 2, mode) * pack->es;
   run_on_device(x, B * M * d, out, B * M * d, dt, trans, *pack, meter,
@@ -426,7 +631,7 @@ void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_lay
   }
   // device
   require_device();
-  std::vector<std::unique_ptr<Pack>> packs;
+  std::vector<std::shared_ptr<Pack>> packs;
   size_t ws = 0, pack_bytes = 0;
   for (size_t i = 0; i < n_layers; ++i) {
     PackRequest q;
@@ -442,7 +647,7 @@ void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_lay
     q.eps2 = layers[i].ln2_eps;
     q.d_model = W;
     q.dense = mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK;
-    packs.emplace_back(build_pack(q, dt));
+    packs.emplace_back(cached_pack(q, dt));
     if (q.dense && !packs.back()->dense)
       fail(Kind::Config, "dense / naive_lowrank modes run only on the bf16 tensor-core path");
     ws = std::max(ws, layer_workspace_bytes(*packs.back(), B * M, mode, pre_ln != 0));
@@ -787,6 +992,27 @@ StreamSet& stream_set() {
   return *slot;
 }
 }  // namespace
+
+fsvd_status fsvd_pack_cache_stats(size_t* entries, size_t* bytes, uint64_t* hits,
+                                  uint64_t* misses) {
+  return guard([&] {
+    PackCache& c = pack_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (entries) *entries = c.map.size();
+    if (bytes) *bytes = c.bytes;
+    if (hits) *hits = c.hits;
+    if (misses) *misses = c.misses;
+  });
+}
+
+fsvd_status fsvd_pack_cache_clear(void) {
+  return guard([&] {
+    PackCache& c = pack_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.map.clear();
+    c.bytes = 0;
+  });
+}
 
 fsvd_status fsvd_model_file_probe(const char* path, size_t* n_layers, fsvd_geometry* geom) {
   return guard([&] {

@@ -218,14 +218,14 @@ int main() {
           LayerRunOptions opts;
           opts.pre_layer_norm = pre;
           compare(std::string("run_layer ") + mode_name(mode) + (pre ? " pre-LN " : " post-LN ") + n,
-                  2 * tol,
+                  tol,
                   [&](MemoryMeter& m, Tensor& o) { run_layer(x, l, mode, plan, m, o, opts); },
                   [&](MemoryMeter& m, Tensor& o) { b200::run_layer(x, l, mode, plan, m, o, opts); },
                   shape_like, shape_like);
         }
       std::vector<EncoderLayer> model{l, layer_of(s.d, s.df, s.H, s.G, s.r, s.pr, s.fr, 801013)};
       if (dt == FSVD_BF16) round_layer(model[1]);
-      compare(std::string("run_model x2 ") + n, 2 * tol,
+      compare(std::string("run_model x2 ") + n, tol,
               [&](MemoryMeter& m, Tensor& o) { run_model(x, model, RunMode::FlashV2, plan, m, o); },
               [&](MemoryMeter& m, Tensor& o) {
                 b200::run_model(x, model, RunMode::FlashV2, plan, m, o);

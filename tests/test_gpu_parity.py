@@ -556,6 +556,40 @@ def test_stream_serving_back_to_back_calls_without_sync(L):
         L.fsvd_layer_pack_destroy(p)
 
 
+def test_host_dropin_pack_cache_hits_and_invalidates(L, ora):
+    """fsvd_run_model caches its device packs by content: a repeated call on
+    the same layers hits the cache and returns the same bits; a weight changed
+    in place (same address) misses, rebuilds and matches the oracle on the new
+    weights; FSVD_PACK_CACHE_MB=0 semantics are covered by clear()."""
+    layers = [oracle.rand_layer(ora, 256, 512, 4, 4, 32, 61 + i, 64, 128) for i in range(2)]
+    x = ora.random((2, 130, 256), 62)
+    layers = [round_layer_bf16(l) for l in layers]
+    x = bf16_round(x)
+    abi.check(L.fsvd_pack_cache_clear())
+
+    def stats():
+        e, b, h, m = C.c_size_t(), C.c_size_t(), C.c_uint64(), C.c_uint64()
+        abi.check(L.fsvd_pack_cache_stats(C.byref(e), C.byref(b), C.byref(h), C.byref(m)))
+        return e.value, b.value, h.value, m.value
+    _, _, h0, m0 = stats()
+    a = H.run_model(x, layers, abi.MODE_FLASH_V2, PLAN, abi.BF16)
+    e1, b1, h1, m1 = stats()
+    assert m1 - m0 == 2 and h1 == h0 and e1 == 2 and b1 > 0
+    b = H.run_model(x, layers, abi.MODE_FLASH_V2, PLAN, abi.BF16)
+    _, _, h2, m2 = stats()
+    assert h2 - h1 == 2 and m2 == m1
+    assert np.array_equal(a, b)
+    layers[1].ffn.up.v[3, 5] = bf16_round(np.array([layers[1].ffn.up.v[3, 5] + 0.5], np.float32))[0]
+    c = H.run_model(x, layers, abi.MODE_FLASH_V2, PLAN, abi.BF16)
+    _, _, h3, m3 = stats()
+    assert m3 - m2 == 1 and h3 - h2 == 1
+    assert not np.array_equal(a, c)
+    ref = ora.run_model(x, layers, abi.MODE_FLASH_V2, PLAN)
+    assert H.rel_err(c, ref) <= H.TOL_BF16
+    abi.check(L.fsvd_pack_cache_clear())
+    assert stats()[0] == 0
+
+
 # ------------------------------------------------------------------ empty inputs
 @pytest.mark.parametrize("shape", [(0, 16, 64), (2, 0, 64)], ids=["batch0", "seq0"])
 def test_empty_inputs_rejected_like_reference(L, ora, reference, shape):
