@@ -258,7 +258,7 @@ def run_reference(args):
     return 0
 
 
-def cpu_baseline_sample(args, steps=12, warmup=2):
+def cpu_baseline_sample(args, steps=8, warmup=1):
     """The reference arm itself (`--impl reference`, same model, same sample)
     for `steps` samples, run on rank 0 at N=1 in a fresh process: inside the
     GPU process the reference's large per-call host allocations run measurably
@@ -765,7 +765,8 @@ def main():
                     help="total sequences per step over all ranks (0: batch x N, weak scaling)")
     ap.add_argument("--seq", type=int, default=SEQ)
     ap.add_argument("--layers", type=int, default=LAYERS)
-    ap.add_argument("--ref-batch", type=int, default=8, help="sequences per reference sample")
+    ap.add_argument("--ref-batch", type=int, default=16,
+                    help="sequences per reference sample (16: the reference's best tokens/s on 16 host cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-torch-baseline", action="store_true")
     ap.add_argument("--no-dropin-e2e", action="store_true")

@@ -93,21 +93,33 @@ namespace {
 #define ATRACE(slot) do { } while (0)
 #endif
 
-template <int RP>
+// X3 (fp32 policy, split planes -- planes.cu): Qt, P_k, P_v arrive as hi and
+// lo planes; S = Q_hi K_hi + Q_hi K_lo + Q_lo K_hi, the probabilities are
+// computed in fp32 (MUFU ex2 only) and stored to TMEM as P_hi and P_lo, and
+// O += P_hi V_hi + P_hi V_lo + P_lo V_hi; the output leaves as two planes.
+// One CTA per SM (twice the tiles, 512 TMEM columns).
+template <int RP, bool X3 = false>
 struct AttnCfg {
-  static constexpr int STAGES = RP >= 64 ? 2 : 3;
+  static constexpr int STAGES = (RP >= 64 && !X3) || (X3 && RP >= 64) ? 2 : 3;
   static constexpr int RB = RP * 2;       // bytes per rank-width row
-  static constexpr int TILE = QT * RB;    // one Qt / P_k / P_v tile
+  static constexpr int TILE = QT * RB;    // one Qt / P_k / P_v tile (one plane)
+  static constexpr int NPL = X3 ? 2 : 1;  // planes per operand
+  static constexpr int Q_SLOT = NPL * up1k(TILE);
   static constexpr int o_q = 0;           // two Qt slots (next item prefetched)
-  static constexpr int o_kv = o_q + 2 * up1k(TILE);
-  static constexpr int KV_STAGE = 2 * up1k(TILE);
+  static constexpr int o_kv = o_q + 2 * Q_SLOT;
+  // KV stage: K_hi [K_lo] V_hi [V_lo]
+  static constexpr int KV_STAGE = 2 * NPL * up1k(TILE);
+  static constexpr int kv_klo = up1k(TILE), kv_v = NPL * up1k(TILE), kv_vlo = kv_v + up1k(TILE);
   static constexpr int o_bar = o_kv + STAGES * KV_STAGE;
   static constexpr int SMEM = 1024 + o_bar + 4608;  // Bars
   // TMEM columns: S (fp32, 128 keys), O (fp32, RP; two buffers when they fit
-  // so an item's output is written while the next item runs), P (bf16 pairs)
-  static constexpr int t_s = 0, t_o = 128, t_p = 192;
+  // so an item's output is written while the next item runs), P (bf16 pairs),
+  // X3: P_lo after P
+  static constexpr int t_s = 0, t_o = 128, t_p = 192, t_p2 = 256;
   static constexpr int NOB = RP <= 32 ? 2 : 1;
-  static_assert(2 * SMEM <= 228 * 1024, "two CTAs per SM");
+  static constexpr int TMEM_COLS = X3 ? 512 : 256;
+  static constexpr int CTAS = X3 ? 1 : 2;
+  static_assert(CTAS * SMEM <= 228 * 1024, "CTAs per SM");
 };
 
 struct Bars {
@@ -147,12 +159,13 @@ __device__ __forceinline__ Item item_of(int w, int nqt, int heads, int batch, in
 // stride gridDim.x; consecutive items share (batch, head) so K/V stay hot in
 // L2.  Q of the next item and its first K/V tiles are prefetched while the
 // current item finishes, and TMEM / barriers are set up once per CTA.
-template <int RP>
-__global__ void __launch_bounds__(kThreads, 2)
+template <int RP, bool X3 = false>
+__global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
     k_attn_rankspace(const __grid_constant__ CUtensorMap tmQKV, bf16* __restrict__ out,
                      int64_t ldo, int batch, int seq, int heads, int groups, int q_off, int k_off,
-                     int v_off, int causal) {
-  using C = AttnCfg<RP>;
+                     int v_off, int causal, const __grid_constant__ CUtensorMap tmQKV2,
+                     bf16* __restrict__ out2) {
+  using C = AttnCfg<RP, X3>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -165,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp == kTma && lane == 0) {
     tma_prefetch(&tmQKV);
+    if (X3) tma_prefetch(&tmQKV2);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->q_full[i], 1);
       mbar_init(&bars->q_empty[i], 1);
@@ -182,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     fence_barrier_init();
   }
   if (threadIdx.x == 0) ATRACE(0);
-  if (warp == kMma) tmem_alloc<256>(&bars->tmem);
+  if (warp == kMma) tmem_alloc<C::TMEM_COLS>(&bars->tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -203,17 +217,24 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int qs = it & 1;
         mbar_wait(&bars->q_empty[qs], ((it >> 1) & 1) ^ 1);
         if (it < 100) ATRACE(500 + it);
-        mbar_arrive_expect_tx(&bars->q_full[qs], C::TILE);
-        tma_load_2d(&tmQKV, &bars->q_full[qs], smem + C::o_q + qs * up1k(C::TILE),
+        mbar_arrive_expect_tx(&bars->q_full[qs], C::NPL * C::TILE);
+        tma_load_2d(&tmQKV, &bars->q_full[qs], smem + C::o_q + qs * C::Q_SLOT,
                     q_off + h * RP, row0 + qt * QT);
+        if (X3)
+          tma_load_2d(&tmQKV2, &bars->q_full[qs], smem + C::o_q + qs * C::Q_SLOT + up1k(C::TILE),
+                      q_off + h * RP, row0 + qt * QT);
         const int nji = causal ? min(nj, qt + 1) : nj;  // key tiles of this item
         for (int j = 0; j < nji; ++j) {
           mbar_wait(&bars->kv_empty[st], ph ^ 1);
           uint8_t* kv = smem + C::o_kv + st * C::KV_STAGE;
-          mbar_arrive_expect_tx(&bars->kv_full[st], 2 * C::TILE);
+          mbar_arrive_expect_tx(&bars->kv_full[st], 2 * C::NPL * C::TILE);
           tma_load_2d(&tmQKV, &bars->kv_full[st], kv, k_off + g * RP, row0 + j * KT);
-          tma_load_2d(&tmQKV, &bars->kv_full[st], kv + up1k(C::TILE), v_off + g * RP,
-                      row0 + j * KT);
+          tma_load_2d(&tmQKV, &bars->kv_full[st], kv + C::kv_v, v_off + g * RP, row0 + j * KT);
+          if (X3) {
+            tma_load_2d(&tmQKV2, &bars->kv_full[st], kv + C::kv_klo, k_off + g * RP, row0 + j * KT);
+            tma_load_2d(&tmQKV2, &bars->kv_full[st], kv + C::kv_vlo, v_off + g * RP,
+                        row0 + j * KT);
+          }
           if (++st == C::STAGES) { st = 0; ph ^= 1; }
         }
       }
@@ -222,7 +243,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   } else if (warp == kMma) {
     // ------------------------------------------------ MMA issuer (warp-uniform)
     const uint64_t dk0 = desc_kmajor(s_kv, C::RB);
-    const uint64_t dv0 = desc_mnmajor(s_kv + up1k(C::TILE), C::RB);
+    const uint64_t dv0 = desc_mnmajor(s_kv + C::kv_v, C::RB);
+    constexpr uint32_t kLoOff = up1k(C::TILE) >> 4;  // lo plane, descriptor units
     int gt = 0;  // key tiles issued so far by this CTA (all items)
     int it = 0;
     // S for global tile index t of the item whose Qt is in slot qs
@@ -231,12 +253,20 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_wait(&bars->kv_full[st], (t / C::STAGES) & 1);
       if (t > 0) mbar_wait(&bars->s_free, (t - 1) & 1);
       tc_fence_after();
-      const uint64_t dq = desc_kmajor(s_q + qs * up1k(C::TILE), C::RB);
+      const uint64_t dq = desc_kmajor(s_q + qs * C::Q_SLOT, C::RB);
       const uint64_t dk = dk0 + ((st * C::KV_STAGE) >> 4);
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < RP / 16; ++k)
           mma_bf16_ss(tmem + C::t_s, dq + 2 * k, dk + 2 * k, idesc_bf16(128, KT), k != 0);
+        if (X3) {  // + Q_hi K_lo + Q_lo K_hi
+#pragma unroll
+          for (int k = 0; k < RP / 16; ++k)
+            mma_bf16_ss(tmem + C::t_s, dq + 2 * k, dk + kLoOff + 2 * k, idesc_bf16(128, KT), 1u);
+#pragma unroll
+          for (int k = 0; k < RP / 16; ++k)
+            mma_bf16_ss(tmem + C::t_s, dq + kLoOff + 2 * k, dk + 2 * k, idesc_bf16(128, KT), 1u);
+        }
         mma_commit(&bars->s_full);
       }
       __syncwarp();
@@ -278,6 +308,17 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (int k = 0; k < KT / 16; ++k)
             mma_bf16_ts(t_o, tmem + C::t_p + k * 8, dv + ((k * 16 * C::RB) >> 4),
                         idesc_bf16(128, RP, 0, 1), (j | k) != 0);
+          if (X3) {  // + P_hi V_lo + P_lo V_hi
+            constexpr uint32_t kVLo = (C::kv_vlo - C::kv_v) >> 4;
+#pragma unroll
+            for (int k = 0; k < KT / 16; ++k)
+              mma_bf16_ts(t_o, tmem + C::t_p + k * 8, dv + kVLo + ((k * 16 * C::RB) >> 4),
+                          idesc_bf16(128, RP, 0, 1), 1u);
+#pragma unroll
+            for (int k = 0; k < KT / 16; ++k)
+              mma_bf16_ts(t_o, tmem + C::t_p2 + k * 8, dv + ((k * 16 * C::RB) >> 4),
+                          idesc_bf16(128, RP, 0, 1), 1u);
+          }
           mma_commit(&bars->o_full);
           mma_commit(&bars->kv_empty[st]);
         }
@@ -325,15 +366,24 @@ __global__ void __launch_bounds__(kThreads, 2)
         tmem_ld16(tq + C::t_o + ob * RP + oc0 + c, r);
         tmem_ld_wait();
         if (qrow < seq) {
-          uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)(row0_e + qrow) * ldo + h_e * RP +
-                                                oc0 + c);
+          const int64_t off = (int64_t)(row0_e + qrow) * ldo + h_e * RP + oc0 + c;
+          float o[16];
 #pragma unroll
-          for (int v = 0; v < 2; ++v)
-            dst[v] = make_uint4(
-                pack_bf16(__uint_as_float(r[8 * v + 0]) * inv, __uint_as_float(r[8 * v + 1]) * inv),
-                pack_bf16(__uint_as_float(r[8 * v + 2]) * inv, __uint_as_float(r[8 * v + 3]) * inv),
-                pack_bf16(__uint_as_float(r[8 * v + 4]) * inv, __uint_as_float(r[8 * v + 5]) * inv),
-                pack_bf16(__uint_as_float(r[8 * v + 6]) * inv, __uint_as_float(r[8 * v + 7]) * inv));
+          for (int i = 0; i < 16; ++i) o[i] = __uint_as_float(r[i]) * inv;
+#pragma unroll
+          for (int pl = 0; pl < C::NPL; ++pl) {
+            if (pl == 1) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o[i] -= bf16_round_f(o[i]);
+            }
+            uint4* dst = reinterpret_cast<uint4*>((pl == 0 ? out : out2) + off);
+#pragma unroll
+            for (int v = 0; v < 2; ++v)
+              dst[v] = make_uint4(pack_bf16(o[8 * v + 0], o[8 * v + 1]),
+                                  pack_bf16(o[8 * v + 2], o[8 * v + 3]),
+                                  pack_bf16(o[8 * v + 4], o[8 * v + 5]),
+                                  pack_bf16(o[8 * v + 6], o[8 * v + 7]));
+          }
         }
       }
       tc_fence_before();
@@ -397,16 +447,19 @@ __global__ void __launch_bounds__(kThreads, 2)
         const float alpha = ex2(m_run - m_new);
         m_run = m_new;
         uint32_t pk[KH / 2];
+        uint32_t pk2[KH / 2];  // X3: P_lo (dead otherwise)
         float2 sum2 = make_float2(0.0f, 0.0f);
         const float2 nm = make_float2(-m_new, -m_new);
 #pragma unroll
         for (int c = 0; c < KH / 2; ++c) {
           const float2 d = __fadd2_rn(make_float2(s[2 * c], s[2 * c + 1]), nm);
-          // one pair in EMU_EVERY on the FMA pipe, the rest on MUFU
-          const float2 p = (c % EMU_EVERY == EMU_EVERY - 1) ? ex2_poly2(d)
-                                                            : make_float2(ex2(d.x), ex2(d.y));
+          // one pair in EMU_EVERY on the FMA pipe, the rest on MUFU (X3: all MUFU)
+          const float2 p = (!X3 && c % EMU_EVERY == EMU_EVERY - 1)
+                               ? ex2_poly2(d)
+                               : make_float2(ex2(d.x), ex2(d.y));
           sum2 = __fadd2_rn(sum2, p);
           pk[c] = pack_bf16(p.x, p.y);
+          if (X3) pk2[c] = pack_bf16(p.x - bf16_round_f(p.x), p.y - bf16_round_f(p.y));
         }
         l_run = fmaf(l_run, alpha, sum2.x + sum2.y);
         // single-buffered probability tile: the previous PV (this item's, or
@@ -419,6 +472,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         // this half's 64 keys -> TMEM columns [t_p + 32*half, +32) of this row
         tmem_st32(tq + C::t_p + half * 32, pk);
+        if (X3) tmem_st32(tq + C::t_p2 + half * 32, pk2);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars->p_full);
@@ -451,26 +505,29 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   if (warp == kMma) {
     tc_fence_after();
-    tmem_free<256>(tmem);
+    tmem_free<C::TMEM_COLS>(tmem);
   }
 }
 
-template <int RP>
+template <int RP, bool X3 = false>
 void launch_attn(const AttnTcArgs& a, cudaStream_t s) {
-  using C = AttnCfg<RP>;
+  using C = AttnCfg<RP, X3>;
   static bool attr = false;
   if (!attr) {
-    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_attn_rankspace<RP>,
+    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_attn_rankspace<RP, X3>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
   const int T = a.batch * a.seq;
   const CUtensorMap tm =
       tmap_bf16(a.qkv, T, a.qkv_cols, a.ldq, 128, RP, swizzle_for_row_bytes(C::RB));
+  const CUtensorMap tm2 =
+      X3 ? tmap_bf16(a.qkv_lo, T, a.qkv_cols, a.ldq, 128, RP, swizzle_for_row_bytes(C::RB)) : tm;
   const int items = ((a.seq + QT - 1) / QT) * a.heads * a.batch;
-  const int grid = items < 2 * num_sms() ? items : 2 * num_sms();
-  launch_pdl(k_attn_rankspace<RP>, dim3(grid), dim3(kThreads), C::SMEM, s, tm, a.out, a.ldo,
-             a.batch, a.seq, a.heads, a.groups, a.q_off, a.k_off, a.v_off, a.causal ? 1 : 0);
+  const int grid = items < C::CTAS * num_sms() ? items : C::CTAS * num_sms();
+  launch_pdl(k_attn_rankspace<RP, X3>, dim3(grid), dim3(kThreads), C::SMEM, s, tm, a.out, a.ldo,
+             a.batch, a.seq, a.heads, a.groups, a.q_off, a.k_off, a.v_off, a.causal ? 1 : 0, tm2,
+             a.out_lo);
   check_launch("k_attn_rankspace");
 }
 
@@ -481,6 +538,14 @@ bool attn_rankspace_supported(int rank_pad) {
 }
 
 void attn_rankspace_bf16(const AttnTcArgs& a, cudaStream_t s) {
+  if (a.qkv_lo != nullptr) {  // split planes (fp32 policy)
+    switch (a.rank_pad) {
+      case 16: launch_attn<16, true>(a, s); return;
+      case 32: launch_attn<32, true>(a, s); return;
+      case 64: launch_attn<64, true>(a, s); return;
+      default: throw CudaError("attn_rankspace (planes): unsupported rank padding");
+    }
+  }
   switch (a.rank_pad) {
     case 16: launch_attn<16>(a, s); break;
     case 32: launch_attn<32>(a, s); break;

@@ -61,11 +61,18 @@ struct GemmCfg {
   static_assert(SMEM <= 227 * 1024, "shared-memory budget");
 };
 
-template <int BN, int STAGES>
+// X3 (fp32 policy): every operand is a pair of bf16 planes v = hi + lo
+// (split_planes), and the K loop runs three times over K -- A_hi B_hi,
+// A_hi B_lo, A_lo B_hi -- into the same fp32 accumulator (the lo*lo term is
+// below 2^-17 of the product).  tmA2 / tmB2 / tmC2 / resid2 address the lo
+// planes; the epilogue re-splits the fp32 result into the two output planes.
+template <int BN, int STAGES, bool X3 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const float* __restrict__ bias, int act,
-                int M, int N, int K, const bf16* resid, int64_t ldr) {
+                int M, int N, int K, const bf16* resid, int64_t ldr,
+                const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
+                const __grid_constant__ CUtensorMap tmC2, const bf16* resid2) {
   using Cfg = GemmCfg<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -83,11 +90,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int nk = (K + BK - 1) / BK;
+  const int nk3 = X3 ? 3 * nk : nk;  // K blocks of the (hi hi | hi lo | lo hi) sweep
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     tma_prefetch(&tmC);
+    if (X3) {
+      tma_prefetch(&tmA2);
+      tma_prefetch(&tmB2);
+      tma_prefetch(&tmC2);
+    }
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -116,12 +129,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       int it = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb3 = 0; kb3 < nk3; ++kb3, ++it) {
           if ((it & 1) == me) {
+            const int seg = X3 ? kb3 / nk : 0, kb = kb3 - seg * nk;
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
-            tma_load_2d(&tmA, &full[stage], sA + stage * Cfg::A_BYTES, kb * BK, m0);
-            tma_load_2d(&tmB, &full[stage], sB + stage * Cfg::B_BYTES, kb * BK, n0);
+            tma_load_2d(seg == 2 ? &tmA2 : &tmA, &full[stage], sA + stage * Cfg::A_BYTES, kb * BK, m0);
+            tma_load_2d(seg == 1 ? &tmB2 : &tmB, &full[stage], sB + stage * Cfg::B_BYTES, kb * BK, n0);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -143,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) GTRACE(17 + 4 * i);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = 0; kb < nk3; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t a0 = da + ((stage * Cfg::A_BYTES) >> 4);
@@ -199,8 +213,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         bias_act_chunk<32>(v, bias != nullptr ? bias + n0 + c0 : nullptr, N - (n0 + c0), act);
-        if (resid != nullptr && m0 + static_cast<int>(row) < M) {  // C = A B^T + bias + R
-          const uint4* rr = reinterpret_cast<const uint4*>(resid + (int64_t)(m0 + row) * ldr + n0 + c0);
+        for (int pl = 0; pl < (X3 ? 2 : 1); ++pl) {  // C = A B^T + bias + R (R = R_hi + R_lo)
+          const bf16* rp = pl == 0 ? resid : resid2;
+          if (rp == nullptr || m0 + static_cast<int>(row) >= M) continue;
+          const uint4* rr = reinterpret_cast<const uint4*>(rp + (int64_t)(m0 + row) * ldr + n0 + c0);
 #pragma unroll
           for (int q8 = 0; q8 < 4; ++q8) {
             if (n0 + c0 + 8 * q8 >= N) break;
@@ -213,27 +229,34 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        const uint32_t box = s_c + (nbox % Cfg::NCBOX) * Cfg::CBOX;
-        if (nbox >= Cfg::NCBOX) {
-          if (et == 0) {
-            if (Cfg::NCBOX == 2) tma_store_wait_read<1>();
-            else tma_store_wait_read<0>();
-          }
-          named_bar_sync(1, kEpiWarps * 32);
-        }
+#pragma unroll 1
+        for (int pl = 0; pl < (X3 ? 2 : 1); ++pl) {
+          if (X3 && pl == 1) {  // lo plane: what the hi plane's bf16 rounding left
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          st_shared_v4(box + swz_offset(row, half * 4 + c, 128), pack_bf16(v[8 * c + 0], v[8 * c + 1]),
-                       pack_bf16(v[8 * c + 2], v[8 * c + 3]),
-                       pack_bf16(v[8 * c + 4], v[8 * c + 5]),
-                       pack_bf16(v[8 * c + 6], v[8 * c + 7]));
-        fence_proxy_async_smem();
-        named_bar_sync(1, kEpiWarps * 32);
-        if (et == 0) {
-          tma_store_2d_u32(&tmC, box, n0 + b0, m0);
-          tma_store_commit();
+            for (int j = 0; j < 32; ++j) v[j] -= bf16_round_f(v[j]);
+          }
+          const uint32_t box = s_c + (nbox % Cfg::NCBOX) * Cfg::CBOX;
+          if (nbox >= Cfg::NCBOX) {
+            if (et == 0) {
+              if (Cfg::NCBOX == 2) tma_store_wait_read<1>();
+              else tma_store_wait_read<0>();
+            }
+            named_bar_sync(1, kEpiWarps * 32);
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            st_shared_v4(box + swz_offset(row, half * 4 + c, 128), pack_bf16(v[8 * c + 0], v[8 * c + 1]),
+                         pack_bf16(v[8 * c + 2], v[8 * c + 3]),
+                         pack_bf16(v[8 * c + 4], v[8 * c + 5]),
+                         pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+          fence_proxy_async_smem();
+          named_bar_sync(1, kEpiWarps * 32);
+          if (et == 0) {
+            tma_store_2d_u32(pl == 0 ? &tmC : &tmC2, box, n0 + b0, m0);
+            tma_store_commit();
+          }
+          ++nbox;
         }
-        ++nbox;
       }
       if (threadIdx.x == 64) GTRACE(514 + 4 * i);
     }
@@ -444,24 +467,28 @@ void launch_gemm2(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* 
   check_launch("k_gemm2_bf16");
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool X3 = false>
 void launch_gemm(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, int64_t ldc,
                  int M, int N, int K, const float* bias, int act, cudaStream_t s,
-                 const bf16* resid = nullptr, int64_t ldr = 0) {
+                 const bf16* resid = nullptr, int64_t ldr = 0, const bf16* A2 = nullptr,
+                 const bf16* B2 = nullptr, bf16* C2 = nullptr, const bf16* resid2 = nullptr) {
   using Cfg = GemmCfg<BN, STAGES>;
   static bool attr = false;
   if (!attr) {
-    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_bf16<BN, STAGES>,
+    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_bf16<BN, STAGES, X3>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     attr = true;
   }
   const CUtensorMap ta = tmap_bf16(A, M, K, lda, BM, BK, TmaSwizzle::B128);
   const CUtensorMap tb = tmap_bf16(B, N, K, ldb, BN, BK, TmaSwizzle::B128);
   const CUtensorMap tc = tmap_bf16(C, M, N, ldc, BM, 64, TmaSwizzle::B128);
+  const CUtensorMap ta2 = X3 ? tmap_bf16(A2, M, K, lda, BM, BK, TmaSwizzle::B128) : ta;
+  const CUtensorMap tb2 = X3 ? tmap_bf16(B2, N, K, ldb, BN, BK, TmaSwizzle::B128) : tb;
+  const CUtensorMap tc2 = X3 ? tmap_bf16(C2, M, N, ldc, BM, 64, TmaSwizzle::B128) : tc;
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  launch_pdl(k_gemm_bf16<BN, STAGES>, dim3(grid), dim3(kThreads), Cfg::SMEM, s, ta, tb, tc, bias,
-             act, M, N, K, resid, ldr);
+  launch_pdl(k_gemm_bf16<BN, STAGES, X3>, dim3(grid), dim3(kThreads), Cfg::SMEM, s, ta, tb, tc,
+             bias, act, M, N, K, resid, ldr, ta2, tb2, tc2, resid2);
   check_launch("k_gemm_bf16");
 }
 
@@ -511,6 +538,22 @@ void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, 
     launch_gemm<128, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
   else
     launch_gemm<64, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
+}
+
+void gemm_x3(const Planes& A, int64_t lda, const Planes& B, int64_t ldb, const PlanesOut& C,
+             int64_t ldc, int M, int N, int K, const float* bias, int act, cudaStream_t s,
+             const Planes* resid, int64_t ldr) {
+  const bf16* r1 = resid ? resid->hi : nullptr;
+  const bf16* r2 = resid ? resid->lo : nullptr;
+  if (M <= 128 && N % 64 == 0 && N >= 128)
+    launch_gemm<64, 8, true>(A.hi, lda, B.hi, ldb, C.hi, ldc, M, N, K, bias, act, s, r1, ldr, A.lo,
+                             B.lo, C.lo, r2);
+  else if (N % 128 == 0 || N > 64)
+    launch_gemm<128, 6, true>(A.hi, lda, B.hi, ldb, C.hi, ldc, M, N, K, bias, act, s, r1, ldr,
+                              A.lo, B.lo, C.lo, r2);
+  else
+    launch_gemm<64, 8, true>(A.hi, lda, B.hi, ldb, C.hi, ldc, M, N, K, bias, act, s, r1, ldr, A.lo,
+                             B.lo, C.lo, r2);
 }
 
 }  // namespace fsvd

@@ -29,6 +29,31 @@ void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, 
                const bf16* resid = nullptr, int64_t ldr = 0);
 bool gemm_bf16_supported(int M, int N, int K, int64_t lda, int64_t ldb, int64_t ldc);
 
+// ---- split planes (fp32 policy on the tensor cores) ---------------------------
+// An fp32 matrix v is held as two bf16 matrices of the same shape, hi = bf16(v)
+// and lo = bf16(v - hi) (|v - hi - lo| <= 2^-17 |v|).  Products run as three
+// bf16 MMA passes into one fp32 accumulator: A_hi B_hi + A_hi B_lo + A_lo B_hi.
+struct Planes {
+  const bf16* hi;
+  const bf16* lo;
+};
+struct PlanesOut {
+  bf16* hi;
+  bf16* lo;
+};
+// K1 in the split-plane form: C = A B^T (+ bias) (act) (+ resid), every
+// matrix as planes with the same leading dimension in both planes.
+void gemm_x3(const Planes& A, int64_t lda, const Planes& B, int64_t ldb, const PlanesOut& C,
+             int64_t ldc, int M, int N, int K, const float* bias, int act, cudaStream_t s,
+             const Planes* resid = nullptr, int64_t ldr = 0);
+// fp32 <-> planes at the API boundary; row kernels between the GEMMs (planes.cu)
+void split_planes(const float* src, bf16* hi, bf16* lo, int64_t n, cudaStream_t s);
+void merge_planes(const bf16* hi, const bf16* lo, float* dst, int64_t n, cudaStream_t s);
+// y = LN(a (+ b)) * gamma + beta, rows of width d; in place allowed for d <= 1024
+void ln_planes(const Planes& a, const Planes* b, const float* gamma, const float* beta, float eps,
+               const PlanesOut& y, int rows, int d, cudaStream_t s);
+void add_planes(const Planes& a, const Planes& b, const PlanesOut& y, int64_t n, cudaStream_t s);
+
 // ---- K6: y = LN(resid + bf16(A[T,K] * B[N,K]^T + bias)) * gamma + beta --------
 // One CTA per 128 complete rows; N <= 768, K <= 512, multiples of 64.
 // sum_out (optional, [T, N]): also store the un-normalised resid + A*B^T + bias
@@ -52,6 +77,10 @@ struct AttnTcArgs {
   bf16* out;
   int64_t ldo;
   bool causal = false;  // decoder prefill: key j visible to query i iff j <= i
+  // split planes (fp32 policy): lo planes of qkv and out, same layout; when
+  // set the kernel runs its X3 form (three bf16 passes per product)
+  const bf16* qkv_lo = nullptr;
+  bf16* out_lo = nullptr;
 };
 void attn_rankspace_bf16(const AttnTcArgs& a, cudaStream_t s);
 

@@ -1,0 +1,173 @@
+// planes.cu -- split-plane elementwise kernels of the fp32 policy.
+//
+// The fp32 policy runs the same tcgen05 kernels as bf16 (K1 / K2 / K3 with
+// their X3 template flag): every fp32 activation lives in HBM as two bf16
+// planes, hi = bf16(v) and lo = bf16(v - hi), so an MMA operand is exact to
+// 2^-17 of v and each product takes three bf16 passes (A_hi B_hi + A_hi B_lo
+// + A_lo B_hi) into an fp32 accumulator.  A [T, N] activation occupies
+// 4*T*N bytes (hi plane, then lo plane) -- the bytes of its fp32 form, so the
+// workspace planner's fp32 sizes hold unchanged.
+//
+// This file holds the conversions at the API boundary (fp32 <-> planes) and
+// the row kernels between the GEMMs: residual + LayerNorm (encoder.cpp:38-50,
+// tensor.cpp:88-102) and the pre-LN residual add, all computing in fp32.
+#include "common.cuh"
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace fsvd {
+namespace {
+
+__device__ __forceinline__ void split1(float v, bf16& hi, bf16& lo) {
+  hi = __float2bfloat16_rn(v);
+  lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+}
+__device__ __forceinline__ float join1(const bf16* hi, const bf16* lo, int64_t i) {
+  return __bfloat162float(hi[i]) + __bfloat162float(lo[i]);
+}
+
+__global__ void k_split_planes(const float* __restrict__ src, bf16* __restrict__ hi,
+                               bf16* __restrict__ lo, int64_t n) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    split1(src[i], hi[i], lo[i]);
+}
+
+__global__ void k_merge_planes(const bf16* __restrict__ hi, const bf16* __restrict__ lo,
+                               float* __restrict__ dst, int64_t n) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = join1(hi, lo, i);
+}
+
+// y = gamma * ((a + b) - mean) / sqrt(var + eps) + beta per row, fp32, biased
+// variance; one warp per row, up to 32*VPL values in registers.  In place
+// (y == a or y == b) is allowed: a row is read completely before it is written.
+template <int VPL>
+__global__ void __launch_bounds__(256)
+    k_ln_planes(Planes a, Planes b, const float* __restrict__ gamma,
+                const float* __restrict__ beta, float eps, PlanesOut y, int rows, int d) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const int64_t base = (int64_t)warp * d;
+  float v[VPL];
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + 32 * i;
+    v[i] = 0.0f;
+    if (c < d) {
+      v[i] = join1(a.hi, a.lo, base + c);
+      if (b.hi) v[i] += join1(b.hi, b.lo, base + c);
+      s += v[i];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float inv_d = 1.0f / static_cast<float>(d);
+  const float mean = s * inv_d;
+  float q = 0.0f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i)
+    if (lane + 32 * i < d) {
+      const float t = v[i] - mean;
+      q = fmaf(t, t, q);
+    }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float inv = 1.0f / sqrtf(q * inv_d + eps);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c < d) split1(gamma[c] * ((v[i] - mean) * inv) + beta[c], y.hi[base + c], y.lo[base + c]);
+  }
+}
+
+// Rows wider than the register path: three strided sweeps.
+__global__ void __launch_bounds__(256)
+    k_ln_planes_wide(Planes a, Planes b, const float* __restrict__ gamma,
+                     const float* __restrict__ beta, float eps, PlanesOut y, int rows, int d) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const int64_t base = (int64_t)warp * d;
+  auto val = [&](int c) {
+    float t = join1(a.hi, a.lo, base + c);
+    if (b.hi) t += join1(b.hi, b.lo, base + c);
+    return t;
+  };
+  float s = 0.0f;
+  for (int c = lane; c < d; c += 32) s += val(c);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / static_cast<float>(d);
+  float q = 0.0f;
+  for (int c = lane; c < d; c += 32) {
+    const float t = val(c) - mean;
+    q = fmaf(t, t, q);
+  }
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float inv = 1.0f / sqrtf(q / static_cast<float>(d) + eps);
+  // in place is not allowed here (a later value of the row is re-read)
+  for (int c = lane; c < d; c += 32)
+    split1(gamma[c] * ((val(c) - mean) * inv) + beta[c], y.hi[base + c], y.lo[base + c]);
+}
+
+__global__ void k_add_planes(Planes a, Planes b, PlanesOut y, int64_t n) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    split1(join1(a.hi, a.lo, i) + join1(b.hi, b.lo, i), y.hi[i], y.lo[i]);
+}
+
+int ew_grid(int64_t n) {
+  const int64_t g = (n + 255) / 256;
+  return static_cast<int>(g < 8 * 148 ? (g > 0 ? g : 1) : 8 * 148);
+}
+
+}  // namespace
+
+void split_planes(const float* src, bf16* hi, bf16* lo, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  launch_pdl(k_split_planes, dim3(ew_grid(n)), dim3(256), 0, s, src, hi, lo, n);
+  check_launch("k_split_planes");
+}
+
+void merge_planes(const bf16* hi, const bf16* lo, float* dst, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  launch_pdl(k_merge_planes, dim3(ew_grid(n)), dim3(256), 0, s, hi, lo, dst, n);
+  check_launch("k_merge_planes");
+}
+
+void ln_planes(const Planes& a, const Planes* b, const float* gamma, const float* beta, float eps,
+               const PlanesOut& y, int rows, int d, cudaStream_t s) {
+  const Planes bb = b ? *b : Planes{nullptr, nullptr};
+  const dim3 grid((rows + 7) / 8);
+  if (d <= 32 * 32) {
+    launch_pdl(k_ln_planes<32>, grid, dim3(256), 0, s, a, bb, gamma, beta, eps, y, rows, d);
+    check_launch("k_ln_planes");
+  } else {
+    if (y.hi == a.hi || (b && y.hi == b->hi))
+      throw CudaError("ln_planes: rows wider than 1024 cannot run in place");
+    launch_pdl(k_ln_planes_wide, grid, dim3(256), 0, s, a, bb, gamma, beta, eps, y, rows, d);
+    check_launch("k_ln_planes_wide");
+  }
+}
+
+void add_planes(const Planes& a, const Planes& b, const PlanesOut& y, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  launch_pdl(k_add_planes, dim3(ew_grid(n)), dim3(256), 0, s, a, b, y, n);
+  check_launch("k_add_planes");
+}
+
+}  // namespace fsvd
