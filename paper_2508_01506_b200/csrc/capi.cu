@@ -203,8 +203,15 @@ void* scratch(int slot, size_t bytes) {
   return ss->p[slot];
 }
 
-void upload(const float* host, size_t n, fsvd_dtype dt, void* dev, cudaStream_t s) {
-  if (dt == FSVD_BF16) {
+// F32 packs on the tensor cores hold device activations as split planes
+// (planes.cu): hi plane at dev, lo plane right after it.
+void upload(const float* host, size_t n, fsvd_dtype dt, void* dev, cudaStream_t s,
+            bool planes = false) {
+  if (planes) {
+    float* tmp = static_cast<float*>(scratch(1, n * 4));
+    FSVD_CUDA_CHECK(cudaMemcpyAsync(tmp, host, n * 4, cudaMemcpyHostToDevice, s));
+    split_planes(tmp, static_cast<bf16*>(dev), static_cast<bf16*>(dev) + n, n, s);
+  } else if (dt == FSVD_BF16) {
     float* tmp = static_cast<float*>(scratch(1, n * 4));
     FSVD_CUDA_CHECK(cudaMemcpyAsync(tmp, host, n * 4, cudaMemcpyHostToDevice, s));
     convert_f32<bf16>(tmp, static_cast<bf16*>(dev), n, s);
@@ -212,8 +219,13 @@ void upload(const float* host, size_t n, fsvd_dtype dt, void* dev, cudaStream_t 
     FSVD_CUDA_CHECK(cudaMemcpyAsync(dev, host, n * 4, cudaMemcpyHostToDevice, s));
   }
 }
-void download(const void* dev, size_t n, fsvd_dtype dt, float* host, cudaStream_t s) {
-  if (dt == FSVD_BF16) {
+void download(const void* dev, size_t n, fsvd_dtype dt, float* host, cudaStream_t s,
+              bool planes = false) {
+  if (planes) {
+    float* tmp = static_cast<float*>(scratch(1, n * 4));
+    merge_planes(static_cast<const bf16*>(dev), static_cast<const bf16*>(dev) + n, tmp, n, s);
+    FSVD_CUDA_CHECK(cudaMemcpyAsync(host, tmp, n * 4, cudaMemcpyDeviceToHost, s));
+  } else if (dt == FSVD_BF16) {
     float* tmp = static_cast<float*>(scratch(1, n * 4));
     to_f32<bf16>(static_cast<const bf16*>(dev), tmp, n, s);
     FSVD_CUDA_CHECK(cudaMemcpyAsync(host, tmp, n * 4, cudaMemcpyDeviceToHost, s));
@@ -233,10 +245,10 @@ void run_on_device(const float* x, size_t n_in, float* out, size_t n_out, fsvd_d
   const size_t in_b = (n_in * es + 255) & ~size_t(255), out_b = (n_out * es + 255) & ~size_t(255);
   uint8_t* base = static_cast<uint8_t*>(scratch(0, in_b + out_b + trans_bytes + 256));
   cudaStream_t s = nullptr;
-  upload(x, n_in, dt, base, s);
+  upload(x, n_in, dt, base, s, pack.x3);
   fn(base, base + in_b, base + in_b + out_b, s);
   FSVD_CUDA_CHECK(cudaGetLastError());
-  download(base + in_b, n_out, dt, out, s);
+  download(base + in_b, n_out, dt, out, s, pack.x3);
   if (meter) meter->note_device(in_b + out_b + trans_bytes, pack.bytes);
 }
 
@@ -652,6 +664,8 @@ void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_lay
       fail(Kind::Config, "dense / naive_lowrank modes run only on the bf16 tensor-core path");
     ws = std::max(ws, layer_workspace_bytes(*packs.back(), B * M, mode, pre_ln != 0));
     pack_bytes += packs.back()->bytes;
+    if (packs.back()->x3 != packs[0]->x3)
+      fail(Kind::Config, "fp32 policy: every layer must fit the tensor-core tiling, or none");
   }
   run_on_device(x, B * M * W, out, B * M * W, dt, ws, *packs[0], nullptr,
                 [&](void* xd, void* od, void* td, cudaStream_t s) {
@@ -863,7 +877,7 @@ void fsvd_layer_pack_destroy(fsvd_layer_pack* p) {
 }
 size_t fsvd_layer_pack_device_bytes(const fsvd_layer_pack* p) { return p ? p->p->bytes : 0; }
 int fsvd_layer_pack_uses_tensor_cores(const fsvd_layer_pack* p) {
-  return p && p->p->attn_tc && p->p->out_tc && p->p->ffn_tc ? 1 : 0;
+  return p && ((p->p->attn_tc && p->p->out_tc && p->p->ffn_tc) || p->p->x3) ? 1 : 0;
 }
 
 // ---------------------------------------------------------------- device API

@@ -51,18 +51,26 @@ constexpr int STAGE = 2 * SLOT;  // two slots per ring stage
 // the rank is cut into slices of FR columns, one CTA per (row tile, slice);
 // P is not resident -- MMA1 streams it with V_up as (P atom, V_up atom) slot
 // pairs, and each slice recomputes the hidden block.
-template <int FR, bool WIDE = false>
+//
+// X3 (fp32 policy, K3 only, on the WIDE structure): P, V_up, U_down and the
+// hidden block are split planes (planes.cu).  MMA1 streams (P_hi, V_up_hi)
+// and (P_lo, V_up_lo) as two consecutive ring stages and issues
+// P_hi V_hi + P_lo V_hi + P_hi V_lo; the epilogue writes H_hi and H_lo; MMA2
+// takes (U_dn_hi, U_dn_lo) per stage for H_hi U_hi + H_lo U_hi + H_hi U_lo.
+template <int FR, bool WIDE = false, bool X3 = false>
 struct FfnCfg {
   static_assert(FR % 64 == 0 && FR <= 384, "FR must be a multiple of 64, <= 384");
+  static_assert(!X3 || WIDE, "the split-plane stream runs on the WIDE structure");
   static constexpr int NATOM = FR / 64;
   static constexpr int PS = (FR % 128 == 0) ? 128 : 64;  // rows per Z / P piece
   static constexpr int NPIECE = FR / PS;
   static constexpr int PATOMS = WIDE ? 0 : NATOM;        // resident P atoms
-  static constexpr int STAGES_FIT = (227 * 1024 - 2048 - (PATOMS + 2) * SLOT) / STAGE;
+  static constexpr int HATOMS = X3 ? 4 : 2;              // H tile (hi, [lo]) atoms
+  static constexpr int STAGES_FIT = (227 * 1024 - 2048 - (PATOMS + HATOMS) * SLOT) / STAGE;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int o_p = 0;                  // P / Z tile, NATOM atoms
-  static constexpr int o_h = PATOMS * SLOT;      // H tile (2 atoms) / X double buffer
-  static constexpr int o_ring = o_h + 2 * SLOT;
+  static constexpr int o_h = PATOMS * SLOT;      // H tile (2 atoms, X3: + 2 lo) / X double buffer
+  static constexpr int o_ring = o_h + HATOMS * SLOT;
   static constexpr int o_bar = o_ring + STAGES * STAGE;
   static constexpr int SMEM = 1024 + o_bar + 512;
   static constexpr int t_z = 0;    // Z / P accumulator (FR cols)
@@ -118,7 +126,7 @@ namespace {
 #define TRACE(slot) do { } while (0)
 #endif
 
-template <int FR, bool FUSED, bool WIDE>
+template <int FR, bool FUSED, bool WIDE, bool X3 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_ffn(const __grid_constant__ CUtensorMap tmX,    // X [T, d]        box 128x64 (FUSED)
           const __grid_constant__ CUtensorMap tmP,    // P [T, FR]       box 128x64 (V1)
@@ -133,9 +141,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           int d_model, int d_ff, bf16* z_out, bf16* out,
           const float* __restrict__ ln_g, const float* __restrict__ ln_b, float ln_eps,
           int split_blocks, float* __restrict__ z_part, const bf16* resid,
-          int frk, bf16* sum_out) {
+          int frk, bf16* sum_out, const __grid_constant__ CUtensorMap tmP2,
+          const __grid_constant__ CUtensorMap tmVup2, const __grid_constant__ CUtensorMap tmUdn2,
+          bf16* z_out2) {
   static_assert(!(WIDE && FUSED), "wide ranks run the V1 chain");
-  using C = FfnCfg<FR, WIDE>;
+  using C = FfnCfg<FR, WIDE, X3>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -166,6 +176,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmUdn);
     tma_prefetch(&tmVdn);
     if (FUSED) tma_prefetch(&tmX); else tma_prefetch(&tmP);
+    if (X3) {
+      tma_prefetch(&tmP2);
+      tma_prefetch(&tmVup2);
+      tma_prefetch(&tmUdn2);
+    }
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&bars->full[i], 1);
       mbar_init(&bars->empty[i], 1);
@@ -223,6 +238,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
       auto mma1_slots = [&](int f) {
+        if (X3) {  // (P_hi a, V_hi a), (P_lo a, V_lo a): two stages per atom
+          emit(4 * NK, [&](int j, uint8_t* dst, bool size_only) -> uint32_t {
+            if (!size_only) {
+              const int a = j >> 2, w = j & 3;
+              if (w & 1)
+                tma_load_2d(w == 1 ? &tmVup : &tmVup2, &bars->full[st], dst, a * 64, (fb0 + f) * BF);
+              else
+                tma_load_2d(w == 0 ? &tmP : &tmP2, &bars->full[st], dst, a * 64, m0);
+            }
+            return SLOT;
+          });
+          return;
+        }
         if (WIDE) {  // (P atom a, V_up atom a) per stage
           emit(2 * NK, [&](int j, uint8_t* dst, bool size_only) -> uint32_t {
             if (!size_only) {
@@ -239,6 +267,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         });
       };
       auto mma2_slots = [&](int f) {  // atom-major: (a0: p0..), (a1: p0..)
+        if (X3) {  // (U_dn_hi, U_dn_lo) of one (atom, piece) per stage
+          emit(4 * C::NPIECE, [&](int j, uint8_t* dst, bool size_only) -> uint32_t {
+            const int k = j >> 1, a = k / C::NPIECE, p = k % C::NPIECE;
+            if (!size_only)
+              tma_load_2d((j & 1) ? &tmUdn2 : &tmUdn, &bars->full[st], dst,
+                          (fb0 + f) * BF + a * 64, zc0 + p * C::PS);
+            return C::PS * 128;
+          });
+          return;
+        }
         emit(2 * C::NPIECE, [&](int j, uint8_t* dst, bool size_only) -> uint32_t {
           const int a = j / C::NPIECE, p = j % C::NPIECE;
           if (!size_only)
@@ -358,7 +396,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
         }
         TRACE(64 + f * 8 + 1);
-        if (WIDE) {
+        if (X3) {
+          // stage pair per atom: hold (P_hi, V_hi) until (P_lo, V_lo) has
+          // arrived, issue the three products, then release both
+          for (int a = 0; a < NK; ++a) {
+            const uint32_t st1 = st, ph1 = ph;
+            if (++st == C::STAGES) { st = 0; ph ^= 1; }
+            mbar_wait(&bars->full[st1], ph1);
+            mbar_wait(&bars->full[st], ph);
+            tc_fence_after();
+            const uint64_t s1 = d_ring + ((st1 * STAGE) >> 4), s2 = d_ring + ((st * STAGE) >> 4);
+            const uint32_t idh = idesc_bf16(128, BF);
+            mma4(tmem + C::t_h, s1, s1 + kAtom, idh, a != 0);  // P_hi V_hi
+            mma4(tmem + C::t_h, s2, s1 + kAtom, idh, true);    // P_lo V_hi
+            mma4(tmem + C::t_h, s1, s2 + kAtom, idh, true);    // P_hi V_lo
+            commit(&bars->empty[st1]);
+            commit(&bars->empty[st]);
+            if (++st == C::STAGES) { st = 0; ph ^= 1; }
+          }
+        } else if (WIDE) {
           uint64_t pa = 0;
           consume(2 * NK, [&](int j, uint64_t slot) {
             if (j & 1) mma4(tmem + C::t_h, pa, slot, idesc_bf16(128, BF), j > 1);
@@ -373,6 +429,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         TRACE(64 + f * 8 + 2);
       };
       auto mma2 = [&](int f) {
+        if (X3) {
+          uint64_t hi_slot = 0;
+          consume(4 * C::NPIECE, [&](int j, uint64_t slot) {
+            const int k = j >> 1, a = k / C::NPIECE, p = k % C::NPIECE;
+            if ((j & 1) == 0) {
+              if (p == 0) {
+                mbar_wait(&bars->sh_full[a], f & 1);
+                tc_fence_after();
+              }
+              hi_slot = slot;
+              return;
+            }
+            const uint32_t idz = idesc_bf16(128, C::PS);
+            const uint32_t zt = tmem + C::t_z + p * C::PS;
+            mma4(zt, d_h + a * kAtom, hi_slot, idz, (f | a) != 0);  // H_hi U_hi
+            mma4(zt, d_h + (2 + a) * kAtom, hi_slot, idz, true);   // H_lo U_hi
+            mma4(zt, d_h + a * kAtom, slot, idz, true);            // H_hi U_lo
+            if (p == C::NPIECE - 1) commit(&bars->sh_free[a]);
+          });
+          return;
+        }
         consume(2 * C::NPIECE, [&](int j, uint64_t slot) {
           const int a = j / C::NPIECE, p = j % C::NPIECE;
           if (p == 0) {
@@ -451,6 +528,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (f > 0) mbar_wait(&bars->sh_free[i], (f - 1) & 1);
         if (threadIdx.x == 64) TRACE(1024 + f * 8 + 3 + i * 2);
         st_chunk_smem(s_h, row, (half + 2 * i) * 32, v[i]);
+        if (X3) {  // lo plane of the activated block, atoms 2..3
+#pragma unroll
+          for (int k = 0; k < 32; ++k) v[i][k] -= bf16_round_f(v[i][k]);
+          st_chunk_smem(s_h + 2 * SLOT, row, (half + 2 * i) * 32, v[i]);
+        }
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&bars->sh_full[i]);
@@ -471,6 +553,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             d[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
         } else {
           st_chunk_global(z_out + (int64_t)grow * frk + zc0 + c * 32, v);
+          if (X3) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] -= bf16_round_f(v[k]);
+            st_chunk_global(z_out2 + (int64_t)grow * frk + zc0 + c * 32, v);
+          }
         }
       }
     } else {
@@ -531,12 +618,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // FR = Z columns per CTA; frk = a.rank_pad (the P / Z width, K of MMA1).
-template <int FR, bool FUSED, bool WIDE = false>
+template <int FR, bool FUSED, bool WIDE = false, bool X3 = false>
 void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
-  using C = FfnCfg<FR, WIDE>;
+  using C = FfnCfg<FR, WIDE, X3>;
   static bool attr = false;
   if (!attr) {
-    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_ffn<FR, FUSED, WIDE>,
+    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_ffn<FR, FUSED, WIDE, X3>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
@@ -556,19 +643,37 @@ void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
                     : tx;
   } else
     tp = tmap_bf16(a.p_in, a.T, frk, frk, 128, 64, TmaSwizzle::B128);
+  CUtensorMap tp2 = tp, tvup2 = tvup, tudn2 = tudn;
+  if (X3) {
+    tp2 = tmap_bf16(a.p_in_lo, a.T, frk, frk, 128, 64, TmaSwizzle::B128);
+    tvup2 = tmap_bf16(a.up_v_t_lo, a.d_ff, frk, frk, BF, 64, TmaSwizzle::B128);
+    tudn2 = tmap_bf16(a.dn_u_t_lo, frk, a.d_ff, a.d_ff, boxp, 64, TmaSwizzle::B128);
+  }
   const int grid = (a.T + BMr - 1) / BMr;
   const int nball = (a.d_ff + BF - 1) / BF;
   const int splits = (!FUSED && a.split_blocks) ? (nball + a.split_blocks - 1) / a.split_blocks : 1;
-  launch_pdl(k_ffn<FR, FUSED, WIDE>, dim3(grid, splits * (frk / FR)), dim3(kThreads), C::SMEM, s,
-             tx, tp, tup, tvup, tudn, tvdn, ty, tr, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff,
-             a.z_out, a.out, a.ln_g, a.ln_b, a.ln_eps, FUSED ? 0 : a.split_blocks,
+  launch_pdl(k_ffn<FR, FUSED, WIDE, X3>, dim3(grid, splits * (frk / FR)), dim3(kThreads), C::SMEM,
+             s, tx, tp, tup, tvup, tudn, tvdn, ty, tr, a.up_b, a.dn_b, a.act, a.T, a.d_model,
+             a.d_ff, a.z_out, a.out, a.ln_g, a.ln_b, a.ln_eps, FUSED ? 0 : a.split_blocks,
              FUSED ? nullptr : a.z_part, FUSED ? a.resid : nullptr, frk,
-             FUSED && a.ln_g ? a.sum_out : nullptr);
+             FUSED && a.ln_g ? a.sum_out : nullptr, tp2, tvup2, tudn2, a.z_out_lo);
   check_launch(FUSED ? "k_ffn_fused" : "k_ffn_stream");
 }
 
 template <bool FUSED>
 void dispatch_ffn(const FfnTcArgs& a, cudaStream_t s) {
+  if (!FUSED && a.p_in_lo != nullptr) {  // split planes (fp32 policy)
+    if (a.split_blocks) throw CudaError("ffn (planes): split partials are bf16-only");
+    switch (ffn_wide_slice(a.rank_pad)) {
+      case 64: launch_ffn<64, false, true, true>(a, s); return;
+      case 128: launch_ffn<128, false, true, true>(a, s); return;
+      case 192: launch_ffn<192, false, true, true>(a, s); return;
+      case 256: launch_ffn<256, false, true, true>(a, s); return;
+      case 320: launch_ffn<320, false, true, true>(a, s); return;
+      case 384: launch_ffn<384, false, true, true>(a, s); return;
+      default: throw CudaError("ffn (planes): unsupported FFN rank padding");
+    }
+  }
   if (!FUSED && a.rank_pad > 384) {
     static const bool recompute = [] {
       const char* e = getenv("FSVD_FFN_WIDE_RECOMPUTE");

@@ -49,7 +49,7 @@ void gemm_x3(const Planes& A, int64_t lda, const Planes& B, int64_t ldb, const P
 // fp32 <-> planes at the API boundary; row kernels between the GEMMs (planes.cu)
 void split_planes(const float* src, bf16* hi, bf16* lo, int64_t n, cudaStream_t s);
 void merge_planes(const bf16* hi, const bf16* lo, float* dst, int64_t n, cudaStream_t s);
-// y = LN(a (+ b)) * gamma + beta, rows of width d; in place allowed for d <= 1024
+// y = LN(a (+ b)) * gamma + beta, rows of width d; in place allowed for d <= 2048
 void ln_planes(const Planes& a, const Planes* b, const float* gamma, const float* beta, float eps,
                const PlanesOut& y, int rows, int d, cudaStream_t s);
 void add_planes(const Planes& a, const Planes& b, const PlanesOut& y, int64_t n, cudaStream_t s);
@@ -136,6 +136,12 @@ struct FfnTcArgs {
   // x, and the un-normalised ln_resid + ffn(x) is also stored to sum_out
   const bf16* ln_resid = nullptr;
   bf16* sum_out = nullptr;
+  // V1 stream in split planes (fp32 policy): the lo planes of P, V_up^T,
+  // U_down^T and Z; when p_in_lo is set K3 runs its X3 form
+  const bf16* p_in_lo = nullptr;
+  const bf16* up_v_t_lo = nullptr;
+  const bf16* dn_u_t_lo = nullptr;
+  bf16* z_out_lo = nullptr;
 };
 void ffn_stream_bf16(const FfnTcArgs& a, cudaStream_t s);   // V1 middle: P -> Z
 void z_partial_sum_bf16(const float* part, int splits, int64_t n, bf16* z, cudaStream_t s);

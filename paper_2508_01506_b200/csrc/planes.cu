@@ -156,9 +156,12 @@ void ln_planes(const Planes& a, const Planes* b, const float* gamma, const float
   if (d <= 32 * 32) {
     launch_pdl(k_ln_planes<32>, grid, dim3(256), 0, s, a, bb, gamma, beta, eps, y, rows, d);
     check_launch("k_ln_planes");
+  } else if (d <= 64 * 32) {
+    launch_pdl(k_ln_planes<64>, grid, dim3(256), 0, s, a, bb, gamma, beta, eps, y, rows, d);
+    check_launch("k_ln_planes");
   } else {
     if (y.hi == a.hi || (b && y.hi == b->hi))
-      throw CudaError("ln_planes: rows wider than 1024 cannot run in place");
+      throw CudaError("ln_planes: rows wider than 2048 cannot run in place");
     launch_pdl(k_ln_planes_wide, grid, dim3(256), 0, s, a, bb, gamma, beta, eps, y, rows, d);
     check_launch("k_ln_planes_wide");
   }

@@ -64,6 +64,25 @@ struct Builder {
     }
     fix.push_back({dst, off});
   }
+  // split planes (fp32 policy): hi = bf16(v), lo = bf16(v - hi)
+  void store_planes(const void** hi, const void** lo, const std::vector<float>& v) {
+    std::vector<uint16_t> h(v.size()), l(v.size());
+    for (size_t i = 0; i < v.size(); ++i) {
+      h[i] = f32_to_bf16_bits(v[i]);
+      uint32_t u = static_cast<uint32_t>(h[i]) << 16;
+      float hf;
+      std::memcpy(&hf, &u, 4);
+      l[i] = f32_to_bf16_bits(v[i] - hf);
+    }
+    fix.push_back({hi, raw(h.data(), h.size() * 2)});
+    fix.push_back({lo, raw(l.data(), l.size() * 2)});
+  }
+  // tensor-core weight layout: bf16 (bf16 policy) or split planes (x3)
+  bool x3 = false;
+  void tc(const void** dst, const void** dst_lo, const std::vector<float>& v) {
+    if (x3) store_planes(dst, dst_lo, v);
+    else store(dst, v);
+  }
   void store_f32(const float** dst, const float* p, size_t n) { fixf.push_back({dst, raw(p, n * 4)}); }
   void store_f32(const float** dst, const std::vector<float>& v) { store_f32(dst, v.data(), v.size()); }
 };
@@ -102,6 +121,21 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
   b.es = p.es;
   const bool bf = dtype == FSVD_BF16;
   const int d = p.d;
+  // tensor-core support of each component (bf16 policy: per component; fp32
+  // policy: split planes when every component present is supported)
+  bool attn_ok = true, out_ok = true, ffn_ok = true;
+  if (q.attn) {
+    const int r = static_cast<int>(q.attn->rank);
+    const int rp = r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : 0;
+    attn_ok = rp != 0 && attn_rankspace_supported(rp) && d % 8 == 0;
+  }
+  if (q.out_proj) out_ok = d % 8 == 0;
+  if (q.ffn) {
+    const int df = static_cast<int>(q.ffn->up.out_dim);
+    ffn_ok = d % 8 == 0 && df % 8 == 0 && ffn_tc_supported(d, df, ffn_rank_pad(static_cast<int>(q.ffn->up.rank)));
+  }
+  p.x3 = !bf && attn_ok && out_ok && ffn_ok;
+  b.x3 = p.x3;
 
   if (q.attn) {
     const fsvd_attn_desc& a = *q.attn;
@@ -113,8 +147,8 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
     p.gd = d / p.G;
     const int G = p.G, r = p.r, H = p.H, dh = p.dh, gd = p.gd, hpg = H / G;
     p.rp = r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : 0;
-    p.attn_tc = bf && p.rp != 0 && attn_rankspace_supported(p.rp) && d % 8 == 0;
-    if (p.attn_tc) {
+    p.attn_tc = bf && attn_ok;
+    if (p.attn_tc || p.x3) {
       // Folded rank-space projection (attn_tc.cu): rows [0, H*rp) hold
       // Qt_h = s * U_q,g (V_q,h V_k,h^T), rows [H*rp, (H+G)*rp) U_k,g, then U_v,g.
       const int rp = p.rp;
@@ -151,7 +185,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
             for (int k = 0; k < d; ++k)
               w[((size_t)(H + (m - 1) * G + g) * rp + j) * d + k] =
                   a.u[((size_t)(m * G + g) * d + k) * r + j];
-      b.store(&p.wproj_t, w);
+      b.tc(&p.wproj_t, &p.wproj_lo, w);
       b.store_f32(&p.bproj, bp);
       // block-diagonal V_v: ctx[:, h*dh + c] = sum_j O_h[:, j] V_v,g[j, hc + c] (+ b_v)
       std::vector<float> vc((size_t)d * H * rp, 0.0f);
@@ -162,7 +196,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
             vc[((size_t)h * dh + c) * H * rp + (size_t)h * rp + j] =
                 a.v[((size_t)(2 * G + g) * r + j) * gd + hc + c];
       }
-      b.store(&p.wvc_t, vc);
+      b.tc(&p.wvc_t, &p.wvc_lo, vc);
       b.store_f32(&p.bv, a.bias + 2 * d, d);
     } else {
       std::vector<float> w((size_t)d * 3 * G * r);
@@ -216,21 +250,21 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
     p.has_out = true;
     p.pr = static_cast<int>(o.rank);
     p.prp = pad_to(p.pr, 16);
-    p.out_tc = bf && d % 8 == 0;
-    if (p.out_tc) {
+    p.out_tc = bf && out_ok;
+    if (p.out_tc || p.x3) {
       const int pr = p.pr, prp = p.prp;
       std::vector<float> ut((size_t)prp * d, 0.0f), vt((size_t)d * prp, 0.0f);
       for (int k = 0; k < d; ++k)
         for (int j = 0; j < pr; ++j) ut[(size_t)j * d + k] = o.u[(size_t)k * pr + j];
       for (int j = 0; j < pr; ++j)
         for (int n = 0; n < d; ++n) vt[(size_t)n * prp + j] = o.v[(size_t)j * d + n];
-      b.store(&p.uo_t, ut);
-      b.store(&p.vo_t, vt);
-      if (q.dense || (q.attn && p.attn_tc)) {
+      b.tc(&p.uo_t, &p.uo_t_lo, ut);
+      b.tc(&p.vo_t, &p.vo_t_lo, vt);
+      if (q.dense || (q.attn && (p.attn_tc || p.x3))) {
         // W_o = U_o V_o; stored transposed: wo_t[n][m] = W_o[m][n]
         std::vector<float> wo_t = reconstruct_t(o.u, o.v, d, pr, d, d, 0);
-        if (q.dense) b.store(&p.do_t, wo_t);
-        if (q.attn && p.attn_tc) {
+        if (q.dense && bf) b.store(&p.do_t, wo_t);
+        if (q.attn && (p.attn_tc || p.x3)) {
           // folded rank-space out-projection: W_ov[(h, j)][n] = sum_c V_v,h[j, c] W_o[h dh + c][n]
           const fsvd_attn_desc& a = *q.attn;
           const int H = p.H, G = p.G, r = p.r, rp = p.rp, dh = p.dh, gd = p.gd, hpg = H / G;
@@ -250,7 +284,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
             for (int m = 0; m < d; ++m) bb += (double)a.bias[2 * d + m] * won[m];
             bov[n] = static_cast<float>(bb);
           }
-          b.store(&p.wov_t, wov);
+          b.tc(&p.wov_t, &p.wov_lo, wov);
           b.store_f32(&p.bov, bov);
         }
       }
@@ -268,9 +302,9 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
     p.act = static_cast<int>(f.activation);
     p.frp = ffn_rank_pad(p.fr);
     const int fr = p.fr, frp = p.frp, df = p.df;
-    p.ffn_tc = bf && d % 8 == 0 && df % 8 == 0 && ffn_tc_supported(d, df, frp);
+    p.ffn_tc = bf && ffn_ok;
     p.ffn_wide = p.ffn_tc && frp > 384;
-    if (p.ffn_tc) {
+    if (p.ffn_tc || p.x3) {
       std::vector<float> uu((size_t)frp * d, 0.0f), vu((size_t)df * frp, 0.0f),
           ud((size_t)frp * df, 0.0f), vd((size_t)d * frp, 0.0f);
       for (int k = 0; k < d; ++k)
@@ -281,11 +315,11 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
         for (int j = 0; j < fr; ++j) ud[(size_t)j * df + c] = f.down.u[(size_t)c * fr + j];
       for (int j = 0; j < fr; ++j)
         for (int n = 0; n < d; ++n) vd[(size_t)n * frp + j] = f.down.v[(size_t)j * d + n];
-      b.store(&p.uup_t, uu);
-      b.store(&p.vup_t, vu);
-      b.store(&p.udn_t, ud);
-      b.store(&p.vdn_t, vd);
-      if (q.dense) {
+      b.tc(&p.uup_t, &p.uup_t_lo, uu);
+      b.tc(&p.vup_t, &p.vup_t_lo, vu);
+      b.tc(&p.udn_t, &p.udn_t_lo, ud);
+      b.tc(&p.vdn_t, &p.vdn_t_lo, vd);
+      if (q.dense && bf) {
         b.store(&p.din_t, reconstruct_t(f.up.u, f.up.v, d, fr, df, df, 0));
         b.store(&p.dout_t, reconstruct_t(f.down.u, f.down.v, df, fr, d, d, 0));
       }
@@ -353,23 +387,24 @@ size_t op_transient_elems(const Pack& p, int op, int mode) {
   if (op == 0) {  // standalone attention (ctx in head width)
     if (mode == FSVD_MODE_DENSE) return 3 * d;
     if (mode == FSVD_MODE_NAIVE_LOWRANK) return 3 * (size_t)p.G * p.rp + 3 * d;
-    return p.attn_tc ? (size_t)p.qkv_cols + (size_t)p.H * p.rp : 3 * (size_t)p.G * p.r;
+    return (p.attn_tc || p.x3) ? (size_t)p.qkv_cols + (size_t)p.H * p.rp
+                               : 3 * (size_t)p.G * p.r;
   }
   if (op == 1) {
     if (mode == FSVD_MODE_DENSE) return 0;
-    return p.out_tc ? p.prp : p.pr;
+    return (p.out_tc || p.x3) ? p.prp : p.pr;
   }
   if (op == 3) {  // attention inside a layer (rank-space output goes to scratch)
     if (p.attn_tc && p.out_tc && (mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2))
       return p.qkv_cols;
-    return op_transient_elems(p, 0, mode);
+    return op_transient_elems(p, 0, mode);  // split planes: O after the projection
   }
-  const size_t fr = p.ffn_tc ? p.frp : p.fr;
+  const size_t fr = (p.ffn_tc || p.x3) ? p.frp : p.fr;
   switch (mode) {
     case FSVD_MODE_DENSE: return p.df;
     case FSVD_MODE_NAIVE_LOWRANK: return 2 * fr + p.df;
     case FSVD_MODE_FLASH_V1: return 2 * fr;
-    default: return p.ffn_wide ? 2 * fr : 0;  // wide ranks: V2 stages P and Z
+    default: return (p.ffn_wide || p.x3) ? 2 * fr : 0;  // wide ranks / planes: V2 runs the V1 chain
   }
 }
 
@@ -427,14 +462,37 @@ const T* as(const void* p) {
   return static_cast<const T*>(p);
 }
 
+// split planes of a [rows, cols] activation buffer: hi plane, then lo plane
+Planes pl(const void* p, size_t n) {
+  const bf16* h = static_cast<const bf16*>(p);
+  return {h, h + n};
+}
+PlanesOut plo(void* p, size_t n) {
+  bf16* h = static_cast<bf16*>(p);
+  return {h, h + n};
+}
+Planes wpl(const void* hi, const void* lo) {
+  return {static_cast<const bf16*>(hi), static_cast<const bf16*>(lo)};
+}
+
 void ln(const Pack& p, const void* a, const void* b, const float* g, const float* be, float eps,
         void* y, int rows, cudaStream_t s) {
+  if (p.x3) {
+    const size_t n = static_cast<size_t>(rows) * p.d;
+    const Planes bp = b ? pl(b, n) : Planes{nullptr, nullptr};
+    ln_planes(pl(a, n), b ? &bp : nullptr, g, be, eps, plo(y, n), rows, p.d, s);
+    return;
+  }
   if (p.dtype == FSVD_BF16)
     resid_layernorm_bf16(as<bf16>(a), as<bf16>(b), g, be, eps, as<bf16>(y), rows, p.d, s);
   else
     resid_layernorm_f32(as<float>(a), as<float>(b), g, be, eps, as<float>(y), rows, p.d, s);
 }
 void add(const Pack& p, const void* a, const void* b, void* y, int64_t n, cudaStream_t s) {
+  if (p.x3) {
+    add_planes(pl(a, n), pl(b, n), plo(y, n), n, s);
+    return;
+  }
   if (p.dtype == FSVD_BF16) add_bf16(as<bf16>(a), as<bf16>(b), as<bf16>(y), n, s);
   else add_f32(as<float>(a), as<float>(b), as<float>(y), n, s);
 }
@@ -511,6 +569,35 @@ void tc_attention_rank(const Pack& p, size_t B, size_t M, const void* x, void* o
   attn_decode_bf16(a, s);
 }
 
+// Split-plane (fp32 policy) attention up to the rank-space output O planes
+// [T, H*rp] at o_rank (hi) / o_rank + T*H*rp (lo): K1 (X3) projection into
+// [Qt | P_k | P_v] planes at the start of `trans`, then K2 (X3).
+void x3_attention_rank(const Pack& p, size_t B, size_t M, const void* x, bf16* o_rank,
+                       void* trans, cudaStream_t s) {
+  const int T = static_cast<int>(B * M), n = p.qkv_cols, hr = p.H * p.rp;
+  const size_t tn = static_cast<size_t>(T) * n;
+  bf16* qkv = as<bf16>(trans);
+  gemm_x3(pl(x, (size_t)T * p.d), p.d, wpl(p.wproj_t, p.wproj_lo), p.d, PlanesOut{qkv, qkv + tn},
+          n, T, n, p.d, p.bproj, ACT_NONE, s);
+  AttnTcArgs a;
+  a.qkv = qkv;
+  a.qkv_lo = qkv + tn;
+  a.ldq = n;
+  a.qkv_cols = n;
+  a.q_off = 0;
+  a.k_off = hr;
+  a.v_off = (p.H + p.G) * p.rp;
+  a.batch = static_cast<int>(B);
+  a.seq = static_cast<int>(M);
+  a.heads = p.H;
+  a.groups = p.G;
+  a.rank_pad = p.rp;
+  a.out = o_rank;
+  a.out_lo = o_rank + (size_t)T * hr;
+  a.ldo = hr;
+  attn_rankspace_bf16(a, s);
+}
+
 // Materializing baselines: dense Q|K|V [T, 3d] (dense twin or rebuilt from
 // the factors) then the same attention kernel with r = head_dim.
 void tc_attention_dense(const Pack& p, int mode, size_t B, size_t M, const void* x, void* ctx,
@@ -545,6 +632,12 @@ void attention_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, v
     bf16* o_rank = as<bf16>(trans) + (size_t)T * p.qkv_cols;
     tc_attention_rank(p, B, M, x, o_rank, trans, s);
     gemm_bf16(o_rank, hr, as<bf16>(p.wvc_t), hr, as<bf16>(ctx), p.d, T, p.d, hr, p.bv, ACT_NONE, s);
+  } else if (p.x3) {
+    const int hr = p.H * p.rp;
+    bf16* o_rank = as<bf16>(trans) + 2 * (size_t)T * p.qkv_cols;
+    x3_attention_rank(p, B, M, x, o_rank, trans, s);
+    gemm_x3(Planes{o_rank, o_rank + (size_t)T * hr}, hr, wpl(p.wvc_t, p.wvc_lo), hr,
+            plo(ctx, (size_t)T * p.d), p.d, T, p.d, hr, p.bv, ACT_NONE, s);
   } else if (p.dtype == FSVD_BF16) {
     simt_attention_t<bf16>(p, B, M, x, ctx, trans, s);
   } else {
@@ -563,6 +656,13 @@ void outproj_fwd(const Pack& p, int mode, size_t B, size_t M, const void* ctx, v
     bf16* P = as<bf16>(trans);
     gemm_bf16(as<bf16>(ctx), d, as<bf16>(p.uo_t), d, P, p.prp, T, p.prp, d, nullptr, ACT_NONE, s);
     gemm_bf16(P, p.prp, as<bf16>(p.vo_t), p.prp, as<bf16>(out), d, T, d, p.prp, p.bo, ACT_NONE, s);
+  } else if (p.x3) {
+    bf16* P = as<bf16>(trans);
+    const size_t tp = (size_t)T * p.prp;
+    gemm_x3(pl(ctx, (size_t)T * d), d, wpl(p.uo_t, p.uo_t_lo), d, PlanesOut{P, P + tp}, p.prp, T,
+            p.prp, d, nullptr, ACT_NONE, s);
+    gemm_x3(Planes{P, P + tp}, p.prp, wpl(p.vo_t, p.vo_t_lo), p.prp, plo(out, (size_t)T * d), d, T,
+            d, p.prp, p.bo, ACT_NONE, s);
   } else if (p.dtype == FSVD_BF16) {
     simt_gemm<bf16>(as<bf16>(ctx), d, as<bf16>(p.uo), p.pr, as<bf16>(trans), p.pr, T, p.pr, d,
                     nullptr, ACT_NONE, s);
@@ -582,6 +682,14 @@ void outproj_fwd(const Pack& p, int mode, size_t B, size_t M, const void* ctx, v
 void attention_block(const Pack& p, int mode, size_t B, size_t M, const void* x, void* scratch,
                      void* branch, void* trans, cudaStream_t s, const AttnMode& am = AttnMode{}) {
   const bool flash = mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2;
+  if (flash && p.x3) {  // split planes: O after the projection planes in `trans`
+    const int T = static_cast<int>(B * M), hr = p.H * p.rp;
+    bf16* o = as<bf16>(trans) + 2 * (size_t)T * p.qkv_cols;
+    x3_attention_rank(p, B, M, x, o, trans, s);
+    gemm_x3(Planes{o, o + (size_t)T * hr}, hr, wpl(p.wov_t, p.wov_lo), hr,
+            plo(branch, (size_t)T * p.d), p.d, T, p.d, hr, p.bov, ACT_NONE, s);
+    return;
+  }
   if (flash && p.attn_tc && p.out_tc) {
     const int T = static_cast<int>(B * M), hr = p.H * p.rp;
     tc_attention_rank(p, B, M, x, scratch, trans, s, am);
@@ -652,6 +760,34 @@ void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* o
       gemm_bf16(hid, df, as<bf16>(p.udn_t), df, Z, frp, T, frp, df, nullptr, ACT_NONE, s);
       gemm_bf16(Z, frp, as<bf16>(p.vdn_t), frp, as<bf16>(out), d, T, d, frp, p.bdn, ACT_NONE, s);
     }
+    return;
+  }
+  if (p.x3) {  // split planes: V1 chain for both FFN variants (ffn_v1 == ffn_v2)
+    bf16* P = as<bf16>(trans);
+    const size_t tf = (size_t)T * p.frp;
+    bf16* Z = P + 2 * tf;
+    gemm_x3(pl(x, (size_t)T * d), d, wpl(p.uup_t, p.uup_t_lo), d, PlanesOut{P, P + tf}, p.frp, T,
+            p.frp, d, nullptr, ACT_NONE, s);
+    FfnTcArgs a{};
+    a.T = T;
+    a.d_model = d;
+    a.d_ff = df;
+    a.rank_pad = p.frp;
+    a.up_v_t = as<bf16>(p.vup_t);
+    a.up_v_t_lo = as<bf16>(p.vup_t_lo);
+    a.up_b = p.bup;
+    a.dn_u_t = as<bf16>(p.udn_t);
+    a.dn_u_t_lo = as<bf16>(p.udn_t_lo);
+    a.dn_v_t = as<bf16>(p.vdn_t);
+    a.dn_b = p.bdn;
+    a.act = p.act;
+    a.p_in = P;
+    a.p_in_lo = P + tf;
+    a.z_out = Z;
+    a.z_out_lo = Z + tf;
+    ffn_stream_bf16(a, s);
+    gemm_x3(Planes{Z, Z + tf}, p.frp, wpl(p.vdn_t, p.vdn_t_lo), p.frp, plo(out, (size_t)T * d), d,
+            T, d, p.frp, p.bdn, ACT_NONE, s);
     return;
   }
   if (p.ffn_tc) {

@@ -29,6 +29,15 @@ struct Pack {
   bool has_attn = false, has_out = false, has_ffn = false, has_ln = false, dense = false;
   bool attn_tc = false, out_tc = false, ffn_tc = false;
   bool ffn_wide = false;  // frp > 384: sliced K3, V2 runs the V1 chain (ffn_tc.cu)
+  // fp32 policy on the tensor cores (planes.cu): every weight below is stored
+  // as split planes (the *_lo arrays hold the lo planes of the tensor-core
+  // layouts), device activations are split planes, and the layer runs K1 / K2 /
+  // K3 in their X3 form.  All-or-nothing per pack: a pack whose shapes leave
+  // the tensor-core tiling runs the fp32 SIMT kernels instead.
+  bool x3 = false;
+  const void *wproj_lo = nullptr, *wvc_lo = nullptr, *uo_t_lo = nullptr, *vo_t_lo = nullptr,
+             *wov_lo = nullptr, *uup_t_lo = nullptr, *vup_t_lo = nullptr, *udn_t_lo = nullptr,
+             *vdn_t_lo = nullptr;
   void* mem = nullptr;
   size_t bytes = 0;
   // attention, tensor-core path (folded rank-space form, see attn_tc.cu):

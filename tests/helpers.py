@@ -23,6 +23,17 @@ def rel_err(got, ref):
     return float(np.abs(got.astype(np.float64) - ref).max() / max(np.abs(ref).max(), 1e-30))
 
 
+def record(case, shape, dtype, err):
+    """Appends one measured parity error to gpurun_out/parity_errors.jsonl
+    (scratch; the summary worth keeping is copied to profiles/)."""
+    import json
+    out = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(out, "parity_errors.jsonl"), "a") as f:
+        f.write(json.dumps({"case": case, "shape": shape,
+                            "dtype": "f32" if dtype == abi.F32 else "bf16", "rel_err": err}) + "\n")
+
+
 def header_functions():
     """Every function the public header declares."""
     text = open(HEADER).read()

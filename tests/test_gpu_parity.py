@@ -124,11 +124,17 @@ def test_sublayers_match_oracle(L, ora, shape, dtype):
     layer, x = prep(layer, x, dtype)
     t = tol(dtype)
     ref = ora.attention(x, layer.attn, heads, PLAN)
-    assert H.rel_err(H.attention(x, layer.attn, heads, PLAN, dtype), ref) <= t
+    e = H.rel_err(H.attention(x, layer.attn, heads, PLAN, dtype), ref)
+    H.record("sublayer_attention", shape[0], dtype, e)
+    assert e <= t
     ctx = ref if dtype == abi.F32 else bf16_round(ref)
-    assert H.rel_err(H.outproj(ctx, layer.out_proj, dtype), ora.outproj(ctx, layer.out_proj)) <= t
+    e = H.rel_err(H.outproj(ctx, layer.out_proj, dtype), ora.outproj(ctx, layer.out_proj))
+    H.record("sublayer_outproj", shape[0], dtype, e)
+    assert e <= t
     for v in (1, 2):
-        assert H.rel_err(H.ffn(v, x, layer.ffn, PLAN, dtype), ora.ffn(v, x, layer.ffn, PLAN)) <= t
+        e = H.rel_err(H.ffn(v, x, layer.ffn, PLAN, dtype), ora.ffn(v, x, layer.ffn, PLAN))
+        H.record(f"sublayer_ffn_v{v}", shape[0], dtype, e)
+        assert e <= t
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=[s[0] for s in SHAPES])
@@ -142,6 +148,8 @@ def test_layer_matches_oracle(L, ora, shape, dtype, mode):
     for pre in (False, True):
         ref = ora.run_model(x, [layer], mode, PLAN, pre_ln=pre)
         got = H.run_layer(x, layer, mode, PLAN, dtype, pre_ln=pre)
+        H.record(f"layer_{'v1' if mode == abi.MODE_FLASH_V1 else 'v2'}_{'pre' if pre else 'post'}",
+                 shape[0], dtype, H.rel_err(got, ref))
         assert H.rel_err(got, ref) <= tol(dtype), (pre, H.rel_err(got, ref))
 
 
@@ -155,6 +163,7 @@ def test_four_layer_model_matches_oracle(L, ora, dtype):
         x = bf16_round(x)
     ref = ora.run_model(x, layers, abi.MODE_FLASH_V2, PLAN)
     got = H.run_model(x, layers, abi.MODE_FLASH_V2, PLAN, dtype)
+    H.record("four_layer_model", "d256", dtype, H.rel_err(got, ref))
     assert H.rel_err(got, ref) <= tol(dtype)
 
 
@@ -214,7 +223,11 @@ def test_zero_weight_layer_is_double_layernorm(L, ora):
         return g * (v - mu) / np.sqrt(var + 1e-5) + b
     want = ln(ln(x.astype(np.float64), layer.ln1_gamma, layer.ln1_beta), layer.ln2_gamma, layer.ln2_beta)
     got = H.run_layer(x, layer, abi.MODE_FLASH_V1, PLAN, abi.F32)
-    assert np.abs(got - want).max() <= 1e-5
+    # the reference's own KAT bar is 1e-6 (fp32 end to end); the fp32 policy
+    # here stores activations as split bf16 planes (2^-16 relative per stored
+    # value, planes.cu), so the bar is the north star's fp32 bound, 1e-4
+    # (measured 2.9e-5 on the B200)
+    assert np.abs(got - want).max() <= H.TOL_F32 * np.abs(want).max()
 
 
 def test_tile_plan_invariance_and_determinism(L, ora):
@@ -588,6 +601,22 @@ def test_host_dropin_pack_cache_hits_and_invalidates(L, ora):
     assert H.rel_err(c, ref) <= H.TOL_BF16
     abi.check(L.fsvd_pack_cache_clear())
     assert stats()[0] == 0
+
+
+@pytest.mark.parametrize("shape", [s for s in SHAPES if s[0] != "tiny_odd"] + SWEEP[:2],
+                         ids=[s[0] for s in SHAPES if s[0] != "tiny_odd"] + [s[0] for s in SWEEP[:2]])
+def test_f32_packs_run_on_tensor_cores(L, ora, shape):
+    """The fp32 policy runs the tcgen05 kernels in split-plane form (K1 / K2 /
+    K3 X3) for every shape inside the tensor-core tiling; only shapes outside
+    it (d_model not a multiple of 64 for the FFN, per-head rank > 64) keep the
+    CUDA-core kernels."""
+    _, d, df, heads, groups, r, pr, fr, B, M = shape
+    layer = oracle.rand_layer(ora, d, df, heads, groups, r, 5000 + d, pr, fr)
+    desc = layer.desc()
+    p = C.c_void_p()
+    abi.check(L.fsvd_layer_pack_create(C.byref(desc), abi.F32, 0, C.byref(p)))
+    assert L.fsvd_layer_pack_uses_tensor_cores(p) == 1
+    L.fsvd_layer_pack_destroy(p)
 
 
 # ------------------------------------------------------------------ empty inputs
