@@ -173,18 +173,33 @@ struct FfnPack {
   }
 };
 
+// One EncoderLayer: whichever of its representations it carries (encoder.hpp:
+// 49-67) -- factorized attention + output projection, factorized FFN, dense
+// weights -- after the reference's own EncoderLayer::validate().
 struct LayerPack {
   std::unique_ptr<AttnPack> attn;
+  fsvd_dense_layer dense{};
   fsvd_layer_desc d{};
   explicit LayerPack(const EncoderLayer& l) {
-    if (!l.attn_factors || !l.out_proj || !l.ffn_factors)
-      throw ConfigError("flashsvd::b200 runs factorized layers: attention, output-projection "
-                        "and FFN factors are required (dense modes use their dense twin)");
-    attn = std::make_unique<AttnPack>(*l.attn_factors);
+    l.validate();
     d.heads = l.heads;
-    d.attn = attn->d;
-    d.out_proj = LinearPack(*l.out_proj).d;
-    d.ffn = FfnPack(*l.ffn_factors).d;
+    d.attn.d_model = l.d_model();
+    if (l.attn_factors) {
+      attn = std::make_unique<AttnPack>(*l.attn_factors);
+      d.attn = attn->d;
+      d.out_proj = LinearPack(*l.out_proj).d;
+    }
+    if (l.ffn_factors) d.ffn = FfnPack(*l.ffn_factors).d;
+    if (l.attn_dense && l.ffn_dense) {
+      const DenseAttentionWeights& a = *l.attn_dense;
+      const DenseFfnWeights& f = *l.ffn_dense;
+      dense = fsvd_dense_layer{l.d_model(), f.b_in.numel(), a.wq.data(), a.bq.data(),
+                               a.wk.data(), a.bk.data(), a.wv.data(), a.bv.data(),
+                               a.wo.data(), a.bo.data(), f.w_in.data(), f.b_in.data(),
+                               f.w_out.data(), f.b_out.data()};
+      d.dense = &dense;
+      if (!l.ffn_factors) d.ffn.activation = static_cast<fsvd_activation>(static_cast<int>(f.activation));
+    }
     d.ln1_gamma = l.ln1.gamma.data();
     d.ln1_beta = l.ln1.beta.data();
     d.ln1_eps = l.ln1.eps;
@@ -193,6 +208,19 @@ struct LayerPack {
     d.ln2_eps = l.ln2.eps;
   }
 };
+
+// encoder.cpp:27-35 (check_mode_weights), same exception and message: the
+// drop-in runs Dense mode only on a layer's own dense weights, like the
+// reference (the C-ABI alone also offers the dense twin of a factor-only layer).
+inline void check_mode_weights(const EncoderLayer& layer, RunMode mode) {
+  if (mode == RunMode::Dense) {
+    if (!layer.attn_dense || !layer.ffn_dense)
+      throw ConfigError("dense mode needs dense weights on both sublayers");
+  } else if (!layer.attn_factors || !layer.out_proj || !layer.ffn_factors) {
+    throw ConfigError(std::string(mode_name(mode)) +
+                      " mode needs factorized weights on both sublayers");
+  }
+}
 
 inline fsvd_tile_plan plan_of(const TilePlan& p) {
   return fsvd_tile_plan{p.bm, p.br, p.bdf, p.sram_budget_bytes};
@@ -285,7 +313,10 @@ inline void run_model(const Tensor& x, const std::vector<EncoderLayer>& layers, 
   }
   std::vector<detail::LayerPack> packs;
   packs.reserve(layers.size());
-  for (const EncoderLayer& l : layers) packs.emplace_back(l);
+  for (const EncoderLayer& l : layers) {
+    packs.emplace_back(l);
+    detail::check_mode_weights(l, mode);
+  }
   std::vector<fsvd_layer_desc> descs;
   for (const auto& p : packs) descs.push_back(p.d);
   detail::MirrorMeter mm;
@@ -304,6 +335,7 @@ inline void run_layer(const Tensor& x, const EncoderLayer& layer, RunMode mode,
                       const TilePlan& plan, MemoryMeter& meter, Tensor& out,
                       const LayerRunOptions& opts = {}) {
   detail::LayerPack pk(layer);
+  detail::check_mode_weights(layer, mode);
   if (x.ndim() != 3 || x.shape()[2] != layer.d_model())
     throw ShapeError("run_layer: x must be (batch, seq, d_model)");
   if (static_cast<const void*>(&out) == static_cast<const void*>(&x))

@@ -127,7 +127,19 @@ typedef struct fsvd_ffn_desc {
   fsvd_activation activation;
 } fsvd_ffn_desc;
 
-/* EncoderLayer (encoder.hpp:49-67), fully factorized form. */
+struct fsvd_dense_layer; /* dense weights, defined below */
+
+/* EncoderLayer (encoder.hpp:49-67).  Like the reference, a layer carries
+ * factorized weights, dense weights, or both:
+ *   - factorized attention: attn.u != NULL (with out_proj); attn.d_model is
+ *     d_model in every case;
+ *   - factorized FFN: ffn.up.u != NULL; ffn.activation is also the dense
+ *     FFN's activation;
+ *   - dense weights (DenseAttentionWeights + DenseFfnWeights): dense != NULL.
+ * RunMode::Dense uses the dense weights (encoder.cpp:27-35 check_mode_weights);
+ * the flash / naive modes need the factors.  Device packs built with dense=1
+ * from a factor-only layer get the dense twin instead (dense_equivalent,
+ * encoder.cpp:295-331). */
 typedef struct fsvd_layer_desc {
   size_t heads;
   fsvd_attn_desc attn;
@@ -135,6 +147,7 @@ typedef struct fsvd_layer_desc {
   fsvd_ffn_desc ffn;
   const float* ln1_gamma; const float* ln1_beta; float ln1_eps;
   const float* ln2_gamma; const float* ln2_beta; float ln2_eps;
+  const struct fsvd_dense_layer* dense; /* NULL: no dense weights */
 } fsvd_layer_desc;
 
 /* ------------------------------------------------------------------ */

@@ -70,13 +70,27 @@ FfnFactors ffn_set(const fsvd_ffn_desc& d) {
   f.activation = static_cast<Activation>(d.activation);
   return f;
 }
+// The descriptor's optional parts (include/fsvd_b200.h): factorized attention
+// when attn.u is set, factorized FFN when ffn.up.u is set, dense weights when
+// L.dense is set -- the reference EncoderLayer's optionals.
 EncoderLayer layer_of(const fsvd_layer_desc& L) {
   EncoderLayer e;
   e.heads = L.heads;
-  e.attn_factors = attn_set(L.attn);
-  e.out_proj = linear(L.out_proj);
-  e.ffn_factors = ffn_set(L.ffn);
+  if (L.attn.u) {
+    e.attn_factors = attn_set(L.attn);
+    e.out_proj = linear(L.out_proj);
+  }
+  if (L.ffn.up.u) e.ffn_factors = ffn_set(L.ffn);
   const size_t d = L.attn.d_model;
+  if (L.dense) {
+    const fsvd_dense_layer& w = *L.dense;
+    const size_t df = w.d_ff;
+    e.attn_dense = DenseAttentionWeights{mat(w.wq, d, d), vec(w.bq, d), mat(w.wk, d, d),
+                                         vec(w.bk, d),    mat(w.wv, d, d), vec(w.bv, d),
+                                         mat(w.wo, d, d), vec(w.bo, d)};
+    e.ffn_dense = DenseFfnWeights{mat(w.w_in, d, df), vec(w.b_in, df), mat(w.w_out, df, d),
+                                  vec(w.b_out, d), static_cast<Activation>(L.ffn.activation)};
+  }
   e.ln1.gamma = vec(L.ln1_gamma, d);
   e.ln1.beta = vec(L.ln1_beta, d);
   e.ln1.eps = L.ln1_eps;
@@ -203,7 +217,9 @@ int ref_run_model(const float* x, size_t b, size_t m, const fsvd_layer_desc* lay
     std::vector<EncoderLayer> ls;
     for (size_t i = 0; i < n_layers; ++i) {
       EncoderLayer e = layer_of(layers[i]);
-      ls.push_back(mode == FSVD_MODE_DENSE ? dense_equivalent(e) : std::move(e));
+      // a factor-only layer in Dense mode runs its dense twin (the C-ABI's
+      // documented extension); a layer carrying dense weights uses them
+      ls.push_back(mode == FSVD_MODE_DENSE && !e.attn_dense ? dense_equivalent(e) : std::move(e));
     }
     Tensor xt({b, m, d}, std::vector<float>(x, x + b * m * d));
     Tensor o({b, m, d});
@@ -222,7 +238,7 @@ int ref_run_layer(const float* x, size_t b, size_t m, const fsvd_layer_desc* L, 
   return guard([&] {
     const size_t d = L->attn.d_model;
     EncoderLayer e = layer_of(*L);
-    if (mode == FSVD_MODE_DENSE) e = dense_equivalent(e);
+    if (mode == FSVD_MODE_DENSE && !e.attn_dense) e = dense_equivalent(e);
     Tensor xt({b, m, d}, std::vector<float>(x, x + b * m * d));
     Tensor o({b, m, d});
     MemoryMeter meter;

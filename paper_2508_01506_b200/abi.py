@@ -80,7 +80,8 @@ class FfnDesc(C.Structure):
 class LayerDesc(C.Structure):
     _fields_ = [("heads", _sz), ("attn", AttnDesc), ("out_proj", LinearDesc), ("ffn", FfnDesc),
                 ("ln1_gamma", _fp), ("ln1_beta", _fp), ("ln1_eps", C.c_float),
-                ("ln2_gamma", _fp), ("ln2_beta", _fp), ("ln2_eps", C.c_float)]
+                ("ln2_gamma", _fp), ("ln2_beta", _fp), ("ln2_eps", C.c_float),
+                ("dense", C.POINTER(DenseLayer))]
 
 
 def fptr(arr):

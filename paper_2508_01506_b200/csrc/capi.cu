@@ -353,6 +353,18 @@ uint64_t hash_request(const PackRequest& q, fsvd_dtype dt) {
   } else {
     hdr.push_back(0);
   }
+  if (q.dense_w) {
+    const fsvd_dense_layer& w = *q.dense_w;
+    const size_t d = w.d_model, df = w.d_ff;
+    hdr.insert(hdr.end(), {3, d, df, static_cast<uint64_t>(q.dense_act)});
+    for (const float* m : {w.wq, w.wk, w.wv, w.wo}) spans.push_back({m, 4 * d * d});
+    for (const float* b : {w.bq, w.bk, w.bv, w.bo, w.b_out}) spans.push_back({b, 4 * d});
+    spans.push_back({w.w_in, 4 * d * df});
+    spans.push_back({w.b_in, 4 * df});
+    spans.push_back({w.w_out, 4 * df * d});
+  } else {
+    hdr.push_back(0);
+  }
   for (const float* v : {q.ln1g, q.ln1b, q.ln2g, q.ln2b}) {
     hdr.push_back(v != nullptr);
     if (v) spans.push_back({v, 4 * q.d_model});
@@ -410,6 +422,28 @@ std::shared_ptr<Pack> cached_pack(const PackRequest& q, fsvd_dtype dt) {
     c.map.erase(lru);
   }
   return ins.first->second.pack;
+}
+
+// Pack request of one layer descriptor: each representation only if present.
+PackRequest request_of(const fsvd_layer_desc& L, bool dense) {
+  PackRequest q;
+  if (L.attn.u) {
+    q.attn = &L.attn;
+    q.out_proj = &L.out_proj;
+  }
+  if (L.ffn.up.u) q.ffn = &L.ffn;
+  q.heads = L.heads;
+  q.ln1g = L.ln1_gamma;
+  q.ln1b = L.ln1_beta;
+  q.ln2g = L.ln2_gamma;
+  q.ln2b = L.ln2_beta;
+  q.eps1 = L.ln1_eps;
+  q.eps2 = L.ln2_eps;
+  q.d_model = L.attn.d_model;
+  q.dense = dense;
+  q.dense_w = dense ? L.dense : nullptr;
+  q.dense_act = static_cast<int>(L.ffn.activation);
+  return q;
 }
 
 std::shared_ptr<Pack> pack_attention(const fsvd_attn_desc& a, size_t heads, fsvd_dtype dt) {
@@ -540,9 +574,10 @@ void host_ffn(int variant, const float* x, size_t B, size_t M, size_t W, const f
 // device work runs separately on the whole model (layer_fwd).
 void meter_layer(Meter* meter, const fsvd_layer_desc& L, int mode, const fsvd_tile_plan& plan,
                  bool pre_ln, const std::string& pfx, size_t B, size_t M) {
-  const size_t d = L.attn.d_model, n = B * M * d, G = L.attn.groups, r = L.attn.rank,
-               gd = d / G, df = L.ffn.up.out_dim, fr = L.ffn.up.rank, pr = L.out_proj.rank,
-               H = L.heads;
+  const size_t d = L.attn.d_model, n = B * M * d, G = L.attn.groups ? L.attn.groups : 1,
+               r = L.attn.rank, gd = d / G,
+               df = L.ffn.up.u ? L.ffn.up.out_dim : (L.dense ? L.dense->d_ff : 0),
+               fr = L.ffn.up.rank, pr = L.out_proj.rank, H = L.heads;
   MeterBuffer ctx(meter, pfx + ".attn_ctx", MeterClass::Excluded, n);
   MeterBuffer branch(meter, pfx + ".sublayer_out", MeterClass::Excluded, n);
   MeterBuffer resid(meter, pfx + ".resid", MeterClass::Excluded, n);
@@ -627,6 +662,7 @@ void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_lay
   }
   for (size_t i = 0; i < n_layers; ++i) {
     validate_layer(layers[i]);
+    check_mode_weights(layers[i], mode, true);
     if (layers[i].attn.d_model != W) fail(Kind::Shape, "run_layer: x must be (batch, seq, d_model)");
   }
   // meter: encoder.cpp:274-292 (ping/pong only for more than one layer)
@@ -646,22 +682,12 @@ void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_lay
   std::vector<std::shared_ptr<Pack>> packs;
   size_t ws = 0, pack_bytes = 0;
   for (size_t i = 0; i < n_layers; ++i) {
-    PackRequest q;
-    q.attn = &layers[i].attn;
-    q.heads = layers[i].heads;
-    q.out_proj = &layers[i].out_proj;
-    q.ffn = &layers[i].ffn;
-    q.ln1g = layers[i].ln1_gamma;
-    q.ln1b = layers[i].ln1_beta;
-    q.ln2g = layers[i].ln2_gamma;
-    q.ln2b = layers[i].ln2_beta;
-    q.eps1 = layers[i].ln1_eps;
-    q.eps2 = layers[i].ln2_eps;
-    q.d_model = W;
-    q.dense = mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK;
+    const PackRequest q =
+        request_of(layers[i], mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK);
     packs.emplace_back(cached_pack(q, dt));
     if (q.dense && !packs.back()->dense)
-      fail(Kind::Config, "dense / naive_lowrank modes run only on the bf16 tensor-core path");
+      fail(Kind::Config, "dense / naive_lowrank modes run on the tensor cores only: head width "
+                         "<= 64, d_model and d_ff multiples of 8");
     ws = std::max(ws, layer_workspace_bytes(*packs.back(), B * M, mode, pre_ln != 0));
     pack_bytes += packs.back()->bytes;
     if (packs.back()->x3 != packs[0]->x3)
@@ -852,19 +878,7 @@ fsvd_status fsvd_layer_pack_create(const fsvd_layer_desc* layer, fsvd_dtype dtyp
     check_dtype(dtype);
     validate_layer(*layer);
     require_device();
-    PackRequest q;
-    q.attn = &layer->attn;
-    q.heads = layer->heads;
-    q.out_proj = &layer->out_proj;
-    q.ffn = &layer->ffn;
-    q.ln1g = layer->ln1_gamma;
-    q.ln1b = layer->ln1_beta;
-    q.ln2g = layer->ln2_gamma;
-    q.ln2b = layer->ln2_beta;
-    q.eps1 = layer->ln1_eps;
-    q.eps2 = layer->ln2_eps;
-    q.d_model = layer->attn.d_model;
-    q.dense = dense != 0;
+    const PackRequest q = request_of(*layer, dense != 0);
     std::unique_ptr<Pack> p(build_pack(q, dtype));
     *out = new fsvd_layer_pack{p.release()};
   });

@@ -111,6 +111,93 @@ std::vector<float> reconstruct_t(const float* u, const float* v, int K, int R, i
 
 }  // namespace
 
+namespace {
+// Dense-mode weights (see Pack): from q.dense_w, or rebuilt from the factors
+// exactly as dense_equivalent does (encoder.cpp:295-331: W = U V per group,
+// reconstruct_t's fp32 j-ascending sums).
+void build_dense(const PackRequest& q, Pack& p, Builder& b) {
+  const int d = p.d, H = static_cast<int>(q.heads), dh = d / H;
+  const int dhp = dh <= 16 ? 16 : dh <= 32 ? 32 : 64, hp = H * dhp;
+  const double sc = 1.4426950408889634 / std::sqrt(static_cast<double>(dh));
+  const fsvd_dense_layer* w = q.dense_w;
+  const int df = w ? static_cast<int>(w->d_ff) : static_cast<int>(q.ffn->up.out_dim);
+  p.dhp = dhp;
+  p.ddf = df;
+  p.H = H;
+  p.dh = dh;
+  p.dact = q.ffn ? static_cast<int>(q.ffn->activation) : q.dense_act;
+  // W^T of the three projections, [n][k] = W[k][n]
+  std::vector<float> wt[3];
+  std::vector<float> bias(3 * (size_t)d);
+  if (w) {
+    const float* ws[3] = {w->wq, w->wk, w->wv};
+    const float* bs[3] = {w->bq, w->bk, w->bv};
+    for (int m = 0; m < 3; ++m) {
+      wt[m].resize((size_t)d * d);
+      for (int k = 0; k < d; ++k)
+        for (int n = 0; n < d; ++n) wt[m][(size_t)n * d + k] = ws[m][(size_t)k * d + n];
+      std::copy(bs[m], bs[m] + d, bias.begin() + (size_t)m * d);
+    }
+  } else {
+    const fsvd_attn_desc& a = *q.attn;
+    const int G = static_cast<int>(a.groups), r = static_cast<int>(a.rank), gd = d / G;
+    for (int m = 0; m < 3; ++m) {
+      wt[m].resize((size_t)d * d);
+      for (int g = 0; g < G; ++g) {
+        std::vector<float> part = reconstruct_t(a.u + (size_t)(m * G + g) * d * r,
+                                                a.v + (size_t)(m * G + g) * r * gd, d, r, gd, gd, 0);
+        std::copy(part.begin(), part.end(), wt[m].begin() + (size_t)g * gd * d);
+      }
+    }
+    std::copy(a.bias, a.bias + 3 * (size_t)d, bias.begin());
+  }
+  std::vector<float> qkv((size_t)3 * hp * d, 0.0f), bq((size_t)3 * hp, 0.0f);
+  for (int m = 0; m < 3; ++m)
+    for (int h = 0; h < H; ++h)
+      for (int c = 0; c < dh; ++c) {
+        const float f = m == 0 ? static_cast<float>(sc) : 1.0f;
+        const size_t row = (size_t)m * hp + (size_t)h * dhp + c, src = (size_t)h * dh + c;
+        for (int k = 0; k < d; ++k) qkv[row * d + k] = wt[m][src * d + k] * f;
+        bq[row] = bias[(size_t)m * d + src] * f;
+      }
+  b.tc(&p.dqkv_t, &p.dqkv_lo, qkv);
+  b.store_f32(&p.dqkv_b, bq);
+  // output projection W_o^T with padded input columns
+  std::vector<float> wo_t = w ? std::vector<float>((size_t)d * d)
+                              : reconstruct_t(q.out_proj->u, q.out_proj->v, d,
+                                              static_cast<int>(q.out_proj->rank), d, d, 0);
+  if (w)
+    for (int k = 0; k < d; ++k)
+      for (int n = 0; n < d; ++n) wo_t[(size_t)n * d + k] = w->wo[(size_t)k * d + n];
+  std::vector<float> wop((size_t)d * hp, 0.0f);
+  for (int n = 0; n < d; ++n)
+    for (int h = 0; h < H; ++h)
+      for (int c = 0; c < dh; ++c)
+        wop[(size_t)n * hp + (size_t)h * dhp + c] = wo_t[(size_t)n * d + h * dh + c];
+  b.tc(&p.do_t, &p.do_lo, wop);
+  b.store_f32(&p.dbo, w ? w->bo : q.out_proj->bias, d);
+  // FFN
+  std::vector<float> win_t, wout_t;
+  if (w) {
+    win_t.resize((size_t)df * d);
+    wout_t.resize((size_t)d * df);
+    for (int k = 0; k < d; ++k)
+      for (int n = 0; n < df; ++n) win_t[(size_t)n * d + k] = w->w_in[(size_t)k * df + n];
+    for (int k = 0; k < df; ++k)
+      for (int n = 0; n < d; ++n) wout_t[(size_t)n * df + k] = w->w_out[(size_t)k * d + n];
+  } else {
+    const fsvd_ffn_desc& f = *q.ffn;
+    const int fr = static_cast<int>(f.up.rank);
+    win_t = reconstruct_t(f.up.u, f.up.v, d, fr, df, df, 0);
+    wout_t = reconstruct_t(f.down.u, f.down.v, df, fr, d, d, 0);
+  }
+  b.tc(&p.din_t, &p.din_lo, win_t);
+  b.tc(&p.dout_t, &p.dout_lo, wout_t);
+  b.store_f32(&p.dbin, w ? w->b_in : q.ffn->up.bias, df);
+  b.store_f32(&p.dbout, w ? w->b_out : q.ffn->down.bias, d);
+}
+}  // namespace
+
 Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
   auto P = std::make_unique<Pack>();
   Pack& p = *P;
@@ -134,7 +221,16 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
     const int df = static_cast<int>(q.ffn->up.out_dim);
     ffn_ok = d % 8 == 0 && df % 8 == 0 && ffn_tc_supported(d, df, ffn_rank_pad(static_cast<int>(q.ffn->up.rank)));
   }
-  p.x3 = !bf && attn_ok && out_ok && ffn_ok;
+  // Dense-mode weights: any head width <= 64 (padded), 16-byte row pitches
+  bool dense_ok = false;
+  if (q.dense && q.heads > 0 && d % q.heads == 0) {
+    const int dh = d / static_cast<int>(q.heads);
+    const int df = q.dense_w ? static_cast<int>(q.dense_w->d_ff)
+                             : (q.ffn ? static_cast<int>(q.ffn->up.out_dim) : 0);
+    dense_ok = dh <= 64 && d % 8 == 0 && df % 8 == 0 && df > 0 &&
+               (q.dense_w != nullptr || (q.attn && q.out_proj && q.ffn));
+  }
+  p.x3 = !bf && attn_ok && out_ok && ffn_ok && (!q.dense || dense_ok);
   b.x3 = p.x3;
 
   if (q.attn) {
@@ -210,23 +306,10 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
       b.store(&p.attn_v, std::vector<float>(a.v, a.v + (size_t)3 * G * r * gd));
     }
     b.store_f32(&p.attn_b, a.bias, 3 * (size_t)d);
-    if (q.dense && p.attn_tc && dh == 64) {
-      // dense twin W = U V per group (encoder.cpp:295-331); Q rows scaled by s
+    if (q.dense && (p.attn_tc || p.x3) && (dh == 16 || dh == 32 || dh == 64)) {
+      // NaiveLowRank (attention.cpp:271-292): P = X [U_q|U_k|U_v], then the
+      // block-diagonal V rebuilds dense Q|K|V [T, 3d] (Q scaled by s)
       const float sc = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(dh)));
-      std::vector<float> wt((size_t)3 * d * d);
-      for (int m = 0; m < 3; ++m)
-        for (int g = 0; g < G; ++g) {
-          std::vector<float> part = reconstruct_t(a.u + (size_t)(m * G + g) * d * r,
-                                                  a.v + (size_t)(m * G + g) * r * gd, d, r, gd,
-                                                  gd, 0);
-          for (int c = 0; c < gd; ++c)
-            for (int k = 0; k < d; ++k)
-              wt[((size_t)m * d + g * gd + c) * d + k] = part[(size_t)c * d + k] * (m == 0 ? sc : 1.0f);
-        }
-      b.store(&p.dqkv_t, wt);
-      std::vector<float> bq(a.bias, a.bias + 3 * (size_t)d);
-      for (int i = 0; i < d; ++i) bq[i] *= sc;
-      b.store_f32(&p.dqkv_b, bq);
       const int rp = p.rp;
       std::vector<float> wn((size_t)3 * G * rp * d, 0.0f);
       for (int m = 0; m < 3; ++m)
@@ -234,7 +317,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
           for (int j = 0; j < r; ++j)
             for (int k = 0; k < d; ++k)
               wn[((size_t)(m * G + g) * rp + j) * d + k] = a.u[((size_t)(m * G + g) * d + k) * r + j];
-      b.store(&p.wpn_t, wn);
+      b.tc(&p.wpn_t, &p.wpn_lo, wn);
       std::vector<float> bd((size_t)3 * d * 3 * G * rp, 0.0f);
       for (int m = 0; m < 3; ++m)
         for (int g = 0; g < G; ++g)
@@ -242,7 +325,10 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
             for (int j = 0; j < r; ++j)
               bd[((size_t)m * d + g * gd + c) * (3 * G * rp) + (m * G + g) * rp + j] =
                   a.v[((size_t)(m * G + g) * r + j) * gd + c] * (m == 0 ? sc : 1.0f);
-      b.store(&p.dvbd_t, bd);
+      b.tc(&p.dvbd_t, &p.dvbd_lo, bd);
+      std::vector<float> bq(a.bias, a.bias + 3 * (size_t)d);
+      for (int i = 0; i < d; ++i) bq[i] *= sc;
+      b.store_f32(&p.nqkv_b, bq);
     }
   }
   if (q.out_proj) {
@@ -260,10 +346,9 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
         for (int n = 0; n < d; ++n) vt[(size_t)n * prp + j] = o.v[(size_t)j * d + n];
       b.tc(&p.uo_t, &p.uo_t_lo, ut);
       b.tc(&p.vo_t, &p.vo_t_lo, vt);
-      if (q.dense || (q.attn && (p.attn_tc || p.x3))) {
+      if (q.attn && (p.attn_tc || p.x3)) {
         // W_o = U_o V_o; stored transposed: wo_t[n][m] = W_o[m][n]
         std::vector<float> wo_t = reconstruct_t(o.u, o.v, d, pr, d, d, 0);
-        if (q.dense && bf) b.store(&p.do_t, wo_t);
         if (q.attn && (p.attn_tc || p.x3)) {
           // folded rank-space out-projection: W_ov[(h, j)][n] = sum_c V_v,h[j, c] W_o[h dh + c][n]
           const fsvd_attn_desc& a = *q.attn;
@@ -319,10 +404,6 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
       b.tc(&p.vup_t, &p.vup_t_lo, vu);
       b.tc(&p.udn_t, &p.udn_t_lo, ud);
       b.tc(&p.vdn_t, &p.vdn_t_lo, vd);
-      if (q.dense && bf) {
-        b.store(&p.din_t, reconstruct_t(f.up.u, f.up.v, d, fr, df, df, 0));
-        b.store(&p.dout_t, reconstruct_t(f.down.u, f.down.v, df, fr, d, d, 0));
-      }
     } else {
       b.store(&p.uup, std::vector<float>(f.up.u, f.up.u + (size_t)d * fr));
       b.store(&p.vup, std::vector<float>(f.up.v, f.up.v + (size_t)fr * df));
@@ -332,6 +413,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
     b.store_f32(&p.bup, f.up.bias, df);
     b.store_f32(&p.bdn, f.down.bias, d);
   }
+  if (q.dense && dense_ok && (bf || p.x3)) build_dense(q, p, b);
   if (q.ln1g) {
     p.has_ln = true;
     b.store_f32(&p.ln1g, q.ln1g, d);
@@ -341,7 +423,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
     p.eps1 = q.eps1;
     p.eps2 = q.eps2;
   }
-  p.dense = q.dense && p.attn_tc && p.out_tc && p.ffn_tc;
+  p.dense = q.dense && dense_ok && (bf || p.x3);
   p.bytes = align256(b.buf.size());
   if (p.bytes) {
     FSVD_CUDA_CHECK(cudaMalloc(&p.mem, p.bytes));
@@ -354,39 +436,83 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
 }
 
 // ---------------------------------------------------------------- validation
+// EncoderLayer::validate (encoder.cpp:156-221) on the flat descriptor: the
+// factorized attention (attn.u set, with out_proj), the factorized FFN
+// (ffn.up.u set) and the dense weights (L.dense) are each optional, but each
+// sublayer needs one representation.
 void validate_layer(const fsvd_layer_desc& L) {
   const size_t d = L.attn.d_model;
   if (d == 0) fail(Kind::Shape, "layer norm parameters are empty");
   if (!L.ln1_gamma || !L.ln1_beta || !L.ln2_gamma || !L.ln2_beta)
     fail(Kind::Shape, "layer norm parameters are missing");
   if (L.heads == 0 || d % L.heads != 0) fail(Kind::Config, "heads must divide d_model");
-  const fsvd_attn_desc& s = L.attn;
-  if (s.groups == 0 || d % s.groups != 0) fail(Kind::Config, "groups must divide d_model");
-  if (L.heads % s.groups != 0) fail(Kind::Config, "groups must divide heads");
-  if (s.rank == 0 || !s.u || !s.v || !s.bias) fail(Kind::Shape, "attention factor U: missing");
-  const fsvd_linear_desc& o = L.out_proj;
-  if (o.in_dim != d || !o.u) fail(Kind::Shape, "out_proj U: expected shape (d, r)");
-  if (o.out_dim != d || !o.v) fail(Kind::Shape, "out_proj V: expected shape (r, d)");
-  if (!o.bias) fail(Kind::Shape, "out_proj bias: expected a length-d vector");
-  const fsvd_ffn_desc& f = L.ffn;
-  if (f.up.rank != f.down.rank) fail(Kind::Config, "FFN up/down factor ranks differ");
-  if (f.up.in_dim != d || !f.up.u) fail(Kind::Shape, "ffn up U: expected shape (d, r)");
-  if (f.down.out_dim != d || !f.down.v) fail(Kind::Shape, "ffn down V: expected shape (r, d)");
-  if (f.up.out_dim != f.down.in_dim || f.up.out_dim == 0)
-    fail(Kind::Shape, "ffn up V / down U: d_ff mismatch");
-  if (!f.up.v || !f.up.bias || !f.down.u || !f.down.bias)
-    fail(Kind::Shape, "ffn factor arrays are missing");
-  if (f.up.rank == 0 || o.rank == 0) fail(Kind::Shape, "factor rank must be positive");
-  if (static_cast<int>(f.activation) < 0 || static_cast<int>(f.activation) > 3)
+  const bool af = L.attn.u != nullptr, ff = L.ffn.up.u != nullptr, dn = L.dense != nullptr;
+  if (!dn && !af) fail(Kind::Config, "layer has no attention weights");
+  if (!dn && !ff) fail(Kind::Config, "layer has no FFN weights");
+  if (L.out_proj.u && !af) fail(Kind::Config, "output projection factors without attention factors");
+  if (af) {
+    const fsvd_attn_desc& s = L.attn;
+    if (s.groups == 0 || d % s.groups != 0) fail(Kind::Config, "groups must divide d_model");
+    if (L.heads % s.groups != 0) fail(Kind::Config, "groups must divide heads");
+    if (s.rank == 0 || !s.v || !s.bias) fail(Kind::Shape, "attention factor U: missing");
+    const fsvd_linear_desc& o = L.out_proj;
+    if (!o.u) fail(Kind::Config, "factorized attention needs an output projection");
+    if (o.in_dim != d) fail(Kind::Shape, "out_proj U: expected shape (d, r)");
+    if (o.out_dim != d || !o.v) fail(Kind::Shape, "out_proj V: expected shape (r, d)");
+    if (!o.bias) fail(Kind::Shape, "out_proj bias: expected a length-d vector");
+    if (o.rank == 0) fail(Kind::Shape, "factor rank must be positive");
+  }
+  if (dn) {
+    const fsvd_dense_layer& w = *L.dense;
+    if (w.d_model != d) fail(Kind::Shape, "attention weight: expected shape (d, d)");
+    for (const float* m : {w.wq, w.wk, w.wv, w.wo})
+      if (!m) fail(Kind::Shape, "attention weight: expected shape (d, d)");
+    for (const float* b : {w.bq, w.bk, w.bv, w.bo})
+      if (!b) fail(Kind::Shape, "attention bias: expected a length-d vector");
+  }
+  const size_t df = ff ? L.ffn.up.out_dim : (dn ? L.dense->d_ff : 0);
+  if (ff) {
+    const fsvd_ffn_desc& f = L.ffn;
+    if (f.up.rank != f.down.rank) fail(Kind::Config, "FFN up/down factor ranks differ");
+    if (f.up.in_dim != d) fail(Kind::Shape, "ffn up U: expected shape (d, r)");
+    if (f.down.out_dim != d || !f.down.v) fail(Kind::Shape, "ffn down V: expected shape (r, d)");
+    if (f.up.out_dim != f.down.in_dim || f.up.out_dim == 0)
+      fail(Kind::Shape, "ffn up V / down U: d_ff mismatch");
+    if (!f.up.v || !f.up.bias || !f.down.u || !f.down.bias)
+      fail(Kind::Shape, "ffn factor arrays are missing");
+    if (f.up.rank == 0) fail(Kind::Shape, "factor rank must be positive");
+  }
+  if (dn) {
+    const fsvd_dense_layer& w = *L.dense;
+    if (w.d_ff != df || df == 0 || !w.w_in) fail(Kind::Shape, "ffn input weight: expected shape (d, d_ff)");
+    if (!w.b_in) fail(Kind::Shape, "ffn input bias: expected a length-d_ff vector");
+    if (!w.w_out) fail(Kind::Shape, "ffn output weight: expected shape (d_ff, d)");
+    if (!w.b_out) fail(Kind::Shape, "ffn output bias: expected a length-d vector");
+  }
+  if (static_cast<int>(L.ffn.activation) < 0 || static_cast<int>(L.ffn.activation) > 3)
     fail(Kind::Config, "unknown activation");
+}
+
+// encoder.cpp:27-35 (check_mode_weights)
+void check_mode_weights(const fsvd_layer_desc& L, int mode, bool dense_twin_ok) {
+  const bool factors = L.attn.u && L.out_proj.u && L.ffn.up.u;
+  if (mode == FSVD_MODE_DENSE) {
+    if (!L.dense && !(dense_twin_ok && factors))
+      fail(Kind::Config, "dense mode needs dense weights on both sublayers");
+  } else if (!factors) {
+    static const char* names[4] = {"dense", "naive_lowrank", "flash_v1", "flash_v2"};
+    fail(Kind::Config, std::string(names[mode & 3]) + " mode needs factorized weights on both sublayers");
+  }
 }
 
 // ---------------------------------------------------------------- planner
 size_t op_transient_elems(const Pack& p, int op, int mode) {
   const size_t d = p.d;
-  if (op == 0) {  // standalone attention (ctx in head width)
-    if (mode == FSVD_MODE_DENSE) return 3 * d;
-    if (mode == FSVD_MODE_NAIVE_LOWRANK) return 3 * (size_t)p.G * p.rp + 3 * d;
+  if (op == 0 || (op == 3 && (mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK))) {
+    // materializing baselines: Q|K|V [3 H dhp] (+ naive P [3 G rp]) + context [H dhp]
+    const size_t hp = (size_t)p.H * p.dhp;
+    if (mode == FSVD_MODE_DENSE) return 4 * hp;
+    if (mode == FSVD_MODE_NAIVE_LOWRANK) return 3 * (size_t)p.G * p.rp + 4 * hp;
     return (p.attn_tc || p.x3) ? (size_t)p.qkv_cols + (size_t)p.H * p.rp
                                : 3 * (size_t)p.G * p.r;
   }
@@ -401,7 +527,7 @@ size_t op_transient_elems(const Pack& p, int op, int mode) {
   }
   const size_t fr = (p.ffn_tc || p.x3) ? p.frp : p.fr;
   switch (mode) {
-    case FSVD_MODE_DENSE: return p.df;
+    case FSVD_MODE_DENSE: return p.ddf;
     case FSVD_MODE_NAIVE_LOWRANK: return 2 * fr + p.df;
     case FSVD_MODE_FLASH_V1: return 2 * fr;
     default: return (p.ffn_wide || p.x3) ? 2 * fr : 0;  // wide ranks / planes: V2 runs the V1 chain
@@ -600,21 +726,62 @@ void x3_attention_rank(const Pack& p, size_t B, size_t M, const void* x, bf16* o
 
 // Materializing baselines: dense Q|K|V [T, 3d] (dense twin or rebuilt from
 // the factors) then the same attention kernel with r = head_dim.
-void tc_attention_dense(const Pack& p, int mode, size_t B, size_t M, const void* x, void* ctx,
-                        void* trans, cudaStream_t s) {
+// C[M,N] = A[M,K] W^T (+ bias) (act) in the pack's storage: bf16, or split
+// planes (plane stride = rows x leading dimension) on the fp32 policy.
+void mm(const Pack& p, const void* A, int64_t lda, const void* W, const void* W_lo, int64_t ldw,
+        void* Cm, int64_t ldc, int M, int N, int K, const float* bias, int act, cudaStream_t s) {
+  if (p.x3)
+    gemm_x3(pl(A, (size_t)M * lda), lda, wpl(W, W_lo), ldw, plo(Cm, (size_t)M * ldc), ldc, M, N,
+            K, bias, act, s);
+  else
+    gemm_bf16(as<bf16>(A), lda, as<bf16>(W), ldw, as<bf16>(Cm), ldc, M, N, K, bias, act, s);
+}
+
+// Materializing baselines: Dense (encoder.cpp:99-105: dense_attention on the
+// layer's dense weights) and NaiveLowRank (attention.cpp:271-292: Q|K|V
+// rebuilt from the factors) -- dense Q|K|V [T, 3*H*dhp] at the start of
+// `trans`, then the attention kernel with r = head width (dhp, zero-padded).
+// Returns the context [T, H*dhp] (head width when dhp == dh), placed in
+// `trans` after Q|K|V (and the naive P).
+bf16* tc_attention_dense(const Pack& p, int mode, size_t B, size_t M, const void* x, void* trans,
+                         cudaStream_t s) {
   if (!p.dense) fail(Kind::Config, "dense / naive_lowrank modes need a pack built with dense=1 "
-                                   "on the bf16 tensor-core path");
-  const int T = static_cast<int>(B * M), d = p.d, d3 = 3 * p.d;
+                                   "(head width <= 64, d_model and d_ff multiples of 8)");
+  if (mode == FSVD_MODE_NAIVE_LOWRANK && !p.wpn_t)
+    fail(Kind::Config, "naive_lowrank mode on the tensor cores needs a head width of 16, 32 or 64");
+  const int T = static_cast<int>(B * M), d = p.d, hp = p.H * p.dhp, n3 = 3 * hp;
+  const size_t ew = p.x3 ? 2 : 1;  // bf16 elements per stored value
   bf16* qkv = as<bf16>(trans);
+  bf16* o = qkv + ew * (size_t)T * n3;
   if (mode == FSVD_MODE_DENSE) {
-    gemm_bf16(as<bf16>(x), d, as<bf16>(p.dqkv_t), d, qkv, d3, T, d3, d, p.dqkv_b, ACT_NONE, s);
+    mm(p, x, d, p.dqkv_t, p.dqkv_lo, d, qkv, n3, T, n3, d, p.dqkv_b, ACT_NONE, s);
   } else {
     const int n = 3 * p.G * p.rp;
-    bf16* P = qkv + (size_t)T * d3;
-    gemm_bf16(as<bf16>(x), d, as<bf16>(p.wpn_t), d, P, n, T, n, d, nullptr, ACT_NONE, s);
-    gemm_bf16(P, n, as<bf16>(p.dvbd_t), n, qkv, d3, T, d3, n, p.dqkv_b, ACT_NONE, s);
+    bf16* P = o;
+    o = P + ew * (size_t)T * n;
+    mm(p, x, d, p.wpn_t, p.wpn_lo, d, P, n, T, n, d, nullptr, ACT_NONE, s);
+    mm(p, P, n, p.dvbd_t, p.dvbd_lo, n, qkv, n3, T, n3, n, p.nqkv_b, ACT_NONE, s);
   }
-  tc_attention(B, M, qkv, d3, 0, d, 2 * d, p.H, p.H, 64, ctx, d, s);
+  AttnTcArgs a;
+  a.qkv = qkv;
+  a.ldq = n3;
+  a.qkv_cols = n3;
+  a.q_off = 0;
+  a.k_off = hp;
+  a.v_off = 2 * hp;
+  a.batch = static_cast<int>(B);
+  a.seq = static_cast<int>(M);
+  a.heads = p.H;
+  a.groups = p.H;
+  a.rank_pad = p.dhp;
+  a.out = o;
+  a.ldo = hp;
+  if (p.x3) {
+    a.qkv_lo = qkv + (size_t)T * n3;
+    a.out_lo = o + (size_t)T * hp;
+  }
+  attn_rankspace_bf16(a, s);
+  return o;
 }
 
 }  // namespace
@@ -622,10 +789,8 @@ void tc_attention_dense(const Pack& p, int mode, size_t B, size_t M, const void*
 void attention_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* ctx,
                    void* trans, cudaStream_t s) {
   const int T = static_cast<int>(B * M);
-  if (mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK) {
-    tc_attention_dense(p, mode, B, M, x, ctx, trans, s);
-    return;
-  }
+  if (mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK)
+    fail(Kind::Config, "the materializing attention baselines run inside a layer (run_layer)");
   if (p.attn_tc) {
     // rank-space output after the projection buffer, then back to head width
     const int hr = p.H * p.rp;
@@ -648,10 +813,8 @@ void attention_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, v
 void outproj_fwd(const Pack& p, int mode, size_t B, size_t M, const void* ctx, void* out,
                  void* trans, cudaStream_t s) {
   const int T = static_cast<int>(B * M), d = p.d;
-  if (mode == FSVD_MODE_DENSE) {
-    gemm_bf16(as<bf16>(ctx), d, as<bf16>(p.do_t), d, as<bf16>(out), d, T, d, d, p.bo, ACT_NONE, s);
-    return;
-  }
+  if (mode == FSVD_MODE_DENSE)
+    fail(Kind::Config, "the dense output projection runs inside a layer (run_layer)");
   if (p.out_tc) {
     bf16* P = as<bf16>(trans);
     gemm_bf16(as<bf16>(ctx), d, as<bf16>(p.uo_t), d, P, p.prp, T, p.prp, d, nullptr, ACT_NONE, s);
@@ -682,6 +845,16 @@ void outproj_fwd(const Pack& p, int mode, size_t B, size_t M, const void* ctx, v
 void attention_block(const Pack& p, int mode, size_t B, size_t M, const void* x, void* scratch,
                      void* branch, void* trans, cudaStream_t s, const AttnMode& am = AttnMode{}) {
   const bool flash = mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2;
+  if (!flash) {
+    const int T = static_cast<int>(B * M);
+    bf16* o = tc_attention_dense(p, mode, B, M, x, trans, s);
+    if (mode == FSVD_MODE_DENSE)  // dense_output_projection on the layer's W_o, b_o
+      mm(p, o, p.H * p.dhp, p.do_t, p.do_lo, p.H * p.dhp, branch, p.d, T, p.d, p.H * p.dhp, p.dbo,
+         ACT_NONE, s);
+    else  // naive_projection (encoder.cpp:65-80): (ctx U_o) V_o + b_o
+      outproj_fwd(p, FSVD_MODE_FLASH_V1, B, M, o, branch, trans, s);
+    return;
+  }
   if (flash && p.x3) {  // split planes: O after the projection planes in `trans`
     const int T = static_cast<int>(B * M), hr = p.H * p.rp;
     bf16* o = as<bf16>(trans) + 2 * (size_t)T * p.qkv_cols;
@@ -746,19 +919,22 @@ void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* o
   const int T = static_cast<int>(B * M), d = p.d, df = p.df;
   if (mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK) {
     if (!p.dense) fail(Kind::Config, "dense / naive_lowrank modes need a pack built with dense=1");
-    if (mode == FSVD_MODE_DENSE) {
+    const size_t ew = p.x3 ? 2 : 1;
+    if (mode == FSVD_MODE_DENSE) {  // ffn_dense (ffn.cpp:187-218) on the layer's dense weights
+      const int ddf = p.ddf;
       bf16* hid = as<bf16>(trans);
-      gemm_bf16(as<bf16>(x), d, as<bf16>(p.din_t), d, hid, df, T, df, d, p.bup, p.act, s);
-      gemm_bf16(hid, df, as<bf16>(p.dout_t), df, as<bf16>(out), d, T, d, df, p.bdn, ACT_NONE, s);
-    } else {
+      mm(p, x, d, p.din_t, p.din_lo, d, hid, ddf, T, ddf, d, p.dbin, p.dact, s);
+      mm(p, hid, ddf, p.dout_t, p.dout_lo, ddf, out, d, T, d, ddf, p.dbout, ACT_NONE, s);
+    } else {  // ffn_naive_lowrank (ffn.cpp:220-255): the hidden materialised
+      if (!p.has_ffn) fail(Kind::Config, "naive_lowrank mode needs factorized FFN weights");
       const int frp = p.frp;
       bf16* P = as<bf16>(trans);
-      bf16* hid = P + (size_t)T * frp;
-      bf16* Z = hid + (size_t)T * df;
-      gemm_bf16(as<bf16>(x), d, as<bf16>(p.uup_t), d, P, frp, T, frp, d, nullptr, ACT_NONE, s);
-      gemm_bf16(P, frp, as<bf16>(p.vup_t), frp, hid, df, T, df, frp, p.bup, p.act, s);
-      gemm_bf16(hid, df, as<bf16>(p.udn_t), df, Z, frp, T, frp, df, nullptr, ACT_NONE, s);
-      gemm_bf16(Z, frp, as<bf16>(p.vdn_t), frp, as<bf16>(out), d, T, d, frp, p.bdn, ACT_NONE, s);
+      bf16* hid = P + ew * (size_t)T * frp;
+      bf16* Z = hid + ew * (size_t)T * df;
+      mm(p, x, d, p.uup_t, p.uup_t_lo, d, P, frp, T, frp, d, nullptr, ACT_NONE, s);
+      mm(p, P, frp, p.vup_t, p.vup_t_lo, frp, hid, df, T, df, frp, p.bup, p.act, s);
+      mm(p, hid, df, p.udn_t, p.udn_t_lo, df, Z, frp, T, frp, df, nullptr, ACT_NONE, s);
+      mm(p, Z, frp, p.vdn_t, p.vdn_t_lo, frp, out, d, T, d, frp, p.bdn, ACT_NONE, s);
     }
     return;
   }
@@ -1036,6 +1212,9 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
     return;
   }
   const size_t T = B * M;
+  if ((mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2 ||
+       mode == FSVD_MODE_NAIVE_LOWRANK) && !(p.has_attn && p.has_out && p.has_ffn))
+    fail(Kind::Config, "this mode needs factorized weights on both sublayers");
   const WsLayout lay = ws_layout(p, T, mode, pre_ln);
   if (ws_bytes < lay.total())
     fail(Kind::Config, "workspace too small: need " + std::to_string(lay.total()) + " bytes, got " +

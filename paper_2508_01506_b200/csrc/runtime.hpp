@@ -69,10 +69,20 @@ struct Pack {
   // dense twin / materializing baselines (tensor-core path only); the Q rows
   // carry the softmax scale s = log2(e)/sqrt(dh)
   const void *dqkv_t = nullptr;   // [3d][d]   dense W_q|W_k|W_v transposed
-  const float* dqkv_b = nullptr;  // [3d]
+  const float* dqkv_b = nullptr;  // [3*H*dhp] (Dense mode, padded head layout)
+  const float* nqkv_b = nullptr;  // [3d] q|k|v biases of the naive low-rank rebuild
   const void *wpn_t = nullptr;    // [3*G*rp][d] U_q|U_k|U_v transposed (naive low-rank)
   const void *dvbd_t = nullptr;   // [3d][3*G*rp] block-diagonal V (naive low-rank)
-  const void *do_t = nullptr, *din_t = nullptr, *dout_t = nullptr;  // [d][d] [df][d] [d][df]
+  // Dense mode (encoder.cpp:99-105, 136-139) from the layer's dense weights,
+  // else the dense twin of its factors: head width padded to dhp in
+  // {16, 32, 64} so K2 runs it as a rank-space kernel with r = dhp:
+  //   dqkv_t [3*H*dhp][d] (Q rows scaled by s, zero pad rows), dqkv_b,
+  //   do_t [d][H*dhp] = W_o^T (zero pad columns), din_t [df][d], dout_t [d][df]
+  int dhp = 0, ddf = 0, dact = 0;
+  const void *do_t = nullptr, *din_t = nullptr, *dout_t = nullptr;
+  const float *dbo = nullptr, *dbin = nullptr, *dbout = nullptr;
+  const void *dqkv_lo = nullptr, *do_lo = nullptr, *din_lo = nullptr, *dout_lo = nullptr,
+             *wpn_lo = nullptr, *dvbd_lo = nullptr;
 
   ~Pack();
 };
@@ -85,13 +95,18 @@ struct PackRequest {
   const float *ln1g = nullptr, *ln1b = nullptr, *ln2g = nullptr, *ln2b = nullptr;
   float eps1 = 1e-5f, eps2 = 1e-5f;
   size_t d_model = 0;
-  bool dense = false;
+  bool dense = false;  // also build the Dense-mode weights (and the naive low-rank ones)
+  const fsvd_dense_layer* dense_w = nullptr;  // the layer's own dense weights, if any
+  int dense_act = 0;  // the dense FFN's activation when the layer has no FFN factors
 };
 
 Pack* build_pack(const PackRequest& req, fsvd_dtype dtype);
 
 // encoder.cpp:156-222 for the flat descriptor (throws Error).
 void validate_layer(const fsvd_layer_desc& L);
+// encoder.cpp:27-35 for a run mode; dense_twin_ok lets a factor-only layer
+// run Dense mode as its dense twin (the C-ABI's documented extension).
+void check_mode_weights(const fsvd_layer_desc& L, int mode, bool dense_twin_ok);
 
 // Activation buffer planner: bytes of device workspace one layer needs for
 // T = batch*seq tokens in the given mode (two [T, d] scratch buffers + the

@@ -7,6 +7,7 @@ include/fsvd_b200.h.  No arithmetic happens here.
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -79,6 +80,52 @@ class FfnFactors:
 
 
 @dataclass
+class DenseWeights:
+    """DenseAttentionWeights + DenseFfnWeights (encoder.hpp:32-47): weights in
+    (in x out) orientation, y = x W + b."""
+    wq: np.ndarray
+    bq: np.ndarray
+    wk: np.ndarray
+    bk: np.ndarray
+    wv: np.ndarray
+    bv: np.ndarray
+    wo: np.ndarray
+    bo: np.ndarray
+    w_in: np.ndarray
+    b_in: np.ndarray
+    w_out: np.ndarray
+    b_out: np.ndarray
+
+    NAMES = ("wq", "bq", "wk", "bk", "wv", "bv", "wo", "bo", "w_in", "b_in", "w_out", "b_out")
+
+    def __post_init__(self):
+        for n in self.NAMES:
+            setattr(self, n, _c(getattr(self, n)))
+        self._desc = None
+
+    def desc(self) -> abi.DenseLayer:
+        if self._desc is None:  # kept alive with the arrays
+            self._desc = abi.DenseLayer(self.wq.shape[0], self.w_in.shape[1],
+                                        *[abi.fptr(getattr(self, n)) for n in self.NAMES])
+        return self._desc
+
+    def arrays(self):
+        return [getattr(self, n) for n in self.NAMES]
+
+    @staticmethod
+    def of(layer: "LayerFactors") -> "DenseWeights":
+        """dense_equivalent (encoder.cpp:295-331): W = U V in fp64, rounded to fp32."""
+        a = layer.attn
+        G, d, gd = a.groups, a.d_model, a.d_model // a.groups
+        w = [np.concatenate([a.u[m, g].astype(np.float64) @ a.v[m, g] for g in range(G)], axis=1)
+             for m in range(3)]
+        return DenseWeights(w[0], a.bias[0], w[1], a.bias[1], w[2], a.bias[2],
+                            layer.out_proj.dense(), layer.out_proj.bias,
+                            layer.ffn.up.dense(), layer.ffn.up.bias,
+                            layer.ffn.down.dense(), layer.ffn.down.bias)
+
+
+@dataclass
 class LayerFactors:
     heads: int
     attn: AttnFactors
@@ -90,6 +137,7 @@ class LayerFactors:
     ln2_beta: np.ndarray
     ln1_eps: float = 1e-5
     ln2_eps: float = 1e-5
+    dense: DenseWeights | None = None  # optional dense weights (RunMode::Dense)
     _keep: list = field(default_factory=list, repr=False)
 
     def __post_init__(self):
@@ -105,16 +153,53 @@ class LayerFactors:
         return self.ffn.up.v.shape[1]
 
     def desc(self) -> abi.LayerDesc:
+        dn = C.pointer(self.dense.desc()) if self.dense is not None else None
         return abi.LayerDesc(self.heads, self.attn.desc(), self.out_proj.desc(), self.ffn.desc(),
                              abi.fptr(self.ln1_gamma), abi.fptr(self.ln1_beta), self.ln1_eps,
-                             abi.fptr(self.ln2_gamma), abi.fptr(self.ln2_beta), self.ln2_eps)
+                             abi.fptr(self.ln2_gamma), abi.fptr(self.ln2_beta), self.ln2_eps, dn)
 
     def arrays(self):
         """Every parameter array, for bulk transforms (e.g. bf16 rounding)."""
         return [self.attn.u, self.attn.v, self.attn.bias, self.out_proj.u, self.out_proj.v,
                 self.out_proj.bias, self.ffn.up.u, self.ffn.up.v, self.ffn.up.bias,
                 self.ffn.down.u, self.ffn.down.v, self.ffn.down.bias, self.ln1_gamma,
-                self.ln1_beta, self.ln2_gamma, self.ln2_beta]
+                self.ln1_beta, self.ln2_gamma, self.ln2_beta] + (
+                    self.dense.arrays() if self.dense is not None else [])
+
+
+@dataclass
+class DenseLayer:
+    """An EncoderLayer carrying only dense weights (encoder.hpp:49-67 with
+    attn_factors / out_proj / ffn_factors empty): runs in RunMode::Dense."""
+    heads: int
+    dense: DenseWeights
+    ln1_gamma: np.ndarray
+    ln1_beta: np.ndarray
+    ln2_gamma: np.ndarray
+    ln2_beta: np.ndarray
+    activation: int = abi.ACT_GELU_ERF
+    ln1_eps: float = 1e-5
+    ln2_eps: float = 1e-5
+
+    def __post_init__(self):
+        for n in ("ln1_gamma", "ln1_beta", "ln2_gamma", "ln2_beta"):
+            setattr(self, n, _c(getattr(self, n)))
+
+    @property
+    def d_model(self):
+        return self.dense.wq.shape[0]
+
+    def desc(self) -> abi.LayerDesc:
+        d = self.d_model
+        empty = abi.LinearDesc(0, 0, 0, None, None, None)
+        return abi.LayerDesc(self.heads, abi.AttnDesc(d, 0, 0, None, None, None), empty,
+                             abi.FfnDesc(empty, empty, self.activation),
+                             abi.fptr(self.ln1_gamma), abi.fptr(self.ln1_beta), self.ln1_eps,
+                             abi.fptr(self.ln2_gamma), abi.fptr(self.ln2_beta), self.ln2_eps,
+                             C.pointer(self.dense.desc()))
+
+    def arrays(self):
+        return self.dense.arrays() + [self.ln1_gamma, self.ln1_beta, self.ln2_gamma, self.ln2_beta]
 
 
 def layer_descs(layers):
