@@ -228,6 +228,12 @@ size_t fsvd_layer_pack_device_bytes(const fsvd_layer_pack* p);
 /* 1 if this pack runs the tcgen05 tensor-core kernels, 0 if the SIMT
  * kernels (fp32 policy or shapes outside the tensor-core tiling). */
 int fsvd_layer_pack_uses_tensor_cores(const fsvd_layer_pack* p);
+/* Row pitch (elements) of this pack's device activations: d_model rounded up
+ * to 64 when the layer runs on the tensor cores (the padding columns are
+ * zero and stay zero), d_model otherwise.  Device-API buffers ([T, pitch])
+ * use it; the host API pads and unpads itself.  fp32 packs on the tensor
+ * cores store activations as split bf16 planes (hi [T, pitch], then lo). */
+size_t fsvd_layer_pack_row_pitch(const fsvd_layer_pack* p);
 
 /* Pack cache of the host drop-ins (fsvd_flash_svd_attention ...
  * fsvd_run_model): their device packs are kept per (device, dtype, content

@@ -137,6 +137,7 @@ def _declare(lib):
         "fsvd_layer_pack_destroy": (None, [vp]),
         "fsvd_layer_pack_device_bytes": (_sz, [vp]),
         "fsvd_layer_pack_uses_tensor_cores": (C.c_int, [vp]),
+        "fsvd_layer_pack_row_pitch": (_sz, [vp]),
         "fsvd_pack_cache_stats": (st, [P(_sz), P(_sz), P(C.c_uint64), P(C.c_uint64)]),
         "fsvd_pack_cache_clear": (st, []),
         "fsvd_workspace_bytes": (st, [P(vp), _sz, _sz, _sz, C.c_int, P(_sz)]),

@@ -155,17 +155,6 @@ size_t expected(int id, const fsvd_geometry& g) {
 // Device copies of a host fp32 activation in the pack dtype, plus the
 // workspace.  The buffers are cached per (host thread, device) and only grow,
 // so a repeated synchronous call does no cudaMalloc / cudaFree.
-struct DevMem {
-  void* p = nullptr;
-  explicit DevMem(size_t bytes) {
-    if (bytes) FSVD_CUDA_CHECK(cudaMalloc(&p, bytes));
-  }
-  ~DevMem() {
-    if (p) cudaFree(p);
-  }
-  DevMem(const DevMem&) = delete;
-  DevMem& operator=(const DevMem&) = delete;
-};
 
 struct ScratchSet {
   void* p[2] = {nullptr, nullptr};  // 0: arena (in / out / workspace), 1: fp32 staging
@@ -203,53 +192,40 @@ void* scratch(int slot, size_t bytes) {
   return ss->p[slot];
 }
 
-// F32 packs on the tensor cores hold device activations as split planes
-// (planes.cu): hi plane at dev, lo plane right after it.
-void upload(const float* host, size_t n, fsvd_dtype dt, void* dev, cudaStream_t s,
-            bool planes = false) {
-  if (planes) {
-    float* tmp = static_cast<float*>(scratch(1, n * 4));
-    FSVD_CUDA_CHECK(cudaMemcpyAsync(tmp, host, n * 4, cudaMemcpyHostToDevice, s));
-    split_planes(tmp, static_cast<bf16*>(dev), static_cast<bf16*>(dev) + n, n, s);
-  } else if (dt == FSVD_BF16) {
-    float* tmp = static_cast<float*>(scratch(1, n * 4));
-    FSVD_CUDA_CHECK(cudaMemcpyAsync(tmp, host, n * 4, cudaMemcpyHostToDevice, s));
-    convert_f32<bf16>(tmp, static_cast<bf16*>(dev), n, s);
-  } else {
-    FSVD_CUDA_CHECK(cudaMemcpyAsync(dev, host, n * 4, cudaMemcpyHostToDevice, s));
-  }
+// Host fp32 [rows, d] <-> device activations [rows, pack.d] in the pack's
+// storage form: bf16, fp32 (CUDA-core fp32 packs) or split planes (fp32 on the
+// tensor cores); the tensor-core layouts pad d up to pack.d with zero columns.
+int storage_form(const Pack& p) { return p.x3 ? 2 : (p.dtype == FSVD_BF16 ? 0 : 1); }
+
+void upload(const float* host, size_t rows, const Pack& p, void* dev, cudaStream_t s) {
+  const size_t n = rows * p.dr;
+  float* tmp = static_cast<float*>(scratch(1, n * 4));
+  FSVD_CUDA_CHECK(cudaMemcpyAsync(tmp, host, n * 4, cudaMemcpyHostToDevice, s));
+  rows_to_device(tmp, static_cast<int>(rows), p.dr, p.d, storage_form(p), dev, s);
 }
-void download(const void* dev, size_t n, fsvd_dtype dt, float* host, cudaStream_t s,
-              bool planes = false) {
-  if (planes) {
-    float* tmp = static_cast<float*>(scratch(1, n * 4));
-    merge_planes(static_cast<const bf16*>(dev), static_cast<const bf16*>(dev) + n, tmp, n, s);
-    FSVD_CUDA_CHECK(cudaMemcpyAsync(host, tmp, n * 4, cudaMemcpyDeviceToHost, s));
-  } else if (dt == FSVD_BF16) {
-    float* tmp = static_cast<float*>(scratch(1, n * 4));
-    to_f32<bf16>(static_cast<const bf16*>(dev), tmp, n, s);
-    FSVD_CUDA_CHECK(cudaMemcpyAsync(host, tmp, n * 4, cudaMemcpyDeviceToHost, s));
-  } else {
-    FSVD_CUDA_CHECK(cudaMemcpyAsync(host, dev, n * 4, cudaMemcpyDeviceToHost, s));
-  }
+void download(const void* dev, size_t rows, const Pack& p, float* host, cudaStream_t s) {
+  const size_t n = rows * p.dr;
+  float* tmp = static_cast<float*>(scratch(1, n * 4));
+  rows_from_device(dev, static_cast<int>(rows), p.dr, p.d, storage_form(p), tmp, s);
+  FSVD_CUDA_CHECK(cudaMemcpyAsync(host, tmp, n * 4, cudaMemcpyDeviceToHost, s));
   FSVD_CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
-// Runs fn(x_dev, out_dev, trans_dev, stream) on the cached device arena and
-// reports the arena to the meter's device high-water.
+// Runs fn(x_dev, out_dev, trans_dev, stream) on the cached device arena for
+// `rows` activation rows of width pack.dr in and out, and reports the arena
+// to the meter's device high-water.
 template <typename F>
-void run_on_device(const float* x, size_t n_in, float* out, size_t n_out, fsvd_dtype dt,
-                   size_t trans_bytes, const Pack& pack, Meter* meter, F&& fn) {
+void run_on_device(const float* x, size_t rows, float* out, const Pack& pack, size_t trans_bytes,
+                   Meter* meter, F&& fn) {
   require_device();
-  const size_t es = dt == FSVD_BF16 ? 2 : 4;
-  const size_t in_b = (n_in * es + 255) & ~size_t(255), out_b = (n_out * es + 255) & ~size_t(255);
-  uint8_t* base = static_cast<uint8_t*>(scratch(0, in_b + out_b + trans_bytes + 256));
+  const size_t bytes = (rows * pack.d * pack.es + 255) & ~size_t(255);
+  uint8_t* base = static_cast<uint8_t*>(scratch(0, 2 * bytes + trans_bytes + 256));
   cudaStream_t s = nullptr;
-  upload(x, n_in, dt, base, s, pack.x3);
-  fn(base, base + in_b, base + in_b + out_b, s);
+  upload(x, rows, pack, base, s);
+  fn(base, base + bytes, base + 2 * bytes, s);
   FSVD_CUDA_CHECK(cudaGetLastError());
-  download(base + in_b, n_out, dt, out, s, pack.x3);
-  if (meter) meter->note_device(in_b + out_b + trans_bytes, pack.bytes);
+  download(base + bytes, rows, pack, out, s);
+  if (meter) meter->note_device(2 * bytes + trans_bytes, pack.bytes);
 }
 
 // ------------------------------------------------------------- pack cache
@@ -491,7 +467,7 @@ void host_attention(const float* x, size_t B, size_t M, size_t W, const fsvd_att
   require_device();
   auto pack = pack_attention(a, heads, dt);
   const size_t trans = B * M * op_transient_elems(*pack, 0, FSVD_MODE_FLASH_V1) * pack->es;
-  run_on_device(x, B * M * d, out, B * M * d, dt, trans, *pack, meter,
+  run_on_device(x, B * M, out, *pack, trans, meter,
                 [&](void* xd, void* od, void* td, cudaStream_t s) {
                   attention_fwd(*pack, FSVD_MODE_FLASH_V1, B, M, xd, od, td, s);
                 });
@@ -518,7 +494,7 @@ void host_outproj(const float* ctx, size_t B, size_t M, size_t W, const fsvd_lin
   q.d_model = d;
   std::shared_ptr<Pack> pack = cached_pack(q, dt);
   const size_t trans = B * M * op_transient_elems(*pack, 1, FSVD_MODE_FLASH_V1) * pack->es;
-  run_on_device(ctx, B * M * d, out, B * M * d, dt, trans, *pack, meter,
+  run_on_device(ctx, B * M, out, *pack, trans, meter,
                 [&](void* xd, void* od, void* td, cudaStream_t s) {
                   outproj_fwd(*pack, FSVD_MODE_FLASH_V1, B, M, xd, od, td, s);
                 });
@@ -562,7 +538,7 @@ void host_ffn(int variant, const float* x, size_t B, size_t M, size_t W, const f
   std::shared_ptr<Pack> pack = cached_pack(q, dt);
   const int mode = variant == 1 ? FSVD_MODE_FLASH_V1 : FSVD_MODE_FLASH_V2;
   const size_t trans = B * M * op_transient_elems(*pack, 2, mode) * pack->es;
-  run_on_device(x, B * M * d, out, B * M * d, dt, trans, *pack, meter,
+  run_on_device(x, B * M, out, *pack, trans, meter,
                 [&](void* xd, void* od, void* td, cudaStream_t s) {
                   ffn_fwd(*pack, mode, B, M, xd, od, td, s);
                 });
@@ -693,7 +669,10 @@ void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_lay
     if (packs.back()->x3 != packs[0]->x3)
       fail(Kind::Config, "fp32 policy: every layer must fit the tensor-core tiling, or none");
   }
-  run_on_device(x, B * M * W, out, B * M * W, dt, ws, *packs[0], nullptr,
+  for (const auto& q : packs)
+    if (q->d != packs[0]->d)
+      fail(Kind::Config, "every layer must use the same device layout (tensor-core tiling)");
+  run_on_device(x, B * M, out, *packs[0], ws, nullptr,
                 [&](void* xd, void* od, void* td, cudaStream_t s) {
                   std::vector<const Pack*> pp;
                   for (auto& p : packs) pp.push_back(p.get());
@@ -890,6 +869,9 @@ void fsvd_layer_pack_destroy(fsvd_layer_pack* p) {
   }
 }
 size_t fsvd_layer_pack_device_bytes(const fsvd_layer_pack* p) { return p ? p->p->bytes : 0; }
+size_t fsvd_layer_pack_row_pitch(const fsvd_layer_pack* p) {
+  return p ? static_cast<size_t>(p->p->d) : 0;
+}
 int fsvd_layer_pack_uses_tensor_cores(const fsvd_layer_pack* p) {
   return p && ((p->p->attn_tc && p->p->out_tc && p->p->ffn_tc) || p->p->x3) ? 1 : 0;
 }

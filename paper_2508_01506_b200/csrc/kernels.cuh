@@ -51,8 +51,15 @@ void split_planes(const float* src, bf16* hi, bf16* lo, int64_t n, cudaStream_t 
 void merge_planes(const bf16* hi, const bf16* lo, float* dst, int64_t n, cudaStream_t s);
 // y = LN(a (+ b)) * gamma + beta, rows of width d; in place allowed for d <= 2048
 void ln_planes(const Planes& a, const Planes* b, const float* gamma, const float* beta, float eps,
-               const PlanesOut& y, int rows, int d, cudaStream_t s);
+               const PlanesOut& y, int rows, int d, cudaStream_t s, int pitch = 0);
 void add_planes(const Planes& a, const Planes& b, const PlanesOut& y, int64_t n, cudaStream_t s);
+// Host fp32 rows [rows, d] (staged on the device) <-> device activations
+// [rows, pitch] in storage form 0 bf16, 1 fp32, 2 split planes; the padding
+// columns d..pitch are written as zeros.
+void rows_to_device(const float* src, int rows, int d, int pitch, int form, void* dst,
+                    cudaStream_t s);
+void rows_from_device(const void* src, int rows, int d, int pitch, int form, float* dst,
+                      cudaStream_t s);
 
 // ---- K6: y = LN(resid + bf16(A[T,K] * B[N,K]^T + bias)) * gamma + beta --------
 // One CTA per 128 complete rows; N <= 768, K <= 512, multiples of 64.
@@ -162,10 +169,12 @@ bool ffn_wide_cluster_supported(const FfnTcArgs& a);
 void ffn_wide_cluster_bf16(const FfnTcArgs& a, cudaStream_t s);
 
 // ---- K5: y = LN(a (+ b)) * gamma + beta, rows of width d ---------------------
+// pitch > d: rows are stored with pitch columns (zero-padded model dimension);
+// statistics over the first d, all pitch columns written.
 void resid_layernorm_bf16(const bf16* a, const bf16* b, const float* gamma, const float* beta,
-                          float eps, bf16* y, int rows, int d, cudaStream_t s);
+                          float eps, bf16* y, int rows, int d, cudaStream_t s, int pitch = 0);
 void resid_layernorm_f32(const float* a, const float* b, const float* gamma, const float* beta,
-                         float eps, float* y, int rows, int d, cudaStream_t s);
+                         float eps, float* y, int rows, int d, cudaStream_t s, int pitch = 0);
 void add_bf16(const bf16* a, const bf16* b, bf16* y, int64_t n, cudaStream_t s);
 void add_f32(const float* a, const float* b, float* y, int64_t n, cudaStream_t s);
 

@@ -47,26 +47,29 @@ __global__ void k_merge_planes(const bf16* __restrict__ hi, const bf16* __restri
 // y = gamma * ((a + b) - mean) / sqrt(var + eps) + beta per row, fp32, biased
 // variance; one warp per row, up to 32*VPL values in registers.  In place
 // (y == a or y == b) is allowed: a row is read completely before it is written.
+// Rows are stored with `pitch` >= d columns (zero-padded model dimension):
+// statistics over the first d, all pitch columns written (gamma = beta = 0 there).
 template <int VPL>
 __global__ void __launch_bounds__(256)
     k_ln_planes(Planes a, Planes b, const float* __restrict__ gamma,
-                const float* __restrict__ beta, float eps, PlanesOut y, int rows, int d) {
+                const float* __restrict__ beta, float eps, PlanesOut y, int rows, int d,
+                int pitch) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
-  const int64_t base = (int64_t)warp * d;
+  const int64_t base = (int64_t)warp * pitch;
   float v[VPL];
   float s = 0.0f;
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
     const int c = lane + 32 * i;
     v[i] = 0.0f;
-    if (c < d) {
+    if (c < pitch) {
       v[i] = join1(a.hi, a.lo, base + c);
       if (b.hi) v[i] += join1(b.hi, b.lo, base + c);
-      s += v[i];
+      if (c < d) s += v[i];
     }
   }
 #pragma unroll
@@ -87,20 +90,22 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
     const int c = lane + 32 * i;
-    if (c < d) split1(gamma[c] * ((v[i] - mean) * inv) + beta[c], y.hi[base + c], y.lo[base + c]);
+    if (c < pitch)
+      split1(gamma[c] * ((v[i] - mean) * inv) + beta[c], y.hi[base + c], y.lo[base + c]);
   }
 }
 
 // Rows wider than the register path: three strided sweeps.
 __global__ void __launch_bounds__(256)
     k_ln_planes_wide(Planes a, Planes b, const float* __restrict__ gamma,
-                     const float* __restrict__ beta, float eps, PlanesOut y, int rows, int d) {
+                     const float* __restrict__ beta, float eps, PlanesOut y, int rows, int d,
+                     int pitch) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
-  const int64_t base = (int64_t)warp * d;
+  const int64_t base = (int64_t)warp * pitch;
   auto val = [&](int c) {
     float t = join1(a.hi, a.lo, base + c);
     if (b.hi) t += join1(b.hi, b.lo, base + c);
@@ -118,7 +123,7 @@ __global__ void __launch_bounds__(256)
   for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
   const float inv = 1.0f / sqrtf(q / static_cast<float>(d) + eps);
   // in place is not allowed here (a later value of the row is re-read)
-  for (int c = lane; c < d; c += 32)
+  for (int c = lane; c < pitch; c += 32)
     split1(gamma[c] * ((val(c) - mean) * inv) + beta[c], y.hi[base + c], y.lo[base + c]);
 }
 
@@ -130,12 +135,60 @@ __global__ void k_add_planes(Planes a, Planes b, PlanesOut y, int64_t n) {
     split1(join1(a.hi, a.lo, i) + join1(b.hi, b.lo, i), y.hi[i], y.lo[i]);
 }
 
+// Host fp32 rows [rows, d] <-> device activations [rows, pitch] in the
+// pack's storage form (0: bf16, 1: fp32, 2: split planes), zero padding.
+__global__ void k_rows_in(const float* __restrict__ src, int rows, int d, int pitch, int form,
+                          void* __restrict__ dst) {
+  const int64_t n = (int64_t)rows * pitch;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / pitch;
+    const int c = static_cast<int>(i - r * pitch);
+    const float v = c < d ? src[r * d + c] : 0.0f;
+    if (form == 1) {
+      static_cast<float*>(dst)[i] = v;
+    } else if (form == 0) {
+      static_cast<bf16*>(dst)[i] = __float2bfloat16_rn(v);
+    } else {
+      bf16* h = static_cast<bf16*>(dst);
+      split1(v, h[i], h[n + i]);
+    }
+  }
+}
+__global__ void k_rows_out(const void* __restrict__ src, int rows, int d, int pitch, int form,
+                           float* __restrict__ dst) {
+  const int64_t n = (int64_t)rows * d, np = (int64_t)rows * pitch;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / d;
+    const int64_t j = r * pitch + (i - r * d);
+    if (form == 1) dst[i] = static_cast<const float*>(src)[j];
+    else if (form == 0) dst[i] = __bfloat162float(static_cast<const bf16*>(src)[j]);
+    else dst[i] = join1(static_cast<const bf16*>(src), static_cast<const bf16*>(src) + np, j);
+  }
+}
+
 int ew_grid(int64_t n) {
   const int64_t g = (n + 255) / 256;
   return static_cast<int>(g < 8 * 148 ? (g > 0 ? g : 1) : 8 * 148);
 }
 
 }  // namespace
+
+void rows_to_device(const float* src, int rows, int d, int pitch, int form, void* dst,
+                    cudaStream_t s) {
+  const int64_t n = (int64_t)rows * pitch;
+  if (n == 0) return;
+  k_rows_in<<<ew_grid(n), 256, 0, s>>>(src, rows, d, pitch, form, dst);
+  check_launch("k_rows_in");
+}
+void rows_from_device(const void* src, int rows, int d, int pitch, int form, float* dst,
+                      cudaStream_t s) {
+  const int64_t n = (int64_t)rows * d;
+  if (n == 0) return;
+  k_rows_out<<<ew_grid(n), 256, 0, s>>>(src, rows, d, pitch, form, dst);
+  check_launch("k_rows_out");
+}
 
 void split_planes(const float* src, bf16* hi, bf16* lo, int64_t n, cudaStream_t s) {
   if (n == 0) return;
@@ -150,19 +203,21 @@ void merge_planes(const bf16* hi, const bf16* lo, float* dst, int64_t n, cudaStr
 }
 
 void ln_planes(const Planes& a, const Planes* b, const float* gamma, const float* beta, float eps,
-               const PlanesOut& y, int rows, int d, cudaStream_t s) {
+               const PlanesOut& y, int rows, int d, cudaStream_t s, int pitch) {
   const Planes bb = b ? *b : Planes{nullptr, nullptr};
   const dim3 grid((rows + 7) / 8);
-  if (d <= 32 * 32) {
-    launch_pdl(k_ln_planes<32>, grid, dim3(256), 0, s, a, bb, gamma, beta, eps, y, rows, d);
+  if (pitch <= 0) pitch = d;
+  if (pitch <= 32 * 32) {
+    launch_pdl(k_ln_planes<32>, grid, dim3(256), 0, s, a, bb, gamma, beta, eps, y, rows, d, pitch);
     check_launch("k_ln_planes");
-  } else if (d <= 64 * 32) {
-    launch_pdl(k_ln_planes<64>, grid, dim3(256), 0, s, a, bb, gamma, beta, eps, y, rows, d);
+  } else if (pitch <= 64 * 32) {
+    launch_pdl(k_ln_planes<64>, grid, dim3(256), 0, s, a, bb, gamma, beta, eps, y, rows, d, pitch);
     check_launch("k_ln_planes");
   } else {
     if (y.hi == a.hi || (b && y.hi == b->hi))
       throw CudaError("ln_planes: rows wider than 2048 cannot run in place");
-    launch_pdl(k_ln_planes_wide, grid, dim3(256), 0, s, a, bb, gamma, beta, eps, y, rows, d);
+    launch_pdl(k_ln_planes_wide, grid, dim3(256), 0, s, a, bb, gamma, beta, eps, y, rows, d,
+               pitch);
     check_launch("k_ln_planes_wide");
   }
 }

@@ -89,6 +89,13 @@ struct Builder {
 
 int pad_to(int x, int m) { return (x + m - 1) / m * m; }
 
+// n values followed by zeros up to length m
+std::vector<float> padded(const float* v, int n, int m) {
+  std::vector<float> out(static_cast<size_t>(m), 0.0f);
+  std::copy(v, v + n, out.begin());
+  return out;
+}
+
 // W^T[n][k] = sum_j U[k][j] V[j][n] (fp32 accumulate, j ascending) for the
 // dense twin (encoder.cpp:295-331 reconstructs W = U V the same way).
 std::vector<float> reconstruct_t(const float* u, const float* v, int K, int R, int N, int ldv,
@@ -116,13 +123,15 @@ namespace {
 // exactly as dense_equivalent does (encoder.cpp:295-331: W = U V per group,
 // reconstruct_t's fp32 j-ascending sums).
 void build_dense(const PackRequest& q, Pack& p, Builder& b) {
-  const int d = p.d, H = static_cast<int>(q.heads), dh = d / H;
+  // d: the callers' model dimension; D: the padded layout (see build_pack)
+  const int d = p.dr, D = p.d, H = static_cast<int>(q.heads), dh = d / H;
   const int dhp = dh <= 16 ? 16 : dh <= 32 ? 32 : 64, hp = H * dhp;
   const double sc = 1.4426950408889634 / std::sqrt(static_cast<double>(dh));
   const fsvd_dense_layer* w = q.dense_w;
   const int df = w ? static_cast<int>(w->d_ff) : static_cast<int>(q.ffn->up.out_dim);
+  const int dfp = pad_to(df, 8);
   p.dhp = dhp;
-  p.ddf = df;
+  p.ddf = dfp;
   p.H = H;
   p.dh = dh;
   p.dact = q.ffn ? static_cast<int>(q.ffn->activation) : q.dense_act;
@@ -151,50 +160,52 @@ void build_dense(const PackRequest& q, Pack& p, Builder& b) {
     }
     std::copy(a.bias, a.bias + 3 * (size_t)d, bias.begin());
   }
-  std::vector<float> qkv((size_t)3 * hp * d, 0.0f), bq((size_t)3 * hp, 0.0f);
+  std::vector<float> qkv((size_t)3 * hp * D, 0.0f), bq((size_t)3 * hp, 0.0f);
   for (int m = 0; m < 3; ++m)
     for (int h = 0; h < H; ++h)
       for (int c = 0; c < dh; ++c) {
         const float f = m == 0 ? static_cast<float>(sc) : 1.0f;
         const size_t row = (size_t)m * hp + (size_t)h * dhp + c, src = (size_t)h * dh + c;
-        for (int k = 0; k < d; ++k) qkv[row * d + k] = wt[m][src * d + k] * f;
+        for (int k = 0; k < d; ++k) qkv[row * D + k] = wt[m][src * d + k] * f;
         bq[row] = bias[(size_t)m * d + src] * f;
       }
   b.tc(&p.dqkv_t, &p.dqkv_lo, qkv);
   b.store_f32(&p.dqkv_b, bq);
-  // output projection W_o^T with padded input columns
+  // output projection W_o^T [D][H dhp], padded rows and head columns zero
   std::vector<float> wo_t = w ? std::vector<float>((size_t)d * d)
                               : reconstruct_t(q.out_proj->u, q.out_proj->v, d,
                                               static_cast<int>(q.out_proj->rank), d, d, 0);
   if (w)
     for (int k = 0; k < d; ++k)
       for (int n = 0; n < d; ++n) wo_t[(size_t)n * d + k] = w->wo[(size_t)k * d + n];
-  std::vector<float> wop((size_t)d * hp, 0.0f);
+  std::vector<float> wop((size_t)D * hp, 0.0f);
   for (int n = 0; n < d; ++n)
     for (int h = 0; h < H; ++h)
       for (int c = 0; c < dh; ++c)
         wop[(size_t)n * hp + (size_t)h * dhp + c] = wo_t[(size_t)n * d + h * dh + c];
   b.tc(&p.do_t, &p.do_lo, wop);
-  b.store_f32(&p.dbo, w ? w->bo : q.out_proj->bias, d);
-  // FFN
-  std::vector<float> win_t, wout_t;
+  b.store_f32(&p.dbo, padded(w ? w->bo : q.out_proj->bias, d, D));
+  // FFN: W_in^T [dfp][D], W_out^T [D][dfp]
+  std::vector<float> win((size_t)dfp * D, 0.0f), wout((size_t)D * dfp, 0.0f);
   if (w) {
-    win_t.resize((size_t)df * d);
-    wout_t.resize((size_t)d * df);
     for (int k = 0; k < d; ++k)
-      for (int n = 0; n < df; ++n) win_t[(size_t)n * d + k] = w->w_in[(size_t)k * df + n];
+      for (int n = 0; n < df; ++n) win[(size_t)n * D + k] = w->w_in[(size_t)k * df + n];
     for (int k = 0; k < df; ++k)
-      for (int n = 0; n < d; ++n) wout_t[(size_t)n * df + k] = w->w_out[(size_t)k * d + n];
+      for (int n = 0; n < d; ++n) wout[(size_t)n * dfp + k] = w->w_out[(size_t)k * d + n];
   } else {
     const fsvd_ffn_desc& f = *q.ffn;
     const int fr = static_cast<int>(f.up.rank);
-    win_t = reconstruct_t(f.up.u, f.up.v, d, fr, df, df, 0);
-    wout_t = reconstruct_t(f.down.u, f.down.v, df, fr, d, d, 0);
+    const std::vector<float> a = reconstruct_t(f.up.u, f.up.v, d, fr, df, df, 0);    // [df][d]
+    const std::vector<float> c = reconstruct_t(f.down.u, f.down.v, df, fr, d, d, 0);  // [d][df]
+    for (int n = 0; n < df; ++n)
+      for (int k = 0; k < d; ++k) win[(size_t)n * D + k] = a[(size_t)n * d + k];
+    for (int n = 0; n < d; ++n)
+      for (int k = 0; k < df; ++k) wout[(size_t)n * dfp + k] = c[(size_t)n * df + k];
   }
-  b.tc(&p.din_t, &p.din_lo, win_t);
-  b.tc(&p.dout_t, &p.dout_lo, wout_t);
-  b.store_f32(&p.dbin, w ? w->b_in : q.ffn->up.bias, df);
-  b.store_f32(&p.dbout, w ? w->b_out : q.ffn->down.bias, d);
+  b.tc(&p.din_t, &p.din_lo, win);
+  b.tc(&p.dout_t, &p.dout_lo, wout);
+  b.store_f32(&p.dbin, padded(w ? w->b_in : q.ffn->up.bias, df, dfp));
+  b.store_f32(&p.dbout, padded(w ? w->b_out : q.ffn->down.bias, d, D));
 }
 }  // namespace
 
@@ -203,34 +214,43 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
   Pack& p = *P;
   p.dtype = dtype;
   p.es = dtype == FSVD_BF16 ? 2 : 4;
-  p.d = static_cast<int>(q.d_model);
   Builder b;
   b.es = p.es;
   const bool bf = dtype == FSVD_BF16;
-  const int d = p.d;
-  // tensor-core support of each component (bf16 policy: per component; fp32
-  // policy: split planes when every component present is supported)
-  bool attn_ok = true, out_ok = true, ffn_ok = true;
+  // d: the model dimension of the caller's arrays; D: the model dimension of
+  // the device layouts -- d rounded up to 64 with zero rows / columns when the
+  // whole pack runs on the tensor cores, so every shape the reference accepts
+  // fits the kernels' tiling (K3/K4 need d % 64, TMA 16-byte row pitches).
+  // LayerNorm statistics use d (runtime ln); the host API pads and unpads.
+  const int d = static_cast<int>(q.d_model);
+  bool attn_ok = true, out_ok = true, ffn_ok = true, dense_ok = true;
   if (q.attn) {
     const int r = static_cast<int>(q.attn->rank);
     const int rp = r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : 0;
-    attn_ok = rp != 0 && attn_rankspace_supported(rp) && d % 8 == 0;
+    attn_ok = rp != 0 && attn_rankspace_supported(rp);
   }
-  if (q.out_proj) out_ok = d % 8 == 0;
-  if (q.ffn) {
-    const int df = static_cast<int>(q.ffn->up.out_dim);
-    ffn_ok = d % 8 == 0 && df % 8 == 0 && ffn_tc_supported(d, df, ffn_rank_pad(static_cast<int>(q.ffn->up.rank)));
-  }
-  // Dense-mode weights: any head width <= 64 (padded), 16-byte row pitches
-  bool dense_ok = false;
-  if (q.dense && q.heads > 0 && d % q.heads == 0) {
-    const int dh = d / static_cast<int>(q.heads);
+  if (q.ffn) ffn_ok = ffn_rank_pad(static_cast<int>(q.ffn->up.rank)) <= kFfnMaxRankPad;
+  // Dense-mode weights: any head width <= 64 (padded to 16 / 32 / 64)
+  if (q.dense) {
     const int df = q.dense_w ? static_cast<int>(q.dense_w->d_ff)
                              : (q.ffn ? static_cast<int>(q.ffn->up.out_dim) : 0);
-    dense_ok = dh <= 64 && d % 8 == 0 && df % 8 == 0 && df > 0 &&
+    dense_ok = q.heads > 0 && d % q.heads == 0 && d / static_cast<int>(q.heads) <= 64 && df > 0 &&
                (q.dense_w != nullptr || (q.attn && q.out_proj && q.ffn));
   }
-  p.x3 = !bf && attn_ok && out_ok && ffn_ok && (!q.dense || dense_ok);
+  const bool all_ok = attn_ok && out_ok && ffn_ok && dense_ok;
+  const int D = all_ok ? pad_to(d, 64) : d;
+  if (!all_ok) {  // bf16 per component on the unpadded layout (CUDA cores otherwise)
+    attn_ok = attn_ok && d % 8 == 0;
+    out_ok = d % 8 == 0;
+    if (q.ffn) {
+      const int df = static_cast<int>(q.ffn->up.out_dim);
+      ffn_ok = ffn_ok && d % 8 == 0 && df % 8 == 0 &&
+               ffn_tc_supported(d, df, ffn_rank_pad(static_cast<int>(q.ffn->up.rank)));
+    }
+  }
+  p.d = D;
+  p.dr = d;
+  p.x3 = !bf && all_ok;
   b.x3 = p.x3;
 
   if (q.attn) {
@@ -250,7 +270,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
       const int rp = p.rp;
       const double sc = 1.4426950408889634 / std::sqrt(static_cast<double>(dh));
       p.qkv_cols = (H + 2 * G) * rp;
-      std::vector<float> w((size_t)p.qkv_cols * d, 0.0f), bp((size_t)p.qkv_cols, 0.0f);
+      std::vector<float> w((size_t)p.qkv_cols * D, 0.0f), bp((size_t)p.qkv_cols, 0.0f);
       std::vector<double> mh((size_t)r * r);
       for (int h = 0; h < H; ++h) {
         const int g = h / hpg, hc = (h % hpg) * dh;
@@ -264,7 +284,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
             mh[(size_t)j * r + i] = acc * sc;
           }
         for (int i = 0; i < r; ++i) {
-          float* row = &w[((size_t)h * rp + i) * d];
+          float* row = &w[((size_t)h * rp + i) * D];
           for (int k = 0; k < d; ++k) {
             double acc = 0.0;
             for (int j = 0; j < r; ++j) acc += (double)uq[(size_t)k * r + j] * mh[(size_t)j * r + i];
@@ -279,12 +299,12 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
         for (int g = 0; g < G; ++g)
           for (int j = 0; j < r; ++j)
             for (int k = 0; k < d; ++k)
-              w[((size_t)(H + (m - 1) * G + g) * rp + j) * d + k] =
+              w[((size_t)(H + (m - 1) * G + g) * rp + j) * D + k] =
                   a.u[((size_t)(m * G + g) * d + k) * r + j];
       b.tc(&p.wproj_t, &p.wproj_lo, w);
       b.store_f32(&p.bproj, bp);
       // block-diagonal V_v: ctx[:, h*dh + c] = sum_j O_h[:, j] V_v,g[j, hc + c] (+ b_v)
-      std::vector<float> vc((size_t)d * H * rp, 0.0f);
+      std::vector<float> vc((size_t)D * H * rp, 0.0f);
       for (int h = 0; h < H; ++h) {
         const int g = h / hpg, hc = (h % hpg) * dh;
         for (int c = 0; c < dh; ++c)
@@ -293,7 +313,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
                 a.v[((size_t)(2 * G + g) * r + j) * gd + hc + c];
       }
       b.tc(&p.wvc_t, &p.wvc_lo, vc);
-      b.store_f32(&p.bv, a.bias + 2 * d, d);
+      b.store_f32(&p.bv, padded(a.bias + 2 * d, d, D));
     } else {
       std::vector<float> w((size_t)d * 3 * G * r);
       for (int m = 0; m < 3; ++m)
@@ -306,7 +326,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
       b.store(&p.attn_v, std::vector<float>(a.v, a.v + (size_t)3 * G * r * gd));
     }
     b.store_f32(&p.attn_b, a.bias, 3 * (size_t)d);
-    if (q.dense && (p.attn_tc || p.x3) && (dh == 16 || dh == 32 || dh == 64)) {
+    if (q.dense && (p.attn_tc || p.x3) && (dh == 16 || dh == 32 || dh == 64) && D == d) {
       // NaiveLowRank (attention.cpp:271-292): P = X [U_q|U_k|U_v], then the
       // block-diagonal V rebuilds dense Q|K|V [T, 3d] (Q scaled by s)
       const float sc = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(dh)));
@@ -339,9 +359,9 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
     p.out_tc = bf && out_ok;
     if (p.out_tc || p.x3) {
       const int pr = p.pr, prp = p.prp;
-      std::vector<float> ut((size_t)prp * d, 0.0f), vt((size_t)d * prp, 0.0f);
+      std::vector<float> ut((size_t)prp * D, 0.0f), vt((size_t)D * prp, 0.0f);
       for (int k = 0; k < d; ++k)
-        for (int j = 0; j < pr; ++j) ut[(size_t)j * d + k] = o.u[(size_t)k * pr + j];
+        for (int j = 0; j < pr; ++j) ut[(size_t)j * D + k] = o.u[(size_t)k * pr + j];
       for (int j = 0; j < pr; ++j)
         for (int n = 0; n < d; ++n) vt[(size_t)n * prp + j] = o.v[(size_t)j * d + n];
       b.tc(&p.uo_t, &p.uo_t_lo, ut);
@@ -353,7 +373,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
           // folded rank-space out-projection: W_ov[(h, j)][n] = sum_c V_v,h[j, c] W_o[h dh + c][n]
           const fsvd_attn_desc& a = *q.attn;
           const int H = p.H, G = p.G, r = p.r, rp = p.rp, dh = p.dh, gd = p.gd, hpg = H / G;
-          std::vector<float> wov((size_t)d * H * rp, 0.0f), bov(d);
+          std::vector<float> wov((size_t)D * H * rp, 0.0f), bov(D, 0.0f);
           for (int n = 0; n < d; ++n) {
             const float* won = &wo_t[(size_t)n * d];
             for (int h = 0; h < H; ++h) {
@@ -377,7 +397,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
       b.store(&p.uo, std::vector<float>(o.u, o.u + (size_t)d * o.rank));
       b.store(&p.vo, std::vector<float>(o.v, o.v + (size_t)o.rank * d));
     }
-    b.store_f32(&p.bo, o.bias, d);
+    b.store_f32(&p.bo, padded(o.bias, d, (p.out_tc || p.x3) ? D : d));
   }
   if (q.ffn) {
     const fsvd_ffn_desc& f = *q.ffn;
@@ -390,14 +410,16 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
     p.ffn_tc = bf && ffn_ok;
     p.ffn_wide = p.ffn_tc && frp > 384;
     if (p.ffn_tc || p.x3) {
-      std::vector<float> uu((size_t)frp * d, 0.0f), vu((size_t)df * frp, 0.0f),
-          ud((size_t)frp * df, 0.0f), vd((size_t)d * frp, 0.0f);
+      const int dfp = all_ok ? pad_to(df, 8) : df;  // padded d_ff rows / columns are zero
+      p.df = dfp;
+      std::vector<float> uu((size_t)frp * D, 0.0f), vu((size_t)dfp * frp, 0.0f),
+          ud((size_t)frp * dfp, 0.0f), vd((size_t)D * frp, 0.0f);
       for (int k = 0; k < d; ++k)
-        for (int j = 0; j < fr; ++j) uu[(size_t)j * d + k] = f.up.u[(size_t)k * fr + j];
+        for (int j = 0; j < fr; ++j) uu[(size_t)j * D + k] = f.up.u[(size_t)k * fr + j];
       for (int j = 0; j < fr; ++j)
         for (int c = 0; c < df; ++c) vu[(size_t)c * frp + j] = f.up.v[(size_t)j * df + c];
       for (int c = 0; c < df; ++c)
-        for (int j = 0; j < fr; ++j) ud[(size_t)j * df + c] = f.down.u[(size_t)c * fr + j];
+        for (int j = 0; j < fr; ++j) ud[(size_t)j * dfp + c] = f.down.u[(size_t)c * fr + j];
       for (int j = 0; j < fr; ++j)
         for (int n = 0; n < d; ++n) vd[(size_t)n * frp + j] = f.down.v[(size_t)j * d + n];
       b.tc(&p.uup_t, &p.uup_t_lo, uu);
@@ -410,20 +432,20 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
       b.store(&p.udn, std::vector<float>(f.down.u, f.down.u + (size_t)df * fr));
       b.store(&p.vdn, std::vector<float>(f.down.v, f.down.v + (size_t)fr * d));
     }
-    b.store_f32(&p.bup, f.up.bias, df);
-    b.store_f32(&p.bdn, f.down.bias, d);
+    b.store_f32(&p.bup, padded(f.up.bias, df, p.df));
+    b.store_f32(&p.bdn, padded(f.down.bias, d, (p.ffn_tc || p.x3) ? D : d));
   }
-  if (q.dense && dense_ok && (bf || p.x3)) build_dense(q, p, b);
+  if (q.dense && all_ok) build_dense(q, p, b);
   if (q.ln1g) {
     p.has_ln = true;
-    b.store_f32(&p.ln1g, q.ln1g, d);
-    b.store_f32(&p.ln1b, q.ln1b, d);
-    b.store_f32(&p.ln2g, q.ln2g, d);
-    b.store_f32(&p.ln2b, q.ln2b, d);
+    b.store_f32(&p.ln1g, padded(q.ln1g, d, D));
+    b.store_f32(&p.ln1b, padded(q.ln1b, d, D));
+    b.store_f32(&p.ln2g, padded(q.ln2g, d, D));
+    b.store_f32(&p.ln2b, padded(q.ln2b, d, D));
     p.eps1 = q.eps1;
     p.eps2 = q.eps2;
   }
-  p.dense = q.dense && dense_ok && (bf || p.x3);
+  p.dense = q.dense && all_ok;
   p.bytes = align256(b.buf.size());
   if (p.bytes) {
     FSVD_CUDA_CHECK(cudaMalloc(&p.mem, p.bytes));
@@ -507,7 +529,6 @@ void check_mode_weights(const fsvd_layer_desc& L, int mode, bool dense_twin_ok) 
 
 // ---------------------------------------------------------------- planner
 size_t op_transient_elems(const Pack& p, int op, int mode) {
-  const size_t d = p.d;
   if (op == 0 || (op == 3 && (mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK))) {
     // materializing baselines: Q|K|V [3 H dhp] (+ naive P [3 G rp]) + context [H dhp]
     const size_t hp = (size_t)p.H * p.dhp;
@@ -540,10 +561,10 @@ namespace {
 // [T, d] FFN output instead when the FFN cannot take its LN fused.
 bool fused_post_ln(const Pack& p, int mode) {
   const bool flash = mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2;
-  return flash && p.attn_tc && p.out_tc && gemm_ln_supported(p.d, p.H * p.rp);
+  return flash && p.attn_tc && p.out_tc && p.d == p.dr && gemm_ln_supported(p.d, p.H * p.rp);
 }
 bool ffn_ln_fusable(const Pack& p, int mode) {
-  return p.ffn_tc && gemm_ln_supported(p.d, p.frp) &&
+  return p.ffn_tc && p.d == p.dr && gemm_ln_supported(p.d, p.frp) &&
          (mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2);
 }
 struct WsLayout {
@@ -603,16 +624,17 @@ Planes wpl(const void* hi, const void* lo) {
 
 void ln(const Pack& p, const void* a, const void* b, const float* g, const float* be, float eps,
         void* y, int rows, cudaStream_t s) {
+  // statistics over the callers' d (p.dr); rows stored with the layout pitch p.d
   if (p.x3) {
     const size_t n = static_cast<size_t>(rows) * p.d;
     const Planes bp = b ? pl(b, n) : Planes{nullptr, nullptr};
-    ln_planes(pl(a, n), b ? &bp : nullptr, g, be, eps, plo(y, n), rows, p.d, s);
+    ln_planes(pl(a, n), b ? &bp : nullptr, g, be, eps, plo(y, n), rows, p.dr, s, p.d);
     return;
   }
   if (p.dtype == FSVD_BF16)
-    resid_layernorm_bf16(as<bf16>(a), as<bf16>(b), g, be, eps, as<bf16>(y), rows, p.d, s);
+    resid_layernorm_bf16(as<bf16>(a), as<bf16>(b), g, be, eps, as<bf16>(y), rows, p.dr, s, p.d);
   else
-    resid_layernorm_f32(as<float>(a), as<float>(b), g, be, eps, as<float>(y), rows, p.d, s);
+    resid_layernorm_f32(as<float>(a), as<float>(b), g, be, eps, as<float>(y), rows, p.dr, s, p.d);
 }
 void add(const Pack& p, const void* a, const void* b, void* y, int64_t n, cudaStream_t s) {
   if (p.x3) {
@@ -1043,7 +1065,7 @@ bool ffn_resid_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, c
 bool ffn_ln_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* out,
                 void* trans, cudaStream_t s) {
   const int T = static_cast<int>(B * M), d = p.d;
-  if (!p.ffn_tc || !gemm_ln_supported(d, p.frp)) return false;
+  if (!p.ffn_tc || p.d != p.dr || !gemm_ln_supported(d, p.frp)) return false;
   if (mode == FSVD_MODE_FLASH_V2 && !p.ffn_wide) {
     FfnTcArgs a{};
     a.T = T;
@@ -1172,7 +1194,7 @@ void layer_decode(const Pack& p, bool pre_ln, size_t B, const void* x, void* out
 namespace {
 // The fused pre-LN tensor-core schedule (layer_fwd) applies to this pack.
 bool pre_ln_fused(const Pack& p, int mode, size_t T) {
-  return p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16 &&
+  return p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16 && p.d == p.dr &&
          (mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2) && !p.ffn_wide &&
          !(mode == FSVD_MODE_FLASH_V2 && use_ffn_pair(p, static_cast<int>(T))) &&
          gemm_ln_supported(p.d, p.H * p.rp) && !pre_ln_unfused();
@@ -1321,7 +1343,7 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
 }
 
 void check_decoder_pack(const Pack& p) {
-  if (!(p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16))
+  if (!(p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16 && p.d == p.dr))
     fail(Kind::Config, "decoder rows run on the bf16 tensor-core flash path (bf16 pack, "
                        "rank padding 16/32/64)");
 }

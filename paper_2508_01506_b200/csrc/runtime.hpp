@@ -23,7 +23,9 @@ namespace fsvd {
 struct Pack {
   fsvd_dtype dtype = FSVD_BF16;
   int es = 2;  // bytes per stored element
-  int d = 0, df = 0, H = 1, G = 1, r = 0, pr = 0, fr = 0, dh = 0, gd = 0, act = 0;
+  // d: model dimension of the device layouts (the callers' dr rounded up to
+  // 64 on the tensor-core path, zero-padded); df likewise (rounded up to 8)
+  int d = 0, dr = 0, df = 0, H = 1, G = 1, r = 0, pr = 0, fr = 0, dh = 0, gd = 0, act = 0;
   float eps1 = 1e-5f, eps2 = 1e-5f;
   int rp = 0, prp = 0, frp = 0;
   bool has_attn = false, has_out = false, has_ffn = false, has_ln = false, dense = false;

@@ -270,26 +270,27 @@ __global__ void __launch_bounds__(256) k_simt_ffn(const T* __restrict__ x, const
 // y = gamma * ((a + b) - mean) / sqrt(var + eps) + beta, one warp per row,
 // biased variance (tensor.cpp:88-102).  Rows up to 32*VPL values stay in
 // registers; wider rows take the strided path.
+// Rows have `pitch` >= d stored columns (the tensor-core layouts pad the
+// model dimension with zeros): statistics over the first d, the normalised
+// value written to all pitch columns (gamma = beta = 0 in the padding -> 0).
 template <typename T, int VPL>
 __global__ void k_resid_ln(const T* a, const T* b,
                            const float* __restrict__ gamma, const float* __restrict__ beta,
-                           float eps, T* y, int rows, int d) {
+                           float eps, T* y, int rows, int d, int pitch) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
-  const int64_t base = (int64_t)warp * d;
+  const int64_t base = (int64_t)warp * pitch;
   const float inv_d = 1.0f / static_cast<float>(d);
-  if (d <= 32 * VPL) {
+  if (pitch <= 32 * VPL) {
     float v[VPL];
     float s = 0.0f;
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       const int c = lane + 32 * i;
       v[i] = 0.0f;
-      if (c < d) {
-        v[i] = ld(a + base + c) + (b ? ld(b + base + c) : 0.0f);
-        s += v[i];
-      }
+      if (c < pitch) v[i] = ld(a + base + c) + (b ? ld(b + base + c) : 0.0f);
+      if (c < d) s += v[i];
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -309,7 +310,7 @@ __global__ void k_resid_ln(const T* a, const T* b,
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       const int c = lane + 32 * i;
-      if (c < d) y[base + c] = cvt<T>(gamma[c] * ((v[i] - mean) * inv) + beta[c]);
+      if (c < pitch) y[base + c] = cvt<T>(gamma[c] * ((v[i] - mean) * inv) + beta[c]);
     }
   } else {
     float s = 0.0f;
@@ -323,7 +324,7 @@ __global__ void k_resid_ln(const T* a, const T* b,
     }
     for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
     const float inv = 1.0f / sqrtf(q * inv_d + eps);
-    for (int c = lane; c < d; c += 32) {
+    for (int c = lane; c < pitch; c += 32) {
       const float t = ld(a + base + c) + (b ? ld(b + base + c) : 0.0f);
       y[base + c] = cvt<T>(gamma[c] * ((t - mean) * inv) + beta[c]);
     }
@@ -441,11 +442,12 @@ int elementwise_grid(int64_t n) {
 
 template <typename T>
 void launch_ln(const T* a, const T* b, const float* gamma, const float* beta, float eps, T* y,
-               int rows, int d, cudaStream_t s) {
+               int rows, int d, cudaStream_t s, int pitch) {
   const int threads = 256;
   const int grid = (rows * 32 + threads - 1) / threads;
+  if (pitch <= 0) pitch = d;
   if constexpr (sizeof(T) == 2) {
-    if (d % 8 == 0 && d <= 32 * 8 * 4) {
+    if (pitch == d && d % 8 == 0 && d <= 32 * 8 * 4) {
       if (d <= 32 * 8 * 2)
         launch_pdl(k_resid_ln_bf16x8<2>, dim3(grid), dim3(threads), 0, s, a, b, gamma, beta, eps, y,
                    rows, d);
@@ -456,12 +458,13 @@ void launch_ln(const T* a, const T* b, const float* gamma, const float* beta, fl
       return;
     }
   }
-  if (d <= 32 * 8)
-    k_resid_ln<T, 8><<<grid, threads, 0, s>>>(a, b, gamma, beta, eps, y, rows, d);
-  else if (d <= 32 * 24)
-    k_resid_ln<T, 24><<<grid, threads, 0, s>>>(a, b, gamma, beta, eps, y, rows, d);
+  // in place (y == a or b) needs the register path: pitch <= 1024
+  if (pitch <= 32 * 8)
+    k_resid_ln<T, 8><<<grid, threads, 0, s>>>(a, b, gamma, beta, eps, y, rows, d, pitch);
+  else if (pitch <= 32 * 24)
+    k_resid_ln<T, 24><<<grid, threads, 0, s>>>(a, b, gamma, beta, eps, y, rows, d, pitch);
   else
-    k_resid_ln<T, 32><<<grid, threads, 0, s>>>(a, b, gamma, beta, eps, y, rows, d);
+    k_resid_ln<T, 32><<<grid, threads, 0, s>>>(a, b, gamma, beta, eps, y, rows, d, pitch);
   check_launch("k_resid_ln");
 }
 
@@ -528,12 +531,12 @@ void simt_ffn_fused(const T* x, const T* up_u, const T* up_v, const float* up_b,
 }
 
 void resid_layernorm_bf16(const bf16* a, const bf16* b, const float* gamma, const float* beta,
-                          float eps, bf16* y, int rows, int d, cudaStream_t s) {
-  launch_ln<bf16>(a, b, gamma, beta, eps, y, rows, d, s);
+                          float eps, bf16* y, int rows, int d, cudaStream_t s, int pitch) {
+  launch_ln<bf16>(a, b, gamma, beta, eps, y, rows, d, s, pitch);
 }
 void resid_layernorm_f32(const float* a, const float* b, const float* gamma, const float* beta,
-                         float eps, float* y, int rows, int d, cudaStream_t s) {
-  launch_ln<float>(a, b, gamma, beta, eps, y, rows, d, s);
+                         float eps, float* y, int rows, int d, cudaStream_t s, int pitch) {
+  launch_ln<float>(a, b, gamma, beta, eps, y, rows, d, s, pitch);
 }
 void add_bf16(const bf16* a, const bf16* b, bf16* y, int64_t n, cudaStream_t s) {
   launch_pdl(k_add<bf16>, dim3(elementwise_grid(n)), dim3(256), 0, s, a, b, y, n);
