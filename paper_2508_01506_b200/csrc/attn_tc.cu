@@ -93,29 +93,32 @@ namespace {
 #define ATRACE(slot) do { } while (0)
 #endif
 
-// X3 (fp32 policy, split planes -- planes.cu): Qt, P_k, P_v arrive as hi and
-// lo planes; S = Q_hi K_hi + Q_hi K_lo + Q_lo K_hi, the probabilities are
-// computed in fp32 (MUFU ex2 only) and stored to TMEM as P_hi and P_lo, and
-// O += P_hi V_hi + P_hi V_lo + P_lo V_hi; the output leaves as two planes.
-// One CTA per SM (twice the tiles, 512 TMEM columns).
+// X3 (fp32 policy, split planes -- kernels.cuh): Qt, P_k, P_v arrive as three
+// bf16 planes each (one stacked tensor map, plane p at row offset p*plane_rows);
+// S and O accumulate the six plane pairs of order <= 2, the probabilities are
+// computed in fp32 (MUFU ex2 only) and stored to TMEM as three planes, and the
+// output leaves as three planes (out_ps elements apart).  One CTA per SM.
+__device__ __forceinline__ int x3_pa(int g) { return (0x120100 >> (4 * g)) & 15; }
+__device__ __forceinline__ int x3_pb(int g) { return (0x102010 >> (4 * g)) & 15; }
+
 template <int RP, bool X3 = false>
 struct AttnCfg {
-  static constexpr int STAGES = (RP >= 64 && !X3) || (X3 && RP >= 64) ? 2 : 3;
+  static constexpr int STAGES = X3 ? (RP >= 64 ? 1 : RP >= 32 ? 2 : 3) : (RP >= 64 ? 2 : 3);
   static constexpr int RB = RP * 2;       // bytes per rank-width row
   static constexpr int TILE = QT * RB;    // one Qt / P_k / P_v tile (one plane)
-  static constexpr int NPL = X3 ? 2 : 1;  // planes per operand
+  static constexpr int NPL = X3 ? 3 : 1;  // planes per operand
   static constexpr int Q_SLOT = NPL * up1k(TILE);
   static constexpr int o_q = 0;           // two Qt slots (next item prefetched)
   static constexpr int o_kv = o_q + 2 * Q_SLOT;
-  // KV stage: K_hi [K_lo] V_hi [V_lo]
+  // KV stage: the K planes, then the V planes
   static constexpr int KV_STAGE = 2 * NPL * up1k(TILE);
-  static constexpr int kv_klo = up1k(TILE), kv_v = NPL * up1k(TILE), kv_vlo = kv_v + up1k(TILE);
+  static constexpr int kv_v = NPL * up1k(TILE);
   static constexpr int o_bar = o_kv + STAGES * KV_STAGE;
   static constexpr int SMEM = 1024 + o_bar + 4608;  // Bars
   // TMEM columns: S (fp32, 128 keys), O (fp32, RP; two buffers when they fit
   // so an item's output is written while the next item runs), P (bf16 pairs),
-  // X3: P_lo after P
-  static constexpr int t_s = 0, t_o = 128, t_p = 192, t_p2 = 256;
+  // X3: the P planes at t_p + 64 * plane
+  static constexpr int t_s = 0, t_o = 128, t_p = 192;
   static constexpr int NOB = RP <= 32 ? 2 : 1;
   static constexpr int TMEM_COLS = X3 ? 512 : 256;
   static constexpr int CTAS = X3 ? 1 : 2;
@@ -163,8 +166,7 @@ template <int RP, bool X3 = false>
 __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
     k_attn_rankspace(const __grid_constant__ CUtensorMap tmQKV, bf16* __restrict__ out,
                      int64_t ldo, int batch, int seq, int heads, int groups, int q_off, int k_off,
-                     int v_off, int causal, const __grid_constant__ CUtensorMap tmQKV2,
-                     bf16* __restrict__ out2) {
+                     int v_off, int causal, int plane_rows, int64_t out_ps) {
   using C = AttnCfg<RP, X3>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -178,7 +180,6 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
 
   if (warp == kTma && lane == 0) {
     tma_prefetch(&tmQKV);
-    if (X3) tma_prefetch(&tmQKV2);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->q_full[i], 1);
       mbar_init(&bars->q_empty[i], 1);
@@ -218,22 +219,19 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
         mbar_wait(&bars->q_empty[qs], ((it >> 1) & 1) ^ 1);
         if (it < 100) ATRACE(500 + it);
         mbar_arrive_expect_tx(&bars->q_full[qs], C::NPL * C::TILE);
-        tma_load_2d(&tmQKV, &bars->q_full[qs], smem + C::o_q + qs * C::Q_SLOT,
-                    q_off + h * RP, row0 + qt * QT);
-        if (X3)
-          tma_load_2d(&tmQKV2, &bars->q_full[qs], smem + C::o_q + qs * C::Q_SLOT + up1k(C::TILE),
-                      q_off + h * RP, row0 + qt * QT);
+        for (int pl = 0; pl < C::NPL; ++pl)
+          tma_load_2d(&tmQKV, &bars->q_full[qs], smem + C::o_q + qs * C::Q_SLOT + pl * up1k(C::TILE),
+                      q_off + h * RP, row0 + qt * QT + pl * plane_rows);
         const int nji = causal ? min(nj, qt + 1) : nj;  // key tiles of this item
         for (int j = 0; j < nji; ++j) {
           mbar_wait(&bars->kv_empty[st], ph ^ 1);
           uint8_t* kv = smem + C::o_kv + st * C::KV_STAGE;
           mbar_arrive_expect_tx(&bars->kv_full[st], 2 * C::NPL * C::TILE);
-          tma_load_2d(&tmQKV, &bars->kv_full[st], kv, k_off + g * RP, row0 + j * KT);
-          tma_load_2d(&tmQKV, &bars->kv_full[st], kv + C::kv_v, v_off + g * RP, row0 + j * KT);
-          if (X3) {
-            tma_load_2d(&tmQKV2, &bars->kv_full[st], kv + C::kv_klo, k_off + g * RP, row0 + j * KT);
-            tma_load_2d(&tmQKV2, &bars->kv_full[st], kv + C::kv_vlo, v_off + g * RP,
-                        row0 + j * KT);
+          for (int pl = 0; pl < C::NPL; ++pl) {
+            tma_load_2d(&tmQKV, &bars->kv_full[st], kv + pl * up1k(C::TILE), k_off + g * RP,
+                        row0 + j * KT + pl * plane_rows);
+            tma_load_2d(&tmQKV, &bars->kv_full[st], kv + C::kv_v + pl * up1k(C::TILE),
+                        v_off + g * RP, row0 + j * KT + pl * plane_rows);
           }
           if (++st == C::STAGES) { st = 0; ph ^= 1; }
         }
@@ -244,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
     // ------------------------------------------------ MMA issuer (warp-uniform)
     const uint64_t dk0 = desc_kmajor(s_kv, C::RB);
     const uint64_t dv0 = desc_mnmajor(s_kv + C::kv_v, C::RB);
-    constexpr uint32_t kLoOff = up1k(C::TILE) >> 4;  // lo plane, descriptor units
+    constexpr uint32_t kPlOff = up1k(C::TILE) >> 4;  // one plane, descriptor units
     int gt = 0;  // key tiles issued so far by this CTA (all items)
     int it = 0;
     // S for global tile index t of the item whose Qt is in slot qs
@@ -259,13 +257,13 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
 #pragma unroll
         for (int k = 0; k < RP / 16; ++k)
           mma_bf16_ss(tmem + C::t_s, dq + 2 * k, dk + 2 * k, idesc_bf16(128, KT), k != 0);
-        if (X3) {  // + Q_hi K_lo + Q_lo K_hi
+        if (X3) {  // the other five plane pairs of order <= 2
 #pragma unroll
-          for (int k = 0; k < RP / 16; ++k)
-            mma_bf16_ss(tmem + C::t_s, dq + 2 * k, dk + kLoOff + 2 * k, idesc_bf16(128, KT), 1u);
+          for (int g = 1; g < 6; ++g)
 #pragma unroll
-          for (int k = 0; k < RP / 16; ++k)
-            mma_bf16_ss(tmem + C::t_s, dq + kLoOff + 2 * k, dk + 2 * k, idesc_bf16(128, KT), 1u);
+            for (int k = 0; k < RP / 16; ++k)
+              mma_bf16_ss(tmem + C::t_s, dq + x3_pa(g) * kPlOff + 2 * k,
+                          dk + x3_pb(g) * kPlOff + 2 * k, idesc_bf16(128, KT), 1u);
         }
         mma_commit(&bars->s_full);
       }
@@ -308,16 +306,15 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
           for (int k = 0; k < KT / 16; ++k)
             mma_bf16_ts(t_o, tmem + C::t_p + k * 8, dv + ((k * 16 * C::RB) >> 4),
                         idesc_bf16(128, RP, 0, 1), (j | k) != 0);
-          if (X3) {  // + P_hi V_lo + P_lo V_hi
-            constexpr uint32_t kVLo = (C::kv_vlo - C::kv_v) >> 4;
+          if (X3) {  // the other five plane pairs: P plane x3_pa(g) (TMEM), V plane x3_pb(g)
+            constexpr uint32_t kPl = up1k(C::TILE) >> 4;
 #pragma unroll
-            for (int k = 0; k < KT / 16; ++k)
-              mma_bf16_ts(t_o, tmem + C::t_p + k * 8, dv + kVLo + ((k * 16 * C::RB) >> 4),
-                          idesc_bf16(128, RP, 0, 1), 1u);
+            for (int g = 1; g < 6; ++g)
 #pragma unroll
-            for (int k = 0; k < KT / 16; ++k)
-              mma_bf16_ts(t_o, tmem + C::t_p2 + k * 8, dv + ((k * 16 * C::RB) >> 4),
-                          idesc_bf16(128, RP, 0, 1), 1u);
+              for (int k = 0; k < KT / 16; ++k)
+                mma_bf16_ts(t_o, tmem + C::t_p + 64 * x3_pa(g) + k * 8,
+                            dv + x3_pb(g) * kPl + ((k * 16 * C::RB) >> 4),
+                            idesc_bf16(128, RP, 0, 1), 1u);
           }
           mma_commit(&bars->o_full);
           mma_commit(&bars->kv_empty[st]);
@@ -372,11 +369,11 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
           for (int i = 0; i < 16; ++i) o[i] = __uint_as_float(r[i]) * inv;
 #pragma unroll
           for (int pl = 0; pl < C::NPL; ++pl) {
-            if (pl == 1) {
+            if (pl > 0) {
 #pragma unroll
               for (int i = 0; i < 16; ++i) o[i] -= bf16_round_f(o[i]);
             }
-            uint4* dst = reinterpret_cast<uint4*>((pl == 0 ? out : out2) + off);
+            uint4* dst = reinterpret_cast<uint4*>(out + pl * out_ps + off);
 #pragma unroll
             for (int v = 0; v < 2; ++v)
               dst[v] = make_uint4(pack_bf16(o[8 * v + 0], o[8 * v + 1]),
@@ -447,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
         const float alpha = ex2(m_run - m_new);
         m_run = m_new;
         uint32_t pk[KH / 2];
-        uint32_t pk2[KH / 2];  // X3: P_lo (dead otherwise)
+        uint32_t pk2[KH / 2], pk3[KH / 2];  // X3: P_mid, P_lo (dead otherwise)
         float2 sum2 = make_float2(0.0f, 0.0f);
         const float2 nm = make_float2(-m_new, -m_new);
 #pragma unroll
@@ -459,7 +456,11 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
                                : make_float2(ex2(d.x), ex2(d.y));
           sum2 = __fadd2_rn(sum2, p);
           pk[c] = pack_bf16(p.x, p.y);
-          if (X3) pk2[c] = pack_bf16(p.x - bf16_round_f(p.x), p.y - bf16_round_f(p.y));
+          if (X3) {
+            const float2 r = make_float2(p.x - bf16_round_f(p.x), p.y - bf16_round_f(p.y));
+            pk2[c] = pack_bf16(r.x, r.y);
+            pk3[c] = pack_bf16(r.x - bf16_round_f(r.x), r.y - bf16_round_f(r.y));
+          }
         }
         l_run = fmaf(l_run, alpha, sum2.x + sum2.y);
         // single-buffered probability tile: the previous PV (this item's, or
@@ -472,7 +473,10 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
         }
         // this half's 64 keys -> TMEM columns [t_p + 32*half, +32) of this row
         tmem_st32(tq + C::t_p + half * 32, pk);
-        if (X3) tmem_st32(tq + C::t_p2 + half * 32, pk2);
+        if (X3) {
+          tmem_st32(tq + C::t_p + 64 + half * 32, pk2);
+          tmem_st32(tq + C::t_p + 128 + half * 32, pk3);
+        }
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars->p_full);
@@ -519,15 +523,14 @@ void launch_attn(const AttnTcArgs& a, cudaStream_t s) {
     attr = true;
   }
   const int T = a.batch * a.seq;
-  const CUtensorMap tm =
-      tmap_bf16(a.qkv, T, a.qkv_cols, a.ldq, 128, RP, swizzle_for_row_bytes(C::RB));
-  const CUtensorMap tm2 =
-      X3 ? tmap_bf16(a.qkv_lo, T, a.qkv_cols, a.ldq, 128, RP, swizzle_for_row_bytes(C::RB)) : tm;
+  // X3: the three planes of qkv stacked ([3T, qkv_cols], plane p at row p*T)
+  const CUtensorMap tm = tmap_bf16(a.qkv, (uint64_t)C::NPL * T, a.qkv_cols, a.ldq, 128, RP,
+                                   swizzle_for_row_bytes(C::RB));
   const int items = ((a.seq + QT - 1) / QT) * a.heads * a.batch;
   const int grid = items < C::CTAS * num_sms() ? items : C::CTAS * num_sms();
   launch_pdl(k_attn_rankspace<RP, X3>, dim3(grid), dim3(kThreads), C::SMEM, s, tm, a.out, a.ldo,
-             a.batch, a.seq, a.heads, a.groups, a.q_off, a.k_off, a.v_off, a.causal ? 1 : 0, tm2,
-             a.out_lo);
+             a.batch, a.seq, a.heads, a.groups, a.q_off, a.k_off, a.v_off, a.causal ? 1 : 0,
+             X3 ? T : 0, X3 ? a.out_ps : (int64_t)0);
   check_launch("k_attn_rankspace");
 }
 
@@ -538,7 +541,7 @@ bool attn_rankspace_supported(int rank_pad) {
 }
 
 void attn_rankspace_bf16(const AttnTcArgs& a, cudaStream_t s) {
-  if (a.qkv_lo != nullptr) {  // split planes (fp32 policy)
+  if (a.planes) {  // split planes (fp32 policy)
     switch (a.rank_pad) {
       case 16: launch_attn<16, true>(a, s); return;
       case 32: launch_attn<32, true>(a, s); return;

@@ -53,10 +53,11 @@ constexpr int STAGE = 2 * SLOT;  // two slots per ring stage
 // pairs, and each slice recomputes the hidden block.
 //
 // X3 (fp32 policy, K3 only, on the WIDE structure): P, V_up, U_down and the
-// hidden block are split planes (planes.cu).  MMA1 streams (P_hi, V_up_hi)
-// and (P_lo, V_up_lo) as two consecutive ring stages and issues
-// P_hi V_hi + P_lo V_hi + P_hi V_lo; the epilogue writes H_hi and H_lo; MMA2
-// takes (U_dn_hi, U_dn_lo) per stage for H_hi U_hi + H_lo U_hi + H_hi U_lo.
+// hidden block are three bf16 planes each (kernels.cuh; P / V_up / U_down
+// through one stacked tensor map each).  MMA1 streams (P_pl, V_up_pl) for the
+// three planes as three consecutive ring stages and issues the six plane
+// pairs of order <= 2; the epilogue writes H in three planes; MMA2 takes
+// (U_dn_hi, U_dn_mid) and (U_dn_lo) as two stages per (atom, piece).
 template <int FR, bool WIDE = false, bool X3 = false>
 struct FfnCfg {
   static_assert(FR % 64 == 0 && FR <= 384, "FR must be a multiple of 64, <= 384");
@@ -65,7 +66,7 @@ struct FfnCfg {
   static constexpr int PS = (FR % 128 == 0) ? 128 : 64;  // rows per Z / P piece
   static constexpr int NPIECE = FR / PS;
   static constexpr int PATOMS = WIDE ? 0 : NATOM;        // resident P atoms
-  static constexpr int HATOMS = X3 ? 4 : 2;              // H tile (hi, [lo]) atoms
+  static constexpr int HATOMS = X3 ? 6 : 2;              // H tile atoms (X3: 3 planes)
   static constexpr int STAGES_FIT = (227 * 1024 - 2048 - (PATOMS + HATOMS) * SLOT) / STAGE;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int o_p = 0;                  // P / Z tile, NATOM atoms
@@ -85,6 +86,10 @@ struct FfnBars {
   uint64_t res_full[2], res_empty[2];  // residual boxes of the fused LN2 (H region)
   uint32_t tmem;
 };
+
+// X3 plane pairs of order <= 2: (hi,hi) (hi,mid) (mid,hi) (hi,lo) (lo,hi) (mid,mid)
+__device__ __forceinline__ int x3_pa(int g) { return (0x120100 >> (4 * g)) & 15; }
+__device__ __forceinline__ int x3_pb(int g) { return (0x102010 >> (4 * g)) & 15; }
 
 // 32 consecutive fp32 columns of this thread's TMEM row.
 __device__ __forceinline__ void ld_chunk(uint32_t taddr, float (&v)[32]) {
@@ -141,9 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           int d_model, int d_ff, bf16* z_out, bf16* out,
           const float* __restrict__ ln_g, const float* __restrict__ ln_b, float ln_eps,
           int split_blocks, float* __restrict__ z_part, const bf16* resid,
-          int frk, bf16* sum_out, const __grid_constant__ CUtensorMap tmP2,
-          const __grid_constant__ CUtensorMap tmVup2, const __grid_constant__ CUtensorMap tmUdn2,
-          bf16* z_out2) {
+          int frk, bf16* sum_out, int64_t z_ps) {
   static_assert(!(WIDE && FUSED), "wide ranks run the V1 chain");
   using C = FfnCfg<FR, WIDE, X3>;
   extern __shared__ uint8_t smem_raw[];
@@ -176,11 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmUdn);
     tma_prefetch(&tmVdn);
     if (FUSED) tma_prefetch(&tmX); else tma_prefetch(&tmP);
-    if (X3) {
-      tma_prefetch(&tmP2);
-      tma_prefetch(&tmVup2);
-      tma_prefetch(&tmUdn2);
-    }
+
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&bars->full[i], 1);
       mbar_init(&bars->empty[i], 1);
@@ -238,14 +237,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
       auto mma1_slots = [&](int f) {
-        if (X3) {  // (P_hi a, V_hi a), (P_lo a, V_lo a): two stages per atom
-          emit(4 * NK, [&](int j, uint8_t* dst, bool size_only) -> uint32_t {
+        if (X3) {  // (P_pl a, V_pl a) for pl = hi, mid, lo: three stages per atom
+          emit(6 * NK, [&](int j, uint8_t* dst, bool size_only) -> uint32_t {
             if (!size_only) {
-              const int a = j >> 2, w = j & 3;
+              const int a = j / 6, w = j % 6, pl = w >> 1;
               if (w & 1)
-                tma_load_2d(w == 1 ? &tmVup : &tmVup2, &bars->full[st], dst, a * 64, (fb0 + f) * BF);
+                tma_load_2d(&tmVup, &bars->full[st], dst, a * 64, (fb0 + f) * BF + pl * d_ff);
               else
-                tma_load_2d(w == 0 ? &tmP : &tmP2, &bars->full[st], dst, a * 64, m0);
+                tma_load_2d(&tmP, &bars->full[st], dst, a * 64, m0 + pl * T);
             }
             return SLOT;
           });
@@ -267,14 +266,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         });
       };
       auto mma2_slots = [&](int f) {  // atom-major: (a0: p0..), (a1: p0..)
-        if (X3) {  // (U_dn_hi, U_dn_lo) of one (atom, piece) per stage
-          emit(4 * C::NPIECE, [&](int j, uint8_t* dst, bool size_only) -> uint32_t {
-            const int k = j >> 1, a = k / C::NPIECE, p = k % C::NPIECE;
-            if (!size_only)
-              tma_load_2d((j & 1) ? &tmUdn2 : &tmUdn, &bars->full[st], dst,
-                          (fb0 + f) * BF + a * 64, zc0 + p * C::PS);
-            return C::PS * 128;
-          });
+        if (X3) {  // per (atom, piece): stages (U_dn_hi, U_dn_mid), (U_dn_lo)
+          for (int k = 0; k < 2 * C::NPIECE; ++k) {
+            const int a = k / C::NPIECE, p = k % C::NPIECE;
+            emit(3, [&](int pl, uint8_t* dst, bool size_only) -> uint32_t {
+              if (!size_only)
+                tma_load_2d(&tmUdn, &bars->full[st], dst, (fb0 + f) * BF + a * 64,
+                            zc0 + p * C::PS + pl * frk);
+              return C::PS * 128;
+            });
+          }
           return;
         }
         emit(2 * C::NPIECE, [&](int j, uint8_t* dst, bool size_only) -> uint32_t {
@@ -397,22 +398,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         TRACE(64 + f * 8 + 1);
         if (X3) {
-          // stage pair per atom: hold (P_hi, V_hi) until (P_lo, V_lo) has
-          // arrived, issue the three products, then release both
+          // three stages per atom (plane pl: P at the stage base, V_up one
+          // slot on): hold all three, issue the six plane pairs, release
           for (int a = 0; a < NK; ++a) {
-            const uint32_t st1 = st, ph1 = ph;
-            if (++st == C::STAGES) { st = 0; ph ^= 1; }
-            mbar_wait(&bars->full[st1], ph1);
-            mbar_wait(&bars->full[st], ph);
+            uint32_t sts[3];
+            uint64_t sd[3];
+            for (int pl = 0; pl < 3; ++pl) {
+              sts[pl] = st;
+              mbar_wait(&bars->full[st], ph);
+              sd[pl] = d_ring + ((st * STAGE) >> 4);
+              if (++st == C::STAGES) { st = 0; ph ^= 1; }
+            }
             tc_fence_after();
-            const uint64_t s1 = d_ring + ((st1 * STAGE) >> 4), s2 = d_ring + ((st * STAGE) >> 4);
             const uint32_t idh = idesc_bf16(128, BF);
-            mma4(tmem + C::t_h, s1, s1 + kAtom, idh, a != 0);  // P_hi V_hi
-            mma4(tmem + C::t_h, s2, s1 + kAtom, idh, true);    // P_lo V_hi
-            mma4(tmem + C::t_h, s1, s2 + kAtom, idh, true);    // P_hi V_lo
-            commit(&bars->empty[st1]);
-            commit(&bars->empty[st]);
-            if (++st == C::STAGES) { st = 0; ph ^= 1; }
+#pragma unroll
+            for (int g = 0; g < 6; ++g)
+              mma4(tmem + C::t_h, sd[x3_pa(g)], sd[x3_pb(g)] + kAtom, idh, (a | g) != 0);
+            for (int pl = 0; pl < 3; ++pl) commit(&bars->empty[sts[pl]]);
           }
         } else if (WIDE) {
           uint64_t pa = 0;
@@ -430,24 +432,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       auto mma2 = [&](int f) {
         if (X3) {
-          uint64_t hi_slot = 0;
-          consume(4 * C::NPIECE, [&](int j, uint64_t slot) {
-            const int k = j >> 1, a = k / C::NPIECE, p = k % C::NPIECE;
-            if ((j & 1) == 0) {
-              if (p == 0) {
-                mbar_wait(&bars->sh_full[a], f & 1);
-                tc_fence_after();
-              }
-              hi_slot = slot;
-              return;
+          for (int k = 0; k < 2 * C::NPIECE; ++k) {
+            const int a = k / C::NPIECE, p = k % C::NPIECE;
+            if (p == 0) {
+              mbar_wait(&bars->sh_full[a], f & 1);
+              tc_fence_after();
             }
+            const uint32_t st1 = st;  // (U_hi, U_mid)
+            mbar_wait(&bars->full[st], ph);
+            const uint64_t s1 = d_ring + ((st * STAGE) >> 4);
+            if (++st == C::STAGES) { st = 0; ph ^= 1; }
+            const uint32_t st2 = st;  // (U_lo)
+            mbar_wait(&bars->full[st], ph);
+            const uint64_t s2 = d_ring + ((st * STAGE) >> 4);
+            if (++st == C::STAGES) { st = 0; ph ^= 1; }
+            tc_fence_after();
+            const uint64_t u[3] = {s1, s1 + kAtom, s2};
             const uint32_t idz = idesc_bf16(128, C::PS);
             const uint32_t zt = tmem + C::t_z + p * C::PS;
-            mma4(zt, d_h + a * kAtom, hi_slot, idz, (f | a) != 0);  // H_hi U_hi
-            mma4(zt, d_h + (2 + a) * kAtom, hi_slot, idz, true);   // H_lo U_hi
-            mma4(zt, d_h + a * kAtom, slot, idz, true);            // H_hi U_lo
+#pragma unroll
+            for (int g = 0; g < 6; ++g)  // H plane x3_pa(g) (atoms 2*pl + a), U plane x3_pb(g)
+              mma4(zt, d_h + (2 * x3_pa(g) + a) * kAtom, u[x3_pb(g)], idz, (f | a | g) != 0);
+            commit(&bars->empty[st1]);
+            commit(&bars->empty[st2]);
             if (p == C::NPIECE - 1) commit(&bars->sh_free[a]);
-          });
+          }
           return;
         }
         consume(2 * C::NPIECE, [&](int j, uint64_t slot) {
@@ -523,15 +532,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&bars->h_free);
 #pragma unroll
       for (int i = 0; i < 2; ++i) {  // i = K atom of the H block
-        bias_act_chunk2<32>(v[i], bb[i], act);
+        if (X3) bias_act_chunk2_exact<32>(v[i], bb[i], act);
+        else bias_act_chunk2<32>(v[i], bb[i], act);
         if (threadIdx.x == 64) TRACE(1024 + f * 8 + 2 + i * 2);
         if (f > 0) mbar_wait(&bars->sh_free[i], (f - 1) & 1);
         if (threadIdx.x == 64) TRACE(1024 + f * 8 + 3 + i * 2);
         st_chunk_smem(s_h, row, (half + 2 * i) * 32, v[i]);
-        if (X3) {  // lo plane of the activated block, atoms 2..3
+        if (X3) {  // mid and lo planes of the activated block, atoms 2..3 and 4..5
 #pragma unroll
-          for (int k = 0; k < 32; ++k) v[i][k] -= bf16_round_f(v[i][k]);
-          st_chunk_smem(s_h + 2 * SLOT, row, (half + 2 * i) * 32, v[i]);
+          for (int pl = 1; pl < 3; ++pl) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[i][k] -= bf16_round_f(v[i][k]);
+            st_chunk_smem(s_h + 2 * pl * SLOT, row, (half + 2 * i) * 32, v[i]);
+          }
         }
         fence_proxy_async_smem();
         tc_fence_before();
@@ -555,8 +568,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           st_chunk_global(z_out + (int64_t)grow * frk + zc0 + c * 32, v);
           if (X3) {
 #pragma unroll
-            for (int k = 0; k < 32; ++k) v[k] -= bf16_round_f(v[k]);
-            st_chunk_global(z_out2 + (int64_t)grow * frk + zc0 + c * 32, v);
+            for (int pl = 1; pl < 3; ++pl) {
+#pragma unroll
+              for (int k = 0; k < 32; ++k) v[k] -= bf16_round_f(v[k]);
+              st_chunk_global(z_out + pl * z_ps + (int64_t)grow * frk + zc0 + c * 32, v);
+            }
           }
         }
       }
@@ -631,8 +647,10 @@ void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
   const int boxp = C::PS;
   const int boxd = (a.d_model % 128 == 0) ? 128 : 64;
   const CUtensorMap tup = tmap_bf16(a.up_u_t, frk, a.d_model, a.d_model, boxp, 64, TmaSwizzle::B128);
-  const CUtensorMap tvup = tmap_bf16(a.up_v_t, a.d_ff, frk, frk, BF, 64, TmaSwizzle::B128);
-  const CUtensorMap tudn = tmap_bf16(a.dn_u_t, frk, a.d_ff, a.d_ff, boxp, 64, TmaSwizzle::B128);
+  // X3: stacked planes (kernels.cuh): V_up^T [3 d_ff, frk], U_dn^T [3 frk, d_ff], P [3T, frk]
+  const uint64_t npl = X3 ? 3 : 1;
+  const CUtensorMap tvup = tmap_bf16(a.up_v_t, npl * a.d_ff, frk, frk, BF, 64, TmaSwizzle::B128);
+  const CUtensorMap tudn = tmap_bf16(a.dn_u_t, npl * frk, a.d_ff, a.d_ff, boxp, 64, TmaSwizzle::B128);
   const CUtensorMap tvdn = tmap_bf16(a.dn_v_t, a.d_model, frk, frk, FUSED && a.ln_g ? 64 : boxd, 64,
                                      TmaSwizzle::B128);
   CUtensorMap tx = tvup, tp = tvup, ty = tvup, tr = tvup;
@@ -642,13 +660,7 @@ void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
     tr = a.ln_resid ? tmap_bf16(a.ln_resid, a.T, a.d_model, a.d_model, 128, 64, TmaSwizzle::B128)
                     : tx;
   } else
-    tp = tmap_bf16(a.p_in, a.T, frk, frk, 128, 64, TmaSwizzle::B128);
-  CUtensorMap tp2 = tp, tvup2 = tvup, tudn2 = tudn;
-  if (X3) {
-    tp2 = tmap_bf16(a.p_in_lo, a.T, frk, frk, 128, 64, TmaSwizzle::B128);
-    tvup2 = tmap_bf16(a.up_v_t_lo, a.d_ff, frk, frk, BF, 64, TmaSwizzle::B128);
-    tudn2 = tmap_bf16(a.dn_u_t_lo, frk, a.d_ff, a.d_ff, boxp, 64, TmaSwizzle::B128);
-  }
+    tp = tmap_bf16(a.p_in, npl * a.T, frk, frk, 128, 64, TmaSwizzle::B128);
   const int grid = (a.T + BMr - 1) / BMr;
   const int nball = (a.d_ff + BF - 1) / BF;
   const int splits = (!FUSED && a.split_blocks) ? (nball + a.split_blocks - 1) / a.split_blocks : 1;
@@ -656,13 +668,13 @@ void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
              s, tx, tp, tup, tvup, tudn, tvdn, ty, tr, a.up_b, a.dn_b, a.act, a.T, a.d_model,
              a.d_ff, a.z_out, a.out, a.ln_g, a.ln_b, a.ln_eps, FUSED ? 0 : a.split_blocks,
              FUSED ? nullptr : a.z_part, FUSED ? a.resid : nullptr, frk,
-             FUSED && a.ln_g ? a.sum_out : nullptr, tp2, tvup2, tudn2, a.z_out_lo);
+             FUSED && a.ln_g ? a.sum_out : nullptr, X3 ? (int64_t)a.T * frk : (int64_t)0);
   check_launch(FUSED ? "k_ffn_fused" : "k_ffn_stream");
 }
 
 template <bool FUSED>
 void dispatch_ffn(const FfnTcArgs& a, cudaStream_t s) {
-  if (!FUSED && a.p_in_lo != nullptr) {  // split planes (fp32 policy)
+  if (!FUSED && a.planes) {  // split planes (fp32 policy)
     if (a.split_blocks) throw CudaError("ffn (planes): split partials are bf16-only");
     switch (ffn_wide_slice(a.rank_pad)) {
       case 64: launch_ffn<64, false, true, true>(a, s); return;

@@ -61,18 +61,24 @@ struct GemmCfg {
   static_assert(SMEM <= 227 * 1024, "shared-memory budget");
 };
 
-// X3 (fp32 policy): every operand is a pair of bf16 planes v = hi + lo
-// (split_planes), and the K loop runs three times over K -- A_hi B_hi,
-// A_hi B_lo, A_lo B_hi -- into the same fp32 accumulator (the lo*lo term is
-// below 2^-17 of the product).  tmA2 / tmB2 / tmC2 / resid2 address the lo
-// planes; the epilogue re-splits the fp32 result into the two output planes.
+// X3 (fp32 policy): every operand is three bf16 planes v = hi + mid + lo
+// (kernels.cuh), and the K loop runs six times over K -- the plane pairs
+// (hi,hi) (hi,mid) (mid,hi) (hi,lo) (lo,hi) (mid,mid) -- into the same fp32
+// accumulator.  A and B are loaded through ONE map each over the stacked
+// planes ([3M, K], [3N, K]; plane p at row offset p*M): rows a tile reads past
+// a plane's end only feed output rows / columns the store clips.  The
+// epilogue re-splits the fp32 result into three planes (tmC, tmC2, tmC3);
+// resid planes are resid_ps elements apart.
+__device__ __forceinline__ int x3_plane_a(int seg) { return (0x120100 >> (4 * seg)) & 15; }
+__device__ __forceinline__ int x3_plane_b(int seg) { return (0x102010 >> (4 * seg)) & 15; }
+
 template <int BN, int STAGES, bool X3 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const float* __restrict__ bias, int act,
                 int M, int N, int K, const bf16* resid, int64_t ldr,
-                const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
-                const __grid_constant__ CUtensorMap tmC2, const bf16* resid2) {
+                const __grid_constant__ CUtensorMap tmC2, const __grid_constant__ CUtensorMap tmC3,
+                int64_t resid_ps) {
   using Cfg = GemmCfg<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -90,16 +96,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int nk = (K + BK - 1) / BK;
-  const int nk3 = X3 ? 3 * nk : nk;  // K blocks of the (hi hi | hi lo | lo hi) sweep
+  const int nk3 = X3 ? 6 * nk : nk;  // K blocks of the six plane-pair sweeps
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     tma_prefetch(&tmC);
     if (X3) {
-      tma_prefetch(&tmA2);
-      tma_prefetch(&tmB2);
       tma_prefetch(&tmC2);
+      tma_prefetch(&tmC3);
     }
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -132,10 +137,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb3 = 0; kb3 < nk3; ++kb3, ++it) {
           if ((it & 1) == me) {
             const int seg = X3 ? kb3 / nk : 0, kb = kb3 - seg * nk;
+            const int ra = X3 ? x3_plane_a(seg) * M : 0, rb = X3 ? x3_plane_b(seg) * N : 0;
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
-            tma_load_2d(seg == 2 ? &tmA2 : &tmA, &full[stage], sA + stage * Cfg::A_BYTES, kb * BK, m0);
-            tma_load_2d(seg == 1 ? &tmB2 : &tmB, &full[stage], sB + stage * Cfg::B_BYTES, kb * BK, n0);
+            tma_load_2d(&tmA, &full[stage], sA + stage * Cfg::A_BYTES, kb * BK, m0 + ra);
+            tma_load_2d(&tmB, &full[stage], sB + stage * Cfg::B_BYTES, kb * BK, n0 + rb);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -212,9 +218,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        bias_act_chunk<32>(v, bias != nullptr ? bias + n0 + c0 : nullptr, N - (n0 + c0), act);
-        for (int pl = 0; pl < (X3 ? 2 : 1); ++pl) {  // C = A B^T + bias + R (R = R_hi + R_lo)
-          const bf16* rp = pl == 0 ? resid : resid2;
+        if (X3)
+          bias_act_chunk_exact<32>(v, bias != nullptr ? bias + n0 + c0 : nullptr, N - (n0 + c0), act);
+        else
+          bias_act_chunk<32>(v, bias != nullptr ? bias + n0 + c0 : nullptr, N - (n0 + c0), act);
+        for (int pl = 0; pl < (X3 ? kPlanes : 1); ++pl) {  // C = A B^T + bias + R (R = sum of planes)
+          const bf16* rp = resid == nullptr ? nullptr : resid + pl * resid_ps;
           if (rp == nullptr || m0 + static_cast<int>(row) >= M) continue;
           const uint4* rr = reinterpret_cast<const uint4*>(rp + (int64_t)(m0 + row) * ldr + n0 + c0);
 #pragma unroll
@@ -230,8 +239,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
 #pragma unroll 1
-        for (int pl = 0; pl < (X3 ? 2 : 1); ++pl) {
-          if (X3 && pl == 1) {  // lo plane: what the hi plane's bf16 rounding left
+        for (int pl = 0; pl < (X3 ? kPlanes : 1); ++pl) {
+          if (X3 && pl > 0) {  // next plane: what the previous planes' rounding left
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] -= bf16_round_f(v[j]);
           }
@@ -252,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           named_bar_sync(1, kEpiWarps * 32);
           if (et == 0) {
-            tma_store_2d_u32(pl == 0 ? &tmC : &tmC2, box, n0 + b0, m0);
+            tma_store_2d_u32(pl == 0 ? &tmC : pl == 1 ? &tmC2 : &tmC3, box, n0 + b0, m0);
             tma_store_commit();
           }
           ++nbox;
@@ -470,8 +479,8 @@ void launch_gemm2(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* 
 template <int BN, int STAGES, bool X3 = false>
 void launch_gemm(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, int64_t ldc,
                  int M, int N, int K, const float* bias, int act, cudaStream_t s,
-                 const bf16* resid = nullptr, int64_t ldr = 0, const bf16* A2 = nullptr,
-                 const bf16* B2 = nullptr, bf16* C2 = nullptr, const bf16* resid2 = nullptr) {
+                 const bf16* resid = nullptr, int64_t ldr = 0, bf16* C2 = nullptr,
+                 bf16* C3 = nullptr, int64_t resid_ps = 0) {
   using Cfg = GemmCfg<BN, STAGES>;
   static bool attr = false;
   if (!attr) {
@@ -479,16 +488,16 @@ void launch_gemm(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     attr = true;
   }
-  const CUtensorMap ta = tmap_bf16(A, M, K, lda, BM, BK, TmaSwizzle::B128);
-  const CUtensorMap tb = tmap_bf16(B, N, K, ldb, BN, BK, TmaSwizzle::B128);
+  const int np = X3 ? kPlanes : 1;  // stacked planes behind A and B
+  const CUtensorMap ta = tmap_bf16(A, (uint64_t)np * M, K, lda, BM, BK, TmaSwizzle::B128);
+  const CUtensorMap tb = tmap_bf16(B, (uint64_t)np * N, K, ldb, BN, BK, TmaSwizzle::B128);
   const CUtensorMap tc = tmap_bf16(C, M, N, ldc, BM, 64, TmaSwizzle::B128);
-  const CUtensorMap ta2 = X3 ? tmap_bf16(A2, M, K, lda, BM, BK, TmaSwizzle::B128) : ta;
-  const CUtensorMap tb2 = X3 ? tmap_bf16(B2, N, K, ldb, BN, BK, TmaSwizzle::B128) : tb;
   const CUtensorMap tc2 = X3 ? tmap_bf16(C2, M, N, ldc, BM, 64, TmaSwizzle::B128) : tc;
+  const CUtensorMap tc3 = X3 ? tmap_bf16(C3, M, N, ldc, BM, 64, TmaSwizzle::B128) : tc;
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   launch_pdl(k_gemm_bf16<BN, STAGES, X3>, dim3(grid), dim3(kThreads), Cfg::SMEM, s, ta, tb, tc,
-             bias, act, M, N, K, resid, ldr, ta2, tb2, tc2, resid2);
+             bias, act, M, N, K, resid, ldr, tc2, tc3, resid_ps);
   check_launch("k_gemm_bf16");
 }
 
@@ -543,17 +552,23 @@ void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, 
 void gemm_x3(const Planes& A, int64_t lda, const Planes& B, int64_t ldb, const PlanesOut& C,
              int64_t ldc, int M, int N, int K, const float* bias, int act, cudaStream_t s,
              const Planes* resid, int64_t ldr) {
-  const bf16* r1 = resid ? resid->hi : nullptr;
-  const bf16* r2 = resid ? resid->lo : nullptr;
+  // the loads address A and B as stacked planes (one tensor map each)
+  const int64_t pa = (int64_t)M * lda, pb = (int64_t)N * ldb;
+  if (A.mid != A.hi + pa || A.lo != A.mid + pa || B.mid != B.hi + pb || B.lo != B.mid + pb)
+    throw CudaError("gemm_x3: the planes of A and B must be stacked contiguously");
+  const bf16* r = resid ? resid->hi : nullptr;
+  const int64_t rps = resid ? resid->mid - resid->hi : 0;
+  if (resid && resid->lo - resid->mid != rps)
+    throw CudaError("gemm_x3: residual planes must be evenly spaced");
   if (M <= 128 && N % 64 == 0 && N >= 128)
-    launch_gemm<64, 8, true>(A.hi, lda, B.hi, ldb, C.hi, ldc, M, N, K, bias, act, s, r1, ldr, A.lo,
-                             B.lo, C.lo, r2);
+    launch_gemm<64, 8, true>(A.hi, lda, B.hi, ldb, C.hi, ldc, M, N, K, bias, act, s, r, ldr, C.mid,
+                             C.lo, rps);
   else if (N % 128 == 0 || N > 64)
-    launch_gemm<128, 6, true>(A.hi, lda, B.hi, ldb, C.hi, ldc, M, N, K, bias, act, s, r1, ldr,
-                              A.lo, B.lo, C.lo, r2);
+    launch_gemm<128, 6, true>(A.hi, lda, B.hi, ldb, C.hi, ldc, M, N, K, bias, act, s, r, ldr,
+                              C.mid, C.lo, rps);
   else
-    launch_gemm<64, 8, true>(A.hi, lda, B.hi, ldb, C.hi, ldc, M, N, K, bias, act, s, r1, ldr, A.lo,
-                             B.lo, C.lo, r2);
+    launch_gemm<64, 8, true>(A.hi, lda, B.hi, ldb, C.hi, ldc, M, N, K, bias, act, s, r, ldr, C.mid,
+                             C.lo, rps);
 }
 
 }  // namespace fsvd

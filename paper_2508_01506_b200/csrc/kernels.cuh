@@ -30,25 +30,32 @@ void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, 
 bool gemm_bf16_supported(int M, int N, int K, int64_t lda, int64_t ldb, int64_t ldc);
 
 // ---- split planes (fp32 policy on the tensor cores) ---------------------------
-// An fp32 matrix v is held as two bf16 matrices of the same shape, hi = bf16(v)
-// and lo = bf16(v - hi) (|v - hi - lo| <= 2^-17 |v|).  Products run as three
-// bf16 MMA passes into one fp32 accumulator: A_hi B_hi + A_hi B_lo + A_lo B_hi.
+// An fp32 matrix v is held as three bf16 matrices of the same shape, stored
+// one after the other: hi = bf16(v), mid = bf16(v - hi), lo = bf16(v - hi -
+// mid) (|v - hi - mid - lo| <= 2^-24 |v|, fp32 resolution).  A product runs
+// as six bf16 MMA passes into one fp32 accumulator -- every plane pair of
+// order <= 2: hi*hi, hi*mid, mid*hi, hi*lo, lo*hi, mid*mid -- leaving out
+// terms below 2^-23 of the product.  A [rows, cols] matrix occupies
+// 6*rows*cols bytes; plane stride = rows * leading dimension.
 struct Planes {
   const bf16* hi;
+  const bf16* mid;
   const bf16* lo;
 };
 struct PlanesOut {
   bf16* hi;
+  bf16* mid;
   bf16* lo;
 };
+constexpr int kPlanes = 3;
 // K1 in the split-plane form: C = A B^T (+ bias) (act) (+ resid), every
-// matrix as planes with the same leading dimension in both planes.
+// matrix as planes with the same leading dimension in every plane.
 void gemm_x3(const Planes& A, int64_t lda, const Planes& B, int64_t ldb, const PlanesOut& C,
              int64_t ldc, int M, int N, int K, const float* bias, int act, cudaStream_t s,
              const Planes* resid = nullptr, int64_t ldr = 0);
 // fp32 <-> planes at the API boundary; row kernels between the GEMMs (planes.cu)
-void split_planes(const float* src, bf16* hi, bf16* lo, int64_t n, cudaStream_t s);
-void merge_planes(const bf16* hi, const bf16* lo, float* dst, int64_t n, cudaStream_t s);
+void split_planes(const float* src, const PlanesOut& y, int64_t n, cudaStream_t s);
+void merge_planes(const Planes& a, float* dst, int64_t n, cudaStream_t s);
 // y = LN(a (+ b)) * gamma + beta, rows of width d; in place allowed for d <= 2048
 void ln_planes(const Planes& a, const Planes* b, const float* gamma, const float* beta, float eps,
                const PlanesOut& y, int rows, int d, cudaStream_t s, int pitch = 0);
@@ -84,10 +91,11 @@ struct AttnTcArgs {
   bf16* out;
   int64_t ldo;
   bool causal = false;  // decoder prefill: key j visible to query i iff j <= i
-  // split planes (fp32 policy): lo planes of qkv and out, same layout; when
-  // set the kernel runs its X3 form (three bf16 passes per product)
-  const bf16* qkv_lo = nullptr;
-  bf16* out_lo = nullptr;
+  // split planes (fp32 policy): qkv and out each hold three planes (qkv plane
+  // stride batch*seq*ldq, out plane stride out_ps elements); the kernel runs
+  // its X3 form (six bf16 passes per product)
+  bool planes = false;
+  int64_t out_ps = 0;
 };
 void attn_rankspace_bf16(const AttnTcArgs& a, cudaStream_t s);
 
@@ -143,12 +151,10 @@ struct FfnTcArgs {
   // x, and the un-normalised ln_resid + ffn(x) is also stored to sum_out
   const bf16* ln_resid = nullptr;
   bf16* sum_out = nullptr;
-  // V1 stream in split planes (fp32 policy): the lo planes of P, V_up^T,
-  // U_down^T and Z; when p_in_lo is set K3 runs its X3 form
-  const bf16* p_in_lo = nullptr;
-  const bf16* up_v_t_lo = nullptr;
-  const bf16* dn_u_t_lo = nullptr;
-  bf16* z_out_lo = nullptr;
+  // V1 stream in split planes (fp32 policy): P, V_up^T, U_down^T and Z each
+  // hold three stacked planes (plane stride = rows x leading dimension); K3
+  // runs its X3 form
+  bool planes = false;
 };
 void ffn_stream_bf16(const FfnTcArgs& a, cudaStream_t s);   // V1 middle: P -> Z
 void z_partial_sum_bf16(const float* part, int splits, int64_t n, bf16* z, cudaStream_t s);

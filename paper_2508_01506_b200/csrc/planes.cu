@@ -1,12 +1,12 @@
 // planes.cu -- split-plane elementwise kernels of the fp32 policy.
 //
 // The fp32 policy runs the same tcgen05 kernels as bf16 (K1 / K2 / K3 with
-// their X3 template flag): every fp32 activation lives in HBM as two bf16
-// planes, hi = bf16(v) and lo = bf16(v - hi), so an MMA operand is exact to
-// 2^-17 of v and each product takes three bf16 passes (A_hi B_hi + A_hi B_lo
-// + A_lo B_hi) into an fp32 accumulator.  A [T, N] activation occupies
-// 4*T*N bytes (hi plane, then lo plane) -- the bytes of its fp32 form, so the
-// workspace planner's fp32 sizes hold unchanged.
+// their X3 template flag): every fp32 activation lives in HBM as three bf16
+// planes (kernels.cuh: hi, mid, lo; v = hi + mid + lo to fp32 resolution), so
+// an MMA operand carries v's full 24-bit significand and each product takes
+// six bf16 passes into an fp32 accumulator.  A [T, N] activation occupies
+// 6*T*N bytes (hi plane, mid plane, lo plane); fp32 packs on the tensor cores
+// have es = 6 for the workspace planner.
 //
 // This file holds the conversions at the API boundary (fp32 <-> planes) and
 // the row kernels between the GEMMs: residual + LayerNorm (encoder.cpp:38-50,
@@ -18,30 +18,33 @@
 namespace fsvd {
 namespace {
 
-__device__ __forceinline__ void split1(float v, bf16& hi, bf16& lo) {
+__device__ __forceinline__ void split1(float v, bf16& hi, bf16& mid, bf16& lo) {
   hi = __float2bfloat16_rn(v);
-  lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+  const float r = v - __bfloat162float(hi);
+  mid = __float2bfloat16_rn(r);
+  lo = __float2bfloat16_rn(r - __bfloat162float(mid));
 }
-__device__ __forceinline__ float join1(const bf16* hi, const bf16* lo, int64_t i) {
-  return __bfloat162float(hi[i]) + __bfloat162float(lo[i]);
+__device__ __forceinline__ void split1(float v, const PlanesOut& y, int64_t i) {
+  split1(v, y.hi[i], y.mid[i], y.lo[i]);
+}
+__device__ __forceinline__ float join1(const Planes& a, int64_t i) {
+  return (__bfloat162float(a.hi[i]) + __bfloat162float(a.mid[i])) + __bfloat162float(a.lo[i]);
 }
 
-__global__ void k_split_planes(const float* __restrict__ src, bf16* __restrict__ hi,
-                               bf16* __restrict__ lo, int64_t n) {
+__global__ void k_split_planes(const float* __restrict__ src, PlanesOut y, int64_t n) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    split1(src[i], hi[i], lo[i]);
+    split1(src[i], y, i);
 }
 
-__global__ void k_merge_planes(const bf16* __restrict__ hi, const bf16* __restrict__ lo,
-                               float* __restrict__ dst, int64_t n) {
+__global__ void k_merge_planes(Planes a, float* __restrict__ dst, int64_t n) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = join1(hi, lo, i);
+    dst[i] = join1(a, i);
 }
 
 // y = gamma * ((a + b) - mean) / sqrt(var + eps) + beta per row, fp32, biased
@@ -67,8 +70,8 @@ __global__ void __launch_bounds__(256)
     const int c = lane + 32 * i;
     v[i] = 0.0f;
     if (c < pitch) {
-      v[i] = join1(a.hi, a.lo, base + c);
-      if (b.hi) v[i] += join1(b.hi, b.lo, base + c);
+      v[i] = join1(a, base + c);
+      if (b.hi) v[i] += join1(b, base + c);
       if (c < d) s += v[i];
     }
   }
@@ -91,7 +94,7 @@ __global__ void __launch_bounds__(256)
   for (int i = 0; i < VPL; ++i) {
     const int c = lane + 32 * i;
     if (c < pitch)
-      split1(gamma[c] * ((v[i] - mean) * inv) + beta[c], y.hi[base + c], y.lo[base + c]);
+      split1(gamma[c] * ((v[i] - mean) * inv) + beta[c], y, base + c);
   }
 }
 
@@ -107,8 +110,8 @@ __global__ void __launch_bounds__(256)
   if (warp >= rows) return;
   const int64_t base = (int64_t)warp * pitch;
   auto val = [&](int c) {
-    float t = join1(a.hi, a.lo, base + c);
-    if (b.hi) t += join1(b.hi, b.lo, base + c);
+    float t = join1(a, base + c);
+    if (b.hi) t += join1(b, base + c);
     return t;
   };
   float s = 0.0f;
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__(256)
   const float inv = 1.0f / sqrtf(q / static_cast<float>(d) + eps);
   // in place is not allowed here (a later value of the row is re-read)
   for (int c = lane; c < pitch; c += 32)
-    split1(gamma[c] * ((val(c) - mean) * inv) + beta[c], y.hi[base + c], y.lo[base + c]);
+    split1(gamma[c] * ((val(c) - mean) * inv) + beta[c], y, base + c);
 }
 
 __global__ void k_add_planes(Planes a, Planes b, PlanesOut y, int64_t n) {
@@ -132,7 +135,7 @@ __global__ void k_add_planes(Planes a, Planes b, PlanesOut y, int64_t n) {
   ptx::pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    split1(join1(a.hi, a.lo, i) + join1(b.hi, b.lo, i), y.hi[i], y.lo[i]);
+    split1(join1(a, i) + join1(b, i), y, i);
 }
 
 // Host fp32 rows [rows, d] <-> device activations [rows, pitch] in the
@@ -151,7 +154,7 @@ __global__ void k_rows_in(const float* __restrict__ src, int rows, int d, int pi
       static_cast<bf16*>(dst)[i] = __float2bfloat16_rn(v);
     } else {
       bf16* h = static_cast<bf16*>(dst);
-      split1(v, h[i], h[n + i]);
+      split1(v, h[i], h[n + i], h[2 * n + i]);
     }
   }
 }
@@ -164,7 +167,10 @@ __global__ void k_rows_out(const void* __restrict__ src, int rows, int d, int pi
     const int64_t j = r * pitch + (i - r * d);
     if (form == 1) dst[i] = static_cast<const float*>(src)[j];
     else if (form == 0) dst[i] = __bfloat162float(static_cast<const bf16*>(src)[j]);
-    else dst[i] = join1(static_cast<const bf16*>(src), static_cast<const bf16*>(src) + np, j);
+    else {
+      const bf16* h = static_cast<const bf16*>(src);
+      dst[i] = join1(Planes{h, h + np, h + 2 * np}, j);
+    }
   }
 }
 
@@ -190,21 +196,21 @@ void rows_from_device(const void* src, int rows, int d, int pitch, int form, flo
   check_launch("k_rows_out");
 }
 
-void split_planes(const float* src, bf16* hi, bf16* lo, int64_t n, cudaStream_t s) {
+void split_planes(const float* src, const PlanesOut& y, int64_t n, cudaStream_t s) {
   if (n == 0) return;
-  launch_pdl(k_split_planes, dim3(ew_grid(n)), dim3(256), 0, s, src, hi, lo, n);
+  launch_pdl(k_split_planes, dim3(ew_grid(n)), dim3(256), 0, s, src, y, n);
   check_launch("k_split_planes");
 }
 
-void merge_planes(const bf16* hi, const bf16* lo, float* dst, int64_t n, cudaStream_t s) {
+void merge_planes(const Planes& a, float* dst, int64_t n, cudaStream_t s) {
   if (n == 0) return;
-  launch_pdl(k_merge_planes, dim3(ew_grid(n)), dim3(256), 0, s, hi, lo, dst, n);
+  launch_pdl(k_merge_planes, dim3(ew_grid(n)), dim3(256), 0, s, a, dst, n);
   check_launch("k_merge_planes");
 }
 
 void ln_planes(const Planes& a, const Planes* b, const float* gamma, const float* beta, float eps,
                const PlanesOut& y, int rows, int d, cudaStream_t s, int pitch) {
-  const Planes bb = b ? *b : Planes{nullptr, nullptr};
+  const Planes bb = b ? *b : Planes{nullptr, nullptr, nullptr};
   const dim3 grid((rows + 7) / 8);
   if (pitch <= 0) pitch = d;
   if (pitch <= 32 * 32) {

@@ -550,6 +550,22 @@ __device__ __forceinline__ void act_chunk(float (&v)[N], int act) {
       break;
   }
 }
+// fp32 policy (split planes): the activations at full precision (erff /
+// tanhf, tensor.cpp:64-74) -- the MUFU forms above are bf16-grade.
+template <int N>
+__device__ __forceinline__ void bias_act_chunk2_exact(float (&v)[N], const float (&b)[N], int act) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) v[j] = apply_act(v[j] + b[j], act);
+}
+template <int N>
+__device__ __forceinline__ void bias_act_chunk_exact(float (&v)[N], const float* bias, int valid,
+                                                     int act) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    if (bias != nullptr && j < valid) v[j] += __ldg(bias + j);
+    v[j] = apply_act(v[j], act);
+  }
+}
 // Loads bias[0..N) into registers (float4 when all N columns are in range).
 template <int N>
 __device__ __forceinline__ void load_bias(float (&b)[N], const float* bias, int valid) {

@@ -64,18 +64,28 @@ struct Builder {
     }
     fix.push_back({dst, off});
   }
-  // split planes (fp32 policy): hi = bf16(v), lo = bf16(v - hi)
-  void store_planes(const void** hi, const void** lo, const std::vector<float>& v) {
-    std::vector<uint16_t> h(v.size()), l(v.size());
-    for (size_t i = 0; i < v.size(); ++i) {
-      h[i] = f32_to_bf16_bits(v[i]);
-      uint32_t u = static_cast<uint32_t>(h[i]) << 16;
-      float hf;
-      std::memcpy(&hf, &u, 4);
-      l[i] = f32_to_bf16_bits(v[i] - hf);
+  // split planes (fp32 policy, kernels.cuh): hi = bf16(v), mid = bf16(v - hi),
+  // lo = bf16(v - hi - mid), stored contiguously; *hi -> the hi plane,
+  // *mid -> the mid plane (the plane stride is mid - hi)
+  void store_planes(const void** hi, const void** mid, const std::vector<float>& v) {
+    const size_t n = v.size();
+    std::vector<uint16_t> h(3 * n);
+    auto widen = [](uint16_t b) {
+      uint32_t u = static_cast<uint32_t>(b) << 16;
+      float f;
+      std::memcpy(&f, &u, 4);
+      return f;
+    };
+    for (size_t i = 0; i < n; ++i) {
+      float r = v[i];
+      for (int pl = 0; pl < 3; ++pl) {
+        h[pl * n + i] = f32_to_bf16_bits(r);
+        r -= widen(h[pl * n + i]);
+      }
     }
-    fix.push_back({hi, raw(h.data(), h.size() * 2)});
-    fix.push_back({lo, raw(l.data(), l.size() * 2)});
+    const size_t off = raw(h.data(), h.size() * 2);
+    fix.push_back({hi, off});
+    fix.push_back({mid, off + n * 2});
   }
   // tensor-core weight layout: bf16 (bf16 policy) or split planes (x3)
   bool x3 = false;
@@ -213,7 +223,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
   auto P = std::make_unique<Pack>();
   Pack& p = *P;
   p.dtype = dtype;
-  p.es = dtype == FSVD_BF16 ? 2 : 4;
+  p.es = dtype == FSVD_BF16 ? 2 : 4;  // split-plane packs: 6 (set below)
   Builder b;
   b.es = p.es;
   const bool bf = dtype == FSVD_BF16;
@@ -252,6 +262,7 @@ Pack* build_pack(const PackRequest& q, fsvd_dtype dtype) {
   p.dr = d;
   p.x3 = !bf && all_ok;
   b.x3 = p.x3;
+  if (p.x3) p.es = 2 * kPlanes;  // three bf16 planes per stored value
 
   if (q.attn) {
     const fsvd_attn_desc& a = *q.attn;
@@ -610,16 +621,22 @@ const T* as(const void* p) {
 }
 
 // split planes of a [rows, cols] activation buffer: hi plane, then lo plane
+// split planes of a [rows, cols] activation buffer (n = rows x pitch): hi,
+// mid, lo planes one after another
 Planes pl(const void* p, size_t n) {
   const bf16* h = static_cast<const bf16*>(p);
-  return {h, h + n};
+  return {h, h + n, h + 2 * n};
 }
 PlanesOut plo(void* p, size_t n) {
   bf16* h = static_cast<bf16*>(p);
-  return {h, h + n};
+  return {h, h + n, h + 2 * n};
 }
-Planes wpl(const void* hi, const void* lo) {
-  return {static_cast<const bf16*>(hi), static_cast<const bf16*>(lo)};
+// a weight's planes: stored contiguously (Builder::store_planes), `mid` its
+// second plane, so the plane stride is mid - hi
+Planes wpl(const void* hi, const void* mid) {
+  const bf16* h = static_cast<const bf16*>(hi);
+  const bf16* m = static_cast<const bf16*>(mid);
+  return {h, m, m + (m - h)};
 }
 
 void ln(const Pack& p, const void* a, const void* b, const float* g, const float* be, float eps,
@@ -627,7 +644,7 @@ void ln(const Pack& p, const void* a, const void* b, const float* g, const float
   // statistics over the callers' d (p.dr); rows stored with the layout pitch p.d
   if (p.x3) {
     const size_t n = static_cast<size_t>(rows) * p.d;
-    const Planes bp = b ? pl(b, n) : Planes{nullptr, nullptr};
+    const Planes bp = b ? pl(b, n) : Planes{nullptr, nullptr, nullptr};
     ln_planes(pl(a, n), b ? &bp : nullptr, g, be, eps, plo(y, n), rows, p.dr, s, p.d);
     return;
   }
@@ -725,11 +742,11 @@ void x3_attention_rank(const Pack& p, size_t B, size_t M, const void* x, bf16* o
   const int T = static_cast<int>(B * M), n = p.qkv_cols, hr = p.H * p.rp;
   const size_t tn = static_cast<size_t>(T) * n;
   bf16* qkv = as<bf16>(trans);
-  gemm_x3(pl(x, (size_t)T * p.d), p.d, wpl(p.wproj_t, p.wproj_lo), p.d, PlanesOut{qkv, qkv + tn},
-          n, T, n, p.d, p.bproj, ACT_NONE, s);
+  gemm_x3(pl(x, (size_t)T * p.d), p.d, wpl(p.wproj_t, p.wproj_lo), p.d, plo(qkv, tn), n, T, n,
+          p.d, p.bproj, ACT_NONE, s);
   AttnTcArgs a;
   a.qkv = qkv;
-  a.qkv_lo = qkv + tn;
+  a.planes = true;
   a.ldq = n;
   a.qkv_cols = n;
   a.q_off = 0;
@@ -741,7 +758,7 @@ void x3_attention_rank(const Pack& p, size_t B, size_t M, const void* x, bf16* o
   a.groups = p.G;
   a.rank_pad = p.rp;
   a.out = o_rank;
-  a.out_lo = o_rank + (size_t)T * hr;
+  a.out_ps = (int64_t)T * hr;
   a.ldo = hr;
   attn_rankspace_bf16(a, s);
 }
@@ -772,7 +789,7 @@ bf16* tc_attention_dense(const Pack& p, int mode, size_t B, size_t M, const void
   if (mode == FSVD_MODE_NAIVE_LOWRANK && !p.wpn_t)
     fail(Kind::Config, "naive_lowrank mode on the tensor cores needs a head width of 16, 32 or 64");
   const int T = static_cast<int>(B * M), d = p.d, hp = p.H * p.dhp, n3 = 3 * hp;
-  const size_t ew = p.x3 ? 2 : 1;  // bf16 elements per stored value
+  const size_t ew = p.x3 ? kPlanes : 1;  // bf16 elements per stored value
   bf16* qkv = as<bf16>(trans);
   bf16* o = qkv + ew * (size_t)T * n3;
   if (mode == FSVD_MODE_DENSE) {
@@ -799,8 +816,8 @@ bf16* tc_attention_dense(const Pack& p, int mode, size_t B, size_t M, const void
   a.out = o;
   a.ldo = hp;
   if (p.x3) {
-    a.qkv_lo = qkv + (size_t)T * n3;
-    a.out_lo = o + (size_t)T * hp;
+    a.planes = true;
+    a.out_ps = (int64_t)T * hp;
   }
   attn_rankspace_bf16(a, s);
   return o;
@@ -821,9 +838,9 @@ void attention_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, v
     gemm_bf16(o_rank, hr, as<bf16>(p.wvc_t), hr, as<bf16>(ctx), p.d, T, p.d, hr, p.bv, ACT_NONE, s);
   } else if (p.x3) {
     const int hr = p.H * p.rp;
-    bf16* o_rank = as<bf16>(trans) + 2 * (size_t)T * p.qkv_cols;
+    bf16* o_rank = as<bf16>(trans) + kPlanes * (size_t)T * p.qkv_cols;
     x3_attention_rank(p, B, M, x, o_rank, trans, s);
-    gemm_x3(Planes{o_rank, o_rank + (size_t)T * hr}, hr, wpl(p.wvc_t, p.wvc_lo), hr,
+    gemm_x3(pl(o_rank, (size_t)T * hr), hr, wpl(p.wvc_t, p.wvc_lo), hr,
             plo(ctx, (size_t)T * p.d), p.d, T, p.d, hr, p.bv, ACT_NONE, s);
   } else if (p.dtype == FSVD_BF16) {
     simt_attention_t<bf16>(p, B, M, x, ctx, trans, s);
@@ -844,9 +861,9 @@ void outproj_fwd(const Pack& p, int mode, size_t B, size_t M, const void* ctx, v
   } else if (p.x3) {
     bf16* P = as<bf16>(trans);
     const size_t tp = (size_t)T * p.prp;
-    gemm_x3(pl(ctx, (size_t)T * d), d, wpl(p.uo_t, p.uo_t_lo), d, PlanesOut{P, P + tp}, p.prp, T,
+    gemm_x3(pl(ctx, (size_t)T * d), d, wpl(p.uo_t, p.uo_t_lo), d, plo(P, tp), p.prp, T,
             p.prp, d, nullptr, ACT_NONE, s);
-    gemm_x3(Planes{P, P + tp}, p.prp, wpl(p.vo_t, p.vo_t_lo), p.prp, plo(out, (size_t)T * d), d, T,
+    gemm_x3(pl(P, tp), p.prp, wpl(p.vo_t, p.vo_t_lo), p.prp, plo(out, (size_t)T * d), d, T,
             d, p.prp, p.bo, ACT_NONE, s);
   } else if (p.dtype == FSVD_BF16) {
     simt_gemm<bf16>(as<bf16>(ctx), d, as<bf16>(p.uo), p.pr, as<bf16>(trans), p.pr, T, p.pr, d,
@@ -879,9 +896,9 @@ void attention_block(const Pack& p, int mode, size_t B, size_t M, const void* x,
   }
   if (flash && p.x3) {  // split planes: O after the projection planes in `trans`
     const int T = static_cast<int>(B * M), hr = p.H * p.rp;
-    bf16* o = as<bf16>(trans) + 2 * (size_t)T * p.qkv_cols;
+    bf16* o = as<bf16>(trans) + kPlanes * (size_t)T * p.qkv_cols;
     x3_attention_rank(p, B, M, x, o, trans, s);
-    gemm_x3(Planes{o, o + (size_t)T * hr}, hr, wpl(p.wov_t, p.wov_lo), hr,
+    gemm_x3(pl(o, (size_t)T * hr), hr, wpl(p.wov_t, p.wov_lo), hr,
             plo(branch, (size_t)T * p.d), p.d, T, p.d, hr, p.bov, ACT_NONE, s);
     return;
   }
@@ -941,7 +958,7 @@ void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* o
   const int T = static_cast<int>(B * M), d = p.d, df = p.df;
   if (mode == FSVD_MODE_DENSE || mode == FSVD_MODE_NAIVE_LOWRANK) {
     if (!p.dense) fail(Kind::Config, "dense / naive_lowrank modes need a pack built with dense=1");
-    const size_t ew = p.x3 ? 2 : 1;
+    const size_t ew = p.x3 ? kPlanes : 1;
     if (mode == FSVD_MODE_DENSE) {  // ffn_dense (ffn.cpp:187-218) on the layer's dense weights
       const int ddf = p.ddf;
       bf16* hid = as<bf16>(trans);
@@ -963,8 +980,8 @@ void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* o
   if (p.x3) {  // split planes: V1 chain for both FFN variants (ffn_v1 == ffn_v2)
     bf16* P = as<bf16>(trans);
     const size_t tf = (size_t)T * p.frp;
-    bf16* Z = P + 2 * tf;
-    gemm_x3(pl(x, (size_t)T * d), d, wpl(p.uup_t, p.uup_t_lo), d, PlanesOut{P, P + tf}, p.frp, T,
+    bf16* Z = P + kPlanes * tf;
+    gemm_x3(pl(x, (size_t)T * d), d, wpl(p.uup_t, p.uup_t_lo), d, plo(P, tf), p.frp, T,
             p.frp, d, nullptr, ACT_NONE, s);
     FfnTcArgs a{};
     a.T = T;
@@ -972,19 +989,16 @@ void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* o
     a.d_ff = df;
     a.rank_pad = p.frp;
     a.up_v_t = as<bf16>(p.vup_t);
-    a.up_v_t_lo = as<bf16>(p.vup_t_lo);
     a.up_b = p.bup;
     a.dn_u_t = as<bf16>(p.udn_t);
-    a.dn_u_t_lo = as<bf16>(p.udn_t_lo);
     a.dn_v_t = as<bf16>(p.vdn_t);
     a.dn_b = p.bdn;
     a.act = p.act;
     a.p_in = P;
-    a.p_in_lo = P + tf;
+    a.planes = true;
     a.z_out = Z;
-    a.z_out_lo = Z + tf;
     ffn_stream_bf16(a, s);
-    gemm_x3(Planes{Z, Z + tf}, p.frp, wpl(p.vdn_t, p.vdn_t_lo), p.frp, plo(out, (size_t)T * d), d,
+    gemm_x3(pl(Z, tf), p.frp, wpl(p.vdn_t, p.vdn_t_lo), p.frp, plo(out, (size_t)T * d), d,
             T, d, p.frp, p.bdn, ACT_NONE, s);
     return;
   }
