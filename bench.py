@@ -657,7 +657,12 @@ def roofline(args, L, packs, work, wsb, stream, dev, peaks, peak_src, ms_max, gb
     ffn_variant = 2 if mode == abi.MODE_FLASH_V2 else 1
     resid = torch.randn((B, M, D), device=dev, dtype=torch.float32).to(torch.bfloat16)
     ffn_out = torch.empty_like(resid)
-    ffn_ws = C.c_size_t(wsb.value)
+    # the sublayer entry points run the unfused schedules, whose transients
+    # exceed the compact layer workspace: a scratch of their own (allocated
+    # after the peak-memory measurement)
+    work = torch.empty(max(wsb.value, T * (3 * H + 2 * G) * R * 2 * 2, T * 2 * FR * 2 * 2),
+                       dtype=torch.uint8, device=dev)
+    ffn_ws = C.c_size_t(work.numel())
     reps = 20
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sub = {}

@@ -164,7 +164,8 @@ __device__ __forceinline__ Item item_of(int w, int nqt, int heads, int batch, in
 // current item finishes, and TMEM / barriers are set up once per CTA.
 template <int RP, bool X3 = false>
 __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
-    k_attn_rankspace(const __grid_constant__ CUtensorMap tmQKV, bf16* __restrict__ out,
+    k_attn_rankspace(const __grid_constant__ CUtensorMap tmQKV,
+                     const __grid_constant__ CUtensorMap tmKV, bf16* out,
                      int64_t ldo, int batch, int seq, int heads, int groups, int q_off, int k_off,
                      int v_off, int causal, int plane_rows, int64_t out_ps) {
   using C = AttnCfg<RP, X3>;
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
 
   if (warp == kTma && lane == 0) {
     tma_prefetch(&tmQKV);
+    tma_prefetch(&tmKV);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->q_full[i], 1);
       mbar_init(&bars->q_empty[i], 1);
@@ -228,9 +230,9 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
           uint8_t* kv = smem + C::o_kv + st * C::KV_STAGE;
           mbar_arrive_expect_tx(&bars->kv_full[st], 2 * C::NPL * C::TILE);
           for (int pl = 0; pl < C::NPL; ++pl) {
-            tma_load_2d(&tmQKV, &bars->kv_full[st], kv + pl * up1k(C::TILE), k_off + g * RP,
+            tma_load_2d(&tmKV, &bars->kv_full[st], kv + pl * up1k(C::TILE), k_off + g * RP,
                         row0 + j * KT + pl * plane_rows);
-            tma_load_2d(&tmQKV, &bars->kv_full[st], kv + C::kv_v + pl * up1k(C::TILE),
+            tma_load_2d(&tmKV, &bars->kv_full[st], kv + C::kv_v + pl * up1k(C::TILE),
                         v_off + g * RP, row0 + j * KT + pl * plane_rows);
           }
           if (++st == C::STAGES) { st = 0; ph ^= 1; }
@@ -281,8 +283,11 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
       const int qs = it & 1;
       const int nji = causal ? min(nj, item_of(w, nqt, heads, batch, causal).qt + 1) : nj;
       if (lane == 0 && it < 100) ATRACE(400 + it);
-      for (int j = 0; j < nji; ++j) {
-        const int t = gt + j;
+      // the next S (this item's next tile, or the next item's first): issued
+      // ahead of this tile's PV when the K/V ring has a second stage; with a
+      // single stage its K/V can only arrive once this PV has released the
+      // stage, so it follows the PV
+      auto next_s = [&](int j, int t) {
         if (j + 1 < nji) {
           issue_s(t + 1, qs);
         } else {
@@ -293,6 +298,10 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
             issue_s(t + 1, qs ^ 1);
           }
         }
+      };
+      for (int j = 0; j < nji; ++j) {
+        const int t = gt + j;
+        if (C::STAGES > 1) next_s(j, t);
         mbar_wait(&bars->p_full, t & 1);
         // this item's O buffer must have been read out by the softmax warps
         if (j == 0 && it >= C::NOB) mbar_wait(&bars->o_free[it % C::NOB], ((it / C::NOB) - 1) & 1);
@@ -320,6 +329,7 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
           mma_commit(&bars->kv_empty[st]);
         }
         __syncwarp();
+        if (C::STAGES == 1) next_s(j, t);
       }
       gt += nji;
     }
@@ -526,9 +536,13 @@ void launch_attn(const AttnTcArgs& a, cudaStream_t s) {
   // X3: the three planes of qkv stacked ([3T, qkv_cols], plane p at row p*T)
   const CUtensorMap tm = tmap_bf16(a.qkv, (uint64_t)C::NPL * T, a.qkv_cols, a.ldq, 128, RP,
                                    swizzle_for_row_bytes(C::RB));
+  // K / V from a separate region (k_off / v_off relative to it) when given
+  const CUtensorMap tkv = a.kv == nullptr ? tm
+                                          : tmap_bf16(a.kv, (uint64_t)C::NPL * T, a.kv_cols, a.ldkv,
+                                                      128, RP, swizzle_for_row_bytes(C::RB));
   const int items = ((a.seq + QT - 1) / QT) * a.heads * a.batch;
   const int grid = items < C::CTAS * num_sms() ? items : C::CTAS * num_sms();
-  launch_pdl(k_attn_rankspace<RP, X3>, dim3(grid), dim3(kThreads), C::SMEM, s, tm, a.out, a.ldo,
+  launch_pdl(k_attn_rankspace<RP, X3>, dim3(grid), dim3(kThreads), C::SMEM, s, tm, tkv, a.out, a.ldo,
              a.batch, a.seq, a.heads, a.groups, a.q_off, a.k_off, a.v_off, a.causal ? 1 : 0,
              X3 ? T : 0, X3 ? a.out_ps : (int64_t)0);
   check_launch("k_attn_rankspace");

@@ -664,7 +664,7 @@ void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_lay
     if (q.dense && !packs.back()->dense)
       fail(Kind::Config, "dense / naive_lowrank modes run on the tensor cores only: head width "
                          "<= 64, d_model and d_ff multiples of 8");
-    ws = std::max(ws, layer_workspace_bytes(*packs.back(), B * M, mode, pre_ln != 0));
+    ws = std::max(ws, layer_workspace_bytes(*packs.back(), B, M, mode, pre_ln != 0));
     pack_bytes += packs.back()->bytes;
     if (packs.back()->x3 != packs[0]->x3)
       fail(Kind::Config, "fp32 policy: every layer must fit the tensor-core tiling, or none");
@@ -884,7 +884,7 @@ fsvd_status fsvd_workspace_bytes(const fsvd_layer_pack* const* packs, size_t n_l
     check_mode(mode);
     size_t ws = 0;
     for (size_t i = 0; i < n_layers; ++i)
-      ws = std::max(ws, layer_workspace_bytes(*packs[i]->p, batch * seq, mode));
+      ws = std::max(ws, layer_workspace_bytes(*packs[i]->p, batch, seq, mode));
     *bytes = ws;
   });
 }
@@ -896,7 +896,7 @@ fsvd_status fsvd_workspace_bytes_ln(const fsvd_layer_pack* const* packs, size_t 
     check_mode(mode);
     size_t ws = 0;
     for (size_t i = 0; i < n_layers; ++i)
-      ws = std::max(ws, layer_workspace_bytes(*packs[i]->p, batch * seq, mode, pre_ln != 0));
+      ws = std::max(ws, layer_workspace_bytes(*packs[i]->p, batch, seq, mode, pre_ln != 0));
     *bytes = ws;
   });
 }
@@ -1341,7 +1341,7 @@ fsvd_status fsvd_stream_workspace_bytes(const fsvd_layer_pack* const* packs, siz
     check_mode(mode);
     size_t ws = 0;
     for (size_t i = 0; i < n_layers; ++i)
-      ws = std::max(ws, layer_workspace_bytes(*packs[i]->p, batch * seq, mode));
+      ws = std::max(ws, layer_workspace_bytes(*packs[i]->p, batch, seq, mode));
     *bytes = ws + 2 * stream_slot_bytes(packs, batch, seq) + 256;
   });
 }
@@ -1359,7 +1359,7 @@ fsvd_status fsvd_model_fwd_stream(const fsvd_layer_pack* const* packs, size_t n_
     require_device();
     size_t need = 0;
     for (size_t i = 0; i < n_layers; ++i)
-      need = std::max(need, layer_workspace_bytes(*packs[i]->p, batch * seq, mode, pre_ln != 0));
+      need = std::max(need, layer_workspace_bytes(*packs[i]->p, batch, seq, mode, pre_ln != 0));
     const size_t slot = stream_slot_bytes(packs, batch, seq);
     if (ws_bytes < need + 2 * slot + 256)
       fail(Kind::Config, "workspace too small: need " + std::to_string(need + 2 * slot + 256) +

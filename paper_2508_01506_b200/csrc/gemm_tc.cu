@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const __grid_constant__ CUtensorMap tmC, const float* __restrict__ bias, int act,
                 int M, int N, int K, const bf16* resid, int64_t ldr,
                 const __grid_constant__ CUtensorMap tmC2, const __grid_constant__ CUtensorMap tmC3,
-                int64_t resid_ps) {
+                int64_t resid_ps, int split_n) {
   using Cfg = GemmCfg<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -261,7 +261,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           named_bar_sync(1, kEpiWarps * 32);
           if (et == 0) {
-            tma_store_2d_u32(pl == 0 ? &tmC : pl == 1 ? &tmC2 : &tmC3, box, n0 + b0, m0);
+            if (!X3 && split_n > 0 && n0 + b0 >= split_n)  // split output: columns >= split_n
+              tma_store_2d_u32(&tmC2, box, n0 + b0 - split_n, m0);
+            else
+              tma_store_2d_u32(pl == 0 ? &tmC : pl == 1 ? &tmC2 : &tmC3, box, n0 + b0, m0);
             tma_store_commit();
           }
           ++nbox;
@@ -480,7 +483,7 @@ template <int BN, int STAGES, bool X3 = false>
 void launch_gemm(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, int64_t ldc,
                  int M, int N, int K, const float* bias, int act, cudaStream_t s,
                  const bf16* resid = nullptr, int64_t ldr = 0, bf16* C2 = nullptr,
-                 bf16* C3 = nullptr, int64_t resid_ps = 0) {
+                 bf16* C3 = nullptr, int64_t resid_ps = 0, int split_n = 0, int64_t ldc2 = 0) {
   using Cfg = GemmCfg<BN, STAGES>;
   static bool attr = false;
   if (!attr) {
@@ -491,13 +494,17 @@ void launch_gemm(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C
   const int np = X3 ? kPlanes : 1;  // stacked planes behind A and B
   const CUtensorMap ta = tmap_bf16(A, (uint64_t)np * M, K, lda, BM, BK, TmaSwizzle::B128);
   const CUtensorMap tb = tmap_bf16(B, (uint64_t)np * N, K, ldb, BN, BK, TmaSwizzle::B128);
-  const CUtensorMap tc = tmap_bf16(C, M, N, ldc, BM, 64, TmaSwizzle::B128);
-  const CUtensorMap tc2 = X3 ? tmap_bf16(C2, M, N, ldc, BM, 64, TmaSwizzle::B128) : tc;
+  // split output (non-X3): columns [0, split_n) -> C, [split_n, N) -> C2 (pitch ldc2)
+  const bool split = !X3 && split_n > 0;
+  const CUtensorMap tc = tmap_bf16(C, M, split ? split_n : N, ldc, BM, 64, TmaSwizzle::B128);
+  const CUtensorMap tc2 = X3      ? tmap_bf16(C2, M, N, ldc, BM, 64, TmaSwizzle::B128)
+                          : split ? tmap_bf16(C2, M, N - split_n, ldc2, BM, 64, TmaSwizzle::B128)
+                                  : tc;
   const CUtensorMap tc3 = X3 ? tmap_bf16(C3, M, N, ldc, BM, 64, TmaSwizzle::B128) : tc;
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   launch_pdl(k_gemm_bf16<BN, STAGES, X3>, dim3(grid), dim3(kThreads), Cfg::SMEM, s, ta, tb, tc,
-             bias, act, M, N, K, resid, ldr, tc2, tc3, resid_ps);
+             bias, act, M, N, K, resid, ldr, tc2, tc3, resid_ps, split ? split_n : 0);
   check_launch("k_gemm_bf16");
 }
 
@@ -547,6 +554,22 @@ void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, 
     launch_gemm<128, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
   else
     launch_gemm<64, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
+}
+
+void gemm_bf16_split(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C,
+                     int64_t ldc, int split_n, bf16* C2, int64_t ldc2, int M, int N, int K,
+                     const float* bias, cudaStream_t s) {
+  if (split_n % 64 != 0 || split_n <= 0 || split_n >= N || ldc2 % 8 != 0)
+    throw CudaError("gemm_bf16_split: split column must be a positive multiple of 64 below N");
+  if (N % 192 == 0)
+    launch_gemm<192, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, ACT_NONE, s, nullptr, 0, C2,
+                        nullptr, 0, split_n, ldc2);
+  else if (N % 256 == 0 || N > 1024)
+    launch_gemm<256, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, ACT_NONE, s, nullptr, 0, C2,
+                        nullptr, 0, split_n, ldc2);
+  else
+    launch_gemm<128, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, ACT_NONE, s, nullptr, 0, C2,
+                        nullptr, 0, split_n, ldc2);
 }
 
 void gemm_x3(const Planes& A, int64_t lda, const Planes& B, int64_t ldb, const PlanesOut& C,

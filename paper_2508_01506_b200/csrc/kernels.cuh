@@ -28,6 +28,13 @@ void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, 
                int M, int N, int K, const float* bias, int act, cudaStream_t s,
                const bf16* resid = nullptr, int64_t ldr = 0);
 bool gemm_bf16_supported(int M, int N, int K, int64_t lda, int64_t ldb, int64_t ldc);
+// Split output: columns [0, split_n) of C = A B^T + bias go to C (pitch ldc),
+// columns [split_n, N) to C2 (pitch ldc2).  split_n % 64 == 0.  The QKV
+// projection uses it to put Qt (which K2 overwrites with its rank-space output)
+// and the [P_k | P_v] chunk (dead after K2) in separate workspace regions.
+void gemm_bf16_split(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C,
+                     int64_t ldc, int split_n, bf16* C2, int64_t ldc2, int M, int N, int K,
+                     const float* bias, cudaStream_t s);
 
 // ---- split planes (fp32 policy on the tensor cores) ---------------------------
 // An fp32 matrix v is held as three bf16 matrices of the same shape, stored
@@ -96,6 +103,13 @@ struct AttnTcArgs {
   // its X3 form (six bf16 passes per product)
   bool planes = false;
   int64_t out_ps = 0;
+  // K / V in their own region ([T, kv_cols], pitch ldkv; k_off / v_off are
+  // then column offsets in it); null: they sit in qkv.  out may alias the Qt
+  // columns of qkv: an item reads its Qt tile before it writes its output
+  // there, and no other item reads those cells.
+  const bf16* kv = nullptr;
+  int64_t ldkv = 0;
+  int kv_cols = 0;
 };
 void attn_rankspace_bf16(const AttnTcArgs& a, cudaStream_t s);
 

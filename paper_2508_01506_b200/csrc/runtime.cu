@@ -581,8 +581,44 @@ bool ffn_ln_fusable(const Pack& p, int mode) {
 struct WsLayout {
   size_t a, b, t;  // bytes of the A / B / transient regions (256-aligned)
   size_t total() const { return a + b + t + 256; }
+  int chunks = 0;  // > 0: the compact fused post-LN layout (qkv_chunks)
 };
-WsLayout ws_layout(const Pack& p, size_t T, int mode, bool pre_ln) {
+// Compact fused post-LN layout (both LayerNorms fused, full attention): the
+// LN1 output goes straight into the layer's output buffer (K6 runs in place
+// over the residual when out == x, the FFN kernel in place over out: every
+// CTA reads its 128 rows before it writes them); region A [T, H*rp] holds Qt
+// from the projection and then, in the same cells, K2's rank-space output;
+// the [P_k | P_v] columns -- dead once K2 has read them -- go to a transient
+// of one chunk of sequences: K1 and K2 run chunk by chunk (qkv_chunks()).
+// The FFN V1 chain's P | Z reuse A and the transient.
+int qkv_chunks(size_t B) {
+  static const int env = [] {
+    const char* e = getenv("FSVD_QKV_CHUNKS");  // developer switch (memory / speed sweep)
+    return e ? atoi(e) : 2;
+  }();
+  const int c = env < 1 ? 1 : env;
+  return static_cast<int>(std::min<size_t>(B, static_cast<size_t>(c)));
+}
+bool compact_post_ln(const Pack& p, int mode) {
+  return fused_post_ln(p, mode) && ffn_ln_fusable(p, mode) && (p.H * p.rp) % 64 == 0 &&
+         p.dtype == FSVD_BF16;
+}
+WsLayout ws_layout(const Pack& p, size_t B, size_t M, int mode, bool pre_ln, bool compact) {
+  const size_t T = B * M;
+  if (!pre_ln && compact && compact_post_ln(p, mode)) {
+    const int c = qkv_chunks(B);
+    const size_t cb = (B + c - 1) / c;  // sequences per chunk
+    const size_t hr = static_cast<size_t>(p.H * p.rp), kvw = 2 * static_cast<size_t>(p.G * p.rp);
+    const size_t a = align256(T * hr * p.es);
+    size_t t = align256(cb * M * kvw * p.es);
+    if (mode == FSVD_MODE_FLASH_V1 || p.ffn_wide) {  // P | Z of the V1 chain over A + transient
+      const size_t pz = align256(2 * T * p.frp * p.es);
+      if (pz > a + t) t = pz - a;
+    }
+    WsLayout w{a, 0, t};
+    w.chunks = c;
+    return w;
+  }
   if (!pre_ln && fused_post_ln(p, mode)) {
     const bool ffn_fused = ffn_ln_fusable(p, mode);
     const size_t a_cols = ffn_fused ? static_cast<size_t>(p.H * p.rp) : p.d;
@@ -601,11 +637,15 @@ WsLayout ws_layout(const Pack& p, size_t T, int mode, bool pre_ln) {
 }
 }  // namespace
 
-size_t layer_workspace_bytes(const Pack& p, size_t T, int mode, bool pre_ln) {
-  return ws_layout(p, T, mode, pre_ln).total();
+size_t layer_workspace_bytes(const Pack& p, size_t B, size_t M, int mode, bool pre_ln) {
+  return ws_layout(p, B, M, mode, pre_ln, true).total();
 }
-size_t layer_workspace_bytes(const Pack& p, size_t T, int mode) {
-  return std::max(layer_workspace_bytes(p, T, mode, false), layer_workspace_bytes(p, T, mode, true));
+size_t layer_workspace_bytes(const Pack& p, size_t B, size_t M, int mode) {
+  return std::max(layer_workspace_bytes(p, B, M, mode, false),
+                  layer_workspace_bytes(p, B, M, mode, true));
+}
+size_t prefill_workspace_bytes(const Pack& p, size_t B, size_t M, bool pre_ln) {
+  return ws_layout(p, B, M, FSVD_MODE_FLASH_V2, pre_ln, false).total();
 }
 
 // ---------------------------------------------------------------- schedule
@@ -1251,7 +1291,7 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
   if ((mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2 ||
        mode == FSVD_MODE_NAIVE_LOWRANK) && !(p.has_attn && p.has_out && p.has_ffn))
     fail(Kind::Config, "this mode needs factorized weights on both sublayers");
-  const WsLayout lay = ws_layout(p, T, mode, pre_ln);
+  const WsLayout lay = ws_layout(p, B, M, mode, pre_ln, am.kind == AttnMode::Full);
   if (ws_bytes < lay.total())
     fail(Kind::Config, "workspace too small: need " + std::to_string(lay.total()) + " bytes, got " +
                            std::to_string(ws_bytes));
@@ -1263,7 +1303,44 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
   if (am.kind != AttnMode::Full && !(p.attn_tc && p.out_tc &&
                                       (mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2)))
     fail(Kind::Config, "decoder rows run on the bf16 tensor-core flash path");
-  if (!pre_ln && fused_post_ln(p, mode)) {
+  if (lay.chunks > 0) {
+    // compact fused post-LN schedule (ws_layout): per chunk of sequences, K1
+    // [Qt -> A | P_k P_v -> transient] and K2 (output over Qt in A); then
+    // K6 (LN1 -> out, in place when out == x) and the FFN in place over out
+    const int hr = p.H * p.rp, kvw = 2 * p.G * p.rp, n = p.qkv_cols;
+    bf16* kv = as<bf16>(base + lay.a);
+    const size_t cb = (B + lay.chunks - 1) / lay.chunks;
+    for (size_t b0 = 0; b0 < B; b0 += cb) {
+      const size_t nb = std::min(cb, B - b0);
+      const int crows = static_cast<int>(nb * M);
+      const size_t r0 = b0 * M;
+      bf16* qa = as<bf16>(A) + r0 * hr;
+      gemm_bf16_split(as<bf16>(x) + r0 * p.d, p.d, as<bf16>(p.wproj_t), p.d, qa, hr, hr, kv, kvw,
+                      crows, n, p.d, p.bproj, s);
+      AttnTcArgs a;
+      a.qkv = qa;
+      a.ldq = hr;
+      a.qkv_cols = hr;
+      a.q_off = 0;
+      a.kv = kv;
+      a.ldkv = kvw;
+      a.kv_cols = kvw;
+      a.k_off = 0;
+      a.v_off = p.G * p.rp;
+      a.batch = static_cast<int>(nb);
+      a.seq = static_cast<int>(M);
+      a.heads = p.H;
+      a.groups = p.G;
+      a.rank_pad = p.rp;
+      a.out = qa;
+      a.ldo = hr;
+      attn_rankspace_bf16(a, s);
+    }
+    gemm_ln_bf16(as<bf16>(A), hr, as<bf16>(p.wov_t), hr, p.bov, as<bf16>(x), p.ln1g, p.ln1b,
+                 p.eps1, as<bf16>(out), rows, p.d, hr, s);
+    if (!ffn_ln_fwd(p, mode, B, M, out, out, A, s))
+      fail(Kind::Config, "compact post-LN schedule without a fused FFN LayerNorm");
+  } else if (!pre_ln && fused_post_ln(p, mode)) {
     // rank-space attention -> A; folded out-projection + residual + LN1 -> B
     tc_attention_rank(p, B, M, x, A, trans, s, am);
     gemm_ln_bf16(as<bf16>(A), p.H * p.rp, as<bf16>(p.wov_t), p.H * p.rp, p.bov, as<bf16>(x),
@@ -1367,8 +1444,7 @@ size_t kv_cache_bytes(const Pack& p, size_t B, size_t max_seq) {
 }
 
 size_t decoder_workspace_bytes(const Pack& p, size_t B, size_t max_seq, bool pre_ln) {
-  const size_t prefill = layer_workspace_bytes(p, B * max_seq, FSVD_MODE_FLASH_V2, pre_ln);
-  (void)pre_ln;
+  const size_t prefill = prefill_workspace_bytes(p, B, max_seq, pre_ln);
   return std::max(prefill, decode_layout(p, B, max_seq).total());
 }
 

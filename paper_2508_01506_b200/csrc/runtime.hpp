@@ -113,8 +113,10 @@ void check_mode_weights(const fsvd_layer_desc& L, int mode, bool dense_twin_ok);
 // Activation buffer planner: bytes of device workspace one layer needs for
 // T = batch*seq tokens in the given mode (two [T, d] scratch buffers + the
 // rank-sized transient region, aliased across sublayers).
-size_t layer_workspace_bytes(const Pack& p, size_t T, int mode);  // max over pre/post-LN
-size_t layer_workspace_bytes(const Pack& p, size_t T, int mode, bool pre_ln);
+// workspace of a [B, M] batch through layer_fwd (full attention); max over
+// pre/post-LN without the flag
+size_t layer_workspace_bytes(const Pack& p, size_t B, size_t M, int mode);
+size_t layer_workspace_bytes(const Pack& p, size_t B, size_t M, int mode, bool pre_ln);
 size_t op_transient_elems(const Pack& p, int op, int mode);  // op: 0 attn, 1 out, 2 ffn
 
 // Device schedule (async on `s`).  x and out may alias in layer_fwd.

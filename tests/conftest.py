@@ -13,6 +13,15 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
 
+def pytest_collection_modifyitems(config, items):
+    # a GPU test that hangs (a kernel waiting on a barrier that never
+    # completes) would block in a CUDA synchronize until the box's limit: cap
+    # each at 10 minutes, thread method (ends the process, printing stacks)
+    for item in items:
+        if item.get_closest_marker("gpu") and not item.get_closest_marker("timeout"):
+            item.add_marker(pytest.mark.timeout(600, method="thread"))
+
+
 @pytest.fixture(scope="session")
 def restatement():
     import oracle

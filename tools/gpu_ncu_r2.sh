@@ -1,0 +1,13 @@
+#!/bin/bash
+# ncu --set full of the four path kernels (one layer, cfg2 shapes), launch list of the bench
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+B="python bench.py --steps 1 --warmup 1 --layers 1 --no-cpu-baseline --no-torch-baseline --no-dropin-e2e"
+for k in k_ffn k_gemm_ln k_attn k_gemm_bf16; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
+    -o gpurun_out/prof_$k -f $B > gpurun_out/prof_$k.log 2>&1
+done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline \
+  --no-torch-baseline --no-dropin-e2e > gpurun_out/b_ncu.log 2>&1
+echo done

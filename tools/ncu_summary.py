@@ -35,6 +35,10 @@ METRICS = {
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
     "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
     "sm__inst_executed.avg.per_cycle_active": "ipc",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_throughput_pct",
+    "lts__t_sectors.avg.pct_of_peak_sustained_elapsed": "l2_sectors_pct",
+    "l1tex__throughput.avg.pct_of_peak_sustained_active": "l1_throughput_pct",
+    "sm__memory_throughput.avg.pct_of_peak_sustained_elapsed": "sm_memory_pct",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1, "usecond": 1,
          "ms": 1e3, "msecond": 1e3, "nsecond": 1e-3, "hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9}
