@@ -39,6 +39,10 @@
 #include "ptx.cuh"
 
 namespace fsvd {
+FSVD_CTA_TIMES(attn)
+}  // namespace fsvd
+
+namespace fsvd {
 namespace {
 
 using namespace ptx;
@@ -169,6 +173,7 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
                      int64_t ldo, int batch, int seq, int heads, int groups, int q_off, int k_off,
                      int v_off, int causal, int plane_rows, int64_t out_ps) {
   using C = AttnCfg<RP, X3>;
+  CTA_T(0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -205,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
   tc_fence_after();
   pdl_trigger();
   pdl_wait();
+  CTA_T(1);
   const uint32_t tmem = bars->tmem;
   const uint32_t s_q = smem_u32(smem + C::o_q), s_kv = smem_u32(smem + C::o_kv);
 
@@ -521,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
     tc_fence_after();
     tmem_free<C::TMEM_COLS>(tmem);
   }
+  CTA_T(2);
 }
 
 template <int RP, bool X3 = false>

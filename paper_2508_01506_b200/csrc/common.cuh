@@ -50,6 +50,33 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
   FSVD_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
+#ifdef FSVD_TRACE
+// per-CTA timeline of the last launch of a kernel in this translation unit
+// (ptx::globaltimer_ns): [cta][entry, after pdl_wait, exit (ns), clock64 after
+// pdl_wait, clock64 at exit, smid, -, -]; the clock64 / ns ratio is the SM
+// clock the CTA ran at
+#define FSVD_CTA_TIMES(tu)                                                              \
+  namespace {                                                                          \
+  __device__ unsigned long long g_cta_t[4096 * 8];                                     \
+  }                                                                                    \
+  extern "C" __attribute__((visibility("default"))) int fsvd_debug_cta_times_##tu(      \
+      unsigned long long* host, int n) {                                                \
+    return static_cast<int>(cudaMemcpyFromSymbol(host, g_cta_t, sizeof(unsigned long long) * n)); \
+  }
+#define CTA_T(slot)                                                                     \
+  do {                                                                                  \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {                                        \
+      unsigned long long* e_ = g_cta_t + blockIdx.x * 8;                                \
+      e_[(slot)] = ::fsvd::ptx::globaltimer_ns();                                       \
+      if ((slot) == 0) e_[5] = ::fsvd::ptx::smid();                                     \
+      if ((slot) >= 1) e_[2 + (slot)] = clock64();                                      \
+    }                                                                                   \
+  } while (0)
+#else
+#define FSVD_CTA_TIMES(tu)
+#define CTA_T(slot) do { } while (0)
+#endif
+
 enum class TmaSwizzle { None, B32, B64, B128 };
 
 // Row-major 2-D tensor [rows, cols] with leading dimension ld (elements);

@@ -174,6 +174,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
+  pdl_trigger();
+  pdl_wait();
   const uint32_t tmem = bars->tmem;
   uint8_t* ring = smem + C::o_ring;
 
@@ -455,9 +457,8 @@ void launch_ffn2(const FfnTcArgs& a, cudaStream_t s) {
   const CUtensorMap ty =
       ln ? tmap_bf16(a.out, a.T, a.d_model, a.d_model, BMr, 64, TmaSwizzle::B128) : tx;
   const int pairs = (a.T + 2 * BMr - 1) / (2 * BMr);
-  k_ffn2<FR><<<2 * pairs, kThreads, C::SMEM, s>>>(tx, tup, tvup, tudn, tvdn, ty, a.up_b, a.dn_b,
-                                                 a.act, a.T, a.d_model, a.d_ff, a.out, a.ln_g,
-                                                 a.ln_b, a.ln_eps);
+  launch_pdl(k_ffn2<FR>, dim3(2 * pairs), dim3(kThreads), C::SMEM, s, tx, tup, tvup, tudn, tvdn,
+             ty, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff, a.out, a.ln_g, a.ln_b, a.ln_eps);
   check_launch("k_ffn2");
 }
 

@@ -32,8 +32,17 @@
 // (ln_epi.cuh; V2 with LN2 only).
 #include "common.cuh"
 #include "kernels.cuh"
+#ifdef FSVD_TRACE
+namespace fsvd { __device__ long long g_trace_ffn_ln[512]; }
+#define LN_TRACE(slot) \
+  do { if (blockIdx.x == 0 && (slot) < 512) ::fsvd::g_trace_ffn_ln[(slot)] = clock64(); } while (0)
+#endif
 #include "ln_epi.cuh"
 #include "ptx.cuh"
+
+namespace fsvd {
+FSVD_CTA_TIMES(ffn)
+}  // namespace fsvd
 
 namespace fsvd {
 namespace {
@@ -125,6 +134,9 @@ __device__ long long g_trace[4096];
 extern "C" __attribute__((visibility("default"))) int fsvd_debug_trace_copy(long long* host, int n) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * n));
 }
+extern "C" __attribute__((visibility("default"))) int fsvd_debug_trace_ffn_ln_copy(long long* host, int n) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace_ffn_ln, sizeof(long long) * n));
+}
 namespace {
 #define TRACE(slot) do { if (blockIdx.x == 0) g_trace[(slot)] = clock64(); } while (0)
 #else
@@ -146,9 +158,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           int d_model, int d_ff, bf16* z_out, bf16* out,
           const float* __restrict__ ln_g, const float* __restrict__ ln_b, float ln_eps,
           int split_blocks, float* __restrict__ z_part, const bf16* resid,
-          int frk, bf16* sum_out, int64_t z_ps) {
+          int frk, bf16* sum_out, int64_t z_ps, int rot_mode) {
   static_assert(!(WIDE && FUSED), "wide ranks run the V1 chain");
   using C = FfnCfg<FR, WIDE, X3>;
+  CTA_T(0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -167,10 +180,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int NBall = (d_ff + BF - 1) / BF;
   const int fb0 = split_blocks ? split * split_blocks : 0;
   const int NB = split_blocks ? min(split_blocks, NBall - fb0) : NBall;
+  // Loop rotation (FUSED): each tile starts its K-chunk, feature-block and
+  // output-piece loops at an offset, so concurrent CTAs read different weight
+  // boxes.  rot_mode > 0: 128-row tiles per sequence (FfnTcArgs::seq_tiles),
+  // the offset follows the tile's place in its sequence (independent of the
+  // batch position); < 0: by CTA index (developer experiment, FSVD_FFN_ROT=1).
+  const int rpos = !FUSED || rot_mode == 0 ? 0
+                   : rot_mode > 0 ? static_cast<int>(blockIdx.x) % rot_mode
+                                  : static_cast<int>(blockIdx.x);
+  const int rdiv = rot_mode > 0 ? rot_mode : 1;
+  const int rot = rot_mode > 0 ? rpos * NBall / rdiv : rpos % NBall;
+  const int rotk = rot_mode > 0 ? rpos * (d_model / 64) / rdiv : rpos;
+  auto blk = [&](int f) { return rot ? (f + rot) % NB : f; };
   const int KC = d_model / 64;                        // X K-chunks (FUSED)
   const bool fuse_ln = FUSED && ln_g != nullptr;     // out = LN2(x + ffn(x)) (ln_epi.cuh)
   const int QS = (d_model % 128 == 0 && !fuse_ln) ? 128 : 64;  // output columns per piece
   const int NQ = d_model / QS;
+  const int rotq = rot_mode > 0 ? rpos * NQ / rdiv : 0;  // fused-LN output pieces
 
   if (threadIdx.x == 0) TRACE(0);
   if (warp == 0 && lane == 0) {
@@ -209,6 +235,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   pdl_trigger();
   pdl_wait();
+  CTA_T(1);
+  if (threadIdx.x == 0) TRACE(5);
   const uint32_t tmem = bars->tmem;
   uint8_t* ring = smem + C::o_ring;
 
@@ -261,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           return;
         }
         emit(C::NATOM, [&](int a, uint8_t* dst, bool size_only) -> uint32_t {
-          if (!size_only) tma_load_2d(&tmVup, &bars->full[st], dst, a * 64, (fb0 + f) * BF);
+          if (!size_only) tma_load_2d(&tmVup, &bars->full[st], dst, a * 64, (fb0 + blk(f)) * BF);
           return SLOT;
         });
       };
@@ -281,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         emit(2 * C::NPIECE, [&](int j, uint8_t* dst, bool size_only) -> uint32_t {
           const int a = j / C::NPIECE, p = j % C::NPIECE;
           if (!size_only)
-            tma_load_2d(&tmUdn, &bars->full[st], dst, (fb0 + f) * BF + a * 64, zc0 + p * C::PS);
+            tma_load_2d(&tmUdn, &bars->full[st], dst, (fb0 + blk(f)) * BF + a * 64, zc0 + p * C::PS);
           return C::PS * 128;
         });
       };
@@ -291,10 +319,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (static_cast<uint32_t>(xb) == me) {
             mbar_wait(&bars->x_empty[xb], ((kc >> 1) & 1) ^ 1);
             mbar_arrive_expect_tx(&bars->x_full[xb], SLOT);
-            tma_load_2d(&tmX, &bars->x_full[xb], smem + C::o_h + xb * SLOT, kc * 64, m0);
+            tma_load_2d(&tmX, &bars->x_full[xb], smem + C::o_h + xb * SLOT, ((kc + rotk) % KC) * 64, m0);
           }
           emit(C::NPIECE, [&](int p, uint8_t* dst, bool size_only) -> uint32_t {
-            if (!size_only) tma_load_2d(&tmUup, &bars->full[st], dst, kc * 64, p * C::PS);
+            if (!size_only) tma_load_2d(&tmUup, &bars->full[st], dst, ((kc + rotk) % KC) * 64, p * C::PS);
             return C::PS * 128;
           });
         }
@@ -316,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           emit(C::NATOM, [&](int a, uint8_t* dst, bool size_only) -> uint32_t {
             if (!size_only)
               tma_load_2d(&tmVdn, &bars->full[st], dst, a * 64,
-                          (fuse_ln ? lnepi::piece_of(q, NQ) : q) * QS);
+                          (fuse_ln ? lnepi::piece_of(q, NQ, rotq) : q) * QS);
             return QS * 128;
           });
       }
@@ -327,9 +355,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // The H tile is idle once every MMA2 has completed (z_full); the residual
     // (= this tile of X) streams through it as two [128 x 64] boxes.
     if (fuse_ln && lane == 0) {
-      mbar_wait(&bars->z_full, 0);
+      mbar_wait_sleep(&bars->z_full, 0, 256);
       lnepi::produce_residual<64>(&tmR, smem + C::o_h, bars->res_full, bars->res_empty, 2,
-                                  d_model, m0);
+                                  d_model, m0, rotq);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -374,7 +402,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // P = X U_up into the Z columns of TMEM
         for (int kc = 0; kc < KC; ++kc) {
           const int xb = kc & 1;
+          TRACE(3000 + kc * 2);
           mbar_wait(&bars->x_full[xb], (kc >> 1) & 1);
+          TRACE(3000 + kc * 2 + 1);
           tc_fence_after();
           consume(C::NPIECE, [&](int p, uint64_t slot) {
             mma4(tmem + C::t_z + p * C::PS, d_h + xb * kAtom, slot, idesc_bf16(128, C::PS),
@@ -518,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float bb[2][32];  // b_up of this block, fetched while the MMA runs
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int fb = (fb0 + f) * BF + (half + 2 * i) * 32;
+        const int fb = (fb0 + blk(f)) * BF + (half + 2 * i) * 32;
         load_bias<32>(bb[i], b_up + fb, d_ff - fb);
       }
       if (threadIdx.x == 64) TRACE(1024 + f * 8 + 0);
@@ -552,6 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     mbar_wait(&bars->z_full, 0);
+    if (threadIdx.x == 64) TRACE(6);
     tc_fence_after();
     if (!FUSED) {
       for (int c = half; c < FR / 32; c += 2) {
@@ -585,13 +616,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&bars->zs_ready);
+      if (threadIdx.x == 64) TRACE(7);
       if (fuse_ln) {
         // residual = the FFN input x, streamed through the idle H tile
         // gamma / beta are staged in the weight ring, idle once all MMAs are done
         lnepi::run<64>(tmem, quad, half, row, d_model, b_dn, smem_u32(smem + C::o_h),
                        bars->res_full, bars->res_empty, 2, ln_g, ln_b, ln_eps, &tmY, m0,
                        reinterpret_cast<float*>(ring), smem_u32(smem + C::o_h), bars->o_full,
-                       bars->o_free, 1, 0, sum_out, T);
+                       bars->o_free, 1, 0, sum_out, T, rotq);
       } else {
         for (int q = 0; q < NQ; ++q) {
           mbar_wait(&bars->o_full[q & 1], (q >> 1) & 1);
@@ -631,9 +663,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_free<512>(tmem);
   }
+  CTA_T(2);
 }
 
 // FR = Z columns per CTA; frk = a.rank_pad (the P / Z width, K of MMA1).
+int ffn_rot_mode() {
+  static const int m = [] {
+    const char* e = getenv("FSVD_FFN_ROT");  // 0 off, 1 by CTA (experiment), 2 by tile in sequence
+    return e ? atoi(e) : 2;
+  }();
+  return m;
+}
+
 template <int FR, bool FUSED, bool WIDE = false, bool X3 = false>
 void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
   using C = FfnCfg<FR, WIDE, X3>;
@@ -668,7 +709,8 @@ void launch_ffn(const FfnTcArgs& a, cudaStream_t s) {
              s, tx, tp, tup, tvup, tudn, tvdn, ty, tr, a.up_b, a.dn_b, a.act, a.T, a.d_model,
              a.d_ff, a.z_out, a.out, a.ln_g, a.ln_b, a.ln_eps, FUSED ? 0 : a.split_blocks,
              FUSED ? nullptr : a.z_part, FUSED ? a.resid : nullptr, frk,
-             FUSED && a.ln_g ? a.sum_out : nullptr, X3 ? (int64_t)a.T * frk : (int64_t)0);
+             FUSED && a.ln_g ? a.sum_out : nullptr, X3 ? (int64_t)a.T * frk : (int64_t)0,
+             !FUSED ? 0 : ffn_rot_mode() == 1 ? -1 : ffn_rot_mode() == 0 ? 0 : a.seq_tiles);
   check_launch(FUSED ? "k_ffn_fused" : "k_ffn_stream");
 }
 

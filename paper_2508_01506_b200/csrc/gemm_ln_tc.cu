@@ -28,6 +28,8 @@
 // Warps: 0 and 11 TMA producers (A, B; alternating stages), 1 MMA issuer +
 // TMEM owner, 2..9 epilogue (two per TMEM lane quadrant; each owns 32 of the
 // 64 columns of a piece), 10 residual producer (ln_epi.cuh).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #ifdef FSVD_TRACE
@@ -36,6 +38,10 @@ namespace fsvd { __device__ long long g_trace_ln[1024]; }
 #endif
 #include "ln_epi.cuh"
 #include "ptx.cuh"
+
+namespace fsvd {
+FSVD_CTA_TIMES(gemm_ln)
+}  // namespace fsvd
 
 namespace fsvd {
 namespace {
@@ -79,7 +85,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float* __restrict__ bias,
               const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
               bf16* y, int T, int N, int K, int stages,
-              bf16* sum_out) {
+              bf16* sum_out, int seq_tiles) {
+  CTA_T(0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -91,6 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   LnBars* bars = reinterpret_cast<LnBars*>(rring + RS * RBOX);
   const uint32_t warp = warp_id(), lane = lane_id();
   const int m0 = blockIdx.x * BMr;
+  const int rot = lnepi::seq_rotation(blockIdx.x, seq_tiles, N / PN);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -118,6 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   pdl_trigger();
   pdl_wait();
+  CTA_T(1);
   const uint32_t tmem = bars->tmem;
 
   if (warp == 0 || warp == 11) {
@@ -137,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int n = (nslots - i) < SPS ? (nslots - i) : SPS;
           mbar_arrive_expect_tx(&bars->full[st], n * SLOT);
           for (int j = 0; j < n; ++j) {
-            const int s = i + j, q = lnepi::piece_of(s / KA, NP), a = s % KA;
+            const int s = i + j, q = lnepi::piece_of(s / KA, NP, rot), a = s % KA;
             tma_load_2d(&tmB, &bars->full[st], ring + st * STAGE + j * SLOT, a * 64, q * PN);
           }
         }
@@ -199,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 10) {
     // ============================================ residual producer (one thread)
     if (lane == 0)
-      lnepi::produce_residual<PN>(&tmR, rring, bars->res_full, bars->res_empty, RS, N, m0);
+      lnepi::produce_residual<PN>(&tmR, rring, bars->res_full, bars->res_empty, RS, N, m0, rot);
     __syncwarp();
   } else {
     // ============================================ epilogue (8 warps)
@@ -210,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // region (both idle once every MMA has completed)
     lnepi::run<PN>(tmem, quad, half, row, N, bias, smem_u32(rring), bars->res_full,
                    bars->res_empty, RS, gamma, beta, eps, &tmY, m0, reinterpret_cast<float*>(sA),
-                   smem_u32(ring), bars->acc_full, bars->acc_empty, 1, 0, sum_out, T);
+                   smem_u32(ring), bars->acc_full, bars->acc_empty, 1, 0, sum_out, T, rot);
   }
   if (threadIdx.x == 64) LTRACE(100);
   tc_fence_before();
@@ -220,6 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_free<512>(tmem);
   }
+  CTA_T(2);
 }
 
 }  // namespace
@@ -230,7 +240,7 @@ bool gemm_ln_supported(int N, int K) {
 
 void gemm_ln_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, const float* bias,
                   const bf16* resid, const float* gamma, const float* beta, float eps, bf16* y,
-                  int T, int N, int K, cudaStream_t s, bf16* sum_out) {
+                  int T, int N, int K, cudaStream_t s, bf16* sum_out, int seq_tiles) {
   if (!gemm_ln_supported(N, K)) throw CudaError("gemm_ln_bf16: unsupported shape");
   const int KA = K / 64;
   int stages =
@@ -249,9 +259,14 @@ void gemm_ln_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, const 
   const CUtensorMap tb = tmap_bf16(B, N, K, ldb, PN, 64, TmaSwizzle::B128);
   const CUtensorMap tr = tmap_bf16(resid, T, N, N, BMr, 64, TmaSwizzle::B128);
   const CUtensorMap ty = tmap_bf16(y, T, N, N, BMr, 64, TmaSwizzle::B128);
+  static const bool rot_off = [] {
+    const char* e = getenv("FSVD_LN_ROT");  // developer A/B switch: 0 = no piece rotation
+    return e && e[0] == '0';
+  }();
+  if (rot_off) seq_tiles = 0;
   const int grid = (T + BMr - 1) / BMr;
   launch_pdl(k_gemm_ln, dim3(grid), dim3(kThreads), smem, s, ta, tb, tr, ty, bias, gamma, beta,
-             eps, y, T, N, K, stages, sum_out);
+             eps, y, T, N, K, stages, sum_out, seq_tiles);
   check_launch("k_gemm_ln");
 }
 

@@ -26,6 +26,10 @@
 #include "ptx.cuh"
 
 namespace fsvd {
+FSVD_CTA_TIMES(gemm)
+}  // namespace fsvd
+
+namespace fsvd {
 namespace {
 
 using namespace ptx;
@@ -80,6 +84,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const __grid_constant__ CUtensorMap tmC2, const __grid_constant__ CUtensorMap tmC3,
                 int64_t resid_ps, int split_n) {
   using Cfg = GemmCfg<BN, STAGES>;
+  CTA_T(0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -122,6 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   pdl_trigger();
   pdl_wait();
+  CTA_T(1);
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0 || warp == kThreads / 32 - 1) {
@@ -280,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_free<Cfg::TMEM_COLS>(tmem);
   }
+  CTA_T(2);
 }
 
 // ============================================================================
@@ -561,7 +568,14 @@ void gemm_bf16_split(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf1
                      const float* bias, cudaStream_t s) {
   if (split_n % 64 != 0 || split_n <= 0 || split_n >= N || ldc2 % 8 != 0)
     throw CudaError("gemm_bf16_split: split column must be a positive multiple of 64 below N");
-  if (N % 192 == 0)
+  static const int bn = [] {
+    const char* e = getenv("FSVD_SPLIT_BN");  // developer A/B switch
+    return e ? atoi(e) : 0;
+  }();
+  if (bn == 128 && N % 128 == 0)
+    launch_gemm<128, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, ACT_NONE, s, nullptr, 0, C2,
+                        nullptr, 0, split_n, ldc2);
+  else if (N % 192 == 0)
     launch_gemm<192, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, ACT_NONE, s, nullptr, 0, C2,
                         nullptr, 0, split_n, ldc2);
   else if (N % 256 == 0 || N > 1024)

@@ -81,7 +81,8 @@ void rows_from_device(const void* src, int rows, int d, int pitch, int form, flo
 // (the pre-LN residual stream).
 void gemm_ln_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, const float* bias,
                   const bf16* resid, const float* gamma, const float* beta, float eps, bf16* y,
-                  int T, int N, int K, cudaStream_t s, bf16* sum_out = nullptr);
+                  int T, int N, int K, cudaStream_t s, bf16* sum_out = nullptr,
+                  int seq_tiles = 0);
 bool gemm_ln_supported(int N, int K);
 
 // ---- K2: rank-space FlashSVD attention --------------------------------------
@@ -159,6 +160,13 @@ struct FfnTcArgs {
   // Z to z_part[split][T][rank_pad] (z_out unused); sum with z_partial_sum.
   int split_blocks = 0;
   float* z_part = nullptr;
+  // V2: 128-row tiles per sequence (seq / 128 when seq % 128 == 0, else 0).
+  // The fused kernel starts each tile's feature-block and K-chunk loops at an
+  // offset set by the tile's position inside its sequence, so concurrent CTAs
+  // read different weight boxes (all CTAs streaming the same boxes at once
+  // hot-spot the L2); a row's summation order depends only on where it sits
+  // in its sequence, so results stay independent of the batch position.
+  int seq_tiles = 0;
   // V2 without LN only: out = resid + ffn(x) (pre-LN layers)
   const bf16* resid = nullptr;
   // V2 with LN (pre-LN layer chaining): the LN residual is ln_resid instead of

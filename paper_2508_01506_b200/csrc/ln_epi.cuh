@@ -61,12 +61,20 @@ __device__ __forceinline__ void release_box(uint64_t* empty) {
   mbar_arrive(empty);
 }
 
-// Column piece handled at step i.  (A per-CTA rotation to spread weight reads
-// across L2 was measured to gain nothing and would make the statistics'
-// summation order -- hence the rounding -- depend on the tile's position.)
-__device__ __forceinline__ int piece_of(int i, int NP) {
-  (void)NP;
-  return i;
+// Column piece handled at step i: the pieces start at `rot`, which the
+// kernels set from the tile's position inside its sequence (FfnTcArgs::
+// seq_tiles), so concurrent CTAs read different weight boxes instead of all
+// pulling the same box through the same L2 slices at once; the statistics'
+// summation order then depends only on the row's place in its sequence, never
+// on the batch position.
+__device__ __forceinline__ int piece_of(int i, int NP, int rot = 0) {
+  const int q = i + rot;
+  return q >= NP ? q - NP : q;
+}
+// Rotation for a CTA whose 128-row tile is `tile` (blockIdx) when a sequence
+// holds seq_tiles tiles (0: no rotation), over n steps.
+__device__ __forceinline__ int seq_rotation(int tile, int seq_tiles, int n) {
+  return seq_tiles > 1 ? (tile % seq_tiles) * n / seq_tiles : 0;
 }
 
 // Residual producer (one thread): streams the [128 x N] residual tile at row
@@ -75,14 +83,14 @@ __device__ __forceinline__ int piece_of(int i, int NP) {
 template <int PN>
 __device__ __forceinline__ void produce_residual(const CUtensorMap* tm, uint8_t* ring,
                                                  uint64_t* full, uint64_t* empty, int depth,
-                                                 int N, int m0) {
+                                                 int N, int m0, int rot = 0) {
   constexpr int BPP = PN / 64;  // boxes per piece
   const int NP = N / PN;
   for (int b = 0; b < NP * BPP; ++b) {
     const int slot = b % depth;
     mbar_wait(&empty[slot], ((b / depth) & 1) ^ 1);
     mbar_arrive_expect_tx(&full[slot], kBox);
-    tma_load_2d(tm, &full[slot], ring + slot * kBox, piece_of(b / BPP, NP) * PN + (b % BPP) * 64,
+    tma_load_2d(tm, &full[slot], ring + slot * kBox, piece_of(b / BPP, NP, rot) * PN + (b % BPP) * 64,
                 m0);
   }
 }
@@ -107,7 +115,7 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
                                     const CUtensorMap* tmY, int m0, float* gb_smem,
                                     uint32_t out_stage, uint64_t* acc_full, uint64_t* acc_empty,
                                     uint32_t bar_id, uint32_t acc_empty_leader = 0,
-                                    bf16* sum_out = nullptr, int rows = 0) {
+                                    bf16* sum_out = nullptr, int rows = 0, int rot = 0) {
   static_assert(PN == 64 || PN == 128, "piece width");
   constexpr int CPT = PN / 64;  // 32-column chunks per thread per piece
   const uint32_t loff = (quad * 32) << 16;
@@ -115,7 +123,7 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
 
   float2 shift = make_float2(0.0f, 0.0f), S1 = shift, S2 = shift;
   for (int i = 0; i < NP; ++i) {
-    const int q = piece_of(i, NP);
+    const int q = piece_of(i, NP, rot);
     const uint32_t acc = PN == 64 ? (i & 1) : 0;
     const uint32_t par = PN == 64 ? ((i >> 1) & 1) : (i & 1);
 #ifdef LN_TRACE
@@ -230,7 +238,7 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
   // half).
   const int ht = et & 127;  // thread index within the half (PN = 128)
   for (int i = 0; i < NP; ++i) {
-    const int q = piece_of(i, NP);
+    const int q = piece_of(i, NP, rot);
     uint32_t box;
     if (PN == 64) {
       box = out_stage + (i & 1) * kBox;

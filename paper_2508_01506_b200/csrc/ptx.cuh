@@ -56,6 +56,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// One non-blocking probe of the phase (test_wait: returns at once).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// For a warp that idles through a long phase (e.g. a tail-only producer
+// waiting out the whole main loop): polls with a sleep in between, so it
+// takes no issue slots or shared-memory cycles from the warps doing the work.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_test(bar, parity)) __nanosleep(ns);
+}
 
 // ---------------------------------------------------------------- PDL
 // Programmatic dependent launch: a kernel launched with launch_pdl() may start
@@ -67,6 +85,21 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// ---------------------------------------------------------------- CTA timeline (trace builds)
+// FSVD_TRACE only: thread 0 of every CTA stamps %globaltimer (ns, comparable
+// across SMs) at kernel entry, after pdl_wait and at exit, plus its SM id,
+// into a per-translation-unit array copied out by fsvd_debug_cta_times_<tu>.
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
 
 // ---------------------------------------------------------------- fences
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -567,6 +567,9 @@ size_t op_transient_elems(const Pack& p, int op, int mode) {
 }
 
 namespace {
+// 128-row tiles per sequence for the kernels' loop rotation (ln_epi.cuh
+// piece_of, FfnTcArgs::seq_tiles); 0 when tiles straddle sequences.
+int seq_tiles_of(size_t M) { return M % 128 == 0 ? static_cast<int>(M / 128) : 0; }
 // Fused post-LN tensor-core schedule (layer_fwd): rank-space attention output
 // A [T, H*rp], LN1 output B [T, d], transient QKV / FFN-V1 region; A holds a
 // [T, d] FFN output instead when the FFN cannot take its LN fused.
@@ -1058,6 +1061,7 @@ void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* o
     a.act = p.act;
     a.out = as<bf16>(out);
     if (mode == FSVD_MODE_FLASH_V2 && !p.ffn_wide) {
+      a.seq_tiles = seq_tiles_of(M);
       if (use_ffn_pair(p, T)) ffn_fused_pair_bf16(a, s);
       else ffn_fused_bf16(a, s);
     } else {
@@ -1099,6 +1103,7 @@ bool ffn_resid_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, c
   a.out = as<bf16>(out);
   if (mode == FSVD_MODE_FLASH_V2 && !p.ffn_wide) {
     a.resid = as<bf16>(resid);
+    a.seq_tiles = seq_tiles_of(M);
     ffn_fused_bf16(a, s);
     return true;
   }
@@ -1138,6 +1143,7 @@ bool ffn_ln_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void
     a.ln_g = p.ln2g;
     a.ln_b = p.ln2b;
     a.ln_eps = p.eps2;
+    a.seq_tiles = seq_tiles_of(M);
     if (use_ffn_pair(p, T)) ffn_fused_pair_bf16(a, s);
     else ffn_fused_bf16(a, s);
     return true;
@@ -1161,7 +1167,7 @@ bool ffn_ln_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void
   a.z_out = Z;
   ffn_stream_bf16(a, s);
   gemm_ln_bf16(Z, p.frp, a.dn_v_t, p.frp, p.bdn, as<bf16>(x), p.ln2g, p.ln2b, p.eps2,
-               as<bf16>(out), T, d, p.frp, s);
+               as<bf16>(out), T, d, p.frp, s, nullptr, seq_tiles_of(M));
   return true;
 }
 
@@ -1337,14 +1343,14 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
       attn_rankspace_bf16(a, s);
     }
     gemm_ln_bf16(as<bf16>(A), hr, as<bf16>(p.wov_t), hr, p.bov, as<bf16>(x), p.ln1g, p.ln1b,
-                 p.eps1, as<bf16>(out), rows, p.d, hr, s);
+                 p.eps1, as<bf16>(out), rows, p.d, hr, s, nullptr, seq_tiles_of(M));
     if (!ffn_ln_fwd(p, mode, B, M, out, out, A, s))
       fail(Kind::Config, "compact post-LN schedule without a fused FFN LayerNorm");
   } else if (!pre_ln && fused_post_ln(p, mode)) {
     // rank-space attention -> A; folded out-projection + residual + LN1 -> B
     tc_attention_rank(p, B, M, x, A, trans, s, am);
     gemm_ln_bf16(as<bf16>(A), p.H * p.rp, as<bf16>(p.wov_t), p.H * p.rp, p.bov, as<bf16>(x),
-                 p.ln1g, p.ln1b, p.eps1, as<bf16>(Bb), rows, p.d, p.H * p.rp, s);
+                 p.ln1g, p.ln1b, p.eps1, as<bf16>(Bb), rows, p.d, p.H * p.rp, s, nullptr, seq_tiles_of(M));
     if (!ffn_ln_fwd(p, mode, B, M, Bb, out, trans, s)) {              // out = LN2(B + ffn(B))
       ffn_fwd(p, mode, B, M, Bb, A, trans, s);
       ln(p, Bb, A, p.ln2g, p.ln2b, p.eps2, out, rows, s);
@@ -1363,7 +1369,7 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
     if (!link.ln1_done) ln(p, x, nullptr, p.ln1g, p.ln1b, p.eps1, A, rows, s);  // normed -> A
     tc_attention_rank(p, B, M, A, Bb, trans, s, am);                  // O_rank  -> B
     gemm_ln_bf16(as<bf16>(Bb), hr, as<bf16>(p.wov_t), hr, p.bov, as<bf16>(x), p.ln2g, p.ln2b,
-                 p.eps2, as<bf16>(A), rows, p.d, hr, s, as<bf16>(out));  // LN2 -> A, s -> out
+                 p.eps2, as<bf16>(A), rows, p.d, hr, s, as<bf16>(out), seq_tiles_of(M));  // LN2 -> A, s -> out
     if (link.next && mode == FSVD_MODE_FLASH_V1) {
       // V1: P = A U_up, K3 stream -> Z, then Z V_down + b on the LN kernel:
       // s + ffn -> out and the next layer's LN1 -> A
@@ -1387,7 +1393,7 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
       ffn_stream_bf16(a, s);
       gemm_ln_bf16(Z, p.frp, as<bf16>(p.vdn_t), p.frp, p.bdn, as<bf16>(out), link.next->ln1g,
                    link.next->ln1b, link.next->eps1, as<bf16>(A), rows, p.d, p.frp, s,
-                   as<bf16>(out));
+                   as<bf16>(out), seq_tiles_of(M));
     } else if (link.next) {
       FfnTcArgs a{};
       a.T = rows;
@@ -1408,6 +1414,7 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
       a.ln_eps = link.next->eps1;
       a.ln_resid = as<bf16>(out);          // s
       a.sum_out = as<bf16>(out);           // s + ffn: the residual stream
+      a.seq_tiles = seq_tiles_of(M);
       ffn_fused_bf16(a, s);
     } else {
       ffn_resid_fwd(p, mode, B, M, A, out, out, trans, s);            // s + ffn -> out
