@@ -596,8 +596,11 @@ struct WsLayout {
 // The FFN V1 chain's P | Z reuse A and the transient.
 int qkv_chunks(size_t B) {
   static const int env = [] {
-    const char* e = getenv("FSVD_QKV_CHUNKS");  // developer switch (memory / speed sweep)
-    return e ? atoi(e) : 2;
+    // memory / speed knob: 1 (default) holds [P_k | P_v] for the whole batch;
+    // n > 1 runs K1 + K2 over n chunks of sequences (transient / n, at the
+    // cost of n - 1 more kernel ramps per layer: ~5% at cfg2 for n = 2)
+    const char* e = getenv("FSVD_QKV_CHUNKS");
+    return e ? atoi(e) : 1;
   }();
   const int c = env < 1 ? 1 : env;
   return static_cast<int>(std::min<size_t>(B, static_cast<size_t>(c)));

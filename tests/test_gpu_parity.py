@@ -404,52 +404,63 @@ def test_model_in_place_equals_out_of_place(L, ora, pre_ln):
         L.fsvd_layer_pack_destroy(p)
 
 
+_COMPACT_SCRIPT = r"""
+import ctypes as C, os, sys, numpy as np, torch
+sys.path.insert(0, os.environ["ROOT"]); sys.path.insert(0, os.path.join(os.environ["ROOT"], "tests"))
+import oracle, helpers as H
+from paper_2508_01506_b200 import abi
+from paper_2508_01506_b200.model import bf16_round, layer_descs, round_layer_bf16
+mode, chunks = int(sys.argv[1]), int(os.environ["FSVD_QKV_CHUNKS"])
+L = abi.lib(); ora = oracle.Restatement()
+layers = [round_layer_bf16(oracle.rand_layer(ora, 256, 1024, 4, 4, 32, 90 + i, 64, 128)) for i in range(2)]
+B, M, d, hr, kvw = 3, 200, 256, 4 * 32, 2 * 4 * 32
+descs = layer_descs(layers); packs = []
+for i in range(2):
+    p = C.c_void_p(); abi.check(L.fsvd_layer_pack_create(C.byref(descs[i]), abi.BF16, 0, C.byref(p))); packs.append(p)
+parr = (C.c_void_p * 2)(*[p.value for p in packs])
+ws = C.c_size_t(); abi.check(L.fsvd_workspace_bytes_ln(parr, 2, B, M, mode, 0, C.byref(ws)))
+up = lambda n: (n + 255) // 256 * 256
+cb = (B + chunks - 1) // chunks
+a, t = up(B * M * hr * 2), up(cb * M * kvw * 2)
+if mode == abi.MODE_FLASH_V1:
+    t = max(t, up(2 * B * M * 128 * 2) - a)
+assert ws.value == a + t + 256, (ws.value, a + t + 256)
+s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+x = torch.from_numpy(bf16_round(ora.random((B, M, d), 91))).cuda().to(torch.bfloat16)
+work = torch.empty(ws.value, dtype=torch.uint8, device="cuda"); out = torch.empty_like(x)
+abi.check(L.fsvd_model_fwd(parr, 2, mode, 0, B, M, C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()),
+                           C.c_void_p(work.data_ptr()), ws.value, s))
+for b in range(B):
+    ws1 = C.c_size_t(); abi.check(L.fsvd_workspace_bytes_ln(parr, 2, 1, M, mode, 0, C.byref(ws1)))
+    w1 = torch.empty(ws1.value, dtype=torch.uint8, device="cuda"); y = x[b:b + 1].clone()
+    abi.check(L.fsvd_model_fwd(parr, 2, mode, 0, 1, M, C.c_void_p(y.data_ptr()), C.c_void_p(y.data_ptr()),
+                               C.c_void_p(w1.data_ptr()), ws1.value, s))
+    torch.cuda.synchronize()
+    assert torch.equal(y[0], out[b]), f"sequence {b} differs from its single-sequence run"
+ref = ora.run_model(x.float().cpu().numpy(), layers, mode, abi.TilePlan(16, 16, 64, 1 << 22))
+err = H.rel_err(out.float().cpu().numpy(), ref)
+assert err <= H.TOL_BF16, err
+print("OK", chunks, mode, err)
+"""
+
+
+@pytest.mark.parametrize("chunks", [1, 2, 3])
 @pytest.mark.parametrize("mode", [abi.MODE_FLASH_V1, abi.MODE_FLASH_V2], ids=["v1", "v2"])
-def test_compact_post_ln_workspace_and_chunks(L, ora, mode):
+def test_compact_post_ln_workspace_and_chunks(mode, chunks):
     """The compact post-LN schedule (runtime.cu ws_layout): the workspace is
-    Qt/O [T, H*rp] plus one chunk of [P_k | P_v] rows (V1: at least P | Z),
-    K1 + K2 run per chunk of sequences -- an odd batch splits 2 + 1 -- and
-    the result equals, bit for bit, each sequence run alone (B = 1, one
-    chunk) and, within the bf16 bound, the oracle."""
-    import torch
-    layers = [round_layer_bf16(oracle.rand_layer(ora, 256, 1024, 4, 4, 32, 90 + i, 64, 128))
-              for i in range(2)]
-    B, M, d, hr, kvw = 3, 200, 256, 4 * 32, 2 * 4 * 32
-    descs = layer_descs(layers)
-    packs = []
-    for i in range(2):
-        p = C.c_void_p()
-        abi.check(L.fsvd_layer_pack_create(C.byref(descs[i]), abi.BF16, 0, C.byref(p)))
-        packs.append(p)
-    parr = (C.c_void_p * 2)(*[p.value for p in packs])
-    ws = C.c_size_t()
-    abi.check(L.fsvd_workspace_bytes_ln(parr, 2, B, M, mode, 0, C.byref(ws)))
-    up = lambda n: (n + 255) // 256 * 256  # noqa: E731
-    a, t = up(B * M * hr * 2), up(2 * M * kvw * 2)
-    if mode == abi.MODE_FLASH_V1:
-        t = max(t, up(2 * B * M * 128 * 2) - a)
-    assert ws.value == a + t + 256
-    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-    x = torch.from_numpy(bf16_round(ora.random((B, M, d), 91))).cuda().to(torch.bfloat16)
-    work = torch.empty(ws.value, dtype=torch.uint8, device="cuda")
-    out = torch.empty_like(x)
-    abi.check(L.fsvd_model_fwd(parr, 2, mode, 0, B, M, C.c_void_p(x.data_ptr()),
-                               C.c_void_p(out.data_ptr()), C.c_void_p(work.data_ptr()), ws.value, s))
-    for b in range(B):
-        ws1 = C.c_size_t()
-        abi.check(L.fsvd_workspace_bytes_ln(parr, 2, 1, M, mode, 0, C.byref(ws1)))
-        w1 = torch.empty(ws1.value, dtype=torch.uint8, device="cuda")
-        y = x[b:b + 1].clone()
-        abi.check(L.fsvd_model_fwd(parr, 2, mode, 0, 1, M, C.c_void_p(y.data_ptr()),
-                                   C.c_void_p(y.data_ptr()), C.c_void_p(w1.data_ptr()),
-                                   ws1.value, s))
-        torch.cuda.synchronize()
-        assert torch.equal(y[0], out[b]), f"sequence {b} differs from its single-sequence run"
-    ref = ora.run_model(x.float().cpu().numpy(), layers, mode, PLAN)
-    got = out.float().cpu().numpy()
-    assert H.rel_err(got, ref) <= H.TOL_BF16
-    for p in packs:
-        L.fsvd_layer_pack_destroy(p)
+    Qt/O [T, H*rp] plus one chunk of [P_k | P_v] rows (V1: at least P | Z);
+    with FSVD_QKV_CHUNKS = n, K1 + K2 run over n chunks of sequences -- an odd
+    batch splits 2 + 1 -- and the result equals, bit for bit, each sequence
+    run alone (B = 1, one chunk) and, within the bf16 bound, the oracle.  Runs
+    in a subprocess (the chunk count is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FSVD_QKV_CHUNKS=str(chunks), ROOT=root)
+    r = subprocess.run([sys.executable, "-c", _COMPACT_SCRIPT, str(mode)], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
 # ------------------------------------------------------------------ full-size properties (cfg2)
