@@ -20,6 +20,8 @@
 //
 // Warps: 0 and 11 TMA producers, 1 MMA issuer (leader) + TMEM owner, 2..9
 // epilogue, 10 residual producer of the fused LN.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "ln_epi.cuh"
@@ -124,7 +126,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
            const __grid_constant__ CUtensorMap tmY,    // out [T, d]      box 128 x 64 (LN)
            const float* __restrict__ b_up, const float* __restrict__ b_dn, int act, int T,
            int d_model, int d_ff, bf16* out, const float* __restrict__ ln_g,
-           const float* __restrict__ ln_b, float ln_eps) {
+           const float* __restrict__ ln_b, float ln_eps, int seq_pairs) {
   if (threadIdx.x == 0) TRACE2(0);
   using C = Ffn2Cfg<FR>;
   extern __shared__ uint8_t smem_raw[];
@@ -139,6 +141,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const bool fuse_ln = ln_g != nullptr;
   const int QS = fuse_ln ? 64 : 128;  // output columns per piece (pair MMA N)
   const int NQ = d_model / QS;
+  // loop rotation by the pair tile's place in its sequence (as k_ffn,
+  // FfnTcArgs::seq_tiles): both CTAs of the pair use the same offsets
+  const int rpos = seq_pairs > 1 ? static_cast<int>(blockIdx.x >> 1) % seq_pairs : 0;
+  const int rdiv = seq_pairs > 1 ? seq_pairs : 1;
+  const int rot = rpos * NB / rdiv, rotk = rpos * KC / rdiv;
+  const int rotq = fuse_ln ? rpos * NQ / rdiv : 0;
+  auto blk = [&](int f) { const int b = f + rot; return b >= NB ? b - NB : b; };
+  auto kch = [&](int kc) { const int k = kc + rotk; return k >= KC ? k - KC : k; };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmX);
@@ -176,6 +186,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   pdl_trigger();
   pdl_wait();
+  if (threadIdx.x == 0) TRACE2(6);
   const uint32_t tmem = bars->tmem;
   uint8_t* ring = smem + C::o_ring;
 
@@ -205,21 +216,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (static_cast<uint32_t>(xb) == me) {
           mbar_wait(&bars->x_empty[xb], ((kc >> 1) & 1) ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&bars->x_full[xb], 2 * ATOM);
-          tma_load_2d_pair(&tmX, &bars->x_full[xb], smem + C::o_h + xb * ATOM, kc * 64, m0);
+          tma_load_2d_pair(&tmX, &bars->x_full[xb], smem + C::o_h + xb * ATOM, kch(kc) * 64, m0);
         }
         emit(C::NPIECE, [&](int p, uint8_t* dst) {
-          tma_load_2d_pair(&tmUup, &bars->full[st], dst, kc * 64, p * C::PS + hr);
+          tma_load_2d_pair(&tmUup, &bars->full[st], dst, kch(kc) * 64, p * C::PS + hr);
         }, HSLOT);
       }
       auto mma1_slots = [&](int f) {
         emit(C::NATOM, [&](int a, uint8_t* dst) {
-          tma_load_2d_pair(&tmVup, &bars->full[st], dst, a * 64, f * BF + hr);
+          tma_load_2d_pair(&tmVup, &bars->full[st], dst, a * 64, blk(f) * BF + hr);
         }, HSLOT);
       };
       auto mma2_slots = [&](int f) {  // atom-major: (a0: p0..), (a1: p0..)
         emit(2 * C::NPIECE, [&](int j, uint8_t* dst) {
           const int a = j / C::NPIECE, p = j % C::NPIECE;
-          tma_load_2d_pair(&tmUdn, &bars->full[st], dst, f * BF + a * 64, p * C::PS + hr);
+          tma_load_2d_pair(&tmUdn, &bars->full[st], dst, blk(f) * BF + a * 64, p * C::PS + hr);
         }, HSLOT);
       };
       mma1_slots(0);
@@ -231,7 +242,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       for (int q = 0; q < NQ; ++q)
         emit(C::NATOM, [&](int a, uint8_t* dst) {
-          tma_load_2d_pair(&tmVdn, &bars->full[st], dst, a * 64, q * QS + static_cast<int>(rank) * (QS / 2));
+          tma_load_2d_pair(&tmVdn, &bars->full[st], dst, a * 64,
+                           lnepi::piece_of(q, NQ, rotq) * QS + static_cast<int>(rank) * (QS / 2));
         }, (QS / 2) * 128);
     }
     __syncwarp();
@@ -245,14 +257,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int f = 0; f < NB; ++f)
         for (int a = 0; a < 2; ++a) {
           mbar_wait(&bars->sh_loc[a], f & 1);
-          mbar_arrive_cluster(mapa_shared(smem_u32(&bars->sh_full[a]), 0));
+          TRACE2(3000 + f * 4 + a * 2);
+          mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&bars->sh_full[a]), 0));
+          TRACE2(3001 + f * 4 + a * 2);
         }
     }
     __syncwarp();
     if (fuse_ln && lane == 0) {
       mbar_wait(&bars->z_full, 0);
       lnepi::produce_residual<64>(&tmX, smem + C::o_h, bars->res_full, bars->res_empty, 2,
-                                  d_model, m0);
+                                  d_model, m0, rotq);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -300,6 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         commit(&bars->x_empty[xb]);
       }
       commit(&bars->p_acc);
+      TRACE2(7);
       mbar_wait(&bars->p_ready, 0);
       tc_fence_after();
       auto mma1 = [&](int f) {
@@ -369,6 +384,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_before();
     warp_arrive_leader(&bars->p_ready);
     for (int f = 0; f < NB; ++f) {
+      float bb[2][32];  // b_up of this block, fetched while the MMA runs
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int fb = blk(f) * BF + (half + 2 * i) * 32;
+        load_bias<32>(bb[i], b_up + fb, d_ff - fb);
+      }
       if (threadIdx.x == 64) TRACE2(1024 + f * 8 + 0);
       mbar_wait(&bars->h_full, f & 1);
       tc_fence_after();
@@ -378,12 +399,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int i = 0; i < 2; ++i) ld_chunk(tmem + C::t_h + loff + (half + 2 * i) * 32, v[i]);
       tc_fence_before();
       warp_arrive_leader_relaxed(&bars->h_free);
-      float bb[2][32];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int fb = f * BF + (half + 2 * i) * 32;
-        load_bias<32>(bb[i], b_up + fb, d_ff - fb);
-      }
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         bias_act_chunk2<32>(v[i], bb[i], act);
@@ -412,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                      bars->res_full, bars->res_empty, 2, ln_g, ln_b, ln_eps, &tmY, m0,
                      reinterpret_cast<float*>(ring), smem_u32(smem + C::o_h), bars->o_full,
                      bars->o_free, 1,
-                     mapa_shared(smem_u32(&bars->o_free[0]), 0));
+                     mapa_shared(smem_u32(&bars->o_free[0]), 0), nullptr, 0, rotq);
     } else {
       for (int q = 0; q < NQ; ++q) {
         mbar_wait(&bars->o_full[q & 1], (q >> 1) & 1);
@@ -438,6 +453,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+bool ffn_pair_rotation() {
+  static const bool on = [] {
+    const char* e = getenv("FSVD_FFN_ROT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int FR>
 void launch_ffn2(const FfnTcArgs& a, cudaStream_t s) {
   using C = Ffn2Cfg<FR>;
@@ -458,7 +481,8 @@ void launch_ffn2(const FfnTcArgs& a, cudaStream_t s) {
       ln ? tmap_bf16(a.out, a.T, a.d_model, a.d_model, BMr, 64, TmaSwizzle::B128) : tx;
   const int pairs = (a.T + 2 * BMr - 1) / (2 * BMr);
   launch_pdl(k_ffn2<FR>, dim3(2 * pairs), dim3(kThreads), C::SMEM, s, tx, tup, tvup, tudn, tvdn,
-             ty, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff, a.out, a.ln_g, a.ln_b, a.ln_eps);
+             ty, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff, a.out, a.ln_g, a.ln_b, a.ln_eps,
+             ffn_pair_rotation() && a.seq_tiles % 2 == 0 ? a.seq_tiles / 2 : 0);
   check_launch("k_ffn2");
 }
 

@@ -248,12 +248,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t me = warp == 0 ? 0 : 1;
       uint32_t st = 0, ph = 0, it = 0;
+#ifdef FSVD_FFN_EXP
+      bool exp_stream = false;  // developer experiment builds only
+#endif
       // Streams n slots, two per stage.  slot(i, dst, size_only) returns the
       // byte count of slot i and, unless size_only, issues its TMA.
       auto emit = [&](int n, auto&& slot) {
         for (int i = 0; i < n; i += 2, ++it) {
           if ((it & 1) == me) {
             mbar_wait(&bars->empty[st], ph ^ 1);
+#ifdef FSVD_FFN_EXP
+            if (FSVD_FFN_EXP == 1 && exp_stream) {  // no refill: MMAs reuse stale stages
+              mbar_arrive(&bars->full[st]);
+              if (++st == C::STAGES) { st = 0; ph ^= 1; }
+              continue;
+            }
+#endif
             uint8_t* base = ring + st * STAGE;
             uint32_t bytes = slot(i, base, true);
             if (i + 1 < n) bytes += slot(i + 1, base + SLOT, true);
@@ -333,12 +343,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       TRACE(2);
       mma1_slots(0);
+#ifdef FSVD_FFN_EXP
+      exp_stream = true;
+#endif
       for (int f = 0; f < NB; ++f) {
         TRACE(2048 + f * 2);
         if (f + 1 < NB) mma1_slots(f + 1);
         TRACE(2048 + f * 2 + 1);
         mma2_slots(f);
       }
+#ifdef FSVD_FFN_EXP
+      exp_stream = false;
+#endif
       if (FUSED) {
         for (int q = 0; q < NQ; ++q)
           emit(C::NATOM, [&](int a, uint8_t* dst, bool size_only) -> uint32_t {
@@ -567,6 +583,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (threadIdx.x == 64) TRACE(1024 + f * 8 + 2 + i * 2);
         if (f > 0) mbar_wait(&bars->sh_free[i], (f - 1) & 1);
         if (threadIdx.x == 64) TRACE(1024 + f * 8 + 3 + i * 2);
+#ifdef FSVD_FFN_EXP
+        if (FSVD_FFN_EXP != 2)
+#endif
         st_chunk_smem(s_h, row, (half + 2 * i) * 32, v[i]);
         if (X3) {  // mid and lo planes of the activated block, atoms 2..3 and 4..5
 #pragma unroll

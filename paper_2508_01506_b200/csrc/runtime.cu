@@ -991,10 +991,13 @@ bool pre_ln_unfused() {
   return v;
 }
 
+// V2 FFN on the CTA-pair kernel (ffn2_tc.cu): the default for the plain and
+// the post-LN fused FFN (the pre-LN residual / chained-LN forms run k_ffn);
+// FSVD_FFN_PAIR=0 selects the single-CTA kernel (developer A/B switch).
 bool use_ffn_pair(const Pack& p, int T) {
   static const bool enabled = [] {
     const char* e = getenv("FSVD_FFN_PAIR");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return enabled && T >= 256 && ffn_pair_supported(p.d, p.df, p.frp);
 }
@@ -1089,7 +1092,6 @@ bool ffn_resid_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, c
                    void* out, void* trans, cudaStream_t s) {
   const int T = static_cast<int>(B * M), d = p.d;
   if (!p.ffn_tc || !(mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2)) return false;
-  if (mode == FSVD_MODE_FLASH_V2 && use_ffn_pair(p, T)) return false;
   FfnTcArgs a{};
   a.T = T;
   a.d_model = d;
@@ -1259,7 +1261,6 @@ namespace {
 bool pre_ln_fused(const Pack& p, int mode, size_t T) {
   return p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16 && p.d == p.dr &&
          (mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2) && !p.ffn_wide &&
-         !(mode == FSVD_MODE_FLASH_V2 && use_ffn_pair(p, static_cast<int>(T))) &&
          gemm_ln_supported(p.d, p.H * p.rp) && !pre_ln_unfused();
 }
 // Layer p can apply q's LN1 in its FFN epilogue (ln_epi.cuh shape range).
@@ -1424,7 +1425,7 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
     }
   } else if (p.attn_tc && p.out_tc && p.dtype == FSVD_BF16 &&
              (mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2) &&
-             !(mode == FSVD_MODE_FLASH_V2 && use_ffn_pair(p, T)) && p.ffn_tc) {
+             p.ffn_tc) {
     // pre-LN, tensor-core path: both residual adds ride in GEMM epilogues
     const int hr = p.H * p.rp;
     ln(p, x, nullptr, p.ln1g, p.ln1b, p.eps1, A, rows, s);            // normed  -> A

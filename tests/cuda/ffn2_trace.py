@@ -23,9 +23,10 @@ x = torch.randn((16384, 768), device="cuda").to(torch.bfloat16)
 out = torch.empty_like(x)
 work = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-for _ in range(3):
-    abi.check(L.fsvd_ffn_fwd(p, 2, 32, 512, C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()),
-                             C.c_void_p(work.data_ptr()), work.numel(), sp))
+for _ in range(3):  # one post-LN layer: the pair FFN with the fused LN2, as in the model
+    abi.check(L.fsvd_layer_fwd(p, abi.MODE_FLASH_V2, 0, 32, 512, C.c_void_p(x.data_ptr()),
+                               C.c_void_p(out.data_ptr()), C.c_void_p(work.data_ptr()),
+                               work.numel(), sp))
 torch.cuda.synchronize()
 buf = (C.c_longlong * 8192)()
 L.fsvd_debug_trace2_copy.argtypes = [C.POINTER(C.c_longlong), C.c_int]
@@ -33,6 +34,7 @@ L.fsvd_debug_trace2_copy(buf, 8192)
 t = np.array(buf[:], dtype=np.int64)
 t0 = t[0]
 rel = lambda v: int(v - t0) if v else -1  # noqa: E731
+print(f"pdl released {rel(t[6])}, P issued (p_acc commit) {rel(t[7])}")
 print(f"pair fr={fr} act={act}: leader start 0, mma thread end {rel(t[1])}, epi end {rel(t[5])}; "
       f"z_full committed {rel(t[2])} zs_ready {rel(t[3])}; peer end {rel(t[4096 + 1])}")
 print(" f | L mma1 start  h_free ok  issued | sh_full0 w->ok | sh_full1 w->ok || epi0 h_full w->ok | shfree0 | shfree1 || epi1 h_full w->ok")
@@ -42,3 +44,6 @@ for f in range(24):
     e1 = [rel(t[4096 + 1024 + f * 8 + i]) for i in range(2)]
     print(f"{f:2d} | {m[0]:8d} {m[1]:8d} {m[2]:8d} | {m[3]:8d} {m[4]:8d} | {m[5]:8d} {m[6]:8d} || "
           f"{e[0]:8d} {e[1]:8d} | {e[2]:8d} {e[3]:8d} | {e[4]:8d} {e[5]:8d} || {e1[0]:8d} {e1[1]:8d}")
+print("relay (leader / peer): sh_loc complete -> remote arrive done, per atom")
+for f in (0, 1, 2, 10, 21, 22, 23):
+    print(f, [(rel(t[c + 3000 + f * 4 + a * 2]), rel(t[c + 3001 + f * 4 + a * 2])) for c in (0, 4096) for a in (0, 1)])
