@@ -393,6 +393,14 @@ fsvd_status fsvd_outproj_fwd(const fsvd_layer_pack* p, size_t batch, size_t seq,
 fsvd_status fsvd_ffn_fwd(const fsvd_layer_pack* p, int variant, size_t batch, size_t seq,
                          const void* x, void* out, void* workspace,
                          size_t workspace_bytes, void* stream);
+/* Post-LN FFN sublayer: out = LN2(x + ffn(x)), the second half of run_layer
+ * (encoder.cpp:245-256; ffn_v1 / ffn_v2 then residual_norm).  On the tensor
+ * cores this is one kernel for variant 2 (K4 with its LayerNorm epilogue). */
+fsvd_status fsvd_ffn_block_workspace_bytes(const fsvd_layer_pack* p, int variant, size_t batch,
+                                           size_t seq, size_t* bytes);
+fsvd_status fsvd_ffn_block_fwd(const fsvd_layer_pack* p, int variant, size_t batch, size_t seq,
+                               const void* x, void* out, void* workspace,
+                               size_t workspace_bytes, void* stream);
 /* encoder.cpp:224-260 (run_layer).  x and out may alias. */
 fsvd_status fsvd_layer_fwd(const fsvd_layer_pack* p, fsvd_run_mode mode, int pre_ln,
                            size_t batch, size_t seq, const void* x, void* out,

@@ -145,6 +145,8 @@ def _declare(lib):
         "fsvd_attention_fwd": (st, [vp, _sz, _sz, vp, vp, vp, _sz, vp]),
         "fsvd_outproj_fwd": (st, [vp, _sz, _sz, vp, vp, vp, _sz, vp]),
         "fsvd_ffn_fwd": (st, [vp, C.c_int, _sz, _sz, vp, vp, vp, _sz, vp]),
+        "fsvd_ffn_block_workspace_bytes": (st, [vp, C.c_int, _sz, _sz, C.POINTER(_sz)]),
+        "fsvd_ffn_block_fwd": (st, [vp, C.c_int, _sz, _sz, vp, vp, vp, _sz, vp]),
         "fsvd_layer_fwd": (st, [vp, C.c_int, C.c_int, _sz, _sz, vp, vp, vp, _sz, vp]),
         "fsvd_model_fwd": (st, [P(vp), _sz, C.c_int, C.c_int, _sz, _sz, vp, vp, vp, _sz, vp]),
         "fsvd_model_file_probe": (st, [C.c_char_p, P(_sz), P(Geometry)]),

@@ -929,6 +929,24 @@ fsvd_status fsvd_ffn_fwd(const fsvd_layer_pack* p, int variant, size_t batch, si
     ffn_fwd(*p->p, mode, batch, seq, x, out, ws, static_cast<cudaStream_t>(stream));
   });
 }
+fsvd_status fsvd_ffn_block_workspace_bytes(const fsvd_layer_pack* p, int variant, size_t batch,
+                                           size_t seq, size_t* bytes) {
+  return guard([&] {
+    if (!p || !bytes) fail(Kind::Config, "null argument");
+    if (variant != 1 && variant != 2) fail(Kind::Config, "ffn variant must be 1 or 2");
+    *bytes = ffn_block_workspace_bytes(*p->p, batch, seq,
+                                       variant == 1 ? FSVD_MODE_FLASH_V1 : FSVD_MODE_FLASH_V2);
+  });
+}
+fsvd_status fsvd_ffn_block_fwd(const fsvd_layer_pack* p, int variant, size_t batch, size_t seq,
+                               const void* x, void* out, void* ws, size_t ws_bytes, void* stream) {
+  return guard([&] {
+    check_extents(batch, seq);
+    if (variant != 1 && variant != 2) fail(Kind::Config, "ffn variant must be 1 or 2");
+    ffn_block_fwd(*p->p, variant == 1 ? FSVD_MODE_FLASH_V1 : FSVD_MODE_FLASH_V2, batch, seq, x,
+                  out, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+  });
+}
 fsvd_status fsvd_layer_fwd(const fsvd_layer_pack* p, fsvd_run_mode mode, int pre_ln, size_t batch,
                            size_t seq, const void* x, void* out, void* ws, size_t ws_bytes,
                            void* stream) {

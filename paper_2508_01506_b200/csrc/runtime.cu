@@ -1444,6 +1444,26 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
   }
 }
 
+// Post-LN FFN sublayer: out = LN2(x + ffn(x)) (run_layer's second half,
+// encoder.cpp:245-256); the fused kernel (K4 with its LayerNorm epilogue, or
+// the V1 chain ending in K6) when the shape allows, else FFN then K5.
+size_t ffn_block_workspace_bytes(const Pack& p, size_t B, size_t M, int mode) {
+  const size_t T = B * M;
+  return align256(T * p.d * p.es) + align256(T * op_transient_elems(p, 2, mode) * p.es) + 256;
+}
+void ffn_block_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* out,
+                   void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (ws_bytes < ffn_block_workspace_bytes(p, B, M, mode))
+    fail(Kind::Config, "workspace too small for the FFN block");
+  const size_t T = B * M;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+  void* A = base;
+  void* trans = base + align256(T * p.d * p.es);
+  if (ffn_ln_fwd(p, mode, B, M, x, out, trans, s)) return;
+  ffn_fwd(p, mode, B, M, x, A, trans, s);
+  ln(p, x, A, p.ln2g, p.ln2b, p.eps2, out, static_cast<int>(T), s);
+}
+
 void check_decoder_pack(const Pack& p) {
   if (!(p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16 && p.d == p.dr))
     fail(Kind::Config, "decoder rows run on the bf16 tensor-core flash path (bf16 pack, "

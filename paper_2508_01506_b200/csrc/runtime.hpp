@@ -124,6 +124,9 @@ void attention_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, v
                    void* trans, cudaStream_t s);
 void outproj_fwd(const Pack& p, int mode, size_t B, size_t M, const void* ctx, void* out,
                  void* trans, cudaStream_t s);
+size_t ffn_block_workspace_bytes(const Pack& p, size_t B, size_t M, int mode);
+void ffn_block_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* out,
+                   void* ws, size_t ws_bytes, cudaStream_t s);
 void ffn_fwd(const Pack& p, int mode, size_t B, size_t M, const void* x, void* out, void* trans,
              cudaStream_t s);
 // Attention variant of a layer run: the encoder's full attention, or the

@@ -463,6 +463,39 @@ def test_compact_post_ln_workspace_and_chunks(mode, chunks):
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("B,M", [(2, 256), (1, 200), (3, 512)], ids=["pairs", "single", "rot"])
+def test_ffn_block_is_ffn_then_residual_norm(L, ora, variant, B, M):
+    """fsvd_ffn_block_fwd (the kernel the bench's roofline times: K4 with the
+    residual + LN2 epilogue, on the CTA pair when T >= 256) equals
+    LN2(x + fsvd_ffn_fwd(x)) computed in fp32 from the plain FFN op's output
+    (the bf16 sublayer value both paths round to), within the bf16 bound."""
+    import torch
+    layer = round_layer_bf16(oracle.rand_layer(ora, 768, 3072, 12, 12, 32, 123, 384, 384))
+    d = 768
+    descs = layer_descs([layer])
+    p = C.c_void_p()
+    abi.check(L.fsvd_layer_pack_create(C.byref(descs[0]), abi.BF16, 0, C.byref(p)))
+    x = torch.from_numpy(bf16_round(ora.random((B, M, d), 5))).cuda().to(torch.bfloat16)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    fb = C.c_size_t()
+    abi.check(L.fsvd_ffn_block_workspace_bytes(p, variant, B, M, C.byref(fb)))
+    work = torch.empty(max(fb.value, B * M * 4096 * 2), dtype=torch.uint8, device="cuda")
+    y = torch.empty_like(x)
+    abi.check(L.fsvd_ffn_block_fwd(p, variant, B, M, C.c_void_p(x.data_ptr()),
+                                   C.c_void_p(y.data_ptr()), C.c_void_p(work.data_ptr()), fb.value, s))
+    f = torch.empty_like(x)
+    abi.check(L.fsvd_ffn_fwd(p, variant, B, M, C.c_void_p(x.data_ptr()), C.c_void_p(f.data_ptr()),
+                             C.c_void_p(work.data_ptr()), work.numel(), s))
+    torch.cuda.synchronize()
+    sres = x.float() + f.float()
+    ref = torch.nn.functional.layer_norm(sres, (d,), torch.from_numpy(layer.ln2_gamma).cuda(),
+                                         torch.from_numpy(layer.ln2_beta).cuda(), layer.ln2_eps)
+    err = float((y.float() - ref).abs().max() / ref.abs().max())
+    assert err <= H.TOL_BF16, err
+    L.fsvd_layer_pack_destroy(p)
+
+
 # ------------------------------------------------------------------ full-size properties (cfg2)
 def test_cfg2_full_size_properties(L, ora):
     """BERT-Base B=32 M=512 bf16 (BASELINE configs[1], 2 of the 12 layers):
