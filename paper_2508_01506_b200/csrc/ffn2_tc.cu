@@ -64,6 +64,7 @@ struct Ffn2Bars {
   uint64_t sh_loc[2];  // this CTA's epilogue warps -> relay (local, no cluster fence)
   uint64_t o_full[2], o_free[2];
   uint64_t res_full[2], res_empty[2];
+  uint64_t box_full[2], box_free[2];  // LN output boxes (ln_epi.cuh store_boxes)
   uint32_t tmem;
 };
 static_assert(sizeof(Ffn2Bars) <= 1024, "barrier block");
@@ -171,6 +172,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&bars->o_free[i], 2 * kEpiWarps);
       mbar_init(&bars->res_full[i], 1);
       mbar_init(&bars->res_empty[i], lnepi::res_box_readers<64>());
+      mbar_init(&bars->box_full[i], lnepi::box_writer_warps<64>());
+      mbar_init(&bars->box_free[i], 1);
     }
     mbar_init(&bars->p_acc, 1);
     mbar_init(&bars->p_ready, 2 * kEpiWarps);
@@ -267,6 +270,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->z_full, 0);
       lnepi::produce_residual<64>(&tmX, smem + C::o_h, bars->res_full, bars->res_empty, 2,
                                   d_model, m0, rotq);
+      lnepi::store_boxes<64>(&tmY, smem_u32(smem + C::o_h), bars->box_full, bars->box_free,
+                             d_model, m0, rotq);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -425,7 +430,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (fuse_ln) {
       lnepi::run<64>(tmem, quad, half, row, d_model, b_dn, smem_u32(smem + C::o_h),
                      bars->res_full, bars->res_empty, 2, ln_g, ln_b, ln_eps, &tmY, m0,
-                     reinterpret_cast<float*>(ring), smem_u32(smem + C::o_h), bars->o_full,
+                     reinterpret_cast<float*>(ring), smem_u32(smem + C::o_h), bars->box_full,
+                     bars->box_free, bars->o_full,
                      bars->o_free, 1,
                      mapa_shared(smem_u32(&bars->o_free[0]), 0), nullptr, 0, rotq);
     } else {

@@ -93,6 +93,7 @@ struct FfnBars {
   uint64_t p_full, p_acc, p_ready, h_full, h_free, sh_full[2], sh_free[2], z_full, zs_ready;
   uint64_t o_full[2], o_free[2];
   uint64_t res_full[2], res_empty[2];  // residual boxes of the fused LN2 (H region)
+  uint64_t box_full[2], box_free[2];   // its output boxes (ln_epi.cuh store_boxes)
   uint32_t tmem;
 };
 
@@ -219,6 +220,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars->o_free[i], kEpi);
       mbar_init(&bars->res_full[i], 1);
       mbar_init(&bars->res_empty[i], kEpi);
+      mbar_init(&bars->box_full[i], lnepi::box_writer_warps<64>());
+      mbar_init(&bars->box_free[i], 1);
     }
     mbar_init(&bars->p_full, 1);
     mbar_init(&bars->p_acc, 1);
@@ -374,6 +377,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait_sleep(&bars->z_full, 0, 256);
       lnepi::produce_residual<64>(&tmR, smem + C::o_h, bars->res_full, bars->res_empty, 2,
                                   d_model, m0, rotq);
+      lnepi::store_boxes<64>(&tmY, smem_u32(smem + C::o_h), bars->box_full, bars->box_free,
+                             d_model, m0, rotq);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -641,7 +646,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // gamma / beta are staged in the weight ring, idle once all MMAs are done
         lnepi::run<64>(tmem, quad, half, row, d_model, b_dn, smem_u32(smem + C::o_h),
                        bars->res_full, bars->res_empty, 2, ln_g, ln_b, ln_eps, &tmY, m0,
-                       reinterpret_cast<float*>(ring), smem_u32(smem + C::o_h), bars->o_full,
+                       reinterpret_cast<float*>(ring), smem_u32(smem + C::o_h), bars->box_full,
+                       bars->box_free, bars->o_full,
                        bars->o_free, 1, 0, sum_out, T, rotq);
       } else {
         for (int q = 0; q < NQ; ++q) {

@@ -74,6 +74,7 @@ namespace {
 struct LnBars {
   uint64_t full[kMaxStages], empty[kMaxStages];
   uint64_t a_full, acc_full[1], acc_empty[1], res_full[RS], res_empty[RS];
+  uint64_t box_full[4], box_free[4];  // second-sweep output boxes (ln_epi.cuh store_boxes)
   uint32_t tmem;
 };
 
@@ -115,6 +116,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < RS; ++i) {
       mbar_init(&bars->res_full[i], 1);
       mbar_init(&bars->res_empty[i], lnepi::res_box_readers<PN>());
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&bars->box_full[i], lnepi::box_writer_warps<PN>());
+      mbar_init(&bars->box_free[i], 1);
     }
     fence_barrier_init();
   }
@@ -206,9 +211,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       LTRACE(48 + q);
     }
   } else if (warp == 10) {
-    // ============================================ residual producer (one thread)
-    if (lane == 0)
+    // ============================================ residual producer, then the
+    // second sweep's store thread (one thread)
+    if (lane == 0) {
       lnepi::produce_residual<PN>(&tmR, rring, bars->res_full, bars->res_empty, RS, N, m0, rot);
+      lnepi::store_boxes<PN>(&tmY, smem_u32(ring), bars->box_full, bars->box_free, N, m0, rot);
+    }
     __syncwarp();
   } else {
     // ============================================ epilogue (8 warps)
@@ -219,7 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // region (both idle once every MMA has completed)
     lnepi::run<PN>(tmem, quad, half, row, N, bias, smem_u32(rring), bars->res_full,
                    bars->res_empty, RS, gamma, beta, eps, &tmY, m0, reinterpret_cast<float*>(sA),
-                   smem_u32(ring), bars->acc_full, bars->acc_empty, 1, 0, sum_out, T, rot);
+                   smem_u32(ring), bars->box_full, bars->box_free, bars->acc_full,
+                   bars->acc_empty, 1, 0, sum_out, T, rot);
   }
   if (threadIdx.x == 64) LTRACE(100);
   tc_fence_before();

@@ -94,6 +94,31 @@ __device__ __forceinline__ void produce_residual(const CUtensorMap* tm, uint8_t*
                 m0);
   }
 }
+// Output boxes of run()'s second sweep: one thread of an otherwise idle warp
+// issues the TMA store of every box as soon as its writers have arrived on
+// box_full[slot] (box_writer_warps() arrivals), and frees the slot once the
+// store has read it.  Box j = (piece j / BPP, 64-column half j % BPP), slot
+// j % (2 * BPP), in piece_of() order.
+template <int PN>
+constexpr int box_writer_warps() { return PN == 64 ? kEpiThreads / 32 : kEpiThreads / 64; }
+template <int PN>
+__device__ __forceinline__ void store_boxes(const CUtensorMap* tmY, uint32_t out_stage,
+                                            uint64_t* box_full, uint64_t* box_free, int N,
+                                            int m0, int rot = 0) {
+  constexpr int BPP = PN / 64;
+  constexpr int NBOX = 2 * BPP;
+  const int NP = N / PN;
+  for (int j = 0; j < NP * BPP; ++j) {
+    const int slot = j % NBOX;
+    mbar_wait(&box_full[slot], (j / NBOX) & 1);
+    tma_store_2d_u32(tmY, out_stage + slot * kBox, piece_of(j / BPP, NP, rot) * PN + (j % BPP) * 64,
+                     m0);
+    tma_store_commit();
+    tma_store_wait_read<1>();  // every store before box j has read its slot
+    if (j >= 1) mbar_arrive(&box_free[(j - 1) % NBOX]);
+  }
+  tma_store_wait<0>();
+}
 // Arrivals a residual box needs before it can be refilled.
 template <int PN>
 constexpr int res_box_readers() { return PN == 64 ? kEpiThreads : kEpiThreads / 2; }
@@ -113,7 +138,8 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
                                     const float* __restrict__ gamma,
                                     const float* __restrict__ beta, float eps,
                                     const CUtensorMap* tmY, int m0, float* gb_smem,
-                                    uint32_t out_stage, uint64_t* acc_full, uint64_t* acc_empty,
+                                    uint32_t out_stage, uint64_t* box_full, uint64_t* box_free,
+                                    uint64_t* acc_full, uint64_t* acc_empty,
                                     uint32_t bar_id, uint32_t acc_empty_leader = 0,
                                     bf16* sum_out = nullptr, int rows = 0, int rot = 0) {
   static_assert(PN == 64 || PN == 128, "piece width");
@@ -236,23 +262,18 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
   // alternate, 256-thread barriers); PN = 128: each half owns a box per piece
   // and alternates its own two boxes (128-thread barriers, ids bar_id + 1 +
   // half).
-  const int ht = et & 127;  // thread index within the half (PN = 128)
+  // Each finished [128 x 64] box is handed to the kernel's store thread
+  // (store_boxes, below) through box_full / box_free, so no epilogue thread
+  // waits on a TMA store instruction: box j of the sweep (piece j / BPP, half
+  // j % BPP) lives in staging slot j % (2 * BPP).
+  constexpr int BPP = PN / 64;
+  constexpr int NBOX = 2 * BPP;
   for (int i = 0; i < NP; ++i) {
     const int q = piece_of(i, NP, rot);
-    uint32_t box;
-    if (PN == 64) {
-      box = out_stage + (i & 1) * kBox;
-      if (i >= 2) {
-        if (et == 0) tma_store_wait_read<1>();
-        named_bar_sync(bar_id, kEpiThreads);
-      }
-    } else {
-      box = out_stage + (2 * half + (i & 1)) * kBox;
-      if (i >= 2) {
-        if (ht == 0) tma_store_wait_read<1>();
-        named_bar_sync(bar_id + 1 + half, kEpiThreads / 2);
-      }
-    }
+    const int j = PN == 64 ? i : 2 * i + static_cast<int>(half);
+    const int slot = j % NBOX;
+    const uint32_t box = out_stage + slot * kBox;
+    if (j >= NBOX) mbar_wait(&box_free[slot], ((j / NBOX) - 1) & 1);
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       const int col = q * PN + half * (PN / 2) + c * 32;
@@ -279,21 +300,9 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
 #ifdef LN_TRACE
     if (threadIdx.x == 64) LN_TRACE(310 + i);
 #endif
-    if (PN == 64) {
-      named_bar_sync(bar_id, kEpiThreads);
-      if (et == 0) {
-        tma_store_2d_u32(tmY, box, q * PN, m0);
-        tma_store_commit();
-      }
-    } else {
-      named_bar_sync(bar_id + 1 + half, kEpiThreads / 2);
-      if (ht == 0) {
-        tma_store_2d_u32(tmY, box, q * PN + half * 64, m0);
-        tma_store_commit();
-      }
-    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&box_full[slot]);
   }
-  if ((PN == 64 && et == 0) || (PN == 128 && ht == 0)) tma_store_wait<0>();
 #ifdef LN_TRACE
   if (threadIdx.x == 64) LN_TRACE(330);
 #endif
