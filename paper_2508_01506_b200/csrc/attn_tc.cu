@@ -67,7 +67,7 @@ __device__ __forceinline__ float ex2(float x) {
 // softmax is not bound by the 16/clk/SM MUFU rate alone (EMU_EVERY: one
 // pair of probabilities in EMU_EVERY takes the polynomial).
 #ifndef EMU_EVERY
-#define EMU_EVERY 4
+#define EMU_EVERY 3
 #endif
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   x.x = fmaxf(x.x, -125.0f);

@@ -585,6 +585,7 @@ struct WsLayout {
   size_t a, b, t;  // bytes of the A / B / transient regions (256-aligned)
   size_t total() const { return a + b + t + 256; }
   int chunks = 0;  // > 0: the compact fused post-LN layout (qkv_chunks)
+  bool unfused_compact = false;  // the compact post-LN layout with K5 LayerNorms
 };
 // Compact fused post-LN layout (both LayerNorms fused, full attention): the
 // LN1 output goes straight into the layer's output buffer (K6 runs in place
@@ -605,6 +606,16 @@ int qkv_chunks(size_t B) {
   const int c = env < 1 ? 1 : env;
   return static_cast<int>(std::min<size_t>(B, static_cast<size_t>(c)));
 }
+// Post-LN tensor-core layers whose LayerNorms cannot ride in the GEMM
+// epilogues (d > 768: the parked row exceeds TMEM): A [T, d] holds the
+// attention branch and then the FFN branch; the transient holds [Qt | P_k |
+// P_v] with K2's output written over Qt, then the FFN chain's P | Z; both
+// LayerNorms (K5) write the layer's output buffer.
+bool compact_unfused_post_ln(const Pack& p, int mode) {
+  const bool flash = mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2;
+  return flash && p.attn_tc && p.out_tc && p.ffn_tc && p.dtype == FSVD_BF16 && !p.x3 &&
+         !fused_post_ln(p, mode);
+}
 bool compact_post_ln(const Pack& p, int mode) {
   return fused_post_ln(p, mode) && ffn_ln_fusable(p, mode) && (p.H * p.rp) % 64 == 0 &&
          p.dtype == FSVD_BF16;
@@ -623,6 +634,12 @@ WsLayout ws_layout(const Pack& p, size_t B, size_t M, int mode, bool pre_ln, boo
     }
     WsLayout w{a, 0, t};
     w.chunks = c;
+    return w;
+  }
+  if (!pre_ln && compact && compact_unfused_post_ln(p, mode)) {
+    const size_t tcols = std::max<size_t>(p.qkv_cols, op_transient_elems(p, 2, mode));
+    WsLayout w{align256(T * p.d * p.es), 0, align256(T * tcols * p.es)};
+    w.unfused_compact = true;
     return w;
   }
   if (!pre_ln && fused_post_ln(p, mode)) {
@@ -1350,6 +1367,18 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
                  p.eps1, as<bf16>(out), rows, p.d, hr, s, nullptr, seq_tiles_of(M));
     if (!ffn_ln_fwd(p, mode, B, M, out, out, A, s))
       fail(Kind::Config, "compact post-LN schedule without a fused FFN LayerNorm");
+  } else if (lay.unfused_compact) {
+    // K1 -> [Qt | P_k | P_v] (transient); K2 writes O over Qt; folded
+    // out-projection -> A; K5 LN1(x + A) -> out; FFN(out) -> A; K5 LN2 -> out
+    const int hr = p.H * p.rp, n = p.qkv_cols;
+    bf16* qkv = as<bf16>(trans);
+    gemm_bf16(as<bf16>(x), p.d, as<bf16>(p.wproj_t), p.d, qkv, n, rows, n, p.d, p.bproj, ACT_NONE,
+              s);
+    tc_attention(B, M, qkv, n, 0, hr, (p.H + p.G) * p.rp, p.H, p.G, p.rp, qkv, n, s);
+    gemm_bf16(qkv, n, as<bf16>(p.wov_t), hr, as<bf16>(A), p.d, rows, p.d, hr, p.bov, ACT_NONE, s);
+    ln(p, x, A, p.ln1g, p.ln1b, p.eps1, out, rows, s);
+    ffn_fwd(p, mode, B, M, out, A, trans, s);
+    ln(p, out, A, p.ln2g, p.ln2b, p.eps2, out, rows, s);
   } else if (!pre_ln && fused_post_ln(p, mode)) {
     // rank-space attention -> A; folded out-projection + residual + LN1 -> B
     tc_attention_rank(p, B, M, x, A, trans, s, am);
