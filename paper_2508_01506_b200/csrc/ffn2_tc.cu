@@ -24,6 +24,11 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#ifdef FSVD_TRACE
+namespace fsvd { __device__ long long g_trace2_ln[512]; }
+#define LN_TRACE(slot) \
+  do { if (blockIdx.x == 0 && (slot) < 512) ::fsvd::g_trace2_ln[(slot)] = clock64(); } while (0)
+#endif
 #include "ln_epi.cuh"
 #include "ptx.cuh"
 
@@ -39,6 +44,9 @@ constexpr int BF = 128;             // features per block
 constexpr int ATOM = BMr * 128;     // [128 x 64] bf16 SW128 atom of own rows (16 KB)
 constexpr int HSLOT = 64 * 128;     // ring slot: half of a 128-row weight box (8 KB)
 constexpr int STAGE = 2 * HSLOT;
+// fused LN2 second sweep: gamma | beta at the ring's start, output staging
+// boxes from here on (the ring is idle once the MMAs are done)
+constexpr int kLnStage = 8192;
 
 template <int FR>
 struct Ffn2Cfg {
@@ -55,6 +63,7 @@ struct Ffn2Cfg {
   static constexpr int SMEM = 1024 + o_bar + 1024;
   static constexpr int t_z = 0, t_h = 384;
   static_assert(SMEM <= 227 * 1024, "shared-memory budget");
+  static_assert(STAGES * STAGE >= kLnStage + 4 * 128 * 128, "LN output staging in the ring");
 };
 
 struct Ffn2Bars {
@@ -64,7 +73,7 @@ struct Ffn2Bars {
   uint64_t sh_loc[2];  // this CTA's epilogue warps -> relay (local, no cluster fence)
   uint64_t o_full[2], o_free[2];
   uint64_t res_full[2], res_empty[2];
-  uint64_t box_full[2], box_free[2];  // LN output boxes (ln_epi.cuh store_boxes)
+  uint64_t box_full[4], box_free[4];  // LN output boxes (ln_epi.cuh store_boxes), ring-staged
   uint32_t tmem;
 };
 static_assert(sizeof(Ffn2Bars) <= 1024, "barrier block");
@@ -109,6 +118,9 @@ __device__ long long g_trace2[8192];
 }  // namespace
 extern "C" __attribute__((visibility("default"))) int fsvd_debug_trace2_copy(long long* host, int n) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace2, sizeof(long long) * n));
+}
+extern "C" __attribute__((visibility("default"))) int fsvd_debug_trace2_ln_copy(long long* host, int n) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace2_ln, sizeof(long long) * n));
 }
 namespace {
 // cluster 0 only; slot offset 4096 for the peer CTA
@@ -174,6 +186,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&bars->res_empty[i], lnepi::res_box_readers<64>());
       mbar_init(&bars->box_full[i], lnepi::box_writer_warps<64>());
       mbar_init(&bars->box_free[i], 1);
+      mbar_init(&bars->box_full[i + 2], lnepi::box_writer_warps<64>());
+      mbar_init(&bars->box_free[i + 2], 1);
     }
     mbar_init(&bars->p_acc, 1);
     mbar_init(&bars->p_ready, 2 * kEpiWarps);
@@ -270,8 +284,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->z_full, 0);
       lnepi::produce_residual<64>(&tmX, smem + C::o_h, bars->res_full, bars->res_empty, 2,
                                   d_model, m0, rotq);
-      lnepi::store_boxes<64>(&tmY, smem_u32(smem + C::o_h), bars->box_full, bars->box_free,
-                             d_model, m0, rotq);
+      // output boxes: 4 staging slots in the weight ring after gamma / beta
+      lnepi::store_boxes<64, 4>(&tmY, smem_u32(ring) + kLnStage, bars->box_full, bars->box_free,
+                                d_model, m0, rotq);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -428,9 +443,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_before();
     warp_arrive_leader(&bars->zs_ready);
     if (fuse_ln) {
-      lnepi::run<64>(tmem, quad, half, row, d_model, b_dn, smem_u32(smem + C::o_h),
+      lnepi::run<64, 4>(tmem, quad, half, row, d_model, b_dn, smem_u32(smem + C::o_h),
                      bars->res_full, bars->res_empty, 2, ln_g, ln_b, ln_eps, &tmY, m0,
-                     reinterpret_cast<float*>(ring), smem_u32(smem + C::o_h), bars->box_full,
+                     reinterpret_cast<float*>(ring), smem_u32(ring) + kLnStage, bars->box_full,
                      bars->box_free, bars->o_full,
                      bars->o_free, 1,
                      mapa_shared(smem_u32(&bars->o_free[0]), 0), nullptr, 0, rotq);

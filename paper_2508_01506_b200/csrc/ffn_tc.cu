@@ -55,6 +55,9 @@ constexpr int BMr = 128;         // token rows per CTA
 constexpr int BF = 128;          // features per block
 constexpr int SLOT = BMr * 128;  // one [128 x 64] bf16 SW128 atom / ring slot (16 KB)
 constexpr int STAGE = 2 * SLOT;  // two slots per ring stage
+// fused LN2 second sweep: gamma | beta (2 x 768 fp32) at the ring's start,
+// output staging boxes from here on (the ring is idle once the MMAs are done)
+constexpr int kLnStage = 8192;
 
 // WIDE (K3 only, FFN ranks above 384): Z no longer fits TMEM next to H, so
 // the rank is cut into slices of FR columns, one CTA per (row tile, slice);
@@ -93,7 +96,7 @@ struct FfnBars {
   uint64_t p_full, p_acc, p_ready, h_full, h_free, sh_full[2], sh_free[2], z_full, zs_ready;
   uint64_t o_full[2], o_free[2];
   uint64_t res_full[2], res_empty[2];  // residual boxes of the fused LN2 (H region)
-  uint64_t box_full[2], box_free[2];   // its output boxes (ln_epi.cuh store_boxes)
+  uint64_t box_full[4], box_free[4];   // its output boxes (ln_epi.cuh store_boxes), ring-staged
   uint32_t tmem;
 };
 
@@ -222,6 +225,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars->res_empty[i], kEpi);
       mbar_init(&bars->box_full[i], lnepi::box_writer_warps<64>());
       mbar_init(&bars->box_free[i], 1);
+      mbar_init(&bars->box_full[i + 2], lnepi::box_writer_warps<64>());
+      mbar_init(&bars->box_free[i + 2], 1);
     }
     mbar_init(&bars->p_full, 1);
     mbar_init(&bars->p_acc, 1);
@@ -377,8 +382,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait_sleep(&bars->z_full, 0, 256);
       lnepi::produce_residual<64>(&tmR, smem + C::o_h, bars->res_full, bars->res_empty, 2,
                                   d_model, m0, rotq);
-      lnepi::store_boxes<64>(&tmY, smem_u32(smem + C::o_h), bars->box_full, bars->box_free,
-                             d_model, m0, rotq);
+      // output boxes: 4 staging slots in the weight ring after gamma / beta
+      lnepi::store_boxes<64, 4>(&tmY, smem_u32(ring) + kLnStage, bars->box_full, bars->box_free,
+                                d_model, m0, rotq);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -644,9 +650,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (fuse_ln) {
         // residual = the FFN input x, streamed through the idle H tile
         // gamma / beta are staged in the weight ring, idle once all MMAs are done
-        lnepi::run<64>(tmem, quad, half, row, d_model, b_dn, smem_u32(smem + C::o_h),
+        lnepi::run<64, 4>(tmem, quad, half, row, d_model, b_dn, smem_u32(smem + C::o_h),
                        bars->res_full, bars->res_empty, 2, ln_g, ln_b, ln_eps, &tmY, m0,
-                       reinterpret_cast<float*>(ring), smem_u32(smem + C::o_h), bars->box_full,
+                       reinterpret_cast<float*>(ring), smem_u32(ring) + kLnStage, bars->box_full,
                        bars->box_free, bars->o_full,
                        bars->o_free, 1, 0, sum_out, T, rotq);
       } else {

@@ -59,6 +59,7 @@ constexpr int STAGE = SPS * SLOT;
 constexpr int kMaxStages = 10;
 constexpr int RS = 2;               // residual ring depth ([128 x 64] bf16 boxes)
 constexpr int RBOX = BMr * 128;
+constexpr int kBoxes = 4;           // second-sweep output staging boxes (in the B ring; K <= 512 leaves 4 stages)
 
 #ifdef FSVD_TRACE
 }  // namespace
@@ -74,7 +75,7 @@ namespace {
 struct LnBars {
   uint64_t full[kMaxStages], empty[kMaxStages];
   uint64_t a_full, acc_full[1], acc_empty[1], res_full[RS], res_empty[RS];
-  uint64_t box_full[4], box_free[4];  // second-sweep output boxes (ln_epi.cuh store_boxes)
+  uint64_t box_full[kBoxes], box_free[kBoxes];  // second-sweep output boxes (ln_epi.cuh store_boxes)
   uint32_t tmem;
 };
 
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars->res_full[i], 1);
       mbar_init(&bars->res_empty[i], lnepi::res_box_readers<PN>());
     }
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kBoxes; ++i) {
       mbar_init(&bars->box_full[i], lnepi::box_writer_warps<PN>());
       mbar_init(&bars->box_free[i], 1);
     }
@@ -215,7 +216,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // second sweep's store thread (one thread)
     if (lane == 0) {
       lnepi::produce_residual<PN>(&tmR, rring, bars->res_full, bars->res_empty, RS, N, m0, rot);
-      lnepi::store_boxes<PN>(&tmY, smem_u32(ring), bars->box_full, bars->box_free, N, m0, rot);
+      lnepi::store_boxes<PN, kBoxes>(&tmY, smem_u32(ring), bars->box_full, bars->box_free, N, m0,
+                                     rot);
     }
     __syncwarp();
   } else {
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t row = quad * 32 + lane;
     // second sweep: output boxes staged in the B ring, gamma / beta in the A
     // region (both idle once every MMA has completed)
-    lnepi::run<PN>(tmem, quad, half, row, N, bias, smem_u32(rring), bars->res_full,
+    lnepi::run<PN, kBoxes>(tmem, quad, half, row, N, bias, smem_u32(rring), bars->res_full,
                    bars->res_empty, RS, gamma, beta, eps, &tmY, m0, reinterpret_cast<float*>(sA),
                    smem_u32(ring), bars->box_full, bars->box_free, bars->acc_full,
                    bars->acc_empty, 1, 0, sum_out, T, rot);
@@ -255,8 +257,9 @@ void gemm_ln_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, const 
   int stages =
       (227 * 1024 - 1024 - KA * ATOM - RS * RBOX - static_cast<int>(sizeof(LnBars))) / STAGE;
   stages = stages > kMaxStages ? kMaxStages : stages;
-  // the ring doubles as the second sweep's 4-box output staging
-  if (stages * STAGE < 4 * RBOX) throw CudaError("gemm_ln_bf16: K too large for the shared-memory ring");
+  // the ring doubles as the second sweep's output staging
+  if (stages * STAGE < kBoxes * RBOX)
+    throw CudaError("gemm_ln_bf16: K too large for the shared-memory ring");
   const int smem = 1024 + KA * ATOM + stages * STAGE + RS * RBOX + static_cast<int>(sizeof(LnBars));
   static int attr = 0;
   if (attr < smem) {

@@ -98,15 +98,16 @@ __device__ __forceinline__ void produce_residual(const CUtensorMap* tm, uint8_t*
 // issues the TMA store of every box as soon as its writers have arrived on
 // box_full[slot] (box_writer_warps() arrivals), and frees the slot once the
 // store has read it.  Box j = (piece j / BPP, 64-column half j % BPP), slot
-// j % (2 * BPP), in piece_of() order.
+// j % NBOX, in piece_of() order; the writers run up to NBOX - 1 boxes ahead
+// of the store issue.
 template <int PN>
 constexpr int box_writer_warps() { return PN == 64 ? kEpiThreads / 32 : kEpiThreads / 64; }
-template <int PN>
+template <int PN, int NBOX = 2 * (PN / 64)>
 __device__ __forceinline__ void store_boxes(const CUtensorMap* tmY, uint32_t out_stage,
                                             uint64_t* box_full, uint64_t* box_free, int N,
                                             int m0, int rot = 0) {
   constexpr int BPP = PN / 64;
-  constexpr int NBOX = 2 * BPP;
+  static_assert(NBOX % BPP == 0 && NBOX >= 2 * BPP, "staging slots");
   const int NP = N / PN;
   for (int j = 0; j < NP * BPP; ++j) {
     const int slot = j % NBOX;
@@ -131,7 +132,7 @@ constexpr int res_box_readers() { return PN == 64 ? kEpiThreads : kEpiThreads / 
 // acc_empty[0]) each warp releases the accumulator with one remote arrive.
 // Arithmetic runs on packed fp32 pairs (FADD2 / FFMA2) to halve the issue
 // count of this epilogue, which is instruction-bound.
-template <int PN>
+template <int PN, int NBOX = 2 * (PN / 64)>
 __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half, uint32_t row,
                                     int N, const float* __restrict__ bias, uint32_t res_ring,
                                     uint64_t* res_full, uint64_t* res_empty, int res_depth,
@@ -265,9 +266,7 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
   // Each finished [128 x 64] box is handed to the kernel's store thread
   // (store_boxes, below) through box_full / box_free, so no epilogue thread
   // waits on a TMA store instruction: box j of the sweep (piece j / BPP, half
-  // j % BPP) lives in staging slot j % (2 * BPP).
-  constexpr int BPP = PN / 64;
-  constexpr int NBOX = 2 * BPP;
+  // j % BPP) lives in staging slot j % NBOX.
   for (int i = 0; i < NP; ++i) {
     const int q = piece_of(i, NP, rot);
     const int j = PN == 64 ? i : 2 * i + static_cast<int>(half);

@@ -47,3 +47,10 @@ for f in range(24):
 print("relay (leader / peer): sh_loc complete -> remote arrive done, per atom")
 for f in (0, 1, 2, 10, 21, 22, 23):
     print(f, [(rel(t[c + 3000 + f * 4 + a * 2]), rel(t[c + 3001 + f * 4 + a * 2])) for c in (0, 4096) for a in (0, 1)])
+tl = (C.c_longlong * 512)()
+L.fsvd_debug_trace2_ln_copy.argtypes = [C.POINTER(C.c_longlong), C.c_int]
+L.fsvd_debug_trace2_ln_copy(tl, 512)
+tl = np.array(tl[:], dtype=np.int64)
+print("LN pieces (acc wait -> got):", " ".join(f"{rel(tl[200 + i])}->{rel(tl[232 + i])}" for i in range(12)))
+print(f"LN stats done {rel(tl[300])}, gamma/beta staged {rel(tl[301])}, pass-2 boxes",
+      " ".join(str(rel(tl[310 + i])) for i in range(12)), f"stores drained {rel(tl[330])}")
