@@ -124,6 +124,30 @@ __device__ __forceinline__ void st_chunk_smem(uint32_t tile, uint32_t row, int c
                  pack_bf16(v[8 * c + 2], v[8 * c + 3]), pack_bf16(v[8 * c + 4], v[8 * c + 5]),
                  pack_bf16(v[8 * c + 6], v[8 * c + 7]));
 }
+// Drains a [128 x FR] fp32 TMEM tile (this thread's row) to bf16 SW128 atoms
+// in shared memory, the thread's chunks c = half, half + 2, ... two TMEM loads
+// in flight per wait.
+template <int FR>
+__device__ __forceinline__ void drain_tile(uint32_t taddr, uint32_t tile, uint32_t row,
+                                           uint32_t half) {
+#pragma unroll
+  for (int c = static_cast<int>(half); c < FR / 32; c += 4) {
+    uint32_t r0[32], r1[32];
+    const bool two = c + 2 < FR / 32;
+    tmem_ld32(taddr + c * 32, r0);
+    if (two) tmem_ld32(taddr + (c + 2) * 32, r1);
+    tmem_ld_wait();
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r0[i]);
+    st_chunk_smem(tile, row, c * 32, v);
+    if (two) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r1[i]);
+      st_chunk_smem(tile, row, (c + 2) * 32, v);
+    }
+  }
+}
 __device__ __forceinline__ void st_chunk_global(bf16* dst, const float (&v)[32]) {
   uint4* d = reinterpret_cast<uint4*>(dst);
 #pragma unroll
@@ -562,11 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (FUSED) {
       mbar_wait(&bars->p_acc, 0);
       tc_fence_after();
-      for (int c = half; c < FR / 32; c += 2) {
-        float v[32];
-        ld_chunk(tmem + C::t_z + loff + c * 32, v);
-        st_chunk_smem(s_p, row, c * 32, v);
-      }
+      drain_tile<FR>(tmem + C::t_z + loff, s_p, row, half);
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&bars->p_ready);
@@ -638,11 +658,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     } else {
-      for (int c = half; c < FR / 32; c += 2) {
-        float v[32];
-        ld_chunk(tmem + C::t_z + loff + c * 32, v);
-        st_chunk_smem(s_p, row, c * 32, v);
-      }
+      drain_tile<FR>(tmem + C::t_z + loff, s_p, row, half);
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&bars->zs_ready);
