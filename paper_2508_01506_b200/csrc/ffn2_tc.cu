@@ -66,9 +66,21 @@ struct Ffn2Cfg {
   static_assert(STAGES * STAGE >= kLnStage + 4 * 128 * 128, "LN output staging in the ring");
 };
 
+// P phase: X chunks ([128 x 64] of the own rows) stream through x_slots()
+// slots -- the two H atoms, then the P tile's atoms, idle until P is drained
+// into them after the last P MMA -- so the loads run that far ahead of the
+// MMAs instead of two chunks.
+constexpr int kXSlotsMax = 8;
+template <int FR>
+constexpr int x_slots() { return 2 + FR / 64 < kXSlotsMax ? 2 + FR / 64 : kXSlotsMax; }
+template <int FR>
+__host__ __device__ constexpr int x_slot_off(int xb) {
+  return xb < 2 ? Ffn2Cfg<FR>::o_h + xb * ATOM : Ffn2Cfg<FR>::o_p + (xb - 2) * ATOM;
+}
+
 struct Ffn2Bars {
   uint64_t full[12], empty[12];
-  uint64_t x_full[2], x_empty[2];
+  uint64_t x_full[kXSlotsMax], x_empty[kXSlotsMax];  // X chunks of the P phase (x_slots)
   uint64_t p_acc, p_ready, h_full, h_free, sh_full[2], sh_free[2], z_full, zs_ready;
   uint64_t sh_loc[2];  // this CTA's epilogue warps -> relay (local, no cluster fence)
   uint64_t o_full[2], o_free[2];
@@ -198,9 +210,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&bars->full[i], 1);
       mbar_init(&bars->empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < x_slots<FR>(); ++i) {
       mbar_init(&bars->x_full[i], 1);
       mbar_init(&bars->x_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->sh_full[i], 2);  // one relay arrival per CTA
       mbar_init(&bars->sh_free[i], 1);
       mbar_init(&bars->sh_loc[i], kEpiWarps);
@@ -253,11 +267,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       };
       const int hr = static_cast<int>(rank) * 64;  // this CTA's half of a 128-row weight box
       for (int kc = 0; kc < KC; ++kc) {
-        const int xb = kc & 1;
-        if (static_cast<uint32_t>(xb) == me) {
-          mbar_wait(&bars->x_empty[xb], ((kc >> 1) & 1) ^ 1);
+        const int xb = kc % x_slots<FR>();
+        if (static_cast<uint32_t>(kc & 1) == me) {
+          mbar_wait(&bars->x_empty[xb], ((kc / x_slots<FR>()) & 1) ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&bars->x_full[xb], 2 * ATOM);
-          tma_load_2d_pair(&tmX, &bars->x_full[xb], smem + C::o_h + xb * ATOM, kch(kc) * 64, m0);
+          tma_load_2d_pair(&tmX, &bars->x_full[xb], smem + x_slot_off<FR>(xb), kch(kc) * 64, m0);
         }
         emit(C::NPIECE, [&](int p, uint8_t* dst) {
           tma_load_2d_pair(&tmUup, &bars->full[st], dst, kch(kc) * 64, p * C::PS + hr);
@@ -348,12 +362,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       constexpr uint32_t kAtom = ATOM >> 4;
       constexpr uint32_t id128 = idesc_bf16(2 * BMr, 128);
       // P = X U_up into the Z columns
+      const uint64_t d_x0 = desc_at(dhi, smem_u32(smem));
       for (int kc = 0; kc < KC; ++kc) {
-        const int xb = kc & 1;
-        mbar_wait(&bars->x_full[xb], (kc >> 1) & 1);
+        const int xb = kc % x_slots<FR>();
+        mbar_wait(&bars->x_full[xb], (kc / x_slots<FR>()) & 1);
         tc_fence_after();
+        const uint64_t dx = d_x0 + (x_slot_off<FR>(xb) >> 4);
         consume(C::NPIECE, [&](int p, uint64_t slot) {
-          mma4(tmem + C::t_z + p * C::PS, d_h + xb * kAtom, slot, id128, kc != 0);
+          mma4(tmem + C::t_z + p * C::PS, dx, slot, id128, kc != 0);
         });
         commit(&bars->x_empty[xb]);
       }
