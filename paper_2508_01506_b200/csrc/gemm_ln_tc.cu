@@ -253,6 +253,10 @@ void gemm_ln_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, const 
                   const bf16* resid, const float* gamma, const float* beta, float eps, bf16* y,
                   int T, int N, int K, cudaStream_t s, bf16* sum_out, int seq_tiles) {
   if (!gemm_ln_supported(N, K)) throw CudaError("gemm_ln_bf16: unsupported shape");
+  if (gemm_ln_pair_enabled() &&
+      gemm_ln_pair_bf16(A, lda, B, ldb, bias, resid, gamma, beta, eps, y, T, N, K, s, sum_out,
+                        seq_tiles))
+    return;
   const int KA = K / 64;
   int stages =
       (227 * 1024 - 1024 - KA * ATOM - RS * RBOX - static_cast<int>(sizeof(LnBars))) / STAGE;

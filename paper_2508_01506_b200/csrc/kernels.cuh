@@ -84,6 +84,13 @@ void gemm_ln_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, const 
                   int T, int N, int K, cudaStream_t s, bf16* sum_out = nullptr,
                   int seq_tiles = 0);
 bool gemm_ln_supported(int N, int K);
+// The same operation on a CTA pair (gemm_ln2_tc.cu, cta_group::2, 256 rows per
+// cluster); returns false (nothing launched) outside its range.  gemm_ln_bf16
+// uses it when gemm_ln_pair_enabled() (FSVD_LN_PAIR=1, opt-in).
+bool gemm_ln_pair_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, const float* bias,
+                       const bf16* resid, const float* gamma, const float* beta, float eps, bf16* y,
+                       int T, int N, int K, cudaStream_t s, bf16* sum_out, int seq_tiles);
+bool gemm_ln_pair_enabled();
 
 // ---- K2: rank-space FlashSVD attention --------------------------------------
 // out[t, h*rp : (h+1)*rp] = softmax(Qt_h K_g^T) V_g for each (sequence, head),
