@@ -188,14 +188,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int NB = (d_ff + BF - 1) / BF;
   const int KC = d_model / 64;
   const bool fuse_ln = ln_g != nullptr;
-  const int QS = fuse_ln ? 64 : 128;  // output columns per piece (pair MMA N)
+  // Z V_down in N = 128 MMA steps (8 KB weight half-slots).  With the fused
+  // LN the epilogue consumes each step as two 64-column pieces, one per warp
+  // group and accumulator buffer (ln_epi.cuh run_groups); the next step waits
+  // for both groups.
+  const int QS = 128;
   const int NQ = d_model / QS;
+  const int NQ64 = d_model / 64;  // LN pieces
   // loop rotation by the pair tile's place in its sequence (as k_ffn,
   // FfnTcArgs::seq_tiles): both CTAs of the pair use the same offsets
   const int rpos = seq_pairs > 1 ? static_cast<int>(blockIdx.x >> 1) % seq_pairs : 0;
   const int rdiv = seq_pairs > 1 ? seq_pairs : 1;
   const int rot = rpos * NB / rdiv, rotk = rpos * KC / rdiv;
-  const int rotq = fuse_ln ? rpos * NQ / rdiv : 0;
+  // in 64-column LN pieces, even so a step's two pieces stay adjacent
+  const int rotq = fuse_ln ? 2 * (rpos * NQ / rdiv) : 0;
   auto blk = [&](int f) { const int b = f + rot; return b >= NB ? b - NB : b; };
   auto kch = [&](int kc) { const int k = kc + rotk; return k >= KC ? k - KC : k; };
 
@@ -219,7 +225,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&bars->sh_free[i], 1);
       mbar_init(&bars->sh_loc[i], kEpiWarps);
       mbar_init(&bars->o_full[i], 1);
-      mbar_init(&bars->o_free[i], 2 * kEpiWarps);
+      // LN epilogue: one warp group per piece (ln_epi.cuh run); plain: all 8 warps
+      mbar_init(&bars->o_free[i], fuse_ln ? 2 * (kEpiWarps / 2) : 2 * kEpiWarps);
       mbar_init(&bars->res_full[i], 1);
       mbar_init(&bars->res_empty[i], lnepi::res_box_readers<64>());
       mbar_init(&bars->box_full[i], lnepi::box_writer_warps<64>());
@@ -298,7 +305,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int q = 0; q < NQ; ++q)
         emit(C::NATOM, [&](int a, uint8_t* dst) {
           tma_load_2d_pair(&tmVdn, &bars->full[st], dst, a * 64,
-                           lnepi::piece_of(q, NQ, rotq) * QS + static_cast<int>(rank) * (QS / 2));
+                           lnepi::piece_of(2 * q, NQ64, rotq) * 64 +
+                               static_cast<int>(rank) * (QS / 2));
         }, (QS / 2) * 128);
     }
     __syncwarp();
@@ -413,16 +421,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->zs_ready, 0);
       tc_fence_after();
       TRACE2(3);
-      const uint32_t idq = fuse_ln ? idesc_bf16(2 * BMr, 64) : idesc_bf16(2 * BMr, 128);
+      const uint32_t idq = idesc_bf16(2 * BMr, 128);
       for (int q = 0; q < NQ; ++q) {
-        if (q >= 2) {
-          mbar_wait(&bars->o_free[q & 1], ((q >> 1) - 1) & 1);
-          tc_fence_after();
+        if (fuse_ln) {
+          // one 128-column step fills both 64-column LN buffers: both groups
+          // must have drained the previous step
+          if (q >= 1) {
+            mbar_wait(&bars->o_free[0], (q - 1) & 1);
+            mbar_wait(&bars->o_free[1], (q - 1) & 1);
+            tc_fence_after();
+          }
+          consume(C::NATOM, [&](int a, uint64_t slot) {
+            mma4(tmem, d_p + a * kAtom, slot, idq, a != 0);
+          });
+          commit(&bars->o_full[0]);
+          commit(&bars->o_full[1]);
+        } else {
+          if (q >= 2) {
+            mbar_wait(&bars->o_free[q & 1], ((q >> 1) - 1) & 1);
+            tc_fence_after();
+          }
+          consume(C::NATOM, [&](int a, uint64_t slot) {
+            mma4(tmem + (q & 1) * QS, d_p + a * kAtom, slot, idq, a != 0);
+          });
+          commit(&bars->o_full[q & 1]);
         }
-        consume(C::NATOM, [&](int a, uint64_t slot) {
-          mma4(tmem + (q & 1) * QS, d_p + a * kAtom, slot, idq, a != 0);
-        });
-        commit(&bars->o_full[q & 1]);
       }
     }
   } else {
@@ -524,12 +547,11 @@ void launch_ffn2(const FfnTcArgs& a, cudaStream_t s) {
     attr = true;
   }
   const bool ln = a.ln_g != nullptr;
-  const int qs = ln ? 64 : 128;
   const CUtensorMap tx = tmap_bf16(a.x, a.T, a.d_model, a.d_model, BMr, 64, TmaSwizzle::B128);
   const CUtensorMap tup = tmap_bf16(a.up_u_t, FR, a.d_model, a.d_model, 64, 64, TmaSwizzle::B128);
   const CUtensorMap tvup = tmap_bf16(a.up_v_t, a.d_ff, FR, FR, 64, 64, TmaSwizzle::B128);
   const CUtensorMap tudn = tmap_bf16(a.dn_u_t, FR, a.d_ff, a.d_ff, 64, 64, TmaSwizzle::B128);
-  const CUtensorMap tvdn = tmap_bf16(a.dn_v_t, a.d_model, FR, FR, qs / 2, 64, TmaSwizzle::B128);
+  const CUtensorMap tvdn = tmap_bf16(a.dn_v_t, a.d_model, FR, FR, 64, 64, TmaSwizzle::B128);
   const CUtensorMap ty =
       ln ? tmap_bf16(a.out, a.T, a.d_model, a.d_model, BMr, 64, TmaSwizzle::B128) : tx;
   const int pairs = (a.T + 2 * BMr - 1) / (2 * BMr);

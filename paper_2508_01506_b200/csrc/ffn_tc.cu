@@ -244,9 +244,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars->sh_full[i], kEpi);
       mbar_init(&bars->sh_free[i], 1);
       mbar_init(&bars->o_full[i], 1);
-      mbar_init(&bars->o_free[i], kEpi);
+      mbar_init(&bars->o_free[i], fuse_ln ? lnepi::acc_drain_arrivals<64>() : kEpi);
       mbar_init(&bars->res_full[i], 1);
-      mbar_init(&bars->res_empty[i], kEpi);
+      mbar_init(&bars->res_empty[i], lnepi::res_box_readers<64>());
       mbar_init(&bars->box_full[i], lnepi::box_writer_warps<64>());
       mbar_init(&bars->box_free[i], 1);
       mbar_init(&bars->box_full[i + 2], lnepi::box_writer_warps<64>());

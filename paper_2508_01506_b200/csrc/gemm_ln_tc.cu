@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(&bars->a_full, 1);
     mbar_init(&bars->acc_full[0], 1);
-    mbar_init(&bars->acc_empty[0], kEpi);
+    mbar_init(&bars->acc_empty[0], lnepi::acc_drain_arrivals<PN>());
     for (int i = 0; i < RS; ++i) {
       mbar_init(&bars->res_full[i], 1);
       mbar_init(&bars->res_empty[i], lnepi::res_box_readers<PN>());

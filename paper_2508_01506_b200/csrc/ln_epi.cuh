@@ -101,7 +101,7 @@ __device__ __forceinline__ void produce_residual(const CUtensorMap* tm, uint8_t*
 // j % NBOX, in piece_of() order; the writers run up to NBOX - 1 boxes ahead
 // of the store issue.
 template <int PN>
-constexpr int box_writer_warps() { return PN == 64 ? kEpiThreads / 32 : kEpiThreads / 64; }
+constexpr int box_writer_warps() { return kEpiThreads / 64; }  // one group (PN 64) / one half (PN 128)
 template <int PN, int NBOX = 2 * (PN / 64)>
 __device__ __forceinline__ void store_boxes(const CUtensorMap* tmY, uint32_t out_stage,
                                             uint64_t* box_full, uint64_t* box_free, int N,
@@ -122,18 +122,217 @@ __device__ __forceinline__ void store_boxes(const CUtensorMap* tmY, uint32_t out
 }
 // Arrivals a residual box needs before it can be refilled.
 template <int PN>
-constexpr int res_box_readers() { return PN == 64 ? kEpiThreads : kEpiThreads / 2; }
+constexpr int res_box_readers() { return kEpiThreads / 2; }  // one group (PN 64) / one half (PN 128)
 
 // Runs in all 256 epilogue threads: `quad` = TMEM lane quadrant (hardware
-// warp id % 4), `half` = which PN/2 columns of each piece, `row` = tile row.
+// warp id % 4), `half` = which of the two warp groups (pieces i with
+// i % 2 == half), `row` = tile row.  The two groups take alternate pieces
+// whole, so one group computes piece i while the other waits for / loads
+// piece i + 1 -- the epilogue is latency-bound (TMEM load, bias, residual
+// box, pack chains) and the two groups' latencies overlap instead of both
+// groups stalling on the same piece.
 // Accumulator protocol: PN = 64 alternates acc_full/empty[0..1] (buffers at
-// columns 0 and 64); PN = 128 uses acc_full/empty[0] only.  In a CTA pair
-// (acc_empty_leader != 0: shared::cluster address of the leader's
-// acc_empty[0]) each warp releases the accumulator with one remote arrive.
-// Arithmetic runs on packed fp32 pairs (FADD2 / FFMA2) to halve the issue
-// count of this epilogue, which is instruction-bound.
+// columns 0 and 64; buffer i % 2 = the group's own); PN = 128 uses
+// acc_full/empty[0] only.  acc_empty takes one group's arrivals per piece:
+// acc_drain_arrivals<64>() threads, or in a CTA pair (acc_empty_leader != 0:
+// shared::cluster address of the leader's acc_empty[0]) one remote arrive
+// per warp of the group from each CTA.  Arithmetic runs on packed fp32 pairs
+// (FADD2 / FFMA2).
+constexpr int kGroupThreads = kEpiThreads / 2;
+// threads that release an accumulator per piece: one group (PN = 64) or all
+// epilogue threads (PN = 128)
+template <int PN>
+constexpr int acc_drain_arrivals() { return PN == 64 ? kGroupThreads : kEpiThreads; }
 template <int PN, int NBOX = 2 * (PN / 64)>
-__device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half, uint32_t row,
+__device__ __forceinline__ void run_groups(uint32_t tmem, uint32_t quad, uint32_t half, uint32_t row,
+                                    int N, const float* __restrict__ bias, uint32_t res_ring,
+                                    uint64_t* res_full, uint64_t* res_empty, int res_depth,
+                                    const float* __restrict__ gamma,
+                                    const float* __restrict__ beta, float eps,
+                                    const CUtensorMap* tmY, int m0, float* gb_smem,
+                                    uint32_t out_stage, uint64_t* box_full, uint64_t* box_free,
+                                    uint64_t* acc_full, uint64_t* acc_empty,
+                                    uint32_t bar_id, uint32_t acc_empty_leader = 0,
+                                    bf16* sum_out = nullptr, int rows = 0, int rot = 0) {
+  static_assert(PN == 64 || PN == 128, "piece width");
+  constexpr int BPP = PN / 64;  // [128 x 64] boxes per piece
+  const uint32_t loff = (quad * 32) << 16;
+  const int NP = N / PN;
+
+  float2 shift = make_float2(0.0f, 0.0f), S1 = shift, S2 = shift;
+  bool first = true;
+  for (int i = static_cast<int>(half); i < NP; i += 2) {
+    const int q = piece_of(i, NP, rot);
+    const uint32_t acc = PN == 64 ? (i & 1) : 0;
+    const uint32_t par = PN == 64 ? ((i >> 1) & 1) : (i & 1);
+#ifdef LN_TRACE
+    if (threadIdx.x == 64) LN_TRACE(200 + i);
+#endif
+    mbar_wait(&acc_full[acc], par);
+    tc_fence_after();
+#ifdef LN_TRACE
+    if (threadIdx.x == 64) LN_TRACE(232 + i);
+#endif
+    // the piece in 64-column boxes: two 32-column TMEM chunks per box
+#pragma unroll
+    for (int bx = 0; bx < BPP; ++bx) {
+      uint32_t v[2][32];
+      tmem_ld32(tmem + loff + acc * 64 + bx * 64, v[0]);
+      tmem_ld32(tmem + loff + acc * 64 + bx * 64 + 32, v[1]);
+      tmem_ld_wait();
+      if (bx == BPP - 1) {  // the whole piece is in registers: hand the accumulator back
+        tc_fence_before();
+        if (acc_empty_leader) {
+          // CTA pair: one arrive per warp on the leader CTA's barrier; the
+          // signal is "TMEM drained" (no shared-memory data), so no release fence
+          __syncwarp();
+          if ((threadIdx.x & 31) == 0) mbar_arrive_cluster_relaxed(acc_empty_leader + acc * 8);
+        } else {
+          mbar_arrive(&acc_empty[acc]);
+        }
+      }
+      // residual box of these 64 columns
+      const int rb = i * BPP + bx;
+      const int slot = rb % res_depth;
+      mbar_wait(&res_full[slot], (rb / res_depth) & 1);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int col = q * PN + bx * 64 + c * 32;  // first output column of the chunk
+        float4 b[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) b[k] = __ldg(reinterpret_cast<const float4*>(bias + col) + k);
+        uint32_t r[16];
+        load_res32(res_ring + slot * kBox, row, c * 32, r);
+        if (c == 1) release_box(&res_empty[slot]);
+        if (first) {
+          const float s00 = bf2(pack2(make_float2(__uint_as_float(v[c][0]) + b[0].x, 0.0f))).x +
+                            bf2(r[0]).x;
+          shift = make_float2(-s00, -s00);
+          first = false;
+        }
+        uint32_t park[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float4& bq = b[k >> 1];
+          const float2 bb = (k & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
+          // o: the sublayer output exactly as the unfused path stores it (bf16)
+          const float2 o = bf2(pack2(__fadd2_rn(
+              make_float2(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])), bb)));
+          const float2 sv = __fadd2_rn(o, bf2(r[k]));
+          park[k] = pack2(sv);
+          const float2 t = __fadd2_rn(sv, shift);
+          S1 = __fadd2_rn(S1, t);
+          S2 = __ffma2_rn(t, t, S2);
+        }
+        tmem_st16(tmem + loff + kPark + col / 2, park);
+        if (sum_out != nullptr && m0 + static_cast<int>(row) < rows) {
+          // pre-LN residual stream: the un-normalised sum, as the unfused path stores it
+          uint4* d = reinterpret_cast<uint4*>(sum_out + (int64_t)(m0 + static_cast<int>(row)) * N + col);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            d[k] = make_uint4(park[4 * k], park[4 * k + 1], park[4 * k + 2], park[4 * k + 3]);
+        }
+      }
+    }
+  }
+  tmem_st_wait();
+#ifdef LN_TRACE
+  if (threadIdx.x == 64) LN_TRACE(300);
+#endif
+  // this group's elements: its pieces (NP may be odd: group 0 then has one more)
+  const int my_pieces = (NP - static_cast<int>(half) + 1) / 2;
+  const int ot_pieces = NP - my_pieces;
+  const float nh = static_cast<float>(my_pieces * PN), no = static_cast<float>(ot_pieces * PN);
+  const float s1 = S1.x + S1.y, s2 = S2.x + S2.y;
+  const float mean_h = my_pieces ? s1 / nh - shift.x : 0.0f;
+  const float m2_h = my_pieces ? fmaxf(s2 - s1 * (s1 / nh), 0.0f) : 0.0f;
+  // exchange with the other group's thread of this row (same TMEM lane)
+  // through columns [0, 4) of the drained accumulator: the last MMA into it
+  // has completed and only this lane's own threads touch this lane
+  tmem_st2(tmem + loff + 2 * half, __float_as_uint(mean_h), __float_as_uint(m2_h));
+  tmem_st_wait();
+  tc_fence_before();
+  named_bar_sync(bar_id, kEpiThreads);
+  tc_fence_after();
+  uint32_t mo, m2o;
+  tmem_ld2(tmem + loff + 2 * (half ^ 1), mo, m2o);
+  tmem_ld_wait();
+  const float mean_o = __uint_as_float(mo), m2_o = __uint_as_float(m2o);
+  // Chan's pairwise merge (counts nh, no)
+  const float ntot = nh + no;
+  const float delta = mean_o - mean_h;
+  const float mean = (nh * mean_h + no * mean_o) / ntot;
+  const float m2 = m2_h + m2_o + delta * delta * (nh * no / ntot);
+  const float rstd = rsqrtf(m2 / static_cast<float>(N) + eps);
+  // y = gamma * ((s - mean) * rstd) + beta = gamma * (s * rstd + off) + beta
+  const float2 rs2 = make_float2(rstd, rstd), off2 = make_float2(-mean * rstd, -mean * rstd);
+
+  // gamma | beta -> shared memory (the caller's region is idle by now)
+  const int et = static_cast<int>(threadIdx.x) - 64;  // 0..255 across the epilogue warps
+  for (int c = et * 4; c < N; c += kEpiThreads * 4) {
+    *reinterpret_cast<float4*>(gb_smem + c) = __ldg(reinterpret_cast<const float4*>(gamma + c));
+    *reinterpret_cast<float4*>(gb_smem + N + c) = __ldg(reinterpret_cast<const float4*>(beta + c));
+  }
+  named_bar_sync(bar_id, kEpiThreads);
+#ifdef LN_TRACE
+  if (threadIdx.x == 64) LN_TRACE(301);
+#endif
+
+  // second sweep: normalise into [128 x 64] bf16 boxes staged at out_stage;
+  // each finished box is handed to the kernel's store thread (store_boxes)
+  // through box_full / box_free, so no epilogue thread waits on a TMA store
+  // instruction.  Box j of the sweep = (piece j / BPP, 64-column part j % BPP),
+  // staging slot j % NBOX; a group fills the boxes of its own pieces.
+  for (int i = static_cast<int>(half); i < NP; i += 2) {
+    const int q = piece_of(i, NP, rot);
+#pragma unroll
+    for (int bx = 0; bx < BPP; ++bx) {
+      const int j = i * BPP + bx;
+      const int slot = j % NBOX;
+      const uint32_t box = out_stage + slot * kBox;
+      if (j >= NBOX) mbar_wait(&box_free[slot], ((j / NBOX) - 1) & 1);
+      uint32_t park[2][16];
+      tmem_ld16(tmem + loff + kPark + (q * PN + bx * 64) / 2, park[0]);
+      tmem_ld16(tmem + loff + kPark + (q * PN + bx * 64 + 32) / 2, park[1]);
+      tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int col = q * PN + bx * 64 + c * 32;
+        uint32_t w[16];
+#pragma unroll
+        for (int k = 0; k < 16; k += 2) {
+          const float4 g = *reinterpret_cast<const float4*>(gb_smem + col + 2 * k);
+          const float4 be = *reinterpret_cast<const float4*>(gb_smem + N + col + 2 * k);
+          const float2 n0 = __ffma2_rn(bf2(park[c][k]), rs2, off2);
+          const float2 n1 = __ffma2_rn(bf2(park[c][k + 1]), rs2, off2);
+          w[k] = pack2(__ffma2_rn(make_float2(g.x, g.y), n0, make_float2(be.x, be.y)));
+          w[k + 1] = pack2(__ffma2_rn(make_float2(g.z, g.w), n1, make_float2(be.z, be.w)));
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          st_shared_v4(box + swz_offset(row, c * 4 + k, 128), w[4 * k], w[4 * k + 1],
+                       w[4 * k + 2], w[4 * k + 3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&box_full[slot]);
+    }
+#ifdef LN_TRACE
+    if (threadIdx.x == 64) LN_TRACE(310 + i);
+#endif
+  }
+#ifdef LN_TRACE
+  if (threadIdx.x == 64) LN_TRACE(330);
+#endif
+}
+
+// Column halves (PN = 128, single accumulator): both warp groups work on
+// every piece, each on half of its columns.  Alternating whole pieces between
+// the groups needs one accumulator per group -- with a single one a group
+// that skips a phase could wait on the wrong parity -- so the single-buffered
+// kernels (K6) keep this form.
+template <int PN, int NBOX = 2 * (PN / 64)>
+__device__ __forceinline__ void run_halves(uint32_t tmem, uint32_t quad, uint32_t half, uint32_t row,
                                     int N, const float* __restrict__ bias, uint32_t res_ring,
                                     uint64_t* res_full, uint64_t* res_empty, int res_depth,
                                     const float* __restrict__ gamma,
@@ -305,6 +504,30 @@ __device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half,
 #ifdef LN_TRACE
   if (threadIdx.x == 64) LN_TRACE(330);
 #endif
+}
+
+// The LayerNorm epilogue: whole pieces per warp group for PN = 64 (double
+// buffered: accumulator i % 2 belongs to group i % 2), column halves for
+// PN = 128 (single accumulator).
+template <int PN, int NBOX = 2 * (PN / 64)>
+__device__ __forceinline__ void run(uint32_t tmem, uint32_t quad, uint32_t half, uint32_t row,
+                                    int N, const float* __restrict__ bias, uint32_t res_ring,
+                                    uint64_t* res_full, uint64_t* res_empty, int res_depth,
+                                    const float* __restrict__ gamma,
+                                    const float* __restrict__ beta, float eps,
+                                    const CUtensorMap* tmY, int m0, float* gb_smem,
+                                    uint32_t out_stage, uint64_t* box_full, uint64_t* box_free,
+                                    uint64_t* acc_full, uint64_t* acc_empty,
+                                    uint32_t bar_id, uint32_t acc_empty_leader = 0,
+                                    bf16* sum_out = nullptr, int rows = 0, int rot = 0) {
+  if constexpr (PN == 64)
+    run_groups<PN, NBOX>(tmem, quad, half, row, N, bias, res_ring, res_full, res_empty, res_depth,
+                         gamma, beta, eps, tmY, m0, gb_smem, out_stage, box_full, box_free,
+                         acc_full, acc_empty, bar_id, acc_empty_leader, sum_out, rows, rot);
+  else
+    run_halves<PN, NBOX>(tmem, quad, half, row, N, bias, res_ring, res_full, res_empty, res_depth,
+                         gamma, beta, eps, tmY, m0, gb_smem, out_stage, box_full, box_free,
+                         acc_full, acc_empty, bar_id, acc_empty_leader, sum_out, rows, rot);
 }
 
 }  // namespace lnepi
