@@ -389,14 +389,37 @@ def run_gpu(args):
                                    C.c_void_p(xout.data_ptr()), C.c_void_p(work.data_ptr()),
                                    wsb.value, sp))
 
+    # N > 1: the output gather to rank 0 (NCCL over NVLink) is part of every
+    # step, issued asynchronously right after the step's forward so that it
+    # overlaps the next step's forward; consecutive steps alternate between
+    # two batch buffers (and two gather destinations on rank 0), and a buffer
+    # is reused only after its gather has completed
+    bufs = [x, torch.empty_like(x)] if multi else [x]
+    gdst = [gbufs, [torch.empty_like(out) for _ in range(ws)]] if (multi and rank == 0) else [None, None]
+    pending = [None, None]
+    step_no = [0]
+
     def step():
+        k = step_no[0] % len(bufs)
+        step_no[0] += 1
+        if pending[k] is not None:
+            pending[k].wait()
+            pending[k] = None
         for i in range(len(micro)):
-            fwd(i)
-        if multi:  # the output gather to rank 0 (NCCL over NVLink), inside the step
-            dist.gather(out, gbufs, dst=0)
+            a, b = micro[i]
+            fwd(i, bufs[k][a - s0:b - s0], bufs[k][a - s0:b - s0])
+        if multi:
+            pending[k] = dist.gather(bufs[k], gdst[k], dst=0, async_op=True)
+
+    def drain():
+        for k in range(2):
+            if pending[k] is not None:
+                pending[k].wait()
+                pending[k] = None
 
     for _ in range(args.warmup):
         step()
+    drain()
     torch.cuda.synchronize(dev)
     assert torch.isfinite(out[:s1 - s0].float()).all().item(), "non-finite output"
 
@@ -413,6 +436,11 @@ def run_gpu(args):
         evs[i][0].record(stream)
         step()
         evs[i][1].record(stream)
+    # the last steps' gathers complete inside the timed total
+    ed0, ed1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ed0.record(stream)
+    drain()
+    ed1.record(stream)
     torch.cuda.synchronize(dev)
     launches = L.fsvd_kernel_launch_count() - n0
     if multi:
@@ -424,7 +452,7 @@ def run_gpu(args):
         fwd(i)
     torch.cuda.synchronize(dev)
     x_in = x0_host.to(dev)  # device copy of the pristine input (after the memory measurement)
-    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    ms = (sum(a.elapsed_time(b) for a, b in evs) + ed0.elapsed_time(ed1)) / args.steps
     ms_t = torch.tensor([ms], device=dev)
     if multi:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
