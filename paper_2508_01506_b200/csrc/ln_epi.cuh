@@ -80,18 +80,32 @@ __device__ __forceinline__ int seq_rotation(int tile, int seq_tiles, int n) {
 // Residual producer (one thread): streams the [128 x N] residual tile at row
 // m0 as [128 x 64] boxes, pieces in piece_of() order, through a ring of
 // `depth` boxes.
+//
+// The residual streams twice, in the same order: run()'s first sweep adds it
+// to the sublayer output for the statistics, the second adds it again to the
+// parked (bf16-exact) sublayer output before normalising, so the value being
+// normalised is the exact fp32 sum -- parking the sum itself in bf16 cost up
+// to 2^-9 of |x + f(x)| per element, which large-magnitude features carried
+// into the 12-layer error.  Box sequence numbers continue across the sweeps
+// (second sweep from NP * BPP on), and so do the ring's phases.  With sum_out
+// (pre-LN chaining: the residual stream is stored in bf16 and overwrites the
+// residual input in place) the stored bf16 sum is what the unfused path
+// normalises, so that sum is parked and the residual streams once
+// (two_pass = false).
 template <int PN>
 __device__ __forceinline__ void produce_residual(const CUtensorMap* tm, uint8_t* ring,
                                                  uint64_t* full, uint64_t* empty, int depth,
-                                                 int N, int m0, int rot = 0) {
+                                                 int N, int m0, int rot = 0,
+                                                 bool two_pass = true) {
   constexpr int BPP = PN / 64;  // boxes per piece
   const int NP = N / PN;
-  for (int b = 0; b < NP * BPP; ++b) {
+  for (int b = 0; b < (two_pass ? 2 : 1) * NP * BPP; ++b) {
     const int slot = b % depth;
+    const int bb = b % (NP * BPP);  // box within the sweep
     mbar_wait(&empty[slot], ((b / depth) & 1) ^ 1);
     mbar_arrive_expect_tx(&full[slot], kBox);
-    tma_load_2d(tm, &full[slot], ring + slot * kBox, piece_of(b / BPP, NP, rot) * PN + (b % BPP) * 64,
-                m0);
+    tma_load_2d(tm, &full[slot], ring + slot * kBox,
+                piece_of(bb / BPP, NP, rot) * PN + (bb % BPP) * 64, m0);
   }
 }
 // Output boxes of run()'s second sweep: one thread of an otherwise idle warp
@@ -210,16 +224,20 @@ __device__ __forceinline__ void run_groups(uint32_t tmem, uint32_t quad, uint32_
           shift = make_float2(-s00, -s00);
           first = false;
         }
-        uint32_t park[16];
+        uint32_t park[16], sums[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const float4& bq = b[k >> 1];
           const float2 bb = (k & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
           // o: the sublayer output exactly as the unfused path stores it (bf16)
-          const float2 o = bf2(pack2(__fadd2_rn(
-              make_float2(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])), bb)));
+          const uint32_t ob = pack2(__fadd2_rn(
+              make_float2(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])), bb));
+          const float2 o = bf2(ob);
           const float2 sv = __fadd2_rn(o, bf2(r[k]));
-          park[k] = pack2(sv);
+          // o itself (exact in bf16; the sum is rebuilt in the second sweep), or
+          // with sum_out the bf16 sum it stores
+          sums[k] = pack2(sv);
+          park[k] = sum_out != nullptr ? sums[k] : ob;
           const float2 t = __fadd2_rn(sv, shift);
           S1 = __fadd2_rn(S1, t);
           S2 = __ffma2_rn(t, t, S2);
@@ -230,7 +248,7 @@ __device__ __forceinline__ void run_groups(uint32_t tmem, uint32_t quad, uint32_
           uint4* d = reinterpret_cast<uint4*>(sum_out + (int64_t)(m0 + static_cast<int>(row)) * N + col);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            d[k] = make_uint4(park[4 * k], park[4 * k + 1], park[4 * k + 2], park[4 * k + 3]);
+            d[k] = make_uint4(sums[4 * k], sums[4 * k + 1], sums[4 * k + 2], sums[4 * k + 3]);
         }
       }
     }
@@ -294,6 +312,20 @@ __device__ __forceinline__ void run_groups(uint32_t tmem, uint32_t quad, uint32_
       uint32_t park[2][16];
       tmem_ld16(tmem + loff + kPark + (q * PN + bx * 64) / 2, park[0]);
       tmem_ld16(tmem + loff + kPark + (q * PN + bx * 64 + 32) / 2, park[1]);
+      // the residual of this box again (second pass of produce_residual);
+      // with sum_out the parked value is the sum already (zero added)
+      uint32_t rr[2][16];
+      if (sum_out == nullptr) {
+        const int rb = NP * BPP + j;
+        const int rs = rb % res_depth;
+        mbar_wait(&res_full[rs], (rb / res_depth) & 1);
+        load_res32(res_ring + rs * kBox, row, 0, rr[0]);
+        load_res32(res_ring + rs * kBox, row, 32, rr[1]);
+        release_box(&res_empty[rs]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) rr[0][k] = rr[1][k] = 0u;
+      }
       tmem_ld_wait();
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -303,8 +335,10 @@ __device__ __forceinline__ void run_groups(uint32_t tmem, uint32_t quad, uint32_
         for (int k = 0; k < 16; k += 2) {
           const float4 g = *reinterpret_cast<const float4*>(gb_smem + col + 2 * k);
           const float4 be = *reinterpret_cast<const float4*>(gb_smem + N + col + 2 * k);
-          const float2 n0 = __ffma2_rn(bf2(park[c][k]), rs2, off2);
-          const float2 n1 = __ffma2_rn(bf2(park[c][k + 1]), rs2, off2);
+          // s = o + x in fp32, exactly as the statistics saw it
+          const float2 n0 = __ffma2_rn(__fadd2_rn(bf2(park[c][k]), bf2(rr[c][k])), rs2, off2);
+          const float2 n1 =
+              __ffma2_rn(__fadd2_rn(bf2(park[c][k + 1]), bf2(rr[c][k + 1])), rs2, off2);
           w[k] = pack2(__ffma2_rn(make_float2(g.x, g.y), n0, make_float2(be.x, be.y)));
           w[k + 1] = pack2(__ffma2_rn(make_float2(g.z, g.w), n1, make_float2(be.z, be.w)));
         }
@@ -394,16 +428,20 @@ __device__ __forceinline__ void run_halves(uint32_t tmem, uint32_t quad, uint32_
                           bf2(r[0]).x;
         shift = make_float2(-s00, -s00);
       }
-      uint32_t park[16];
+      uint32_t park[16], sums[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         const float4& bq = b[k >> 1];
         const float2 bb = (k & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
         // o: the sublayer output exactly as the unfused path stores it (bf16)
-        const float2 o = bf2(pack2(__fadd2_rn(
-            make_float2(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])), bb)));
+        const uint32_t ob = pack2(__fadd2_rn(
+            make_float2(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])), bb));
+        const float2 o = bf2(ob);
         const float2 sv = __fadd2_rn(o, bf2(r[k]));
-        park[k] = pack2(sv);
+        // o itself (exact in bf16; the sum is rebuilt in the second sweep), or
+        // with sum_out the bf16 sum it stores
+        sums[k] = pack2(sv);
+        park[k] = sum_out != nullptr ? sums[k] : ob;
         const float2 t = __fadd2_rn(sv, shift);
         S1 = __fadd2_rn(S1, t);
         S2 = __ffma2_rn(t, t, S2);
@@ -414,7 +452,7 @@ __device__ __forceinline__ void run_halves(uint32_t tmem, uint32_t quad, uint32_
         uint4* d = reinterpret_cast<uint4*>(sum_out + (int64_t)(m0 + static_cast<int>(row)) * N + col);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          d[k] = make_uint4(park[4 * k], park[4 * k + 1], park[4 * k + 2], park[4 * k + 3]);
+          d[k] = make_uint4(sums[4 * k], sums[4 * k + 1], sums[4 * k + 2], sums[4 * k + 3]);
       }
     }
   }
@@ -472,19 +510,35 @@ __device__ __forceinline__ void run_halves(uint32_t tmem, uint32_t quad, uint32_
     const int slot = j % NBOX;
     const uint32_t box = out_stage + slot * kBox;
     if (j >= NBOX) mbar_wait(&box_free[slot], ((j / NBOX) - 1) & 1);
+    // the residual of this thread's columns again (second pass of
+    // produce_residual): PN = 64 both halves read box i, PN = 128 each half
+    // its own box 2 i + half
+    // (with sum_out the parked value is the sum already: zero added)
+    const bool two = sum_out == nullptr;
+    const int rb = (PN == 64 ? NP : 2 * NP) + j;
+    const int rs = rb % res_depth;
+    if (two) mbar_wait(&res_full[rs], (rb / res_depth) & 1);
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       const int col = q * PN + half * (PN / 2) + c * 32;
-      uint32_t park[16];
+      uint32_t park[16], rr[16];
       tmem_ld16(tmem + loff + kPark + col / 2, park);
+      if (two) {
+        load_res32(res_ring + rs * kBox, row, PN == 64 ? half * 32 : c * 32, rr);
+        if (c == CPT - 1) release_box(&res_empty[rs]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) rr[k] = 0u;
+      }
       tmem_ld_wait();
       uint32_t w[16];
 #pragma unroll
       for (int k = 0; k < 16; k += 2) {
         const float4 g = *reinterpret_cast<const float4*>(gb_smem + col + 2 * k);
         const float4 be = *reinterpret_cast<const float4*>(gb_smem + N + col + 2 * k);
-        const float2 n0 = __ffma2_rn(bf2(park[k]), rs2, off2);
-        const float2 n1 = __ffma2_rn(bf2(park[k + 1]), rs2, off2);
+        // s = o + x in fp32, exactly as the statistics saw it
+        const float2 n0 = __ffma2_rn(__fadd2_rn(bf2(park[k]), bf2(rr[k])), rs2, off2);
+        const float2 n1 = __ffma2_rn(__fadd2_rn(bf2(park[k + 1]), bf2(rr[k + 1])), rs2, off2);
         w[k] = pack2(__ffma2_rn(make_float2(g.x, g.y), n0, make_float2(be.x, be.y)));
         w[k + 1] = pack2(__ffma2_rn(make_float2(g.z, g.w), n1, make_float2(be.z, be.w)));
       }

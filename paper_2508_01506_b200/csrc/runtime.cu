@@ -573,9 +573,17 @@ int seq_tiles_of(size_t M) { return M % 128 == 0 ? static_cast<int>(M / 128) : 0
 // Fused post-LN tensor-core schedule (layer_fwd): rank-space attention output
 // A [T, H*rp], LN1 output B [T, d], transient QKV / FFN-V1 region; A holds a
 // [T, d] FFN output instead when the FFN cannot take its LN fused.
+bool fused_ln_disabled() {
+  static const bool off = [] {
+    const char* e = getenv("FSVD_UNFUSED_LN");  // developer switch: K5 LayerNorms
+    return e && e[0] == '1';
+  }();
+  return off;
+}
 bool fused_post_ln(const Pack& p, int mode) {
   const bool flash = mode == FSVD_MODE_FLASH_V1 || mode == FSVD_MODE_FLASH_V2;
-  return flash && p.attn_tc && p.out_tc && p.d == p.dr && gemm_ln_supported(p.d, p.H * p.rp);
+  return flash && p.attn_tc && p.out_tc && p.d == p.dr && gemm_ln_supported(p.d, p.H * p.rp) &&
+         !fused_ln_disabled();
 }
 bool ffn_ln_fusable(const Pack& p, int mode) {
   return p.ffn_tc && p.d == p.dr && gemm_ln_supported(p.d, p.frp) &&
