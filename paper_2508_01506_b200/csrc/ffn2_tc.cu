@@ -308,11 +308,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                            lnepi::piece_of(2 * q, NQ64, rotq) * 64 +
                                static_cast<int>(rank) * (QS / 2));
         }, (QS / 2) * 128);
-      // fused LN2: this thread then issues the second sweep's stores (output
-      // boxes in 4 staging slots of the weight ring after gamma / beta)
-      if (fuse_ln && me == 0)
-        lnepi::store_boxes<64, 4>(&tmY, smem_u32(ring) + kLnStage, bars->box_full,
-                                  bars->box_free, d_model, m0, rotq);
     }
     __syncwarp();
   } else if (warp == 10) {
@@ -335,6 +330,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->z_full, 0);
       lnepi::produce_residual<64>(&tmX, smem + C::o_h, bars->res_full, bars->res_empty, 2,
                                   d_model, m0, rotq);
+      // output boxes: 4 staging slots in the weight ring after gamma / beta
+      lnepi::store_boxes<64, 4>(&tmY, smem_u32(ring) + kLnStage, bars->box_full, bars->box_free,
+                                d_model, m0, rotq);
     }
     __syncwarp();
   } else if (warp == 1) {

@@ -396,11 +396,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             return QS * 128;
           });
       }
-      // fused LN2: this thread then issues the second sweep's stores (output
-      // boxes in 4 staging slots of the weight ring after gamma / beta)
-      if (fuse_ln && me == 0)
-        lnepi::store_boxes<64, 4>(&tmY, smem_u32(ring) + kLnStage, bars->box_full,
-                                  bars->box_free, d_model, m0, rotq);
     }
     __syncwarp();
   } else if (warp == 10) {
@@ -410,7 +405,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (fuse_ln && lane == 0) {
       mbar_wait_sleep(&bars->z_full, 0, 256);
       lnepi::produce_residual<64>(&tmR, smem + C::o_h, bars->res_full, bars->res_empty, 2,
-                                  d_model, m0, rotq, sum_out == nullptr);
+                                  d_model, m0, rotq);
+      // output boxes: 4 staging slots in the weight ring after gamma / beta
+      lnepi::store_boxes<64, 4>(&tmY, smem_u32(ring) + kLnStage, bars->box_full, bars->box_free,
+                                d_model, m0, rotq);
     }
     __syncwarp();
   } else if (warp == 1) {

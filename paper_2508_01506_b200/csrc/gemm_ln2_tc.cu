@@ -25,9 +25,9 @@
 // both CTAs' epilogue warps arrive on its acc_empty); empty and acc_full exist
 // in both CTAs and receive multicast commits.
 //
-// Warps: 0 and 11 TMA producers (A, B half slots; both CTAs; warp 0 then
-// issues the second sweep's stores), 1 MMA issuer (leader) + TMEM owner, 2..9
-// epilogue, 10 residual producer.
+// Warps: 0 and 11 TMA producers (A, B half slots; both CTAs), 1 MMA issuer
+// (leader) + TMEM owner, 2..9 epilogue, 10 residual producer and store
+// thread of the second sweep.
 #include <cstdlib>
 
 #include "common.cuh"
@@ -131,10 +131,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if (++st == static_cast<uint32_t>(stages)) { st = 0; ph ^= 1; }
       }
-      // then the second sweep's store thread (own rows)
-      if (me == 0)
-        lnepi::store_boxes<PN, kBoxes>(&tmY, smem_u32(ring), bars->box_full, bars->box_free, N,
-                                       m0, rot);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -173,11 +169,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 10) {
-    // ============================================ residual producer (one
-    // thread, own rows, both sweeps)
+    // ============================================ residual producer, then the
+    // second sweep's store thread (one thread, own rows)
     if (lane == 0) {
-      lnepi::produce_residual<PN>(&tmR, rring, bars->res_full, bars->res_empty, RS, N, m0, rot,
-                                  sum_out == nullptr);
+      lnepi::produce_residual<PN>(&tmR, rring, bars->res_full, bars->res_empty, RS, N, m0, rot);
+      lnepi::store_boxes<PN, kBoxes>(&tmY, smem_u32(ring), bars->box_full, bars->box_free, N, m0,
+                                     rot);
     }
     __syncwarp();
   } else {

@@ -158,10 +158,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (++st == (uint32_t)stages) { st = 0; ph ^= 1; }
       }
-      // then the second sweep's store thread (ln_epi.cuh store_boxes)
-      if (me == 0)
-        lnepi::store_boxes<PN, kBoxes>(&tmY, smem_u32(ring), bars->box_full, bars->box_free, N,
-                                       m0, rot);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -216,11 +212,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       LTRACE(48 + q);
     }
   } else if (warp == 10) {
-    // ============================================ residual producer (one thread;
-    // both sweeps)
+    // ============================================ residual producer, then the
+    // second sweep's store thread (one thread)
     if (lane == 0) {
-      lnepi::produce_residual<PN>(&tmR, rring, bars->res_full, bars->res_empty, RS, N, m0, rot,
-                                  sum_out == nullptr);
+      lnepi::produce_residual<PN>(&tmR, rring, bars->res_full, bars->res_empty, RS, N, m0, rot);
+      lnepi::store_boxes<PN, kBoxes>(&tmY, smem_u32(ring), bars->box_full, bars->box_free, N, m0,
+                                     rot);
     }
     __syncwarp();
   } else {
