@@ -43,10 +43,11 @@ for tu in ("gemm", "attn", "gemm_ln", "ffn"):
     fn(buf, 4096 * 8)
     a = np.array(buf[:], dtype=np.uint64).reshape(4096, 8)
     a = a[a[:, 2] > 0]
-    res[tu] = a
+    if len(a):  # kernels this layer did not launch (e.g. k_ffn when the pair FFN runs) are skipped
+        res[tu] = a
 t0 = min(int(r[:, 0].min()) for r in res.values())
 print(f"B={B} M={M}: last layer of a 2-layer forward; times in us from the first CTA entry")
-for tu in ("gemm", "attn", "gemm_ln", "ffn"):
+for tu in [k for k in ("gemm", "attn", "gemm_ln", "ffn") if k in res]:
     a = res[tu].astype(np.int64) - t0
     work = (a[:, 2] - a[:, 1]) / 1e3
     print(f"{tu:8s} ctas={len(a):4d} SMs={len(set(res[tu][:, 5].tolist())):3d} | entry {a[:, 0].min() / 1e3:7.2f}"
