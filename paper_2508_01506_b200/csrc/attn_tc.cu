@@ -34,6 +34,14 @@
 // producer, 9 MMA issuer and TMEM owner.  ~92 KB smem and 256 TMEM columns,
 // so two CTAs share an SM (16 softmax warps per SM to hide MUFU / TMEM
 // latency; the softmax is issue- and latency-bound, not exp-bound).
+//
+// Output (bf16 RP <= 32): each quadrant pair stages its 32 rows of O / l in
+// shared memory and one thread TMA-stores them as a [32 x RP] box of a
+// [batch, seq, H*RP] map (rows past the sequence are clipped); the store of
+// item e is issued during item e+1 and drained two items later.  Against
+// per-thread row stores this is -0.8% on the 12-layer step; keeping Bars in
+// the shared window (LDS / STS instead of generic loads) and the spill
+// reduction that came with it another -1.3% (`tools/ab.sh`).
 #include "common.cuh"
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -118,7 +126,12 @@ struct AttnCfg {
   static constexpr int KV_STAGE = 2 * NPL * up1k(TILE);
   static constexpr int kv_v = NPL * up1k(TILE);
   static constexpr int o_bar = o_kv + STAGES * KV_STAGE;
-  static constexpr int SMEM = 1024 + o_bar + 4608;  // Bars
+  // output staging (two items, swizzled like the output tensor map) for the
+  // TMA-store epilogue; the fp32-policy planes and RP = 64 store directly
+  static constexpr bool TMA_OUT = !X3 && RP <= 32;
+  static constexpr int OUT_TILE = QT * RB;
+  static constexpr int o_stage = up1k(o_bar + 4608);
+  static constexpr int SMEM = 1024 + (TMA_OUT ? o_stage + 2 * OUT_TILE : o_bar + 4608);
   // TMEM columns: S (fp32, 128 keys), O (fp32, RP; two buffers when they fit
   // so an item's output is written while the next item runs), P (bf16 pairs),
   // X3: the P planes at t_p + 64 * plane
@@ -127,6 +140,7 @@ struct AttnCfg {
   static constexpr int TMEM_COLS = X3 ? 512 : 256;
   static constexpr int CTAS = X3 ? 1 : 2;
   static_assert(CTAS * SMEM <= 228 * 1024, "CTAs per SM");
+  static_assert(!TMA_OUT || NOB == 2, "the staged epilogue runs during the next item");
 };
 
 struct Bars {
@@ -166,17 +180,20 @@ __device__ __forceinline__ Item item_of(int w, int nqt, int heads, int batch, in
 // stride gridDim.x; consecutive items share (batch, head) so K/V stay hot in
 // L2.  Q of the next item and its first K/V tiles are prefetched while the
 // current item finishes, and TMEM / barriers are set up once per CTA.
-template <int RP, bool X3 = false>
+template <int RP, bool X3 = false, bool TMAO = false>
 __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
     k_attn_rankspace(const __grid_constant__ CUtensorMap tmQKV,
-                     const __grid_constant__ CUtensorMap tmKV, bf16* out,
+                     const __grid_constant__ CUtensorMap tmKV,
+                     const __grid_constant__ CUtensorMap tmO, bf16* out,
                      int64_t ldo, int batch, int seq, int heads, int groups, int q_off, int k_off,
                      int v_off, int causal, int plane_rows, int64_t out_ps) {
   using C = AttnCfg<RP, X3>;
+  constexpr bool staged = C::TMA_OUT && TMAO;
   CTA_T(0);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1 KB aligned by pointer arithmetic on the __shared__ array, so the
+  // compiler keeps the shared address space (LDS / STS, not generic LD / ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Bars* bars = reinterpret_cast<Bars*>(smem + C::o_bar);
   const uint32_t warp = warp_id(), lane = lane_id();
   const int nqt = (seq + QT - 1) / QT;
@@ -187,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
   if (warp == kTma && lane == 0) {
     tma_prefetch(&tmQKV);
     tma_prefetch(&tmKV);
+    if (staged) tma_prefetch(&tmO);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->q_full[i], 1);
       mbar_init(&bars->q_empty[i], 1);
@@ -368,10 +386,43 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
     // O / l of a finished item -> out (rank space); releases its O buffer.
     // The partner half's l is in xsum[item parity], written before a named
     // barrier both halves have passed since.
-    auto epilogue = [&](int it_e, int row0_e, int q0_e, int h_e, float l_e) {
+    // TMA-store form: each lane-quadrant pair (warps q, q+4) stages its 32
+    // rows in shared memory (item parity buffer) and one thread stores them as
+    // a [32 x RP] box of the [batch, seq, H*RP] output map, so the scattered
+    // row stores leave the softmax warps' path.
+    auto store_thread = [&] { return threadIdx.x < 128 && (threadIdx.x & 31) == 0; };
+    auto epilogue = [&](int it_e, int b_e, int q0_e, int h_e, float l_e) {
       const int ob = it_e % C::NOB;
-      const float inv = 1.0f / (l_e + bars->xsum[it_e & 1][half ^ 1][row]);
+      const float lt = l_e + bars->xsum[it_e & 1][half ^ 1][row];
+      const float inv = X3 ? 1.0f / lt : __fdividef(1.0f, lt);
+      const int row0_e = b_e * seq;
       const int qrow = q0_e + static_cast<int>(row);
+      if constexpr (staged) {
+        const uint32_t stg = smem_u32(smem + C::o_stage) + quad * (32 * C::RB) + (it_e & 1) * C::OUT_TILE;
+#pragma unroll
+        for (int c = 0; c < CH; c += 16) {
+          if (!owns_o) break;
+          uint32_t r[16];
+          tmem_ld16(tq + C::t_o + ob * RP + oc0 + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+            st_shared_v4(stg + swz_offset(lane, (oc0 + c) / 8 + v, C::RB),
+                         pack_bf16(__uint_as_float(r[8 * v + 0]) * inv, __uint_as_float(r[8 * v + 1]) * inv),
+                         pack_bf16(__uint_as_float(r[8 * v + 2]) * inv, __uint_as_float(r[8 * v + 3]) * inv),
+                         pack_bf16(__uint_as_float(r[8 * v + 4]) * inv, __uint_as_float(r[8 * v + 5]) * inv),
+                         pack_bf16(__uint_as_float(r[8 * v + 6]) * inv, __uint_as_float(r[8 * v + 7]) * inv));
+        }
+        tc_fence_before();
+        mbar_arrive(&bars->o_free[ob]);
+        fence_proxy_async_smem();
+        named_bar_sync(1 + quad, 64);
+        if (store_thread()) {
+          tma_store_3d(&tmO, stg, h_e * RP, q0_e + static_cast<int>(quad) * 32, b_e);
+          tma_store_commit();
+        }
+        return;
+      }
 #pragma unroll
       for (int c = 0; c < CH; c += 16) {
         if (!owns_o) break;
@@ -406,12 +457,12 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
     int gt = 0;
     int it = 0;
     // the previous item, whose output is written during this item's first tile
-    int pv_row0 = 0, pv_q0 = 0, pv_h = 0;
+    int pv_b = 0, pv_q0 = 0, pv_h = 0;
     float pv_l = 0.0f;
     for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
       const Item iw = item_of(w, nqt, heads, batch, causal);
       const int qt = iw.qt, h = iw.h, b = iw.b;
-      const int row0 = b * seq, q0 = qt * QT;
+      const int q0 = qt * QT;
       const int nji = causal ? min(nj, qt + 1) : nj;
       const uint32_t t_o = C::t_o + (it % C::NOB) * RP;
       if (threadIdx.x == 0 && it < 100) ATRACE(300 + it);
@@ -421,6 +472,7 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
         if (threadIdx.x == 0 && it == 0) ATRACE(112 + j);
         mbar_wait(&bars->s_full, t & 1);
         if (threadIdx.x == 0 && it == 0) ATRACE(144 + j);
+        if (threadIdx.x == 0 && it < 100 && j <= 1) ATRACE(1100 + it * 8 + (j ? 5 : 0));
         tc_fence_after();
         float s[KH];
 #pragma unroll
@@ -450,8 +502,12 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
         float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                            fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         bars->xmax[t & 1][half][row] = tmax;
+        // the staging buffer the coming epilogue writes: its store (two items
+        // back) has been read out before anyone passes this barrier
+        if (staged && j == 0 && store_thread()) tma_store_wait_read<1>();
         named_bar_sync(1 + quad, 64);
         tmax = fmaxf(tmax, bars->xmax[t & 1][half ^ 1][row]);
+        if (threadIdx.x == 0 && it < 100 && j <= 1) ATRACE(1100 + it * 8 + (j ? 7 : 1));
         // Lazy rescaling: keep the running max unless the tile's max exceeds
         // it by more than kRescaleSlack (log2 units), so p <= 2^slack and the
         // O / l rescale (and its TMEM round trip) is skipped for most tiles.
@@ -487,6 +543,7 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
           tc_fence_after();
           if (j >= 1 && owns_o && __any_sync(0xffffffffu, alpha != 1.0f)) rescale_o(t_o, alpha);
         }
+        if (threadIdx.x == 0 && it < 100 && j == 0) ATRACE(1100 + it * 8 + 2);
         // this half's 64 keys -> TMEM columns [t_p + 32*half, +32) of this row
         tmem_st32(tq + C::t_p + half * 32, pk);
         if (X3) {
@@ -496,18 +553,21 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars->p_full);
-        if (C::NOB == 2 && j == 0 && it > 0) epilogue(it - 1, pv_row0, pv_q0, pv_h, pv_l);
+        if (threadIdx.x == 0 && it < 100 && j == 0) ATRACE(1100 + it * 8 + 3);
+        if (C::NOB == 2 && j == 0 && it > 0) epilogue(it - 1, pv_b, pv_q0, pv_h, pv_l);
+        if (threadIdx.x == 0 && it < 100 && j == 0) ATRACE(1100 + it * 8 + 4);
         if (threadIdx.x == 0 && it < 100) ATRACE(600 + it * 4 + min(j, 3));
       }
       gt += nji;
+      if (threadIdx.x == 0 && it < 100) ATRACE(1100 + it * 8 + 6);
       bars->xsum[it & 1][half][row] = l_run;
       if (C::NOB == 1) {
         mbar_wait(&bars->o_full, (gt - 1) & 1);
         tc_fence_after();
         named_bar_sync(1 + quad, 64);
-        epilogue(it, row0, q0, h, l_run);
+        epilogue(it, b, q0, h, l_run);
       }
-      pv_row0 = row0;
+      pv_b = b;
       pv_q0 = q0;
       pv_h = h;
       pv_l = l_run;
@@ -516,9 +576,11 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
     if (C::NOB == 2 && it > 0) {  // the last item's output
       mbar_wait(&bars->o_full, (gt - 1) & 1);
       tc_fence_after();
+      if (staged && store_thread()) tma_store_wait_read<1>();
       named_bar_sync(1 + quad, 64);
-      epilogue(it - 1, pv_row0, pv_q0, pv_h, pv_l);
+      epilogue(it - 1, pv_b, pv_q0, pv_h, pv_l);
     }
+    if (staged && store_thread()) tma_store_wait<0>();
   }
   if (threadIdx.x == 0) ATRACE(3);
   tc_fence_before();
@@ -530,15 +592,36 @@ __global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
   CTA_T(2);
 }
 
-template <int RP, bool X3 = false>
-void launch_attn(const AttnTcArgs& a, cudaStream_t s) {
+// developer A/B switch: FSVD_ATTN_TMA_OUT=0 writes the output with per-thread stores
+bool attn_tma_out_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FSVD_ATTN_TMA_OUT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int RP, bool X3, bool TMAO>
+void launch_attn_k(const AttnTcArgs& a, cudaStream_t s, const CUtensorMap& tm, const CUtensorMap& tkv,
+                   const CUtensorMap& to, int T) {
   using C = AttnCfg<RP, X3>;
   static bool attr = false;
   if (!attr) {
-    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_attn_rankspace<RP, X3>,
+    FSVD_CUDA_CHECK(cudaFuncSetAttribute(k_attn_rankspace<RP, X3, TMAO>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
+  const int items = ((a.seq + QT - 1) / QT) * a.heads * a.batch;
+  const int grid = items < C::CTAS * num_sms() ? items : C::CTAS * num_sms();
+  launch_pdl(k_attn_rankspace<RP, X3, TMAO>, dim3(grid), dim3(kThreads), C::SMEM, s, tm, tkv, to,
+             a.out, a.ldo, a.batch, a.seq, a.heads, a.groups, a.q_off, a.k_off, a.v_off,
+             a.causal ? 1 : 0, X3 ? T : 0, X3 ? a.out_ps : (int64_t)0);
+  check_launch("k_attn_rankspace");
+}
+
+template <int RP, bool X3 = false>
+void launch_attn(const AttnTcArgs& a, cudaStream_t s) {
+  using C = AttnCfg<RP, X3>;
   const int T = a.batch * a.seq;
   // X3: the three planes of qkv stacked ([3T, qkv_cols], plane p at row p*T)
   const CUtensorMap tm = tmap_bf16(a.qkv, (uint64_t)C::NPL * T, a.qkv_cols, a.ldq, 128, RP,
@@ -547,12 +630,19 @@ void launch_attn(const AttnTcArgs& a, cudaStream_t s) {
   const CUtensorMap tkv = a.kv == nullptr ? tm
                                           : tmap_bf16(a.kv, (uint64_t)C::NPL * T, a.kv_cols, a.ldkv,
                                                       128, RP, swizzle_for_row_bytes(C::RB));
-  const int items = ((a.seq + QT - 1) / QT) * a.heads * a.batch;
-  const int grid = items < C::CTAS * num_sms() ? items : C::CTAS * num_sms();
-  launch_pdl(k_attn_rankspace<RP, X3>, dim3(grid), dim3(kThreads), C::SMEM, s, tm, tkv, a.out, a.ldo,
-             a.batch, a.seq, a.heads, a.groups, a.q_off, a.k_off, a.v_off, a.causal ? 1 : 0,
-             X3 ? T : 0, X3 ? a.out_ps : (int64_t)0);
-  check_launch("k_attn_rankspace");
+  // output as [batch, seq, H*RP] boxes of [32 x RP] (TMA store epilogue) when
+  // the layout allows a tensor map (16-byte aligned base and row stride)
+  const bool tma_out = C::TMA_OUT && reinterpret_cast<uintptr_t>(a.out) % 16 == 0 &&
+                       a.ldo % 8 == 0 && attn_tma_out_enabled();
+  const CUtensorMap to = tma_out ? make_tmap_3d(a.out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                                (uint64_t)a.heads * RP, a.seq, a.batch, a.ldo,
+                                                (uint64_t)a.seq * a.ldo, RP, 32,
+                                                swizzle_for_row_bytes(C::RB))
+                                 : tm;
+  if (tma_out)
+    launch_attn_k<RP, X3, C::TMA_OUT>(a, s, tm, tkv, to, T);
+  else
+    launch_attn_k<RP, X3, false>(a, s, tm, tkv, to, T);
 }
 
 }  // namespace

@@ -81,4 +81,27 @@ CUtensorMap make_tmap_2d(const void* base, CUtensorMapDataType dtype, int elem_b
   return map;
 }
 
+CUtensorMap make_tmap_3d(const void* base, CUtensorMapDataType dtype, int elem_bytes,
+                         uint64_t d0, uint64_t d1, uint64_t d2, uint64_t ld1, uint64_t ld2,
+                         uint32_t box0, uint32_t box1, TmaSwizzle swz) {
+  CUtensorMap map;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {ld1 * static_cast<uint64_t>(elem_bytes),
+                           ld2 * static_cast<uint64_t>(elem_bytes)};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMapSwizzle s = swz == TmaSwizzle::B128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                         : swz == TmaSwizzle::B64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                         : swz == TmaSwizzle::B32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                  : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = encode_fn()(&map, dtype, 3, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, s, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw CudaError("cuTensorMapEncodeTiled (3d) failed (" + std::to_string(static_cast<int>(r)) +
+                    ") dims=" + std::to_string(d0) + "x" + std::to_string(d1) + "x" +
+                    std::to_string(d2));
+  return map;
+}
+
 }  // namespace fsvd

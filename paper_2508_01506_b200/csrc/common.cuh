@@ -85,6 +85,11 @@ CUtensorMap make_tmap_2d(const void* base, CUtensorMapDataType dtype, int elem_b
                          uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows,
                          uint32_t box_cols, TmaSwizzle swz);
 
+// [d2][d1][d0] elements, d0 contiguous, ld1 / ld2 the strides of d1 / d2 in
+// elements; box {box0, box1, 1}
+CUtensorMap make_tmap_3d(const void* base, CUtensorMapDataType dtype, int elem_bytes,
+                         uint64_t d0, uint64_t d1, uint64_t d2, uint64_t ld1, uint64_t ld2,
+                         uint32_t box0, uint32_t box1, TmaSwizzle swz);
 inline CUtensorMap tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
                              uint32_t box_rows, uint32_t box_cols, TmaSwizzle swz) {
   return make_tmap_2d(base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, cols, ld, box_rows,

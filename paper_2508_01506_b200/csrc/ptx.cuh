@@ -145,6 +145,17 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
       "r"(smem_u32(src)), "r"(c0), "r"(c1)
       : "memory");
 }
+// 3-D store: box {c0, c1, c2} (innermost first); rows past a dimension's
+// extent are clipped, so a [batch, seq, cols] map never writes a short
+// sequence's tail into the next sequence
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int32_t c0,
+                                             int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 __device__ __forceinline__ void tma_store_2d_u32(const CUtensorMap* map, uint32_t src, int32_t c0,
                                                  int32_t c1) {
   asm volatile(

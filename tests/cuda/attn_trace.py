@@ -34,3 +34,7 @@ print("item | tma_q  mma_start  softmax_start  tile_p_arrive[0..3]")
 for it in range(12):
     print(f"{it:3d} | {r(500 + it):7d} {r(400 + it):7d} {r(300 + it):7d} | " +
           " ".join(f"{r(600 + it * 4 + j):7d}" for j in range(4)))
+print("item (softmax thread 0, tile 0 / 1): got_s0 maxx0 got_o0 p_arr0 epi_done | got_s1 maxx1 | item_end")
+for it in range(12):
+    print(f"{it:3d} | " + " ".join(f"{r(1100 + it * 8 + k):7d}" for k in (0, 1, 2, 3, 4)) + " | " +
+          " ".join(f"{r(1100 + it * 8 + k):7d}" for k in (5, 7)) + f" | {r(1100 + it * 8 + 6):7d}")

@@ -61,3 +61,28 @@ for tu in [k for k in ("gemm", "attn", "gemm_ln", "ffn") if k in res]:
     rel = (a[:, 2] - a[:, 1].min()) / 1e3
     print("          exits (us after first release), deciles:",
           " ".join(f"{v:6.2f}" for v in np.percentile(rel, [0, 10, 25, 50, 75, 90, 100])))
+if "attn" in res and os.environ.get("ATTN_DETAIL"):
+    # K2: exit time by the CTA's item count and by its SM's total item count / die half
+    a = res["attn"].astype(np.int64)
+    rel = (a[:, 2] - a[:, 1].min()) / 1e3
+    grid = len(a)
+    items = (M // 128) * 12 * B
+    bid = np.arange(grid)
+    n_it = (items - bid + grid - 1) // grid
+    sm = res["attn"][:, 5].astype(np.int64)
+    sm_items = {s: n_it[sm == s].sum() for s in set(sm.tolist())}
+    for k in sorted(set(n_it.tolist())):
+        sel = n_it == k
+        print(f"  attn CTAs with {k} items: {sel.sum():4d}, exit min {rel[sel].min():6.2f} med {np.median(rel[sel]):6.2f} max {rel[sel].max():6.2f}")
+    tot = np.array([sm_items[s] for s in sm])
+    for k in sorted(set(tot.tolist())):
+        sel = tot == k
+        print(f"  attn CTAs on SMs with {k} items: {sel.sum():4d}, exit med {np.median(rel[sel]):6.2f} max {rel[sel].max():6.2f}")
+    for half in (0, 1):
+        sel = (sm >= 74) == bool(half)
+        print(f"  attn SMs {'74-147' if half else '0-73'}: exit med {np.median(rel[sel]):6.2f} max {rel[sel].max():6.2f}")
+    per_item = (rel - 0) / n_it
+    print("  attn per-item time by smid (first 16 SMs):", " ".join(f"{s}:{np.mean(per_item[sm == s]):.2f}" for s in range(16)))
+    order = np.argsort(rel)
+    print("  slowest 12 CTAs (bid, sm, items, exit):", [(int(b), int(sm[b]), int(n_it[b]), round(float(rel[b]), 1)) for b in order[-12:]])
+    print("  fastest 12 CTAs (bid, sm, items, exit):", [(int(b), int(sm[b]), int(n_it[b]), round(float(rel[b]), 1)) for b in order[:12]])
