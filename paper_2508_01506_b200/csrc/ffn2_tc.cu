@@ -179,8 +179,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) TRACE2(0);
   using C = Ffn2Cfg<FR>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays __shared__
   Ffn2Bars* bars = reinterpret_cast<Ffn2Bars*>(smem + C::o_bar);
   const uint32_t warp = warp_id(), lane = lane_id();
   const uint32_t rank = cluster_rank();

@@ -191,8 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = FfnCfg<FR, WIDE, X3>;
   CTA_T(0);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays __shared__
   FfnBars* bars = reinterpret_cast<FfnBars*>(smem + C::o_bar);
   const uint32_t warp = warp_id(), lane = lane_id();
   const int m0 = blockIdx.x * BMr;

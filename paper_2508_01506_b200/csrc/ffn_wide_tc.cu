@@ -99,8 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                bf16* __restrict__ z_out) {
   using C = WideCfg<FR>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays __shared__
   WideBars* bars = reinterpret_cast<WideBars*>(smem + C::o_bar);
   const uint32_t warp = warp_id(), lane = lane_id();
   const int rank = static_cast<int>(cluster_rank()), ns = static_cast<int>(cluster_nctarank());

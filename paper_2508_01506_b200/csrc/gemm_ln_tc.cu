@@ -90,8 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               bf16* sum_out, int seq_tiles) {
   CTA_T(0);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays __shared__
   const int KA = K / 64;        // A atoms
   const int NP = N / PN;        // output pieces
   uint8_t* sA = smem;
