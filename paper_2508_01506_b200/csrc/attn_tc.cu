@@ -181,7 +181,7 @@ __device__ __forceinline__ Item item_of(int w, int nqt, int heads, int batch, in
 // L2.  Q of the next item and its first K/V tiles are prefetched while the
 // current item finishes, and TMEM / barriers are set up once per CTA.
 template <int RP, bool X3 = false, bool TMAO = false>
-__global__ void __launch_bounds__(kThreads, X3 ? 1 : 2)
+__global__ void __launch_bounds__(kThreads) __maxnreg__(X3 ? 168 : 96)  // X3: one CTA per SM
     k_attn_rankspace(const __grid_constant__ CUtensorMap tmQKV,
                      const __grid_constant__ CUtensorMap tmKV,
                      const __grid_constant__ CUtensorMap tmO, bf16* out,

@@ -21,6 +21,9 @@
 // i+1's MMAs.
 #include <cstdlib>
 
+#include <algorithm>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -76,6 +79,27 @@ struct GemmCfg {
 __device__ __forceinline__ int x3_plane_a(int seg) { return (0x120100 >> (4 * seg)) & 15; }
 __device__ __forceinline__ int x3_plane_b(int seg) { return (0x102010 >> (4 * seg)) & 15; }
 
+// Tile walk.  Tiles are listed full-width first ((m, n) row-major over the
+// N / BN full column tiles), then the narrow last column (N % BN wide) of
+// every row tile; CTA b takes list positions k * G + (k even ? b : G-1-b)
+// (a snake over the size-sorted list), so when N % BN != 0 the narrow tiles
+// fill the CTAs that got one full tile fewer.  Narrow tiles run MMAs of
+// their own width.
+struct TileWalk {
+  int num_m, nfull, tiles, G, bid;
+  __device__ int pos(int k) const { return k * G + ((k & 1) ? G - 1 - bid : bid); }
+  __device__ void at(int p, int bn, int& m0, int& n0) const {
+    const int nf = num_m * nfull;
+    if (p < nf) {
+      m0 = (p / nfull) * BM;
+      n0 = (p % nfull) * bn;
+    } else {
+      m0 = (p - nf) * BM;
+      n0 = nfull * bn;
+    }
+  }
+};
+
 template <int BN, int STAGES, bool X3 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -101,6 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tiles = num_m * num_n;
   const int nk = (K + BK - 1) / BK;
   const int nk3 = X3 ? 6 * nk : nk;  // K blocks of the six plane-pair sweeps
+  const TileWalk walk{num_m, N / BN, tiles, static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x)};
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -137,8 +162,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int me = warp == 0 ? 0 : 1;
       uint32_t stage = 0, phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+      for (int k = 0; walk.pos(k) < tiles; ++k) {
+        int m0, n0;
+        walk.at(walk.pos(k), BN, m0, n0);
         for (int kb3 = 0; kb3 < nk3; ++kb3, ++it) {
           if ((it & 1) == me) {
             const int seg = X3 ? kb3 / nk : 0, kb = kb3 - seg * nk;
@@ -156,12 +182,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (warp-uniform loop, one elected lane issues) ----------------
     {
-      constexpr uint32_t idesc = idesc_bf16(BM, BN);
       const uint64_t dhi = desc_hi_kmajor(128);
       const uint64_t da = desc_at(dhi, smem_u32(sA)), db = desc_at(dhi, smem_u32(sB));
       uint32_t stage = 0, phase = 0;
       int i = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      for (int k = 0; walk.pos(k) < tiles; ++k, ++i) {
+        int m0, n0;
+        walk.at(walk.pos(k), BN, m0, n0);
+        // narrow last column: an MMA of its own width (rounded up to 16)
+        const uint32_t idesc = idesc_bf16(BM, min(BN, (N - n0 + 15) / 16 * 16));
         const uint32_t acc = i & 1, use = i >> 1;
         if (lane == 0) GTRACE(16 + 4 * i);
         mbar_wait(&tempty[acc], (use & 1) ^ 1);
@@ -175,8 +204,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t b0 = db + ((stage * Cfg::B_BYTES) >> 4);
           if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              mma_bf16_ss(d, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
+            for (int kk = 0; kk < BK / 16; ++kk)
+              mma_bf16_ss(d, a0 + 2 * kk, b0 + 2 * kk, idesc, (kb | kk) != 0);
             mma_commit(&empty[stage]);
           }
           __syncwarp();
@@ -199,8 +228,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t s_c = smem_u32(sC);
     uint32_t nbox = 0;
     int i = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
-      const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+    for (int k = 0; walk.pos(k) < tiles; ++k, ++i) {
+      int m0, n0;
+      walk.at(walk.pos(k), BN, m0, n0);
       const uint32_t acc = i & 1, use = i >> 1;
       if (threadIdx.x == 64) GTRACE(512 + 4 * i);
       mbar_wait(&tfull[acc], use & 1);
@@ -513,6 +543,30 @@ void launch_gemm(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C
   check_launch("k_gemm_bf16");
 }
 
+// Heaviest CTA of the snake walk (TileWalk), in 64-column units of MMA work.
+int snake_units(int M, int N, int BN) {
+  const int G = num_sms();
+  const int num_m = (M + BM - 1) / BM, nfull = N / BN, rem = N % BN;
+  const int tiles = num_m * (nfull + (rem ? 1 : 0));
+  std::vector<int> load(G, 0);
+  for (int p = 0; p < tiles; ++p) {
+    const int k = p / G, r = p % G, b = (k & 1) ? G - 1 - r : r;
+    load[b] += (p < num_m * nfull ? BN : rem + 63) / 64;
+  }
+  return *std::max_element(load.begin(), load.end());
+}
+
+// N divisible by 192 but not 256 (the folded QKV width 1152 at cfg2): 256-wide
+// tiles plus a narrow last column when their snake walk is lighter
+// (cfg2: 16 vs 18 units on the busiest CTA).  FSVD_GEMM_SNAKE256=0 keeps 192.
+bool prefer_256(int M, int N) {
+  static const bool on = [] {
+    const char* e = getenv("FSVD_GEMM_SNAKE256");
+    return !(e && e[0] == '0');
+  }();
+  return on && N > 256 && snake_units(M, N, 256) < snake_units(M, N, 192);
+}
+
 }  // namespace
 
 bool gemm_bf16_supported(int M, int N, int K, int64_t lda, int64_t ldb, int64_t ldc) {
@@ -549,7 +603,7 @@ void gemm_bf16(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf16* C, 
   }
   if (M <= 128 && N % 64 == 0 && N >= 128)  // one row tile (decode rows): most CTAs
     launch_gemm<64, 8>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
-  else if (N % 256 == 0)
+  else if (N % 256 == 0 || (N % 192 == 0 && prefer_256(M, N)))
     launch_gemm<256, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
   else if (N % 192 == 0)
     launch_gemm<192, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, act, s, resid, ldr);
@@ -572,6 +626,9 @@ void gemm_bf16_split(const bf16* A, int64_t lda, const bf16* B, int64_t ldb, bf1
   }();
   if (bn == 128 && N % 128 == 0)
     launch_gemm<128, 6>(A, lda, B, ldb, C, ldc, M, N, K, bias, ACT_NONE, s, nullptr, 0, C2,
+                        nullptr, 0, split_n, ldc2);
+  else if (N % 192 == 0 && prefer_256(M, N))
+    launch_gemm<256, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, ACT_NONE, s, nullptr, 0, C2,
                         nullptr, 0, split_n, ldc2);
   else if (N % 192 == 0)
     launch_gemm<192, 4>(A, lda, B, ldb, C, ldc, M, N, K, bias, ACT_NONE, s, nullptr, 0, C2,
