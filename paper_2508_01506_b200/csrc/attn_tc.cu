@@ -42,6 +42,10 @@
 // per-thread row stores this is -0.8% on the 12-layer step; keeping Bars in
 // the shared window (LDS / STS instead of generic loads) and the spill
 // reduction that came with it another -1.3% (`tools/ab.sh`).
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -147,6 +151,8 @@ struct Bars {
   uint64_t q_full[2], q_empty[2];
   uint64_t kv_full[3], kv_empty[3];
   uint64_t s_full, s_free, p_full, o_full, o_free[2];
+  uint64_t item_full[4], item_empty[4];  // dynamic schedule: item ids, producer -> MMA / softmax
+  int item_ring[4];
   uint32_t tmem;
   float xmax[2][2][QT];  // [tile parity][half][row]: per-half row maxima
   float xsum[2][2][QT];  // [item parity][half][row]: per-half row sums of an item
@@ -184,7 +190,7 @@ template <int RP, bool X3 = false, bool TMAO = false>
 __global__ void __launch_bounds__(kThreads) __maxnreg__(X3 ? 168 : 96)  // X3: one CTA per SM
     k_attn_rankspace(const __grid_constant__ CUtensorMap tmQKV,
                      const __grid_constant__ CUtensorMap tmKV,
-                     const __grid_constant__ CUtensorMap tmO, bf16* out,
+                     const __grid_constant__ CUtensorMap tmO, int* sched, bf16* out,
                      int64_t ldo, int batch, int seq, int heads, int groups, int q_off, int k_off,
                      int v_off, int causal, int plane_rows, int64_t out_ps) {
   using C = AttnCfg<RP, X3>;
@@ -219,6 +225,10 @@ __global__ void __launch_bounds__(kThreads) __maxnreg__(X3 ? 168 : 96)  // X3: o
     mbar_init(&bars->o_full, 1);
     mbar_init(&bars->o_free[0], kSoftmax);
     mbar_init(&bars->o_free[1], kSoftmax);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&bars->item_full[i], 1);
+      mbar_init(&bars->item_empty[i], 1 + kSoftmax);
+    }
     fence_barrier_init();
   }
   if (threadIdx.x == 0) ATRACE(0);
@@ -231,13 +241,31 @@ __global__ void __launch_bounds__(kThreads) __maxnreg__(X3 ? 168 : 96)  // X3: o
   CTA_T(1);
   const uint32_t tmem = bars->tmem;
   const uint32_t s_q = smem_u32(smem + C::o_q), s_kv = smem_u32(smem + C::o_kv);
+  // Work items: the first is blockIdx.x; then, with a schedule counter
+  // (sched[0]), the TMA thread takes the next free one (gridDim.x +
+  // atomicAdd) as it starts loading it and publishes the id through a
+  // four-slot ring (-1: done), so a CTA that runs ahead -- or shares its SM
+  // with a slower one -- takes more items; without one, stride gridDim.x.
+  const bool dyn = sched != nullptr;
+  const int G = static_cast<int>(gridDim.x);
+  auto ring_get = [&](int k) -> int {
+    mbar_wait(&bars->item_full[k & 3], (k >> 2) & 1);
+    return reinterpret_cast<volatile int*>(bars->item_ring)[k & 3];
+  };
 
   if (warp == kTma) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t st = 0, ph = 0;
-      int it = 0;
-      for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+      int w = blockIdx.x;
+      for (int it = 0;; ++it) {
+        if (it > 0) w = dyn ? G + atomicAdd(sched, 1) : w + G;
+        if (dyn) {
+          mbar_wait(&bars->item_empty[it & 3], ((it >> 2) & 1) ^ 1);
+          reinterpret_cast<volatile int*>(bars->item_ring)[it & 3] = w < items ? w : -1;
+          mbar_arrive(&bars->item_full[it & 3]);
+        }
+        if (w >= items) break;
         const Item iw = item_of(w, nqt, heads, batch, causal);
         const int qt = iw.qt, h = iw.h, b = iw.b;
         const int g = h / hpg, row0 = b * seq;
@@ -298,12 +326,18 @@ __global__ void __launch_bounds__(kThreads) __maxnreg__(X3 ? 168 : 96)  // X3: o
     // S of an item's first tile is issued while the previous item's last
     // tile is still in the softmax (right after its S was read out), so the
     // softmax warps find it ready when they move on.
-    if (static_cast<int>(blockIdx.x) < items) {
+    int w = dyn ? ring_get(0) : static_cast<int>(blockIdx.x);
+    if (w >= 0 && w < items) {
       mbar_wait(&bars->q_full[0], 0);
       if (lane == 0) ATRACE(1);
       issue_s(0, 0);
     }
-    for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+    for (; w >= 0 && w < items; ++it) {
+      if (dyn && lane == 0) mbar_arrive(&bars->item_empty[it & 3]);  // id read
+      int w_next = -2;  // not fetched yet
+      auto fetch_next = [&] {
+        if (w_next == -2) w_next = dyn ? ring_get(it + 1) : (w + G < items ? w + G : -1);
+      };
       const int qs = it & 1;
       const int nji = causal ? min(nj, item_of(w, nqt, heads, batch, causal).qt + 1) : nj;
       if (lane == 0 && it < 100) ATRACE(400 + it);
@@ -317,7 +351,8 @@ __global__ void __launch_bounds__(kThreads) __maxnreg__(X3 ? 168 : 96)  // X3: o
         } else {
           if (elect_one()) mma_commit(&bars->q_empty[qs]);  // after this item's last S
           __syncwarp();
-          if (w + static_cast<int>(gridDim.x) < items) {
+          fetch_next();  // (the producer has loaded this item's last tile: no wait on us)
+          if (w_next >= 0 && w_next < items) {
             mbar_wait(&bars->q_full[qs ^ 1], ((it + 1) >> 1) & 1);
             issue_s(t + 1, qs ^ 1);
           }
@@ -356,6 +391,8 @@ __global__ void __launch_bounds__(kThreads) __maxnreg__(X3 ? 168 : 96)  // X3: o
         if (C::STAGES == 1) next_s(j, t);
       }
       gt += nji;
+      fetch_next();
+      w = w_next;
     }
   } else {
     // ------------------------------------------------ softmax (8 warps)
@@ -459,7 +496,9 @@ __global__ void __launch_bounds__(kThreads) __maxnreg__(X3 ? 168 : 96)  // X3: o
     // the previous item, whose output is written during this item's first tile
     int pv_b = 0, pv_q0 = 0, pv_h = 0;
     float pv_l = 0.0f;
-    for (int w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+    for (int w = dyn ? ring_get(0) : static_cast<int>(blockIdx.x); w >= 0 && w < items;
+         w = dyn ? ring_get(it + 1) : w + G, ++it) {
+      if (dyn) mbar_arrive(&bars->item_empty[it & 3]);  // id read
       const Item iw = item_of(w, nqt, heads, batch, causal);
       const int qt = iw.qt, h = iw.h, b = iw.b;
       const int q0 = qt * QT;
@@ -589,7 +628,50 @@ __global__ void __launch_bounds__(kThreads) __maxnreg__(X3 ? 168 : 96)  // X3: o
     tc_fence_after();
     tmem_free<C::TMEM_COLS>(tmem);
   }
+  // the last CTA out returns the schedule counters to zero for the next
+  // launch on this stream (every CTA has taken its last item by now)
+  if (dyn && threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(sched + 1, 1) == G - 1) {
+      atomicExch(sched, 0);
+      atomicExch(sched + 1, 0);
+    }
+  }
   CTA_T(2);
+}
+
+// Per-(device, stream) counters of the dynamic item schedule ([next item,
+// CTAs done], zero between launches).  Allocated outside stream capture on
+// first use; none (static schedule) while a stream is being captured before
+// that, past 64 streams, or with FSVD_ATTN_DYN=0.
+int* attn_sched_slot(cudaStream_t s) {
+  static const bool on = [] {
+    const char* e = getenv("FSVD_ATTN_DYN");
+    return !(e && e[0] == '0');
+  }();
+  if (!on) return nullptr;
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, int*> slots;
+  static std::map<int, std::pair<int*, int>> pools;
+  int dev = 0;
+  FSVD_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  const auto f = slots.find({dev, s});
+  if (f != slots.end()) return f->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  FSVD_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return nullptr;
+  auto& pool = pools[dev];
+  constexpr int kSlots = 64, kStride = 32;  // 128 B apart
+  if (pool.first == nullptr) {
+    FSVD_CUDA_CHECK(cudaMalloc(&pool.first, kSlots * kStride * sizeof(int)));
+    FSVD_CUDA_CHECK(cudaMemset(pool.first, 0, kSlots * kStride * sizeof(int)));
+    FSVD_CUDA_CHECK(cudaDeviceSynchronize());
+  }
+  if (pool.second >= kSlots) return nullptr;
+  int* p = pool.first + kStride * pool.second++;
+  slots[{dev, s}] = p;
+  return p;
 }
 
 // developer A/B switch: FSVD_ATTN_TMA_OUT=0 writes the output with per-thread stores
@@ -613,8 +695,10 @@ void launch_attn_k(const AttnTcArgs& a, cudaStream_t s, const CUtensorMap& tm, c
   }
   const int items = ((a.seq + QT - 1) / QT) * a.heads * a.batch;
   const int grid = items < C::CTAS * num_sms() ? items : C::CTAS * num_sms();
+  // causal items are pre-ordered longest first for the stride walk: static
+  int* sched = a.causal || grid >= items ? nullptr : attn_sched_slot(s);
   launch_pdl(k_attn_rankspace<RP, X3, TMAO>, dim3(grid), dim3(kThreads), C::SMEM, s, tm, tkv, to,
-             a.out, a.ldo, a.batch, a.seq, a.heads, a.groups, a.q_off, a.k_off, a.v_off,
+             sched, a.out, a.ldo, a.batch, a.seq, a.heads, a.groups, a.q_off, a.k_off, a.v_off,
              a.causal ? 1 : 0, X3 ? T : 0, X3 ? a.out_ps : (int64_t)0);
   check_launch("k_attn_rankspace");
 }
