@@ -42,10 +42,6 @@
 // per-thread row stores this is -0.8% on the 12-layer step; keeping Bars in
 // the shared window (LDS / STS instead of generic loads) and the spill
 // reduction that came with it another -1.3% (`tools/ab.sh`).
-#include <map>
-#include <mutex>
-#include <utility>
-
 #include "common.cuh"
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -640,40 +636,6 @@ __global__ void __launch_bounds__(kThreads) __maxnreg__(X3 ? 168 : 96)  // X3: o
   CTA_T(2);
 }
 
-// Per-(device, stream) counters of the dynamic item schedule ([next item,
-// CTAs done], zero between launches).  Allocated outside stream capture on
-// first use; none (static schedule) while a stream is being captured before
-// that, past 64 streams, or with FSVD_ATTN_DYN=0.
-int* attn_sched_slot(cudaStream_t s) {
-  static const bool on = [] {
-    const char* e = getenv("FSVD_ATTN_DYN");
-    return !(e && e[0] == '0');
-  }();
-  if (!on) return nullptr;
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, int*> slots;
-  static std::map<int, std::pair<int*, int>> pools;
-  int dev = 0;
-  FSVD_CUDA_CHECK(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> lock(mu);
-  const auto f = slots.find({dev, s});
-  if (f != slots.end()) return f->second;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  FSVD_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
-  if (cs != cudaStreamCaptureStatusNone) return nullptr;
-  auto& pool = pools[dev];
-  constexpr int kSlots = 64, kStride = 32;  // 128 B apart
-  if (pool.first == nullptr) {
-    FSVD_CUDA_CHECK(cudaMalloc(&pool.first, kSlots * kStride * sizeof(int)));
-    FSVD_CUDA_CHECK(cudaMemset(pool.first, 0, kSlots * kStride * sizeof(int)));
-    FSVD_CUDA_CHECK(cudaDeviceSynchronize());
-  }
-  if (pool.second >= kSlots) return nullptr;
-  int* p = pool.first + kStride * pool.second++;
-  slots[{dev, s}] = p;
-  return p;
-}
-
 // developer A/B switch: FSVD_ATTN_TMA_OUT=0 writes the output with per-thread stores
 bool attn_tma_out_enabled() {
   static const bool on = [] {
@@ -696,7 +658,7 @@ void launch_attn_k(const AttnTcArgs& a, cudaStream_t s, const CUtensorMap& tm, c
   const int items = ((a.seq + QT - 1) / QT) * a.heads * a.batch;
   const int grid = items < C::CTAS * num_sms() ? items : C::CTAS * num_sms();
   // causal items are pre-ordered longest first for the stride walk: static
-  int* sched = a.causal || grid >= items ? nullptr : attn_sched_slot(s);
+  int* sched = a.causal || grid >= items || !sched_enabled("FSVD_ATTN_DYN") ? nullptr : sched_counter(s);
   launch_pdl(k_attn_rankspace<RP, X3, TMAO>, dim3(grid), dim3(kThreads), C::SMEM, s, tm, tkv, to,
              sched, a.out, a.ldo, a.batch, a.seq, a.heads, a.groups, a.q_off, a.k_off, a.v_off,
              a.causal ? 1 : 0, X3 ? T : 0, X3 ? a.out_ps : (int64_t)0);

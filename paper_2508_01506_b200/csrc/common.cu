@@ -1,7 +1,10 @@
-// common.cu -- TMA descriptor encoding, launch accounting, device queries.
+// common.cu -- TMA descriptor encoding, launch accounting, device queries,
+// dynamic-schedule counters.
 #include <atomic>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "common.cuh"
 
@@ -102,6 +105,42 @@ CUtensorMap make_tmap_3d(const void* base, CUtensorMapDataType dtype, int elem_b
                     ") dims=" + std::to_string(d0) + "x" + std::to_string(d1) + "x" +
                     std::to_string(d2));
   return map;
+}
+
+// Per-(device, stream) work counters of the dynamic tile / item schedules
+// ([next, CTAs done]; zero between launches: the last CTA out resets them).
+// One slot serves every kernel on a stream: a kernel touches it only after
+// griddepcontrol.wait, i.e. after the previous kernel has finished.
+// Allocated outside stream capture on first use; null (static schedule)
+// while a stream is captured before that, or past 64 streams.
+int* sched_counter(cudaStream_t s) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, int*> slots;
+  static std::map<int, std::pair<int*, int>> pools;
+  int dev = 0;
+  FSVD_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  const auto f = slots.find({dev, s});
+  if (f != slots.end()) return f->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  FSVD_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return nullptr;
+  auto& pool = pools[dev];
+  constexpr int kSlots = 64, kStride = 32;  // 128 B apart
+  if (pool.first == nullptr) {
+    FSVD_CUDA_CHECK(cudaMalloc(&pool.first, kSlots * kStride * sizeof(int)));
+    FSVD_CUDA_CHECK(cudaMemset(pool.first, 0, kSlots * kStride * sizeof(int)));
+    FSVD_CUDA_CHECK(cudaDeviceSynchronize());
+  }
+  if (pool.second >= kSlots) return nullptr;
+  int* p = pool.first + kStride * pool.second++;
+  slots[{dev, s}] = p;
+  return p;
+}
+
+bool sched_enabled(const char* env) {
+  const char* e = getenv(env);  // developer A/B switches: =0 keeps the static schedule
+  return !(e && e[0] == '0');
 }
 
 }  // namespace fsvd

@@ -33,6 +33,9 @@ int num_sms();
 
 // FSVD_NO_PDL=1 turns programmatic dependent launch off (developer traces).
 bool pdl_enabled();
+// dynamic-schedule counters for kernels launched on stream s (see common.cu)
+int* sched_counter(cudaStream_t s);
+bool sched_enabled(const char* env);
 // Launch with programmatic stream serialization (see ptx::pdl_wait).
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
