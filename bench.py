@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes as C
+import datetime
 import json
 import math
 import os
@@ -95,23 +96,44 @@ def relaunch(n):
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """nvidia-smi sampler (every 10 ms, host-timestamped).  Started before the
+    warm-up and waited on until it has produced a sample, so it is running
+    when the timed region opens; stop() keeps the samples stamped inside
+    [mark(), stop()] -- the timed region -- and falls back to the samples
+    under load when the region was shorter than the sampling period."""
 
     def __init__(self, gpu_index):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        self.t0 = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-i", str(gpu_index), "-lms", "20"], stdout=self.f,
+                                       "-i", str(gpu_index), "-lms", "10"], stdout=self.f,
                                       stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
+    def wait_ready(self, timeout=10.0):
+        """Block until the sampler has written its first line."""
+        end = time.time() + timeout
+        while self.p is not None and time.time() < end:
+            try:
+                if os.path.getsize(self.f.name) > 0:
+                    return
+            except OSError:
+                pass
+            time.sleep(0.01)
+
+    def mark(self):
+        self.t0 = time.time()
+
     def stop(self):
         if self.p is None:
             return None
+        t1 = time.time()
+        time.sleep(0.03)  # the sample in flight when the region closed
         self.p.terminate()
         try:
             self.p.wait(timeout=5)
@@ -119,26 +141,30 @@ class Clocks:
             self.p.kill()
         self.f.flush()
         self.f.seek(0)
-        sm, mx, reasons = [], 0, set()
+        rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.f.read().splitlines():
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 9:
                 continue
             try:
-                sm.append(float(parts[1]))
-                mx = max(mx, float(parts[2]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(parts[1]), float(parts[2]),
+                             {n for n, v in zip(names, parts[5:9]) if v.lower().startswith("active")}))
             except ValueError:
                 continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
         os.unlink(self.f.name)
-        if not sm:
+        if not rows:
             return None
-        loaded = [s for s in sm if s > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        mx = max(r[2] for r in rows)
+        inside = [r for r in rows if self.t0 is not None and self.t0 <= r[0] <= t1 + 0.005]
+        window = "timed region"
+        if not inside:  # region shorter than the sampling period: samples under load
+            inside = [r for r in rows if r[1] > 0.5 * mx] or rows
+            window = "under load around the timed region"
+        reasons = set().union(*(r[3] for r in inside))
+        return {"sm_mhz": statistics.median(r[1] for r in inside), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(inside), "window": window}
 
 
 # This pool's MEASURED_PEAKS.json as recorded in SURVEY.md (line 6) when the
@@ -417,16 +443,18 @@ def run_gpu(args):
                 pending[k].wait()
                 pending[k] = None
 
+    clocks = Clocks(local)  # sampling from the warm-up on
     for _ in range(args.warmup):
         step()
     drain()
     torch.cuda.synchronize(dev)
     assert torch.isfinite(out[:s1 - s0].float()).all().item(), "non-finite output"
+    clocks.wait_ready()
 
     # ---------------- timed region (device-resident inputs) ----------------
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    clocks = Clocks(local)
+    clocks.mark()
     if multi:
         dist.barrier()
     torch.cuda.synchronize(dev)
