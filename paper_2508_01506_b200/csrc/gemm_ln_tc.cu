@@ -51,12 +51,21 @@ using namespace ptx;
 constexpr int kThreads = 384;
 constexpr int kEpi = 256;
 constexpr int BMr = 128;            // rows per CTA
-constexpr int PN = 128;             // output columns per piece (N = 128 MMAs)
+// 128-column pieces into one TMEM accumulator.  The FSVD_LN_PN=64 build runs
+// 64-column pieces into two accumulators ([0, 64), [64, 128)) so the MMA of
+// piece q+1 overlaps the drain of piece q (run_groups): measured slower
+// (23.7 vs 17.8 us at cfg2 -- N = 64 MMAs are shared-memory bound and the
+// epilogue pays its per-piece latency twelve times instead of six).
+#ifndef FSVD_LN_PN
+#define FSVD_LN_PN 128
+#endif
+constexpr int PN = FSVD_LN_PN;      // output columns per piece
+constexpr int NACC = PN == 64 ? 2 : 1;
 constexpr int ATOM = BMr * 128;     // [128 x 64] bf16 A atom (16 KB)
 constexpr int SLOT = PN * 128;      // [128 x 64] bf16 B slot (16 KB)
 constexpr int SPS = 1;              // slots per ring stage
 constexpr int STAGE = SPS * SLOT;
-constexpr int kMaxStages = 10;
+constexpr int kMaxStages = 12;
 constexpr int RS = 2;               // residual ring depth ([128 x 64] bf16 boxes)
 constexpr int RBOX = BMr * 128;
 constexpr int kBoxes = 4;           // second-sweep output staging boxes (in the B ring; K <= 512 leaves 4 stages)
@@ -74,7 +83,7 @@ namespace {
 
 struct LnBars {
   uint64_t full[kMaxStages], empty[kMaxStages];
-  uint64_t a_full, acc_full[1], acc_empty[1], res_full[RS], res_empty[RS];
+  uint64_t a_full, acc_full[2], acc_empty[2], res_full[RS], res_empty[RS];
   uint64_t box_full[kBoxes], box_free[kBoxes];  // second-sweep output boxes (ln_epi.cuh store_boxes)
   uint32_t tmem;
 };
@@ -111,8 +120,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars->empty[i], 1);
     }
     mbar_init(&bars->a_full, 1);
-    mbar_init(&bars->acc_full[0], 1);
-    mbar_init(&bars->acc_empty[0], lnepi::acc_drain_arrivals<PN>());
+    for (int i = 0; i < NACC; ++i) {
+      mbar_init(&bars->acc_full[i], 1);
+      mbar_init(&bars->acc_empty[i], lnepi::acc_drain_arrivals<PN>());
+    }
     for (int i = 0; i < RS; ++i) {
       mbar_init(&bars->res_full[i], 1);
       mbar_init(&bars->res_empty[i], lnepi::res_box_readers<PN>());
@@ -175,13 +186,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t st = 0, ph = 0;
     int in_stage = 0;
     for (int q = 0; q < NP; ++q) {
-      // single accumulator: the epilogue must have drained piece q-1
-      if (q >= 1) {
-        mbar_wait(&bars->acc_empty[0], (q - 1) & 1);
+      // accumulator q % NACC: the epilogue must have drained piece q - NACC
+      const int acc = q % NACC;
+      if (q >= NACC) {
+        mbar_wait(&bars->acc_empty[acc], ((q / NACC) - 1) & 1);
         tc_fence_after();
       }
       LTRACE(16 + q);
-      const uint32_t d = tmem;
+      const uint32_t d = tmem + acc * PN;
       for (int a = 0; a < KA; ++a) {
         if (in_stage == 0) {
           mbar_wait(&bars->full[st], ph);
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++st == (uint32_t)stages) { st = 0; ph ^= 1; }
         }
       }
-      if (elect_one()) mma_commit(&bars->acc_full[0]);
+      if (elect_one()) mma_commit(&bars->acc_full[acc]);
       __syncwarp();
       LTRACE(48 + q);
     }
