@@ -57,8 +57,12 @@ def test_gemm_ln_vs_torch(env, T, N, K):
     assert _rel(y, ref) < 1.5e-2
 
 
+# (16384, 1152): 256-wide tiles + a 128-wide last column on the snake walk;
+# 1096 / 1088: narrow last columns of 72 (MMA N = 80, partial store box) / 64
 @pytest.mark.parametrize("M,N,K,act", [(16384, 1152, 768, None), (16384, 768, 384, None),
-                                       (333, 200, 72, 0), (4096, 3072, 384, 1), (128, 64, 64, 2)])
+                                       (333, 200, 72, 0), (4096, 3072, 384, 1), (128, 64, 64, 2),
+                                       (4096, 1096, 256, None), (2048, 1088, 128, 2),
+                                       (16384, 576, 384, None)])
 def test_gemm_vs_torch(env, M, N, K, act):
     L, torch = env
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
@@ -97,8 +101,10 @@ def test_resid_layernorm_vs_torch(env, rows, d):
     assert _rel(y, ref) < 1e-2
 
 
+# (8, 1000, 12, 12, 32): 768 items on 296 CTAs -- the dynamic item schedule,
+# with a ragged last query tile
 @pytest.mark.parametrize("B,M,H,G,rp", [(2, 512, 12, 12, 32), (1, 130, 4, 2, 16), (3, 77, 2, 2, 64),
-                                         (1, 1024, 4, 4, 32)])
+                                         (1, 1024, 4, 4, 32), (8, 1000, 12, 12, 32)])
 def test_attention_rankspace_vs_torch(env, B, M, H, G, rp):
     """K2 against softmax(2^(Qt K^T)) V in fp32 on the same bf16 inputs."""
     L, torch = env
@@ -120,6 +126,26 @@ def test_attention_rankspace_vs_torch(env, B, M, H, G, rp):
         sc = (q @ k.transpose(1, 2)) * 0.6931471805599453  # log2-domain scores -> natural
         ref[:, :, h * rp:(h + 1) * rp] = torch.softmax(sc, -1) @ v
     assert _rel(out.view(B, M, H * rp), ref) < 2e-2
+
+
+def test_attention_dynamic_schedule_repeatable(env):
+    """Back-to-back launches on one stream reuse the schedule counter (reset by
+    each launch's last CTA): every launch computes every item, bit for bit."""
+    L, torch = env
+    B, M, H, G, rp = 16, 512, 12, 12, 32
+    g = torch.Generator(device="cuda").manual_seed(7)
+    cols = (H + 2 * G) * rp
+    qkv = (torch.randn(B * M, cols, device="cuda", generator=g) * 0.6).bfloat16()
+    outs = []
+    s = torch.cuda.current_stream().cuda_stream
+    for _ in range(3):
+        out = torch.full((B * M, H * rp), float("nan"), device="cuda", dtype=torch.bfloat16)
+        abi.check(L.fsvd_test_attention(_p(qkv), cols, 0, H * rp, (H + G) * rp, B, M, H, G, rp,
+                                        _p(out), H * rp, C.c_void_p(s)))
+        outs.append(out)
+    torch.cuda.synchronize()
+    assert torch.isfinite(outs[0].float()).all()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
 
 
 @pytest.mark.parametrize("pair", ["1", "0"])
