@@ -175,6 +175,16 @@ __device__ __forceinline__ void run_groups(uint32_t tmem, uint32_t quad, uint32_
   constexpr int BPP = PN / 64;  // [128 x 64] boxes per piece
   const uint32_t loff = (quad * 32) << 16;
   const int NP = N / PN;
+  // gamma / beta for the second sweep: this thread's float4 of each, loaded
+  // now so the load latency hides behind the first sweep (N <= kMaxN < 4 *
+  // kEpiThreads: at most one float4 per thread)
+  static_assert(kMaxN <= 4 * kEpiThreads, "one gamma / beta float4 per epilogue thread");
+  const int gb_c = (static_cast<int>(threadIdx.x) - 64) * 4;
+  float4 gb_g = make_float4(0.0f, 0.0f, 0.0f, 0.0f), gb_b = gb_g;
+  if (gb_c < N) {
+    gb_g = __ldg(reinterpret_cast<const float4*>(gamma + gb_c));
+    gb_b = __ldg(reinterpret_cast<const float4*>(beta + gb_c));
+  }
 
   float2 shift = make_float2(0.0f, 0.0f), S1 = shift, S2 = shift;
   bool first = true;
@@ -286,10 +296,9 @@ __device__ __forceinline__ void run_groups(uint32_t tmem, uint32_t quad, uint32_
   const float2 rs2 = make_float2(rstd, rstd), off2 = make_float2(-mean * rstd, -mean * rstd);
 
   // gamma | beta -> shared memory (the caller's region is idle by now)
-  const int et = static_cast<int>(threadIdx.x) - 64;  // 0..255 across the epilogue warps
-  for (int c = et * 4; c < N; c += kEpiThreads * 4) {
-    *reinterpret_cast<float4*>(gb_smem + c) = __ldg(reinterpret_cast<const float4*>(gamma + c));
-    *reinterpret_cast<float4*>(gb_smem + N + c) = __ldg(reinterpret_cast<const float4*>(beta + c));
+  if (gb_c < N) {
+    *reinterpret_cast<float4*>(gb_smem + gb_c) = gb_g;
+    *reinterpret_cast<float4*>(gb_smem + N + gb_c) = gb_b;
   }
   named_bar_sync(bar_id, kEpiThreads);
 #ifdef LN_TRACE
@@ -364,6 +373,16 @@ __device__ __forceinline__ void run_halves(uint32_t tmem, uint32_t quad, uint32_
   constexpr int CPT = PN / 64;  // 32-column chunks per thread per piece
   const uint32_t loff = (quad * 32) << 16;
   const int NP = N / PN;
+  // gamma / beta for the second sweep: this thread's float4 of each, loaded
+  // now so the load latency hides behind the first sweep (N <= kMaxN < 4 *
+  // kEpiThreads: at most one float4 per thread)
+  static_assert(kMaxN <= 4 * kEpiThreads, "one gamma / beta float4 per epilogue thread");
+  const int gb_c = (static_cast<int>(threadIdx.x) - 64) * 4;
+  float4 gb_g = make_float4(0.0f, 0.0f, 0.0f, 0.0f), gb_b = gb_g;
+  if (gb_c < N) {
+    gb_g = __ldg(reinterpret_cast<const float4*>(gamma + gb_c));
+    gb_b = __ldg(reinterpret_cast<const float4*>(beta + gb_c));
+  }
 
   float2 shift = make_float2(0.0f, 0.0f), S1 = shift, S2 = shift;
   for (int i = 0; i < NP; ++i) {
@@ -465,10 +484,9 @@ __device__ __forceinline__ void run_halves(uint32_t tmem, uint32_t quad, uint32_
   const float2 rs2 = make_float2(rstd, rstd), off2 = make_float2(-mean * rstd, -mean * rstd);
 
   // gamma | beta -> shared memory (the caller's region is idle by now)
-  const int et = static_cast<int>(threadIdx.x) - 64;  // 0..255 across the epilogue warps
-  for (int c = et * 4; c < N; c += kEpiThreads * 4) {
-    *reinterpret_cast<float4*>(gb_smem + c) = __ldg(reinterpret_cast<const float4*>(gamma + c));
-    *reinterpret_cast<float4*>(gb_smem + N + c) = __ldg(reinterpret_cast<const float4*>(beta + c));
+  if (gb_c < N) {
+    *reinterpret_cast<float4*>(gb_smem + gb_c) = gb_g;
+    *reinterpret_cast<float4*>(gb_smem + N + gb_c) = gb_b;
   }
   named_bar_sync(bar_id, kEpiThreads);
 #ifdef LN_TRACE
