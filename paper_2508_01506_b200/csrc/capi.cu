@@ -11,9 +11,14 @@
 // (attention.cpp:216-233, :375-379; ffn.cpp:123-128, :163-165;
 // encoder.cpp:224-293), then uploads, runs the device schedule and
 // downloads.
+#include <algorithm>
+#include <chrono>
 #include <cmath>
-#include <cstring>
+#include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -197,17 +202,150 @@ void* scratch(int slot, size_t bytes) {
 // tensor cores); the tensor-core layouts pad d up to pack.d with zero columns.
 int storage_form(const Pack& p) { return p.x3 ? 2 : (p.dtype == FSVD_BF16 ? 0 : 1); }
 
+// Pageable host <-> device copies for the drop-ins.  A pageable cudaMemcpy
+// runs at 7-15 GB/s on the B200 hosts (D2H the slower); instead the bytes go
+// through two pinned 8 MiB chunks: host threads copy chunk k into one while
+// the DMA engine moves chunk k-1 out of the other (51 GB/s), so a 50 MB
+// activation crosses in ~2 ms each way instead of 3.5 / 7 ms.
+class CopyTeam {  // a few persistent host threads for chunk memcpys
+ public:
+  static CopyTeam& get() {
+    static CopyTeam t;
+    return t;
+  }
+  // memcpy n bytes split over the team (blocks until done)
+  void copy(void* dst, const void* src, size_t n) {
+    const size_t parts = n < (size_t(1) << 20) ? 1 : workers_.size() + 1;
+    const size_t step = (n / parts + 63) & ~size_t(63);
+    auto part = [=](size_t i) {
+      const size_t o = std::min(n, i * step), e = std::min(n, o + step);
+      if (e > o) std::memcpy(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o, e - o);
+    };
+    if (parts == 1) {
+      part(0);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      job_ = part;
+      pending_ = workers_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    part(0);
+    std::unique_lock<std::mutex> g(mu_);
+    done_.wait(g, [&] { return pending_ == 0; });
+  }
+
+ private:
+  CopyTeam() {
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    const size_t nw = std::min<size_t>(7, hw - 1);
+    for (size_t w = 0; w < nw; ++w)
+      workers_.emplace_back([this, w] {
+        uint64_t seen = 0;
+        for (;;) {
+          std::function<void(size_t)> job;
+          {
+            std::unique_lock<std::mutex> g(mu_);
+            cv_.wait(g, [&] { return gen_ != seen || stop_; });
+            if (stop_) return;
+            seen = gen_;
+            job = job_;
+          }
+          job(w + 1);
+          std::lock_guard<std::mutex> g(mu_);
+          if (--pending_ == 0) done_.notify_one();
+        }
+      });
+  }
+  ~CopyTeam() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  std::function<void(size_t)> job_;
+  size_t pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+struct PinnedChunks {
+  static constexpr size_t kChunk = size_t(8) << 20;
+  void* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int device = -1;
+};
+std::mutex g_pinned_mu;  // one staged copy at a time per process
+
+PinnedChunks& pinned_chunks() {
+  static std::map<int, PinnedChunks> per_dev;
+  int dev = 0;
+  FSVD_CUDA_CHECK(cudaGetDevice(&dev));
+  PinnedChunks& pc = per_dev[dev];
+  if (pc.buf[0] == nullptr) {
+    for (int i = 0; i < 2; ++i) {
+      FSVD_CUDA_CHECK(cudaHostAlloc(&pc.buf[i], PinnedChunks::kChunk, cudaHostAllocDefault));
+      FSVD_CUDA_CHECK(cudaEventCreateWithFlags(&pc.ev[i], cudaEventDisableTiming));
+    }
+    pc.device = dev;
+  }
+  return pc;
+}
+
+void staged_h2d(void* dst, const void* src, size_t n, cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(g_pinned_mu);
+  PinnedChunks& pc = pinned_chunks();
+  const size_t nch = (n + PinnedChunks::kChunk - 1) / PinnedChunks::kChunk;
+  for (size_t k = 0; k < nch; ++k) {
+    const int b = static_cast<int>(k & 1);
+    const size_t o = k * PinnedChunks::kChunk, len = std::min(PinnedChunks::kChunk, n - o);
+    FSVD_CUDA_CHECK(cudaEventSynchronize(pc.ev[b]));  // the last DMA from this chunk is out
+    CopyTeam::get().copy(pc.buf[b], static_cast<const uint8_t*>(src) + o, len);
+    FSVD_CUDA_CHECK(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + o, pc.buf[b], len,
+                                    cudaMemcpyHostToDevice, s));
+    FSVD_CUDA_CHECK(cudaEventRecord(pc.ev[b], s));
+  }
+}
+
+void staged_d2h(void* dst, const void* src, size_t n, cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(g_pinned_mu);
+  PinnedChunks& pc = pinned_chunks();
+  const size_t nch = (n + PinnedChunks::kChunk - 1) / PinnedChunks::kChunk;
+  auto dma = [&](size_t k) {
+    const int b = static_cast<int>(k & 1);
+    const size_t o = k * PinnedChunks::kChunk, len = std::min(PinnedChunks::kChunk, n - o);
+    FSVD_CUDA_CHECK(cudaMemcpyAsync(pc.buf[b], static_cast<const uint8_t*>(src) + o, len,
+                                    cudaMemcpyDeviceToHost, s));
+    FSVD_CUDA_CHECK(cudaEventRecord(pc.ev[b], s));
+  };
+  if (nch > 0) dma(0);
+  for (size_t k = 0; k < nch; ++k) {
+    const int b = static_cast<int>(k & 1);
+    const size_t o = k * PinnedChunks::kChunk, len = std::min(PinnedChunks::kChunk, n - o);
+    if (k + 1 < nch) dma(k + 1);  // into the other chunk (its host copy finished last round)
+    FSVD_CUDA_CHECK(cudaEventSynchronize(pc.ev[b]));
+    CopyTeam::get().copy(static_cast<uint8_t*>(dst) + o, pc.buf[b], len);
+  }
+}
+
 void upload(const float* host, size_t rows, const Pack& p, void* dev, cudaStream_t s) {
   const size_t n = rows * p.dr;
   float* tmp = static_cast<float*>(scratch(1, n * 4));
-  FSVD_CUDA_CHECK(cudaMemcpyAsync(tmp, host, n * 4, cudaMemcpyHostToDevice, s));
+  staged_h2d(tmp, host, n * 4, s);
   rows_to_device(tmp, static_cast<int>(rows), p.dr, p.d, storage_form(p), dev, s);
 }
 void download(const void* dev, size_t rows, const Pack& p, float* host, cudaStream_t s) {
   const size_t n = rows * p.dr;
   float* tmp = static_cast<float*>(scratch(1, n * 4));
   rows_from_device(dev, static_cast<int>(rows), p.dr, p.d, storage_form(p), tmp, s);
-  FSVD_CUDA_CHECK(cudaMemcpyAsync(host, tmp, n * 4, cudaMemcpyDeviceToHost, s));
+  staged_d2h(host, tmp, n * 4, s);
   FSVD_CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
@@ -655,6 +793,7 @@ void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_lay
   }
   // device
   require_device();
+  const auto t0 = std::chrono::steady_clock::now();
   std::vector<std::shared_ptr<Pack>> packs;
   size_t ws = 0, pack_bytes = 0;
   for (size_t i = 0; i < n_layers; ++i) {
@@ -672,12 +811,29 @@ void host_run_model(const float* x, size_t B, size_t M, size_t W, const fsvd_lay
   for (const auto& q : packs)
     if (q->d != packs[0]->d)
       fail(Kind::Config, "every layer must use the same device layout (tensor-core tiling)");
+  static const bool prof = std::getenv("FSVD_DROPIN_PROFILE") != nullptr;  // developer timing
+  const auto t1 = std::chrono::steady_clock::now();
   run_on_device(x, B * M, out, *packs[0], ws, nullptr,
                 [&](void* xd, void* od, void* td, cudaStream_t s) {
                   std::vector<const Pack*> pp;
                   for (auto& p : packs) pp.push_back(p.get());
+                  if (prof) {
+                    FSVD_CUDA_CHECK(cudaStreamSynchronize(s));
+                    std::fprintf(stderr, "[dropin] upload %.2f ms\n",
+                                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
+                  }
+                  const auto t2 = std::chrono::steady_clock::now();
                   model_layers_fwd(pp.data(), n_layers, mode, pre_ln, B, M, xd, od, td, ws, s);
+                  if (prof) {
+                    FSVD_CUDA_CHECK(cudaStreamSynchronize(s));
+                    std::fprintf(stderr, "[dropin] forward %.2f ms\n",
+                                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t2).count());
+                  }
                 });
+  if (prof)
+    std::fprintf(stderr, "[dropin] packs (hash) %.2f ms, total after packs %.2f ms\n",
+                 std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
   if (meter) meter->note_device(2 * B * M * W * packs[0]->es + ws, pack_bytes);
 }
 
