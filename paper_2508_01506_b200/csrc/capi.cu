@@ -207,45 +207,53 @@ int storage_form(const Pack& p) { return p.x3 ? 2 : (p.dtype == FSVD_BF16 ? 0 : 
 // through two pinned 8 MiB chunks: host threads copy chunk k into one while
 // the DMA engine moves chunk k-1 out of the other (51 GB/s), so a 50 MB
 // activation crosses in ~2 ms each way instead of 3.5 / 7 ms.
-class CopyTeam {  // a few persistent host threads for chunk memcpys
+// A few persistent host threads for the drop-ins' bulk host work (chunk
+// memcpys, content hashes): run(job) calls job(part, parts) on every member
+// and the caller, and returns when all are done.  One job at a time.
+class HostTeam {
  public:
-  static CopyTeam& get() {
-    static CopyTeam t;
+  static HostTeam& get() {
+    static HostTeam t;
     return t;
   }
-  // memcpy n bytes split over the team (blocks until done)
-  void copy(void* dst, const void* src, size_t n) {
-    const size_t parts = n < (size_t(1) << 20) ? 1 : workers_.size() + 1;
-    const size_t step = (n / parts + 63) & ~size_t(63);
-    auto part = [=](size_t i) {
-      const size_t o = std::min(n, i * step), e = std::min(n, o + step);
-      if (e > o) std::memcpy(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o, e - o);
-    };
-    if (parts == 1) {
-      part(0);
-      return;
-    }
+  size_t parts() const { return workers_.size() + 1; }
+  void run(const std::function<void(size_t, size_t)>& job) {
+    std::lock_guard<std::mutex> one(run_mu_);
     {
       std::lock_guard<std::mutex> g(mu_);
-      job_ = part;
+      job_ = &job;
       pending_ = workers_.size();
       ++gen_;
     }
     cv_.notify_all();
-    part(0);
+    job(0, parts());
     std::unique_lock<std::mutex> g(mu_);
     done_.wait(g, [&] { return pending_ == 0; });
   }
+  // memcpy of n bytes split over the team
+  void copy(void* dst, const void* src, size_t n) {
+    if (n < (size_t(1) << 20)) {
+      std::memcpy(dst, src, n);
+      return;
+    }
+    run([=](size_t i, size_t np) {
+      np = std::min<size_t>(np, 8);  // more copy threads measured slower
+      if (i >= np) return;
+      const size_t step = (n / np + 63) & ~size_t(63);
+      const size_t o = std::min(n, i * step), e = std::min(n, o + step);
+      if (e > o) std::memcpy(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o, e - o);
+    });
+  }
 
  private:
-  CopyTeam() {
+  HostTeam() {
     const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
-    const size_t nw = std::min<size_t>(7, hw - 1);
+    const size_t nw = std::min<size_t>(15, hw - 1);
     for (size_t w = 0; w < nw; ++w)
       workers_.emplace_back([this, w] {
         uint64_t seen = 0;
         for (;;) {
-          std::function<void(size_t)> job;
+          const std::function<void(size_t, size_t)>* job;
           {
             std::unique_lock<std::mutex> g(mu_);
             cv_.wait(g, [&] { return gen_ != seen || stop_; });
@@ -253,13 +261,13 @@ class CopyTeam {  // a few persistent host threads for chunk memcpys
             seen = gen_;
             job = job_;
           }
-          job(w + 1);
+          (*job)(w + 1, workers_.size() + 1);
           std::lock_guard<std::mutex> g(mu_);
           if (--pending_ == 0) done_.notify_one();
         }
       });
   }
-  ~CopyTeam() {
+  ~HostTeam() {
     {
       std::lock_guard<std::mutex> g(mu_);
       stop_ = true;
@@ -268,9 +276,9 @@ class CopyTeam {  // a few persistent host threads for chunk memcpys
     for (auto& t : workers_) t.join();
   }
   std::vector<std::thread> workers_;
-  std::mutex mu_;
+  std::mutex mu_, run_mu_;
   std::condition_variable cv_, done_;
-  std::function<void(size_t)> job_;
+  const std::function<void(size_t, size_t)>* job_ = nullptr;
   size_t pending_ = 0;
   uint64_t gen_ = 0;
   bool stop_ = false;
@@ -307,7 +315,7 @@ void staged_h2d(void* dst, const void* src, size_t n, cudaStream_t s) {
     const int b = static_cast<int>(k & 1);
     const size_t o = k * PinnedChunks::kChunk, len = std::min(PinnedChunks::kChunk, n - o);
     FSVD_CUDA_CHECK(cudaEventSynchronize(pc.ev[b]));  // the last DMA from this chunk is out
-    CopyTeam::get().copy(pc.buf[b], static_cast<const uint8_t*>(src) + o, len);
+    HostTeam::get().copy(pc.buf[b], static_cast<const uint8_t*>(src) + o, len);
     FSVD_CUDA_CHECK(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + o, pc.buf[b], len,
                                     cudaMemcpyHostToDevice, s));
     FSVD_CUDA_CHECK(cudaEventRecord(pc.ev[b], s));
@@ -331,7 +339,7 @@ void staged_d2h(void* dst, const void* src, size_t n, cudaStream_t s) {
     const size_t o = k * PinnedChunks::kChunk, len = std::min(PinnedChunks::kChunk, n - o);
     if (k + 1 < nch) dma(k + 1);  // into the other chunk (its host copy finished last round)
     FSVD_CUDA_CHECK(cudaEventSynchronize(pc.ev[b]));
-    CopyTeam::get().copy(static_cast<uint8_t*>(dst) + o, pc.buf[b], len);
+    HostTeam::get().copy(static_cast<uint8_t*>(dst) + o, pc.buf[b], len);
   }
 }
 
@@ -421,12 +429,10 @@ uint64_t hash_spans(const std::vector<Span>& spans) {
       hs[i] = chunks[i].p ? hash_bytes(static_cast<const uint8_t*>(chunks[i].p), chunks[i].n, i)
                           : kP3 + i;
   };
-  size_t nw = std::min<size_t>(std::max(1u, std::thread::hardware_concurrency()), 16);
-  nw = std::min(nw, chunks.size() / 2 + 1);
-  std::vector<std::thread> pool;
-  for (size_t w = 1; w < nw; ++w) pool.emplace_back(work, w, nw);
-  work(0, nw);
-  for (auto& t : pool) t.join();
+  if (chunks.size() <= 2)
+    work(0, 1);
+  else
+    HostTeam::get().run(work);  // persistent threads: no spawn per call
   uint64_t h = kP1 ^ chunks.size();
   for (uint64_t x : hs) h = rotl64(h ^ (x * kP2), 27) * kP1 + kP3;
   return h;
