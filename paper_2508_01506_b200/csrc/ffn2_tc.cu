@@ -173,9 +173,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
            const __grid_constant__ CUtensorMap tmUdn,  // U_dn^T [FR, df] box 64 x 64
            const __grid_constant__ CUtensorMap tmVdn,  // V_dn^T [d, FR]  box QS/2 x 64
            const __grid_constant__ CUtensorMap tmY,    // out [T, d]      box 128 x 64 (LN)
+           const __grid_constant__ CUtensorMap tmR,    // residual [T, d] box 128 x 64 (LN; X
+                                                       //   post-LN, the residual stream pre-LN)
            const float* __restrict__ b_up, const float* __restrict__ b_dn, int act, int T,
            int d_model, int d_ff, bf16* out, const float* __restrict__ ln_g,
-           const float* __restrict__ ln_b, float ln_eps, int seq_pairs) {
+           const float* __restrict__ ln_b, float ln_eps, int seq_pairs, bf16* sum_out) {
   if (threadIdx.x == 0) TRACE2(0);
   using C = Ffn2Cfg<FR>;
   extern __shared__ uint8_t smem_raw[];
@@ -210,7 +212,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmVup);
     tma_prefetch(&tmUdn);
     tma_prefetch(&tmVdn);
-    if (fuse_ln) tma_prefetch(&tmY);
+    if (fuse_ln) {
+      tma_prefetch(&tmY);
+      tma_prefetch(&tmR);
+    }
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&bars->full[i], 1);
       mbar_init(&bars->empty[i], 1);
@@ -327,7 +332,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     __syncwarp();
     if (fuse_ln && lane == 0) {
       mbar_wait(&bars->z_full, 0);
-      lnepi::produce_residual<64>(&tmX, smem + C::o_h, bars->res_full, bars->res_empty, 2,
+      lnepi::produce_residual<64>(&tmR, smem + C::o_h, bars->res_full, bars->res_empty, 2,
                                   d_model, m0, rotq);
       // output boxes: 4 staging slots in the weight ring after gamma / beta
       lnepi::store_boxes<64, 4>(&tmY, smem_u32(ring) + kLnStage, bars->box_full, bars->box_free,
@@ -502,7 +507,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                      reinterpret_cast<float*>(ring), smem_u32(ring) + kLnStage, bars->box_full,
                      bars->box_free, bars->o_full,
                      bars->o_free, 1,
-                     mapa_shared(smem_u32(&bars->o_free[0]), 0), nullptr, 0, rotq);
+                     mapa_shared(smem_u32(&bars->o_free[0]), 0), sum_out, T, rotq);
     } else {
       for (int q = 0; q < NQ; ++q) {
         mbar_wait(&bars->o_full[q & 1], (q >> 1) & 1);
@@ -553,10 +558,16 @@ void launch_ffn2(const FfnTcArgs& a, cudaStream_t s) {
   const CUtensorMap tvdn = tmap_bf16(a.dn_v_t, a.d_model, FR, FR, 64, 64, TmaSwizzle::B128);
   const CUtensorMap ty =
       ln ? tmap_bf16(a.out, a.T, a.d_model, a.d_model, BMr, 64, TmaSwizzle::B128) : tx;
+  // pre-LN chains: the LN2 epilogue adds the residual stream (ln_resid), not
+  // X, and stores the un-normalised sum to sum_out (the single K4's contract)
+  const CUtensorMap tr = ln && a.ln_resid
+                             ? tmap_bf16(a.ln_resid, a.T, a.d_model, a.d_model, BMr, 64, TmaSwizzle::B128)
+                             : tx;
   const int pairs = (a.T + 2 * BMr - 1) / (2 * BMr);
   launch_pdl(k_ffn2<FR>, dim3(2 * pairs), dim3(kThreads), C::SMEM, s, tx, tup, tvup, tudn, tvdn,
-             ty, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff, a.out, a.ln_g, a.ln_b, a.ln_eps,
-             ffn_pair_rotation() && a.seq_tiles % 2 == 0 ? a.seq_tiles / 2 : 0);
+             ty, tr, a.up_b, a.dn_b, a.act, a.T, a.d_model, a.d_ff, a.out, a.ln_g, a.ln_b, a.ln_eps,
+             ffn_pair_rotation() && a.seq_tiles % 2 == 0 ? a.seq_tiles / 2 : 0,
+             ln ? a.sum_out : nullptr);
   check_launch("k_ffn2");
 }
 

@@ -1456,7 +1456,8 @@ void layer_fwd(const Pack& p, int mode, bool pre_ln, size_t B, size_t M, const v
       a.ln_resid = as<bf16>(out);          // s
       a.sum_out = as<bf16>(out);           // s + ffn: the residual stream
       a.seq_tiles = seq_tiles_of(M);
-      ffn_fused_bf16(a, s);
+      if (use_ffn_pair(p, rows)) ffn_fused_pair_bf16(a, s);
+      else ffn_fused_bf16(a, s);
     } else {
       ffn_resid_fwd(p, mode, B, M, A, out, out, trans, s);            // s + ffn -> out
     }
