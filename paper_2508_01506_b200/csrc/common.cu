@@ -111,9 +111,14 @@ CUtensorMap make_tmap_3d(const void* base, CUtensorMapDataType dtype, int elem_b
 // ([next, CTAs done]; zero between launches: the last CTA out resets them).
 // One slot serves every kernel on a stream: a kernel touches it only after
 // griddepcontrol.wait, i.e. after the previous kernel has finished.
-// Allocated outside stream capture on first use; null (static schedule)
-// while a stream is captured before that, or past 64 streams.
+// Allocated on first use; null (static schedule) while the stream is being
+// captured, or past 64 streams.
 int* sched_counter(cudaStream_t s) {
+  // a captured graph may be replayed on another stream next to eager work on
+  // this one: captured launches keep the static schedule
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  FSVD_CUDA_CHECK(cudaStreamIsCapturing(s, &cap));
+  if (cap != cudaStreamCaptureStatusNone) return nullptr;
   static std::mutex mu;
   static std::map<std::pair<int, cudaStream_t>, int*> slots;
   static std::map<int, std::pair<int*, int>> pools;
@@ -122,9 +127,6 @@ int* sched_counter(cudaStream_t s) {
   std::lock_guard<std::mutex> lock(mu);
   const auto f = slots.find({dev, s});
   if (f != slots.end()) return f->second;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  FSVD_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
-  if (cs != cudaStreamCaptureStatusNone) return nullptr;
   auto& pool = pools[dev];
   constexpr int kSlots = 64, kStride = 32;  // 128 B apart
   if (pool.first == nullptr) {

@@ -148,6 +148,50 @@ def test_attention_dynamic_schedule_repeatable(env):
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
 
 
+def test_model_forward_in_cuda_graph_equals_eager(env):
+    """A 2-layer cfg2-shaped forward captured into a CUDA graph (PDL launches,
+    captured K2 keeps the static item schedule) and replayed twice equals the
+    eager forward (dynamic schedule) bit for bit."""
+    import numpy as np
+    from paper_2508_01506_b200.model import layer_descs, random_layer
+    L, torch = env
+    B, M, NL = 8, 512, 2
+    rng = np.random.default_rng(99)
+    layers = [random_layer(768, 3072, 12, 12, 32, 384, 384, rng) for _ in range(NL)]
+    descs = layer_descs(layers)
+    packs = []
+    for i in range(NL):
+        pk = C.c_void_p()
+        abi.check(L.fsvd_layer_pack_create(C.byref(descs[i]), abi.BF16, 0, C.byref(pk)))
+        packs.append(pk)
+    parr = (C.c_void_p * NL)(*[q.value for q in packs])
+    wsb = C.c_size_t()
+    abi.check(L.fsvd_workspace_bytes_ln(parr, NL, B, M, abi.MODE_FLASH_V2, 0, C.byref(wsb)))
+    work = torch.empty(wsb.value, dtype=torch.uint8, device="cuda")
+    x = torch.randn((B, M, 768), device="cuda").to(torch.bfloat16)
+    outs = [torch.empty_like(x) for _ in range(3)]
+
+    def fwd(o):
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        abi.check(L.fsvd_model_fwd(parr, NL, abi.MODE_FLASH_V2, 0, B, M, _p(x), _p(o), _p(work),
+                                   wsb.value, st))
+
+    try:
+        fwd(outs[0])  # eager
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fwd(outs[1])
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        assert torch.isfinite(outs[0].float()).all()
+        assert torch.equal(outs[0], outs[1])
+    finally:
+        for q in packs:
+            L.fsvd_layer_pack_destroy(q)
+
+
 @pytest.mark.parametrize("pair", ["1", "0"])
 def test_ffn_pair_and_single_agree(env, pair):
     """The CTA-pair FFN (ffn2_tc.cu, opt-in) and the single-CTA kernel compute the same
