@@ -463,6 +463,50 @@ def test_compact_post_ln_workspace_and_chunks(mode, chunks):
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+_SCHED_SCRIPT = r"""
+import ctypes as C, os, sys, numpy as np
+sys.path.insert(0, os.environ["ROOT"])
+from paper_2508_01506_b200 import abi
+from paper_2508_01506_b200.model import layer_descs, random_layer
+dt = abi.BF16 if sys.argv[1] == "bf16" else abi.F32
+L = abi.lib(); rng = np.random.default_rng(5)
+layers = [random_layer(768, 3072, 12, 12, 32, 384, 384, rng)]  # kept alive: descs point into it
+descs = layer_descs(layers)
+B, M = 8, 500  # 4 query tiles x 12 heads x 8 = 384 items: more than the grid in both policies
+x = rng.standard_normal((B, M, 768)).astype(np.float32)
+out = np.zeros_like(x)
+# host drop-in: fp32 in / out, converted to the policy's device form (bf16 or split planes)
+abi.check(L.fsvd_run_model(abi.fptr(x), B, M, 768, descs, 1, abi.MODE_FLASH_V2,
+                           abi.TilePlan(16, 16, 64, 1 << 20), 0, b"layer", dt, None, abi.fptr(out)))
+np.save(sys.argv[2], out)
+print("OK")
+"""
+
+
+@pytest.mark.parametrize("policy", ["bf16", "f32"])
+def test_attention_dynamic_and_static_schedules_agree(policy, tmp_path):
+    """K2 hands out work items dynamically (per-stream counter) unless
+    FSVD_ATTN_DYN=0; an item's result does not depend on the CTA that takes
+    it, so a 1-layer forward with 384 items -- more than the grid, ragged last
+    query tile -- is bit-identical under both schedules, in the bf16 and the
+    fp32 (split-plane, one CTA per SM) policy.  Subprocesses: the switch is
+    read once per process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for dyn in ("1", "0"):
+        f = str(tmp_path / f"out_{dyn}.npy")
+        env = dict(os.environ, FSVD_ATTN_DYN=dyn, ROOT=root)
+        r = subprocess.run([sys.executable, "-c", _SCHED_SCRIPT, policy, f], env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+        res.append(np.load(f))
+    assert np.isfinite(res[0]).all()
+    assert np.array_equal(res[0], res[1])
+
+
 @pytest.mark.parametrize("variant", [1, 2])
 @pytest.mark.parametrize("B,M", [(2, 256), (1, 200), (3, 512)], ids=["pairs", "single", "rot"])
 def test_ffn_block_is_ffn_then_residual_norm(L, ora, variant, B, M):
